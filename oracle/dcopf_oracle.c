@@ -1,0 +1,327 @@
+/*
+ * dcopf_oracle.c -- plain, slow, obviously-correct fp64 CPU ORACLE for the
+ * projected dual ascent of arXiv 2406.13191, written from the paper
+ * and SURVEY.md §8(c).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code, header, table or helper with the CUDA path
+ * (paper_2406_13191_b200/csrc, include/), and neither side includes the other.
+ *
+ * What it computes, per instance, in ORIGINAL numbering, single-threaded
+ * (OpenMP only across independent instances):
+ *
+ *   Primal (Eq. 1 written sparsely, B-theta form):
+ *     min  sum_g a_g p_g^2 + c_g p_g
+ *     s.t. G p - A^T f = d                    (KCL, multiplier lambda, free)
+ *          f = diag(b) A theta                (Kirchhoff, multiplier nu, free)   [F2]
+ *          |f| <= F, pmin <= p <= pmax, |theta_i| <= Theta_i, theta_ref = 0
+ *     F1 instead keeps theta only and dualises the 2 n_l limit rows
+ *     +-diag(b) A theta <= F with mu+, mu- >= 0 (the C x <= d rows
+ *     of Eq. 2).
+ *
+ *   Dual function (Eqs. 3-5): G(y) = inf over the boxes of the
+ *   Lagrangian.  The inner minimum over a box is the dual-norm / bound
+ *   selection of Eq. 7b (App. A2) for
+ *   linear terms, and per-generator clipping for a_g > 0, which is Eq. 15
+ *    with the free vector s maximised out (SURVEY F-6).
+ *
+ *   Gradient: the constraint residual at that minimiser (from Eq. 7b; the
+ *   "+b" in Alg. 1 lines 2-3, is read as a sign slip,
+ *   DESIGN.md reading A-5).  Tie rule sign(0) -> box midpoint (A-4).
+ *
+ *   Ascent: y <- y + alpha_k * grad, then mu <- max(mu, 0) (PAPER.md:245,
+ *   Alg. 1 line "mu <- max(mu,0)" PAPER.md:264) with an explicit schedule
+ *   alpha[K] (A-9).  K+1 evaluations: k = 0..K, no step after the last.
+ *
+ * Step-by-step order (SURVEY §8(c) oracle algorithm, a-h) is followed
+ * literally; every sum runs in ascending index order; no FMA contraction
+ * (compile with -ffp-contract=off, reading A-19).
+ *
+ * Divergence (reading A-23 in DESIGN.md): if g(y_k) is not
+ * finite or |g(y_k)| > 1e15 the instance is marked DIVERGED; the step of
+ * iteration k is still taken, every later step is skipped (y frozen at
+ * y_{k+1}) and best never again changes.  best only takes valid values.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_FORM_FLOW_BOX 0   /* F2: boxes p, f, theta; multipliers lambda, nu      */
+#define ORC_FORM_LIMIT_ROWS 1 /* F1: boxes p, theta; multipliers lambda, mu+, mu-   */
+#define ORC_DIVERGED 1
+
+typedef struct {
+  int n_bus, n_branch, n_gen, ref_bus;
+  const int *br_from, *br_to;
+  const double *br_b, *br_fmax, *theta_max;
+  const int *gen_bus;
+  const double *gen_pmin, *gen_pmax, *gen_c, *gen_a; /* gen_a may be NULL */
+} orc_net;
+
+typedef struct {
+  double *b, *F;                 /* per-instance susceptance / limit (outages applied) */
+  double *r, *p, *q, *f, *w, *th, *phi, *glam, *gbr;
+} orc_work;
+
+static void work_alloc(orc_work *W, const orc_net *N, int form) {
+  int nb = N->n_bus, nl = N->n_branch, ng = N->n_gen;
+  int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * nl : nl;
+  W->b = malloc(sizeof(double) * (nl + 1));
+  W->F = malloc(sizeof(double) * (nl + 1));
+  W->r = malloc(sizeof(double) * (ng + 1));
+  W->p = malloc(sizeof(double) * (ng + 1));
+  W->q = malloc(sizeof(double) * (nl + 1));
+  W->f = malloc(sizeof(double) * (nl + 1));
+  W->w = malloc(sizeof(double) * (nb + 1));
+  W->th = malloc(sizeof(double) * (nb + 1));
+  W->phi = malloc(sizeof(double) * (nl + 1));
+  W->glam = malloc(sizeof(double) * (nb + 1));
+  W->gbr = malloc(sizeof(double) * (nbr + 1));
+}
+
+static void work_free(orc_work *W) {
+  free(W->b); free(W->F); free(W->r); free(W->p); free(W->q); free(W->f);
+  free(W->w); free(W->th); free(W->phi); free(W->glam); free(W->gbr);
+}
+
+/* step 2: outaged branches get b_l = 0 and F_l = 0 (reading A-16) */
+static void apply_outages(orc_work *W, const orc_net *N, const int *out, int max_out) {
+  int l, j;
+  for (l = 0; l < N->n_branch; l++) { W->b[l] = N->br_b[l]; W->F[l] = N->br_fmax[l]; }
+  for (j = 0; j < max_out; j++) {
+    l = out ? out[j] : -1;
+    if (l >= 0 && l < N->n_branch) { W->b[l] = 0.0; W->F[l] = 0.0; }
+  }
+}
+
+/*
+ * Steps 4(a)-(e) and 4(g): value g(y) and its gradient (the residual at the
+ * inner minimiser).  lam[n_bus]; br = nu[n_branch] (F2) or mu+[n_branch]
+ * followed by mu-[n_branch] (F1).  Gradient left in W->glam, W->gbr.
+ */
+static double evaluate(const orc_net *N, orc_work *W, int form, const double *d,
+                       const double *lam, const double *br) {
+  const int nb = N->n_bus, nl = N->n_branch, ng = N->n_gen, ref = N->ref_bus;
+  const double *nu = br, *mup = br, *mum = br + nl;
+  int i, g, l;
+  double s_gen = 0.0, s_br = 0.0, s_th = 0.0, s_ld = 0.0, s_mu = 0.0, val;
+
+  /* (a) r_g = c_g + lambda_{beta(g)}  (argument of Eq. 7b's 1-norm, generator part) */
+  for (g = 0; g < ng; g++) W->r[g] = N->gen_c[g] + lam[N->gen_bus[g]];
+
+  /* (b)/(c) branch cost q_l and bus angle cost w_i */
+  for (i = 0; i < nb; i++) W->w[i] = 0.0;
+  if (form == ORC_FORM_FLOW_BOX) {
+    for (l = 0; l < nl; l++) W->q[l] = nu[l] - (lam[N->br_from[l]] - lam[N->br_to[l]]);
+    for (l = 0; l < nl; l++) {
+      W->w[N->br_from[l]] += -(W->b[l] * nu[l]);
+      W->w[N->br_to[l]] += W->b[l] * nu[l];
+    }
+  } else {
+    for (l = 0; l < nl; l++) {
+      /* u_l, stored in q */
+      W->q[l] = W->b[l] * ((mup[l] - mum[l]) - (lam[N->br_from[l]] - lam[N->br_to[l]]));
+    }
+    for (l = 0; l < nl; l++) {
+      W->w[N->br_from[l]] += W->q[l];
+      W->w[N->br_to[l]] -= W->q[l];
+    }
+  }
+
+  /* (d) closed-form inner minimiser over the boxes */
+  for (g = 0; g < ng; g++) {
+    double lo = N->gen_pmin[g], hi = N->gen_pmax[g], r = W->r[g];
+    if (N->gen_a && N->gen_a[g] > 0.0) {          /* QP: clip(-r/(2a)) */
+      double x = -r / (2.0 * N->gen_a[g]);
+      W->p[g] = (x < lo) ? lo : ((x > hi) ? hi : x);
+    } else if (r > 0.0) {
+      W->p[g] = lo;
+    } else if (r < 0.0) {
+      W->p[g] = hi;
+    } else {
+      W->p[g] = 0.5 * (lo + hi);
+    }
+  }
+  if (form == ORC_FORM_FLOW_BOX) {
+    for (l = 0; l < nl; l++) {
+      double q = W->q[l];
+      W->f[l] = (q > 0.0) ? -W->F[l] : ((q < 0.0) ? W->F[l] : 0.0);
+    }
+  }
+  for (i = 0; i < nb; i++) {
+    double w = W->w[i];
+    if (i == ref) W->th[i] = 0.0;
+    else W->th[i] = (w > 0.0) ? -N->theta_max[i] : ((w < 0.0) ? N->theta_max[i] : 0.0);
+  }
+  for (l = 0; l < nl; l++) W->phi[l] = W->b[l] * (W->th[N->br_from[l]] - W->th[N->br_to[l]]);
+
+  /* (e) dual value: brackets in ascending index order, then left to right */
+  for (g = 0; g < ng; g++) {
+    double t = W->r[g] * W->p[g];
+    if (N->gen_a && N->gen_a[g] > 0.0) t = N->gen_a[g] * W->p[g] * W->p[g] + t;
+    s_gen += t;
+  }
+  if (form == ORC_FORM_FLOW_BOX)
+    for (l = 0; l < nl; l++) s_br += W->q[l] * W->f[l];
+  for (i = 0; i < nb; i++)
+    if (i != ref) s_th += W->w[i] * W->th[i];
+  for (i = 0; i < nb; i++) s_ld += lam[i] * d[i];
+  if (form == ORC_FORM_FLOW_BOX) {
+    val = ((s_gen + s_br) + s_th) - s_ld;
+  } else {
+    for (l = 0; l < nl; l++) s_mu += W->F[l] * (mup[l] + mum[l]);
+    val = ((s_gen + s_th) - s_ld) - s_mu;
+  }
+
+  /* (g) gradient = residual at the minimiser */
+  for (i = 0; i < nb; i++) W->glam[i] = -d[i];
+  for (g = 0; g < ng; g++) W->glam[N->gen_bus[g]] += W->p[g];
+  if (form == ORC_FORM_FLOW_BOX) {
+    for (l = 0; l < nl; l++) {
+      W->glam[N->br_from[l]] -= W->f[l];
+      W->glam[N->br_to[l]] += W->f[l];
+    }
+    for (l = 0; l < nl; l++) W->gbr[l] = W->f[l] - W->phi[l];
+  } else {
+    for (l = 0; l < nl; l++) {
+      W->glam[N->br_from[l]] -= W->phi[l];
+      W->glam[N->br_to[l]] += W->phi[l];
+    }
+    for (l = 0; l < nl; l++) {
+      W->gbr[l] = W->phi[l] - W->F[l];
+      W->gbr[nl + l] = -W->phi[l] - W->F[l];
+    }
+  }
+  return val;
+}
+
+static int valid_bound(double g) { return isfinite(g) && fabs(g) <= 1e15; }
+
+static void run_instance(const orc_net *N, int form, const double *d, const int *out, int max_out,
+                         long K, const double *alpha, double *lam, double *br, double *bound,
+                         double *best, int *status, double *hist, int warm) {
+  const int nb = N->n_bus, nl = N->n_branch;
+  const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * nl : nl;
+  orc_work W;
+  long k;
+  int i, j, frozen = 0;
+  work_alloc(&W, N, form);
+  apply_outages(&W, N, out, max_out);
+  if (!warm) {                                   /* step 3: y_0 = 0 */
+    for (i = 0; i < nb; i++) lam[i] = 0.0;
+    for (j = 0; j < nbr; j++) br[j] = 0.0;
+  }
+  *best = -INFINITY;
+  *status = 0;
+  for (k = 0;; k++) {                            /* step 4: k = 0..K inclusive */
+    double g = evaluate(N, &W, form, d, lam, br);
+    int was_frozen = frozen;
+    if (hist) hist[k] = g;
+    if (!was_frozen) {                           /* (f) best = max(best, g) */
+      if (valid_bound(g)) { if (g > *best) *best = g; }
+      else { *status = ORC_DIVERGED; frozen = 1; }
+    }
+    if (k == K) { *bound = g; break; }
+    if (was_frozen) continue;
+    {                                            /* (h) ascent step and projection */
+      double a = alpha[k];
+      for (i = 0; i < nb; i++) lam[i] = lam[i] + a * W.glam[i];
+      if (form == ORC_FORM_FLOW_BOX) {
+        for (j = 0; j < nl; j++) br[j] = br[j] + a * W.gbr[j];
+      } else {
+        for (j = 0; j < 2 * nl; j++) {
+          double v = br[j] + a * W.gbr[j];
+          br[j] = (v > 0.0) ? v : 0.0;           /* mu <- max(mu, 0) */
+        }
+      }
+    }
+  }
+  work_free(&W);
+}
+
+#define NET_ARGS                                                                     \
+  int n_bus, int n_branch, int n_gen, int ref_bus, const int *br_from, const int *br_to, \
+      const double *br_b, const double *br_fmax, const double *theta_max,             \
+      const int *gen_bus, const double *gen_pmin, const double *gen_pmax,             \
+      const double *gen_c, const double *gen_a
+
+#define NET_INIT                                                                        \
+  orc_net N;                                                                            \
+  N.n_bus = n_bus; N.n_branch = n_branch; N.n_gen = n_gen; N.ref_bus = ref_bus;         \
+  N.br_from = br_from; N.br_to = br_to; N.br_b = br_b; N.br_fmax = br_fmax;             \
+  N.theta_max = theta_max; N.gen_bus = gen_bus; N.gen_pmin = gen_pmin;                  \
+  N.gen_pmax = gen_pmax; N.gen_c = gen_c; N.gen_a = gen_a;
+
+/*
+ * Run K ascent steps for B independent instances (instance-major arrays).
+ *   load[B][n_bus]; outages[B][max_out] (-1 padded) or NULL;
+ *   lam[B][n_bus], br[B][nbr] (nbr = n_branch for F2, 2 n_branch for F1):
+ *     in: start point if warm != 0; out: y_K;
+ *   bound[B] = g(y_K); best[B] = max valid g(y_k), k=0..K; status[B];
+ *   hist[B][K+1] (g(y_k)) or NULL.
+ * Returns 0, or -1 on bad arguments.
+ */
+int oracle_solve(NET_ARGS, int form, long B, const double *load, const int *outages, int max_out,
+                 long K, const double *alpha, double *lam, double *br, double *bound,
+                 double *best, int *status, double *hist, int warm, int n_threads) {
+  NET_INIT
+  long j;
+  const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * n_branch : n_branch;
+  if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0 || K < 0) return -1;
+  if (form != ORC_FORM_FLOW_BOX && form != ORC_FORM_LIMIT_ROWS) return -1;
+  (void)n_threads;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(n_threads > 0 ? n_threads : 1)
+  for (j = 0; j < B; j++) {
+    run_instance(&N, form, load + j * (long)n_bus, outages ? outages + j * (long)max_out : NULL,
+                 max_out, K, alpha, lam + j * (long)n_bus, br + j * (long)nbr, bound + j,
+                 best + j, status + j, hist ? hist + j * (K + 1) : NULL, warm);
+  }
+  return 0;
+}
+
+/* Value and gradient at given multipliers (no step). */
+int oracle_evaluate(NET_ARGS, int form, long B, const double *load, const int *outages, int max_out,
+                    const double *lam, const double *br, double *value, double *grad_lam,
+                    double *grad_br) {
+  NET_INIT
+  long j;
+  const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * n_branch : n_branch;
+  if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0) return -1;
+  if (form != ORC_FORM_FLOW_BOX && form != ORC_FORM_LIMIT_ROWS) return -1;
+  for (j = 0; j < B; j++) {
+    orc_work W;
+    work_alloc(&W, &N, form);
+    apply_outages(&W, &N, outages ? outages + j * (long)max_out : NULL, max_out);
+    value[j] = evaluate(&N, &W, form, load + j * (long)n_bus, lam + j * (long)n_bus,
+                        br + j * (long)nbr);
+    if (grad_lam) memcpy(grad_lam + j * (long)n_bus, W.glam, sizeof(double) * n_bus);
+    if (grad_br) memcpy(grad_br + j * (long)nbr, W.gbr, sizeof(double) * nbr);
+    work_free(&W);
+  }
+  return 0;
+}
+
+/* Inner minimiser at given multipliers, for the brute-force pins:
+ * p[B][n_gen], flow[B][n_branch] (F2: f*; F1: phi), theta[B][n_bus]. */
+int oracle_minimiser(NET_ARGS, int form, long B, const double *load, const int *outages,
+                     int max_out, const double *lam, const double *br, double *p, double *flow,
+                     double *theta) {
+  NET_INIT
+  long j;
+  const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * n_branch : n_branch;
+  if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0) return -1;
+  for (j = 0; j < B; j++) {
+    orc_work W;
+    work_alloc(&W, &N, form);
+    apply_outages(&W, &N, outages ? outages + j * (long)max_out : NULL, max_out);
+    evaluate(&N, &W, form, load + j * (long)n_bus, lam + j * (long)n_bus, br + j * (long)nbr);
+    memcpy(p + j * (long)n_gen, W.p, sizeof(double) * n_gen);
+    memcpy(flow + j * (long)n_branch, form == ORC_FORM_FLOW_BOX ? W.f : W.phi,
+           sizeof(double) * n_branch);
+    memcpy(theta + j * (long)n_bus, W.th, sizeof(double) * n_bus);
+    work_free(&W);
+  }
+  return 0;
+}
