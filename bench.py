@@ -1,0 +1,360 @@
+#!/usr/bin/env python3
+"""Throughput of the fused projected dual-ascent iteration (arXiv 2406.13191)
+on B200, in dual-ascent instance-iterations per second (BASELINE.json metric).
+
+Default workload = BASELINE.json configs[4]: the 10000-bus / 12700-branch /
+2500-generator network, 8192 load-scenario / line-switching instances, linear
+cost, form F2, sharded contiguously over the ranks (weak-per-instance, fixed
+total batch => "scaling": "strong" over the batch... see --scaling note below).
+
+A "step" is one ascent iteration (S1-S4) over the rank's whole batch = one
+launch of the batched kernel.  The timed region is one dcopf_dual_iterate(K)
+call: K step launches plus the final evaluation launch at y_K (counted as
+work-free overhead, i.e. the reported rate is conservative).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload config4|config4b|config0|config1|config2|config3|config3q]
+                  [--form F2|F1]
+
+Multi-GPU: launched by torchrun; one process per GPU; the instances are
+sharded with no communication in the loop; one NCCL all_gather of the
+per-instance (bound, best, status) after the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2406_13191_b200 import instances as inst  # noqa: E402
+
+WORKLOADS = {
+    # name: (config, quadratic, batch)
+    "config0": (0, False, 1),
+    "config1": (1, False, 1),
+    "config2": (2, True, 1),
+    "config3": (3, False, 1),
+    "config3q": (3, True, 1),
+    "config4": (4, False, inst.CONFIG4_BATCH),
+    "config4b": (4, False, inst.CONFIG4_BATCH),
+}
+METRIC = "dual-ascent instance-iterations/sec"
+UNIT = "instance-iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
+    ap.add_argument("--form", default="F2", choices=["F2", "F1"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(B, rank, world):
+    """Contiguous shard of [0, B) for `rank` (sizes differ by at most 1)."""
+    base, rem = divmod(B, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def make_inputs(workload, lo, hi):
+    config, quad, _ = WORKLOADS[workload]
+    net = inst.make_network(config, quadratic=quad)
+    if config == 4:
+        batch = inst.config4_batch(net, range(lo, hi), variant="4b" if workload == "config4b" else "4")
+    else:
+        batch = inst.single_batch(net)
+    return net, batch
+
+
+def cpu_oracle_rate(net, batch, form, cores, target_s=12.0):
+    """The oracle as it stands, timed on this host's cores over a bounded
+    sample of the workload (instances x iterations), inst-it/s."""
+    import oracle
+    B = batch.B
+    n_inst = min(B, max(1, 4 * cores)) if B > 1 else 1
+    idx = np.linspace(0, B - 1, n_inst).astype(int) if B > 1 else np.array([0])
+    loads = batch.load[idx]
+    outs = None if batch.outages is None else batch.outages[idx]
+    # calibrate the iteration count to ~target_s of wall time
+    K0 = 20
+    t0 = time.perf_counter()
+    oracle.solve(net, loads, outages=outs, K=K0, alpha=inst.alpha_schedule(K0), form=form, threads=cores)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    K = int(max(K0, min(200000, K0 * target_s / dt)))
+    t0 = time.perf_counter()
+    oracle.solve(net, loads, outages=outs, K=K, alpha=inst.alpha_schedule(K), form=form, threads=cores)
+    dt = time.perf_counter() - t0
+    return n_inst * K / dt, f"{n_inst} instances x {K} iterations ({dt:.1f} s wall)"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    form = 0 if args.form == "F2" else 1
+    _, _, B = WORKLOADS[args.workload]
+    net, batch = make_inputs(args.workload, 0, B if B == 1 else min(B, 256))
+    cores = os.cpu_count() or 1
+    per_step = []
+    import oracle
+    n_inst = min(batch.B, 2 * cores)
+    loads = batch.load[:n_inst]
+    outs = None if batch.outages is None else batch.outages[:n_inst]
+    K_s = 50 if net.n_bus > 1000 else 2000
+    a = inst.alpha_schedule(K_s)
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.solve(net, loads, outages=outs, K=K_s, alpha=a, form=form, threads=cores)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            per_step.append(dt)
+    T = sum(per_step)
+    value = n_inst * K_s * args.steps / T
+    sample = f"{n_inst} instances x {K_s} iterations per step, oracle/dcopf_oracle.c OpenMP over instances"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, BASELINE.json recipe)",
+            "config": {"workload": args.workload, "form": args.form, "n_bus": net.n_bus,
+                       "n_branch": net.n_branch, "n_gen": net.n_gen, "B": batch.B},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2406_13191_b200 import dual
+
+    rank, world, local = dist_env()
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    form = dual.FORM_F2 if args.form == "F2" else dual.FORM_F1
+    config, quad, B_total = WORKLOADS[args.workload]
+    lo, hi = shard(B_total, rank, world) if B_total > 1 else (0, 1)
+    net, batch = make_inputs(args.workload, lo, hi)
+    B = batch.B
+    path = dual.PATH_BATCHED if B_total > 1 else dual.PATH_SINGLE
+
+    h = dual.DcopfDual(net, form=form, device=local, path=path)
+    stream = torch.cuda.current_stream(dev)
+    load_dev = torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev)
+    outs_dev = None if batch.outages is None else torch.from_numpy(batch.outages).to(dev)
+    h.set_instance_batch(load_dev, outs_dev, stream=stream)
+    info = h.info()
+    K, W = args.steps, args.warmup
+    alpha = inst.alpha_schedule(max(K, W, 1))
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    # ---- warm-up (untimed) --------------------------------------------------
+    if path == dual.PATH_BATCHED:
+        for _ in range(W):
+            h.iterate(1, alpha, stream=stream)
+    else:
+        h.iterate(W, alpha, stream=stream)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device events on the launching stream ----------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h.iterate(K, alpha, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # ---- per-instance results gathered once (NCCL, off the hot loop) ---------
+    bound = torch.empty(B, dtype=torch.float64, device=dev)
+    best = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    h.get_bound(bound, best, status, stream=stream)
+    gather_ms = None
+    if world > 1 and B_total > 1:
+        res = torch.stack([bound, best, status.to(torch.float64)])
+        sizes = [shard(B_total, r, world) for r in range(world)]
+        maxB = max(b - a for a, b in sizes)
+        pad = torch.full((3, maxB), float("nan"), dtype=torch.float64, device=dev)
+        pad[:, :B] = res
+        out = torch.empty((world, 3, maxB), dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        tdist.all_gather_into_tensor(out, pad)
+        torch.cuda.synchronize()
+        gather_ms = 1e3 * (time.perf_counter() - g0)
+
+    # ---- end-to-end through the public API with host buffers -----------------
+    e2e = None
+    if not args.no_e2e:
+        load_host = torch.from_numpy(np.ascontiguousarray(batch.load.T)).pin_memory()
+        outs_host = None if batch.outages is None else torch.from_numpy(batch.outages).pin_memory()
+        bound_h = torch.empty(B, dtype=torch.float64).pin_memory()
+        best_h = torch.empty(B, dtype=torch.float64).pin_memory()
+        status_h = torch.empty(B, dtype=torch.int32).pin_memory()
+        h2d = load_host.numel() * 8 + (0 if outs_host is None else outs_host.numel() * 4)
+        d2h = B * (8 + 8 + 4)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h.set_instance_batch(load_host, outs_host, stream=stream)
+        h.iterate(K, alpha, stream=stream)
+        h.get_bound(bound_h, best_h, status_h, stream=stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+        e2e = {"value": B_total * K / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "timed": "set_instance_batch(host pinned) + iterate(K) + "
+                                                      "get_bound(host), wall clock, max over ranks"}
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        inst_it = B_total * K
+        value = inst_it / (ms_max / 1e3)
+        per_gpu_bytes = info.alg_bytes_per_inst_iter * B * K
+        achieved = per_gpu_bytes / (ms / 1e3) / 1e9  # GB/s on this rank's kernel launches
+        traffic = None
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+            ent = prof.get(f"{args.workload}/{args.form}")
+            if ent and ent.get("dram_bytes_per_launch"):
+                traffic = ent["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            rate, sample = cpu_oracle_rate(net, batch, form, cores)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_max / K, "higher_is_better": True,
+            "scaling": "strong" if B_total > 1 else "replicas",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE.json recipe)",
+            "config": {"workload": args.workload, "form": args.form, "cost": "QP" if quad else "LP",
+                       "n_bus": net.n_bus, "n_branch": net.n_branch, "n_gen": net.n_gen,
+                       "B_total": B_total, "B_per_gpu": B, "path": "batched" if path == 1 else "single",
+                       "parallelism": f"instance-shard x{world}",
+                       "l2": ("inputs larger than L2: state %.2f GB per GPU" %
+                              ((info.B_padded * (2 * net.n_bus + 2 * net.n_branch * (1 if form == 0 else 2)
+                                                 + net.n_bus) * 8) / 1e9))
+                       if B_total > 1 else "state on chip (single instance)",
+                       "timed_launches": f"{K} step launches + 1 final evaluation"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": (K + 1) if path == 1 else 1,
+            "clocks": clk,
+            "gather_ms": gather_ms,
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        tdist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

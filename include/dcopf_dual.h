@@ -1,0 +1,183 @@
+/*
+ * dcopf_dual.h -- C ABI of the B200 (sm_100a) projected dual-ascent library
+ * for DC optimal power flow, after arXiv 2406.13191 ("PAPER.md").
+ *
+ * What one iteration computes (PAPER.md line numbers):
+ *   S1  inner cost vectors from the multipliers by sparse incidence products:
+ *       r_g = c_g + lambda_{bus(g)}, q_l = nu_l - (lambda_s - lambda_t),
+ *       w_i = -sum_{l at i} sigma_il b_l nu_l                   (Eq. 3)
+ *   S2  closed-form inner minimiser over the generator / flow / angle boxes:
+ *       bound selection for linear cost (dual norm, Eq. 7b PAPER.md:157-160,
+ *       App. A2), clip(-r/(2a), pmin, pmax) for quadratic
+ *       cost (Eq. 15 PAPER.md:230-236 with s maximised out); sign(0) -> midpoint
+ *   S3  dual value g (a valid lower bound, Remarks 1-2
+ *       PAPER.md:164-172, 237-242) and its gradient = constraint residual at
+ *       that minimiser
+ *   S4  y <- y + alpha_k grad, then mu <- max(mu, 0) (Alg. 1 line
+ *       "mu <- max(mu,0)" PAPER.md:264).  Jacobi: all of S1-S3 read y_k.
+ *
+ * The primal problem is PAPER.md:94-101 (Eq. 1) in sparse B-theta form:
+ *   min sum_g a_g p_g^2 + c_g p_g  s.t.  G p - A^T f = d (lambda),
+ *   f = diag(b) A theta, |f| <= F, pmin <= p <= pmax, |theta_i| <= Theta_i,
+ *   theta_ref = 0.
+ * Form F2 (DCOPF_FORM_FLOW_BOX, default) dualises Kirchhoff with free nu and
+ * keeps p, f, theta as boxes.  Form F1 (DCOPF_FORM_LIMIT_ROWS) keeps p, theta
+ * as boxes and dualises the 2 n_branch limit rows +-diag(b) A theta <= F with
+ * mu+, mu- >= 0 (the C x <= d rows of Eq. 2).
+ *
+ * Conventions for every call:
+ *   - All functions return an int status (DCOPF_OK or a negative code) and
+ *     never throw across the ABI; dcopf_dual_last_error() gives the message.
+ *   - Numbering in and out is the caller's ORIGINAL numbering; the library
+ *     reorders buses and branches internally and never exposes that order.
+ *   - "array pointers" may be host or device memory (resolved through CUDA
+ *     unified addressing, cudaMemcpyDefault); device pointers avoid a copy.
+ *     The caller owns every buffer it passes; the handle owns all device state.
+ *   - Every call is ordered on the CUDA stream it is given (NULL = legacy
+ *     default stream) and does not synchronise the device, except where a
+ *     host buffer forces a synchronous copy or create/set validates inputs.
+ *   - Per-instance arrays are instance-contiguous: element (entity e,
+ *     instance j) of an [n_entity][B] array is at e*B + j.
+ *   - A handle is not thread-safe; independent handles are independent.
+ *   - Results are deterministic: identical inputs and schedule give bitwise
+ *     identical outputs on the same GPU model, independent of how a batch is
+ *     split across handles / GPUs (instances never interact).
+ */
+#ifndef DCOPF_DUAL_H
+#define DCOPF_DUAL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dcopf_dual_s *dcopf_dual_t; /* opaque; owned by the library */
+
+enum {
+  DCOPF_OK = 0,
+  DCOPF_EINVAL = -1,    /* bad argument / out-of-range index / malformed data */
+  DCOPF_ETOPOLOGY = -2, /* network (or the never-switchable part) disconnected */
+  DCOPF_ECUDA = -3,     /* a CUDA runtime call failed (message has the error) */
+  DCOPF_ENOMEM = -4,    /* device allocation failed */
+  DCOPF_ESTATE = -5     /* call out of order (e.g. iterate before set_instance_batch) */
+};
+
+enum { DCOPF_FORM_FLOW_BOX = 0 /* F2 */, DCOPF_FORM_LIMIT_ROWS = 1 /* F1 */ };
+
+/* per-instance status: a diverged instance is frozen; the
+ * others continue.  DIVERGED = g(y_k) non-finite or |g(y_k)| > 1e15; the step
+ * of that iteration is still taken, no later step is (y frozen at y_{k+1}),
+ * best keeps only valid values (reading A-23). */
+enum { DCOPF_INST_OK = 0, DCOPF_INST_DIVERGED = 1 };
+
+/* kernel path selection */
+enum {
+  DCOPF_PATH_AUTO = 0,    /* SINGLE when B <= single_max_batch, else BATCHED */
+  DCOPF_PATH_BATCHED = 1, /* 32 instances per warp lane-group, one fused launch per iteration */
+  DCOPF_PATH_SINGLE = 2   /* one persistent CTA per instance running all K iterations on chip */
+};
+
+/* Network description.  Host pointers,
+ * copied and validated at create; the caller keeps ownership. */
+typedef struct {
+  int32_t n_bus, n_branch, n_gen, ref_bus;
+  const int32_t *br_from, *br_to;   /* [n_branch] endpoints, original bus ids, from != to */
+  const double *br_b, *br_fmax;     /* [n_branch] susceptance b >= 0, flow limit F >= 0 (p.u.) */
+  const double *theta_max;          /* [n_bus] angle-box half widths >= 0 (theta_ref is
+                                       pinned to 0 whatever is given); NULL => the library
+                                       computes the box implied by the flow limits:
+                                       Theta_i = shortest path ref->i with weights F_l/b_l
+                                       over never-switchable branches (A-2) */
+  const int32_t *gen_bus;           /* [n_gen] bus of each generator (several per bus allowed) */
+  const double *gen_pmin, *gen_pmax;/* [n_gen] pmin <= pmax */
+  const double *gen_c;              /* [n_gen] linear cost */
+  const double *gen_a;              /* [n_gen] quadratic cost a >= 0, or NULL (linear) */
+  const uint8_t *br_switchable;     /* [n_branch] nonzero = an instance may take it out,
+                                       or NULL (any branch may be out; no check) */
+} dcopf_network_desc;
+
+typedef struct {
+  int32_t form;             /* DCOPF_FORM_FLOW_BOX (0) or DCOPF_FORM_LIMIT_ROWS (1) */
+  int32_t precision;        /* 64 (fp64; the only mode in this build) */
+  int32_t device;           /* CUDA device ordinal */
+  int32_t path;             /* DCOPF_PATH_* */
+  int32_t single_max_batch; /* AUTO threshold; <= 0 means 128 */
+  int32_t reserved[3];      /* zero */
+} dcopf_options;
+
+/* Create a handle: validates and copies the network, reorders buses
+ * (reverse Cuthill-McKee) and builds the bus->branch incidence (CSR, entries
+ * in ascending original branch id) and the generator map on the device.
+ * Errors: EINVAL (sizes, indices, self loops, negative b/F/Theta/a,
+ * pmin > pmax, non-finite data, bad options), ETOPOLOGY (disconnected over
+ * b > 0, or over never-switchable branches when br_switchable is given),
+ * ECUDA / ENOMEM.  *out is NULL on failure. */
+int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, dcopf_dual_t *out);
+
+/* Load B instances that share the network: load[n_bus][B] (p.u.), and per
+ * instance up to max_out outaged branch ids (original numbering, -1 padded),
+ * outages[B][max_out] or NULL (max_out = 0).  An outaged branch has b = F = 0
+ * for that instance (A-16).  Resets the multipliers to 0, best to
+ * -inf, status to OK.  B >= 1; max_out <= 8.  Errors: EINVAL (B < 1,
+ * max_out out of range, an id out of range or not switchable), ECUDA,
+ * ENOMEM. */
+int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
+                                  const int32_t *outages, int32_t max_out, void *cuda_stream);
+
+/* Run K ascent steps with the explicit schedule alpha[K] (host array, any
+ * values; reading A-9), then evaluate once more at y_K:
+ *   bound = g(y_K), best = max over valid g(y_k), k in [0, K] (and over
+ *   previous calls since set_instance_batch).
+ * history: NULL or an [K][B] array that receives g(y_k), k = 0..K-1 (device
+ * or host).  K = 0 only evaluates.  Errors: ESTATE (no batch loaded),
+ * EINVAL (K < 0, alpha NULL with K > 0), ECUDA. */
+int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *history,
+                       void *cuda_stream);
+
+/* bound[B] = g(y) at the last evaluation, best[B], status[B]; any may be NULL. */
+int dcopf_dual_get_bound(dcopf_dual_t h, double *bound, double *best, int32_t *status,
+                         void *cuda_stream);
+
+/* lambda[n_bus][B]; branch: F2 nu[n_branch][B]; F1 mu+[n_branch][B] followed
+ * by mu-[n_branch][B].  Either may be NULL. */
+int dcopf_dual_get_multipliers(dcopf_dual_t h, double *lambda, double *branch, void *cuda_stream);
+
+/* Warm start / checkpoint restore: same layouts as get_multipliers.  Any
+ * lambda (and nu) with mu >= 0 is dual feasible, so the anytime-bound property
+ * is kept.  Does not reset best or status.
+ * Errors: EINVAL (F1 and some mu < 0 or non-finite value), ESTATE. */
+int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const double *branch,
+                               void *cuda_stream);
+
+/* Value and gradient at the current multipliers, no step and no change to
+ * best/status: value[B], grad_lambda[n_bus][B], grad_branch (layout of
+ * get_multipliers; for F1 the unprojected d g / d mu).  Any may be NULL. */
+int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, double *grad_branch,
+                        void *cuda_stream);
+
+/* Static facts about the handle, for reporting. */
+typedef struct {
+  int64_t B;                      /* instances loaded (0 before set_instance_batch) */
+  int64_t B_padded;               /* instances actually computed (batched path pads to 32) */
+  int32_t path;                   /* DCOPF_PATH_BATCHED or DCOPF_PATH_SINGLE in use */
+  int32_t form;
+  int32_t n_bus, n_branch, n_gen, quadratic;
+  int64_t alg_bytes_per_inst_iter;/* algorithmic HBM bytes per instance-iteration:
+                                     F2 8(3 n_bus + 2 n_branch), F1 8(3 n_bus + 4 n_branch) */
+  int32_t bandwidth;              /* bus bandwidth of the internal (RCM) order */
+  int32_t smem_bytes;             /* dynamic shared memory of the iteration kernel */
+  int32_t threads_per_block;
+  int32_t grid;                   /* CTAs per iteration launch */
+  int32_t launches_per_iter;      /* kernel launches per ascent step */
+  int32_t state_on_chip;          /* single path: multipliers resident in shared memory */
+} dcopf_info;
+int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info);
+
+const char *dcopf_dual_last_error(dcopf_dual_t h); /* never NULL; h may be NULL (last create error) */
+void dcopf_dual_destroy(dcopf_dual_t h);           /* NULL is a no-op */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCOPF_DUAL_H */

@@ -1,0 +1,206 @@
+"""Thin Python binding of the C ABI in include/dcopf_dual.h (ctypes).
+
+Argument marshalling only: every step of the dual iteration runs in the
+library's sm_100a kernels.  There is no CPU fallback -- if the shared library
+or a CUDA device is missing, every call raises.
+
+Arrays may be torch tensors (device or host) or numpy arrays (host); they are
+passed to the library as raw pointers.  Per-instance arrays use the ABI's
+instance-contiguous layout: load[n_bus][B], lambda[n_bus][B], ...
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import _build
+
+FORM_F2 = 0  # DCOPF_FORM_FLOW_BOX
+FORM_F1 = 1  # DCOPF_FORM_LIMIT_ROWS
+PATH_AUTO, PATH_BATCHED, PATH_SINGLE = 0, 1, 2
+INST_OK, INST_DIVERGED = 0, 1
+ERRORS = {-1: "EINVAL", -2: "ETOPOLOGY", -3: "ECUDA", -4: "ENOMEM", -5: "ESTATE"}
+
+
+class DcopfError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class NetworkDesc(ctypes.Structure):
+    _fields_ = [("n_bus", ctypes.c_int32), ("n_branch", ctypes.c_int32), ("n_gen", ctypes.c_int32),
+                ("ref_bus", ctypes.c_int32), ("br_from", ctypes.c_void_p), ("br_to", ctypes.c_void_p),
+                ("br_b", ctypes.c_void_p), ("br_fmax", ctypes.c_void_p), ("theta_max", ctypes.c_void_p),
+                ("gen_bus", ctypes.c_void_p), ("gen_pmin", ctypes.c_void_p), ("gen_pmax", ctypes.c_void_p),
+                ("gen_c", ctypes.c_void_p), ("gen_a", ctypes.c_void_p), ("br_switchable", ctypes.c_void_p)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("form", ctypes.c_int32), ("precision", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("path", ctypes.c_int32), ("single_max_batch", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("B_padded", ctypes.c_int64), ("path", ctypes.c_int32),
+                ("form", ctypes.c_int32), ("n_bus", ctypes.c_int32), ("n_branch", ctypes.c_int32),
+                ("n_gen", ctypes.c_int32), ("quadratic", ctypes.c_int32),
+                ("alg_bytes_per_inst_iter", ctypes.c_int64), ("bandwidth", ctypes.c_int32),
+                ("smem_bytes", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
+                ("grid", ctypes.c_int32), ("launches_per_iter", ctypes.c_int32),
+                ("state_on_chip", ctypes.c_int32)]
+
+
+SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",
+           "dcopf_dual_get_bound", "dcopf_dual_get_multipliers", "dcopf_dual_set_multipliers",
+           "dcopf_dual_evaluate", "dcopf_dual_get_info", "dcopf_dual_last_error", "dcopf_dual_destroy"]
+
+_lib = None
+
+
+def load_library(path: Optional[str] = None):
+    """Load libdcopf_dual.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    path = path or _build.LIB
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run __graft_entry__.build() (no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.dcopf_dual_create.argtypes = [ctypes.POINTER(NetworkDesc), ctypes.POINTER(Options), ctypes.POINTER(P)]
+    lib.dcopf_dual_set_instance_batch.argtypes = [P, I64, P, P, I32, P]
+    lib.dcopf_dual_iterate.argtypes = [P, I64, P, P, P]
+    lib.dcopf_dual_get_bound.argtypes = [P, P, P, P, P]
+    lib.dcopf_dual_get_multipliers.argtypes = [P, P, P, P]
+    lib.dcopf_dual_set_multipliers.argtypes = [P, P, P, P]
+    lib.dcopf_dual_evaluate.argtypes = [P, P, P, P, P]
+    lib.dcopf_dual_get_info.argtypes = [P, ctypes.POINTER(Info)]
+    lib.dcopf_dual_last_error.argtypes = [P]
+    lib.dcopf_dual_last_error.restype = ctypes.c_char_p
+    lib.dcopf_dual_destroy.argtypes = [P]
+    lib.dcopf_dual_destroy.restype = None
+    for s in SYMBOLS[:-2]:
+        getattr(lib, s).restype = ctypes.c_int
+    if path == _build.LIB:
+        _lib = lib
+    return lib
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor / numpy array / None (must be contiguous)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        assert x.is_contiguous(), "tensor must be contiguous"
+        return ctypes.c_void_p(x.data_ptr())
+    assert isinstance(x, np.ndarray) and x.flags["C_CONTIGUOUS"]
+    return x.ctypes.data_as(ctypes.c_void_p)
+
+
+def _stream(s):
+    if s is None:
+        return None
+    if hasattr(s, "cuda_stream"):
+        return ctypes.c_void_p(s.cuda_stream)
+    return ctypes.c_void_p(int(s))
+
+
+class DcopfDual:
+    """One library handle: a network + (after set_instance_batch) a batch."""
+
+    def __init__(self, net, form: int = FORM_F2, device: int = 0, path: int = PATH_AUTO,
+                 single_max_batch: int = 0, switchable=None, implied_theta: bool = False):
+        self.lib = load_library()
+        self._keep = []
+        k = lambda a, dt: (self._keep.append(np.ascontiguousarray(a, dtype=dt)) or self._keep[-1])
+        d = NetworkDesc()
+        d.n_bus, d.n_branch, d.n_gen, d.ref_bus = net.n_bus, net.n_branch, net.n_gen, net.ref_bus
+        d.br_from = _ptr(k(net.br_from, np.int32))
+        d.br_to = _ptr(k(net.br_to, np.int32))
+        d.br_b = _ptr(k(net.br_b, np.float64))
+        d.br_fmax = _ptr(k(net.br_fmax, np.float64))
+        d.theta_max = None if implied_theta else _ptr(k(net.theta_max, np.float64))
+        d.gen_bus = _ptr(k(net.gen_bus, np.int32))
+        d.gen_pmin = _ptr(k(net.gen_pmin, np.float64))
+        d.gen_pmax = _ptr(k(net.gen_pmax, np.float64))
+        d.gen_c = _ptr(k(net.gen_c, np.float64))
+        d.gen_a = None if net.gen_a is None else _ptr(k(net.gen_a, np.float64))
+        d.br_switchable = None if switchable is None else _ptr(k(switchable, np.uint8))
+        o = Options()
+        o.form, o.precision, o.device, o.path, o.single_max_batch = form, 64, device, path, single_max_batch
+        h = ctypes.c_void_p()
+        rc = self.lib.dcopf_dual_create(ctypes.byref(d), ctypes.byref(o), ctypes.byref(h))
+        if rc != 0:
+            raise DcopfError(rc, self.lib.dcopf_dual_last_error(None).decode())
+        self.h = h
+        self.net = net
+        self.form = form
+        self._keep = []
+
+    # -- helpers --------------------------------------------------------------
+    def _check(self, rc):
+        if rc != 0:
+            raise DcopfError(rc, self.lib.dcopf_dual_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.dcopf_dual_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_branch_mult(self):
+        return self.net.n_branch * (2 if self.form == FORM_F1 else 1)
+
+    # -- ABI calls ------------------------------------------------------------
+    def set_instance_batch(self, load, outages=None, stream=None):
+        """load: [n_bus][B]; outages: [B][max_out] int32 (-1 padded) or None."""
+        B = int(load.shape[1])
+        max_out = 0 if outages is None else int(outages.shape[1])
+        self._check(self.lib.dcopf_dual_set_instance_batch(self.h, B, _ptr(load), _ptr(outages), max_out,
+                                                           _stream(stream)))
+        self.B = B
+
+    def iterate(self, K, alpha, history=None, stream=None):
+        a = np.ascontiguousarray(alpha, dtype=np.float64)
+        assert a.shape[0] >= K
+        self._check(self.lib.dcopf_dual_iterate(self.h, int(K), _ptr(a), _ptr(history), _stream(stream)))
+
+    def get_bound(self, bound=None, best=None, status=None, stream=None):
+        self._check(self.lib.dcopf_dual_get_bound(self.h, _ptr(bound), _ptr(best), _ptr(status), _stream(stream)))
+
+    def get_multipliers(self, lam=None, branch=None, stream=None):
+        self._check(self.lib.dcopf_dual_get_multipliers(self.h, _ptr(lam), _ptr(branch), _stream(stream)))
+
+    def set_multipliers(self, lam=None, branch=None, stream=None):
+        self._check(self.lib.dcopf_dual_set_multipliers(self.h, _ptr(lam), _ptr(branch), _stream(stream)))
+
+    def evaluate(self, value=None, grad_lam=None, grad_branch=None, stream=None):
+        self._check(self.lib.dcopf_dual_evaluate(self.h, _ptr(value), _ptr(grad_lam), _ptr(grad_branch),
+                                                 _stream(stream)))
+
+    def info(self) -> Info:
+        inf = Info()
+        self._check(self.lib.dcopf_dual_get_info(self.h, ctypes.byref(inf)))
+        return inf
+
+    # -- numpy conveniences (host buffers; the library does the copies) --------
+    def results_numpy(self):
+        B = self.B
+        bound, best = np.empty(B), np.empty(B)
+        status = np.empty(B, dtype=np.int32)
+        self.get_bound(bound, best, status)
+        lam = np.empty((self.net.n_bus, B))
+        br = np.empty((self.n_branch_mult, B))
+        self.get_multipliers(lam, br)
+        return bound, best, status, lam, br

@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+identical seeded inputs, at the north_star tolerances (1e-9 relative on the
+bound, 1e-8 normalised max-abs on the multipliers), plus the edge cases.
+
+The per-entity arithmetic reproduces the oracle's operation order, so the
+multipliers are expected to match bitwise; the tests that say so assert it.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import FORM_F1, FORM_F2
+from paper_2406_13191_b200 import dual
+from paper_2406_13191_b200 import instances as inst
+
+from gpu_helpers import BOUND_RTOL, assert_parity, cost_scale, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+PATHS = [dual.PATH_SINGLE, dual.PATH_BATCHED]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    dual.load_library()
+
+
+# ---------------------------------------------------------------------------
+# config 0 at its full K (BASELINE.json configs[0]), both forms, both paths
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+@pytest.mark.parametrize("path", PATHS)
+def test_config0_full_K(form, path):
+    net = inst.make_network(0)
+    K = inst.ITERS[0]
+    a = inst.alpha_schedule(K)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=path, history=True)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+@pytest.mark.parametrize("path", PATHS)
+def test_config0_tuned_step(form, path):
+    """alpha = 1e-2, theta = min(pi/3, implied): a trajectory that moves."""
+    net = inst.make_network(0, theta_mode="min")
+    K = 5000
+    a = inst.alpha_schedule(K, 1e-2)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=path, history=True)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+    assert gpu["best"][0] > 0.9 * 77.578167948 * 0.9
+
+
+# ---------------------------------------------------------------------------
+# tiny random instances: QP, several generators per bus, ragged tiles
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("quad", [False, True])
+def test_tiny_batch_ragged(form, path, quad):
+    net = inst.tiny_network(23, 37, 30, seed=5, quadratic=quad)  # 30 gens on 23 buses
+    rng = np.random.default_rng(9)
+    B = 37  # two tiles, ragged tail
+    loads = net.base_load[None, :] * rng.uniform(0.7, 1.3, (B, net.n_bus))
+    outs = np.full((B, 3), -1, np.int32)
+    non_tree = np.arange(net.n_tree, net.n_branch)
+    for j in range(B):
+        k = j % 4
+        if k:
+            outs[j, :k] = rng.choice(non_tree, k, replace=False)
+    K = 700
+    a = inst.alpha_schedule(K, 4e-3) * np.linspace(1.0, 0.2, K)  # non-constant schedule
+    orc = oracle.solve(net, loads, outages=outs, K=K, alpha=a, form=form, history=True)
+    gpu = run_gpu(net, loads, outages=outs, K=K, alpha=a, form=form, path=path, history=True)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+# ---------------------------------------------------------------------------
+# the large single-instance configs (1, 2 QP, 3 LP/QP) at full K on the single
+# path, and shortened on the batched path (B = 1)
+
+
+@pytest.mark.parametrize("config,quad,form", [(1, False, FORM_F2), (1, False, FORM_F1), (2, True, FORM_F2),
+                                              (2, True, FORM_F1), (3, False, FORM_F2), (3, True, FORM_F2),
+                                              (3, False, FORM_F1)])
+def test_large_single_instance_full_K(config, quad, form):
+    net = inst.make_network(config, quadratic=quad)
+    K = inst.ITERS[config]
+    a = inst.alpha_schedule(K)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=dual.PATH_SINGLE, history=True)
+    assert_parity(net, gpu, orc)
+
+
+@pytest.mark.parametrize("config,form", [(1, FORM_F2), (3, FORM_F1)])
+def test_large_network_batched_path(config, form):
+    net = inst.make_network(config)
+    K = 300
+    a = inst.alpha_schedule(K)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=dual.PATH_BATCHED, history=True)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+# ---------------------------------------------------------------------------
+# config 4: the bench's launch configuration (B = 8192, batched) at full K,
+# checked on sampled instances; and a 64-instance cut checked everywhere
+
+
+def test_config4_full_batch_sampled():
+    net = inst.make_network(4)
+    B = inst.CONFIG4_BATCH
+    K = inst.ITERS[4]
+    batch = inst.config4_batch(net, range(B))
+    a = inst.alpha_schedule(K)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=FORM_F2,
+                  path=dual.PATH_BATCHED)
+    assert gpu["info"].grid == B // 32
+    idx = np.array([0, 31, 4097, 8191])
+    orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=FORM_F2,
+                       threads=4)
+    assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+def test_config4_cut_all_instances(form):
+    net = inst.make_network(4)
+    batch = inst.config4_batch(net, range(64))
+    K = 150
+    a = inst.alpha_schedule(K)
+    orc = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, history=True,
+                       threads=8)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, path=dual.PATH_BATCHED,
+                  history=True)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+# ---------------------------------------------------------------------------
+# evaluate-only kernel (value and gradient at given multipliers)
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+@pytest.mark.parametrize("path", PATHS)
+def test_evaluate_at_random_points(form, path):
+    import torch
+    net = inst.tiny_network(40, 61, 12, seed=3, quadratic=True)
+    rng = np.random.default_rng(1)
+    B = 45
+    loads = net.base_load[None, :] * rng.uniform(0.5, 1.5, (B, net.n_bus))
+    lam, br = inst.random_multipliers(rng, net, B, form)
+    val_o, gl_o, gb_o = oracle.evaluate(net, loads, lam, br, form=form)
+    dev = torch.device("cuda:0")
+    h = dual.DcopfDual(net, form=form, path=path)
+    h.set_instance_batch(torch.from_numpy(loads.T.copy()).to(dev))
+    h.set_multipliers(torch.from_numpy(lam.T.copy()).to(dev), torch.from_numpy(br.T.copy()).to(dev))
+    val = torch.empty(B, dtype=torch.float64, device=dev)
+    gl = torch.empty((net.n_bus, B), dtype=torch.float64, device=dev)
+    gb = torch.empty((h.n_branch_mult, B), dtype=torch.float64, device=dev)
+    h.evaluate(val, gl, gb)
+    torch.cuda.synchronize()
+    S = cost_scale(net)
+    assert np.all(np.abs(val.cpu().numpy() - val_o) <= 1e-12 * np.maximum(np.abs(val_o), S))
+    np.testing.assert_array_equal(gl.cpu().numpy().T, gl_o)
+    np.testing.assert_array_equal(gb.cpu().numpy().T, gb_o)
+    # evaluate does not move the state
+    lam2 = np.empty((net.n_bus, B))
+    h.get_multipliers(lam2, None)
+    np.testing.assert_array_equal(lam2.T, lam)
+    h.close()
+
+
+# ---------------------------------------------------------------------------
+# warm start, host buffers, invariants, edge cases
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_warm_start_and_host_buffers(path):
+    net = inst.make_network(0)
+    rng = np.random.default_rng(4)
+    lam0, br0 = inst.random_multipliers(rng, net, 3, FORM_F1, scale=3.0)
+    loads = np.tile(net.base_load, (3, 1))
+    K = 400
+    a = inst.alpha_schedule(K, 2e-3)
+    orc = oracle.solve(net, loads, K=K, alpha=a, form=FORM_F1, lam0=lam0, br0=br0, history=True)
+    # host (numpy) buffers straight through the ABI
+    h = dual.DcopfDual(net, form=FORM_F1, path=path)
+    h.set_instance_batch(np.ascontiguousarray(loads.T))
+    h.set_multipliers(np.ascontiguousarray(lam0.T), np.ascontiguousarray(br0.T))
+    hist = np.empty((K, 3))
+    h.iterate(K, a, hist)
+    bound, best, status, lam, br = h.results_numpy()
+    gpu = dict(bound=bound, best=best, status=status, lam=lam.T, br=br.T, hist=hist.T)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+    # F1 rejects a negative mu
+    bad = br0.copy()
+    bad[1, 3] = -1.0
+    with pytest.raises(dual.DcopfError):
+        h.set_multipliers(np.ascontiguousarray(lam0.T), np.ascontiguousarray(bad.T))
+    h.close()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_divergence_isolated(path):
+    net = inst.make_network(0)
+    loads = np.stack([net.base_load, net.base_load * 1e14, net.base_load])
+    K = 50
+    a = inst.alpha_schedule(K)
+    orc = oracle.solve(net, loads, K=K, alpha=a, history=True)
+    gpu = run_gpu(net, loads, K=K, alpha=a, path=path, history=True)
+    np.testing.assert_array_equal(gpu["status"], [0, 1, 0])
+    np.testing.assert_array_equal(gpu["status"], orc.status)
+    assert_parity(net, {k: (v[[0, 2]] if isinstance(v, np.ndarray) else v) for k, v in gpu.items()},
+                  oracle.solve(net, loads[[0, 2]], K=K, alpha=a, history=True))
+    # the diverged instance is frozen at the same y as the oracle's
+    np.testing.assert_array_equal(gpu["lam"][1], orc.lam[1])
+
+
+def test_sharding_invariance_and_determinism():
+    """Instances never interact: 64 at once == 2 x 32 (bitwise), reruns bitwise."""
+    net = inst.make_network(4)
+    batch = inst.config4_batch(net, range(64))
+    K = 60
+    a = inst.alpha_schedule(K)
+    full = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, path=dual.PATH_BATCHED)
+    again = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, path=dual.PATH_BATCHED)
+    lo = run_gpu(net, batch.load[:32], outages=batch.outages[:32], K=K, alpha=a, path=dual.PATH_BATCHED)
+    hi = run_gpu(net, batch.load[32:], outages=batch.outages[32:], K=K, alpha=a, path=dual.PATH_BATCHED)
+    for key in ("bound", "best", "lam", "br", "status"):
+        np.testing.assert_array_equal(full[key], again[key])
+        np.testing.assert_array_equal(full[key], np.concatenate([lo[key], hi[key]]))
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_single_bus_no_branches(path):
+    """n_branch = 0 (SPEC 1-bus worked example): bound 250."""
+    net = inst.Network(n_bus=1, n_branch=0, n_gen=1, ref_bus=0, br_from=np.zeros(0, np.int32),
+                       br_to=np.zeros(0, np.int32), br_b=np.zeros(0), br_fmax=np.zeros(0),
+                       theta_max=np.zeros(1), gen_bus=np.zeros(1, np.int32), gen_pmin=np.zeros(1),
+                       gen_pmax=np.array([100.0]), gen_c=np.array([5.0]))
+    gpu = run_gpu(net, np.array([[50.0]]), K=20, alpha=inst.alpha_schedule(20, 0.02), path=path)
+    assert gpu["best"][0] == 250.0 and gpu["bound"][0] == 250.0
+
+
+def test_implied_theta_box_matches_generator():
+    """theta_max = NULL: the library computes the implied box (A-2) itself."""
+    net = inst.make_network(1)
+    K = 200
+    a = inst.alpha_schedule(K, 1e-2)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, history=True)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, path=dual.PATH_SINGLE, history=True, implied_theta=True)
+    assert_parity(net, gpu, orc)
+
+
+def test_zero_iterations_evaluates_origin():
+    net = inst.make_network(0)
+    gpu = run_gpu(net, net.base_load, K=0, path=dual.PATH_BATCHED)
+    assert gpu["bound"][0] == 0.0 and gpu["best"][0] == 0.0
