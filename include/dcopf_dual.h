@@ -74,8 +74,11 @@ enum { DCOPF_INST_OK = 0, DCOPF_INST_DIVERGED = 1 };
 /* kernel path selection */
 enum {
   DCOPF_PATH_AUTO = 0,    /* SINGLE when B <= single_max_batch, else BATCHED */
-  DCOPF_PATH_BATCHED = 1, /* 32 instances per warp lane-group, one fused launch per iteration */
-  DCOPF_PATH_SINGLE = 2   /* one persistent CTA per instance running all K iterations on chip */
+  DCOPF_PATH_BATCHED = 1, /* 32 instances per CTA tile (lane = instance); one persistent launch
+                             runs all K iterations as wavefront sweeps in RCM bus order */
+  DCOPF_PATH_SINGLE = 2,  /* one persistent CTA per instance running all K iterations on chip */
+  DCOPF_PATH_BATCHED_SIMPLE = 3 /* batched, one 3-phase launch per iteration (first design; kept
+                                   for comparison) */
 };
 
 /* Network description.  Host pointers,
@@ -169,8 +172,10 @@ typedef struct {
   int32_t smem_bytes;             /* dynamic shared memory of the iteration kernel */
   int32_t threads_per_block;
   int32_t grid;                   /* CTAs per iteration launch */
-  int32_t launches_per_iter;      /* kernel launches per ascent step */
+  int32_t launches_per_iter;      /* kernel launches per ascent step (0: one launch per call) */
   int32_t state_on_chip;          /* single path: multipliers resident in shared memory */
+  int32_t chunk;                  /* batched path: buses per wavefront chunk */
+  int32_t ring_bus, ring_branch;  /* batched path: theta* / f* code ring sizes (entries) */
 } dcopf_info;
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info);
 

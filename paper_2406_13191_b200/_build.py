@@ -10,8 +10,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libdcopf_dual.so")
-SOURCES = [os.path.join(CSRC, "dcopf_dual.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "dual_kernels.cuh"), os.path.join(ROOT, "include", "dcopf_dual.h")]
+SOURCES = [os.path.join(CSRC, "dcopf_dual.cu"), os.path.join(CSRC, "schedule.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dual_kernels.cuh", "pipe_kernel.cuh", "schedule.h")] + [
+    os.path.join(ROOT, "include", "dcopf_dual.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <queue>
@@ -22,6 +23,8 @@
 
 #include "../../include/dcopf_dual.h"
 #include "dual_kernels.cuh"
+#include "pipe_kernel.cuh"
+#include "schedule.h"
 
 using namespace dcopf;
 
@@ -51,7 +54,19 @@ struct dcopf_dual_s {
   size_t alpha_cap = 0;
   cudaEvent_t alpha_ev = nullptr;                     // staging may be reused once this fired
   double *g_lam = nullptr, *g_br = nullptr;  // evaluate scratch (internal layout)
+  // compiled sweep schedule of the batched path (per network and form)
+  Schedule sch;
+  int smem_pipe = 0, sched_ok = 0;
+  uint8_t *d_prog = nullptr;
+  long long *d_prog_off = nullptr;
+  int *d_prog_bytes = nullptr, *d_tx_bytes = nullptr, *d_ld_ptr = nullptr, *d_ld_ent = nullptr,
+      *d_ld_slot = nullptr;
+  std::string sched_err;
 };
+
+static const int kPipeWarps = 8;  // consumer warps of k_pipe (+1 producer warp)
+
+static bool batched_path(int path) { return path == DCOPF_PATH_BATCHED || path == DCOPF_PATH_BATCHED_SIMPLE; }
 
 namespace {
 
@@ -123,63 +138,6 @@ bool connected(int n, const std::vector<int> &fr, const std::vector<int> &to,
       }
   }
   return cnt == n;
-}
-
-// reverse Cuthill-McKee from a pseudo-peripheral start
-std::vector<int> rcm_order(int n, const std::vector<std::vector<int>> &adj) {
-  std::vector<int> deg(n);
-  for (int i = 0; i < n; ++i) deg[i] = (int)adj[i].size();
-  auto bfs_last = [&](int s, int *ecc) {
-    std::vector<int> lev(n, -1);
-    std::queue<int> q;
-    q.push(s);
-    lev[s] = 0;
-    int last = s;
-    while (!q.empty()) {
-      int v = q.front();
-      q.pop();
-      if (lev[v] > lev[last] || (lev[v] == lev[last] && deg[v] < deg[last])) last = v;
-      for (int u : adj[v])
-        if (lev[u] < 0) {
-          lev[u] = lev[v] + 1;
-          q.push(u);
-        }
-    }
-    *ecc = lev[last];
-    return last;
-  };
-  std::vector<int> order;
-  order.reserve(n);
-  std::vector<char> vis(n, 0);
-  for (int comp_start = 0; comp_start < n; ++comp_start) {
-    if (vis[comp_start]) continue;
-    int s = comp_start, ecc = 0, ecc2 = 0;
-    s = bfs_last(s, &ecc);
-    for (int it = 0; it < 4; ++it) {
-      int s2 = bfs_last(s, &ecc2);
-      if (ecc2 <= ecc) break;
-      ecc = ecc2;
-      s = s2;
-    }
-    std::queue<int> q;
-    q.push(s);
-    vis[s] = 1;
-    while (!q.empty()) {
-      int v = q.front();
-      q.pop();
-      order.push_back(v);
-      std::vector<int> nb;
-      for (int u : adj[v])
-        if (!vis[u]) {
-          vis[u] = 1;
-          nb.push_back(u);
-        }
-      std::sort(nb.begin(), nb.end(), [&](int x, int y) { return deg[x] != deg[y] ? deg[x] < deg[y] : x < y; });
-      for (int u : nb) q.push(u);
-    }
-  }
-  std::reverse(order.begin(), order.end());
-  return order;
 }
 
 int ensure_scratch(dcopf_dual_t h, size_t bytes) {
@@ -319,6 +277,28 @@ int launch_batched_form(dcopf_dual_t h, const BatchArgs &a, double alpha, long k
   return launch_batched<kFormF1, MODE>(h, a, alpha, k, s);
 }
 
+// copy the schedule alpha[K] to the device through pinned staging; the staging
+// buffer is reused only after the previous copy has executed (event)
+int stage_alpha(dcopf_dual_t h, int64_t K, const double *alpha, cudaStream_t s) {
+  if (!h->alpha_ev) CK(h, cudaEventCreateWithFlags(&h->alpha_ev, cudaEventDisableTiming));
+  CK(h, cudaEventSynchronize(h->alpha_ev));
+  if ((size_t)K > h->alpha_cap) {
+    cudaFree(h->alpha_dev);
+    cudaFreeHost(h->alpha_pin);
+    h->alpha_dev = h->alpha_pin = nullptr;
+    h->alpha_cap = 0;
+    CK(h, cudaMalloc(&h->alpha_dev, K * 8));
+    CK(h, cudaMallocHost(&h->alpha_pin, K * 8));
+    h->alpha_cap = K;
+  }
+  if (K > 0) {
+    CK(h, cudaMemcpy(h->alpha_pin, alpha, K * 8, cudaMemcpyDefault));
+    CK(h, cudaMemcpyAsync(h->alpha_dev, h->alpha_pin, K * 8, cudaMemcpyHostToDevice, s));
+    CK(h, cudaEventRecord(h->alpha_ev, s));
+  }
+  return DCOPF_OK;
+}
+
 template <typename F>
 int set_smem(dcopf_dual_t h, F fn, int bytes) {
   CK(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -328,8 +308,10 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
 // opt every kernel instantiation into the dynamic shared memory it needs
 int configure_kernels(dcopf_dual_t h) {
   int rc = DCOPF_OK;
-  if (h->path == DCOPF_PATH_BATCHED) {
+  if (batched_path(h->path)) {
     const int b = h->smem_batched;
+    if (!rc && h->sched_ok) rc = set_smem(h, k_pipe<kFormF2, kPipeWarps>, h->smem_pipe);
+    if (!rc && h->sched_ok) rc = set_smem(h, k_pipe<kFormF1, kPipeWarps>, h->smem_pipe);
     if (!rc) rc = set_smem(h, k_batched<kFormF2, kModeStep>, b);
     if (!rc) rc = set_smem(h, k_batched<kFormF2, kModeFinal>, b);
     if (!rc) rc = set_smem(h, k_batched<kFormF2, kModeEval>, b);
@@ -382,6 +364,59 @@ SingleArgs single_args(dcopf_dual_t h) {
   return a;
 }
 
+
+
+// Compile and upload the batched sweep schedule (schedule.h).  The chunk size
+// starts at DCOPF_CHUNK (default 32) and halves until the kernel's shared
+// memory fits two CTAs per SM (else one).  Failure only disables the batched
+// path (sched_err says why).
+int compile_schedule(dcopf_dual_t h, const NetInternal &ni) {
+  int dev_smem = 0;
+  CK(h, cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  int CH = 32, P = 2;
+  if (const char *e = getenv("DCOPF_CHUNK")) CH = std::max(1, atoi(e));
+  if (const char *e = getenv("DCOPF_PREFETCH")) P = std::max(1, atoi(e));
+  const int two_per_sm = dev_smem / 2 - 1024;
+  Schedule best;
+  bool have = false;
+  for (int ch = CH; ch >= 1; ch /= 2) {
+    Schedule sc;
+    std::string err = build_schedule(ni, ch, P, kPipeWarps, &sc);
+    if (!err.empty()) {
+      h->sched_err = err;
+      return DCOPF_OK;
+    }
+    if (sc.total <= dev_smem && !have) {
+      best = sc;
+      have = true;
+    }
+    if (sc.total <= two_per_sm) {
+      best = sc;
+      have = true;
+      break;
+    }
+  }
+  if (!have) {
+    h->sched_err = "no chunk size fits the shared memory";
+    return DCOPF_OK;
+  }
+  h->sch = best;
+  h->smem_pipe = best.total;
+  std::vector<uint8_t> &pg = h->sch.prog;
+  int rc = upload(h, &h->d_prog, pg);
+  if (!rc) rc = upload(h, &h->d_prog_off, h->sch.prog_off);
+  if (!rc) rc = upload(h, &h->d_prog_bytes, h->sch.prog_bytes);
+  if (!rc) rc = upload(h, &h->d_tx_bytes, h->sch.tx_bytes);
+  if (!rc) rc = upload(h, &h->d_ld_ptr, h->sch.ld_ptr);
+  if (!rc) rc = upload(h, &h->d_ld_ent, h->sch.ld_ent);
+  if (!rc) rc = upload(h, &h->d_ld_slot, h->sch.ld_slot);
+  if (!rc) {
+    h->sched_ok = 1;
+    std::vector<uint8_t>().swap(h->sch.prog);  // device copy only
+  }
+  return rc;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -396,12 +431,15 @@ void dcopf_dual_destroy(dcopf_dual_t h) {
   cudaSetDevice(h->device);
   free_batch(h);
   int *ip[] = {h->d_bus_ptr, h->d_bus_inc, h->d_gen_ptr, h->d_br_s, h->d_br_t,
-               h->d_bus_perm, h->d_bus_inv, h->d_br_perm, h->d_br_inv};
+               h->d_bus_perm, h->d_bus_inv, h->d_br_perm, h->d_br_inv,
+               h->d_prog_bytes, h->d_tx_bytes, h->d_ld_ptr, h->d_ld_ent, h->d_ld_slot};
   for (int *p : ip) cudaFree(p);
   double *dp[] = {h->d_theta, h->d_gen_c, h->d_gen_lo, h->d_gen_hi, h->d_gen_a, h->d_br_b, h->d_br_F,
                   h->scratch, h->alpha_dev};
   for (double *p : dp) cudaFree(p);
   cudaFreeHost(h->alpha_pin);
+  cudaFree(h->d_prog);
+  cudaFree(h->d_prog_off);
   if (h->alpha_ev) cudaEventDestroy(h->alpha_ev);
   cudaFree(h->flag);
   delete h;
@@ -419,7 +457,7 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
     return fail(nullptr, DCOPF_EINVAL, "unknown form %d", o.form);
   if (o.precision != 64 && o.precision != 0)
     return fail(nullptr, DCOPF_EINVAL, "precision %d not supported (fp64 only)", o.precision);
-  if (o.path < 0 || o.path > 2) return fail(nullptr, DCOPF_EINVAL, "unknown path %d", o.path);
+  if (o.path < 0 || o.path > 3) return fail(nullptr, DCOPF_EINVAL, "unknown path %d", o.path);
   const int nb = net->n_bus, nl = net->n_branch, ng = net->n_gen;
   if (nb < 1 || nl < 0 || ng < 0) return fail(nullptr, DCOPF_EINVAL, "bad sizes n_bus=%d n_branch=%d n_gen=%d", nb, nl, ng);
   if (net->ref_bus < 0 || net->ref_bus >= nb) return fail(nullptr, DCOPF_EINVAL, "ref_bus %d out of range", net->ref_bus);
@@ -509,76 +547,28 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   }
   theta[net->ref_bus] = 0.0;
 
-  // ---- internal bus order: reverse Cuthill-McKee over all branches ----
-  std::vector<std::vector<int>> adj(nb);
-  for (int l = 0; l < nl; ++l) {
-    adj[fr[l]].push_back(to[l]);
-    adj[to[l]].push_back(fr[l]);
+  // ---- internal numbering: bus order, branch order, CSR, generator map ----
+  const char *ord = getenv("DCOPF_ORDER");
+  Internalized in;
+  std::string ierr = internalize(nb, nl, ng, net->ref_bus, fr.data(), to.data(), net->br_b, net->br_fmax,
+                                 theta.data(), net->gen_bus, net->gen_pmin, net->gen_pmax, net->gen_c,
+                                 net->gen_a, h->form, ord && std::string(ord) == "rcm", &in);
+  if (!ierr.empty()) {
+    int rc = fail(nullptr, DCOPF_EINVAL, "%s", ierr.c_str());
+    delete h;
+    return rc;
   }
-  for (auto &v : adj) {
-    std::sort(v.begin(), v.end());
-    v.erase(std::unique(v.begin(), v.end()), v.end());
-  }
-  h->bus_perm = rcm_order(nb, adj);
-  h->bus_inv.assign(nb, 0);
-  for (int i = 0; i < nb; ++i) h->bus_inv[h->bus_perm[i]] = i;
-  h->ref_int = h->bus_inv[net->ref_bus];
-  // branch order: by (max, min) internal endpoint, then original id
-  h->br_perm.resize(nl);
-  for (int l = 0; l < nl; ++l) h->br_perm[l] = l;
-  auto key = [&](int l) {
-    int a = h->bus_inv[fr[l]], b = h->bus_inv[to[l]];
-    return std::make_pair(std::max(a, b), std::min(a, b));
-  };
-  std::sort(h->br_perm.begin(), h->br_perm.end(), [&](int x, int y) {
-    auto kx = key(x), ky = key(y);
-    return kx != ky ? kx < ky : x < y;
-  });
-  h->br_inv.assign(nl, 0);
-  for (int l = 0; l < nl; ++l) h->br_inv[h->br_perm[l]] = l;
-  int bw = 0;
-  for (int l = 0; l < nl; ++l) bw = std::max(bw, std::abs(h->bus_inv[fr[l]] - h->bus_inv[to[l]]));
-  h->bandwidth = bw;
-
-  // ---- CSR bus -> incident branches, ascending ORIGINAL branch id ----
-  std::vector<std::vector<int>> inc(nb);  // original branch ids per internal bus
-  for (int l = 0; l < nl; ++l) {          // ascending l => sorted
-    inc[h->bus_inv[fr[l]]].push_back(l);
-    inc[h->bus_inv[to[l]]].push_back(l);
-  }
-  std::vector<int> bus_ptr(nb + 1, 0), bus_inc;
-  bus_inc.reserve(2 * (size_t)nl);
-  for (int i = 0; i < nb; ++i) {
-    for (int l : inc[i]) {
-      int is_to = (h->bus_inv[to[l]] == i) ? 1 : 0;
-      bus_inc.push_back((h->br_inv[l] << 1) | is_to);
-    }
-    bus_ptr[i + 1] = (int)bus_inc.size();
-  }
-  // ---- generators grouped by internal bus, ascending original id ----
-  std::vector<std::vector<int>> gens(nb);
-  for (int g = 0; g < ng; ++g) gens[h->bus_inv[net->gen_bus[g]]].push_back(g);
-  std::vector<int> gen_ptr(nb + 1, 0);
-  std::vector<double> gc, glo, ghi, ga;
-  for (int i = 0; i < nb; ++i) {
-    for (int g : gens[i]) {
-      gc.push_back(net->gen_c[g]);
-      glo.push_back(net->gen_pmin[g]);
-      ghi.push_back(net->gen_pmax[g]);
-      ga.push_back(net->gen_a ? net->gen_a[g] : 0.0);
-    }
-    gen_ptr[i + 1] = (int)gc.size();
-  }
-  std::vector<double> th_int(nb), bb(nl), FF(nl);
-  std::vector<int> bs(nl), bt(nl);
-  for (int i = 0; i < nb; ++i) th_int[i] = theta[h->bus_perm[i]];
-  for (int li = 0; li < nl; ++li) {
-    int l = h->br_perm[li];
-    bs[li] = h->bus_inv[fr[l]];
-    bt[li] = h->bus_inv[to[l]];
-    bb[li] = net->br_b[l];
-    FF[li] = net->br_fmax[l];
-  }
+  h->bus_perm = in.bus_perm;
+  h->bus_inv = in.bus_inv;
+  h->br_perm = in.br_perm;
+  h->br_inv = in.br_inv;
+  h->ref_int = in.net.ref;
+  h->bandwidth = in.bandwidth;
+  const NetInternal &ni = in.net;
+  const std::vector<int> &bus_ptr = ni.bus_ptr, &bus_inc = ni.bus_inc, &gen_ptr = ni.gen_ptr, &bs = ni.bs,
+                         &bt = ni.bt;
+  const std::vector<double> &gc = ni.gc, &glo = ni.glo, &ghi = ni.ghi, &ga = ni.ga, &th_int = ni.theta,
+                            &bb = ni.b, &FF = ni.F;
 
   cudaError_t e = cudaSetDevice(h->device);
   if (e != cudaSuccess) {
@@ -603,6 +593,7 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   if (!rc) rc = upload(h, &h->d_gen_a, ga);
   if (!rc) rc = upload(h, &h->d_br_b, bb);
   if (!rc) rc = upload(h, &h->d_br_F, FF);
+  if (!rc) rc = compile_schedule(h, ni);
   if (!rc) {
     e = cudaMalloc(&h->flag, sizeof(int));
     if (e != cudaSuccess) rc = fail(h, DCOPF_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e));
@@ -631,8 +622,11 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   int dev_smem = 0;
   CK(h, cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   size_t need_b = batched_smem(h->n_bus, h->n_br, h->form);
-  if (path == DCOPF_PATH_BATCHED && need_b > (size_t)dev_smem)
-    return fail(h, DCOPF_EINVAL, "batched path needs %zu B shared memory (> %d); use the single path", need_b, dev_smem);
+  if (batched_path(path) && need_b > (size_t)dev_smem)
+    return fail(h, DCOPF_EINVAL, "batched path needs %zu B shared memory (> %d); use the single path",
+                need_b, dev_smem);
+  if (path == DCOPF_PATH_BATCHED && !h->sched_ok)
+    return fail(h, DCOPF_EINVAL, "batched schedule unavailable: %s", h->sched_err.c_str());
   size_t ss_state = single_smem(h->n_bus, h->n_br, h->form, true);
   size_t ss_nostate = single_smem(h->n_bus, h->n_br, h->form, false);
   if (path == DCOPF_PATH_SINGLE && ss_nostate > (size_t)dev_smem)
@@ -656,7 +650,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   if (!reuse) free_batch(h);
   h->path = path;
   h->B = B;
-  h->T = (path == DCOPF_PATH_BATCHED) ? kTile : 1;
+  h->T = batched_path(path) ? kTile : 1;
   h->B_pad = (B + h->T - 1) / h->T * h->T;
   h->max_out = max_out;
   h->cur = 0;
@@ -664,7 +658,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   h->single_smem = ss_state <= (size_t)dev_smem;
   h->smem_single = (int)(h->single_smem ? ss_state : ss_nostate);
   const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_br * brw(h->form);
-  const int nbuf = (path == DCOPF_PATH_BATCHED) ? 2 : 1;
+  const int nbuf = batched_path(path) ? 2 : 1;
   if (!reuse) {
     for (int i = 0; i < nbuf; ++i) {
       CK(h, cudaMalloc(&h->lam[i], std::max<size_t>(nlam, 1) * 8));
@@ -709,7 +703,7 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     if (rc) return rc;
     hist = h->scratch;
   }
-  if (h->path == DCOPF_PATH_BATCHED) {
+  if (h->path == DCOPF_PATH_BATCHED_SIMPLE) {
     for (int64_t k = 0; k < K; ++k) {
       BatchArgs a = batch_args(h);
       a.hist = hist;
@@ -721,28 +715,64 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     int rc = launch_batched_form<kModeFinal>(h, a, 0.0, (long)K, s);
     if (rc) return rc;
   } else {
-    if (!h->alpha_ev) CK(h, cudaEventCreateWithFlags(&h->alpha_ev, cudaEventDisableTiming));
-    CK(h, cudaEventSynchronize(h->alpha_ev));  // previous call's staging consumed
-    if ((size_t)K > h->alpha_cap) {
-      cudaFree(h->alpha_dev);
-      cudaFreeHost(h->alpha_pin);
-      h->alpha_dev = h->alpha_pin = nullptr;
-      h->alpha_cap = 0;
-      CK(h, cudaMalloc(&h->alpha_dev, K * 8));
-      CK(h, cudaMallocHost(&h->alpha_pin, K * 8));
-      h->alpha_cap = K;
-    }
-    if (K > 0) {
-      CK(h, cudaMemcpy(h->alpha_pin, alpha, K * 8, cudaMemcpyDefault));
-      CK(h, cudaMemcpyAsync(h->alpha_dev, h->alpha_pin, K * 8, cudaMemcpyHostToDevice, s));
-      CK(h, cudaEventRecord(h->alpha_ev, s));
-    }
-    SingleArgs a = single_args(h);
-    a.alpha = h->alpha_dev;
-    a.K = K;
-    a.hist = hist;
-    int rc = launch_single<kModeStep>(h, a, s);
+    int rc = stage_alpha(h, K, alpha, s);
     if (rc) return rc;
+    if (h->path == DCOPF_PATH_BATCHED) {
+      PipeArgs a;
+      a.lam0 = h->lam[0];
+      a.lam1 = h->lam[1];
+      a.br0 = h->br[0];
+      a.br1 = h->br[1];
+      a.d = h->load;
+      a.outs = h->outs;
+      a.max_out = h->max_out;
+      a.cur = h->cur;
+      a.alpha = h->alpha_dev;
+      a.K = K;
+      a.bound = h->bound;
+      a.best = h->best;
+      a.status = h->status;
+      a.hist = hist;
+      a.B = h->B;
+      a.n_bus = h->n_bus;
+      a.n_br = h->n_br;
+      a.ref = h->ref_int;
+      a.prog = h->d_prog;
+      a.prog_off = h->d_prog_off;
+      a.prog_bytes = h->d_prog_bytes;
+      a.tx_bytes = h->d_tx_bytes;
+      a.ld_ptr = h->d_ld_ptr;
+      a.ld_ent = h->d_ld_ent;
+      a.ld_slot = h->d_ld_slot;
+      const Schedule &sc = h->sch;
+      a.nch = sc.nch;
+      a.S = sc.S;
+      a.off_bar = sc.off_bar;
+      a.off_red = sc.off_red;
+      a.off_frz = sc.off_frz;
+      a.off_prog = sc.off_prog;
+      a.prog_stride = (sc.max_prog_bytes + 127) & ~127;
+      a.off_brp = sc.off_brp;
+      a.off_lamp = sc.off_lamp;
+      a.off_dp = sc.off_dp;
+      a.off_th = sc.off_th;
+      a.off_fc = sc.off_fc;
+      const unsigned grid = (unsigned)(h->B_pad / kTile);
+      const unsigned threads = (kPipeWarps + 1) * 32;
+      if (h->form == DCOPF_FORM_FLOW_BOX)
+        k_pipe<kFormF2, kPipeWarps><<<grid, threads, h->smem_pipe, s>>>(a);
+      else
+        k_pipe<kFormF1, kPipeWarps><<<grid, threads, h->smem_pipe, s>>>(a);
+      CK(h, cudaGetLastError());
+      h->cur = (int)((h->cur + K) & 1);
+    } else {
+      SingleArgs a = single_args(h);
+      a.alpha = h->alpha_dev;
+      a.K = K;
+      a.hist = hist;
+      rc = launch_single<kModeStep>(h, a, s);
+      if (rc) return rc;
+    }
   }
   if (hist_host) {
     CK(h, cudaMemcpyAsync(history, hist, (size_t)K * h->B * 8, cudaMemcpyDefault, s));
@@ -767,7 +797,7 @@ int dcopf_dual_get_multipliers(dcopf_dual_t h, double *lambda, double *branch, v
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  const int cur = (h->path == DCOPF_PATH_BATCHED) ? h->cur : 0;
+  const int cur = batched_path(h->path) ? h->cur : 0;
   int rc = export_ext(h, h->lam[cur], lambda, h->d_bus_inv, h->n_bus, 1, s);
   if (!rc) rc = export_ext(h, h->br[cur], branch, h->d_br_inv, h->n_br, brw(h->form), s);
   return rc;
@@ -778,7 +808,7 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  const int cur = (h->path == DCOPF_PATH_BATCHED) ? h->cur : 0;
+  const int cur = batched_path(h->path) ? h->cur : 0;
   // validate into scratch-free temporaries: import, then check the internal copy
   const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_br * brw(h->form);
   double *tl = nullptr, *tb = nullptr;
@@ -817,7 +847,7 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
   if (!h->g_lam) CK(h, cudaMalloc(&h->g_lam, std::max<size_t>(nlam, 1) * 8));
   if (!h->g_br) CK(h, cudaMalloc(&h->g_br, std::max<size_t>(nbr, 1) * 8));
   int rc;
-  if (h->path == DCOPF_PATH_BATCHED) {
+  if (batched_path(h->path)) {
     BatchArgs a = batch_args(h);
     a.lam_o = h->g_lam;
     a.br_o = h->g_br;
@@ -851,7 +881,15 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
   info->alg_bytes_per_inst_iter =
       8LL * (3LL * h->n_bus + (h->form == DCOPF_FORM_LIMIT_ROWS ? 4LL : 2LL) * h->n_br);
   info->bandwidth = h->bandwidth;
+  info->chunk = h->sch.CH;
+  info->ring_bus = h->sch.n_lam_slots;
+  info->ring_branch = h->sch.n_br_slots;
   if (h->path == DCOPF_PATH_BATCHED) {
+    info->smem_bytes = h->smem_pipe;
+    info->threads_per_block = (kPipeWarps + 1) * 32;
+    info->grid = (int)(h->B_pad / kTile);
+    info->launches_per_iter = 0;
+  } else if (h->path == DCOPF_PATH_BATCHED_SIMPLE) {
     info->smem_bytes = h->smem_batched;
     info->threads_per_block = kWarps * 32;
     info->grid = (int)(h->B_pad / kTile);

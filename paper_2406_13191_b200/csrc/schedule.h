@@ -1,0 +1,91 @@
+// schedule.h -- host-side compiler of the batched path's sweep schedule.
+//
+// The batched kernel (pipe_kernel.cuh) sweeps each 32-instance tile once per
+// iteration in chunks of CH buses (internal order).  For every chunk this
+// compiler emits
+//   * a "program" block: the bus / branch / ready-bus lists of the chunk's
+//     three phases with every topology constant and every shared-memory slot
+//     index they touch, laid out contiguously so one TMA bulk copy brings it
+//     on chip;
+//   * a load list: the state rows (lambda, d, nu or mu) whose first use is in
+//     this chunk, each with the shared-memory slot it is copied to.
+// Slots are assigned by greedy interval colouring over each row's live range
+// [first use - P, last use] in chunks (P = prefetch depth), so a slot is only
+// reloaded after its previous occupant's last reader finished; the number of
+// slots is the maximum overlap, which the bus order (DFS over a BFS spanning
+// tree, smallest subtree first) keeps small.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dcopf {
+
+// program block header: int32 words
+enum ProgHeader {
+  PH_NA = 0, PH_NIA, PH_NB, PH_NC, PH_NIC, PH_NG, PH_A0, PH_B0,
+  // byte offsets of the sections
+  PH_A_PTR, PH_A_THS, PH_A_TH,
+  PH_IA_ROW, PH_IA_BR, PH_IA_B, PH_IA_LS, PH_IA_LT,
+  PH_B_ROW, PH_B_TS, PH_B_TT, PH_B_B, PH_B_F, PH_B_THS, PH_B_THT, PH_B_LS, PH_B_LT, PH_B_FS,
+  PH_C_BUS, PH_C_LS, PH_C_DS, PH_C_GP, PH_C_IP,
+  PH_G_C, PH_G_LO, PH_G_HI, PH_G_A,
+  PH_IC_A, PH_IC_BR, PH_IC_X, PH_IC_TT, PH_IC_THS, PH_IC_THT,
+  PH_BYTES,
+  PH_COUNT
+};
+constexpr int kProgHeaderBytes = ((PH_COUNT * 4 + 15) / 16) * 16;
+
+// load-list entry kinds (top 2 bits of the packed entity word)
+enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
+
+struct NetInternal {
+  int nb, nl, ref, form;                   // internal numbering
+  std::vector<int> bus_ptr, bus_inc;        // CSR, entries (l << 1) | is_to, ascending original id
+  std::vector<int> bs, bt;                  // branch endpoints
+  std::vector<double> b, F, theta;          // per branch / per bus
+  std::vector<int> gen_ptr;                 // per bus
+  std::vector<double> gc, glo, ghi, ga;     // per generator (grouped by bus)
+};
+
+struct Schedule {
+  int CH = 0, P = 0, S = 0, nch = 0;
+  int n_br_slots = 0, n_lam_slots = 0, n_d_slots = 0, n_th_slots = 0, n_f_slots = 0;
+  int br_row_bytes = 0;                     // 256 (nu) or 512 (mu+, mu-)
+  int max_prog_bytes = 0;
+  std::vector<uint8_t> prog;                // all program blocks
+  std::vector<long long> prog_off;          // [nch] byte offset of each block
+  std::vector<int> prog_bytes;              // [nch]
+  std::vector<int> tx_bytes;                // [nch] program + rows (expect_tx)
+  std::vector<int> ld_ptr, ld_ent, ld_slot; // load lists
+  size_t smem_bytes(int nw) const;
+  // smem layout offsets (bytes)
+  int off_bar, off_red, off_frz, off_prog, off_brp, off_lamp, off_dp, off_th, off_fc, total;
+};
+
+struct Internalized {
+  NetInternal net;
+  std::vector<int> bus_perm, bus_inv, br_perm, br_inv;  // perm: internal -> original
+  int bandwidth = 0;
+};
+
+// Reverse Cuthill-McKee order (pseudo-peripheral start); kept for comparison.
+std::vector<int> rcm_order(int n, const std::vector<std::vector<int>> &adj);
+
+// Internal numbering of a validated network: bus order (DFS tree order, or
+// RCM), branches sorted by (larger, smaller) internal endpoint, CSR with
+// entries in ascending original branch id, generators grouped per bus.
+// theta is indexed by ORIGINAL bus id.
+std::string internalize(int nb, int nl, int ng, int ref, const int *fr, const int *to, const double *b,
+                        const double *F, const double *theta, const int *gen_bus, const double *pmin,
+                        const double *pmax, const double *c, const double *a, int form, bool rcm,
+                        Internalized *out);
+
+// Bus order: DFS preorder of a BFS spanning tree rooted at `root`, children
+// visited smallest subtree first (keeps the live re-read window small).
+std::vector<int> dfs_tree_order(int n, const std::vector<std::vector<int>> &adj, int root);
+
+// Build the schedule; returns an empty string or an error message.
+std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedule *out);
+
+}  // namespace dcopf

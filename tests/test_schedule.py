@@ -1,0 +1,68 @@
+"""CPU check of the batched path's host-compiled sweep schedule (the slot
+allocator behind the TMA pipeline): tests/sched_check.cpp replays the
+producer/consumer order of k_pipe with worst-case (instant) copy landing and
+asserts every shared-memory slot read holds the expected row / code and every
+bus and branch is visited once per phase.  Shares schedule.cpp with the
+library (host logic, no GPU, no oracle)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2406_13191_b200 import instances as inst
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = "/tmp/dcopf_sched_check"
+
+
+@pytest.fixture(scope="module")
+def checker():
+    src = [os.path.join(ROOT, "tests", "sched_check.cpp"),
+           os.path.join(ROOT, "paper_2406_13191_b200", "csrc", "schedule.cpp")]
+    subprocess.check_call(["g++", "-O2", "-std=c++17", "-o", EXE] + src)
+    return EXE
+
+
+def run(checker, net, form, CH, P, order="dfs"):
+    lines = [f"{net.n_bus} {net.n_branch} {net.ref_bus} {form} {CH} {P}"]
+    lines += [f"{a} {b}" for a, b in zip(net.br_from, net.br_to)]
+    res = subprocess.run([checker, order], input="\n".join(lines) + "\n", capture_output=True, text=True)
+    return res.returncode, res.stdout
+
+
+@pytest.mark.parametrize("config", [0, 1, 3])
+@pytest.mark.parametrize("form", [0, 1])
+@pytest.mark.parametrize("CH,P", [(32, 2), (8, 1), (64, 3)])
+def test_schedule_slots_valid(checker, config, form, CH, P):
+    net = inst.make_network(config)
+    rc, out = run(checker, net, form, CH, P)
+    assert rc == 0, out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_schedule_random_small(checker, seed):
+    rng = np.random.default_rng(seed)
+    nb = int(rng.integers(1, 60))
+    nl = int(rng.integers(nb - 1, 3 * nb)) if nb > 1 else 0
+    net = inst.tiny_network(nb, max(nl, nb - 1), 3, seed=seed) if nb > 1 else None
+    if net is None:
+        return
+    for form in (0, 1):
+        for CH, P in ((1, 1), (3, 2), (16, 1)):
+            rc, out = run(checker, net, form, CH, P)
+            assert rc == 0, out
+            rc, out = run(checker, net, form, CH, P, order="rcm")
+            assert rc == 0, out
+
+
+def test_dfs_order_keeps_smem_small(checker):
+    """The DFS tree order is what makes the window fit: config-3 network,
+    CH=16, P=2 fits two CTAs per SM (<= ~113 KB) for both forms; RCM does not
+    come close."""
+    net = inst.make_network(3)
+    for form in (0, 1):
+        rc, out = run(checker, net, form, 16, 2)
+        assert rc == 0 and int(out.split("smem ")[1].split()[0]) <= 113 * 1024, out
+    rc, out = run(checker, net, 0, 16, 2, order="rcm")
+    assert int(out.split("smem ")[1].split()[0]) > 227 * 1024, out
