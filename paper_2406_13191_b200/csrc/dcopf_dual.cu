@@ -757,6 +757,18 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
       a.off_dp = sc.off_dp;
       a.off_th = sc.off_th;
       a.off_fc = sc.off_fc;
+      a.dbg = nullptr;
+      if (getenv("DCOPF_DEBUG_PROGRESS")) {
+        static int *dbg_host = nullptr;
+        if (!dbg_host) {
+          CK(h, cudaHostAlloc(&dbg_host, 64 * sizeof(int), cudaHostAllocMapped));
+          memset(dbg_host, 0xff, 64 * sizeof(int));
+        }
+        int *dev = nullptr;
+        CK(h, cudaHostGetDevicePointer(&dev, dbg_host, 0));
+        a.dbg = dev;
+        fprintf(stderr, "DCOPF_DEBUG_PROGRESS host=%p\n", (void *)dbg_host);
+      }
       const unsigned grid = (unsigned)(h->B_pad / kTile);
       const unsigned threads = (kPipeWarps + 1) * 32;
       if (h->form == DCOPF_FORM_FLOW_BOX)

@@ -58,6 +58,7 @@ struct PipeArgs {
   const int *ld_ptr, *ld_ent, *ld_slot;
   int nch, S;
   int off_bar, off_red, off_frz, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th, off_fc;
+  volatile int *dbg;                // debug progress (mapped host memory) or null
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -138,17 +139,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) k_pipe(const PipeArgs a) {
         const long g = k * nch + c;
         const int st = (int)(g % S);
         const long u = g / S;
+        if (a.dbg && lane == 0 && tile == 0) a.dbg[0] = (int)(2 * g);
         if (u > 0) mbar_wait(&empty[st], (unsigned)((u - 1) & 1));
+        if (a.dbg && lane == 0 && tile == 0) a.dbg[0] = (int)(2 * g + 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(&full[st], (unsigned)a.tx_bytes[c]);
           tma_load_1d(smem + a.off_prog + st * a.prog_stride, a.prog + a.prog_off[c], (unsigned)a.prog_bytes[c],
                       &full[st]);
         }
         __syncwarp();
+        if (a.dbg && lane == 0 && tile == 0) a.dbg[9] = (int)(g);
         const int e0 = a.ld_ptr[c], e1 = a.ld_ptr[c + 1];
         for (int e = e0 + lane; e < e1; e += 32) {
           const int x = a.ld_ent[e], slot = a.ld_slot[e];
-          const int kind = x >> 30, ent = x & 0x3fffffff;
+          const int kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff;
           if (kind == LD_LAM)
             tma_load_1d(smem + a.off_lamp + slot * 256, lam_src + (size_t)ent * 256, 256, &full[st]);
           else if (kind == LD_D)
@@ -187,7 +191,31 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) k_pipe(const PipeArgs a) {
     for (int c = 0; c < nch; ++c) {
       const long g = k * nch + c;
       const int st = (int)(g % S);
+      if (a.dbg && lane == 0 && tile == 0) a.dbg[1 + warp] = (int)(4 * g);
+      if (a.dbg) {
+        long spins = 0;
+        unsigned done = 0;
+        do {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+              "selp.u32 %0, 1, 0, p;\n\t}"
+              : "=r"(done)
+              : "r"(smem_u32(&full[st])), "r"((unsigned)((g / S) & 1))
+              : "memory");
+          if (++spins == 2000000 && lane == 0 && warp == 0 && tile == 0) {
+            const unsigned long long raw = *reinterpret_cast<volatile unsigned long long *>(&full[st]);
+            a.dbg[10] = (int)(raw & 0xffffffffu);
+            a.dbg[11] = (int)(raw >> 32);
+            a.dbg[12] = st;
+            a.dbg[13] = a.tx_bytes[c];
+            a.dbg[14] = a.prog_bytes[c];
+            a.dbg[15] = a.ld_ptr[c + 1] - a.ld_ptr[c];
+          }
+        } while (!done);
+      }
       mbar_wait(&full[st], (unsigned)((g / S) & 1));
+      if (a.dbg && lane == 0 && tile == 0) a.dbg[1 + warp] = (int)(4 * g + 1);
       const uint8_t *prog = smem + a.off_prog + st * a.prog_stride;
       const int *hd = reinterpret_cast<const int *>(prog);
 
@@ -224,6 +252,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) k_pipe(const PipeArgs a) {
           if (notref) val += w * (pos ? tv : (neg ? -tv : 0.0));
         }
       }
+      if (a.dbg && lane == 0 && tile == 0) a.dbg[1 + warp] = (int)(4 * g + 2);
       named_bar(1, CT);
       // ---------------- B: branches ----------------
       {

@@ -333,7 +333,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
   std::vector<int> row_bytes(nch, 0);
   for (int c = 0; c < nch; ++c) {
     for (int x : lds[c]) {
-      int kind = x >> 30, ent = x & 0x3fffffff;
+      int kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff;
       S.ld_ent.push_back(x);
       int slot = kind == LD_LAM ? lam_slot[ent] : (kind == LD_D ? d_slot[ent] : br_slot[ent]);
       S.ld_slot.push_back(slot);

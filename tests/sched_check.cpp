@@ -40,7 +40,7 @@ int main(int argc, char **argv) {
   auto issue = [&](int c) {
     if (c >= S.nch) return;
     for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
-      int x = S.ld_ent[e], kind = x >> 30, ent = x & 0x3fffffff, slot = S.ld_slot[e];
+      int x = S.ld_ent[e], kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff, slot = S.ld_slot[e];
       (kind == LD_LAM ? lamp : kind == LD_D ? dp : brp)[slot] = ent;
     }
   };
@@ -51,6 +51,19 @@ int main(int argc, char **argv) {
       ++bad;
     }
   };
+  // expect_tx of every chunk = program block + the rows the producer copies
+  for (int c = 0; c < S.nch; ++c) {
+    long bytes = S.prog_bytes[c];
+    for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
+      int kind = (int)((unsigned)S.ld_ent[e] >> 30);
+      if (kind != LD_LAM && kind != LD_D && kind != LD_BR) { printf("BAD kind %d\n", kind); ++bad; }
+      bytes += (kind == LD_BR) ? S.br_row_bytes : 256;
+    }
+    if (bytes != S.tx_bytes[c] || S.prog_bytes[c] % 16 || S.prog_bytes[c] > S.max_prog_bytes) {
+      printf("BAD tx chunk %d: %ld vs %d\n", c, bytes, S.tx_bytes[c]);
+      ++bad;
+    }
+  }
   for (int c = 0; c <= P; ++c) issue(c);
   for (int c = 0; c < S.nch; ++c) {
     const uint8_t *pg = S.prog.data() + S.prog_off[c];
