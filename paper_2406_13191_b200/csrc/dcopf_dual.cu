@@ -750,6 +750,7 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
       a.off_bar = sc.off_bar;
       a.off_red = sc.off_red;
       a.off_frz = sc.off_frz;
+      a.off_obm = sc.off_obm;
       a.off_prog = sc.off_prog;
       a.prog_stride = (sc.max_prog_bytes + 127) & ~127;
       a.off_brp = sc.off_brp;

@@ -57,7 +57,7 @@ struct PipeArgs {
   const int *prog_bytes, *tx_bytes; // [nch]
   const int *ld_ptr, *ld_ent, *ld_slot;
   int nch, S;
-  int off_bar, off_red, off_frz, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th, off_fc;
+  int off_bar, off_red, off_frz, off_obm, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th, off_fc;
   volatile int *dbg;                // debug progress (mapped host memory) or null
 };
 
@@ -98,10 +98,6 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-template <typename T>
-__device__ __forceinline__ const T *sec(const uint8_t *prog, int field) {
-  return reinterpret_cast<const T *>(prog + reinterpret_cast<const int *>(prog)[field]);
-}
 
 template <int FORM, int NW>
 __global__ void __launch_bounds__((NW + 1) * 32, 2) k_pipe(const PipeArgs a) {
@@ -166,17 +162,28 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) k_pipe(const PipeArgs a) {
   }
 
   // =========================== consumers ===========================
-  const double *brp = reinterpret_cast<const double *>(smem + a.off_brp) + lane;
-  const double *lamp = reinterpret_cast<const double *>(smem + a.off_lamp) + lane;
-  const double *dp = reinterpret_cast<const double *>(smem + a.off_dp) + lane;
+  const uint8_t *brp = smem + a.off_brp + lane * 8;   // + row byte offset
+  const uint8_t *lamp = smem + a.off_lamp + lane * 8;
+  const uint8_t *dp = smem + a.off_dp + lane * 8;
   uint2 *th = reinterpret_cast<uint2 *>(smem + a.off_th);
   uint2 *fc = reinterpret_cast<uint2 *>(smem + a.off_fc);
+  unsigned *obm = reinterpret_cast<unsigned *>(smem + a.off_obm);
+  constexpr int CT = NW * 32;
+  auto ld = [](const uint8_t *base, int off) { return *reinterpret_cast<const double *>(base + off); };
   int o[kMaxOut];
   const int nout = a.max_out;
 #pragma unroll
   for (int j = 0; j < kMaxOut; ++j) o[j] = (j < nout) ? a.outs[b * nout + j] : -1;
+  // per-tile outage bitmap: bit l set if some instance of the tile has branch l
+  // out; the per-lane check only runs for flagged branches (rare)
+  for (int x = threadIdx.x; x < (a.n_br + 31) / 32; x += CT) obm[x] = 0u;
+  named_bar(1, CT);
+#pragma unroll
+  for (int j = 0; j < kMaxOut; ++j)
+    if (o[j] >= 0) atomicOr(&obm[o[j] >> 5], 1u << (o[j] & 31));
+  named_bar(1, CT);
+  auto flagged = [&](int l) { return (obm[l >> 5] >> (l & 31)) & 1u; };
   double best = a.best[b];
-  constexpr int CT = NW * 32;
 
   for (long k = 0; k <= a.K; ++k) {
     const bool last = (k == a.K);
@@ -192,96 +199,72 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) k_pipe(const PipeArgs a) {
       const long g = k * nch + c;
       const int st = (int)(g % S);
       if (a.dbg && lane == 0 && tile == 0) a.dbg[1 + warp] = (int)(4 * g);
-      if (a.dbg) {
-        long spins = 0;
-        unsigned done = 0;
-        do {
-          asm volatile(
-              "{\n\t.reg .pred p;\n\t"
-              "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-              "selp.u32 %0, 1, 0, p;\n\t}"
-              : "=r"(done)
-              : "r"(smem_u32(&full[st])), "r"((unsigned)((g / S) & 1))
-              : "memory");
-          if (++spins == 2000000 && lane == 0 && warp == 0 && tile == 0) {
-            const unsigned long long raw = *reinterpret_cast<volatile unsigned long long *>(&full[st]);
-            a.dbg[10] = (int)(raw & 0xffffffffu);
-            a.dbg[11] = (int)(raw >> 32);
-            a.dbg[12] = st;
-            a.dbg[13] = a.tx_bytes[c];
-            a.dbg[14] = a.prog_bytes[c];
-            a.dbg[15] = a.ld_ptr[c + 1] - a.ld_ptr[c];
-          }
-        } while (!done);
-      }
       mbar_wait(&full[st], (unsigned)((g / S) & 1));
-      if (a.dbg && lane == 0 && tile == 0) a.dbg[1 + warp] = (int)(4 * g + 1);
       const uint8_t *prog = smem + a.off_prog + st * a.prog_stride;
-      const int *hd = reinterpret_cast<const int *>(prog);
+      const int4 h0 = *reinterpret_cast<const int4 *>(prog);        // nA nIA nB nC
+      const int4 h1 = *reinterpret_cast<const int4 *>(prog + 16);   // nIC nG a0 b0
+      const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);   // offA offIA offB offC
+      const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);   // offG offIC
 
       // ---------------- A: w_i, theta* codes ----------------
       {
-        const int nA = hd[PH_NA], a0 = hd[PH_A0];
-        const int *A_ptr = sec<int>(prog, PH_A_PTR), *A_ths = sec<int>(prog, PH_A_THS);
-        const double *A_th = sec<double>(prog, PH_A_TH);
-        const int *IA_row = sec<int>(prog, PH_IA_ROW), *IA_br = sec<int>(prog, PH_IA_BR);
-        const double *IA_b = sec<double>(prog, PH_IA_B);
-        const int *IA_ls = sec<int>(prog, PH_IA_LS), *IA_lt = sec<int>(prog, PH_IA_LT);
-        for (int j = warp; j < nA; j += NW) {
-          const int bus = a0 + j;
+        const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
+        for (int j = warp; j < h0.x; j += NW) {
+          const RecA ra = A[j];
+          const int bus = h1.z + j;
           double w = 0.0;
-          const int e1 = A_ptr[j + 1];
-          for (int e = A_ptr[j]; e < e1; ++e) {
-            const unsigned code = (unsigned)IA_row[e];
-            const int slot = (int)(code & 0x7fffffffu);
-            const bool to = code >> 31;
-            const double bl = is_out(o, nout, IA_br[e]) ? 0.0 : IA_b[e];
-            if (FORM == kFormF2) {
-              const double t = bl * brp[slot * 32];
-              w = to ? w + t : w + (-t);
-            } else {
-              const double u = bl * ((brp[slot * 64] - brp[slot * 64 + 32]) - (lamp[IA_ls[e] * 32] - lamp[IA_lt[e] * 32]));
-              w = to ? w - u : w + u;
+          if (FORM == kFormF2) {
+            const RecIA2 *IA = reinterpret_cast<const RecIA2 *>(prog + h2.y);
+            for (int e = ra.e0; e < ra.e1; ++e) {
+              const RecIA2 r = IA[e];
+              double sb = r.sb;
+              if (flagged(r.br) && is_out(o, nout, r.br)) sb = copysign(0.0, sb);
+              w = w + sb * ld(brp, r.row);                  // w_s += -(b nu), w_t += b nu
+            }
+          } else {
+            const RecIA1 *IA = reinterpret_cast<const RecIA1 *>(prog + h2.y);
+            for (int e = ra.e0; e < ra.e1; ++e) {
+              const RecIA1 r = IA[e];
+              double sb = r.sb;
+              if (flagged(r.br) && is_out(o, nout, r.br)) sb = copysign(0.0, sb);
+              const double x = (ld(brp, r.row) - ld(brp, r.row + 256)) - (ld(lamp, r.ls) - ld(lamp, r.lt));
+              w = w + sb * x;                                // w_s += u, w_t -= u
             }
           }
           const bool notref = (bus != a.ref);
           const bool pos = notref && (w < 0.0), neg = notref && (w > 0.0);
           const unsigned mp = __ballot_sync(0xffffffffu, pos), mn = __ballot_sync(0xffffffffu, neg);
-          if (lane == 0) th[A_ths[j]] = make_uint2(mp, mn);
-          const double tv = A_th[j];
-          if (notref) val += w * (pos ? tv : (neg ? -tv : 0.0));
+          if (lane == 0) th[ra.th] = make_uint2(mp, mn);
+          if (notref) val += w * (pos ? ra.theta : (neg ? -ra.theta : 0.0));
         }
       }
-      if (a.dbg && lane == 0 && tile == 0) a.dbg[1 + warp] = (int)(4 * g + 2);
       named_bar(1, CT);
       // ---------------- B: branches ----------------
       {
-        const int nB = hd[PH_NB], b0 = hd[PH_B0];
-        const int *B_row = sec<int>(prog, PH_B_ROW), *B_ts = sec<int>(prog, PH_B_TS), *B_tt = sec<int>(prog, PH_B_TT);
-        const double *B_b = sec<double>(prog, PH_B_B), *B_F = sec<double>(prog, PH_B_F);
-        const double *B_Ts = sec<double>(prog, PH_B_THS), *B_Tt = sec<double>(prog, PH_B_THT);
-        const int *B_ls = sec<int>(prog, PH_B_LS), *B_lt = sec<int>(prog, PH_B_LT), *B_fs = sec<int>(prog, PH_B_FS);
-        for (int j = warp; j < nB; j += NW) {
-          const int l = b0 + j;
-          const bool out = is_out(o, nout, l);
-          const double bl = out ? 0.0 : B_b[j];
-          const double Fl = out ? 0.0 : B_F[j];
-          const double ths = decode(th[B_ts[j]], lane, B_Ts[j]);
-          const double tht = decode(th[B_tt[j]], lane, B_Tt[j]);
+        const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
+        for (int j = warp; j < h0.z; j += NW) {
+          const RecB r = Bv[j];
+          const int l = h1.w + j;
+          double bl = r.b, Fl = r.F;
+          if (flagged(l) && is_out(o, nout, l)) {
+            bl = 0.0;
+            Fl = 0.0;
+          }
+          const double ths = decode(th[r.ts], lane, r.Ts);
+          const double tht = decode(th[r.tt], lane, r.Tt);
           const double phi = bl * (ths - tht);
-          const int row = B_row[j];
           if (FORM == kFormF2) {
-            const double nu = brp[row * 32];
-            const double q = nu - (lamp[B_ls[j] * 32] - lamp[B_lt[j] * 32]);
+            const double nu = ld(brp, r.row);
+            const double q = nu - (ld(lamp, r.ls) - ld(lamp, r.lt));
             const bool fneg = q > 0.0, fpos = q < 0.0;
             const unsigned mp = __ballot_sync(0xffffffffu, fpos), mn = __ballot_sync(0xffffffffu, fneg);
-            if (lane == 0) fc[B_fs[j]] = make_uint2(mp, mn);
+            if (lane == 0) fc[r.fs] = make_uint2(mp, mn);
             const double f = fneg ? -Fl : (fpos ? Fl : 0.0);
             const double gv = f - phi;
             val += q * f;
             if (!last) br_o[(size_t)l * kTile] = step ? nu + alpha * gv : nu;
           } else {
-            const double mp = brp[row * 64], mm = brp[row * 64 + 32];
+            const double mp = ld(brp, r.row), mm = ld(brp, r.row + 256);
             const double gp = phi - Fl, gm = -phi - Fl;
             val += -(Fl * (mp + mm));
             if (!last) {
@@ -301,44 +284,42 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2) k_pipe(const PipeArgs a) {
       named_bar(1, CT);
       // ---------------- C: ready buses ----------------
       {
-        const int nC = hd[PH_NC];
-        const int *C_bus = sec<int>(prog, PH_C_BUS), *C_ls = sec<int>(prog, PH_C_LS), *C_ds = sec<int>(prog, PH_C_DS);
-        const int *C_gp = sec<int>(prog, PH_C_GP), *C_ip = sec<int>(prog, PH_C_IP);
-        const double *G_c = sec<double>(prog, PH_G_C), *G_lo = sec<double>(prog, PH_G_LO);
-        const double *G_hi = sec<double>(prog, PH_G_HI), *G_a = sec<double>(prog, PH_G_A);
-        const int *IC_a = sec<int>(prog, PH_IC_A), *IC_br = sec<int>(prog, PH_IC_BR), *IC_tt = sec<int>(prog, PH_IC_TT);
-        const double *IC_x = sec<double>(prog, PH_IC_X), *IC_Ts = sec<double>(prog, PH_IC_THS),
-                     *IC_Tt = sec<double>(prog, PH_IC_THT);
-        for (int j = warp; j < nC; j += NW) {
-          const int i = C_bus[j];
-          const double li = lamp[C_ls[j] * 32];
-          const double di = dp[C_ds[j] * 32];
+        const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
+        const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
+        for (int j = warp; j < h0.w; j += NW) {
+          const RecC r = Cv[j];
+          const double li = ld(lamp, r.ls);
+          const double di = ld(dp, r.ds);
           double gl = -di;
-          const int g1 = C_gp[j + 1];
-          for (int gg = C_gp[j]; gg < g1; ++gg) {
-            const double r = G_c[gg] + li;
-            const double ag = G_a[gg];
-            const double p = gen_minimiser(r, G_lo[gg], G_hi[gg], ag);
+          for (int gg = r.g0; gg < r.g1; ++gg) {
+            const RecG gr = G[gg];
+            const double rr = gr.c + li;
+            const double p = gen_minimiser(rr, gr.lo, gr.hi, gr.a);
             gl = gl + p;
-            val += (ag > 0.0) ? ag * p * p + r * p : r * p;
+            val += (gr.a > 0.0) ? gr.a * p * p + rr * p : rr * p;
           }
-          const int e1 = C_ip[j + 1];
-          for (int e = C_ip[j]; e < e1; ++e) {
-            const unsigned code = (unsigned)IC_a[e];
-            const int sl = (int)(code & 0x7fffffffu);
-            const bool to = code >> 31;
-            const bool out = is_out(o, nout, IC_br[e]);
-            double fl;
-            if (FORM == kFormF2) {
-              fl = decode(fc[sl], lane, out ? 0.0 : IC_x[e]);
-            } else {
-              const double bl = out ? 0.0 : IC_x[e];
-              fl = bl * (decode(th[sl], lane, IC_Ts[e]) - decode(th[IC_tt[e]], lane, IC_Tt[e]));
+          if (FORM == kFormF2) {
+            const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y);
+            for (int e = r.e0; e < r.e1; ++e) {
+              const RecIC2 x = IC[e];
+              double sF = x.sF;
+              if (flagged(x.br) && is_out(o, nout, x.br)) sF = copysign(0.0, sF);
+              const uint2 cw = fc[x.fs];
+              // +f* at the to bus, -f* at the from bus (sign folded into sF)
+              const double v = ((cw.x >> lane) & 1u) ? sF : (((cw.y >> lane) & 1u) ? -sF : sF * 0.0);
+              gl = gl + v;
             }
-            gl = to ? gl + fl : gl - fl;
+          } else {
+            const RecIC1 *IC = reinterpret_cast<const RecIC1 *>(prog + h3.y);
+            for (int e = r.e0; e < r.e1; ++e) {
+              const RecIC1 x = IC[e];
+              double sb = x.sb;
+              if (flagged(x.br) && is_out(o, nout, x.br)) sb = copysign(0.0, sb);
+              gl = gl + sb * (decode(th[x.ts], lane, x.Ts) - decode(th[x.tt], lane, x.Tt));
+            }
           }
           val += -(li * di);
-          if (!last) lam_o[(size_t)i * kTile] = step ? li + alpha * gl : li;
+          if (!last) lam_o[(size_t)r.bus * kTile] = step ? li + alpha * gl : li;
         }
       }
       named_bar(1, CT);

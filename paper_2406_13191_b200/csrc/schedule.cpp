@@ -215,26 +215,6 @@ int colour(std::vector<Interval> iv, std::vector<int> &slot) {
   return n;
 }
 
-struct Writer {
-  std::vector<uint8_t> buf;
-  int32_t *hdr() { return reinterpret_cast<int32_t *>(buf.data()); }
-  void begin() {
-    buf.assign(kProgHeaderBytes, 0);
-  }
-  template <typename T>
-  void put(int field, const std::vector<T> &v) {
-    size_t off = (buf.size() + 7) & ~size_t(7);
-    buf.resize(off + v.size() * sizeof(T));
-    if (!v.empty()) memcpy(buf.data() + off, v.data(), v.size() * sizeof(T));
-    hdr()[field] = (int32_t)off;
-  }
-  void finish() {
-    size_t n = (buf.size() + 15) & ~size_t(15);
-    buf.resize(n, 0);
-    hdr()[PH_BYTES] = (int32_t)n;
-  }
-};
-
 }  // namespace
 
 size_t Schedule::smem_bytes(int) const { return (size_t)total; }
@@ -348,125 +328,125 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
   S.prog_bytes.assign(nch, 0);
   S.tx_bytes.assign(nch, 0);
   S.max_prog_bytes = 0;
-  Writer w;
+  const int BR = S.br_row_bytes;
   for (int c = 0; c < nch; ++c) {
-    w.begin();
     const int a0 = c * CH, a1 = std::min(nb, a0 + CH);
     const int nA = a1 - a0;
-    std::vector<int> A_ptr(nA + 1, 0), A_ths(nA), IA_row, IA_br, IA_ls, IA_lt;
-    std::vector<double> A_th(nA), IA_b;
-    for (int a = 0; a < nA; ++a) {
-      const int i = a0 + a;
-      A_ths[a] = th_slot[i];
-      A_th[a] = net.theta[i];
+    std::vector<RecA> A(nA);
+    std::vector<RecIA2> IA2;
+    std::vector<RecIA1> IA1;
+    for (int j = 0; j < nA; ++j) {
+      const int i = a0 + j;
+      RecA r{};
+      r.th = th_slot[i];
+      r.theta = net.theta[i];
+      r.e0 = f1 ? (int)IA1.size() : (int)IA2.size();
       for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
-        int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
-        IA_row.push_back(br_slot[l] | (to << 31));
-        IA_br.push_back(l);
-        IA_b.push_back(net.b[l]);
-        if (f1) {
-          IA_ls.push_back(lam_slot[net.bs[l]]);
-          IA_lt.push_back(lam_slot[net.bt[l]]);
+        const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
+        if (!f1) {
+          RecIA2 x{};
+          x.row = br_slot[l] * BR;
+          x.br = l;
+          x.sb = to ? net.b[l] : -net.b[l];   // w_s += -b nu ; w_t += b nu
+          IA2.push_back(x);
+        } else {
+          RecIA1 x{};
+          x.row = br_slot[l] * BR;
+          x.br = l;
+          x.ls = lam_slot[net.bs[l]] * 256;
+          x.lt = lam_slot[net.bt[l]] * 256;
+          x.sb = to ? -net.b[l] : net.b[l];   // w_s += u ; w_t -= u
+          IA1.push_back(x);
         }
       }
-      A_ptr[a + 1] = (int)IA_row.size();
+      r.e1 = f1 ? (int)IA1.size() : (int)IA2.size();
+      A[j] = r;
     }
     const int b0 = bch[c], nB = bch[c + 1] - bch[c];
-    std::vector<int> B_row(nB), B_ts(nB), B_tt(nB), B_ls, B_lt, B_fs;
-    std::vector<double> B_b(nB), B_F(nB), B_Ts(nB), B_Tt(nB);
+    std::vector<RecB> Bv(nB);
     for (int j = 0; j < nB; ++j) {
       const int l = b0 + j, s = net.bs[l], t = net.bt[l];
-      B_row[j] = br_slot[l];
-      B_ts[j] = th_slot[s];
-      B_tt[j] = th_slot[t];
-      B_b[j] = net.b[l];
-      B_F[j] = net.F[l];
-      B_Ts[j] = net.theta[s];
-      B_Tt[j] = net.theta[t];
+      RecB r{};
+      r.row = br_slot[l] * BR;
+      r.ts = th_slot[s];
+      r.tt = th_slot[t];
+      r.b = net.b[l];
+      r.F = net.F[l];
+      r.Ts = net.theta[s];
+      r.Tt = net.theta[t];
       if (!f1) {
-        B_ls.push_back(lam_slot[s]);
-        B_lt.push_back(lam_slot[t]);
-        B_fs.push_back(f_slot[l]);
+        r.ls = lam_slot[s] * 256;
+        r.lt = lam_slot[t] * 256;
+        r.fs = f_slot[l];
       }
+      Bv[j] = r;
     }
     const int nC = cch[c + 1] - cch[c];
-    std::vector<int> C_bus(nC), C_ls(nC), C_ds(nC), C_gp(nC + 1, 0), C_ip(nC + 1, 0), IC_a, IC_br, IC_tt;
-    std::vector<double> G_c, G_lo, G_hi, G_a, IC_x, IC_Ts, IC_Tt;
+    std::vector<RecC> Cv(nC);
+    std::vector<RecG> G;
+    std::vector<RecIC2> IC2;
+    std::vector<RecIC1> IC1;
     for (int j = 0; j < nC; ++j) {
       const int i = cord[cch[c] + j];
-      C_bus[j] = i;
-      C_ls[j] = lam_slot[i];
-      C_ds[j] = d_slot[i];
-      for (int g = net.gen_ptr[i]; g < net.gen_ptr[i + 1]; ++g) {
-        G_c.push_back(net.gc[g]);
-        G_lo.push_back(net.glo[g]);
-        G_hi.push_back(net.ghi[g]);
-        G_a.push_back(net.ga[g]);
-      }
-      C_gp[j + 1] = (int)G_c.size();
+      RecC r{};
+      r.bus = i;
+      r.ls = lam_slot[i] * 256;
+      r.ds = d_slot[i] * 256;
+      r.g0 = (int)G.size();
+      for (int g = net.gen_ptr[i]; g < net.gen_ptr[i + 1]; ++g) G.push_back(RecG{net.gc[g], net.glo[g], net.ghi[g], net.ga[g]});
+      r.g1 = (int)G.size();
+      r.e0 = f1 ? (int)IC1.size() : (int)IC2.size();
       for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
-        int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
-        IC_br.push_back(l);
+        const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
         if (!f1) {
-          IC_a.push_back(f_slot[l] | (to << 31));
-          IC_x.push_back(net.F[l]);
+          RecIC2 x{};
+          x.fs = f_slot[l];
+          x.br = l;
+          x.sF = to ? net.F[l] : -net.F[l];  // lambda grad: +f* at to, -f* at from
+          IC2.push_back(x);
         } else {
-          IC_a.push_back(th_slot[net.bs[l]] | (to << 31));
-          IC_tt.push_back(th_slot[net.bt[l]]);
-          IC_x.push_back(net.b[l]);
-          IC_Ts.push_back(net.theta[net.bs[l]]);
-          IC_Tt.push_back(net.theta[net.bt[l]]);
+          RecIC1 x{};
+          x.ts = th_slot[net.bs[l]];
+          x.tt = th_slot[net.bt[l]];
+          x.br = l;
+          x.sb = to ? net.b[l] : -net.b[l];  // +phi at to, -phi at from
+          x.Ts = net.theta[net.bs[l]];
+          x.Tt = net.theta[net.bt[l]];
+          IC1.push_back(x);
         }
       }
-      C_ip[j + 1] = (int)IC_a.size();
+      r.e1 = f1 ? (int)IC1.size() : (int)IC2.size();
+      Cv[j] = r;
     }
-    int32_t *h = w.hdr();
-    h[PH_NA] = nA;
-    h[PH_NIA] = (int)IA_row.size();
-    h[PH_NB] = nB;
-    h[PH_NC] = nC;
-    h[PH_NIC] = (int)IC_a.size();
-    h[PH_NG] = (int)G_c.size();
-    h[PH_A0] = a0;
-    h[PH_B0] = b0;
-    w.put(PH_A_PTR, A_ptr);
-    w.put(PH_A_THS, A_ths);
-    w.put(PH_A_TH, A_th);
-    w.put(PH_IA_ROW, IA_row);
-    w.put(PH_IA_BR, IA_br);
-    w.put(PH_IA_B, IA_b);
-    w.put(PH_IA_LS, IA_ls);
-    w.put(PH_IA_LT, IA_lt);
-    w.put(PH_B_ROW, B_row);
-    w.put(PH_B_TS, B_ts);
-    w.put(PH_B_TT, B_tt);
-    w.put(PH_B_B, B_b);
-    w.put(PH_B_F, B_F);
-    w.put(PH_B_THS, B_Ts);
-    w.put(PH_B_THT, B_Tt);
-    w.put(PH_B_LS, B_ls);
-    w.put(PH_B_LT, B_lt);
-    w.put(PH_B_FS, B_fs);
-    w.put(PH_C_BUS, C_bus);
-    w.put(PH_C_LS, C_ls);
-    w.put(PH_C_DS, C_ds);
-    w.put(PH_C_GP, C_gp);
-    w.put(PH_C_IP, C_ip);
-    w.put(PH_G_C, G_c);
-    w.put(PH_G_LO, G_lo);
-    w.put(PH_G_HI, G_hi);
-    w.put(PH_G_A, G_a);
-    w.put(PH_IC_A, IC_a);
-    w.put(PH_IC_BR, IC_br);
-    w.put(PH_IC_X, IC_x);
-    w.put(PH_IC_TT, IC_tt);
-    w.put(PH_IC_THS, IC_Ts);
-    w.put(PH_IC_THT, IC_Tt);
-    w.finish();
+    std::vector<uint8_t> blk(kProgHeaderBytes, 0);
+    int32_t hd[16] = {0};
+    auto app = [&](const void *p, size_t n) {
+      size_t off = (blk.size() + 15) & ~size_t(15);
+      blk.resize(off + n);
+      if (n) memcpy(blk.data() + off, p, n);
+      return (int32_t)off;
+    };
+    hd[PH_NA] = nA;
+    hd[PH_NIA] = f1 ? (int)IA1.size() : (int)IA2.size();
+    hd[PH_NB] = nB;
+    hd[PH_NC] = nC;
+    hd[PH_NIC] = f1 ? (int)IC1.size() : (int)IC2.size();
+    hd[PH_NG] = (int)G.size();
+    hd[PH_A0] = a0;
+    hd[PH_B0] = b0;
+    hd[PH_OFF_A] = app(A.data(), A.size() * sizeof(RecA));
+    hd[PH_OFF_IA] = f1 ? app(IA1.data(), IA1.size() * sizeof(RecIA1)) : app(IA2.data(), IA2.size() * sizeof(RecIA2));
+    hd[PH_OFF_B] = app(Bv.data(), Bv.size() * sizeof(RecB));
+    hd[PH_OFF_C] = app(Cv.data(), Cv.size() * sizeof(RecC));
+    hd[PH_OFF_G] = app(G.data(), G.size() * sizeof(RecG));
+    hd[PH_OFF_IC] = f1 ? app(IC1.data(), IC1.size() * sizeof(RecIC1)) : app(IC2.data(), IC2.size() * sizeof(RecIC2));
+    blk.resize((blk.size() + 15) & ~size_t(15), 0);
+    hd[PH_BYTES] = (int32_t)blk.size();
+    memcpy(blk.data(), hd, sizeof hd);
     S.prog_off[c] = (long long)S.prog.size();
-    S.prog_bytes[c] = (int)w.buf.size();
-    S.prog.insert(S.prog.end(), w.buf.begin(), w.buf.end());
-    S.max_prog_bytes = std::max(S.max_prog_bytes, (int)w.buf.size());
+    S.prog_bytes[c] = (int)blk.size();
+    S.prog.insert(S.prog.end(), blk.begin(), blk.end());
+    S.max_prog_bytes = std::max(S.max_prog_bytes, (int)blk.size());
     S.tx_bytes[c] = S.prog_bytes[c] + row_bytes[c];
   }
 
@@ -479,6 +459,8 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
   off = al(off + 8 * 32 * nw);
   S.off_frz = off;
   off = al(off + 4 * 32);
+  S.off_obm = off;                       // per-tile outage bitmap over branches
+  off = al(off + 4 * ((nl + 31) / 32 + 1));
   S.off_prog = off;
   off = al(off + S.S * al(S.max_prog_bytes));
   S.off_brp = off;

@@ -21,20 +21,27 @@
 
 namespace dcopf {
 
-// program block header: int32 words
+// Program block of one chunk: a 64-byte header followed by arrays of 16-B
+// aligned records (read with vector shared-memory loads).  Row fields are BYTE
+// offsets into the corresponding shared-memory pool; th/ts/tt/fs are indices
+// of 8-byte code words.  Signs of the incidence are folded into the
+// coefficients (sb = +-b, sF = +-F): x*(-y) == -(x*y) exactly in IEEE
+// arithmetic, so the per-entity results stay bitwise equal to the oracle's.
 enum ProgHeader {
   PH_NA = 0, PH_NIA, PH_NB, PH_NC, PH_NIC, PH_NG, PH_A0, PH_B0,
-  // byte offsets of the sections
-  PH_A_PTR, PH_A_THS, PH_A_TH,
-  PH_IA_ROW, PH_IA_BR, PH_IA_B, PH_IA_LS, PH_IA_LT,
-  PH_B_ROW, PH_B_TS, PH_B_TT, PH_B_B, PH_B_F, PH_B_THS, PH_B_THT, PH_B_LS, PH_B_LT, PH_B_FS,
-  PH_C_BUS, PH_C_LS, PH_C_DS, PH_C_GP, PH_C_IP,
-  PH_G_C, PH_G_LO, PH_G_HI, PH_G_A,
-  PH_IC_A, PH_IC_BR, PH_IC_X, PH_IC_TT, PH_IC_THS, PH_IC_THT,
-  PH_BYTES,
+  PH_OFF_A, PH_OFF_IA, PH_OFF_B, PH_OFF_C, PH_OFF_G, PH_OFF_IC, PH_BYTES, PH_PAD,
   PH_COUNT
 };
-constexpr int kProgHeaderBytes = ((PH_COUNT * 4 + 15) / 16) * 16;
+constexpr int kProgHeaderBytes = 64;
+
+struct alignas(16) RecA { int e0, e1, th, pad; double theta, pad2; };                      // bus of phase A
+struct alignas(16) RecIA2 { int row, br; double sb; };                                      // F2: sb = to ? b : -b
+struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };                         // F1: sb = to ? -b : b
+struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, pad0, pad1; double b, F, Ts, Tt; };  // branch of phase B
+struct alignas(16) RecC { int bus, ls, ds, g0, g1, e0, e1, pad; };                         // bus of phase C
+struct alignas(16) RecG { double c, lo, hi, a; };                                            // generator
+struct alignas(16) RecIC2 { int fs, br; double sF; };                                       // F2: sF = to ? F : -F
+struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, Ts, Tt, pad2; };               // F1: sb = to ? b : -b
 
 // load-list entry kinds (top 2 bits of the packed entity word)
 enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
@@ -60,7 +67,7 @@ struct Schedule {
   std::vector<int> ld_ptr, ld_ent, ld_slot; // load lists
   size_t smem_bytes(int nw) const;
   // smem layout offsets (bytes)
-  int off_bar, off_red, off_frz, off_prog, off_brp, off_lamp, off_dp, off_th, off_fc, total;
+  int off_bar, off_red, off_frz, off_obm, off_prog, off_brp, off_lamp, off_dp, off_th, off_fc, total;
 };
 
 struct Internalized {

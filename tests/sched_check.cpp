@@ -14,15 +14,14 @@
 
 using namespace dcopf;
 
-template <typename T>
-const T *sec(const uint8_t *p, int f) { return reinterpret_cast<const T *>(p + reinterpret_cast<const int *>(p)[f]); }
 
 int main(int argc, char **argv) {
   int nb, nl, ref, form, CH, P;
   if (scanf("%d %d %d %d %d %d", &nb, &nl, &ref, &form, &CH, &P) != 6) return 2;
   std::vector<int> fr(nl), to(nl);
   for (int l = 0; l < nl; ++l) if (scanf("%d %d", &fr[l], &to[l]) != 2) return 2;
-  std::vector<double> b(nl, 1.0), F(nl, 1.0), theta(nb, 1.0);
+  std::vector<double> b(nl), F(nl), theta(nb, 1.0);
+  for (int l = 0; l < nl; ++l) { b[l] = 1.0 + (l % 7); F[l] = 0.5 * (l % 5); }
   Internalized in;
   bool rcm = argc > 1 && std::string(argv[1]) == "rcm";
   std::string e0 = internalize(nb, nl, 0, ref, fr.data(), to.data(), b.data(), F.data(), theta.data(), nullptr,
@@ -68,49 +67,62 @@ int main(int argc, char **argv) {
   for (int c = 0; c < S.nch; ++c) {
     const uint8_t *pg = S.prog.data() + S.prog_off[c];
     const int *h = reinterpret_cast<const int *>(pg);
-    // A
-    const int *A_ptr = sec<int>(pg, PH_A_PTR), *A_ths = sec<int>(pg, PH_A_THS), *IA_row = sec<int>(pg, PH_IA_ROW),
-              *IA_br = sec<int>(pg, PH_IA_BR), *IA_ls = sec<int>(pg, PH_IA_LS), *IA_lt = sec<int>(pg, PH_IA_LT);
+    const int BR = S.br_row_bytes;
+    const RecA *A = reinterpret_cast<const RecA *>(pg + h[PH_OFF_A]);
+    const RecIA2 *IA2 = reinterpret_cast<const RecIA2 *>(pg + h[PH_OFF_IA]);
+    const RecIA1 *IA1 = reinterpret_cast<const RecIA1 *>(pg + h[PH_OFF_IA]);
     for (int j = 0; j < h[PH_NA]; ++j) {
       int bus = h[PH_A0] + j;
       seenA[bus]++;
-      if (A_ptr[j + 1] - A_ptr[j] != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD A degree\n"); ++bad; }
-      for (int e = A_ptr[j]; e < A_ptr[j + 1]; ++e) {
-        int l = IA_br[e];
-        if (l != (n.bus_inc[n.bus_ptr[bus] + e - A_ptr[j]] >> 1)) { printf("BAD A order\n"); ++bad; }
-        want(brp, IA_row[e] & 0x7fffffff, l, "A br", c);
-        if (f1) { want(lamp, IA_ls[e], n.bs[l], "A lam_s", c); want(lamp, IA_lt[e], n.bt[l], "A lam_t", c); }
+      if (A[j].e1 - A[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD A degree\n"); ++bad; }
+      for (int e = A[j].e0; e < A[j].e1; ++e) {
+        const int k = n.bus_ptr[bus] + e - A[j].e0;
+        const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
+        const int br = f1 ? IA1[e].br : IA2[e].br;
+        const double sb = f1 ? IA1[e].sb : IA2[e].sb;
+        if (br != l) { printf("BAD A order\n"); ++bad; }
+        if (sb != ((to ^ (int)f1) ? n.b[l] : -n.b[l])) { printf("BAD A sign\n"); ++bad; }
+        const int row = f1 ? IA1[e].row : IA2[e].row;
+        if (row % BR) { printf("BAD A row align\n"); ++bad; }
+        want(brp, row / BR, l, "A br", c);
+        if (f1) { want(lamp, IA1[e].ls / 256, n.bs[l], "A lam_s", c); want(lamp, IA1[e].lt / 256, n.bt[l], "A lam_t", c); }
       }
-      th[A_ths[j]] = bus;
+      th[A[j].th] = bus;
     }
-    // B
-    const int *B_row = sec<int>(pg, PH_B_ROW), *B_ts = sec<int>(pg, PH_B_TS), *B_tt = sec<int>(pg, PH_B_TT),
-              *B_ls = sec<int>(pg, PH_B_LS), *B_lt = sec<int>(pg, PH_B_LT), *B_fs = sec<int>(pg, PH_B_FS);
+    const RecB *Bv = reinterpret_cast<const RecB *>(pg + h[PH_OFF_B]);
     for (int j = 0; j < h[PH_NB]; ++j) {
       int l = h[PH_B0] + j;
       seenB[l]++;
-      want(brp, B_row[j], l, "B br", c);
-      want(th, B_ts[j], n.bs[l], "B th_s", c);
-      want(th, B_tt[j], n.bt[l], "B th_t", c);
+      want(brp, Bv[j].row / BR, l, "B br", c);
+      want(th, Bv[j].ts, n.bs[l], "B th_s", c);
+      want(th, Bv[j].tt, n.bt[l], "B th_t", c);
       if (!f1) {
-        want(lamp, B_ls[j], n.bs[l], "B lam_s", c);
-        want(lamp, B_lt[j], n.bt[l], "B lam_t", c);
-        fc[B_fs[j]] = l;
+        want(lamp, Bv[j].ls / 256, n.bs[l], "B lam_s", c);
+        want(lamp, Bv[j].lt / 256, n.bt[l], "B lam_t", c);
+        fc[Bv[j].fs] = l;
       }
     }
-    // C
-    const int *C_bus = sec<int>(pg, PH_C_BUS), *C_ls = sec<int>(pg, PH_C_LS), *C_ds = sec<int>(pg, PH_C_DS),
-              *C_ip = sec<int>(pg, PH_C_IP), *IC_a = sec<int>(pg, PH_IC_A), *IC_br = sec<int>(pg, PH_IC_BR),
-              *IC_tt = sec<int>(pg, PH_IC_TT);
+    const RecC *Cv = reinterpret_cast<const RecC *>(pg + h[PH_OFF_C]);
+    const RecIC2 *IC2 = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
+    const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
     for (int j = 0; j < h[PH_NC]; ++j) {
-      int bus = C_bus[j];
+      int bus = Cv[j].bus;
       seenC[bus]++;
-      want(lamp, C_ls[j], bus, "C lam", c);
-      want(dp, C_ds[j], bus, "C d", c);
-      for (int e = C_ip[j]; e < C_ip[j + 1]; ++e) {
-        int l = IC_br[e];
-        if (!f1) want(fc, IC_a[e] & 0x7fffffff, l, "C f", c);
-        else { want(th, IC_a[e] & 0x7fffffff, n.bs[l], "C th_s", c); want(th, IC_tt[e], n.bt[l], "C th_t", c); }
+      want(lamp, Cv[j].ls / 256, bus, "C lam", c);
+      want(dp, Cv[j].ds / 256, bus, "C d", c);
+      if (Cv[j].e1 - Cv[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD C degree\n"); ++bad; }
+      for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
+        const int k = n.bus_ptr[bus] + e - Cv[j].e0;
+        const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
+        if ((f1 ? IC1[e].br : IC2[e].br) != l) { printf("BAD C order\n"); ++bad; }
+        if (!f1) {
+          want(fc, IC2[e].fs, l, "C f", c);
+          if (IC2[e].sF != (to ? n.F[l] : -n.F[l])) { printf("BAD C sign\n"); ++bad; }
+        } else {
+          want(th, IC1[e].ts, n.bs[l], "C th_s", c);
+          want(th, IC1[e].tt, n.bt[l], "C th_t", c);
+          if (IC1[e].sb != (to ? n.b[l] : -n.b[l])) { printf("BAD C sign\n"); ++bad; }
+        }
       }
     }
     issue(c + P + 1);
