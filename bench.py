@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
     ap.add_argument("--form", default="F2", choices=["F2", "F1"])
-    ap.add_argument("--path", default="auto", choices=["auto", "batched", "simple", "single"])
+    ap.add_argument("--path", default="auto", choices=["auto", "batched", "single"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -221,8 +221,7 @@ def main():
     net, batch = make_inputs(args.workload, lo, hi)
     B = batch.B
     path = dual.PATH_BATCHED if B_total > 1 else dual.PATH_SINGLE
-    path = {"auto": path, "batched": dual.PATH_BATCHED, "simple": dual.PATH_BATCHED_SIMPLE,
-            "single": dual.PATH_SINGLE}[args.path]
+    path = {"auto": path, "batched": dual.PATH_BATCHED, "single": dual.PATH_SINGLE}[args.path]
 
     h = dual.DcopfDual(net, form=form, device=local, path=path)
     stream = torch.cuda.current_stream(dev)
@@ -238,11 +237,7 @@ def main():
             tdist.barrier()
 
     # ---- warm-up (untimed) --------------------------------------------------
-    if path == dual.PATH_BATCHED_SIMPLE:
-        for _ in range(W):
-            h.iterate(1, alpha, stream=stream)
-    else:
-        h.iterate(W, alpha, stream=stream)
+    h.iterate(W, alpha, stream=stream)
     torch.cuda.synchronize()
 
     # ---- timed region: device events on the launching stream ----------------
@@ -337,23 +332,23 @@ def main():
             "config": {"workload": args.workload, "form": args.form, "cost": "QP" if quad else "LP",
                        "n_bus": net.n_bus, "n_branch": net.n_branch, "n_gen": net.n_gen,
                        "B_total": B_total, "B_per_gpu": B,
-                       "path": {1: "batched-wavefront", 2: "single", 3: "batched-simple"}[path],
+                       "path": {1: "batched-sweep", 2: "single"}[path],
                        "kernel": {"grid": info.grid, "threads": info.threads_per_block, "smem": info.smem_bytes,
-                                  "chunk": info.chunk, "ring_bus": info.ring_bus, "ring_branch": info.ring_branch,
-                                  "rcm_bandwidth": info.bandwidth},
+                                  "chunk": info.chunk, "tile_width": info.tile_width,
+                                  "smem_slots_lambda": info.ring_bus, "smem_slots_branch": info.ring_branch,
+                                  "order_bandwidth": info.bandwidth},
                        "parallelism": f"instance-shard x{world}",
                        "l2": ("inputs larger than L2: state %.2f GB per GPU" %
                               ((info.B_padded * (2 * net.n_bus + 2 * net.n_branch * (1 if form == 0 else 2)
                                                  + net.n_bus) * 8) / 1e9))
                        if B_total > 1 else "state on chip (single instance)",
-                       "timed_launches": (f"{K} step launches + 1 final evaluation" if path == 3 else
-                                          f"1 persistent launch: {K} iterations + final evaluation")},
+                       "timed_launches": f"1 persistent launch: {K} iterations + final evaluation"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (K + 1) if path == 3 else 1,
+            "gpu_launches": 1,
             "clocks": clk,
             "gather_ms": gather_ms,
         }

@@ -74,11 +74,10 @@ enum { DCOPF_INST_OK = 0, DCOPF_INST_DIVERGED = 1 };
 /* kernel path selection */
 enum {
   DCOPF_PATH_AUTO = 0,    /* SINGLE when B <= single_max_batch, else BATCHED */
-  DCOPF_PATH_BATCHED = 1, /* 32 instances per CTA tile (lane = instance); one persistent launch
-                             runs all K iterations as wavefront sweeps in RCM bus order */
-  DCOPF_PATH_SINGLE = 2,  /* one persistent CTA per instance running all K iterations on chip */
-  DCOPF_PATH_BATCHED_SIMPLE = 3 /* batched, one 3-phase launch per iteration (first design; kept
-                                   for comparison) */
+  DCOPF_PATH_BATCHED = 1, /* tiles of W <= 64 instances (2 per lane), one CTA per tile, one
+                             persistent launch for all K iterations: a TMA-fed sweep over a
+                             host-compiled schedule of the network (DFS tree bus order) */
+  DCOPF_PATH_SINGLE = 2   /* one persistent CTA per instance running all K iterations on chip */
 };
 
 /* Network description.  Host pointers,
@@ -149,7 +148,10 @@ int dcopf_dual_get_multipliers(dcopf_dual_t h, double *lambda, double *branch, v
 /* Warm start / checkpoint restore: same layouts as get_multipliers.  Any
  * lambda (and nu) with mu >= 0 is dual feasible, so the anytime-bound property
  * is kept.  Does not reset best or status.
- * Errors: EINVAL (F1 and some mu < 0 or non-finite value), ESTATE. */
+ * Errors: EINVAL (a non-finite value; F1 and some mu < 0; F2 and
+ * a nonzero nu on one of the instance's outaged branches -- such a branch has
+ * b = F = 0, its nu does not enter the instance's dual, and the batched kernel
+ * relies on it staying 0, reading A-24), ESTATE. */
 int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const double *branch,
                                void *cuda_stream);
 
@@ -162,7 +164,7 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
 /* Static facts about the handle, for reporting. */
 typedef struct {
   int64_t B;                      /* instances loaded (0 before set_instance_batch) */
-  int64_t B_padded;               /* instances actually computed (batched path pads to 32) */
+  int64_t B_padded;               /* instances actually computed (batched path pads to a multiple of W) */
   int32_t path;                   /* DCOPF_PATH_BATCHED or DCOPF_PATH_SINGLE in use */
   int32_t form;
   int32_t n_bus, n_branch, n_gen, quadratic;
@@ -174,8 +176,9 @@ typedef struct {
   int32_t grid;                   /* CTAs per iteration launch */
   int32_t launches_per_iter;      /* kernel launches per ascent step (0: one launch per call) */
   int32_t state_on_chip;          /* single path: multipliers resident in shared memory */
-  int32_t chunk;                  /* batched path: buses per wavefront chunk */
-  int32_t ring_bus, ring_branch;  /* batched path: theta* / f* code ring sizes (entries) */
+  int32_t chunk;                  /* batched path: buses per schedule chunk */
+  int32_t ring_bus, ring_branch;  /* batched path: shared-memory slots for lambda / branch rows */
+  int32_t tile_width;             /* instances per CTA (batched W; 1 for the single path) */
 } dcopf_info;
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info);
 

@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libdcopf_dual.so")
 SOURCES = [os.path.join(CSRC, "dcopf_dual.cu"), os.path.join(CSRC, "schedule.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dual_kernels.cuh", "pipe_kernel.cuh", "schedule.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dual_kernels.cuh", "sweep_kernel.cuh", "schedule.h")] + [
     os.path.join(ROOT, "include", "dcopf_dual.h")]
 
 NVCC_FLAGS = [

@@ -219,16 +219,20 @@ int colour(std::vector<Interval> iv, std::vector<int> &slot) {
 
 size_t Schedule::smem_bytes(int) const { return (size_t)total; }
 
-std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedule *out) {
+std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out) {
   Schedule &S = *out;
   const int nb = net.nb, nl = net.nl;
   const bool f1 = net.form == 1;
+  if (W < 2 || W > 64 || (W & 1)) return "tile width must be even in [2, 64]";
   S.CH = CH;
   S.P = P;
   S.S = P + 1;
+  S.W = W;
   S.nch = (nb + CH - 1) / CH;
-  S.br_row_bytes = f1 ? 512 : 256;
-  const int nch = S.nch;
+  S.nsteps = S.nch + 2;
+  S.row_bytes = 8 * W;
+  S.br_row_bytes = f1 ? 16 * W : 8 * W;
+  const int nch = S.nch, nst = S.nsteps, RB = S.row_bytes, BR = S.br_row_bytes;
   auto chunk = [&](int bus) { return bus / CH; };
   std::vector<int> hi(nl), lo(nl);
   for (int l = 0; l < nl; ++l) {
@@ -236,12 +240,13 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
     lo[l] = std::min(net.bs[l], net.bt[l]);
     if (l > 0 && hi[l] < hi[l - 1]) return "internal branch order not sorted by larger endpoint";
   }
+  // B(c): branches whose larger endpoint lies in chunk c (contiguous)
   std::vector<int> bch(nch + 1, 0);
   for (int c = 0, l = 0; c <= nch; ++c) {
     while (l < nl && chunk(hi[l]) < c) ++l;
     bch[c] = (c == nch) ? nl : l;
   }
-  // ready position: a bus's C phase runs once all its neighbours passed phase A
+  // C(c): buses whose last neighbour lies in chunk c ("ready" position rp)
   std::vector<int> rp(nb);
   for (int i = 0; i < nb; ++i) rp[i] = i;
   for (int l = 0; l < nl; ++l) {
@@ -253,170 +258,179 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
   std::stable_sort(cord.begin(), cord.end(), [&](int x, int y) { return chunk(rp[x]) < chunk(rp[y]); });
   for (int i = 0; i < nb; ++i) cch[chunk(rp[i]) + 1]++;
   for (int c = 0; c < nch; ++c) cch[c + 1] += cch[c];
+  // step of each phase (skewed pipeline): A(c) at step c, B(c) at c+1, C(c) at c+2
+  auto stA = [&](int c) { return c; };
+  auto stB = [&](int c) { return c + 1; };
+  auto stC = [&](int c) { return c + 2; };
 
-  // ---- live ranges (in chunks) ----
-  // branch state rows (nu or mu pair): A at both endpoints, B at the larger
+  // ---- live ranges in steps ----
   std::vector<Interval> iv_br(nl), iv_lam(nb), iv_d(nb), iv_th(nb), iv_f;
   std::vector<int> br_first(nl), lam_first(nb), d_first(nb);
-  for (int l = 0; l < nl; ++l) {
-    br_first[l] = chunk(lo[l]);
-    iv_br[l] = {std::max(0, br_first[l] - P), chunk(hi[l]), l};
+  for (int l = 0; l < nl; ++l) {  // A at both endpoints, B at the larger one
+    br_first[l] = stA(chunk(lo[l]));
+    iv_br[l] = {std::max(0, br_first[l] - P), stB(chunk(hi[l])), l};
   }
   for (int i = 0; i < nb; ++i) {
-    int first = chunk(rp[i]), last = chunk(rp[i]);
+    const int last = stC(chunk(rp[i]));
+    int first = last;
     for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
-      int l = net.bus_inc[e] >> 1;
-      if (f1) {
-        // A phase of both endpoints reads lambda_s, lambda_t
-        first = std::min(first, chunk(lo[l]));
-      } else {
-        first = std::min(first, chunk(hi[l]));  // B phase of the branch
-      }
+      const int l = net.bus_inc[e] >> 1;
+      if (f1) first = std::min(first, stA(chunk(lo[l])));  // u_l in A of both endpoints
+      else first = std::min(first, stB(chunk(hi[l])));     // q_l in B
     }
     lam_first[i] = first;
     iv_lam[i] = {std::max(0, first - P), last, i};
-    d_first[i] = chunk(rp[i]);
-    iv_d[i] = {std::max(0, d_first[i] - P), chunk(rp[i]), i};
-    // theta code: written A(chunk i); read B(chunk hi_l) (+ F1: C of i and neighbours)
-    int tl = chunk(i);
+    d_first[i] = last;
+    iv_d[i] = {std::max(0, last - P), last, i};
+    // theta* code: written A(chunk i); read by B of incident branches and
+    // (F1) by C of i and of its neighbours
+    int tl = stA(chunk(i));
     for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
-      int l = net.bus_inc[e] >> 1;
-      tl = std::max(tl, chunk(hi[l]));
+      const int l = net.bus_inc[e] >> 1;
+      tl = std::max(tl, stB(chunk(hi[l])));
       if (f1) {
-        int j = (net.bs[l] == i) ? net.bt[l] : net.bs[l];
-        tl = std::max(tl, chunk(rp[j]));
+        const int j = (net.bs[l] == i) ? net.bt[l] : net.bs[l];
+        tl = std::max(tl, stC(chunk(rp[j])));
       }
     }
-    if (f1) tl = std::max(tl, chunk(rp[i]));
-    iv_th[i] = {chunk(i), tl, i};
+    if (f1) tl = std::max(tl, stC(chunk(rp[i])));
+    iv_th[i] = {stA(chunk(i)), tl, i};
   }
   std::vector<int> br_slot(nl), lam_slot(nb), d_slot(nb), th_slot(nb), f_slot(nl, 0);
   S.n_br_slots = colour(iv_br, br_slot);
   S.n_lam_slots = colour(iv_lam, lam_slot);
   S.n_d_slots = colour(iv_d, d_slot);
   S.n_th_slots = colour(iv_th, th_slot);
-  if (!f1) {
+  S.n_f_slots = 0;
+  if (!f1) {  // f* code: written B(chunk hi), read C of both endpoints
     iv_f.resize(nl);
     for (int l = 0; l < nl; ++l)
-      iv_f[l] = {chunk(hi[l]), std::max(chunk(rp[net.bs[l]]), chunk(rp[net.bt[l]])), l};
+      iv_f[l] = {stB(chunk(hi[l])), std::max(stC(chunk(rp[net.bs[l]])), stC(chunk(rp[net.bt[l]]))), l};
     S.n_f_slots = colour(iv_f, f_slot);
   }
 
-  // ---- load lists: rows whose first use is chunk c ----
-  std::vector<std::vector<int>> lds(nch);
+  // ---- load lists: rows grouped by the step of their first use ----
+  std::vector<std::vector<int>> lds(nst);
   for (int i = 0; i < nb; ++i) lds[lam_first[i]].push_back((LD_LAM << 30) | i);
   for (int i = 0; i < nb; ++i) lds[d_first[i]].push_back((LD_D << 30) | i);
   for (int l = 0; l < nl; ++l) lds[br_first[l]].push_back((LD_BR << 30) | l);
-  S.ld_ptr.assign(nch + 1, 0);
+  S.ld_ptr.assign(nst + 1, 0);
   S.ld_ent.clear();
   S.ld_slot.clear();
-  std::vector<int> row_bytes(nch, 0);
-  for (int c = 0; c < nch; ++c) {
-    for (int x : lds[c]) {
-      int kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff;
+  std::vector<int> row_bytes(nst, 0);
+  for (int st = 0; st < nst; ++st) {
+    for (int x : lds[st]) {
+      const int kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff;
       S.ld_ent.push_back(x);
-      int slot = kind == LD_LAM ? lam_slot[ent] : (kind == LD_D ? d_slot[ent] : br_slot[ent]);
-      S.ld_slot.push_back(slot);
-      row_bytes[c] += (kind == LD_BR) ? S.br_row_bytes : 256;
+      S.ld_slot.push_back(kind == LD_LAM ? lam_slot[ent] : (kind == LD_D ? d_slot[ent] : br_slot[ent]));
+      row_bytes[st] += (kind == LD_BR) ? BR : RB;
     }
-    S.ld_ptr[c + 1] = (int)S.ld_ent.size();
+    S.ld_ptr[st + 1] = (int)S.ld_ent.size();
   }
 
-  // ---- program blocks ----
+  // ---- program blocks, one per step ----
   S.prog.clear();
-  S.prog_off.assign(nch, 0);
-  S.prog_bytes.assign(nch, 0);
-  S.tx_bytes.assign(nch, 0);
+  S.prog_off.assign(nst, 0);
+  S.prog_bytes.assign(nst, 0);
+  S.tx_bytes.assign(nst, 0);
   S.max_prog_bytes = 0;
-  const int BR = S.br_row_bytes;
-  for (int c = 0; c < nch; ++c) {
-    const int a0 = c * CH, a1 = std::min(nb, a0 + CH);
-    const int nA = a1 - a0;
-    std::vector<RecA> A(nA);
+  for (int st = 0; st < nst; ++st) {
+    std::vector<RecA> A;
     std::vector<RecIA2> IA2;
     std::vector<RecIA1> IA1;
-    for (int j = 0; j < nA; ++j) {
-      const int i = a0 + j;
-      RecA r{};
-      r.th = th_slot[i];
-      r.theta = net.theta[i];
-      r.e0 = f1 ? (int)IA1.size() : (int)IA2.size();
-      for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
-        const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
-        if (!f1) {
-          RecIA2 x{};
-          x.row = br_slot[l] * BR;
-          x.br = l;
-          x.sb = to ? net.b[l] : -net.b[l];   // w_s += -b nu ; w_t += b nu
-          IA2.push_back(x);
-        } else {
-          RecIA1 x{};
-          x.row = br_slot[l] * BR;
-          x.br = l;
-          x.ls = lam_slot[net.bs[l]] * 256;
-          x.lt = lam_slot[net.bt[l]] * 256;
-          x.sb = to ? -net.b[l] : net.b[l];   // w_s += u ; w_t -= u
-          IA1.push_back(x);
+    int a0 = 0, b0 = 0;
+    const int ca = st;  // A(ca)
+    if (ca < nch) {
+      a0 = ca * CH;
+      const int a1 = std::min(nb, a0 + CH);
+      for (int i = a0; i < a1; ++i) {
+        RecA r{};
+        r.th = th_slot[i];
+        r.theta = net.theta[i];
+        r.e0 = f1 ? (int)IA1.size() : (int)IA2.size();
+        for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
+          const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
+          if (!f1) {
+            RecIA2 x{};
+            x.row = br_slot[l] * BR;
+            x.br = l;
+            x.sb = to ? net.b[l] : -net.b[l];  // w_s += -(b nu) ; w_t += b nu
+            IA2.push_back(x);
+          } else {
+            RecIA1 x{};
+            x.row = br_slot[l] * BR;
+            x.br = l;
+            x.ls = lam_slot[net.bs[l]] * RB;
+            x.lt = lam_slot[net.bt[l]] * RB;
+            x.sb = to ? -net.b[l] : net.b[l];  // w_s += u ; w_t -= u
+            IA1.push_back(x);
+          }
         }
+        r.e1 = f1 ? (int)IA1.size() : (int)IA2.size();
+        A.push_back(r);
       }
-      r.e1 = f1 ? (int)IA1.size() : (int)IA2.size();
-      A[j] = r;
     }
-    const int b0 = bch[c], nB = bch[c + 1] - bch[c];
-    std::vector<RecB> Bv(nB);
-    for (int j = 0; j < nB; ++j) {
-      const int l = b0 + j, s = net.bs[l], t = net.bt[l];
-      RecB r{};
-      r.row = br_slot[l] * BR;
-      r.ts = th_slot[s];
-      r.tt = th_slot[t];
-      r.b = net.b[l];
-      r.F = net.F[l];
-      r.Ts = net.theta[s];
-      r.Tt = net.theta[t];
-      if (!f1) {
-        r.ls = lam_slot[s] * 256;
-        r.lt = lam_slot[t] * 256;
-        r.fs = f_slot[l];
+    std::vector<RecB> Bv;
+    const int cb = st - 1;  // B(cb)
+    if (cb >= 0 && cb < nch) {
+      b0 = bch[cb];
+      for (int l = bch[cb]; l < bch[cb + 1]; ++l) {
+        const int s = net.bs[l], t = net.bt[l];
+        RecB r{};
+        r.row = br_slot[l] * BR;
+        r.ts = th_slot[s];
+        r.tt = th_slot[t];
+        r.b = net.b[l];
+        r.F = net.F[l];
+        r.Ts = net.theta[s];
+        r.Tt = net.theta[t];
+        if (!f1) {
+          r.ls = lam_slot[s] * RB;
+          r.lt = lam_slot[t] * RB;
+          r.fs = f_slot[l];
+        }
+        Bv.push_back(r);
       }
-      Bv[j] = r;
     }
-    const int nC = cch[c + 1] - cch[c];
-    std::vector<RecC> Cv(nC);
+    std::vector<RecC> Cv;
     std::vector<RecG> G;
     std::vector<RecIC2> IC2;
     std::vector<RecIC1> IC1;
-    for (int j = 0; j < nC; ++j) {
-      const int i = cord[cch[c] + j];
-      RecC r{};
-      r.bus = i;
-      r.ls = lam_slot[i] * 256;
-      r.ds = d_slot[i] * 256;
-      r.g0 = (int)G.size();
-      for (int g = net.gen_ptr[i]; g < net.gen_ptr[i + 1]; ++g) G.push_back(RecG{net.gc[g], net.glo[g], net.ghi[g], net.ga[g]});
-      r.g1 = (int)G.size();
-      r.e0 = f1 ? (int)IC1.size() : (int)IC2.size();
-      for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
-        const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
-        if (!f1) {
-          RecIC2 x{};
-          x.fs = f_slot[l];
-          x.br = l;
-          x.sF = to ? net.F[l] : -net.F[l];  // lambda grad: +f* at to, -f* at from
-          IC2.push_back(x);
-        } else {
-          RecIC1 x{};
-          x.ts = th_slot[net.bs[l]];
-          x.tt = th_slot[net.bt[l]];
-          x.br = l;
-          x.sb = to ? net.b[l] : -net.b[l];  // +phi at to, -phi at from
-          x.Ts = net.theta[net.bs[l]];
-          x.Tt = net.theta[net.bt[l]];
-          IC1.push_back(x);
+    const int cc = st - 2;  // C(cc)
+    if (cc >= 0 && cc < nch) {
+      for (int j = cch[cc]; j < cch[cc + 1]; ++j) {
+        const int i = cord[j];
+        RecC r{};
+        r.bus = i;
+        r.ls = lam_slot[i] * RB;
+        r.ds = d_slot[i] * RB;
+        r.g0 = (int)G.size();
+        for (int g = net.gen_ptr[i]; g < net.gen_ptr[i + 1]; ++g)
+          G.push_back(RecG{net.gc[g], net.glo[g], net.ghi[g], net.ga[g]});
+        r.g1 = (int)G.size();
+        r.e0 = f1 ? (int)IC1.size() : (int)IC2.size();
+        for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
+          const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
+          if (!f1) {
+            RecIC2 x{};
+            x.fs = f_slot[l];
+            x.br = l;
+            x.sF = to ? net.F[l] : -net.F[l];  // d/dlambda: +f* at the to bus, -f* at the from bus
+            IC2.push_back(x);
+          } else {
+            RecIC1 x{};
+            x.ts = th_slot[net.bs[l]];
+            x.tt = th_slot[net.bt[l]];
+            x.br = l;
+            x.sb = to ? net.b[l] : -net.b[l];  // +phi at the to bus, -phi at the from bus
+            x.Ts = net.theta[net.bs[l]];
+            x.Tt = net.theta[net.bt[l]];
+            IC1.push_back(x);
+          }
         }
+        r.e1 = f1 ? (int)IC1.size() : (int)IC2.size();
+        Cv.push_back(r);
       }
-      r.e1 = f1 ? (int)IC1.size() : (int)IC2.size();
-      Cv[j] = r;
     }
     std::vector<uint8_t> blk(kProgHeaderBytes, 0);
     int32_t hd[16] = {0};
@@ -426,10 +440,10 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
       if (n) memcpy(blk.data() + off, p, n);
       return (int32_t)off;
     };
-    hd[PH_NA] = nA;
+    hd[PH_NA] = (int)A.size();
     hd[PH_NIA] = f1 ? (int)IA1.size() : (int)IA2.size();
-    hd[PH_NB] = nB;
-    hd[PH_NC] = nC;
+    hd[PH_NB] = (int)Bv.size();
+    hd[PH_NC] = (int)Cv.size();
     hd[PH_NIC] = f1 ? (int)IC1.size() : (int)IC2.size();
     hd[PH_NG] = (int)G.size();
     hd[PH_A0] = a0;
@@ -443,11 +457,11 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
     blk.resize((blk.size() + 15) & ~size_t(15), 0);
     hd[PH_BYTES] = (int32_t)blk.size();
     memcpy(blk.data(), hd, sizeof hd);
-    S.prog_off[c] = (long long)S.prog.size();
-    S.prog_bytes[c] = (int)blk.size();
+    S.prog_off[st] = (long long)S.prog.size();
+    S.prog_bytes[st] = (int)blk.size();
     S.prog.insert(S.prog.end(), blk.begin(), blk.end());
     S.max_prog_bytes = std::max(S.max_prog_bytes, (int)blk.size());
-    S.tx_bytes[c] = S.prog_bytes[c] + row_bytes[c];
+    S.tx_bytes[st] = S.prog_bytes[st] + row_bytes[st];
   }
 
   // ---- shared-memory layout ----
@@ -456,23 +470,25 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedu
   S.off_bar = off;
   off = al(off + 16 * S.S);
   S.off_red = off;
-  off = al(off + 8 * 32 * nw);
+  off = al(off + 8 * 64 * nw);
   S.off_frz = off;
-  off = al(off + 4 * 32);
-  S.off_obm = off;                       // per-tile outage bitmap over branches
+  off = al(off + 4 * 64);
+  S.off_obm = off;  // per-tile outage bitmap over branches
   off = al(off + 4 * ((nl + 31) / 32 + 1));
+  S.off_outs = off;  // per-instance outage lists of the tile
+  off = al(off + 4 * 64 * 8);
   S.off_prog = off;
   off = al(off + S.S * al(S.max_prog_bytes));
   S.off_brp = off;
-  off = al(off + S.n_br_slots * S.br_row_bytes);
+  off = al(off + S.n_br_slots * BR + 512);  // +512: lanes past the tile width read padding
   S.off_lamp = off;
-  off = al(off + S.n_lam_slots * 256);
+  off = al(off + S.n_lam_slots * RB + 512);
   S.off_dp = off;
-  off = al(off + S.n_d_slots * 256);
+  off = al(off + S.n_d_slots * RB + 512);
   S.off_th = off;
-  off = al(off + S.n_th_slots * 8);
+  off = al(off + S.n_th_slots * 16);
   S.off_fc = off;
-  off = al(off + S.n_f_slots * 8);
+  off = al(off + S.n_f_slots * 16);
   S.total = off;
   return "";
 }

@@ -43,6 +43,8 @@ struct alignas(16) RecG { double c, lo, hi, a; };                               
 struct alignas(16) RecIC2 { int fs, br; double sF; };                                       // F2: sF = to ? F : -F
 struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, Ts, Tt, pad2; };               // F1: sb = to ? b : -b
 
+// code words: 16 B per entity = ballots {pos0, neg0, pos1, neg1} of the
+// first / second instance of every lane
 // load-list entry kinds (top 2 bits of the packed entity word)
 enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
 
@@ -56,18 +58,19 @@ struct NetInternal {
 };
 
 struct Schedule {
-  int CH = 0, P = 0, S = 0, nch = 0;
+  int CH = 0, P = 0, S = 0, W = 0, nch = 0, nsteps = 0;
+  int row_bytes = 0;                        // lambda / d / nu row: 8 W
   int n_br_slots = 0, n_lam_slots = 0, n_d_slots = 0, n_th_slots = 0, n_f_slots = 0;
-  int br_row_bytes = 0;                     // 256 (nu) or 512 (mu+, mu-)
+  int br_row_bytes = 0;                     // 8 W (nu) or 16 W (mu+, mu-)
   int max_prog_bytes = 0;
   std::vector<uint8_t> prog;                // all program blocks
-  std::vector<long long> prog_off;          // [nch] byte offset of each block
-  std::vector<int> prog_bytes;              // [nch]
-  std::vector<int> tx_bytes;                // [nch] program + rows (expect_tx)
+  std::vector<long long> prog_off;          // [nsteps] byte offset of each block
+  std::vector<int> prog_bytes;              // [nsteps]
+  std::vector<int> tx_bytes;                // [nsteps] program + rows (expect_tx)
   std::vector<int> ld_ptr, ld_ent, ld_slot; // load lists
   size_t smem_bytes(int nw) const;
   // smem layout offsets (bytes)
-  int off_bar, off_red, off_frz, off_obm, off_prog, off_brp, off_lamp, off_dp, off_th, off_fc, total;
+  int off_bar, off_red, off_frz, off_obm, off_outs, off_prog, off_brp, off_lamp, off_dp, off_th, off_fc, total;
 };
 
 struct Internalized {
@@ -92,7 +95,9 @@ std::string internalize(int nb, int nl, int ng, int ref, const int *fr, const in
 // visited smallest subtree first (keeps the live re-read window small).
 std::vector<int> dfs_tree_order(int n, const std::vector<std::vector<int>> &adj, int root);
 
-// Build the schedule; returns an empty string or an error message.
-std::string build_schedule(const NetInternal &net, int CH, int P, int nw, Schedule *out);
+// Build the schedule for tiles of W instances (2 per lane); the sweep runs in
+// nch + 2 skewed steps: step s executes A(s), B(s-1) and C(s-2) between two
+// barriers.  Returns an empty string or an error message.
+std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out);
 
 }  // namespace dcopf

@@ -1,0 +1,454 @@
+// sweep_kernel.cuh -- the batched path: one persistent, warp-specialised,
+// TMA-fed sweep kernel per dcopf_dual_iterate() call (sm_100a).
+//
+// Layout: instances are grouped in tiles of W (even, <= 64) -- the tile width
+// is chosen per batch so the number of tiles is about the SM count -- and
+// every per-instance array is tile-major [tile][entity][W] (F1 mu:
+// [tile][branch][2][W]).  A row (one entity of one tile) is 8 W contiguous
+// bytes.  Lane l of a warp owns instances 2l and 2l+1 of its tile, so every
+// shared-memory / global access of a row is one 16-byte vector per lane and
+// every topology record is a warp-uniform broadcast shared by 2*32 instances.
+//
+// One CTA = one tile, for all K iterations (instances never interact: no grid
+// synchronisation, one launch per call).  Each iteration is a sweep over a
+// host-compiled schedule (schedule.h) of nch chunks in nch+2 skewed steps;
+// step s runs, between two barriers,
+//     A(s)    buses of chunk s: w_i over the incidence -> theta* codes
+//     B(s-1)  branches whose larger endpoint is in chunk s-1: q_l, f* codes,
+//             phi_l, Kirchhoff (F2) / limit (F1) residual, nu' / mu' -> HBM
+//     C(s-2)  buses whose last neighbour is in chunk s-2: generators,
+//             d/dlambda, lambda' -> HBM
+// (the three read only codes produced in earlier steps, so they need no
+// barrier between them).  A producer warp streams each step's program block
+// and state rows into interval-coloured shared-memory slots with
+// cp.async.bulk (TMA 1-D bulk copies) P steps ahead, synchronised by
+// full/empty mbarriers.  Every HBM byte of the iteration is read once and
+// written once: the traffic is the algorithmic 8 (3 n_b + 2 n_l) B per
+// instance-iteration (F2).  Between sweeps the pipeline drains (y_{k+1} rows
+// are read by TMA in sweep k+1, so writers fence generic -> async proxy).
+//
+// Outages (F2): an outaged branch's nu is held at exactly zero (it starts at
+// 0 and its gradient f* - phi is +-0), so b nu vanishes in phase A without a
+// check; phase B applies b = F = 0 per lane (a per-tile bitmap makes the
+// check one broadcast load for unflagged branches) and forces the f* code to
+// the tie, so phase C decodes +-0 without a check.  F1 checks in all phases.
+//
+// Per-entity arithmetic and operation order match dual_kernels.cuh and the
+// oracle (reading A-19); only the dual value is summed in another fixed order.
+#pragma once
+#include "dual_kernels.cuh"
+#include "schedule.h"
+
+namespace dcopf {
+
+struct SweepArgs {
+  double *lam0, *lam1, *br0, *br1;  // ping-pong state (tile-major)
+  const double *d;
+  const int *outs;                  // [B_pad][max_out] internal ids, -1 padded
+  int max_out;
+  int cur;
+  const double *alpha;              // [K] device
+  long K;
+  double *bound, *best;             // [B_pad]
+  int *status;
+  double *hist;                     // [K][B] or null
+  long B;
+  double *out_val;                  // EVAL: value [B_pad]
+  double *g_lam, *g_br;             // EVAL: gradients (tile-major)
+  int n_bus, n_br, ref, W;
+  const uint8_t *prog;
+  const long long *prog_off;
+  const int *prog_bytes, *tx_bytes;
+  const int *ld_ptr, *ld_ent, *ld_slot;
+  int nsteps, S, row_bytes, br_row_bytes;
+  int off_bar, off_red, off_frz, off_obm, off_outs, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th,
+      off_fc;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// the two instances of a lane
+struct D2 {
+  double x, y;
+};
+__device__ __forceinline__ D2 ld2(const uint8_t *base, int off) {
+  const double2 v = *reinterpret_cast<const double2 *>(base + off);
+  return D2{v.x, v.y};
+}
+__device__ __forceinline__ void st2(double *p, double x, double y) {
+  *reinterpret_cast<double2 *>(p) = make_double2(x, y);
+}
+// code word {pos0, neg0, pos1, neg1}: +x, -x or z for instance t of this lane
+__device__ __forceinline__ double dec(unsigned pos, unsigned neg, int lane, double x, double z) {
+  return ((pos >> lane) & 1u) ? x : (((neg >> lane) & 1u) ? -x : z);
+}
+
+template <int FORM, bool EVAL, int NW>
+__global__ void __maxnreg__(120) k_sweep(const SweepArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + a.off_bar);
+  uint64_t *empty = full + a.S;
+  double *red = reinterpret_cast<double *>(smem + a.off_red);   // [NW][64]
+  int *frz = reinterpret_cast<int *>(smem + a.off_frz);         // [64]
+  unsigned *obm = reinterpret_cast<unsigned *>(smem + a.off_obm);
+  int *outs_s = reinterpret_cast<int *>(smem + a.off_outs);     // [64][kMaxOut]
+  constexpr int BRW = (FORM == kFormF2) ? 1 : 2;
+  constexpr int CT = NW * 32;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int W = a.W, L = W >> 1;
+  const bool act = lane < L;
+  const size_t tile = blockIdx.x;
+  const long ib = (long)tile * W;          // first instance of the tile
+  const int S = a.S, nst = a.nsteps;
+  const long K = EVAL ? 0 : a.K;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int x = threadIdx.x; x < (a.n_br + 31) / 32; x += blockDim.x) obm[x] = 0u;
+  for (int t = threadIdx.x; t < 64; t += blockDim.x) frz[t] = (!EVAL && t < W) ? a.status[ib + t] : 0;
+  for (int x = threadIdx.x; x < 64 * kMaxOut; x += blockDim.x) {
+    const int t = x / kMaxOut, j = x % kMaxOut;
+    outs_s[x] = (t < W && j < a.max_out) ? a.outs[(ib + t) * a.max_out + j] : -1;
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < 64 * kMaxOut; x += blockDim.x)
+    if (outs_s[x] >= 0) atomicOr(&obm[outs_s[x] >> 5], 1u << (outs_s[x] & 31));
+  __syncthreads();
+
+  if (warp == NW) {
+    // =========================== producer ===========================
+    const int RB = a.row_bytes, BR = a.br_row_bytes;
+    for (long k = 0; k <= K; ++k) {
+      if (k > 0) named_bar(2, (NW + 1) * 32);  // sweep k-1 written and fenced
+      const int par = (a.cur + (int)(k & 1)) & 1;
+      const uint8_t *lam_src = reinterpret_cast<const uint8_t *>(par ? a.lam1 : a.lam0) + tile * (size_t)a.n_bus * RB;
+      const uint8_t *br_src = reinterpret_cast<const uint8_t *>(par ? a.br1 : a.br0) + tile * (size_t)a.n_br * BR;
+      const uint8_t *d_src = reinterpret_cast<const uint8_t *>(a.d) + tile * (size_t)a.n_bus * RB;
+      for (int c = 0; c < nst; ++c) {
+        const long g = k * nst + c;
+        const int st = (int)(g % S);
+        const long u = g / S;
+        if (u > 0) mbar_wait(&empty[st], (unsigned)((u - 1) & 1));
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[st], (unsigned)a.tx_bytes[c]);
+          tma_load_1d(smem + a.off_prog + st * a.prog_stride, a.prog + a.prog_off[c], (unsigned)a.prog_bytes[c],
+                      &full[st]);
+        }
+        __syncwarp();
+        const int e1 = a.ld_ptr[c + 1];
+        for (int e = a.ld_ptr[c] + lane; e < e1; e += 32) {
+          const int x = a.ld_ent[e], slot = a.ld_slot[e];
+          const int kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff;
+          if (kind == LD_LAM)
+            tma_load_1d(smem + a.off_lamp + slot * RB, lam_src + (size_t)ent * RB, RB, &full[st]);
+          else if (kind == LD_D)
+            tma_load_1d(smem + a.off_dp + slot * RB, d_src + (size_t)ent * RB, RB, &full[st]);
+          else
+            tma_load_1d(smem + a.off_brp + slot * BR, br_src + (size_t)ent * BR, BR, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+
+  // =========================== consumers ===========================
+  const int RB = a.row_bytes, BR = a.br_row_bytes;
+  const uint8_t *brp = smem + a.off_brp + lane * 16;
+  const uint8_t *lamp = smem + a.off_lamp + lane * 16;
+  const uint8_t *dp = smem + a.off_dp + lane * 16;
+  uint4 *th = reinterpret_cast<uint4 *>(smem + a.off_th);
+  uint4 *fc = reinterpret_cast<uint4 *>(smem + a.off_fc);
+  const int nout = a.max_out;
+  const int *my_outs0 = outs_s + (2 * lane) * kMaxOut, *my_outs1 = my_outs0 + kMaxOut;
+  auto flagged = [&](int l) { return (obm[l >> 5] >> (l & 31)) & 1u; };
+  auto out_t = [&](const int *lst, int l) {
+    bool r = false;
+    for (int j = 0; j < nout; ++j) r |= (lst[j] == l);
+    return r;
+  };
+  double best0 = 0.0, best1 = 0.0;
+  if (!EVAL && warp == 0 && act) {
+    best0 = a.best[ib + 2 * lane];
+    best1 = a.best[ib + 2 * lane + 1];
+  }
+
+  for (long k = 0; k <= K; ++k) {
+    const bool last = (k == K);
+    const bool write = EVAL || !last;
+    const int par = (a.cur + (int)(k & 1)) & 1;
+    uint8_t *lam_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_lam : (par ? a.lam0 : a.lam1)) + tile * (size_t)a.n_bus * RB +
+                     lane * 16;
+    uint8_t *br_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_br : (par ? a.br0 : a.br1)) + tile * (size_t)a.n_br * BR +
+                    lane * 16;
+    const bool step0 = !EVAL && !last && !frz[2 * lane], step1 = !EVAL && !last && !frz[2 * lane + 1];
+    const double alpha = (EVAL || last) ? 0.0 : a.alpha[k];
+    double v0 = 0.0, v1 = 0.0;
+
+    for (int c = 0; c < nst; ++c) {
+      const long g = k * nst + c;
+      const int st = (int)(g % S);
+      mbar_wait(&full[st], (unsigned)((g / S) & 1));
+      const uint8_t *prog = smem + a.off_prog + st * a.prog_stride;
+      const int4 h0 = *reinterpret_cast<const int4 *>(prog);       // nA nIA nB nC
+      const int4 h1 = *reinterpret_cast<const int4 *>(prog + 16);  // nIC nG a0 b0
+      const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);  // offA offIA offB offC
+      const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC
+      const int nA = h0.x, nB = h0.z, nC = h0.w;
+
+      // ---------------- A(s): w_i, theta* codes ----------------
+      {
+        const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
+        for (int j = warp; j < nA; j += NW) {
+          const RecA ra = A[j];
+          const int bus = h1.z + j;
+          double w0 = 0.0, w1 = 0.0;
+          if (FORM == kFormF2) {
+            const RecIA2 *IA = reinterpret_cast<const RecIA2 *>(prog + h2.y);
+            for (int e = ra.e0; e < ra.e1; ++e) {
+              const RecIA2 r = IA[e];
+              const D2 nu = ld2(brp, r.row);
+              w0 = w0 + r.sb * nu.x;  // w_s += -(b nu), w_t += b nu (outaged: nu == 0)
+              w1 = w1 + r.sb * nu.y;
+            }
+          } else {
+            const RecIA1 *IA = reinterpret_cast<const RecIA1 *>(prog + h2.y);
+            for (int e = ra.e0; e < ra.e1; ++e) {
+              const RecIA1 r = IA[e];
+              double sb0 = r.sb, sb1 = r.sb;
+              if (flagged(r.br)) {
+                if (out_t(my_outs0, r.br)) sb0 = copysign(0.0, sb0);
+                if (out_t(my_outs1, r.br)) sb1 = copysign(0.0, sb1);
+              }
+              const D2 mp = ld2(brp, r.row), mm = ld2(brp, r.row + RB);
+              const D2 ls = ld2(lamp, r.ls), lt = ld2(lamp, r.lt);
+              w0 = w0 + sb0 * ((mp.x - mm.x) - (ls.x - lt.x));  // w_s += u, w_t -= u
+              w1 = w1 + sb1 * ((mp.y - mm.y) - (ls.y - lt.y));
+            }
+          }
+          const bool nr = (bus != a.ref) && act;
+          const bool p0 = nr && (w0 < 0.0), n0 = nr && (w0 > 0.0);
+          const bool p1 = nr && (w1 < 0.0), n1 = nr && (w1 > 0.0);
+          const uint4 cw = make_uint4(__ballot_sync(0xffffffffu, p0), __ballot_sync(0xffffffffu, n0),
+                                      __ballot_sync(0xffffffffu, p1), __ballot_sync(0xffffffffu, n1));
+          if (lane == 0) th[ra.th] = cw;
+          if (nr) {
+            v0 += w0 * (p0 ? ra.theta : (n0 ? -ra.theta : 0.0));
+            v1 += w1 * (p1 ? ra.theta : (n1 ? -ra.theta : 0.0));
+          }
+        }
+      }
+      // ---------------- B(s-1): branches ----------------
+      {
+        const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
+        for (int j = (warp + NW - nA % NW) % NW; j < nB; j += NW) {
+          const RecB r = Bv[j];
+          const int l = h1.w + j;
+          double b0 = r.b, b1 = r.b, F0 = r.F, F1v = r.F;
+          bool o0 = false, o1 = false;
+          if (flagged(l)) {
+            o0 = out_t(my_outs0, l);
+            o1 = out_t(my_outs1, l);
+            if (o0) b0 = F0 = 0.0;
+            if (o1) b1 = F1v = 0.0;
+          }
+          const uint4 cs = th[r.ts], ct = th[r.tt];
+          const double phi0 = b0 * (dec(cs.x, cs.y, lane, r.Ts, 0.0) - dec(ct.x, ct.y, lane, r.Tt, 0.0));
+          const double phi1 = b1 * (dec(cs.z, cs.w, lane, r.Ts, 0.0) - dec(ct.z, ct.w, lane, r.Tt, 0.0));
+          double* dst = reinterpret_cast<double *>(br_o + (size_t)l * BR);
+          if (FORM == kFormF2) {
+            const D2 nu = ld2(brp, r.row), ls = ld2(lamp, r.ls), lt = ld2(lamp, r.lt);
+            const double q0 = nu.x - (ls.x - lt.x), q1 = nu.y - (ls.y - lt.y);
+            // f* = -F if q > 0, +F if q < 0, 0 on a tie; an outaged lane's code is the tie
+            const bool fn0 = act && !o0 && q0 > 0.0, fp0 = act && !o0 && q0 < 0.0;
+            const bool fn1 = act && !o1 && q1 > 0.0, fp1 = act && !o1 && q1 < 0.0;
+            const uint4 cw = make_uint4(__ballot_sync(0xffffffffu, fp0), __ballot_sync(0xffffffffu, fn0),
+                                        __ballot_sync(0xffffffffu, fp1), __ballot_sync(0xffffffffu, fn1));
+            if (lane == 0) fc[r.fs] = cw;
+            const double f0 = (q0 > 0.0) ? -F0 : ((q0 < 0.0) ? F0 : 0.0);
+            const double f1 = (q1 > 0.0) ? -F1v : ((q1 < 0.0) ? F1v : 0.0);
+            const double g0 = f0 - phi0, g1 = f1 - phi1;  // Kirchhoff residual
+            v0 += q0 * f0;
+            v1 += q1 * f1;
+            if (write && act) {
+              if (EVAL) st2(dst, g0, g1);
+              else st2(dst, step0 ? nu.x + alpha * g0 : nu.x, step1 ? nu.y + alpha * g1 : nu.y);
+            }
+          } else {
+            const D2 mp = ld2(brp, r.row), mm = ld2(brp, r.row + RB);
+            const double gp0 = phi0 - F0, gm0 = -phi0 - F0, gp1 = phi1 - F1v, gm1 = -phi1 - F1v;
+            v0 += -(F0 * (mp.x + mm.x));
+            v1 += -(F1v * (mp.y + mm.y));
+            if (write && act) {
+              double* dst2 = reinterpret_cast<double *>(br_o + (size_t)l * BR + RB);
+              if (EVAL) {
+                st2(dst, gp0, gp1);
+                st2(dst2, gm0, gm1);
+              } else {
+                double p0 = mp.x, m0 = mm.x, p1 = mp.y, m1 = mm.y;
+                if (step0) {
+                  p0 = mp.x + alpha * gp0;
+                  m0 = mm.x + alpha * gm0;
+                  p0 = (p0 > 0.0) ? p0 : 0.0;  // mu <- max(mu, 0)
+                  m0 = (m0 > 0.0) ? m0 : 0.0;
+                }
+                if (step1) {
+                  p1 = mp.y + alpha * gp1;
+                  m1 = mm.y + alpha * gm1;
+                  p1 = (p1 > 0.0) ? p1 : 0.0;
+                  m1 = (m1 > 0.0) ? m1 : 0.0;
+                }
+                st2(dst, p0, p1);
+                st2(dst2, m0, m1);
+              }
+            }
+          }
+        }
+      }
+      // ---------------- C(s-2): ready buses ----------------
+      {
+        const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
+        const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
+        for (int j = (warp + 2 * NW - (nA + nB) % NW) % NW; j < nC; j += NW) {
+          const RecC r = Cv[j];
+          const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
+          double gl0 = -di.x, gl1 = -di.y;
+          for (int gg = r.g0; gg < r.g1; ++gg) {
+            const RecG gr = G[gg];
+            const double r0 = gr.c + li.x, r1 = gr.c + li.y;
+            const double p0 = gen_minimiser(r0, gr.lo, gr.hi, gr.a), p1 = gen_minimiser(r1, gr.lo, gr.hi, gr.a);
+            gl0 = gl0 + p0;
+            gl1 = gl1 + p1;
+            if (gr.a > 0.0) {
+              v0 += gr.a * p0 * p0 + r0 * p0;
+              v1 += gr.a * p1 * p1 + r1 * p1;
+            } else {
+              v0 += r0 * p0;
+              v1 += r1 * p1;
+            }
+          }
+          if (FORM == kFormF2) {
+            const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y);
+            for (int e = r.e0; e < r.e1; ++e) {
+              const RecIC2 x = IC[e];
+              const uint4 cw = fc[x.fs];
+              const double z = x.sF * 0.0;  // signed zero of the tie: +0 at the to bus, -0 at the from bus
+              gl0 = gl0 + dec(cw.x, cw.y, lane, x.sF, z);  // +f* at to, -f* at from (sign folded)
+              gl1 = gl1 + dec(cw.z, cw.w, lane, x.sF, z);
+            }
+          } else {
+            const RecIC1 *IC = reinterpret_cast<const RecIC1 *>(prog + h3.y);
+            for (int e = r.e0; e < r.e1; ++e) {
+              const RecIC1 x = IC[e];
+              double sb0 = x.sb, sb1 = x.sb;
+              if (flagged(x.br)) {
+                if (out_t(my_outs0, x.br)) sb0 = copysign(0.0, sb0);
+                if (out_t(my_outs1, x.br)) sb1 = copysign(0.0, sb1);
+              }
+              const uint4 cs = th[x.ts], ct = th[x.tt];
+              gl0 = gl0 + sb0 * (dec(cs.x, cs.y, lane, x.Ts, 0.0) - dec(ct.x, ct.y, lane, x.Tt, 0.0));
+              gl1 = gl1 + sb1 * (dec(cs.z, cs.w, lane, x.Ts, 0.0) - dec(ct.z, ct.w, lane, x.Tt, 0.0));
+            }
+          }
+          v0 += -(li.x * di.x);
+          v1 += -(li.y * di.y);
+          if (write && act) {
+            double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.bus * RB);
+            if (EVAL) st2(dst, gl0, gl1);
+            else st2(dst, step0 ? li.x + alpha * gl0 : li.x, step1 ? li.y + alpha * gl1 : li.y);
+          }
+        }
+      }
+      named_bar(1, CT);
+      if (threadIdx.x == 0) mbar_arrive(&empty[st]);
+    }
+    // ---------------- dual value, best, status ----------------
+    red[warp * 64 + 2 * lane] = v0;
+    red[warp * 64 + 2 * lane + 1] = v1;
+    named_bar(1, CT);
+    if (warp == 0 && act) {
+      double g0 = 0.0, g1 = 0.0;
+      for (int w = 0; w < NW; ++w) {
+        g0 += red[w * 64 + 2 * lane];
+        g1 += red[w * 64 + 2 * lane + 1];
+      }
+      const long b0i = ib + 2 * lane, b1i = b0i + 1;
+      if (EVAL) {
+        a.out_val[b0i] = g0;
+        a.out_val[b1i] = g1;
+      } else {
+        if (!last && a.hist) {
+          if (b0i < a.B) a.hist[(size_t)k * a.B + b0i] = g0;
+          if (b1i < a.B) a.hist[(size_t)k * a.B + b1i] = g1;
+        }
+        if (last) {
+          a.bound[b0i] = g0;
+          a.bound[b1i] = g1;
+        }
+        if (!frz[2 * lane]) {
+          if (valid_bound(g0)) best0 = (g0 > best0) ? g0 : best0;
+          else frz[2 * lane] = 1;
+        }
+        if (!frz[2 * lane + 1]) {
+          if (valid_bound(g1)) best1 = (g1 > best1) ? g1 : best1;
+          else frz[2 * lane + 1] = 1;
+        }
+      }
+    }
+    if (!last) {
+      // y_{k+1} rows must be visible to the async proxy before the producer
+      // issues sweep k+1's bulk copies
+      __threadfence();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      named_bar(2, (NW + 1) * 32);
+    } else {
+      named_bar(1, CT);
+    }
+  }
+  if (!EVAL && warp == 0 && act) {
+    a.best[ib + 2 * lane] = best0;
+    a.best[ib + 2 * lane + 1] = best1;
+    a.status[ib + 2 * lane] = frz[2 * lane];
+    a.status[ib + 2 * lane + 1] = frz[2 * lane + 1];
+  }
+}
+
+}  // namespace dcopf

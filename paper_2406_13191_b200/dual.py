@@ -20,7 +20,7 @@ from . import _build
 
 FORM_F2 = 0  # DCOPF_FORM_FLOW_BOX
 FORM_F1 = 1  # DCOPF_FORM_LIMIT_ROWS
-PATH_AUTO, PATH_BATCHED, PATH_SINGLE, PATH_BATCHED_SIMPLE = 0, 1, 2, 3
+PATH_AUTO, PATH_BATCHED, PATH_SINGLE = 0, 1, 2
 INST_OK, INST_DIVERGED = 0, 1
 ERRORS = {-1: "EINVAL", -2: "ETOPOLOGY", -3: "ECUDA", -4: "ENOMEM", -5: "ESTATE"}
 
@@ -53,7 +53,7 @@ class Info(ctypes.Structure):
                 ("smem_bytes", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
                 ("grid", ctypes.c_int32), ("launches_per_iter", ctypes.c_int32),
                 ("state_on_chip", ctypes.c_int32), ("chunk", ctypes.c_int32),
-                ("ring_bus", ctypes.c_int32), ("ring_branch", ctypes.c_int32)]
+                ("ring_bus", ctypes.c_int32), ("ring_branch", ctypes.c_int32), ("tile_width", ctypes.c_int32)]
 
 
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",

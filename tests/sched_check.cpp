@@ -6,6 +6,7 @@
 // (internal ids, branches sorted by larger endpoint), then per bus its
 // incident branch list "deg l0 to0 l1 to1 ...".
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -29,7 +30,8 @@ int main(int argc, char **argv) {
   if (!e0.empty()) { printf("ERR %s\n", e0.c_str()); return 1; }
   NetInternal &n = in.net;
   Schedule S;
-  std::string err = build_schedule(n, CH, P, 8, &S);
+  const int W = argc > 2 ? atoi(argv[2]) : 32;
+  std::string err = build_schedule(n, CH, P, W, 8, &S);
   if (!err.empty()) { printf("ERR %s\n", err.c_str()); return 1; }
   const bool f1 = n.form == 1;
   std::vector<int> brp(S.n_br_slots, -1), lamp(S.n_lam_slots, -1), dp(S.n_d_slots, -1), th(S.n_th_slots, -1),
@@ -37,7 +39,7 @@ int main(int argc, char **argv) {
   std::vector<int> seenA(n.nb, 0), seenB(n.nl, 0), seenC(n.nb, 0);
   int bad = 0;
   auto issue = [&](int c) {
-    if (c >= S.nch) return;
+    if (c >= S.nsteps) return;
     for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
       int x = S.ld_ent[e], kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff, slot = S.ld_slot[e];
       (kind == LD_LAM ? lamp : kind == LD_D ? dp : brp)[slot] = ent;
@@ -51,12 +53,12 @@ int main(int argc, char **argv) {
     }
   };
   // expect_tx of every chunk = program block + the rows the producer copies
-  for (int c = 0; c < S.nch; ++c) {
+  for (int c = 0; c < S.nsteps; ++c) {
     long bytes = S.prog_bytes[c];
     for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
       int kind = (int)((unsigned)S.ld_ent[e] >> 30);
       if (kind != LD_LAM && kind != LD_D && kind != LD_BR) { printf("BAD kind %d\n", kind); ++bad; }
-      bytes += (kind == LD_BR) ? S.br_row_bytes : 256;
+      bytes += (kind == LD_BR) ? S.br_row_bytes : S.row_bytes;
     }
     if (bytes != S.tx_bytes[c] || S.prog_bytes[c] % 16 || S.prog_bytes[c] > S.max_prog_bytes) {
       printf("BAD tx chunk %d: %ld vs %d\n", c, bytes, S.tx_bytes[c]);
@@ -64,16 +66,25 @@ int main(int argc, char **argv) {
     }
   }
   for (int c = 0; c <= P; ++c) issue(c);
-  for (int c = 0; c < S.nch; ++c) {
+  const int RB = S.row_bytes, BR = S.br_row_bytes;
+  for (int c = 0; c < S.nsteps; ++c) {
     const uint8_t *pg = S.prog.data() + S.prog_off[c];
     const int *h = reinterpret_cast<const int *>(pg);
-    const int BR = S.br_row_bytes;
     const RecA *A = reinterpret_cast<const RecA *>(pg + h[PH_OFF_A]);
     const RecIA2 *IA2 = reinterpret_cast<const RecIA2 *>(pg + h[PH_OFF_IA]);
     const RecIA1 *IA1 = reinterpret_cast<const RecIA1 *>(pg + h[PH_OFF_IA]);
+    const RecB *Bv = reinterpret_cast<const RecB *>(pg + h[PH_OFF_B]);
+    const RecC *Cv = reinterpret_cast<const RecC *>(pg + h[PH_OFF_C]);
+    const RecIC2 *IC2 = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
+    const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
+    // the step's code writes land first (worst case for the concurrent readers)
+    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th] = h[PH_A0] + j;
+    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs] = h[PH_B0] + j;
+    // A(c)
     for (int j = 0; j < h[PH_NA]; ++j) {
       int bus = h[PH_A0] + j;
       seenA[bus]++;
+      if (bus / S.CH != c) { printf("BAD A step\n"); ++bad; }
       if (A[j].e1 - A[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD A degree\n"); ++bad; }
       for (int e = A[j].e0; e < A[j].e1; ++e) {
         const int k = n.bus_ptr[bus] + e - A[j].e0;
@@ -85,11 +96,10 @@ int main(int argc, char **argv) {
         const int row = f1 ? IA1[e].row : IA2[e].row;
         if (row % BR) { printf("BAD A row align\n"); ++bad; }
         want(brp, row / BR, l, "A br", c);
-        if (f1) { want(lamp, IA1[e].ls / 256, n.bs[l], "A lam_s", c); want(lamp, IA1[e].lt / 256, n.bt[l], "A lam_t", c); }
+        if (f1) { want(lamp, IA1[e].ls / RB, n.bs[l], "A lam_s", c); want(lamp, IA1[e].lt / RB, n.bt[l], "A lam_t", c); }
       }
-      th[A[j].th] = bus;
     }
-    const RecB *Bv = reinterpret_cast<const RecB *>(pg + h[PH_OFF_B]);
+    // B(c-1)
     for (int j = 0; j < h[PH_NB]; ++j) {
       int l = h[PH_B0] + j;
       seenB[l]++;
@@ -97,19 +107,16 @@ int main(int argc, char **argv) {
       want(th, Bv[j].ts, n.bs[l], "B th_s", c);
       want(th, Bv[j].tt, n.bt[l], "B th_t", c);
       if (!f1) {
-        want(lamp, Bv[j].ls / 256, n.bs[l], "B lam_s", c);
-        want(lamp, Bv[j].lt / 256, n.bt[l], "B lam_t", c);
-        fc[Bv[j].fs] = l;
+        want(lamp, Bv[j].ls / RB, n.bs[l], "B lam_s", c);
+        want(lamp, Bv[j].lt / RB, n.bt[l], "B lam_t", c);
       }
     }
-    const RecC *Cv = reinterpret_cast<const RecC *>(pg + h[PH_OFF_C]);
-    const RecIC2 *IC2 = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
-    const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
+    // C(c-2)
     for (int j = 0; j < h[PH_NC]; ++j) {
       int bus = Cv[j].bus;
       seenC[bus]++;
-      want(lamp, Cv[j].ls / 256, bus, "C lam", c);
-      want(dp, Cv[j].ds / 256, bus, "C d", c);
+      want(lamp, Cv[j].ls / RB, bus, "C lam", c);
+      want(dp, Cv[j].ds / RB, bus, "C d", c);
       if (Cv[j].e1 - Cv[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD C degree\n"); ++bad; }
       for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
         const int k = n.bus_ptr[bus] + e - Cv[j].e0;

@@ -121,7 +121,7 @@ def test_config4_full_batch_sampled():
     a = inst.alpha_schedule(K)
     gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=FORM_F2,
                   path=dual.PATH_BATCHED)
-    assert gpu["info"].grid == B // 32
+    assert gpu["info"].grid * gpu["info"].tile_width >= B and gpu["info"].grid <= 148
     idx = np.array([0, 31, 4097, 8191])
     orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=FORM_F2,
                        threads=4)

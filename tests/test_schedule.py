@@ -24,19 +24,19 @@ def checker():
     return EXE
 
 
-def run(checker, net, form, CH, P, order="dfs"):
+def run(checker, net, form, CH, P, order="dfs", W=32):
     lines = [f"{net.n_bus} {net.n_branch} {net.ref_bus} {form} {CH} {P}"]
     lines += [f"{a} {b}" for a, b in zip(net.br_from, net.br_to)]
-    res = subprocess.run([checker, order], input="\n".join(lines) + "\n", capture_output=True, text=True)
+    res = subprocess.run([checker, order, str(W)], input="\n".join(lines) + "\n", capture_output=True, text=True)
     return res.returncode, res.stdout
 
 
 @pytest.mark.parametrize("config", [0, 1, 3])
 @pytest.mark.parametrize("form", [0, 1])
-@pytest.mark.parametrize("CH,P", [(32, 2), (8, 1), (64, 3)])
-def test_schedule_slots_valid(checker, config, form, CH, P):
+@pytest.mark.parametrize("CH,P,W", [(32, 2, 56), (8, 1, 2), (64, 3, 64)])
+def test_schedule_slots_valid(checker, config, form, CH, P, W):
     net = inst.make_network(config)
-    rc, out = run(checker, net, form, CH, P)
+    rc, out = run(checker, net, form, CH, P, W=W)
     assert rc == 0, out
 
 
@@ -57,12 +57,12 @@ def test_schedule_random_small(checker, seed):
 
 
 def test_dfs_order_keeps_smem_small(checker):
-    """The DFS tree order is what makes the window fit: config-3 network,
-    CH=16, P=2 fits two CTAs per SM (<= ~113 KB) for both forms; RCM does not
-    come close."""
+    """The DFS tree order is what makes the window fit: config-3 network with
+    56-instance tiles (the config-4 bench tiling) fits one CTA's shared memory
+    at CH=16 for both forms; with RCM order it does not come close."""
     net = inst.make_network(3)
     for form in (0, 1):
-        rc, out = run(checker, net, form, 16, 2)
-        assert rc == 0 and int(out.split("smem ")[1].split()[0]) <= 113 * 1024, out
-    rc, out = run(checker, net, 0, 16, 2, order="rcm")
+        rc, out = run(checker, net, form, 16, 2, W=56)
+        assert rc == 0 and int(out.split("smem ")[1].split()[0]) <= 220 * 1024, out
+    rc, out = run(checker, net, 0, 16, 2, order="rcm", W=56)
     assert int(out.split("smem ")[1].split()[0]) > 227 * 1024, out
