@@ -31,7 +31,7 @@ using namespace dcopf;
 
 static thread_local std::string g_create_error;
 
-static const int kSweepWarps = 16;  // consumer warps of k_sweep (+1 producer warp)
+static const int kSweepWarps = 15;  // consumer warps of k_sweep (+1 producer warp = 16 warps, 4 per SMSP)
 
 struct dcopf_dual_s {
   std::string err;
@@ -242,14 +242,18 @@ size_t single_smem(int n_bus, int n_br, int form, bool state) {
 int stage_alpha(dcopf_dual_t h, int64_t K, const double *alpha, cudaStream_t s) {
   if (!h->alpha_ev) CK(h, cudaEventCreateWithFlags(&h->alpha_ev, cudaEventDisableTiming));
   CK(h, cudaEventSynchronize(h->alpha_ev));
-  if ((size_t)K > h->alpha_cap) {
+  if ((size_t)K > h->alpha_cap || !h->alpha_dev) {
+    // capacity grows geometrically from 64 Ki steps, so a run never allocates
+    // (a synchronising call) once its longest schedule has been seen
+    size_t cap = std::max<size_t>(65536, h->alpha_cap);
+    while (cap < (size_t)K) cap *= 2;
     cudaFree(h->alpha_dev);
     cudaFreeHost(h->alpha_pin);
     h->alpha_dev = h->alpha_pin = nullptr;
     h->alpha_cap = 0;
-    CK(h, cudaMalloc(&h->alpha_dev, K * 8));
-    CK(h, cudaMallocHost(&h->alpha_pin, K * 8));
-    h->alpha_cap = K;
+    CK(h, cudaMalloc(&h->alpha_dev, cap * 8));
+    CK(h, cudaMallocHost(&h->alpha_pin, cap * 8));
+    h->alpha_cap = cap;
   }
   if (K > 0) {
     memcpy(h->alpha_pin, alpha, K * 8);

@@ -117,7 +117,7 @@ __device__ __forceinline__ double dec(unsigned pos, unsigned neg, int lane, doub
 }
 
 template <int FORM, bool EVAL, int NW>
-__global__ void __maxnreg__(120) k_sweep(const SweepArgs a) {
+__global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + a.off_bar);
   uint64_t *empty = full + a.S;
