@@ -335,6 +335,7 @@ def main():
                        "path": {1: "batched-sweep", 2: "single"}[path],
                        "kernel": {"grid": info.grid, "threads": info.threads_per_block, "smem": info.smem_bytes,
                                   "chunk": info.chunk, "tile_width": info.tile_width,
+                                  "copies_per_sweep": info.copies_per_sweep, "ring_life": info.ring_life,
                                   "smem_slots_lambda": info.ring_bus, "smem_slots_branch": info.ring_branch,
                                   "order_bandwidth": info.bandwidth},
                        "parallelism": f"instance-shard x{world}",

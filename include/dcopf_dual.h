@@ -179,6 +179,8 @@ typedef struct {
   int32_t chunk;                  /* batched path: buses per schedule chunk */
   int32_t ring_bus, ring_branch;  /* batched path: shared-memory slots for lambda / branch rows */
   int32_t tile_width;             /* instances per CTA (batched W; 1 for the single path) */
+  int32_t copies_per_sweep;       /* batched path: bulk copies per tile per iteration */
+  int32_t ring_life;              /* batched path: rows live <= this many steps use the rings */
 } dcopf_info;
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info);
 

@@ -63,8 +63,10 @@ struct dcopf_dual_s {
   int sched_W = 0;
   uint8_t *d_prog = nullptr;
   long long *d_prog_off = nullptr;
-  int *d_prog_bytes = nullptr, *d_tx_bytes = nullptr, *d_ld_ptr = nullptr, *d_ld_ent = nullptr,
-      *d_ld_slot = nullptr;
+  int *d_prog_bytes = nullptr, *d_tx_bytes = nullptr, *d_ld_ptr = nullptr, *d_ld = nullptr;
+  // batched path state layout: storage position <-> original id, per kind
+  int *d_lam_perm_b = nullptr, *d_lam_inv_b = nullptr, *d_d_perm_b = nullptr, *d_br_perm_b = nullptr,
+      *d_br_inv_b = nullptr, *d_br_pos_b = nullptr;
 };
 
 namespace {
@@ -273,15 +275,29 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
 // DCOPF_CHUNK (default 32) and halves until the kernel's shared memory fits.
 int compile_schedule(dcopf_dual_t h, int W) {
   if (h->sched_W == W) return DCOPF_OK;
-  int CH = 32, P = 2;
-  if (const char *e = getenv("DCOPF_CHUNK")) CH = std::max(1, atoi(e));
+  // search (chunk, ring life) from large to small until the kernel's shared
+  // memory fits: larger chunks mean fewer steps, longer ring lives fewer copies
+  int P = 2;
   if (const char *e = getenv("DCOPF_PREFETCH")) P = std::max(1, atoi(e));
+  std::vector<std::pair<int, int>> cands;
+  if (const char *e = getenv("DCOPF_CHUNK")) {
+    const int life = getenv("DCOPF_RING_LIFE") ? atoi(getenv("DCOPF_RING_LIFE")) : 4;
+    cands.push_back({std::max(1, atoi(e)), life});
+  }
+  const int chs[] = {32, 16, 8, 4, 2, 1}, lifes[] = {6, 4, 2};
+  for (int ch : chs)
+    for (int life : lifes) cands.push_back({ch, life});
   Schedule sc;
   bool ok = false;
-  for (int ch = CH; ch >= 1 && !ok; ch /= 2) {
-    std::string err = build_schedule(h->ni, ch, P, W, kSweepWarps, &sc);
+  for (auto &cd : cands) {
+    sc = Schedule();
+    sc.ring_life = cd.second;
+    std::string err = build_schedule(h->ni, cd.first, P, W, kSweepWarps, &sc);
     if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
-    ok = sc.total <= h->dev_smem;
+    if (sc.total <= h->dev_smem) {
+      ok = true;
+      break;
+    }
   }
   if (!ok) return fail(h, DCOPF_EINVAL, "batched schedule does not fit shared memory; use the single path");
   h->sch = sc;
@@ -290,8 +306,36 @@ int compile_schedule(dcopf_dual_t h, int W) {
   if (!rc) rc = upload(h, &h->d_prog_bytes, h->sch.prog_bytes);
   if (!rc) rc = upload(h, &h->d_tx_bytes, h->sch.tx_bytes);
   if (!rc) rc = upload(h, &h->d_ld_ptr, h->sch.ld_ptr);
-  if (!rc) rc = upload(h, &h->d_ld_ent, h->sch.ld_ent);
-  if (!rc) rc = upload(h, &h->d_ld_slot, h->sch.ld_slot);
+  if (!rc) {
+    std::vector<int> ld(4 * h->sch.ld.size());
+    for (size_t x = 0; x < h->sch.ld.size(); ++x) {
+      ld[4 * x] = h->sch.ld[x].a;
+      ld[4 * x + 1] = h->sch.ld[x].b;
+      ld[4 * x + 2] = h->sch.ld[x].c;
+      ld[4 * x + 3] = h->sch.ld[x].d;
+    }
+    rc = upload(h, &h->d_ld, ld);
+  }
+  // storage order of the batched state (per kind) in terms of original ids
+  if (!rc) {
+    const int nb = h->n_bus, nl = h->n_br;
+    std::vector<int> lam_perm(nb), lam_inv(nb), d_perm(nb), br_perm(nl), br_inv(nl);
+    for (int p = 0; p < nb; ++p) {
+      lam_perm[p] = h->bus_perm[h->sch.perm_lam[p]];
+      lam_inv[lam_perm[p]] = p;
+      d_perm[p] = h->bus_perm[h->sch.perm_d[p]];
+    }
+    for (int p = 0; p < nl; ++p) {
+      br_perm[p] = h->br_perm[h->sch.perm_br[p]];
+      br_inv[br_perm[p]] = p;
+    }
+    if (!rc) rc = upload(h, &h->d_lam_perm_b, lam_perm);
+    if (!rc) rc = upload(h, &h->d_lam_inv_b, lam_inv);
+    if (!rc) rc = upload(h, &h->d_d_perm_b, d_perm);
+    if (!rc) rc = upload(h, &h->d_br_perm_b, br_perm);
+    if (!rc) rc = upload(h, &h->d_br_inv_b, br_inv);
+    if (!rc) rc = upload(h, &h->d_br_pos_b, h->sch.pos_br);
+  }
   if (rc) return rc;
   std::vector<uint8_t>().swap(h->sch.prog);  // device copy only
   const int b = h->sch.total;
@@ -301,6 +345,16 @@ int compile_schedule(dcopf_dual_t h, int W) {
   if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps>, b);
   if (!rc) h->sched_W = W;
   return rc;
+}
+
+// state-layout permutations of the current path (storage position <-> original id)
+struct Perms {
+  const int *lam_perm, *lam_inv, *d_perm, *br_perm, *br_inv;
+};
+Perms perms(dcopf_dual_t h) {
+  if (h->path == DCOPF_PATH_BATCHED)
+    return Perms{h->d_lam_perm_b, h->d_lam_inv_b, h->d_d_perm_b, h->d_br_perm_b, h->d_br_inv_b};
+  return Perms{h->d_bus_perm, h->d_bus_inv, h->d_bus_perm, h->d_br_perm, h->d_br_inv};
 }
 
 int configure_single(dcopf_dual_t h) {
@@ -342,8 +396,7 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.prog_bytes = h->d_prog_bytes;
   a.tx_bytes = h->d_tx_bytes;
   a.ld_ptr = h->d_ld_ptr;
-  a.ld_ent = h->d_ld_ent;
-  a.ld_slot = h->d_ld_slot;
+  a.ld = reinterpret_cast<const int4 *>(h->d_ld);
   a.nsteps = sc.nsteps;
   a.S = sc.S;
   a.row_bytes = sc.row_bytes;
@@ -360,6 +413,7 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.off_dp = sc.off_dp;
   a.off_th = sc.off_th;
   a.off_fc = sc.off_fc;
+  if (const char *e = getenv("DCOPF_DEBUG_MODE")) a.debug_mode = atoi(e);  // measurement only
   return a;
 }
 
@@ -417,7 +471,8 @@ void dcopf_dual_destroy(dcopf_dual_t h) {
   free_batch(h);
   int *ip[] = {h->d_bus_ptr, h->d_bus_inc, h->d_gen_ptr,    h->d_br_s,      h->d_br_t,    h->d_bus_perm,
                h->d_bus_inv, h->d_br_perm, h->d_br_inv,     h->d_prog_bytes, h->d_tx_bytes, h->d_ld_ptr,
-               h->d_ld_ent,  h->d_ld_slot, h->flag};
+               h->d_ld,      h->flag,      h->d_lam_perm_b, h->d_lam_inv_b, h->d_d_perm_b, h->d_br_perm_b,
+               h->d_br_inv_b, h->d_br_pos_b};
   for (int *p : ip) cudaFree(p);
   double *dp[] = {h->d_theta, h->d_gen_c, h->d_gen_lo, h->d_gen_hi, h->d_gen_a, h->d_br_b, h->d_br_F,
                   h->scratch, h->alpha_dev};
@@ -658,7 +713,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
     CK(h, cudaMemcpyAsync(h->outs, padded.data(), padded.size() * 4, cudaMemcpyHostToDevice, s));
     CK(h, cudaStreamSynchronize(s));  // `padded` dies at scope exit
   }
-  int rc = import_ext(h, load, h->load, h->d_bus_perm, h->n_bus, 1, s);
+  int rc = import_ext(h, load, h->load, perms(h).d_perm, h->n_bus, 1, s);
   if (rc) return rc;
   k_fill_d<<<grid_for(nlam), 256, 0, s>>>(h->lam[0], 0.0, nlam);
   k_fill_d<<<grid_for(nbr), 256, 0, s>>>(h->br[0], 0.0, nbr);
@@ -724,8 +779,9 @@ int dcopf_dual_get_multipliers(dcopf_dual_t h, double *lambda, double *branch, v
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   const int cur = (h->path == DCOPF_PATH_BATCHED) ? h->cur : 0;
-  int rc = export_ext(h, h->lam[cur], lambda, h->d_bus_inv, h->n_bus, 1, s);
-  if (!rc) rc = export_ext(h, h->br[cur], branch, h->d_br_inv, h->n_br, brw(h->form), s);
+  const Perms pm = perms(h);
+  int rc = export_ext(h, h->lam[cur], lambda, pm.lam_inv, h->n_bus, 1, s);
+  if (!rc) rc = export_ext(h, h->br[cur], branch, pm.br_inv, h->n_br, brw(h->form), s);
   return rc;
 }
 
@@ -744,8 +800,9 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
     return fail(h, DCOPF_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e));
   }
   int rc = DCOPF_OK;
-  if (lambda) rc = import_ext(h, lambda, tl, h->d_bus_perm, h->n_bus, 1, s);
-  if (!rc && branch) rc = import_ext(h, branch, tb, h->d_br_perm, h->n_br, brw(h->form), s);
+  const Perms pm = perms(h);
+  if (lambda) rc = import_ext(h, lambda, tl, pm.lam_perm, h->n_bus, 1, s);
+  if (!rc && branch) rc = import_ext(h, branch, tb, pm.br_perm, h->n_br, brw(h->form), s);
   if (!rc) {
     int bad = 0;
     cudaMemsetAsync(h->flag, 0, sizeof(int), s);
@@ -755,8 +812,9 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
       // the batched F2 kernel holds an outaged branch's nu at exactly 0 (it does
       // not enter that instance's dual); a warm start must respect that
       if (h->form == DCOPF_FORM_FLOW_BOX && h->max_out > 0)
-        k_check_outaged<<<grid_for((size_t)h->B * h->max_out), 256, 0, s>>>(tb, h->outs, h->max_out, h->B, h->n_br,
-                                                                            h->T, h->flag);
+        k_check_outaged<<<grid_for((size_t)h->B * h->max_out), 256, 0, s>>>(
+            tb, h->outs, h->path == DCOPF_PATH_BATCHED ? h->d_br_pos_b : nullptr, h->max_out, h->B, h->n_br, h->T,
+            h->flag);
     }
     cudaMemcpyAsync(&bad, h->flag, sizeof(int), cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
@@ -801,8 +859,9 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
   }
   if (rc) return rc;
   rc = copy_out(h, value, h->value, s);
-  if (!rc) rc = export_ext(h, h->g_lam, grad_lambda, h->d_bus_inv, h->n_bus, 1, s);
-  if (!rc) rc = export_ext(h, h->g_br, grad_branch, h->d_br_inv, h->n_br, brw(h->form), s);
+  const Perms pm = perms(h);
+  if (!rc) rc = export_ext(h, h->g_lam, grad_lambda, pm.lam_inv, h->n_bus, 1, s);
+  if (!rc) rc = export_ext(h, h->g_br, grad_branch, pm.br_inv, h->n_br, brw(h->form), s);
   return rc;
 }
 
@@ -827,6 +886,8 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
     info->chunk = h->sch.CH;
     info->ring_bus = h->sch.n_lam_slots;
     info->ring_branch = h->sch.n_br_slots;
+    info->copies_per_sweep = h->sch.n_copies;
+    info->ring_life = h->sch.ring_life;
     info->tile_width = h->T;
   } else if (h->path == DCOPF_PATH_SINGLE) {
     info->smem_bytes = h->smem_single;

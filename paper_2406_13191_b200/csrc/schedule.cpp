@@ -297,35 +297,100 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     iv_th[i] = {stA(chunk(i)), tl, i};
   }
   std::vector<int> br_slot(nl), lam_slot(nb), d_slot(nb), th_slot(nb), f_slot(nl, 0);
-  S.n_br_slots = colour(iv_br, br_slot);
-  S.n_lam_slots = colour(iv_lam, lam_slot);
-  S.n_d_slots = colour(iv_d, d_slot);
   S.n_th_slots = colour(iv_th, th_slot);
   S.n_f_slots = 0;
-  if (!f1) {  // f* code: written B(chunk hi), read C of both endpoints
+  if (!f1) {  // f*: written B(chunk hi), read C of both endpoints
     iv_f.resize(nl);
     for (int l = 0; l < nl; ++l)
       iv_f[l] = {stB(chunk(hi[l])), std::max(stC(chunk(rp[net.bs[l]])), stC(chunk(rp[net.bt[l]]))), l};
     S.n_f_slots = colour(iv_f, f_slot);
   }
 
-  // ---- load lists: rows grouped by the step of their first use ----
-  std::vector<std::vector<int>> lds(nst);
-  for (int i = 0; i < nb; ++i) lds[lam_first[i]].push_back((LD_LAM << 30) | i);
-  for (int i = 0; i < nb; ++i) lds[d_first[i]].push_back((LD_D << 30) | i);
-  for (int l = 0; l < nl; ++l) lds[br_first[l]].push_back((LD_BR << 30) | l);
-  S.ld_ptr.assign(nst + 1, 0);
-  S.ld_ent.clear();
-  S.ld_slot.clear();
-  std::vector<int> row_bytes(nst, 0);
-  for (int st = 0; st < nst; ++st) {
-    for (int x : lds[st]) {
-      const int kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff;
-      S.ld_ent.push_back(x);
-      S.ld_slot.push_back(kind == LD_LAM ? lam_slot[ent] : (kind == LD_D ? d_slot[ent] : br_slot[ent]));
-      row_bytes[st] += (kind == LD_BR) ? BR : RB;
+  // ---- storage order and shared-memory slots of the state rows ----
+  // Rows of each kind are stored in HBM in load order, short-lived rows
+  // (live range <= LIFE steps) first: a step's short-lived rows are then one
+  // contiguous range, copied by one TMA bulk copy (two at the ring wrap) into
+  // a ring of slots (slot = position mod R, R = the largest number of rows
+  // issued-but-not-dead at once).  The few long-lived rows follow in storage
+  // and get individual copies into interval-coloured "sticky" slots R, R+1, ...
+  const int LIFE = S.ring_life;
+  auto place = [&](int n, const std::vector<Interval> &iv, const std::vector<int> &first, std::vector<int> &pos,
+                   std::vector<int> &perm, std::vector<int> &slot, int *ring, int *nslots) {
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return first[x] < first[y]; });
+    std::vector<int> rr, sticky;
+    for (int id : idx) (iv[id].hi - first[id] <= LIFE ? rr : sticky).push_back(id);
+    pos.assign(n, 0);
+    perm.assign(n, 0);
+    int p = 0;
+    for (int id : rr) { pos[id] = p; perm[p++] = id; }
+    for (int id : sticky) { pos[id] = p; perm[p++] = id; }
+    int R = 1;
+    for (size_t k = 0, j = 0; k < rr.size(); ++k) {  // j: oldest ring row still live at issue time of k
+      const int t = iv[rr[k]].lo;                   // issue time (first - P, clamped)
+      while (j < k && iv[rr[j]].hi < t) ++j;
+      R = std::max(R, (int)(k - j + 1));
     }
-    S.ld_ptr[st + 1] = (int)S.ld_ent.size();
+    for (size_t k = 0; k < rr.size(); ++k) slot[rr[k]] = (int)(k % R);
+    std::vector<Interval> siv;
+    for (int id : sticky) siv.push_back({iv[id].lo, iv[id].hi, id});
+    std::vector<int> sslot(n, 0);
+    const int ns = colour(siv, sslot);
+    for (int id : sticky) slot[id] = R + sslot[id];
+    *ring = R;
+    *nslots = R + ns;
+    return (int)rr.size();
+  };
+  int ring_lam = 0, ring_d = 0, ring_br = 0;
+  const int nr_lam = place(nb, iv_lam, lam_first, S.pos_lam, S.perm_lam, lam_slot, &ring_lam, &S.n_lam_slots);
+  const int nr_d = place(nb, iv_d, d_first, S.pos_d, S.perm_d, d_slot, &ring_d, &S.n_d_slots);
+  const int nr_br = place(nl, iv_br, br_first, S.pos_br, S.perm_br, br_slot, &ring_br, &S.n_br_slots);
+  S.ring_lam = ring_lam;
+  S.ring_d = ring_d;
+  S.ring_br = ring_br;
+
+  // ---- load lists: per step, ranges of rows (kind, first position, count, first slot) ----
+  S.ld_ptr.assign(nst + 1, 0);
+  S.ld.clear();
+  std::vector<int> row_bytes(nst, 0);
+  S.n_copies = 0;
+  S.n_sticky_copies = 0;
+  struct KindInfo {
+    int kind, n, nring, R, bytes;
+    const std::vector<int> *first, *pos, *perm, *slot;
+  };
+  const KindInfo kinds[3] = {{LD_LAM, nb, nr_lam, ring_lam, RB, &lam_first, &S.pos_lam, &S.perm_lam, &lam_slot},
+                             {LD_D, nb, nr_d, ring_d, RB, &d_first, &S.pos_d, &S.perm_d, &d_slot},
+                             {LD_BR, nl, nr_br, ring_br, BR, &br_first, &S.pos_br, &S.perm_br, &br_slot}};
+  std::vector<std::vector<int4_t>> per(nst);
+  for (const KindInfo &K : kinds) {
+    // ring rows: positions [0, nring) sorted by first use -> one run per step
+    for (int p0 = 0; p0 < K.nring;) {
+      const int st = (*K.first)[(*K.perm)[p0]];
+      int p1 = p0;
+      while (p1 < K.nring && (*K.first)[(*K.perm)[p1]] == st) ++p1;
+      for (int q = p0; q < p1;) {  // split at the ring wrap
+        const int sl = q % K.R;
+        const int cnt = std::min(p1 - q, K.R - sl);
+        per[st].push_back({K.kind, q, cnt, sl});
+        q += cnt;
+      }
+      p0 = p1;
+    }
+    for (int p = K.nring; p < K.n; ++p) {  // sticky rows
+      const int id = (*K.perm)[p];
+      per[(*K.first)[id]].push_back({K.kind, p, 1, (*K.slot)[id]});
+      ++S.n_sticky_copies;
+    }
+  }
+  for (int st = 0; st < nst; ++st) {
+    for (const int4_t &x : per[st]) {
+      S.ld.push_back(x);
+      row_bytes[st] += x.c * (x.a == LD_BR ? BR : RB);
+    }
+    S.n_copies += (int)per[st].size();
+    S.ld_ptr[st + 1] = (int)S.ld.size();
   }
 
   // ---- program blocks, one per step ----
@@ -345,7 +410,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
       const int a1 = std::min(nb, a0 + CH);
       for (int i = a0; i < a1; ++i) {
         RecA r{};
-        r.th = th_slot[i];
+        r.th = th_slot[i] * RB;
         r.theta = net.theta[i];
         r.e0 = f1 ? (int)IA1.size() : (int)IA2.size();
         for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
@@ -378,16 +443,15 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
         const int s = net.bs[l], t = net.bt[l];
         RecB r{};
         r.row = br_slot[l] * BR;
-        r.ts = th_slot[s];
-        r.tt = th_slot[t];
+        r.wpos = S.pos_br[l];
+        r.ts = th_slot[s] * RB;
+        r.tt = th_slot[t] * RB;
         r.b = net.b[l];
         r.F = net.F[l];
-        r.Ts = net.theta[s];
-        r.Tt = net.theta[t];
         if (!f1) {
           r.ls = lam_slot[s] * RB;
           r.lt = lam_slot[t] * RB;
-          r.fs = f_slot[l];
+          r.fs = f_slot[l] * RB;
         }
         Bv.push_back(r);
       }
@@ -401,7 +465,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
       for (int j = cch[cc]; j < cch[cc + 1]; ++j) {
         const int i = cord[j];
         RecC r{};
-        r.bus = i;
+        r.wpos = S.pos_lam[i];
         r.ls = lam_slot[i] * RB;
         r.ds = d_slot[i] * RB;
         r.g0 = (int)G.size();
@@ -413,18 +477,16 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
           const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
           if (!f1) {
             RecIC2 x{};
-            x.fs = f_slot[l];
+            x.f = f_slot[l] * RB;
             x.br = l;
-            x.sF = to ? net.F[l] : -net.F[l];  // d/dlambda: +f* at the to bus, -f* at the from bus
+            x.s = to ? 1.0 : -1.0;  // d/dlambda: +f* at the to bus, -f* at the from bus
             IC2.push_back(x);
           } else {
             RecIC1 x{};
-            x.ts = th_slot[net.bs[l]];
-            x.tt = th_slot[net.bt[l]];
+            x.ts = th_slot[net.bs[l]] * RB;
+            x.tt = th_slot[net.bt[l]] * RB;
             x.br = l;
             x.sb = to ? net.b[l] : -net.b[l];  // +phi at the to bus, -phi at the from bus
-            x.Ts = net.theta[net.bs[l]];
-            x.Tt = net.theta[net.bt[l]];
             IC1.push_back(x);
           }
         }
@@ -485,10 +547,10 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   off = al(off + S.n_lam_slots * RB + 512);
   S.off_dp = off;
   off = al(off + S.n_d_slots * RB + 512);
-  S.off_th = off;
-  off = al(off + S.n_th_slots * 16);
-  S.off_fc = off;
-  off = al(off + S.n_f_slots * 16);
+  S.off_th = off;  // theta*_i rows
+  off = al(off + S.n_th_slots * RB + 512);
+  S.off_fc = off;  // f*_l rows (F2)
+  off = al(off + S.n_f_slots * RB + 512);
   S.total = off;
   return "";
 }

@@ -34,17 +34,17 @@ enum ProgHeader {
 };
 constexpr int kProgHeaderBytes = 64;
 
-struct alignas(16) RecA { int e0, e1, th, pad; double theta, pad2; };                      // bus of phase A
-struct alignas(16) RecIA2 { int row, br; double sb; };                                      // F2: sb = to ? b : -b
-struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };                         // F1: sb = to ? -b : b
-struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, pad0, pad1; double b, F, Ts, Tt; };  // branch of phase B
-struct alignas(16) RecC { int bus, ls, ds, g0, g1, e0, e1, pad; };                         // bus of phase C
-struct alignas(16) RecG { double c, lo, hi, a; };                                            // generator
-struct alignas(16) RecIC2 { int fs, br; double sF; };                                       // F2: sF = to ? F : -F
-struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, Ts, Tt, pad2; };               // F1: sb = to ? b : -b
+// All row / value fields are byte offsets into their shared-memory pool; the
+// minimiser values theta*_i and f*_l are kept per instance (one W-wide row).
+struct alignas(16) RecA { int e0, e1, th, pad; double theta, pad2; };   // bus of phase A
+struct alignas(16) RecIA2 { int row, br; double sb; };                   // F2: sb = to ? b : -b
+struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };      // F1: sb = to ? -b : b
+struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, wpos, pad1; double b, F; };  // branch of phase B (wpos: nu' row)
+struct alignas(16) RecC { int wpos, ls, ds, g0, g1, e0, e1, pad; };     // bus of phase C (wpos: lambda' row)
+struct alignas(16) RecG { double c, lo, hi, a; };                         // generator
+struct alignas(16) RecIC2 { int f, br; double s; };                      // F2: s = to ? +1 : -1
+struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, pad2; };     // F1: sb = to ? b : -b
 
-// code words: 16 B per entity = ballots {pos0, neg0, pos1, neg1} of the
-// first / second instance of every lane
 // load-list entry kinds (top 2 bits of the packed entity word)
 enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
 
@@ -57,8 +57,16 @@ struct NetInternal {
   std::vector<double> gc, glo, ghi, ga;     // per generator (grouped by bus)
 };
 
+struct int4_t {
+  int a, b, c, d;  // load entry: kind, first storage position, row count, first slot
+};
+
 struct Schedule {
   int CH = 0, P = 0, S = 0, W = 0, nch = 0, nsteps = 0;
+  int ring_life = 6;                        // rows live <= this many steps go to the rings
+  int ring_lam = 0, ring_d = 0, ring_br = 0, n_copies = 0, n_sticky_copies = 0;
+  // storage order of the state rows in HBM (positions) and its inverse, per kind
+  std::vector<int> pos_lam, perm_lam, pos_d, perm_d, pos_br, perm_br;
   int row_bytes = 0;                        // lambda / d / nu row: 8 W
   int n_br_slots = 0, n_lam_slots = 0, n_d_slots = 0, n_th_slots = 0, n_f_slots = 0;
   int br_row_bytes = 0;                     // 8 W (nu) or 16 W (mu+, mu-)
@@ -67,7 +75,8 @@ struct Schedule {
   std::vector<long long> prog_off;          // [nsteps] byte offset of each block
   std::vector<int> prog_bytes;              // [nsteps]
   std::vector<int> tx_bytes;                // [nsteps] program + rows (expect_tx)
-  std::vector<int> ld_ptr, ld_ent, ld_slot; // load lists
+  std::vector<int> ld_ptr;                  // [nsteps+1] into ld
+  std::vector<int4_t> ld;                   // load entries (one bulk copy each)
   size_t smem_bytes(int nw) const;
   // smem layout offsets (bytes)
   int off_bar, off_red, off_frz, off_obm, off_outs, off_prog, off_brp, off_lamp, off_dp, off_th, off_fc, total;

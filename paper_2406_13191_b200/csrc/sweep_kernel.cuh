@@ -59,10 +59,12 @@ struct SweepArgs {
   const uint8_t *prog;
   const long long *prog_off;
   const int *prog_bytes, *tx_bytes;
-  const int *ld_ptr, *ld_ent, *ld_slot;
+  const int *ld_ptr;
+  const int4 *ld;                   // load entries {kind, first storage position, rows, first slot}
   int nsteps, S, row_bytes, br_row_bytes;
   int off_bar, off_red, off_frz, off_obm, off_outs, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th,
       off_fc;
+  int debug_mode;                   // 0; 1 = data movement only; 2 = no row copies (measurement only)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -110,10 +112,6 @@ __device__ __forceinline__ D2 ld2(const uint8_t *base, int off) {
 }
 __device__ __forceinline__ void st2(double *p, double x, double y) {
   *reinterpret_cast<double2 *>(p) = make_double2(x, y);
-}
-// code word {pos0, neg0, pos1, neg1}: +x, -x or z for instance t of this lane
-__device__ __forceinline__ double dec(unsigned pos, unsigned neg, int lane, double x, double z) {
-  return ((pos >> lane) & 1u) ? x : (((neg >> lane) & 1u) ? -x : z);
 }
 
 template <int FORM, bool EVAL, int NW>
@@ -169,21 +167,22 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
         const long u = g / S;
         if (u > 0) mbar_wait(&empty[st], (unsigned)((u - 1) & 1));
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[st], (unsigned)a.tx_bytes[c]);
+          mbar_arrive_expect_tx(&full[st], (unsigned)(a.debug_mode == 2 ? a.prog_bytes[c] : a.tx_bytes[c]));
           tma_load_1d(smem + a.off_prog + st * a.prog_stride, a.prog + a.prog_off[c], (unsigned)a.prog_bytes[c],
                       &full[st]);
         }
         __syncwarp();
-        const int e1 = a.ld_ptr[c + 1];
+        // each entry is one bulk copy of `rows` consecutive rows (storage
+        // order = load order) into consecutive slots
+        const int e1 = (a.debug_mode == 2) ? a.ld_ptr[c] : a.ld_ptr[c + 1];
         for (int e = a.ld_ptr[c] + lane; e < e1; e += 32) {
-          const int x = a.ld_ent[e], slot = a.ld_slot[e];
-          const int kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff;
-          if (kind == LD_LAM)
-            tma_load_1d(smem + a.off_lamp + slot * RB, lam_src + (size_t)ent * RB, RB, &full[st]);
-          else if (kind == LD_D)
-            tma_load_1d(smem + a.off_dp + slot * RB, d_src + (size_t)ent * RB, RB, &full[st]);
+          const int4 x = a.ld[e];
+          if (x.x == LD_LAM)
+            tma_load_1d(smem + a.off_lamp + x.w * RB, lam_src + (size_t)x.y * RB, x.z * RB, &full[st]);
+          else if (x.x == LD_D)
+            tma_load_1d(smem + a.off_dp + x.w * RB, d_src + (size_t)x.y * RB, x.z * RB, &full[st]);
           else
-            tma_load_1d(smem + a.off_brp + slot * BR, br_src + (size_t)ent * BR, BR, &full[st]);
+            tma_load_1d(smem + a.off_brp + x.w * BR, br_src + (size_t)x.y * BR, x.z * BR, &full[st]);
         }
       }
     }
@@ -195,8 +194,8 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
   const uint8_t *brp = smem + a.off_brp + lane * 16;
   const uint8_t *lamp = smem + a.off_lamp + lane * 16;
   const uint8_t *dp = smem + a.off_dp + lane * 16;
-  uint4 *th = reinterpret_cast<uint4 *>(smem + a.off_th);
-  uint4 *fc = reinterpret_cast<uint4 *>(smem + a.off_fc);
+  uint8_t *thp = smem + a.off_th + lane * 16;  // theta*_i rows
+  uint8_t *fcp = smem + a.off_fc + lane * 16;  // f*_l rows (F2)
   const int nout = a.max_out;
   const int *my_outs0 = outs_s + (2 * lane) * kMaxOut, *my_outs1 = my_outs0 + kMaxOut;
   auto flagged = [&](int l) { return (obm[l >> 5] >> (l & 31)) & 1u; };
@@ -234,6 +233,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
       const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC
       const int nA = h0.x, nB = h0.z, nC = h0.w;
 
+      if (a.debug_mode != 1) {
       // ---------------- A(s): w_i, theta* codes ----------------
       {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
@@ -264,15 +264,14 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
               w1 = w1 + sb1 * ((mp.y - mm.y) - (ls.y - lt.y));
             }
           }
-          const bool nr = (bus != a.ref) && act;
-          const bool p0 = nr && (w0 < 0.0), n0 = nr && (w0 > 0.0);
-          const bool p1 = nr && (w1 < 0.0), n1 = nr && (w1 > 0.0);
-          const uint4 cw = make_uint4(__ballot_sync(0xffffffffu, p0), __ballot_sync(0xffffffffu, n0),
-                                      __ballot_sync(0xffffffffu, p1), __ballot_sync(0xffffffffu, n1));
-          if (lane == 0) th[ra.th] = cw;
+          // theta* = -Theta if w > 0, +Theta if w < 0, 0 on a tie and at the reference bus
+          const bool nr = (bus != a.ref);
+          const double t0 = (nr && w0 < 0.0) ? ra.theta : ((nr && w0 > 0.0) ? -ra.theta : 0.0);
+          const double t1 = (nr && w1 < 0.0) ? ra.theta : ((nr && w1 > 0.0) ? -ra.theta : 0.0);
+          if (act) *reinterpret_cast<double2 *>(thp + ra.th) = make_double2(t0, t1);
           if (nr) {
-            v0 += w0 * (p0 ? ra.theta : (n0 ? -ra.theta : 0.0));
-            v1 += w1 * (p1 ? ra.theta : (n1 ? -ra.theta : 0.0));
+            v0 += w0 * t0;
+            v1 += w1 * t1;
           }
         }
       }
@@ -281,7 +280,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
         for (int j = (warp + NW - nA % NW) % NW; j < nB; j += NW) {
           const RecB r = Bv[j];
-          const int l = h1.w + j;
+          const int l = h1.w + j;  // internal branch id (outage lists)
           double b0 = r.b, b1 = r.b, F0 = r.F, F1v = r.F;
           bool o0 = false, o1 = false;
           if (flagged(l)) {
@@ -290,21 +289,17 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
             if (o0) b0 = F0 = 0.0;
             if (o1) b1 = F1v = 0.0;
           }
-          const uint4 cs = th[r.ts], ct = th[r.tt];
-          const double phi0 = b0 * (dec(cs.x, cs.y, lane, r.Ts, 0.0) - dec(ct.x, ct.y, lane, r.Tt, 0.0));
-          const double phi1 = b1 * (dec(cs.z, cs.w, lane, r.Ts, 0.0) - dec(ct.z, ct.w, lane, r.Tt, 0.0));
-          double* dst = reinterpret_cast<double *>(br_o + (size_t)l * BR);
+          const D2 ths = ld2(thp, r.ts), tht = ld2(thp, r.tt);
+          const double phi0 = b0 * (ths.x - tht.x);
+          const double phi1 = b1 * (ths.y - tht.y);
+          double* dst = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR);
           if (FORM == kFormF2) {
             const D2 nu = ld2(brp, r.row), ls = ld2(lamp, r.ls), lt = ld2(lamp, r.lt);
             const double q0 = nu.x - (ls.x - lt.x), q1 = nu.y - (ls.y - lt.y);
-            // f* = -F if q > 0, +F if q < 0, 0 on a tie; an outaged lane's code is the tie
-            const bool fn0 = act && !o0 && q0 > 0.0, fp0 = act && !o0 && q0 < 0.0;
-            const bool fn1 = act && !o1 && q1 > 0.0, fp1 = act && !o1 && q1 < 0.0;
-            const uint4 cw = make_uint4(__ballot_sync(0xffffffffu, fp0), __ballot_sync(0xffffffffu, fn0),
-                                        __ballot_sync(0xffffffffu, fp1), __ballot_sync(0xffffffffu, fn1));
-            if (lane == 0) fc[r.fs] = cw;
+            // f* = -F if q > 0, +F if q < 0, 0 on a tie (an outaged lane has F = 0)
             const double f0 = (q0 > 0.0) ? -F0 : ((q0 < 0.0) ? F0 : 0.0);
             const double f1 = (q1 > 0.0) ? -F1v : ((q1 < 0.0) ? F1v : 0.0);
+            if (act) *reinterpret_cast<double2 *>(fcp + r.fs) = make_double2(f0, f1);
             const double g0 = f0 - phi0, g1 = f1 - phi1;  // Kirchhoff residual
             v0 += q0 * f0;
             v1 += q1 * f1;
@@ -318,7 +313,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
             v0 += -(F0 * (mp.x + mm.x));
             v1 += -(F1v * (mp.y + mm.y));
             if (write && act) {
-              double* dst2 = reinterpret_cast<double *>(br_o + (size_t)l * BR + RB);
+              double* dst2 = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR + RB);
               if (EVAL) {
                 st2(dst, gp0, gp1);
                 st2(dst2, gm0, gm1);
@@ -369,10 +364,9 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
             const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y);
             for (int e = r.e0; e < r.e1; ++e) {
               const RecIC2 x = IC[e];
-              const uint4 cw = fc[x.fs];
-              const double z = x.sF * 0.0;  // signed zero of the tie: +0 at the to bus, -0 at the from bus
-              gl0 = gl0 + dec(cw.x, cw.y, lane, x.sF, z);  // +f* at to, -f* at from (sign folded)
-              gl1 = gl1 + dec(cw.z, cw.w, lane, x.sF, z);
+              const D2 f = ld2(fcp, x.f);
+              gl0 = gl0 + x.s * f.x;  // +f* at the to bus, -f* at the from bus ((-1)*f == -f exactly)
+              gl1 = gl1 + x.s * f.y;
             }
           } else {
             const RecIC1 *IC = reinterpret_cast<const RecIC1 *>(prog + h3.y);
@@ -383,20 +377,21 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
                 if (out_t(my_outs0, x.br)) sb0 = copysign(0.0, sb0);
                 if (out_t(my_outs1, x.br)) sb1 = copysign(0.0, sb1);
               }
-              const uint4 cs = th[x.ts], ct = th[x.tt];
-              gl0 = gl0 + sb0 * (dec(cs.x, cs.y, lane, x.Ts, 0.0) - dec(ct.x, ct.y, lane, x.Tt, 0.0));
-              gl1 = gl1 + sb1 * (dec(cs.z, cs.w, lane, x.Ts, 0.0) - dec(ct.z, ct.w, lane, x.Tt, 0.0));
+              const D2 ts = ld2(thp, x.ts), tt = ld2(thp, x.tt);
+              gl0 = gl0 + sb0 * (ts.x - tt.x);
+              gl1 = gl1 + sb1 * (ts.y - tt.y);
             }
           }
           v0 += -(li.x * di.x);
           v1 += -(li.y * di.y);
           if (write && act) {
-            double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.bus * RB);
+            double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.wpos * RB);
             if (EVAL) st2(dst, gl0, gl1);
             else st2(dst, step0 ? li.x + alpha * gl0 : li.x, step1 ? li.y + alpha * gl1 : li.y);
           }
         }
       }
+      }  // debug_mode
       named_bar(1, CT);
       if (threadIdx.x == 0) mbar_arrive(&empty[st]);
     }

@@ -53,7 +53,8 @@ class Info(ctypes.Structure):
                 ("smem_bytes", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
                 ("grid", ctypes.c_int32), ("launches_per_iter", ctypes.c_int32),
                 ("state_on_chip", ctypes.c_int32), ("chunk", ctypes.c_int32),
-                ("ring_bus", ctypes.c_int32), ("ring_branch", ctypes.c_int32), ("tile_width", ctypes.c_int32)]
+                ("ring_bus", ctypes.c_int32), ("ring_branch", ctypes.c_int32), ("tile_width", ctypes.c_int32),
+                ("copies_per_sweep", ctypes.c_int32), ("ring_life", ctypes.c_int32)]
 
 
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",

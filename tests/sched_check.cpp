@@ -31,7 +31,9 @@ int main(int argc, char **argv) {
   NetInternal &n = in.net;
   Schedule S;
   const int W = argc > 2 ? atoi(argv[2]) : 32;
+  if (argc > 3) S.ring_life = atoi(argv[3]);
   std::string err = build_schedule(n, CH, P, W, 8, &S);
+
   if (!err.empty()) { printf("ERR %s\n", err.c_str()); return 1; }
   const bool f1 = n.form == 1;
   std::vector<int> brp(S.n_br_slots, -1), lamp(S.n_lam_slots, -1), dp(S.n_d_slots, -1), th(S.n_th_slots, -1),
@@ -41,8 +43,13 @@ int main(int argc, char **argv) {
   auto issue = [&](int c) {
     if (c >= S.nsteps) return;
     for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
-      int x = S.ld_ent[e], kind = (int)((unsigned)x >> 30), ent = x & 0x3fffffff, slot = S.ld_slot[e];
-      (kind == LD_LAM ? lamp : kind == LD_D ? dp : brp)[slot] = ent;
+      const int4_t x = S.ld[e];
+      std::vector<int> &pool = x.a == LD_LAM ? lamp : x.a == LD_D ? dp : brp;
+      const std::vector<int> &perm = x.a == LD_LAM ? S.perm_lam : x.a == LD_D ? S.perm_d : S.perm_br;
+      for (int r = 0; r < x.c; ++r) {
+        if (x.d + r >= (int)pool.size()) { printf("BAD slot range\n"); ++bad; continue; }
+        pool[x.d + r] = perm[x.b + r];
+      }
     }
   };
   auto want = [&](std::vector<int> &pool, int slot, int ent, const char *what, int c) {
@@ -56,17 +63,17 @@ int main(int argc, char **argv) {
   for (int c = 0; c < S.nsteps; ++c) {
     long bytes = S.prog_bytes[c];
     for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
-      int kind = (int)((unsigned)S.ld_ent[e] >> 30);
-      if (kind != LD_LAM && kind != LD_D && kind != LD_BR) { printf("BAD kind %d\n", kind); ++bad; }
-      bytes += (kind == LD_BR) ? S.br_row_bytes : S.row_bytes;
+      const int4_t x = S.ld[e];
+      if (x.a != LD_LAM && x.a != LD_D && x.a != LD_BR) { printf("BAD kind %d\n", x.a); ++bad; }
+      bytes += (long)x.c * ((x.a == LD_BR) ? S.br_row_bytes : S.row_bytes);
     }
     if (bytes != S.tx_bytes[c] || S.prog_bytes[c] % 16 || S.prog_bytes[c] > S.max_prog_bytes) {
       printf("BAD tx chunk %d: %ld vs %d\n", c, bytes, S.tx_bytes[c]);
       ++bad;
     }
   }
-  for (int c = 0; c <= P; ++c) issue(c);
   const int RB = S.row_bytes, BR = S.br_row_bytes;
+  for (int c = 0; c <= P; ++c) issue(c);
   for (int c = 0; c < S.nsteps; ++c) {
     const uint8_t *pg = S.prog.data() + S.prog_off[c];
     const int *h = reinterpret_cast<const int *>(pg);
@@ -78,8 +85,8 @@ int main(int argc, char **argv) {
     const RecIC2 *IC2 = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
     const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
     // the step's code writes land first (worst case for the concurrent readers)
-    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th] = h[PH_A0] + j;
-    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs] = h[PH_B0] + j;
+    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th / RB] = h[PH_A0] + j;
+    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs / RB] = h[PH_B0] + j;
     // A(c)
     for (int j = 0; j < h[PH_NA]; ++j) {
       int bus = h[PH_A0] + j;
@@ -103,9 +110,10 @@ int main(int argc, char **argv) {
     for (int j = 0; j < h[PH_NB]; ++j) {
       int l = h[PH_B0] + j;
       seenB[l]++;
+      if (S.perm_br[Bv[j].wpos] != l) { printf("BAD B wpos\n"); ++bad; }
       want(brp, Bv[j].row / BR, l, "B br", c);
-      want(th, Bv[j].ts, n.bs[l], "B th_s", c);
-      want(th, Bv[j].tt, n.bt[l], "B th_t", c);
+      want(th, Bv[j].ts / RB, n.bs[l], "B th_s", c);
+      want(th, Bv[j].tt / RB, n.bt[l], "B th_t", c);
       if (!f1) {
         want(lamp, Bv[j].ls / RB, n.bs[l], "B lam_s", c);
         want(lamp, Bv[j].lt / RB, n.bt[l], "B lam_t", c);
@@ -113,7 +121,7 @@ int main(int argc, char **argv) {
     }
     // C(c-2)
     for (int j = 0; j < h[PH_NC]; ++j) {
-      int bus = Cv[j].bus;
+      int bus = S.perm_lam[Cv[j].wpos];
       seenC[bus]++;
       want(lamp, Cv[j].ls / RB, bus, "C lam", c);
       want(dp, Cv[j].ds / RB, bus, "C d", c);
@@ -123,20 +131,27 @@ int main(int argc, char **argv) {
         const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
         if ((f1 ? IC1[e].br : IC2[e].br) != l) { printf("BAD C order\n"); ++bad; }
         if (!f1) {
-          want(fc, IC2[e].fs, l, "C f", c);
-          if (IC2[e].sF != (to ? n.F[l] : -n.F[l])) { printf("BAD C sign\n"); ++bad; }
+          want(fc, IC2[e].f / RB, l, "C f", c);
+          if (IC2[e].s != (to ? 1.0 : -1.0)) { printf("BAD C sign\n"); ++bad; }
         } else {
-          want(th, IC1[e].ts, n.bs[l], "C th_s", c);
-          want(th, IC1[e].tt, n.bt[l], "C th_t", c);
+          want(th, IC1[e].ts / RB, n.bs[l], "C th_s", c);
+          want(th, IC1[e].tt / RB, n.bt[l], "C th_t", c);
           if (IC1[e].sb != (to ? n.b[l] : -n.b[l])) { printf("BAD C sign\n"); ++bad; }
         }
       }
     }
     issue(c + P + 1);
   }
+  if (getenv("DUMP_ROWS")) {
+    for (int st = 0; st < S.nsteps; ++st)
+      for (int e = S.ld_ptr[st]; e < S.ld_ptr[st + 1]; ++e) {
+        const int4_t x = S.ld[e];
+        fprintf(stderr, "L %d %d %d %d\n", x.a, x.b, x.c, st);
+      }
+  }
   for (int i = 0; i < n.nb; ++i) if (seenA[i] != 1 || seenC[i] != 1) { printf("BAD cover bus %d\n", i); ++bad; break; }
   for (int l = 0; l < n.nl; ++l) if (seenB[l] != 1) { printf("BAD cover br %d\n", l); ++bad; break; }
-  printf("chunks %d slots br %d lam %d d %d th %d f %d smem %d bad %d\n", S.nch, S.n_br_slots, S.n_lam_slots,
-         S.n_d_slots, S.n_th_slots, S.n_f_slots, S.total, bad);
+  printf("chunks %d slots br %d lam %d d %d th %d f %d smem %d copies %d sticky %d bad %d\n", S.nch, S.n_br_slots,
+         S.n_lam_slots, S.n_d_slots, S.n_th_slots, S.n_f_slots, S.total, S.n_copies, S.n_sticky_copies, bad);
   return bad ? 1 : 0;
 }

@@ -24,19 +24,19 @@ def checker():
     return EXE
 
 
-def run(checker, net, form, CH, P, order="dfs", W=32):
+def run(checker, net, form, CH, P, order="dfs", W=32, life=4):
     lines = [f"{net.n_bus} {net.n_branch} {net.ref_bus} {form} {CH} {P}"]
     lines += [f"{a} {b}" for a, b in zip(net.br_from, net.br_to)]
-    res = subprocess.run([checker, order, str(W)], input="\n".join(lines) + "\n", capture_output=True, text=True)
+    res = subprocess.run([checker, order, str(W), str(life)], input="\n".join(lines) + "\n", capture_output=True, text=True)
     return res.returncode, res.stdout
 
 
 @pytest.mark.parametrize("config", [0, 1, 3])
 @pytest.mark.parametrize("form", [0, 1])
-@pytest.mark.parametrize("CH,P,W", [(32, 2, 56), (8, 1, 2), (64, 3, 64)])
-def test_schedule_slots_valid(checker, config, form, CH, P, W):
+@pytest.mark.parametrize("CH,P,W,life", [(32, 2, 56, 4), (8, 1, 2, 0), (64, 3, 64, 6), (16, 2, 56, 2)])
+def test_schedule_slots_valid(checker, config, form, CH, P, W, life):
     net = inst.make_network(config)
-    rc, out = run(checker, net, form, CH, P, W=W)
+    rc, out = run(checker, net, form, CH, P, W=W, life=life)
     assert rc == 0, out
 
 
@@ -49,20 +49,23 @@ def test_schedule_random_small(checker, seed):
     if net is None:
         return
     for form in (0, 1):
-        for CH, P in ((1, 1), (3, 2), (16, 1)):
-            rc, out = run(checker, net, form, CH, P)
+        for CH, P, life in ((1, 1, 0), (3, 2, 2), (16, 1, 6)):
+            rc, out = run(checker, net, form, CH, P, life=life)
             assert rc == 0, out
-            rc, out = run(checker, net, form, CH, P, order="rcm")
+            rc, out = run(checker, net, form, CH, P, order="rcm", life=life)
             assert rc == 0, out
 
 
 def test_dfs_order_keeps_smem_small(checker):
     """The DFS tree order is what makes the window fit: config-3 network with
     56-instance tiles (the config-4 bench tiling) fits one CTA's shared memory
-    at CH=16 for both forms; with RCM order it does not come close."""
+    (F2 at CH=16, F1 at CH=8, ring life 2) with ~10x fewer bulk copies than
+    rows; with RCM order it does not come close."""
     net = inst.make_network(3)
-    for form in (0, 1):
-        rc, out = run(checker, net, form, 16, 2, W=56)
-        assert rc == 0 and int(out.split("smem ")[1].split()[0]) <= 220 * 1024, out
-    rc, out = run(checker, net, 0, 16, 2, order="rcm", W=56)
+    for form, ch in ((0, 16), (1, 8)):
+        rc, out = run(checker, net, form, ch, 2, W=56, life=2)
+        smem = int(out.split("smem ")[1].split()[0])
+        copies = int(out.split("copies ")[1].split()[0])
+        assert rc == 0 and smem <= 220 * 1024 and copies * 5 < net.n_bus * 2 + net.n_branch, out
+    rc, out = run(checker, net, 0, 16, 2, order="rcm", W=56, life=2)
     assert int(out.split("smem ")[1].split()[0]) > 227 * 1024, out
