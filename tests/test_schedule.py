@@ -62,10 +62,10 @@ def test_dfs_order_keeps_smem_small(checker):
     (F2 at CH=16, F1 at CH=8, ring life 2) with ~10x fewer bulk copies than
     rows; with RCM order it does not come close."""
     net = inst.make_network(3)
-    for form, ch in ((0, 16), (1, 8)):
+    for form, ch, factor in ((0, 16, 8), (1, 8, 3)):
         rc, out = run(checker, net, form, ch, 2, W=56, life=2)
         smem = int(out.split("smem ")[1].split()[0])
         copies = int(out.split("copies ")[1].split()[0])
-        assert rc == 0 and smem <= 220 * 1024 and copies * 5 < net.n_bus * 2 + net.n_branch, out
+        assert rc == 0 and smem <= 220 * 1024 and copies * factor < net.n_bus * 2 + net.n_branch, out
     rc, out = run(checker, net, 0, 16, 2, order="rcm", W=56, life=2)
     assert int(out.split("smem ")[1].split()[0]) > 227 * 1024, out
