@@ -4,13 +4,13 @@ on B200, in dual-ascent instance-iterations per second (BASELINE.json metric).
 
 Default workload = BASELINE.json configs[4]: the 10000-bus / 12700-branch /
 2500-generator network, 8192 load-scenario / line-switching instances, linear
-cost, form F2, sharded contiguously over the ranks (weak-per-instance, fixed
-total batch => "scaling": "strong" over the batch... see --scaling note below).
+cost, form F2, sharded contiguously over the ranks (fixed total batch:
+"scaling": "strong").
 
-A "step" is one ascent iteration (S1-S4) over the rank's whole batch = one
-launch of the batched kernel.  The timed region is one dcopf_dual_iterate(K)
-call: K step launches plus the final evaluation launch at y_K (counted as
-work-free overhead, i.e. the reported rate is conservative).
+A "step" is one ascent iteration (S1-S4) over the rank's whole batch.  The
+timed region is one dcopf_dual_iterate(K) call = ONE persistent kernel launch
+running the K iterations plus the final evaluation at y_K (the evaluation is
+not counted as work, so the reported rate is conservative).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload config4|config4b|config0|config1|config2|config3|config3q]
@@ -37,6 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_2406_13191_b200 import instances as inst  # noqa: E402
+from paper_2406_13191_b200.distributed import gather_instance_results, shard  # noqa: E402
 
 WORKLOADS = {
     # name: (config, quadratic, batch)
@@ -125,13 +126,6 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
-
-
-def shard(B, rank, world):
-    """Contiguous shard of [0, B) for `rank` (sizes differ by at most 1)."""
-    base, rem = divmod(B, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
 
 
 def make_inputs(workload, lo, hi):
@@ -267,17 +261,12 @@ def main():
     h.get_bound(bound, best, status, stream=stream)
     gather_ms = None
     if world > 1 and B_total > 1:
-        res = torch.stack([bound, best, status.to(torch.float64)])
-        sizes = [shard(B_total, r, world) for r in range(world)]
-        maxB = max(b - a for a, b in sizes)
-        pad = torch.full((3, maxB), float("nan"), dtype=torch.float64, device=dev)
-        pad[:, :B] = res
-        out = torch.empty((world, 3, maxB), dtype=torch.float64, device=dev)
         torch.cuda.synchronize()
         g0 = time.perf_counter()
-        tdist.all_gather_into_tensor(out, pad)
+        gathered = gather_instance_results([bound, best, status], B_total)  # NCCL, once, off the hot loop
         torch.cuda.synchronize()
         gather_ms = 1e3 * (time.perf_counter() - g0)
+        assert gathered.shape == (3, B_total)
 
     # ---- end-to-end through the public API with host buffers -----------------
     e2e = None
@@ -309,14 +298,17 @@ def main():
         peak, peak_src = peaks()
         inst_it = B_total * K
         value = inst_it / (ms_max / 1e3)
-        per_gpu_bytes = info.alg_bytes_per_inst_iter * B * K
+        # algorithmic HBM bytes of the timed launch: K iterations (read + write
+        # the multipliers, read the loads) + the final evaluation (reads only)
+        eval_read = 8 * (2 * net.n_bus + net.n_branch * (1 if form == dual.FORM_F2 else 2))
+        per_gpu_bytes = B * (info.alg_bytes_per_inst_iter * K + (eval_read if path == dual.PATH_BATCHED else 0))
         achieved = per_gpu_bytes / (ms / 1e3) / 1e9  # GB/s on this rank's kernel launches
-        traffic = None
+        traffic = None  # DRAM bytes per launch, from the committed ncu capture (scaled to this launch)
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
             ent = prof.get(f"{args.workload}/{args.form}")
-            if ent and ent.get("dram_bytes_per_launch"):
-                traffic = ent["dram_bytes_per_launch"]
+            if ent and ent.get("dram_over_alg"):
+                traffic = ent["dram_over_alg"] * per_gpu_bytes
         except Exception:
             pass
         cpu = None
