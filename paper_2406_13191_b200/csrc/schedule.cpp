@@ -495,7 +495,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
       }
     }
     std::vector<uint8_t> blk(kProgHeaderBytes, 0);
-    int32_t hd[16] = {0};
+    int32_t hd[PH_COUNT] = {0};
     auto app = [&](const void *p, size_t n) {
       size_t off = (blk.size() + 15) & ~size_t(15);
       blk.resize(off + n);
@@ -510,6 +510,10 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     hd[PH_NG] = (int)G.size();
     hd[PH_A0] = a0;
     hd[PH_B0] = b0;
+    // items are dealt round-robin to the nw consumer warps in the order A, B, C:
+    // warp w starts B at (w - nA) mod nw and C at (w - nA - nB) mod nw
+    hd[PH_ROT_B] = (nw - (int)A.size() % nw) % nw;
+    hd[PH_ROT_C] = (nw - ((int)A.size() + (int)Bv.size()) % nw) % nw;
     hd[PH_OFF_A] = app(A.data(), A.size() * sizeof(RecA));
     hd[PH_OFF_IA] = f1 ? app(IA1.data(), IA1.size() * sizeof(RecIA1)) : app(IA2.data(), IA2.size() * sizeof(RecIA2));
     hd[PH_OFF_B] = app(Bv.data(), Bv.size() * sizeof(RecB));

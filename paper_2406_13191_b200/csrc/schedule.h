@@ -30,9 +30,10 @@ namespace dcopf {
 enum ProgHeader {
   PH_NA = 0, PH_NIA, PH_NB, PH_NC, PH_NIC, PH_NG, PH_A0, PH_B0,
   PH_OFF_A, PH_OFF_IA, PH_OFF_B, PH_OFF_C, PH_OFF_G, PH_OFF_IC, PH_BYTES, PH_PAD,
+  PH_ROT_B, PH_ROT_C, PH_PAD2, PH_PAD3,  // first B / C item index of warp 0 (round-robin over all items)
   PH_COUNT
 };
-constexpr int kProgHeaderBytes = 64;
+constexpr int kProgHeaderBytes = 80;
 
 // All row / value fields are byte offsets into their shared-memory pool; the
 // minimiser values theta*_i and f*_l are kept per instance (one W-wide row).

@@ -155,6 +155,9 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
   if (warp == NW) {
     // =========================== producer ===========================
     const int RB = a.row_bytes, BR = a.br_row_bytes;
+    int pst = 0;           // stage of the next step
+    unsigned pph = 0;      // its use parity
+    bool pused = false;    // every stage used at least once
     for (long k = 0; k <= K; ++k) {
       if (k > 0) named_bar(2, (NW + 1) * 32);  // sweep k-1 written and fenced
       const int par = (a.cur + (int)(k & 1)) & 1;
@@ -162,10 +165,14 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
       const uint8_t *br_src = reinterpret_cast<const uint8_t *>(par ? a.br1 : a.br0) + tile * (size_t)a.n_br * BR;
       const uint8_t *d_src = reinterpret_cast<const uint8_t *>(a.d) + tile * (size_t)a.n_bus * RB;
       for (int c = 0; c < nst; ++c) {
-        const long g = k * nst + c;
-        const int st = (int)(g % S);
-        const long u = g / S;
-        if (u > 0) mbar_wait(&empty[st], (unsigned)((u - 1) & 1));
+        const int st = pst;
+        const unsigned pu = pph;  // parity of this use of stage st
+        if (++pst == S) {
+          pst = 0;
+          pph ^= 1u;
+        }
+        if (pused) mbar_wait(&empty[st], pu ^ 1u);  // previous use of the stage released
+        if (pst == 0) pused = true;
         if (lane == 0) {
           mbar_arrive_expect_tx(&full[st], (unsigned)(a.debug_mode == 2 ? a.prog_bytes[c] : a.tx_bytes[c]));
           tma_load_1d(smem + a.off_prog + st * a.prog_stride, a.prog + a.prog_off[c], (unsigned)a.prog_bytes[c],
@@ -204,6 +211,8 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
     for (int j = 0; j < nout; ++j) r |= (lst[j] == l);
     return r;
   };
+  int cst = 0;         // stage of the next step
+  unsigned cph = 0;    // parity of its full barrier
   double best0 = 0.0, best1 = 0.0;
   if (!EVAL && warp == 0 && act) {
     best0 = a.best[ib + 2 * lane];
@@ -223,14 +232,18 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
     double v0 = 0.0, v1 = 0.0;
 
     for (int c = 0; c < nst; ++c) {
-      const long g = k * nst + c;
-      const int st = (int)(g % S);
-      mbar_wait(&full[st], (unsigned)((g / S) & 1));
+      const int st = cst;
+      mbar_wait(&full[st], cph);
+      if (++cst == S) {
+        cst = 0;
+        cph ^= 1u;
+      }
       const uint8_t *prog = smem + a.off_prog + st * a.prog_stride;
       const int4 h0 = *reinterpret_cast<const int4 *>(prog);       // nA nIA nB nC
       const int4 h1 = *reinterpret_cast<const int4 *>(prog + 16);  // nIC nG a0 b0
       const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);  // offA offIA offB offC
-      const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC
+      const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC bytes -
+      const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // rotB rotC
       const int nA = h0.x, nB = h0.z, nC = h0.w;
 
       if (a.debug_mode != 1) {
@@ -278,7 +291,9 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
       // ---------------- B(s-1): branches ----------------
       {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
-        for (int j = (warp + NW - nA % NW) % NW; j < nB; j += NW) {
+        int jb = warp + h4.x;
+        if (jb >= NW) jb -= NW;
+        for (int j = jb; j < nB; j += NW) {
           const RecB r = Bv[j];
           const int l = h1.w + j;  // internal branch id (outage lists)
           double b0 = r.b, b1 = r.b, F0 = r.F, F1v = r.F;
@@ -342,7 +357,9 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
       {
         const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
         const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
-        for (int j = (warp + 2 * NW - (nA + nB) % NW) % NW; j < nC; j += NW) {
+        int jc = warp + h4.y;
+        if (jc >= NW) jc -= NW;
+        for (int j = jc; j < nC; j += NW) {
           const RecC r = Cv[j];
           const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
           double gl0 = -di.x, gl1 = -di.y;
