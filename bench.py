@@ -217,7 +217,13 @@ def main():
     path = dual.PATH_BATCHED if B_total > 1 else dual.PATH_SINGLE
     path = {"auto": path, "batched": dual.PATH_BATCHED, "single": dual.PATH_SINGLE}[args.path]
 
-    h = dual.DcopfDual(net, form=form, device=local, path=path)
+    # config 4 takes branches out among the non-tree ones only: declaring that
+    # lets the library skip the outage test on the (never switched) tree
+    sw = None
+    if config == 4:
+        sw = np.zeros(net.n_branch, np.uint8)
+        sw[net.n_tree:] = 1
+    h = dual.DcopfDual(net, form=form, device=local, path=path, switchable=sw)
     stream = torch.cuda.current_stream(dev)
     load_dev = torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev)
     outs_dev = None if batch.outages is None else torch.from_numpy(batch.outages).to(dev)

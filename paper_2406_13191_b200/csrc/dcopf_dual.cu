@@ -590,7 +590,8 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   Internalized in;
   const std::string ierr = internalize(nb, nl, ng, net->ref_bus, fr.data(), to.data(), net->br_b, net->br_fmax,
                                        theta.data(), net->gen_bus, net->gen_pmin, net->gen_pmax, net->gen_c,
-                                       net->gen_a, h->form, ord && std::string(ord) == "rcm", &in);
+                                       net->gen_a, net->br_switchable, h->form, ord && std::string(ord) == "rcm",
+                                       &in);
   if (!ierr.empty()) {
     delete h;
     return fail(nullptr, DCOPF_EINVAL, "%s", ierr.c_str());

@@ -106,8 +106,8 @@ std::vector<int> rcm_order(int n, const std::vector<std::vector<int>> &adj) {
 
 std::string internalize(int nb, int nl, int ng, int ref, const int *fr, const int *to, const double *b,
                         const double *F, const double *theta, const int *gen_bus, const double *pmin,
-                        const double *pmax, const double *c, const double *a, int form, bool rcm,
-                        Internalized *out) {
+                        const double *pmax, const double *c, const double *a, const uint8_t *switchable,
+                        int form, bool rcm, Internalized *out) {
   Internalized &R = *out;
   std::vector<std::vector<int>> adj(nb);
   for (int l = 0; l < nl; ++l) {
@@ -171,9 +171,10 @@ std::string internalize(int nb, int nl, int ng, int ref, const int *fr, const in
   }
   N.theta.resize(nb);
   for (int i = 0; i < nb; ++i) N.theta[i] = theta[R.bus_perm[i]];
-  N.bs.resize(nl); N.bt.resize(nl); N.b.resize(nl); N.F.resize(nl);
+  N.bs.resize(nl); N.bt.resize(nl); N.b.resize(nl); N.F.resize(nl); N.sw.resize(nl);
   for (int li = 0; li < nl; ++li) {
     int l = R.br_perm[li];
+    N.sw[li] = switchable ? (switchable[l] != 0) : 1;
     N.bs[li] = R.bus_inv[fr[l]];
     N.bt[li] = R.bus_inv[to[l]];
     N.b[li] = b[l];
@@ -424,7 +425,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
           } else {
             RecIA1 x{};
             x.row = br_slot[l] * BR;
-            x.br = l;
+            x.br = net.sw.empty() || net.sw[l] ? l : -1;
             x.ls = lam_slot[net.bs[l]] * RB;
             x.lt = lam_slot[net.bt[l]] * RB;
             x.sb = to ? -net.b[l] : net.b[l];  // w_s += u ; w_t -= u
@@ -444,6 +445,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
         RecB r{};
         r.row = br_slot[l] * BR;
         r.wpos = S.pos_br[l];
+        r.obr = net.sw.empty() || net.sw[l] ? l : -1;
         r.ts = th_slot[s] * RB;
         r.tt = th_slot[t] * RB;
         r.b = net.b[l];
@@ -485,7 +487,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
             RecIC1 x{};
             x.ts = th_slot[net.bs[l]] * RB;
             x.tt = th_slot[net.bt[l]] * RB;
-            x.br = l;
+            x.br = net.sw.empty() || net.sw[l] ? l : -1;
             x.sb = to ? net.b[l] : -net.b[l];  // +phi at the to bus, -phi at the from bus
             IC1.push_back(x);
           }

@@ -39,12 +39,13 @@ constexpr int kProgHeaderBytes = 80;
 // minimiser values theta*_i and f*_l are kept per instance (one W-wide row).
 struct alignas(16) RecA { int e0, e1, th, pad; double theta, pad2; };   // bus of phase A
 struct alignas(16) RecIA2 { int row, br; double sb; };                   // F2: sb = to ? b : -b
-struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };      // F1: sb = to ? -b : b
-struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, wpos, pad1; double b, F; };  // branch of phase B (wpos: nu' row)
+struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };      // F1: sb = to ? -b : b (br -1: never out)
+struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, wpos, obr; double b, F; };  // branch of phase B (wpos: nu' row;
+                                                                                      // obr: id if switchable, else -1)
 struct alignas(16) RecC { int wpos, ls, ds, g0, g1, e0, e1, pad; };     // bus of phase C (wpos: lambda' row)
 struct alignas(16) RecG { double c, lo, hi, a; };                         // generator
 struct alignas(16) RecIC2 { int f, br; double s; };                      // F2: s = to ? +1 : -1
-struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, pad2; };     // F1: sb = to ? b : -b
+struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, pad2; };     // F1: sb = to ? b : -b (br -1: never out)
 
 // load-list entry kinds (top 2 bits of the packed entity word)
 enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
@@ -54,6 +55,7 @@ struct NetInternal {
   std::vector<int> bus_ptr, bus_inc;        // CSR, entries (l << 1) | is_to, ascending original id
   std::vector<int> bs, bt;                  // branch endpoints
   std::vector<double> b, F, theta;          // per branch / per bus
+  std::vector<uint8_t> sw;                  // per branch: 1 if an instance may take it out
   std::vector<int> gen_ptr;                 // per bus
   std::vector<double> gc, glo, ghi, ga;     // per generator (grouped by bus)
 };
@@ -98,8 +100,8 @@ std::vector<int> rcm_order(int n, const std::vector<std::vector<int>> &adj);
 // theta is indexed by ORIGINAL bus id.
 std::string internalize(int nb, int nl, int ng, int ref, const int *fr, const int *to, const double *b,
                         const double *F, const double *theta, const int *gen_bus, const double *pmin,
-                        const double *pmax, const double *c, const double *a, int form, bool rcm,
-                        Internalized *out);
+                        const double *pmax, const double *c, const double *a, const uint8_t *switchable,
+                        int form, bool rcm, Internalized *out);
 
 // Bus order: DFS preorder of a BFS spanning tree rooted at `root`, children
 // visited smallest subtree first (keeps the live re-read window small).

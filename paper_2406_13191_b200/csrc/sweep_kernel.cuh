@@ -36,6 +36,8 @@
 // Per-entity arithmetic and operation order match dual_kernels.cuh and the
 // oracle (reading A-19); only the dual value is summed in another fixed order.
 #pragma once
+#include <type_traits>
+
 #include "dual_kernels.cuh"
 #include "schedule.h"
 
@@ -231,6 +233,10 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
     const double alpha = (EVAL || last) ? 0.0 : a.alpha[k];
     double v0 = 0.0, v1 = 0.0;
 
+    // the step loop, instantiated twice: CHK = some instance of the tile is
+    // frozen (diverged) and its state must be carried over unchanged
+    auto run_steps = [&](auto chk_tag) {
+    constexpr bool CHK = decltype(chk_tag)::value;
     for (int c = 0; c < nst; ++c) {
       const int st = cst;
       mbar_wait(&full[st], cph);
@@ -267,7 +273,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
             for (int e = ra.e0; e < ra.e1; ++e) {
               const RecIA1 r = IA[e];
               double sb0 = r.sb, sb1 = r.sb;
-              if (flagged(r.br)) {
+              if (r.br >= 0 && flagged(r.br)) {  // br < 0: branch never taken out
                 if (out_t(my_outs0, r.br)) sb0 = copysign(0.0, sb0);
                 if (out_t(my_outs1, r.br)) sb1 = copysign(0.0, sb1);
               }
@@ -298,9 +304,9 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
           const int l = h1.w + j;  // internal branch id (outage lists)
           double b0 = r.b, b1 = r.b, F0 = r.F, F1v = r.F;
           bool o0 = false, o1 = false;
-          if (flagged(l)) {
-            o0 = out_t(my_outs0, l);
-            o1 = out_t(my_outs1, l);
+          if (r.obr >= 0 && flagged(r.obr)) {  // obr < 0: branch never taken out
+            o0 = out_t(my_outs0, r.obr);
+            o1 = out_t(my_outs1, r.obr);
             if (o0) b0 = F0 = 0.0;
             if (o1) b1 = F1v = 0.0;
           }
@@ -320,7 +326,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
             v1 += q1 * f1;
             if (write && act) {
               if (EVAL) st2(dst, g0, g1);
-              else st2(dst, step0 ? nu.x + alpha * g0 : nu.x, step1 ? nu.y + alpha * g1 : nu.y);
+              else st2(dst, (!CHK || step0) ? nu.x + alpha * g0 : nu.x, (!CHK || step1) ? nu.y + alpha * g1 : nu.y);
             }
           } else {
             const D2 mp = ld2(brp, r.row), mm = ld2(brp, r.row + RB);
@@ -334,13 +340,13 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
                 st2(dst2, gm0, gm1);
               } else {
                 double p0 = mp.x, m0 = mm.x, p1 = mp.y, m1 = mm.y;
-                if (step0) {
+                if (!CHK || step0) {
                   p0 = mp.x + alpha * gp0;
                   m0 = mm.x + alpha * gm0;
                   p0 = (p0 > 0.0) ? p0 : 0.0;  // mu <- max(mu, 0)
                   m0 = (m0 > 0.0) ? m0 : 0.0;
                 }
-                if (step1) {
+                if (!CHK || step1) {
                   p1 = mp.y + alpha * gp1;
                   m1 = mm.y + alpha * gm1;
                   p1 = (p1 > 0.0) ? p1 : 0.0;
@@ -390,7 +396,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
             for (int e = r.e0; e < r.e1; ++e) {
               const RecIC1 x = IC[e];
               double sb0 = x.sb, sb1 = x.sb;
-              if (flagged(x.br)) {
+              if (x.br >= 0 && flagged(x.br)) {
                 if (out_t(my_outs0, x.br)) sb0 = copysign(0.0, sb0);
                 if (out_t(my_outs1, x.br)) sb1 = copysign(0.0, sb1);
               }
@@ -404,7 +410,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
           if (write && act) {
             double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.wpos * RB);
             if (EVAL) st2(dst, gl0, gl1);
-            else st2(dst, step0 ? li.x + alpha * gl0 : li.x, step1 ? li.y + alpha * gl1 : li.y);
+            else st2(dst, (!CHK || step0) ? li.x + alpha * gl0 : li.x, (!CHK || step1) ? li.y + alpha * gl1 : li.y);
           }
         }
       }
@@ -412,6 +418,10 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
       named_bar(1, CT);
       if (threadIdx.x == 0) mbar_arrive(&empty[st]);
     }
+    };
+    const bool anyf = __any_sync(0xffffffffu, (frz[2 * lane] | frz[2 * lane + 1]) != 0);
+    if (anyf) run_steps(std::integral_constant<bool, true>{});
+    else run_steps(std::integral_constant<bool, false>{});
     // ---------------- dual value, best, status ----------------
     red[warp * 64 + 2 * lane] = v0;
     red[warp * 64 + 2 * lane + 1] = v1;

@@ -20,13 +20,13 @@ def cost_scale(net):
 
 
 def run_gpu(net, loads, outages=None, K=0, alpha=None, form=0, path=dual.PATH_AUTO, history=False,
-            lam0=None, br0=None, implied_theta=False):
+            lam0=None, br0=None, implied_theta=False, switchable=None):
     """loads [B][n_bus] (instance-major, like the oracle); returns instance-major results."""
     import torch
     dev = torch.device("cuda:0")
     loads = np.atleast_2d(loads)
     B = loads.shape[0]
-    h = dual.DcopfDual(net, form=form, path=path, implied_theta=implied_theta)
+    h = dual.DcopfDual(net, form=form, path=path, implied_theta=implied_theta, switchable=switchable)
     ld = torch.from_numpy(np.ascontiguousarray(loads.T)).to(dev)
     out = None if outages is None else torch.from_numpy(np.ascontiguousarray(outages, dtype=np.int32)).to(dev)
     h.set_instance_batch(ld, out)
@@ -50,6 +50,13 @@ def run_gpu(net, loads, outages=None, K=0, alpha=None, form=0, path=dual.PATH_AU
                hist=None if hist is None else hist.cpu().numpy().T.copy(), info=h.info())
     h.close()
     return res
+
+
+def non_tree_switchable(net):
+    """config 4: only non-tree branches are ever taken out"""
+    sw = np.zeros(net.n_branch, np.uint8)
+    sw[net.n_tree:] = 1
+    return sw
 
 
 def assert_parity(net, gpu, orc, idx=None, check_hist=True, bitwise_multipliers=False):

@@ -26,7 +26,7 @@ int main(int argc, char **argv) {
   Internalized in;
   bool rcm = argc > 1 && std::string(argv[1]) == "rcm";
   std::string e0 = internalize(nb, nl, 0, ref, fr.data(), to.data(), b.data(), F.data(), theta.data(), nullptr,
-                               nullptr, nullptr, nullptr, nullptr, form, rcm, &in);
+                               nullptr, nullptr, nullptr, nullptr, nullptr, form, rcm, &in);
   if (!e0.empty()) { printf("ERR %s\n", e0.c_str()); return 1; }
   NetInternal &n = in.net;
   Schedule S;
@@ -96,7 +96,7 @@ int main(int argc, char **argv) {
       for (int e = A[j].e0; e < A[j].e1; ++e) {
         const int k = n.bus_ptr[bus] + e - A[j].e0;
         const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
-        const int br = f1 ? IA1[e].br : IA2[e].br;
+        const int br = f1 ? (IA1[e].br < 0 ? l : IA1[e].br) : IA2[e].br;
         const double sb = f1 ? IA1[e].sb : IA2[e].sb;
         if (br != l) { printf("BAD A order\n"); ++bad; }
         if (sb != ((to ^ (int)f1) ? n.b[l] : -n.b[l])) { printf("BAD A sign\n"); ++bad; }
@@ -129,7 +129,7 @@ int main(int argc, char **argv) {
       for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
         const int k = n.bus_ptr[bus] + e - Cv[j].e0;
         const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
-        if ((f1 ? IC1[e].br : IC2[e].br) != l) { printf("BAD C order\n"); ++bad; }
+        if ((f1 ? (IC1[e].br < 0 ? l : IC1[e].br) : IC2[e].br) != l) { printf("BAD C order\n"); ++bad; }
         if (!f1) {
           want(fc, IC2[e].f / RB, l, "C f", c);
           if (IC2[e].s != (to ? 1.0 : -1.0)) { printf("BAD C sign\n"); ++bad; }

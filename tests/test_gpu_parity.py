@@ -13,7 +13,7 @@ from oracle import FORM_F1, FORM_F2
 from paper_2406_13191_b200 import dual
 from paper_2406_13191_b200 import instances as inst
 
-from gpu_helpers import BOUND_RTOL, assert_parity, cost_scale, run_gpu
+from gpu_helpers import BOUND_RTOL, assert_parity, cost_scale, non_tree_switchable, run_gpu
 
 pytestmark = pytest.mark.gpu
 
@@ -120,7 +120,7 @@ def test_config4_full_batch_sampled():
     batch = inst.config4_batch(net, range(B))
     a = inst.alpha_schedule(K)
     gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=FORM_F2,
-                  path=dual.PATH_BATCHED)
+                  path=dual.PATH_BATCHED, switchable=non_tree_switchable(net))
     assert gpu["info"].grid * gpu["info"].tile_width >= B and gpu["info"].grid <= 148
     idx = np.array([0, 31, 4097, 8191])
     orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=FORM_F2,
@@ -136,8 +136,10 @@ def test_config4_cut_all_instances(form):
     a = inst.alpha_schedule(K)
     orc = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, history=True,
                        threads=8)
+    # with and without the switchable declaration (outage test on every branch)
+    sw = non_tree_switchable(net) if form == FORM_F2 else None
     gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, path=dual.PATH_BATCHED,
-                  history=True)
+                  history=True, switchable=sw)
     assert_parity(net, gpu, orc, bitwise_multipliers=True)
 
 
