@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--path", default="auto", choices=["auto", "batched", "single"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap run (the workload's full K)")
     return ap.parse_args()
 
 
@@ -157,6 +158,56 @@ def cpu_oracle_rate(net, batch, form, cores, target_s=12.0):
     oracle.solve(net, loads, outages=outs, K=K, alpha=inst.alpha_schedule(K), form=form, threads=cores)
     dt = time.perf_counter() - t0
     return n_inst * K / dt, f"{n_inst} instances x {K} iterations ({dt:.1f} s wall)"
+
+
+def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, dev, rel=1e-3):
+    import torch
+    import torch.distributed as tdist
+    key = f"{args.workload}/{args.form}"
+    try:
+        ref = json.load(open(os.path.join(ROOT, "tests", "golden", "targets.json")))[key]
+    except (OSError, KeyError):
+        return {"unavailable": f"no oracle reference for {key} (run tools/make_targets.py)"}
+    K = int(ref["K"])
+    ids = np.asarray(ref["instance_ids"], dtype=np.int64)
+    best_ref = np.asarray(ref["best"], dtype=np.float64)
+    B = batch.B
+    target = np.full(B, np.inf)
+    mine = (ids >= lo) & (ids < hi)
+    # within `rel` of the reference on the lower side: best >= ref - rel |ref|
+    target[ids[mine] - lo] = best_ref[mine] - rel * np.abs(best_ref[mine])
+    h.set_instance_batch(load_dev, outs_dev, stream=stream)
+    h.set_target(target, stream=stream)
+    alpha = inst.alpha_schedule(K, float(ref["alpha"]))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    h.iterate(K, alpha, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    run_s = e0.elapsed_time(e1) / 1e3
+    hit = h.get_first_hit()[ids[mine] - lo] if mine.any() else np.zeros(0, np.int64)
+    reached = int(np.sum(hit >= 0))
+    worst = int(hit.max()) if reached == len(hit) and len(hit) else -1
+    secs = run_s * worst / K if worst >= 0 else None
+    t = torch.tensor([run_s, secs if secs is not None else -1.0, reached, len(hit)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)
+        tsum = t.clone()
+        tdist.all_reduce(tsum, op=tdist.ReduceOp.SUM)
+        run_s, reached, n = float(tmax[0]), int(tsum[2]), int(tsum[3])
+        secs = float(tmax[1]) if reached == n and n else None
+    else:
+        n = len(hit)
+    out = {"rel_gap": rel, "K": K, "alpha": ref["alpha"], "reference": "oracle final running best at the same K "
+           "and schedule (tests/golden/targets.json)", "sampled_instances": n, "reached": reached,
+           "max_hit_iteration": worst if world == 1 else None, "seconds": secs, "run_seconds_full_K": run_s,
+           "reference_best_range": [float(best_ref.min()), float(best_ref.max())]}
+    opt = ref.get("primal_opt")
+    if opt is not None:
+        out["true_gap_at_K"] = ref.get("true_gap_at_K")
+    return out
 
 
 def run_reference(args):
@@ -274,6 +325,13 @@ def main():
         gather_ms = 1e3 * (time.perf_counter() - g0)
         assert gathered.shape == (3, B_total)
 
+    # ---- time to gap: the workload's full K once, with the
+    # oracle's final best (tests/golden/targets.json, tools/make_targets.py) as
+    # reference on the sampled instances; the hit iteration is recorded on device
+    ttg = None
+    if not args.no_gap:
+        ttg = time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, dev)
+
     # ---- end-to-end through the public API with host buffers -----------------
     e2e = None
     if not args.no_e2e:
@@ -346,6 +404,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src},
             "cpu_baseline": cpu,
+            "time_to_gap": ttg,
             "e2e": e2e,
             "gpu_launches": 1,
             "clocks": clk,

@@ -161,6 +161,22 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
 int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, double *grad_branch,
                         void *cuda_stream);
 
+/* Time to gap (BASELINE.json metric "time to 1e-3 gap"):
+ * per-instance thresholds target[B] (host or device; NULL clears them).  The
+ * kernels then record, per instance, the index k of the FIRST evaluation whose
+ * running best bound satisfies best_k >= target, counting the evaluations
+ * g(y_0), g(y_1), ... of every iterate() call since set_instance_batch()
+ * continuously (a call of K steps covers indices base .. base+K, base = the
+ * total number of steps taken before it; its first evaluation re-evaluates the
+ * point the previous call ended on).  Cleared (no target, hit = -1) by
+ * set_instance_batch().  The threshold is a caller-supplied number (e.g.
+ * (1 - 1e-3) x a reference bound); the library never computes one.
+ * Errors: EINVAL (a NaN target), ESTATE. */
+int dcopf_dual_set_target(dcopf_dual_t h, const double *target, void *cuda_stream);
+
+/* hit[B] (int64): the first evaluation index reaching the target, or -1. */
+int dcopf_dual_get_first_hit(dcopf_dual_t h, int64_t *hit, void *cuda_stream);
+
 /* Static facts about the handle, for reporting. */
 typedef struct {
   int64_t B;                      /* instances loaded (0 before set_instance_batch) */

@@ -31,7 +31,10 @@ using namespace dcopf;
 
 static thread_local std::string g_create_error;
 
-static const int kSweepWarps = 15;  // consumer warps of k_sweep (+1 producer warp = 16 warps, 4 per SMSP)
+#ifndef DCOPF_SWEEP_WARPS
+#define DCOPF_SWEEP_WARPS 19
+#endif
+static const int kSweepWarps = DCOPF_SWEEP_WARPS;  // consumer warps of k_sweep (+1 producer warp = 20 warps, 640 threads)
 
 struct dcopf_dual_s {
   std::string err;
@@ -52,6 +55,10 @@ struct dcopf_dual_s {
   double *lam[2] = {nullptr, nullptr}, *br[2] = {nullptr, nullptr}, *load = nullptr;
   double *bound = nullptr, *best = nullptr, *value = nullptr;
   int *status = nullptr, *outs = nullptr, *flag = nullptr;
+  double *target = nullptr;                           // time-to-gap thresholds [B_pad]
+  long long *hit = nullptr;                           // first evaluation index reaching them [B_pad]
+  bool has_target = false;
+  long k_base = 0;                                    // steps taken since set_instance_batch
   double *g_lam = nullptr, *g_br = nullptr;  // evaluate scratch (internal layout)
   double *scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -61,6 +68,7 @@ struct dcopf_dual_s {
   // compiled sweep schedule of the batched path (for tile width sched_W)
   Schedule sch;
   int sched_W = 0;
+  int soft_sync = 0;  // k_sweep step synchronisation (see sweep_kernel.cuh); DCOPF_SYNC=soft|hard
   uint8_t *d_prog = nullptr;
   long long *d_prog_off = nullptr;
   int *d_prog_bytes = nullptr, *d_tx_bytes = nullptr, *d_ld_ptr = nullptr, *d_ld = nullptr;
@@ -165,6 +173,10 @@ void free_batch(dcopf_dual_t h) {
   cudaFree(h->status);
   cudaFree(h->outs);
   h->status = h->outs = nullptr;
+  cudaFree(h->target);
+  cudaFree(h->hit);
+  h->target = nullptr;
+  h->hit = nullptr;
   h->B = h->B_pad = 0;
 }
 
@@ -275,6 +287,8 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
 // DCOPF_CHUNK (default 32) and halves until the kernel's shared memory fits.
 int compile_schedule(dcopf_dual_t h, int W) {
   if (h->sched_W == W) return DCOPF_OK;
+  h->soft_sync = 1;  // measured faster for both forms at 19 consumer warps
+  if (const char *e = getenv("DCOPF_SYNC")) h->soft_sync = std::string(e) == "soft";
   // search (chunk, ring life) from large to small until the kernel's shared
   // memory fits: larger chunks mean fewer steps, longer ring lives fewer copies
   int P = 2;
@@ -284,7 +298,7 @@ int compile_schedule(dcopf_dual_t h, int W) {
     const int life = getenv("DCOPF_RING_LIFE") ? atoi(getenv("DCOPF_RING_LIFE")) : 4;
     cands.push_back({std::max(1, atoi(e)), life});
   }
-  const int chs[] = {32, 16, 8, 4, 2, 1}, lifes[] = {6, 4, 2};
+  const int chs[] = {32, 24, 20, 16, 14, 12, 10, 8, 6, 4, 2, 1}, lifes[] = {6, 4, 2};
   for (int ch : chs)
     for (int life : lifes) cands.push_back({ch, life});
   Schedule sc;
@@ -292,6 +306,7 @@ int compile_schedule(dcopf_dual_t h, int W) {
   for (auto &cd : cands) {
     sc = Schedule();
     sc.ring_life = cd.second;
+    sc.pool_gap = h->soft_sync ? 2 : 1;  // soft sync: consumer warps drift by up to one step
     std::string err = build_schedule(h->ni, cd.first, P, W, kSweepWarps, &sc);
     if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
     if (sc.total <= h->dev_smem) {
@@ -339,10 +354,14 @@ int compile_schedule(dcopf_dual_t h, int W) {
   if (rc) return rc;
   std::vector<uint8_t>().swap(h->sch.prog);  // device copy only
   const int b = h->sch.total;
-  if (!rc) rc = set_smem(h, k_sweep<kFormF2, false, kSweepWarps>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF2, true, kSweepWarps>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF2, false, kSweepWarps, false>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF2, true, kSweepWarps, false>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps, false>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps, false>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF2, false, kSweepWarps, true>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF2, true, kSweepWarps, true>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps, true>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps, true>, b);
   if (!rc) h->sched_W = W;
   return rc;
 }
@@ -386,6 +405,9 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.best = h->best;
   a.status = h->status;
   a.B = h->B;
+  a.target = h->has_target ? h->target : nullptr;
+  a.hit = h->hit;
+  a.k_base = h->k_base;
   a.n_bus = h->n_bus;
   a.n_br = h->n_br;
   a.ref = h->ref_int;
@@ -413,6 +435,7 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.off_dp = sc.off_dp;
   a.off_th = sc.off_th;
   a.off_fc = sc.off_fc;
+  a.soft = h->soft_sync;
   if (const char *e = getenv("DCOPF_DEBUG_MODE")) a.debug_mode = atoi(e);  // measurement only
   return a;
 }
@@ -420,10 +443,14 @@ SweepArgs sweep_args(dcopf_dual_t h) {
 template <bool EVAL>
 int launch_sweep(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
   const unsigned grid = (unsigned)(h->B_pad / h->T), threads = (kSweepWarps + 1) * 32;
-  if (h->form == DCOPF_FORM_FLOW_BOX)
-    k_sweep<kFormF2, EVAL, kSweepWarps><<<grid, threads, h->sch.total, s>>>(a);
-  else
-    k_sweep<kFormF1, EVAL, kSweepWarps><<<grid, threads, h->sch.total, s>>>(a);
+  const size_t sm = h->sch.total;
+  if (h->form == DCOPF_FORM_FLOW_BOX) {
+    if (h->soft_sync) k_sweep<kFormF2, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);
+    else k_sweep<kFormF2, EVAL, kSweepWarps, false><<<grid, threads, sm, s>>>(a);
+  } else {
+    if (h->soft_sync) k_sweep<kFormF1, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);
+    else k_sweep<kFormF1, EVAL, kSweepWarps, false><<<grid, threads, sm, s>>>(a);
+  }
   CK(h, cudaGetLastError());
   return DCOPF_OK;
 }
@@ -440,6 +467,9 @@ SingleArgs single_args(dcopf_dual_t h) {
   a.best = h->best;
   a.status = h->status;
   a.B = h->B;
+  a.target = h->has_target ? h->target : nullptr;
+  a.hit = h->hit;
+  a.k_base = h->k_base;
   return a;
 }
 
@@ -707,7 +737,11 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
     CK(h, cudaMalloc(&h->value, B_pad * 8));
     CK(h, cudaMalloc(&h->status, B_pad * 4));
     CK(h, cudaMalloc(&h->outs, std::max<size_t>((size_t)B_pad * max_out, 1) * 4));
+    CK(h, cudaMalloc(&h->target, B_pad * 8));
+    CK(h, cudaMalloc(&h->hit, B_pad * 8));
   }
+  h->has_target = false;
+  h->k_base = 0;
   if (max_out > 0) {
     std::vector<int> padded((size_t)B_pad * max_out, -1);
     std::copy(outs_h.begin(), outs_h.end(), padded.begin());
@@ -721,6 +755,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   k_fill_d<<<grid_for(B_pad), 256, 0, s>>>(h->best, -std::numeric_limits<double>::infinity(), B_pad);
   k_fill_d<<<grid_for(B_pad), 256, 0, s>>>(h->bound, std::numeric_limits<double>::quiet_NaN(), B_pad);
   k_fill_i<<<grid_for(B_pad), 256, 0, s>>>(h->status, 0, B_pad);
+  CK(h, cudaMemsetAsync(h->hit, 0xff, B_pad * 8, s));  // -1
   CK(h, cudaGetLastError());
   return DCOPF_OK;
 }
@@ -748,6 +783,7 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     rc = launch_sweep<false>(h, a, s);
     if (rc) return rc;
     h->cur = (int)((h->cur + K) & 1);
+    h->k_base += (long)K;
   } else {
     SingleArgs a = single_args(h);
     a.alpha = h->alpha_dev;
@@ -755,6 +791,7 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     a.hist = hist;
     rc = launch_single<kModeStep>(h, a, s);
     if (rc) return rc;
+    h->k_base += (long)K;
   }
   if (hist_host) {
     CK(h, cudaMemcpyAsync(history, hist, (size_t)K * h->B * 8, cudaMemcpyDefault, s));
@@ -864,6 +901,33 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
   if (!rc) rc = export_ext(h, h->g_lam, grad_lambda, pm.lam_inv, h->n_bus, 1, s);
   if (!rc) rc = export_ext(h, h->g_br, grad_branch, pm.br_inv, h->n_br, brw(h->form), s);
   return rc;
+}
+
+int dcopf_dual_set_target(dcopf_dual_t h, const double *target, void *cuda_stream) {
+  if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
+  if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
+  CK(h, cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (!target) {
+    h->has_target = false;
+    return DCOPF_OK;
+  }
+  std::vector<double> t(h->B_pad, std::numeric_limits<double>::infinity());  // padding never hits
+  CK(h, cudaMemcpyAsync(t.data(), target, h->B * 8, cudaMemcpyDefault, s));
+  CK(h, cudaStreamSynchronize(s));
+  for (long b = 0; b < h->B; ++b)
+    if (std::isnan(t[b])) return fail(h, DCOPF_EINVAL, "target[%ld] is NaN", b);
+  CK(h, cudaMemcpyAsync(h->target, t.data(), h->B_pad * 8, cudaMemcpyHostToDevice, s));
+  CK(h, cudaStreamSynchronize(s));  // `t` dies at scope exit
+  h->has_target = true;
+  return DCOPF_OK;
+}
+
+int dcopf_dual_get_first_hit(dcopf_dual_t h, int64_t *hit, void *cuda_stream) {
+  if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
+  if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
+  CK(h, cudaSetDevice(h->device));
+  return copy_out(h, reinterpret_cast<long long *>(hit), h->hit, (cudaStream_t)cuda_stream);
 }
 
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {

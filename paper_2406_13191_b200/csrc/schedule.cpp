@@ -2,6 +2,7 @@
 #include "schedule.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <set>
@@ -295,7 +296,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
       }
     }
     if (f1) tl = std::max(tl, stC(chunk(rp[i])));
-    iv_th[i] = {stA(chunk(i)), tl, i};
+    iv_th[i] = {stA(chunk(i)), tl + S.pool_gap - 1, i};
   }
   std::vector<int> br_slot(nl), lam_slot(nb), d_slot(nb), th_slot(nb), f_slot(nl, 0);
   S.n_th_slots = colour(iv_th, th_slot);
@@ -303,7 +304,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   if (!f1) {  // f*: written B(chunk hi), read C of both endpoints
     iv_f.resize(nl);
     for (int l = 0; l < nl; ++l)
-      iv_f[l] = {stB(chunk(hi[l])), std::max(stC(chunk(rp[net.bs[l]])), stC(chunk(rp[net.bt[l]]))), l};
+      iv_f[l] = {stB(chunk(hi[l])), std::max(stC(chunk(rp[net.bs[l]])), stC(chunk(rp[net.bt[l]]))) + S.pool_gap - 1, l};
     S.n_f_slots = colour(iv_f, f_slot);
   }
 
@@ -535,28 +536,38 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   // ---- shared-memory layout ----
   auto al = [](int x) { return (x + 127) & ~127; };
   int off = 0;
-  S.off_bar = off;
-  off = al(off + 16 * S.S);
-  S.off_red = off;
-  off = al(off + 8 * 64 * nw);
-  S.off_frz = off;
-  off = al(off + 4 * 64);
+  S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers
+  off = al(off + 16 * S.S + 64);
+  S.off_frz = off;  // frozen flags [64] int, then running best [64] double
+  off = al(off + 4 * 64 + 8 * 64);
   S.off_obm = off;  // per-tile outage bitmap over branches
   off = al(off + 4 * ((nl + 31) / 32 + 1));
   S.off_outs = off;  // per-instance outage lists of the tile
   off = al(off + 4 * 64 * 8);
   S.off_prog = off;
   off = al(off + S.S * al(S.max_prog_bytes));
+  // state / minimiser pools; lanes past the tile width read up to 512 - RB
+  // bytes past a pool's last slot
+  int pad = 512 - RB;
+  if (const char *e = getenv("DCOPF_POOL_PAD")) pad = atoi(e);  // measurement only
   S.off_brp = off;
-  off = al(off + S.n_br_slots * BR + 512);  // +512: lanes past the tile width read padding
+  off = al(off + S.n_br_slots * BR + pad);
   S.off_lamp = off;
-  off = al(off + S.n_lam_slots * RB + 512);
+  off = al(off + S.n_lam_slots * RB + pad);
   S.off_dp = off;
-  off = al(off + S.n_d_slots * RB + 512);
+  off = al(off + S.n_d_slots * RB + pad);
   S.off_th = off;  // theta*_i rows
-  off = al(off + S.n_th_slots * RB + 512);
+  off = al(off + S.n_th_slots * RB + pad);
   S.off_fc = off;  // f*_l rows (F2)
-  off = al(off + S.n_f_slots * RB + 512);
+  off = al(off + S.n_f_slots * RB + pad);
+  // the per-warp dual-value partials [nw][64] are needed only at the end of a
+  // sweep, when every pool is dead: they alias the pools
+  S.off_red = S.off_brp;
+  off = std::max(off, al(S.off_brp + 8 * 64 * nw));
+  if (getenv("DCOPF_RED_SEPARATE")) {  // measurement only
+    S.off_red = off;
+    off = al(off + 8 * 64 * nw);
+  }
   S.total = off;
   return "";
 }

@@ -67,6 +67,8 @@ struct int4_t {
 struct Schedule {
   int CH = 0, P = 0, S = 0, W = 0, nch = 0, nsteps = 0;
   int ring_life = 6;                        // rows live <= this many steps go to the rings
+  int pool_gap = 1;                         // theta* / f* pool slots are reused only pool_gap steps after
+                                            // their last read (2: consumer warps may drift by one step)
   int ring_lam = 0, ring_d = 0, ring_br = 0, n_copies = 0, n_sticky_copies = 0;
   // storage order of the state rows in HBM (positions) and its inverse, per kind
   std::vector<int> pos_lam, perm_lam, pos_d, perm_d, pos_br, perm_br;

@@ -55,6 +55,9 @@ struct SweepArgs {
   int *status;
   double *hist;                     // [K][B] or null
   long B;
+  const double *target;             // [B_pad] time-to-gap thresholds or null
+  long long *hit;                   // [B_pad] first evaluation index with best >= target (-1: none)
+  long k_base;                      // evaluation index of this launch's k = 0
   double *out_val;                  // EVAL: value [B_pad]
   double *g_lam, *g_br;             // EVAL: gradients (tile-major)
   int n_bus, n_br, ref, W;
@@ -66,6 +69,7 @@ struct SweepArgs {
   int nsteps, S, row_bytes, br_row_bytes;
   int off_bar, off_red, off_frz, off_obm, off_outs, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th,
       off_fc;
+  int soft;                         // 1: consumer warps drift by <= 1 step (pool_gap 2); 0: lock-step
   int debug_mode;                   // 0; 1 = data movement only; 2 = no row copies (measurement only)
 };
 
@@ -80,6 +84,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned by
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// one arrival for the whole warp: __syncwarp orders every lane's shared-memory
+// accesses before lane 0's release-arrive (the count of such barriers is the
+// number of warps)
+__device__ __forceinline__ void warp_arrive(uint64_t *bar, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   unsigned done = 0;
@@ -116,13 +127,19 @@ __device__ __forceinline__ void st2(double *p, double x, double y) {
   *reinterpret_cast<double2 *>(p) = make_double2(x, y);
 }
 
-template <int FORM, bool EVAL, int NW>
-__global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
+template <int FORM, bool EVAL, int NW, bool SOFT>
+#ifndef DCOPF_SWEEP_MAXREG
+#define DCOPF_SWEEP_MAXREG 96  // 20 warps x 32 x 96 + allocation granularity fit the 64K register file
+#endif
+__global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + a.off_bar);
   uint64_t *empty = full + a.S;
+  uint64_t *adone = empty + a.S;  // [4] all consumer threads finished phase A of step g (slot g & 3)
+  uint64_t *bdone = adone + 4;    // [4] ... phase B of step g
   double *red = reinterpret_cast<double *>(smem + a.off_red);   // [NW][64]
   int *frz = reinterpret_cast<int *>(smem + a.off_frz);         // [64]
+  double *bst = reinterpret_cast<double *>(smem + a.off_frz + 256);  // [64] running best (no registers held)
   unsigned *obm = reinterpret_cast<unsigned *>(smem + a.off_obm);
   int *outs_s = reinterpret_cast<int *>(smem + a.off_outs);     // [64][kMaxOut]
   constexpr int BRW = (FORM == kFormF2) ? 1 : 2;
@@ -139,12 +156,19 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], SOFT ? NW : 1);  // soft: one arrival per consumer warp
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&adone[s], NW);
+      mbar_init(&bdone[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int x = threadIdx.x; x < (a.n_br + 31) / 32; x += blockDim.x) obm[x] = 0u;
-  for (int t = threadIdx.x; t < 64; t += blockDim.x) frz[t] = (!EVAL && t < W) ? a.status[ib + t] : 0;
+  for (int t = threadIdx.x; t < 64; t += blockDim.x) {
+    frz[t] = (!EVAL && t < W) ? a.status[ib + t] : 0;
+    bst[t] = (!EVAL && t < W) ? a.best[ib + t] : 0.0;
+  }
   for (int x = threadIdx.x; x < 64 * kMaxOut; x += blockDim.x) {
     const int t = x / kMaxOut, j = x % kMaxOut;
     outs_s[x] = (t < W && j < a.max_out) ? a.outs[(ib + t) * a.max_out + j] : -1;
@@ -200,11 +224,23 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
 
   // =========================== consumers ===========================
   const int RB = a.row_bytes, BR = a.br_row_bytes;
-  const uint8_t *brp = smem + a.off_brp + lane * 16;
-  const uint8_t *lamp = smem + a.off_lamp + lane * 16;
-  const uint8_t *dp = smem + a.off_dp + lane * 16;
-  uint8_t *thp = smem + a.off_th + lane * 16;  // theta*_i rows
-  uint8_t *fcp = smem + a.off_fc + lane * 16;  // f*_l rows (F2)
+  // lanes past the tile width (W < 64) read the pools' tail padding and never
+  // store (mirroring lane 0 instead would put them in lane 0's banks)
+  const int lofs = lane * 16;
+  const uint8_t *brp = smem + a.off_brp + lofs;
+  const uint8_t *lamp = smem + a.off_lamp + lofs;
+  const uint8_t *dp = smem + a.off_dp + lofs;
+  uint8_t *thp = smem + a.off_th + lofs;  // theta*_i rows
+  uint8_t *fcp = smem + a.off_fc + lofs;  // f*_l rows (F2)
+  // Consumer warps are not stepped in lock-step: step g waits only for
+  //   A-done(g-1): theta* of chunk g-1 (read by B) exists, and every warp has
+  //                finished step g-2, so the theta* / f* slots this step
+  //                overwrites are dead (pool slots are reused only 2 steps
+  //                after their last read: schedule pool_gap = 2);
+  //   B-done(g-1): f* of the branches C reads exists;
+  //   full[stage]: the step's program block and rows have landed.
+  // A warp may therefore run up to one step ahead of the slowest one.
+  unsigned gs = 0;  // global step counter (continues across sweeps; only gs mod 8 matters)
   const int nout = a.max_out;
   const int *my_outs0 = outs_s + (2 * lane) * kMaxOut, *my_outs1 = my_outs0 + kMaxOut;
   auto flagged = [&](int l) { return (obm[l >> 5] >> (l & 31)) & 1u; };
@@ -215,20 +251,15 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
   };
   int cst = 0;         // stage of the next step
   unsigned cph = 0;    // parity of its full barrier
-  double best0 = 0.0, best1 = 0.0;
-  if (!EVAL && warp == 0 && act) {
-    best0 = a.best[ib + 2 * lane];
-    best1 = a.best[ib + 2 * lane + 1];
-  }
 
   for (long k = 0; k <= K; ++k) {
     const bool last = (k == K);
     const bool write = EVAL || !last;
     const int par = (a.cur + (int)(k & 1)) & 1;
     uint8_t *lam_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_lam : (par ? a.lam0 : a.lam1)) + tile * (size_t)a.n_bus * RB +
-                     lane * 16;
+                     lofs;
     uint8_t *br_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_br : (par ? a.br0 : a.br1)) + tile * (size_t)a.n_br * BR +
-                    lane * 16;
+                    lofs;
     const bool step0 = !EVAL && !last && !frz[2 * lane], step1 = !EVAL && !last && !frz[2 * lane + 1];
     const double alpha = (EVAL || last) ? 0.0 : a.alpha[k];
     double v0 = 0.0, v1 = 0.0;
@@ -252,7 +283,8 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
       const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // rotB rotC
       const int nA = h0.x, nB = h0.z, nC = h0.w;
 
-      if (a.debug_mode != 1) {
+      if (a.debug_mode != 1) {  // (1: data movement only -- measurement)
+      if (SOFT && gs > 0) mbar_wait(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       // ---------------- A(s): w_i, theta* codes ----------------
       {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
@@ -261,15 +293,24 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
           const int bus = h1.z + j;
           double w0 = 0.0, w1 = 0.0;
           if (FORM == kFormF2) {
-            const RecIA2 *IA = reinterpret_cast<const RecIA2 *>(prog + h2.y);
-            for (int e = ra.e0; e < ra.e1; ++e) {
-              const RecIA2 r = IA[e];
+            // incidence entries in ascending original branch id (the oracle's
+            // order); degree <= 4 for ~97% of buses: a fixed 4-way body with
+            // warp-uniform guards instead of a counted loop, the rest in a tail
+            const RecIA2 *IA = reinterpret_cast<const RecIA2 *>(prog + h2.y) + ra.e0;
+            const int n = ra.e1 - ra.e0;
+            auto acc = [&](const RecIA2 &r) {
               const D2 nu = ld2(brp, r.row);
               w0 = w0 + r.sb * nu.x;  // w_s += -(b nu), w_t += b nu (outaged: nu == 0)
               w1 = w1 + r.sb * nu.y;
-            }
+            };
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (e < n) acc(IA[e]);
+#pragma unroll 1
+            for (int e = 4; e < n; ++e) acc(IA[e]);
           } else {
             const RecIA1 *IA = reinterpret_cast<const RecIA1 *>(prog + h2.y);
+#pragma unroll 1
             for (int e = ra.e0; e < ra.e1; ++e) {
               const RecIA1 r = IA[e];
               double sb0 = r.sb, sb1 = r.sb;
@@ -294,6 +335,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
           }
         }
       }
+      if (SOFT) warp_arrive(&adone[gs & 3], lane);
       // ---------------- B(s-1): branches ----------------
       {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
@@ -359,6 +401,10 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
           }
         }
       }
+      if (SOFT) {
+        warp_arrive(&bdone[gs & 3], lane);
+        if (gs > 0) mbar_wait(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+      }
       // ---------------- C(s-2): ready buses ----------------
       {
         const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
@@ -369,7 +415,8 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
           const RecC r = Cv[j];
           const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
           double gl0 = -di.x, gl1 = -di.y;
-          for (int gg = r.g0; gg < r.g1; ++gg) {
+#pragma unroll 1
+          for (int gg = r.g0; gg < r.g1; ++gg) {  // mostly 0 or 1 generator
             const RecG gr = G[gg];
             const double r0 = gr.c + li.x, r1 = gr.c + li.y;
             const double p0 = gen_minimiser(r0, gr.lo, gr.hi, gr.a), p1 = gen_minimiser(r1, gr.lo, gr.hi, gr.a);
@@ -384,15 +431,21 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
             }
           }
           if (FORM == kFormF2) {
-            const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y);
-            for (int e = r.e0; e < r.e1; ++e) {
-              const RecIC2 x = IC[e];
+            const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y) + r.e0;
+            const int n = r.e1 - r.e0;
+            auto acc = [&](const RecIC2 &x) {
               const D2 f = ld2(fcp, x.f);
               gl0 = gl0 + x.s * f.x;  // +f* at the to bus, -f* at the from bus ((-1)*f == -f exactly)
               gl1 = gl1 + x.s * f.y;
-            }
+            };
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (e < n) acc(IC[e]);
+#pragma unroll 1
+            for (int e = 4; e < n; ++e) acc(IC[e]);
           } else {
             const RecIC1 *IC = reinterpret_cast<const RecIC1 *>(prog + h3.y);
+#pragma unroll 1
             for (int e = r.e0; e < r.e1; ++e) {
               const RecIC1 x = IC[e];
               double sb0 = x.sb, sb1 = x.sb;
@@ -415,14 +468,20 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
         }
       }
       }  // debug_mode
-      named_bar(1, CT);
-      if (threadIdx.x == 0) mbar_arrive(&empty[st]);
+      if (SOFT) {
+        warp_arrive(&empty[st], lane);
+      } else {  // lock-step mode: every warp finished the step
+        named_bar(1, CT);
+        if (threadIdx.x == 0) mbar_arrive(&empty[st]);
+      }
+      ++gs;
     }
     };
     const bool anyf = __any_sync(0xffffffffu, (frz[2 * lane] | frz[2 * lane + 1]) != 0);
     if (anyf) run_steps(std::integral_constant<bool, true>{});
     else run_steps(std::integral_constant<bool, false>{});
     // ---------------- dual value, best, status ----------------
+    named_bar(1, CT);  // every warp is past the sweep's last step: the pools red aliases are dead
     red[warp * 64 + 2 * lane] = v0;
     red[warp * 64 + 2 * lane + 1] = v1;
     named_bar(1, CT);
@@ -445,6 +504,7 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
           a.bound[b0i] = g0;
           a.bound[b1i] = g1;
         }
+        double best0 = bst[2 * lane], best1 = bst[2 * lane + 1];
         if (!frz[2 * lane]) {
           if (valid_bound(g0)) best0 = (g0 > best0) ? g0 : best0;
           else frz[2 * lane] = 1;
@@ -452,6 +512,13 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
         if (!frz[2 * lane + 1]) {
           if (valid_bound(g1)) best1 = (g1 > best1) ? g1 : best1;
           else frz[2 * lane + 1] = 1;
+        }
+        bst[2 * lane] = best0;
+        bst[2 * lane + 1] = best1;
+        if (a.target) {  // time to gap: first evaluation whose running best reaches the target
+          // (state kept in global memory, touched once per sweep: no registers held)
+          if (a.hit[b0i] < 0 && best0 >= a.target[b0i]) a.hit[b0i] = a.k_base + k;
+          if (a.hit[b1i] < 0 && best1 >= a.target[b1i]) a.hit[b1i] = a.k_base + k;
         }
       }
     }
@@ -466,8 +533,8 @@ __global__ void __maxnreg__(128) k_sweep(const SweepArgs a) {
     }
   }
   if (!EVAL && warp == 0 && act) {
-    a.best[ib + 2 * lane] = best0;
-    a.best[ib + 2 * lane + 1] = best1;
+    a.best[ib + 2 * lane] = bst[2 * lane];
+    a.best[ib + 2 * lane + 1] = bst[2 * lane + 1];
     a.status[ib + 2 * lane] = frz[2 * lane];
     a.status[ib + 2 * lane + 1] = frz[2 * lane + 1];
   }

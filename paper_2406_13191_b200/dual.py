@@ -59,7 +59,8 @@ class Info(ctypes.Structure):
 
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",
            "dcopf_dual_get_bound", "dcopf_dual_get_multipliers", "dcopf_dual_set_multipliers",
-           "dcopf_dual_evaluate", "dcopf_dual_get_info", "dcopf_dual_last_error", "dcopf_dual_destroy"]
+           "dcopf_dual_evaluate", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info",
+           "dcopf_dual_last_error", "dcopf_dual_destroy"]
 
 _lib = None
 
@@ -69,7 +70,7 @@ def load_library(path: Optional[str] = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    path = path or _build.LIB
+    path = path or os.environ.get("DCOPF_LIB") or _build.LIB  # DCOPF_LIB: A/B measurement of another build
     if not os.path.exists(path):
         raise ImportError(f"{path} not built; run __graft_entry__.build() (no CPU fallback exists)")
     lib = ctypes.CDLL(path)
@@ -81,13 +82,17 @@ def load_library(path: Optional[str] = None):
     lib.dcopf_dual_get_multipliers.argtypes = [P, P, P, P]
     lib.dcopf_dual_set_multipliers.argtypes = [P, P, P, P]
     lib.dcopf_dual_evaluate.argtypes = [P, P, P, P, P]
+    if hasattr(lib, "dcopf_dual_set_target"):
+        lib.dcopf_dual_set_target.argtypes = [P, P, P]
+        lib.dcopf_dual_get_first_hit.argtypes = [P, P, P]
     lib.dcopf_dual_get_info.argtypes = [P, ctypes.POINTER(Info)]
     lib.dcopf_dual_last_error.argtypes = [P]
     lib.dcopf_dual_last_error.restype = ctypes.c_char_p
     lib.dcopf_dual_destroy.argtypes = [P]
     lib.dcopf_dual_destroy.restype = None
     for s in SYMBOLS[:-2]:
-        getattr(lib, s).restype = ctypes.c_int
+        if hasattr(lib, s):
+            getattr(lib, s).restype = ctypes.c_int
     if path == _build.LIB:
         _lib = lib
     return lib
@@ -190,6 +195,17 @@ class DcopfDual:
     def evaluate(self, value=None, grad_lam=None, grad_branch=None, stream=None):
         self._check(self.lib.dcopf_dual_evaluate(self.h, _ptr(value), _ptr(grad_lam), _ptr(grad_branch),
                                                  _stream(stream)))
+
+    def set_target(self, target=None, stream=None):
+        """Per-instance time-to-gap thresholds [B] (None clears them)."""
+        self._check(self.lib.dcopf_dual_set_target(self.h, _ptr(target), _stream(stream)))
+
+    def get_first_hit(self, hit=None, stream=None):
+        """[B] int64: first evaluation index whose running best >= target, or -1."""
+        if hit is None:
+            hit = np.empty(self.B, dtype=np.int64)
+        self._check(self.lib.dcopf_dual_get_first_hit(self.h, _ptr(hit), _stream(stream)))
+        return hit
 
     def info(self) -> Info:
         inf = Info()

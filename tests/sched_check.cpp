@@ -32,6 +32,7 @@ int main(int argc, char **argv) {
   Schedule S;
   const int W = argc > 2 ? atoi(argv[2]) : 32;
   if (argc > 3) S.ring_life = atoi(argv[3]);
+  if (argc > 4) S.pool_gap = atoi(argv[4]);
   std::string err = build_schedule(n, CH, P, W, 8, &S);
 
   if (!err.empty()) { printf("ERR %s\n", err.c_str()); return 1; }

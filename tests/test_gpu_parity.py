@@ -263,3 +263,65 @@ def test_zero_iterations_evaluates_origin():
     net = inst.make_network(0)
     gpu = run_gpu(net, net.base_load, K=0, path=dual.PATH_BATCHED)
     assert gpu["bound"][0] == 0.0 and gpu["best"][0] == 0.0
+
+
+# ---------------------------------------------------------------------------
+# time to gap: the device-recorded first evaluation whose running best reaches
+# a per-instance target equals the one read off the oracle's
+# g(y_k) history; two iterate() calls continue the evaluation count
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+@pytest.mark.parametrize("path", PATHS)
+def test_first_hit_matches_oracle_history(form, path):
+    import torch
+    net = inst.make_network(0, theta_mode="min")
+    rng = np.random.default_rng(7)
+    B = 5
+    loads = net.base_load[None, :] * rng.uniform(0.8, 1.1, (B, 1))
+    K1, K2 = 1200, 1800
+    K = K1 + K2
+    a = inst.alpha_schedule(K, 1e-2)
+    orc = oracle.solve(net, loads, K=K, alpha=a, form=form, history=True)
+    rb = np.maximum.accumulate(orc.hist, axis=1)   # running best over k = 0..K
+    S = cost_scale(net)
+    target = np.full(B, np.inf)
+    expect = np.full(B, -1, dtype=np.int64)
+    for b in range(B - 1):  # the last instance keeps an unreachable target
+        # a target strictly between two running-best values far apart (robust
+        # to the 1e-9 relative bound tolerance): the first big jump past 50%
+        fin = rb[b, -1]
+        ks = np.nonzero((rb[b] >= 0.5 * fin) & (np.diff(rb[b], prepend=-np.inf) > 1e-7 * S))[0]
+        k = int(ks[0])
+        target[b] = 0.5 * (rb[b, k - 1] + rb[b, k]) if k > 0 else rb[b, 0] - 1.0
+        expect[b] = k
+    dev = torch.device("cuda:0")
+    h = dual.DcopfDual(net, form=form, path=path)
+    h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(loads.T)).to(dev))
+    h.set_target(target)
+    h.iterate(K1, a[:K1])
+    h.iterate(K2, a[K1:])
+    hit = h.get_first_hit()
+    best = np.empty(B)
+    h.get_bound(best=best)
+    h.close()
+    np.testing.assert_array_equal(hit, expect)
+    assert np.all(np.abs(best - orc.best) <= BOUND_RTOL * np.maximum(np.abs(orc.best), S))
+
+
+def test_first_hit_cleared_by_new_batch():
+    import torch
+    net = inst.make_network(0)
+    dev = torch.device("cuda:0")
+    h = dual.DcopfDual(net, path=dual.PATH_SINGLE)
+    ld = torch.from_numpy(net.base_load[:, None].copy()).to(dev)
+    h.set_instance_batch(ld)
+    h.set_target(np.array([-1.0]))            # g(y_0) = 0 >= -1: hit at evaluation 0
+    h.iterate(3, inst.alpha_schedule(3))
+    assert h.get_first_hit()[0] == 0
+    h.set_instance_batch(ld)                  # cleared: no target, no hit
+    h.iterate(3, inst.alpha_schedule(3))
+    assert h.get_first_hit()[0] == -1
+    with pytest.raises(dual.DcopfError):
+        h.set_target(np.array([np.nan]))
+    h.close()

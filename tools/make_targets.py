@@ -1,0 +1,67 @@
+#!/usr/bin/env python3
+"""Reference bounds for the time-to-gap measurement.
+
+For each benched workload and form, runs the ORACLE (oracle/, fp64 CPU) for
+the workload's K (BASELINE.json configs: 20000 / 20000 / 50000 / 5000) with
+the fixed step alpha = 1e-3 (reading A-9) and stores its final running best
+bound per sampled instance in tests/golden/targets.json.  bench.py reads the
+file and asks the library for the first iteration at which the GPU's running
+best reaches (1 - 1e-3) of it (on the sign-aware side).  Config 4 uses the
+deterministic sample of every 128th instance (64 instances), as SURVEY.md
+§8(d) prescribes for the oracle at that size.
+
+Calls only oracle/ and the seeded input generator; nothing here comes from
+the CUDA path.
+
+  python tools/make_targets.py [--only config4/F2 ...] [--threads N]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_2406_13191_b200 import instances as inst  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden", "targets.json")
+WORKLOADS = {"config1": (1, False), "config2": (2, True), "config3": (3, False), "config3q": (3, True),
+             "config4": (4, False)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", nargs="*")
+    ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    a = ap.parse_args()
+    js = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    for wl, (config, quad) in WORKLOADS.items():
+        for form_name, form in (("F2", oracle.FORM_F2), ("F1", oracle.FORM_F1)):
+            key = f"{wl}/{form_name}"
+            if a.only and key not in a.only:
+                continue
+            net = inst.make_network(config, quadratic=quad)
+            K = inst.ITERS[config]
+            if config == 4:
+                ids = np.arange(0, inst.CONFIG4_BATCH, 128)
+                batch = inst.config4_batch(net, ids)
+            else:
+                ids = np.zeros(1, dtype=np.int64)
+                batch = inst.single_batch(net)
+            t0 = time.time()
+            res = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K),
+                               form=form, threads=a.threads)
+            js[key] = {"K": K, "alpha": inst.ALPHA, "instance_ids": ids.tolist(), "best": res.best.tolist(),
+                       "bound": res.bound.tolist(), "status": res.status.tolist(),
+                       "source": "oracle/dcopf_oracle.c via tools/make_targets.py"}
+            print(key, f"{time.time() - t0:.1f}s", "best[:4] =", res.best[:4], flush=True)
+            json.dump(js, open(OUT, "w"), indent=0)
+
+
+if __name__ == "__main__":
+    main()
