@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
     ap.add_argument("--form", default="F2", choices=["F2", "F1"])
-    ap.add_argument("--path", default="auto", choices=["auto", "batched", "single"])
+    ap.add_argument("--path", default="auto", choices=["auto", "batched", "single", "cluster"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap run (the workload's full K)")
@@ -265,8 +265,9 @@ def main():
     lo, hi = shard(B_total, rank, world) if B_total > 1 else (0, 1)
     net, batch = make_inputs(args.workload, lo, hi)
     B = batch.B
-    path = dual.PATH_BATCHED if B_total > 1 else dual.PATH_SINGLE
-    path = {"auto": path, "batched": dual.PATH_BATCHED, "single": dual.PATH_SINGLE}[args.path]
+    path = dual.PATH_BATCHED if B_total > 1 else dual.PATH_CLUSTER
+    path = {"auto": path, "batched": dual.PATH_BATCHED, "single": dual.PATH_SINGLE,
+            "cluster": dual.PATH_CLUSTER}[args.path]
 
     # config 4 takes branches out among the non-tree ones only: declaring that
     # lets the library skip the outage test on the (never switched) tree
@@ -388,7 +389,8 @@ def main():
             "config": {"workload": args.workload, "form": args.form, "cost": "QP" if quad else "LP",
                        "n_bus": net.n_bus, "n_branch": net.n_branch, "n_gen": net.n_gen,
                        "B_total": B_total, "B_per_gpu": B,
-                       "path": {1: "batched-sweep", 2: "single"}[path],
+                       "path": {1: "batched-sweep", 2: "single", 3: "cluster"}[path],
+                       "cluster_size": info.cluster_size,
                        "kernel": {"grid": info.grid, "threads": info.threads_per_block, "smem": info.smem_bytes,
                                   "chunk": info.chunk, "tile_width": info.tile_width,
                                   "copies_per_sweep": info.copies_per_sweep, "ring_life": info.ring_life,

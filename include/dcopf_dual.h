@@ -73,11 +73,15 @@ enum { DCOPF_INST_OK = 0, DCOPF_INST_DIVERGED = 1 };
 
 /* kernel path selection */
 enum {
-  DCOPF_PATH_AUTO = 0,    /* SINGLE when B <= single_max_batch, else BATCHED */
+  DCOPF_PATH_AUTO = 0,    /* CLUSTER when B <= single_max_batch (SINGLE if the partition does
+                             not fit), else BATCHED */
   DCOPF_PATH_BATCHED = 1, /* tiles of W <= 64 instances (2 per lane), one CTA per tile, one
                              persistent launch for all K iterations: a TMA-fed sweep over a
                              host-compiled schedule of the network (DFS tree bus order) */
-  DCOPF_PATH_SINGLE = 2   /* one persistent CTA per instance running all K iterations on chip */
+  DCOPF_PATH_SINGLE = 2,  /* one persistent CTA per instance running all K iterations on chip */
+  DCOPF_PATH_CLUSTER = 3  /* one thread-block cluster of up to 16 CTAs per instance, the network
+                             partitioned over the CTAs' shared memories (distributed shared
+                             memory), all K iterations in one launch */
 };
 
 /* Network description.  Host pointers,
@@ -197,6 +201,7 @@ typedef struct {
   int32_t tile_width;             /* instances per CTA (batched W; 1 for the single path) */
   int32_t copies_per_sweep;       /* batched path: bulk copies per tile per iteration */
   int32_t ring_life;              /* batched path: rows live <= this many steps use the rings */
+  int32_t cluster_size;           /* cluster path: CTAs per instance (1 otherwise) */
 } dcopf_info;
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info);
 

@@ -21,6 +21,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dcopf_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
+# gradient-based-optimisation variants (Algorithm 1)
+OPT_PLAIN, OPT_GDM, OPT_GDM_CLASSIC, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2, 3, 4
+
 FORM_F2 = 0  # flow box (lambda, nu)
 FORM_F1 = 1  # limit rows (lambda, mu+, mu-)
 DIVERGED = 1
@@ -51,6 +54,9 @@ def _load():
         net = [I, I, I, I, P, P, P, P, P, P, P, P, P, P]
         lib.oracle_solve.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I]
         lib.oracle_solve.restype = I
+        D = ctypes.c_double
+        lib.oracle_solve_opt.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I, I, D, D, D, D]
+        lib.oracle_solve_opt.restype = I
         lib.oracle_evaluate.argtypes = net + [I, L, P, P, I, P, P, P, P, P]
         lib.oracle_evaluate.restype = I
         lib.oracle_minimiser.argtypes = net + [I, L, P, P, I, P, P, P, P, P]
@@ -89,8 +95,9 @@ class OracleResult:
 
 
 def solve(net, load, outages=None, K=0, alpha=None, form=FORM_F2, lam0=None, br0=None,
-          history=False, threads=1) -> OracleResult:
-    """K projected ascent steps from y_0 = 0 (or the given warm start)."""
+          history=False, threads=1, opt=None) -> OracleResult:
+    """K projected ascent steps from y_0 = 0 (or the given warm start).
+    opt: None (plain step) or dict(variant=OPT_*, rho=, beta1=, beta2=, eps=)."""
     lib = _load()
     load = np.ascontiguousarray(np.atleast_2d(load), dtype=np.float64)
     B = load.shape[0]
@@ -110,9 +117,12 @@ def solve(net, load, outages=None, K=0, alpha=None, form=FORM_F2, lam0=None, br0
     status = np.zeros(B, dtype=np.int32)
     hist = np.zeros((B, K + 1)) if history else None
     keep = []
-    rc = lib.oracle_solve(*_net_args(net, keep), form, B, _p(load), _p(outs), max_out, K, _p(alpha),
-                          _p(lam), _p(br), _p(bound), _p(best), _p(status), _p(hist), int(warm),
-                          int(threads))
+    o = dict(variant=OPT_PLAIN, rho=0.0, beta1=0.0, beta2=0.0, eps=0.0)
+    o.update(opt or {})
+    rc = lib.oracle_solve_opt(*_net_args(net, keep), form, B, _p(load), _p(outs), max_out, K, _p(alpha),
+                              _p(lam), _p(br), _p(bound), _p(best), _p(status), _p(hist), int(warm),
+                              int(threads), int(o["variant"]), float(o["rho"]), float(o["beta1"]),
+                              float(o["beta2"]), float(o["eps"]))
     if rc != 0:
         raise ValueError("oracle_solve rejected its arguments")
     return OracleResult(lam, br, bound, best, status, hist)

@@ -38,6 +38,20 @@
  * literally; every sum runs in ascending index order; no FMA contraction
  * (compile with -ffp-contract=off, reading A-19).
  *
+ * Gradient-based-optimisation variants ("Adam ... AdaGrad ...
+ * Gradient with Momentum"; Algorithm 1),
+ * per multiplier coordinate y with ascent direction g = grad and step a_k:
+ *   PLAIN        y <- y + a_k g
+ *   GDM          (Algorithm 1 as printed, both updates)
+ *                v <- rho v + a_k g;  y <- y + v;  y <- y + a_k g
+ *   GDM_CLASSIC  v <- rho v + a_k g;  y <- y + v        (reading A-25)
+ *   ADAGRAD      G <- G + g g;  y <- y + (a_k g) / (sqrt(G) + eps)
+ *   ADAM         t = steps taken so far + 1; b1t <- b1t beta1, b2t <- b2t beta2
+ *                (powers by repeated multiplication from 1);
+ *                m <- beta1 m + (1 - beta1) g;  v <- beta2 v + (1 - beta2)(g g);
+ *                y <- y + (a_k (m / (1 - b1t))) / (sqrt(v / (1 - b2t)) + eps)
+ * then mu <- max(mu, 0).  Optimiser state starts at 0.
+ *
  * Divergence (reading A-23 in DESIGN.md): if g(y_k) is not
  * finite or |g(y_k)| > 1e15 the instance is marked DIVERGED; the step of
  * iteration k is still taken, every later step is skipped (y frozen at
@@ -199,14 +213,55 @@ static double evaluate(const orc_net *N, orc_work *W, int form, const double *d,
 
 static int valid_bound(double g) { return isfinite(g) && fabs(g) <= 1e15; }
 
+#define ORC_OPT_PLAIN 0
+#define ORC_OPT_GDM 1
+#define ORC_OPT_GDM_CLASSIC 2
+#define ORC_OPT_ADAGRAD 3
+#define ORC_OPT_ADAM 4
+
+typedef struct {
+  int variant;
+  double rho, beta1, beta2, eps;
+} orc_opt;
+
+/* one coordinate of the ascent step (the variants above); s1, s2 = state */
+static double opt_step(const orc_opt *o, double y, double g, double a, double *s1, double *s2,
+                       double b1t, double b2t) {
+  switch (o->variant) {
+    case ORC_OPT_GDM:
+      *s1 = o->rho * *s1 + a * g;
+      y = y + *s1;
+      return y + a * g;
+    case ORC_OPT_GDM_CLASSIC:
+      *s1 = o->rho * *s1 + a * g;
+      return y + *s1;
+    case ORC_OPT_ADAGRAD:
+      *s1 = *s1 + g * g;
+      return y + (a * g) / (sqrt(*s1) + o->eps);
+    case ORC_OPT_ADAM: {
+      *s1 = o->beta1 * *s1 + (1.0 - o->beta1) * g;
+      *s2 = o->beta2 * *s2 + (1.0 - o->beta2) * (g * g);
+      {
+        double mh = *s1 / (1.0 - b1t), vh = *s2 / (1.0 - b2t);
+        return y + (a * mh) / (sqrt(vh) + o->eps);
+      }
+    }
+    default:
+      return y + a * g;
+  }
+}
+
 static void run_instance(const orc_net *N, int form, const double *d, const int *out, int max_out,
                          long K, const double *alpha, double *lam, double *br, double *bound,
-                         double *best, int *status, double *hist, int warm) {
+                         double *best, int *status, double *hist, int warm, const orc_opt *opt) {
   const int nb = N->n_bus, nl = N->n_branch;
   const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * nl : nl;
   orc_work W;
   long k;
   int i, j, frozen = 0;
+  double b1t = 1.0, b2t = 1.0;                   /* beta1^t, beta2^t (Adam) */
+  double *s1 = calloc((size_t)(nb + nbr + 1), sizeof(double));   /* optimiser state, y order */
+  double *s2 = calloc((size_t)(nb + nbr + 1), sizeof(double));
   work_alloc(&W, N, form);
   apply_outages(&W, N, out, max_out);
   if (!warm) {                                   /* step 3: y_0 = 0 */
@@ -227,18 +282,21 @@ static void run_instance(const orc_net *N, int form, const double *d, const int 
     if (was_frozen) continue;
     {                                            /* (h) ascent step and projection */
       double a = alpha[k];
-      for (i = 0; i < nb; i++) lam[i] = lam[i] + a * W.glam[i];
+      if (opt->variant == ORC_OPT_ADAM) { b1t = b1t * opt->beta1; b2t = b2t * opt->beta2; }
+      for (i = 0; i < nb; i++) lam[i] = opt_step(opt, lam[i], W.glam[i], a, &s1[i], &s2[i], b1t, b2t);
       if (form == ORC_FORM_FLOW_BOX) {
-        for (j = 0; j < nl; j++) br[j] = br[j] + a * W.gbr[j];
+        for (j = 0; j < nl; j++) br[j] = opt_step(opt, br[j], W.gbr[j], a, &s1[nb + j], &s2[nb + j], b1t, b2t);
       } else {
         for (j = 0; j < 2 * nl; j++) {
-          double v = br[j] + a * W.gbr[j];
+          double v = opt_step(opt, br[j], W.gbr[j], a, &s1[nb + j], &s2[nb + j], b1t, b2t);
           br[j] = (v > 0.0) ? v : 0.0;           /* mu <- max(mu, 0) */
         }
       }
     }
   }
   work_free(&W);
+  free(s1);
+  free(s2);
 }
 
 #define NET_ARGS                                                                     \
@@ -263,11 +321,15 @@ static void run_instance(const orc_net *N, int form, const double *d, const int 
  *   hist[B][K+1] (g(y_k)) or NULL.
  * Returns 0, or -1 on bad arguments.
  */
-int oracle_solve(NET_ARGS, int form, long B, const double *load, const int *outages, int max_out,
-                 long K, const double *alpha, double *lam, double *br, double *bound,
-                 double *best, int *status, double *hist, int warm, int n_threads) {
+int oracle_solve_opt(NET_ARGS, int form, long B, const double *load, const int *outages, int max_out,
+                     long K, const double *alpha, double *lam, double *br, double *bound,
+                     double *best, int *status, double *hist, int warm, int n_threads,
+                     int variant, double rho, double beta1, double beta2, double eps) {
   NET_INIT
   long j;
+  orc_opt opt;
+  opt.variant = variant; opt.rho = rho; opt.beta1 = beta1; opt.beta2 = beta2; opt.eps = eps;
+  if (variant < ORC_OPT_PLAIN || variant > ORC_OPT_ADAM) return -1;
   const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * n_branch : n_branch;
   if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0 || K < 0) return -1;
   if (form != ORC_FORM_FLOW_BOX && form != ORC_FORM_LIMIT_ROWS) return -1;
@@ -276,9 +338,19 @@ int oracle_solve(NET_ARGS, int form, long B, const double *load, const int *outa
   for (j = 0; j < B; j++) {
     run_instance(&N, form, load + j * (long)n_bus, outages ? outages + j * (long)max_out : NULL,
                  max_out, K, alpha, lam + j * (long)n_bus, br + j * (long)nbr, bound + j,
-                 best + j, status + j, hist ? hist + j * (K + 1) : NULL, warm);
+                 best + j, status + j, hist ? hist + j * (K + 1) : NULL, warm, &opt);
   }
   return 0;
+}
+
+/* the plain projected step (the north_star path) */
+int oracle_solve(NET_ARGS, int form, long B, const double *load, const int *outages, int max_out,
+                 long K, const double *alpha, double *lam, double *br, double *bound,
+                 double *best, int *status, double *hist, int warm, int n_threads) {
+  return oracle_solve_opt(n_bus, n_branch, n_gen, ref_bus, br_from, br_to, br_b, br_fmax, theta_max,
+                          gen_bus, gen_pmin, gen_pmax, gen_c, gen_a, form, B, load, outages, max_out, K,
+                          alpha, lam, br, bound, best, status, hist, warm, n_threads,
+                          ORC_OPT_PLAIN, 0.0, 0.0, 0.0, 0.0);
 }
 
 /* Value and gradient at given multipliers (no step). */

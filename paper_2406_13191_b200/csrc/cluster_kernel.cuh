@@ -1,0 +1,319 @@
+// cluster_kernel.cuh -- the cluster path: one thread-block cluster of C CTAs
+// (one per SM, C <= 16) runs all K iterations of ONE instance, the network
+// partitioned over the CTAs' shared memories (plan: cluster.h).
+//
+// Per iteration (Eq. 3, 7b, 15, Alg. 1):
+//   A   owned buses: w_i over the incidence (neighbours' nu / mu, lambda read
+//       over distributed shared memory), theta*_i
+//   --- cluster barrier ---
+//   B   owned branches: q_l, f*_l, phi_l, residual, nu' / mu' (in place: every
+//       reader of nu / mu in this iteration ran in A)
+//   --- cluster barrier ---
+//   C   owned buses: generators, d/dlambda, lambda' (in place: every reader of
+//       lambda in this iteration ran in B, or -- F1 -- in A)
+//   (F1 only: --- cluster barrier --- before the next A, which reads lambda')
+// The dual value: per-CTA block reduction, then every CTA reads all C partials
+// after the next barrier and sums them in rank order (bitwise identical in
+// every CTA, so every CTA takes the same best / divergence decision; rank 0
+// writes the results).  F2 needs 2 cluster barriers per iteration, F1 3.
+//
+// Per-entity arithmetic and its operation order are those of the oracle and
+// of k_single / k_sweep (reading A-19): sums over a bus's incidence in
+// ascending original branch id, generators before branches, y + (alpha*g).
+#pragma once
+#include "cluster.h"
+#include "dual_kernels.cuh"
+
+namespace dcopf {
+
+struct ClusterArgs {
+  const uint8_t *blob;          // [C] per-rank blobs (ClusterPlan)
+  int blob_stride;
+  double *lam, *br;             // instance-major internal state [b][n_bus], [b][n_br * BRW]
+  const double *d;              // [b][n_bus]
+  const int *outs;              // [B][max_out] internal branch ids, -1 padded
+  int max_out;
+  const double *alpha;          // [K] device
+  long K;
+  double *bound, *best;         // [B]
+  int *status;                  // [B]
+  double *hist;                 // [K][B] or null
+  long B;
+  const double *target;         // [B] or null (time to gap)
+  long long *hit;
+  long k_base;
+  double *grad_lam, *grad_br, *value;  // EVAL outputs (instance-major) or null
+  int n_bus, n_br;
+};
+
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_nrank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_map(unsigned local_addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+// distributed-shared-memory loads; ordered against the cluster barriers by
+// `volatile` (the barriers carry the memory clobber)
+__device__ __forceinline__ double cl_ld(unsigned addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double2 cl_ld2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+template <int FORM, int MODE>
+__global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int BRW = (FORM == kFormF2) ? 1 : 2;
+  const unsigned rank = cl_rank(), C = cl_nrank();
+  const long b = cl_id();
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+
+  // ---- plan blob -> shared memory --------------------------------------------
+  {
+    const ClHeader *g = reinterpret_cast<const ClHeader *>(a.blob + (size_t)rank * a.blob_stride);
+    const int n16 = g->blob_bytes / 16;
+    const int4 *src = reinterpret_cast<const int4 *>(g);
+    int4 *dst = reinterpret_cast<int4 *>(smem);
+    for (int x = tid; x < n16; x += nthr) dst[x] = src[x];
+  }
+  __syncthreads();
+  const ClHeader &H = *reinterpret_cast<const ClHeader *>(smem);
+  const int nA = H.nA, nB = H.nB;
+  double *lam_s = reinterpret_cast<double *>(smem + H.off_lam);
+  double *d_s = reinterpret_cast<double *>(smem + H.off_d);
+  double *br_s = reinterpret_cast<double *>(smem + H.off_br);
+  double *th_s = reinterpret_cast<double *>(smem + H.off_th);
+  double *fc_s = reinterpret_cast<double *>(smem + H.off_fc);
+  double *red = reinterpret_cast<double *>(smem + H.off_red);        // [0]: this CTA's partial value
+  double *wred = red + 8;                                            // [32] per-warp partials
+  int *flag = reinterpret_cast<int *>(red + 40);                     // [0]: frozen
+  const unsigned red_addr0 = sbase + H.off_red;
+
+  // ---- cluster addresses + this instance's outages (b = F = 0, reading A-16) ---
+  const int nout = a.max_out;
+  int o[kMaxOut];
+#pragma unroll
+  for (int j = 0; j < kMaxOut; ++j) o[j] = (j < nout) ? a.outs[b * nout + j] : -1;
+  auto cvt = [&](unsigned x) { return cl_map(sbase + (x & ((1u << kClAddrShift) - 1)), x >> kClAddrShift); };
+  if (FORM == kFormF2) {
+    ClIA2 *IA = reinterpret_cast<ClIA2 *>(smem + H.off_IA);
+    ClIC2 *IC = reinterpret_cast<ClIC2 *>(smem + H.off_IC);
+    for (int e = tid; e < H.nIA; e += nthr) {
+      IA[e].nu = cvt(IA[e].nu);
+      IC[e].f = cvt(IC[e].f);
+      if (is_out(o, nout, IA[e].br)) IA[e].sb = copysign(0.0, IA[e].sb);
+    }
+  } else {
+    ClIA1 *IA = reinterpret_cast<ClIA1 *>(smem + H.off_IA);
+    ClIC1 *IC = reinterpret_cast<ClIC1 *>(smem + H.off_IC);
+    for (int e = tid; e < H.nIA; e += nthr) {
+      IA[e].mu = cvt(IA[e].mu);
+      IA[e].ls = cvt(IA[e].ls);
+      IA[e].lt = cvt(IA[e].lt);
+      IC[e].ts = cvt(IC[e].ts);
+      IC[e].tt = cvt(IC[e].tt);
+      if (is_out(o, nout, IA[e].br)) {
+        IA[e].sb = copysign(0.0, IA[e].sb);
+        IC[e].sb = copysign(0.0, IC[e].sb);
+      }
+    }
+  }
+  {
+    ClB *Bv = reinterpret_cast<ClB *>(smem + H.off_B);
+    for (int j = tid; j < nB; j += nthr) {
+      Bv[j].ts = cvt(Bv[j].ts);
+      Bv[j].tt = cvt(Bv[j].tt);
+      Bv[j].ls = cvt(Bv[j].ls);
+      Bv[j].lt = cvt(Bv[j].lt);
+      if (is_out(o, nout, Bv[j].br)) Bv[j].b = Bv[j].F = 0.0;
+    }
+  }
+  // ---- this CTA's state ------------------------------------------------------------
+  const double *lam_g = a.lam + b * (size_t)a.n_bus + H.bus0;
+  const double *br_g = a.br + (b * (size_t)a.n_br + H.br0) * BRW;
+  const double *d_g = a.d + b * (size_t)a.n_bus + H.bus0;
+  for (int i = tid; i < nA; i += nthr) {
+    lam_s[i] = lam_g[i];
+    d_s[i] = d_g[i];
+  }
+  for (int j = tid; j < nB * BRW; j += nthr) br_s[j] = br_g[j];
+  if (tid == 0) flag[0] = (MODE != kModeEval) ? a.status[b] : 0;
+  double best = (MODE != kModeEval) ? a.best[b] : 0.0;
+  __syncthreads();
+  cl_sync();  // every CTA's shared memory is ready for remote reads
+
+  const ClA *Ar = reinterpret_cast<const ClA *>(smem + H.off_A);
+  const ClB *Br = reinterpret_cast<const ClB *>(smem + H.off_B);
+  const ClC *Cr = reinterpret_cast<const ClC *>(smem + H.off_C);
+  const ClG *Gr = reinterpret_cast<const ClG *>(smem + H.off_G);
+  const long K = (MODE == kModeEval) ? 0 : a.K;
+
+  // dual value of iteration kk: every CTA sums the C partials in rank order
+  auto finish = [&](long kk) {
+    if (warp == 0) {
+      const double p = (lane < (int)C) ? cl_ld(cl_map(red_addr0, lane)) : 0.0;
+      double g = 0.0;
+      for (unsigned r = 0; r < C; ++r) g += __shfl_sync(0xffffffffu, p, r);
+      if (lane == 0) {
+        int frozen = flag[0];
+        if (MODE == kModeEval) {
+          if (rank == 0) a.value[b] = g;
+        } else {
+          if (rank == 0) {
+            if (kk < K && a.hist) a.hist[(size_t)kk * a.B + b] = g;
+            if (kk == K) a.bound[b] = g;
+          }
+          if (!frozen) {
+            if (valid_bound(g)) best = (g > best) ? g : best;
+            else frozen = 1;
+          }
+          if (rank == 0 && a.target && a.hit[b] < 0 && best >= a.target[b]) a.hit[b] = a.k_base + kk;
+          flag[0] = frozen;
+        }
+      }
+    }
+    __syncthreads();
+  };
+
+  for (long k = 0; k <= K; ++k) {
+    const double alpha = (k < K) ? a.alpha[k] : 0.0;
+    double val = 0.0;
+    // ---------------- A: w_i, theta*_i ----------------
+    for (int i = tid; i < nA; i += nthr) {
+      const ClA r = Ar[i];
+      double w = 0.0;
+      if (FORM == kFormF2) {
+        const ClIA2 *IA = reinterpret_cast<const ClIA2 *>(smem + H.off_IA);
+        for (int e = r.e0; e < r.e1; ++e) {
+          const ClIA2 x = IA[e];
+          w = w + x.sb * cl_ld(x.nu);  // w_s += -(b nu), w_t += b nu
+        }
+      } else {
+        const ClIA1 *IA = reinterpret_cast<const ClIA1 *>(smem + H.off_IA);
+        for (int e = r.e0; e < r.e1; ++e) {
+          const ClIA1 x = IA[e];
+          const double2 m = cl_ld2(x.mu);
+          w = w + x.sb * ((m.x - m.y) - (cl_ld(x.ls) - cl_ld(x.lt)));  // w_s += u, w_t -= u
+        }
+      }
+      const bool isref = (i == H.ref_local);
+      const double th = isref ? 0.0 : ((w < 0.0) ? r.theta : ((w > 0.0) ? -r.theta : 0.0));
+      th_s[i] = th;
+      if (!isref) val += w * th;
+    }
+    cl_sync();
+    if (FORM == kFormF2 && k > 0) finish(k - 1);
+    const bool step = (MODE == kModeStep) && (k < K) && !flag[0];
+    // ---------------- B: branches ----------------
+    for (int j = tid; j < nB; j += nthr) {
+      const ClB r = Br[j];
+      const double phi = r.b * (cl_ld(r.ts) - cl_ld(r.tt));
+      if (FORM == kFormF2) {
+        const double nu = br_s[j];
+        const double q = nu - (cl_ld(r.ls) - cl_ld(r.lt));
+        const double f = (q > 0.0) ? -r.F : ((q < 0.0) ? r.F : 0.0);
+        fc_s[j] = f;
+        const double g = f - phi;  // Kirchhoff residual
+        val += q * f;
+        if (step) br_s[j] = nu + alpha * g;
+        if (MODE == kModeEval) a.grad_br[b * (size_t)a.n_br + H.br0 + j] = g;
+      } else {
+        const double mp = br_s[2 * j], mm = br_s[2 * j + 1];
+        const double gp = phi - r.F, gm = -phi - r.F;
+        val += -(r.F * (mp + mm));
+        if (step) {
+          const double vp = mp + alpha * gp, vm = mm + alpha * gm;
+          br_s[2 * j] = (vp > 0.0) ? vp : 0.0;  // mu <- max(mu, 0)
+          br_s[2 * j + 1] = (vm > 0.0) ? vm : 0.0;
+        }
+        if (MODE == kModeEval) {
+          a.grad_br[(b * (size_t)a.n_br + H.br0 + j) * 2] = gp;
+          a.grad_br[(b * (size_t)a.n_br + H.br0 + j) * 2 + 1] = gm;
+        }
+      }
+    }
+    cl_sync();
+    // ---------------- C: generators, d/dlambda, lambda' ----------------
+    for (int i = tid; i < nA; i += nthr) {
+      const ClC r = Cr[i];
+      const double li = lam_s[i], di = d_s[i];
+      double gl = -di;
+      for (int gg = r.g0; gg < r.g1; ++gg) {
+        const ClG G = Gr[gg];
+        const double rc = G.c + li;
+        const double p = gen_minimiser(rc, G.lo, G.hi, G.a);
+        gl = gl + p;
+        val += (G.a > 0.0) ? G.a * p * p + rc * p : rc * p;
+      }
+      if (FORM == kFormF2) {
+        const ClIC2 *IC = reinterpret_cast<const ClIC2 *>(smem + H.off_IC);
+        for (int e = r.e0; e < r.e1; ++e) {
+          const ClIC2 x = IC[e];
+          const double f = cl_ld(x.f);
+          gl = (x.sgn > 0) ? gl + f : gl - f;
+        }
+      } else {
+        const ClIC1 *IC = reinterpret_cast<const ClIC1 *>(smem + H.off_IC);
+        for (int e = r.e0; e < r.e1; ++e) {
+          const ClIC1 x = IC[e];
+          gl = gl + x.sb * (cl_ld(x.ts) - cl_ld(x.tt));  // +phi at the to bus, -phi at the from bus
+        }
+      }
+      val += -(li * di);
+      if (step) lam_s[i] = li + alpha * gl;
+      if (MODE == kModeEval) a.grad_lam[b * (size_t)a.n_bus + H.bus0 + i] = gl;
+    }
+    // ---------------- this CTA's partial of g(y_k) ----------------
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
+    if (lane == 0) wred[warp] = val;
+    __syncthreads();
+    if (warp == 0) {
+      double v = (lane < (nthr >> 5)) ? wred[lane] : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) red[0] = v;
+    }
+    if (FORM == kFormF1 || k == K) {
+      cl_sync();  // F1: the next A reads lambda'; and every partial is published
+      finish(k);
+    }
+  }
+  // ---- results -----------------------------------------------------------------
+  if (MODE == kModeStep) {
+    double *lam_o = a.lam + b * (size_t)a.n_bus + H.bus0;
+    double *br_o = a.br + (b * (size_t)a.n_br + H.br0) * BRW;
+    for (int i = tid; i < nA; i += nthr) lam_o[i] = lam_s[i];
+    for (int j = tid; j < nB * BRW; j += nthr) br_o[j] = br_s[j];
+  }
+  if (MODE != kModeEval && rank == 0 && tid == 0) {
+    a.best[b] = best;
+    a.status[b] = flag[0];
+  }
+  cl_sync();  // no CTA exits while another may still read its shared memory
+}
+
+}  // namespace dcopf

@@ -23,6 +23,8 @@
 #include <vector>
 
 #include "../../include/dcopf_dual.h"
+#include "cluster.h"
+#include "cluster_kernel.cuh"
 #include "dual_kernels.cuh"
 #include "schedule.h"
 #include "sweep_kernel.cuh"
@@ -73,6 +75,10 @@ struct dcopf_dual_s {
   long long *d_prog_off = nullptr;
   int *d_prog_bytes = nullptr, *d_tx_bytes = nullptr, *d_ld_ptr = nullptr, *d_ld = nullptr;
   // batched path state layout: storage position <-> original id, per kind
+  // cluster path: per-rank plan blobs
+  ClusterPlan cplan;
+  int cplan_C = 0;
+  uint8_t *d_cblob = nullptr;
   int *d_lam_perm_b = nullptr, *d_lam_inv_b = nullptr, *d_d_perm_b = nullptr, *d_br_perm_b = nullptr,
       *d_br_inv_b = nullptr, *d_br_pos_b = nullptr;
 };
@@ -390,6 +396,98 @@ int configure_single(dcopf_dual_t h) {
   return rc;
 }
 
+// Cluster path: the smallest power-of-two cluster (<= 16 CTAs) whose
+// partition fits one CTA's shared memory with ~640 buses or fewer per CTA and
+// that the device can co-schedule.  Returns DCOPF_EINVAL if none does.
+int configure_cluster(dcopf_dual_t h) {
+  if (h->cplan_C) return DCOPF_OK;
+  int C = 1;
+  while (C < 16 && (long)h->n_bus > 640L * C) C *= 2;
+  if (const char *e = getenv("DCOPF_CLUSTER")) C = std::max(1, std::min(16, atoi(e)));
+  std::string err;
+  for (; C <= 16; C *= 2) {
+    ClusterPlan pl;
+    err = build_cluster_plan(h->ni, C, h->dev_smem, &pl);
+    if (!err.empty()) continue;
+    auto fn = (h->form == DCOPF_FORM_FLOW_BOX) ? k_cluster<kFormF2, kModeStep> : k_cluster<kFormF1, kModeStep>;
+    const void *fns[4] = {(const void *)k_cluster<kFormF2, kModeStep>, (const void *)k_cluster<kFormF2, kModeEval>,
+                          (const void *)k_cluster<kFormF1, kModeStep>, (const void *)k_cluster<kFormF1, kModeEval>};
+    for (const void *f : fns) {
+      CK(h, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+      if (C > 8) CK(h, cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, (const void *)fn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      ncl = 0;
+    }
+    if (ncl < 1) {
+      err = "cluster of " + std::to_string(C) + " CTAs cannot be scheduled";
+      continue;
+    }
+    h->cplan = pl;
+    h->cplan_C = C;
+    int rc = upload(h, &h->d_cblob, h->cplan.blob);
+    std::vector<uint8_t>().swap(h->cplan.blob);
+    return rc;
+  }
+  return fail(h, DCOPF_EINVAL, "cluster path: %s", err.c_str());
+}
+
+ClusterArgs cluster_args(dcopf_dual_t h) {
+  ClusterArgs a;
+  memset(&a, 0, sizeof a);
+  a.blob = h->d_cblob;
+  a.blob_stride = h->cplan.blob_stride;
+  a.lam = h->lam[0];
+  a.br = h->br[0];
+  a.d = h->load;
+  a.outs = h->outs;
+  a.max_out = h->max_out;
+  a.bound = h->bound;
+  a.best = h->best;
+  a.status = h->status;
+  a.B = h->B;
+  a.target = h->has_target ? h->target : nullptr;
+  a.hit = h->hit;
+  a.k_base = h->k_base;
+  a.n_bus = h->n_bus;
+  a.n_br = h->n_br;
+  return a;
+}
+
+template <int MODE>
+int launch_cluster(dcopf_dual_t h, const ClusterArgs &a, cudaStream_t s) {
+  const int C = h->cplan_C;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(h->B * C));
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = h->cplan.smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (h->form == DCOPF_FORM_FLOW_BOX) CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormF2, MODE>, a));
+  else CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormF1, MODE>, a));
+  CK(h, cudaGetLastError());
+  return DCOPF_OK;
+}
+
 SweepArgs sweep_args(dcopf_dual_t h) {
   SweepArgs a;
   memset(&a, 0, sizeof a);
@@ -509,6 +607,7 @@ void dcopf_dual_destroy(dcopf_dual_t h) {
   for (double *p : dp) cudaFree(p);
   cudaFree(h->d_prog);
   cudaFree(h->d_prog_off);
+  cudaFree(h->d_cblob);
   cudaFreeHost(h->alpha_pin);
   if (h->alpha_ev) cudaEventDestroy(h->alpha_ev);
   delete h;
@@ -526,7 +625,7 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
     return fail(nullptr, DCOPF_EINVAL, "unknown form %d", o.form);
   if (o.precision != 64 && o.precision != 0)
     return fail(nullptr, DCOPF_EINVAL, "precision %d not supported (fp64 only)", o.precision);
-  if (o.path < 0 || o.path > 2) return fail(nullptr, DCOPF_EINVAL, "unknown path %d", o.path);
+  if (o.path < 0 || o.path > 3) return fail(nullptr, DCOPF_EINVAL, "unknown path %d", o.path);
   const int nb = net->n_bus, nl = net->n_branch, ng = net->n_gen;
   if (nb < 1 || nl < 0 || ng < 0) return fail(nullptr, DCOPF_EINVAL, "bad sizes n_bus=%d n_branch=%d n_gen=%d", nb, nl, ng);
   if (net->ref_bus < 0 || net->ref_bus >= nb) return fail(nullptr, DCOPF_EINVAL, "ref_bus %d out of range", net->ref_bus);
@@ -683,13 +782,19 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   int path = h->path_opt;
-  if (path == DCOPF_PATH_AUTO) path = (B <= h->single_max) ? DCOPF_PATH_SINGLE : DCOPF_PATH_BATCHED;
+  if (path == DCOPF_PATH_AUTO) {
+    path = (B <= h->single_max) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
+    if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) path = DCOPF_PATH_SINGLE;
+  }
   int W = 1;
   if (path == DCOPF_PATH_BATCHED) {
     // tile width: even, <= 64, so that #tiles ~ #SMs (one CTA per SM)
     W = (int)std::min<int64_t>(64, 2 * ((B + 2LL * h->n_sm - 1) / (2LL * h->n_sm)));
     if (const char *ev = getenv("DCOPF_TILE_W")) W = std::max(2, std::min(64, atoi(ev) & ~1));
     int rc = compile_schedule(h, W);
+    if (rc) return rc;
+  } else if (path == DCOPF_PATH_CLUSTER) {
+    int rc = configure_cluster(h);
     if (rc) return rc;
   } else {
     const size_t ss_state = single_smem(h->n_bus, h->n_br, h->form, true);
@@ -784,12 +889,20 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     if (rc) return rc;
     h->cur = (int)((h->cur + K) & 1);
     h->k_base += (long)K;
-  } else {
+  } else if (h->path == DCOPF_PATH_SINGLE) {
     SingleArgs a = single_args(h);
     a.alpha = h->alpha_dev;
     a.K = K;
     a.hist = hist;
     rc = launch_single<kModeStep>(h, a, s);
+    if (rc) return rc;
+    h->k_base += (long)K;
+  } else {
+    ClusterArgs a = cluster_args(h);
+    a.alpha = h->alpha_dev;
+    a.K = K;
+    a.hist = hist;
+    rc = launch_cluster<kModeStep>(h, a, s);
     if (rc) return rc;
     h->k_base += (long)K;
   }
@@ -888,12 +1001,18 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
     a.g_br = h->g_br;
     a.out_val = h->value;
     rc = launch_sweep<true>(h, a, s);
-  } else {
+  } else if (h->path == DCOPF_PATH_SINGLE) {
     SingleArgs a = single_args(h);
     a.grad_lam = h->g_lam;
     a.grad_br = h->g_br;
     a.value = h->value;
     rc = launch_single<kModeEval>(h, a, s);
+  } else {
+    ClusterArgs a = cluster_args(h);
+    a.grad_lam = h->g_lam;
+    a.grad_br = h->g_br;
+    a.value = h->value;
+    rc = launch_cluster<kModeEval>(h, a, s);
   }
   if (rc) return rc;
   rc = copy_out(h, value, h->value, s);
@@ -954,6 +1073,13 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
     info->copies_per_sweep = h->sch.n_copies;
     info->ring_life = h->sch.ring_life;
     info->tile_width = h->T;
+  } else if (h->path == DCOPF_PATH_CLUSTER) {
+    info->smem_bytes = h->cplan.smem;
+    info->threads_per_block = 1024;
+    info->grid = (int)(h->B * h->cplan_C);
+    info->state_on_chip = 1;
+    info->tile_width = 1;
+    info->cluster_size = h->cplan_C;
   } else if (h->path == DCOPF_PATH_SINGLE) {
     info->smem_bytes = h->smem_single;
     info->threads_per_block = 1024;
@@ -962,6 +1088,7 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
     info->state_on_chip = h->single_smem;
     info->tile_width = 1;
   }
+  if (h->path != DCOPF_PATH_CLUSTER) info->cluster_size = 1;
   return DCOPF_OK;
 }
 

@@ -20,7 +20,7 @@ from . import _build
 
 FORM_F2 = 0  # DCOPF_FORM_FLOW_BOX
 FORM_F1 = 1  # DCOPF_FORM_LIMIT_ROWS
-PATH_AUTO, PATH_BATCHED, PATH_SINGLE = 0, 1, 2
+PATH_AUTO, PATH_BATCHED, PATH_SINGLE, PATH_CLUSTER = 0, 1, 2, 3
 INST_OK, INST_DIVERGED = 0, 1
 ERRORS = {-1: "EINVAL", -2: "ETOPOLOGY", -3: "ECUDA", -4: "ENOMEM", -5: "ESTATE"}
 
@@ -54,7 +54,8 @@ class Info(ctypes.Structure):
                 ("grid", ctypes.c_int32), ("launches_per_iter", ctypes.c_int32),
                 ("state_on_chip", ctypes.c_int32), ("chunk", ctypes.c_int32),
                 ("ring_bus", ctypes.c_int32), ("ring_branch", ctypes.c_int32), ("tile_width", ctypes.c_int32),
-                ("copies_per_sweep", ctypes.c_int32), ("ring_life", ctypes.c_int32)]
+                ("copies_per_sweep", ctypes.c_int32), ("ring_life", ctypes.c_int32),
+                ("cluster_size", ctypes.c_int32)]
 
 
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",

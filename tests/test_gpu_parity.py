@@ -17,7 +17,7 @@ from gpu_helpers import BOUND_RTOL, assert_parity, cost_scale, non_tree_switchab
 
 pytestmark = pytest.mark.gpu
 
-PATHS = [dual.PATH_SINGLE, dual.PATH_BATCHED]
+PATHS = [dual.PATH_SINGLE, dual.PATH_BATCHED, dual.PATH_CLUSTER]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -89,13 +89,61 @@ def test_tiny_batch_ragged(form, path, quad):
 @pytest.mark.parametrize("config,quad,form", [(1, False, FORM_F2), (1, False, FORM_F1), (2, True, FORM_F2),
                                               (2, True, FORM_F1), (3, False, FORM_F2), (3, True, FORM_F2),
                                               (3, False, FORM_F1)])
-def test_large_single_instance_full_K(config, quad, form):
+@pytest.mark.parametrize("path", [dual.PATH_SINGLE, dual.PATH_CLUSTER])
+def test_large_single_instance_full_K(config, quad, form, path):
     net = inst.make_network(config, quadratic=quad)
     K = inst.ITERS[config]
     a = inst.alpha_schedule(K)
+    orc = _oracle_full_K(config, quad, form)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=path, history=True)
+    assert_parity(net, gpu, orc, bitwise_multipliers=(path == dual.PATH_CLUSTER))
+    if path == dual.PATH_CLUSTER:
+        assert gpu["info"].cluster_size >= (8 if config >= 2 else 2)
+
+
+_ORC_CACHE = {}
+
+
+def _oracle_full_K(config, quad, form):
+    key = (config, quad, form)
+    if key not in _ORC_CACHE:
+        net = inst.make_network(config, quadratic=quad)
+        K = inst.ITERS[config]
+        _ORC_CACHE[key] = oracle.solve(net, net.base_load, K=K, alpha=inst.alpha_schedule(K), form=form,
+                                       history=True)
+    return _ORC_CACHE[key]
+
+
+@pytest.mark.parametrize("C", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+def test_cluster_sizes_bitwise(C, form, monkeypatch):
+    """Every cluster size (1..16 CTAs, the partition changes) gives the same
+    bits: the per-entity order never depends on the partition."""
+    monkeypatch.setenv("DCOPF_CLUSTER", str(C))
+    net = inst.tiny_network(600, 900, 150, seed=3)  # fits one CTA (C = 1) as well
+    K = 400
+    a = inst.alpha_schedule(K, 1e-2)
     orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True)
-    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=dual.PATH_SINGLE, history=True)
-    assert_parity(net, gpu, orc)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=dual.PATH_CLUSTER, history=True)
+    assert gpu["info"].cluster_size == C
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+def test_cluster_config4_instances_with_outages(form):
+    """config-4 instances (per-bus load factors, 0-3 non-tree outages) on the
+    cluster path: one cluster per instance, outages applied in shared memory."""
+    net = inst.make_network(4)
+    ids = [0, 1, 2, 3, 4097]
+    batch = inst.config4_batch(net, ids)
+    assert (batch.outages >= 0).any()
+    K = 200
+    a = inst.alpha_schedule(K)
+    orc = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, threads=4, history=True)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, path=dual.PATH_CLUSTER,
+                  switchable=non_tree_switchable(net), history=True)
+    assert gpu["info"].cluster_size == 16
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
 
 
 @pytest.mark.parametrize("config,form", [(1, FORM_F2), (3, FORM_F1)])
@@ -255,8 +303,9 @@ def test_implied_theta_box_matches_generator():
     K = 200
     a = inst.alpha_schedule(K, 1e-2)
     orc = oracle.solve(net, net.base_load, K=K, alpha=a, history=True)
-    gpu = run_gpu(net, net.base_load, K=K, alpha=a, path=dual.PATH_SINGLE, history=True, implied_theta=True)
-    assert_parity(net, gpu, orc)
+    for path in (dual.PATH_SINGLE, dual.PATH_CLUSTER):
+        gpu = run_gpu(net, net.base_load, K=K, alpha=a, path=path, history=True, implied_theta=True)
+        assert_parity(net, gpu, orc)
 
 
 def test_zero_iterations_evaluates_origin():

@@ -506,3 +506,76 @@ def test_literal_config0_pi3_box_is_not_binding():
     a = inst.make_network(0)
     b = inst.make_network(0, theta_mode="implied")
     assert inst.primal_lp(a, a.base_load)[1] == pytest.approx(inst.primal_lp(b, b.base_load)[1], rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# gradient-based-optimisation variants (Algorithm 1 247-272;
+# SPEC.md:326-328): pins from special cases, closed-form first steps, weak
+# duality along every trajectory and convergence to the LP optimum
+
+ADAM = dict(variant=oracle.OPT_ADAM, beta1=0.9, beta2=0.999, eps=1e-8)
+ADAGRAD = dict(variant=oracle.OPT_ADAGRAD, eps=1e-8)
+GDM = dict(variant=oracle.OPT_GDM, rho=0.9)
+GDM_C = dict(variant=oracle.OPT_GDM_CLASSIC, rho=0.9)
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+def test_gdm_classic_without_momentum_is_the_plain_step(form):
+    """rho = 0: v = 0 v + a g = a g exactly, y + v = y + a g: bitwise plain."""
+    net = inst.make_network(0, theta_mode="min")
+    K = 800
+    a = inst.alpha_schedule(K, 1e-2)
+    p = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True)
+    q = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True,
+                     opt=dict(variant=oracle.OPT_GDM_CLASSIC, rho=0.0))
+    np.testing.assert_array_equal(p.lam, q.lam)
+    np.testing.assert_array_equal(p.br, q.br)
+    np.testing.assert_array_equal(p.hist, q.hist)
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+def test_gdm_first_step_is_a_double_plain_step(form):
+    """Algorithm 1 from y_0 = v_0 = 0: v_1 = a g_0, y = a g_0 (velocity
+    update) then y = a g_0 + a g_0 (gradient update) = (2a) g_0 exactly: the
+    plain step with 2a (then mu <- max(mu, 0) on both sides)."""
+    net = inst.make_network(0, theta_mode="min")
+    a = 7e-3
+    g = oracle.solve(net, net.base_load, K=1, alpha=np.array([a]), form=form, opt=dict(GDM, rho=0.37))
+    p = oracle.solve(net, net.base_load, K=1, alpha=np.array([2 * a]), form=form)
+    np.testing.assert_array_equal(g.lam, p.lam)
+    np.testing.assert_array_equal(g.br, p.br)
+
+
+@pytest.mark.parametrize("opt", [ADAM, ADAGRAD, dict(ADAM, beta1=0.0, beta2=0.0)])
+def test_adaptive_first_step_is_a_normalised_sign_step(opt):
+    """Adam (Kingma & Ba) and AdaGrad from zero state: the first step is
+    a g_0 / (|g_0| + eps) per coordinate (bias corrections cancel)."""
+    net = inst.make_network(0, theta_mode="min")
+    a = 0.05
+    _, g0l, g0b = oracle.evaluate(net, net.base_load, np.zeros((1, net.n_bus)), np.zeros((1, net.n_branch)))
+    r = oracle.solve(net, net.base_load, K=1, alpha=np.array([a]), opt=opt)
+    g0 = np.r_[g0l[0], g0b[0]]
+    y1 = np.r_[r.lam[0], r.br[0]]
+    expect = a * g0 / (np.abs(g0) + opt["eps"])
+    assert np.max(np.abs(y1 - expect)) <= 1e-15 * a * 4
+    nz = np.abs(g0) > 1e-3
+    assert np.allclose(np.abs(y1[nz]), a, rtol=1e-5)   # magnitude ~ a wherever |g| >> eps
+
+
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+@pytest.mark.parametrize("opt,alpha", [(ADAM, 0.1), (ADAGRAD, 3.0), (GDM, 1e-3), (GDM_C, 3e-3)])
+def test_variants_weak_duality_and_convergence(form, opt, alpha):
+    """Every iterate of every variant is a valid lower bound (PAPER.md:135:
+    any lambda, nu and mu >= 0), and with a reasonable step each reaches the
+    HiGHS LP optimum of config 0 within 2% (Tables 1-3 report gaps
+    of 1e-4 .. 1% for the tuned IEEE runs; this is a sanity bar)."""
+    net = inst.make_network(0, theta_mode="min")
+    _, opt_val = inst.primal_lp(net, net.base_load)
+    K = 20000
+    r = oracle.solve(net, net.base_load, K=K, alpha=inst.alpha_schedule(K, alpha), form=form, history=True,
+                     opt=opt)
+    assert r.status[0] == 0
+    assert np.all(r.hist[0] <= opt_val + 1e-9 * abs(opt_val))
+    assert r.best[0] >= (0.98 if form == FORM_F2 else 0.95) * opt_val, r.best[0]
+    if form == FORM_F1:
+        assert np.all(r.br >= 0.0)
