@@ -165,6 +165,33 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
 int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, double *grad_branch,
                         void *cuda_stream);
 
+/* Gradient-based-optimisation variant of the ascent step ("Adam
+ * ... AdaGrad ... Gradient with Momentum", Algorithm 1 PAPER.md:247-272;
+ * SURVEY.md NEXT-2), per multiplier coordinate y with gradient g and the
+ * schedule's step a_k, followed by mu <- max(mu, 0):
+ *   PLAIN        y <- y + a_k g                                  (default)
+ *   GDM          v <- rho v + a_k g; y <- y + v; y <- y + a_k g   (Algorithm 1 as printed)
+ *   GDM_CLASSIC  v <- rho v + a_k g; y <- y + v
+ *   ADAGRAD      G <- G + g g; y <- y + (a_k g) / (sqrt(G) + eps)
+ *   ADAM         m <- b1 m + (1-b1) g; v <- b2 v + (1-b2)(g g);
+ *                y <- y + (a_k (m / (1 - b1^t))) / (sqrt(v / (1 - b2^t)) + eps),
+ *                t = steps since the state was reset (b^t by repeated products)
+ * Optimiser state starts at 0 and persists across iterate() calls; it is reset
+ * by set_instance_batch() and by this call.  Variants other than PLAIN run on
+ * the cluster path only (AUTO selects it for them; iterate() on another path
+ * fails with ESTATE).  Errors: EINVAL (unknown variant, rho/b1/b2 outside
+ * [0, 1), eps < 0, or the cluster partition plus the optimiser state does not
+ * fit shared memory). */
+enum { DCOPF_OPT_PLAIN = 0, DCOPF_OPT_GDM = 1, DCOPF_OPT_GDM_CLASSIC = 2, DCOPF_OPT_ADAGRAD = 3, DCOPF_OPT_ADAM = 4 };
+typedef struct {
+  int32_t variant;   /* DCOPF_OPT_* */
+  int32_t reserved;  /* zero */
+  double momentum;   /* rho (GDM variants) */
+  double beta1, beta2;
+  double epsilon;    /* AdaGrad / Adam guard (SPEC.md:359 suggests 1e-8) */
+} dcopf_optimizer;
+int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt);
+
 /* Time to gap (BASELINE.json metric "time to 1e-3 gap"):
  * per-instance thresholds target[B] (host or device; NULL clears them).  The
  * kernels then record, per instance, the index k of the FIRST evaluation whose

@@ -11,7 +11,7 @@ inline int al16(int x) { return (x + 15) & ~15; }
 inline unsigned enc(int rank, int off) { return ((unsigned)rank << kClAddrShift) | (unsigned)off; }
 }  // namespace
 
-std::string build_cluster_plan(const NetInternal &net, int C, int max_smem, ClusterPlan *out) {
+std::string build_cluster_plan(const NetInternal &net, int C, int max_smem, int nstate, ClusterPlan *out) {
   ClusterPlan &P = *out;
   const int nb = net.nb, nl = net.nl;
   const bool f1 = net.form == 1;
@@ -90,6 +90,18 @@ std::string build_cluster_plan(const NetInternal &net, int C, int max_smem, Clus
   off = al16(off + NL * 8);
   H.off_red = off;  // [0] partial value, [8..40) per-warp partials, [40] frozen flag
   off = al16(off + 512);
+  if (nstate >= 1) {
+    H.off_s1l = off;
+    off = al16(off + NB * 8);
+    H.off_s1b = off;
+    off = al16(off + NL * 8 * BRW);
+  }
+  if (nstate >= 2) {
+    H.off_s2l = off;
+    off = al16(off + NB * 8);
+    H.off_s2b = off;
+    off = al16(off + NL * 8 * BRW);
+  }
   H.blob_bytes = blob;
   P.smem = off;
   if (P.smem > max_smem) return "cluster partition does not fit shared memory";

@@ -34,7 +34,8 @@ struct ClHeader {
   int off_A, off_IA, off_B, off_C, off_IC, off_G;       // record arrays (bytes)
   int off_lam, off_d, off_br, off_th, off_fc, off_red;  // state arrays (bytes)
   int blob_bytes;               // records + header (copied from global)
-  int pad[11];
+  int off_s1l, off_s2l, off_s1b, off_s2b;  // optimiser state (lambda / branch), 0 if absent
+  int pad[7];
 };
 static_assert(sizeof(ClHeader) == 128, "ClHeader is 128 bytes");
 
@@ -58,6 +59,7 @@ struct ClusterPlan {
 
 // Partition the internal network over C CTAs and lay out their shared memory.
 // Returns "" or an error (e.g. a partition does not fit max_smem).
-std::string build_cluster_plan(const NetInternal &net, int C, int max_smem, ClusterPlan *out);
+// nstate: optimiser state arrays per multiplier (0 plain, 1 GDM / AdaGrad, 2 Adam).
+std::string build_cluster_plan(const NetInternal &net, int C, int max_smem, int nstate, ClusterPlan *out);
 
 }  // namespace dcopf

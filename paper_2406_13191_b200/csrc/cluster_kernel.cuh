@@ -21,6 +21,7 @@
 // of k_single / k_sweep (reading A-19): sums over a bus's incidence in
 // ascending original branch id, generators before branches, y + (alpha*g).
 #pragma once
+#include "../../include/dcopf_dual.h"
 #include "cluster.h"
 #include "dual_kernels.cuh"
 
@@ -44,7 +45,48 @@ struct ClusterArgs {
   long k_base;
   double *grad_lam, *grad_br, *value;  // EVAL outputs (instance-major) or null
   int n_bus, n_br;
+  // ascent-step variant (dcopf_dual.h DCOPF_OPT_*) and its persistent state
+  int opt;
+  double rho, beta1, beta2, eps;
+  double b1t, b2t;              // beta1^t, beta2^t at this launch's first step (Adam)
+  double *s1_lam, *s2_lam;      // [b][n_bus] instance-major internal, or null
+  double *s1_br, *s2_br;        // [b][n_br * BRW]
 };
+
+// One coordinate of the ascent step for the gradient-based-optimisation
+// variants (Algorithm 1; the oracle's opt_step, same operation
+// order, no contraction).
+__device__ __forceinline__ double opt_step(const ClusterArgs &a, double y, double g, double al, double *s1,
+                                           double *s2, double b1t, double b2t) {
+  switch (a.opt) {
+    case DCOPF_OPT_GDM: {
+      const double v = a.rho * *s1 + al * g;
+      *s1 = v;
+      y = y + v;
+      return y + al * g;
+    }
+    case DCOPF_OPT_GDM_CLASSIC: {
+      const double v = a.rho * *s1 + al * g;
+      *s1 = v;
+      return y + v;
+    }
+    case DCOPF_OPT_ADAGRAD: {
+      const double G = *s1 + g * g;
+      *s1 = G;
+      return y + (al * g) / (sqrt(G) + a.eps);
+    }
+    case DCOPF_OPT_ADAM: {
+      const double m = a.beta1 * *s1 + (1.0 - a.beta1) * g;
+      const double v = a.beta2 * *s2 + (1.0 - a.beta2) * (g * g);
+      *s1 = m;
+      *s2 = v;
+      const double mh = m / (1.0 - b1t), vh = v / (1.0 - b2t);
+      return y + (al * mh) / (sqrt(vh) + a.eps);
+    }
+    default:
+      return y + al * g;
+  }
+}
 
 __device__ __forceinline__ unsigned cl_rank() {
   unsigned r;
@@ -160,6 +202,23 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
     d_s[i] = d_g[i];
   }
   for (int j = tid; j < nB * BRW; j += nthr) br_s[j] = br_g[j];
+  // optimiser state (same layout as the multipliers)
+  const bool ost = (MODE == kModeStep) && a.opt != DCOPF_OPT_PLAIN;
+  const bool ost2 = ost && a.opt == DCOPF_OPT_ADAM;
+  double *s1l = reinterpret_cast<double *>(smem + H.off_s1l), *s2l = reinterpret_cast<double *>(smem + H.off_s2l);
+  double *s1b = reinterpret_cast<double *>(smem + H.off_s1b), *s2b = reinterpret_cast<double *>(smem + H.off_s2b);
+  if (ost) {
+    const size_t ol = b * (size_t)a.n_bus + H.bus0, ob = (b * (size_t)a.n_br + H.br0) * BRW;
+    for (int i = tid; i < nA; i += nthr) {
+      s1l[i] = a.s1_lam[ol + i];
+      if (ost2) s2l[i] = a.s2_lam[ol + i];
+    }
+    for (int j = tid; j < nB * BRW; j += nthr) {
+      s1b[j] = a.s1_br[ob + j];
+      if (ost2) s2b[j] = a.s2_br[ob + j];
+    }
+  }
+  double b1t = a.b1t, b2t = a.b2t;
   if (tid == 0) flag[0] = (MODE != kModeEval) ? a.status[b] : 0;
   double best = (MODE != kModeEval) ? a.best[b] : 0.0;
   __syncthreads();
@@ -200,6 +259,10 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
 
   for (long k = 0; k <= K; ++k) {
     const double alpha = (k < K) ? a.alpha[k] : 0.0;
+    if (ost2 && k < K) {  // Adam's beta^t, t = steps since the state was reset
+      b1t = b1t * a.beta1;
+      b2t = b2t * a.beta2;
+    }
     double val = 0.0;
     // ---------------- A: w_i, theta*_i ----------------
     for (int i = tid; i < nA; i += nthr) {
@@ -238,14 +301,16 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
         fc_s[j] = f;
         const double g = f - phi;  // Kirchhoff residual
         val += q * f;
-        if (step) br_s[j] = nu + alpha * g;
+        if (step) br_s[j] = ost ? opt_step(a, nu, g, alpha, &s1b[j], &s2b[j], b1t, b2t) : nu + alpha * g;
         if (MODE == kModeEval) a.grad_br[b * (size_t)a.n_br + H.br0 + j] = g;
       } else {
         const double mp = br_s[2 * j], mm = br_s[2 * j + 1];
         const double gp = phi - r.F, gm = -phi - r.F;
         val += -(r.F * (mp + mm));
         if (step) {
-          const double vp = mp + alpha * gp, vm = mm + alpha * gm;
+          const double vp = ost ? opt_step(a, mp, gp, alpha, &s1b[2 * j], &s2b[2 * j], b1t, b2t) : mp + alpha * gp;
+          const double vm =
+              ost ? opt_step(a, mm, gm, alpha, &s1b[2 * j + 1], &s2b[2 * j + 1], b1t, b2t) : mm + alpha * gm;
           br_s[2 * j] = (vp > 0.0) ? vp : 0.0;  // mu <- max(mu, 0)
           br_s[2 * j + 1] = (vm > 0.0) ? vm : 0.0;
         }
@@ -283,7 +348,7 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
         }
       }
       val += -(li * di);
-      if (step) lam_s[i] = li + alpha * gl;
+      if (step) lam_s[i] = ost ? opt_step(a, li, gl, alpha, &s1l[i], &s2l[i], b1t, b2t) : li + alpha * gl;
       if (MODE == kModeEval) a.grad_lam[b * (size_t)a.n_bus + H.bus0 + i] = gl;
     }
     // ---------------- this CTA's partial of g(y_k) ----------------
@@ -308,6 +373,17 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
     double *br_o = a.br + (b * (size_t)a.n_br + H.br0) * BRW;
     for (int i = tid; i < nA; i += nthr) lam_o[i] = lam_s[i];
     for (int j = tid; j < nB * BRW; j += nthr) br_o[j] = br_s[j];
+    if (ost) {
+      const size_t ol = b * (size_t)a.n_bus + H.bus0, ob = (b * (size_t)a.n_br + H.br0) * BRW;
+      for (int i = tid; i < nA; i += nthr) {
+        a.s1_lam[ol + i] = s1l[i];
+        if (ost2) a.s2_lam[ol + i] = s2l[i];
+      }
+      for (int j = tid; j < nB * BRW; j += nthr) {
+        a.s1_br[ob + j] = s1b[j];
+        if (ost2) a.s2_br[ob + j] = s2b[j];
+      }
+    }
   }
   if (MODE != kModeEval && rank == 0 && tid == 0) {
     a.best[b] = best;

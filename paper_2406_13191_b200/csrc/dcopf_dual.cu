@@ -75,6 +75,10 @@ struct dcopf_dual_s {
   long long *d_prog_off = nullptr;
   int *d_prog_bytes = nullptr, *d_tx_bytes = nullptr, *d_ld_ptr = nullptr, *d_ld = nullptr;
   // batched path state layout: storage position <-> original id, per kind
+  // ascent-step variant (set_optimizer) and its persistent state (cluster path)
+  dcopf_optimizer opt = {DCOPF_OPT_PLAIN, 0, 0.0, 0.0, 0.0, 0.0};
+  double *os[4] = {nullptr, nullptr, nullptr, nullptr};  // s1_lam, s2_lam, s1_br, s2_br
+  double b1t = 1.0, b2t = 1.0;                            // beta^t after the steps taken so far
   // cluster path: per-rank plan blobs
   ClusterPlan cplan;
   int cplan_C = 0;
@@ -171,7 +175,8 @@ void free_batch(dcopf_dual_t h) {
     cudaFree(h->br[i]);
     h->lam[i] = h->br[i] = nullptr;
   }
-  double **dp[] = {&h->load, &h->bound, &h->best, &h->value, &h->g_lam, &h->g_br};
+  double **dp[] = {&h->load, &h->bound, &h->best, &h->value, &h->g_lam, &h->g_br, &h->os[0], &h->os[1], &h->os[2],
+                   &h->os[3]};
   for (double **p : dp) {
     cudaFree(*p);
     *p = nullptr;
@@ -396,6 +401,31 @@ int configure_single(dcopf_dual_t h) {
   return rc;
 }
 
+int opt_nstate(dcopf_dual_t h) {
+  switch (h->opt.variant) {
+    case DCOPF_OPT_PLAIN: return 0;
+    case DCOPF_OPT_ADAM: return 2;
+    default: return 1;
+  }
+}
+
+// optimiser state arrays of the loaded batch (cluster path), zeroed
+int reset_opt_state(dcopf_dual_t h, cudaStream_t s) {
+  h->b1t = h->b2t = 1.0;
+  const int ns = opt_nstate(h);
+  if (h->B == 0 || h->path != DCOPF_PATH_CLUSTER || ns == 0) return DCOPF_OK;
+  const size_t n[4] = {(size_t)h->B * h->n_bus, (size_t)h->B * h->n_bus, (size_t)h->B * h->n_br * brw(h->form),
+                       (size_t)h->B * h->n_br * brw(h->form)};
+  for (int x = 0; x < 4; ++x) {
+    if (x == 1 || x == 3) {
+      if (ns < 2) continue;
+    }
+    if (!h->os[x]) CK(h, cudaMalloc(&h->os[x], std::max<size_t>(n[x], 1) * 8));
+    CK(h, cudaMemsetAsync(h->os[x], 0, std::max<size_t>(n[x], 1) * 8, s));
+  }
+  return DCOPF_OK;
+}
+
 // Cluster path: the smallest power-of-two cluster (<= 16 CTAs) whose
 // partition fits one CTA's shared memory with ~640 buses or fewer per CTA and
 // that the device can co-schedule.  Returns DCOPF_EINVAL if none does.
@@ -407,7 +437,7 @@ int configure_cluster(dcopf_dual_t h) {
   std::string err;
   for (; C <= 16; C *= 2) {
     ClusterPlan pl;
-    err = build_cluster_plan(h->ni, C, h->dev_smem, &pl);
+    err = build_cluster_plan(h->ni, C, h->dev_smem, opt_nstate(h), &pl);
     if (!err.empty()) continue;
     auto fn = (h->form == DCOPF_FORM_FLOW_BOX) ? k_cluster<kFormF2, kModeStep> : k_cluster<kFormF1, kModeStep>;
     const void *fns[4] = {(const void *)k_cluster<kFormF2, kModeStep>, (const void *)k_cluster<kFormF2, kModeEval>,
@@ -464,6 +494,17 @@ ClusterArgs cluster_args(dcopf_dual_t h) {
   a.k_base = h->k_base;
   a.n_bus = h->n_bus;
   a.n_br = h->n_br;
+  a.opt = h->opt.variant;
+  a.rho = h->opt.momentum;
+  a.beta1 = h->opt.beta1;
+  a.beta2 = h->opt.beta2;
+  a.eps = h->opt.epsilon;
+  a.b1t = h->b1t;
+  a.b2t = h->b2t;
+  a.s1_lam = h->os[0];
+  a.s2_lam = h->os[1];
+  a.s1_br = h->os[2];
+  a.s2_br = h->os[3];
   return a;
 }
 
@@ -783,7 +824,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   cudaStream_t s = (cudaStream_t)cuda_stream;
   int path = h->path_opt;
   if (path == DCOPF_PATH_AUTO) {
-    path = (B <= h->single_max) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
+    path = (B <= h->single_max || h->opt.variant != DCOPF_OPT_PLAIN) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
     if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) path = DCOPF_PATH_SINGLE;
   }
   int W = 1;
@@ -861,6 +902,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   k_fill_d<<<grid_for(B_pad), 256, 0, s>>>(h->bound, std::numeric_limits<double>::quiet_NaN(), B_pad);
   k_fill_i<<<grid_for(B_pad), 256, 0, s>>>(h->status, 0, B_pad);
   CK(h, cudaMemsetAsync(h->hit, 0xff, B_pad * 8, s));  // -1
+  if (int rc2 = reset_opt_state(h, s)) return rc2;
   CK(h, cudaGetLastError());
   return DCOPF_OK;
 }
@@ -878,6 +920,8 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     if (rc) return rc;
     hist = h->scratch;
   }
+  if (h->opt.variant != DCOPF_OPT_PLAIN && h->path != DCOPF_PATH_CLUSTER)
+    return fail(h, DCOPF_ESTATE, "optimiser variants run on the cluster path only");
   int rc = stage_alpha(h, K, alpha, s);
   if (rc) return rc;
   if (h->path == DCOPF_PATH_BATCHED) {
@@ -905,6 +949,11 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     rc = launch_cluster<kModeStep>(h, a, s);
     if (rc) return rc;
     h->k_base += (long)K;
+    if (h->opt.variant == DCOPF_OPT_ADAM)
+      for (int64_t k = 0; k < K; ++k) {  // the kernel's repeated products, continued
+        h->b1t = h->b1t * h->opt.beta1;
+        h->b2t = h->b2t * h->opt.beta2;
+      }
   }
   if (hist_host) {
     CK(h, cudaMemcpyAsync(history, hist, (size_t)K * h->B * 8, cudaMemcpyDefault, s));
@@ -1019,6 +1068,33 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
   const Perms pm = perms(h);
   if (!rc) rc = export_ext(h, h->g_lam, grad_lambda, pm.lam_inv, h->n_bus, 1, s);
   if (!rc) rc = export_ext(h, h->g_br, grad_branch, pm.br_inv, h->n_br, brw(h->form), s);
+  return rc;
+}
+
+int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt) {
+  if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
+  dcopf_optimizer o = {DCOPF_OPT_PLAIN, 0, 0.0, 0.0, 0.0, 0.0};
+  if (opt) o = *opt;
+  if (o.variant < DCOPF_OPT_PLAIN || o.variant > DCOPF_OPT_ADAM)
+    return fail(h, DCOPF_EINVAL, "unknown optimiser variant %d", o.variant);
+  auto unit = [](double x) { return std::isfinite(x) && x >= 0.0 && x < 1.0; };
+  if (!unit(o.momentum) || !unit(o.beta1) || !unit(o.beta2) || !(o.epsilon >= 0.0) || !std::isfinite(o.epsilon))
+    return fail(h, DCOPF_EINVAL, "momentum, beta1, beta2 must be in [0, 1) and epsilon finite >= 0");
+  if (h->B > 0 && h->path != DCOPF_PATH_CLUSTER && o.variant != DCOPF_OPT_PLAIN)
+    return fail(h, DCOPF_EINVAL, "optimiser variants run on the cluster path: set the optimiser before "
+                                 "set_instance_batch (AUTO then selects it) or use DCOPF_PATH_CLUSTER");
+  CK(h, cudaSetDevice(h->device));
+  const int ns_old = opt_nstate(h);
+  h->opt = o;
+  if (opt_nstate(h) != ns_old) {  // the shared-memory plan holds the state arrays: rebuild it
+    h->cplan_C = 0;
+    if (h->B > 0 && h->path == DCOPF_PATH_CLUSTER) {
+      int rc = configure_cluster(h);
+      if (rc) return rc;
+    }
+  }
+  int rc = reset_opt_state(h, nullptr);
+  if (!rc) CK(h, cudaDeviceSynchronize());
   return rc;
 }
 

@@ -22,6 +22,7 @@ FORM_F2 = 0  # DCOPF_FORM_FLOW_BOX
 FORM_F1 = 1  # DCOPF_FORM_LIMIT_ROWS
 PATH_AUTO, PATH_BATCHED, PATH_SINGLE, PATH_CLUSTER = 0, 1, 2, 3
 INST_OK, INST_DIVERGED = 0, 1
+OPT_PLAIN, OPT_GDM, OPT_GDM_CLASSIC, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2, 3, 4
 ERRORS = {-1: "EINVAL", -2: "ETOPOLOGY", -3: "ECUDA", -4: "ENOMEM", -5: "ESTATE"}
 
 
@@ -58,9 +59,14 @@ class Info(ctypes.Structure):
                 ("cluster_size", ctypes.c_int32)]
 
 
+class Optimizer(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int32), ("reserved", ctypes.c_int32), ("momentum", ctypes.c_double),
+                ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("epsilon", ctypes.c_double)]
+
+
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",
            "dcopf_dual_get_bound", "dcopf_dual_get_multipliers", "dcopf_dual_set_multipliers",
-           "dcopf_dual_evaluate", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info",
+           "dcopf_dual_evaluate", "dcopf_dual_set_optimizer", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info",
            "dcopf_dual_last_error", "dcopf_dual_destroy"]
 
 _lib = None
@@ -83,6 +89,8 @@ def load_library(path: Optional[str] = None):
     lib.dcopf_dual_get_multipliers.argtypes = [P, P, P, P]
     lib.dcopf_dual_set_multipliers.argtypes = [P, P, P, P]
     lib.dcopf_dual_evaluate.argtypes = [P, P, P, P, P]
+    if hasattr(lib, "dcopf_dual_set_optimizer"):
+        lib.dcopf_dual_set_optimizer.argtypes = [P, ctypes.POINTER(Optimizer)]
     if hasattr(lib, "dcopf_dual_set_target"):
         lib.dcopf_dual_set_target.argtypes = [P, P, P]
         lib.dcopf_dual_get_first_hit.argtypes = [P, P, P]
@@ -196,6 +204,12 @@ class DcopfDual:
     def evaluate(self, value=None, grad_lam=None, grad_branch=None, stream=None):
         self._check(self.lib.dcopf_dual_evaluate(self.h, _ptr(value), _ptr(grad_lam), _ptr(grad_branch),
                                                  _stream(stream)))
+
+    def set_optimizer(self, variant=OPT_PLAIN, momentum=0.0, beta1=0.0, beta2=0.0, epsilon=0.0):
+        """Ascent-step variant (Algorithm 1); resets its state."""
+        o = Optimizer()
+        o.variant, o.momentum, o.beta1, o.beta2, o.epsilon = int(variant), momentum, beta1, beta2, epsilon
+        self._check(self.lib.dcopf_dual_set_optimizer(self.h, ctypes.byref(o)))
 
     def set_target(self, target=None, stream=None):
         """Per-instance time-to-gap thresholds [B] (None clears them)."""

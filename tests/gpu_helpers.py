@@ -20,13 +20,16 @@ def cost_scale(net):
 
 
 def run_gpu(net, loads, outages=None, K=0, alpha=None, form=0, path=dual.PATH_AUTO, history=False,
-            lam0=None, br0=None, implied_theta=False, switchable=None):
+            lam0=None, br0=None, implied_theta=False, switchable=None, opt=None, split=None):
     """loads [B][n_bus] (instance-major, like the oracle); returns instance-major results."""
     import torch
     dev = torch.device("cuda:0")
     loads = np.atleast_2d(loads)
     B = loads.shape[0]
     h = dual.DcopfDual(net, form=form, path=path, implied_theta=implied_theta, switchable=switchable)
+    if opt is not None:  # oracle-style dict(variant=, rho=, beta1=, beta2=, eps=)
+        h.set_optimizer(opt.get("variant", 0), opt.get("rho", 0.0), opt.get("beta1", 0.0), opt.get("beta2", 0.0),
+                        opt.get("eps", 0.0))
     ld = torch.from_numpy(np.ascontiguousarray(loads.T)).to(dev)
     out = None if outages is None else torch.from_numpy(np.ascontiguousarray(outages, dtype=np.int32)).to(dev)
     h.set_instance_batch(ld, out)
@@ -36,7 +39,11 @@ def run_gpu(net, loads, outages=None, K=0, alpha=None, form=0, path=dual.PATH_AU
                           torch.from_numpy(np.ascontiguousarray(np.atleast_2d(br0).T)).to(dev))
     hist = torch.empty((K, B), dtype=torch.float64, device=dev) if history else None
     a = alpha if alpha is not None else np.zeros(0)
-    h.iterate(K, a, hist)
+    if split:  # K steps as two iterate() calls (state and counters must carry over)
+        h.iterate(split, a[:split], None if hist is None else hist[:split])
+        h.iterate(K - split, a[split:], None if hist is None else hist[split:])
+    else:
+        h.iterate(K, a, hist)
     bound = torch.empty(B, dtype=torch.float64, device=dev)
     best = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)

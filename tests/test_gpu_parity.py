@@ -374,3 +374,71 @@ def test_first_hit_cleared_by_new_batch():
     with pytest.raises(dual.DcopfError):
         h.set_target(np.array([np.nan]))
     h.close()
+
+
+# ---------------------------------------------------------------------------
+# gradient-based-optimisation variants (Algorithm 1) on the
+# cluster path: bitwise multipliers against the oracle's variants
+
+OPTS = {
+    "gdm": (dict(variant=oracle.OPT_GDM, rho=0.9), 1e-3),
+    "gdm_classic": (dict(variant=oracle.OPT_GDM_CLASSIC, rho=0.8), 3e-3),
+    "adagrad": (dict(variant=oracle.OPT_ADAGRAD, eps=1e-8), 3.0),
+    "adam": (dict(variant=oracle.OPT_ADAM, beta1=0.9, beta2=0.999, eps=1e-8), 0.1),
+}
+
+
+@pytest.mark.parametrize("name", sorted(OPTS))
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+def test_optimizer_variants_config0(name, form):
+    opt, alpha = OPTS[name]
+    net = inst.make_network(0, theta_mode="min")
+    K = 3000
+    a = inst.alpha_schedule(K, alpha)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True, opt=opt)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=dual.PATH_CLUSTER, history=True, opt=opt,
+                  split=1234)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("name", sorted(OPTS))
+def test_optimizer_variants_batch_with_outages(name):
+    opt, alpha = OPTS[name]
+    net = inst.tiny_network(23, 37, 30, seed=5)
+    rng = np.random.default_rng(2)
+    B = 6
+    loads = net.base_load[None, :] * rng.uniform(0.7, 1.3, (B, net.n_bus))
+    outs = np.full((B, 2), -1, np.int32)
+    for j in range(B):
+        if j % 3:
+            outs[j, :j % 3] = rng.choice(np.arange(net.n_tree, net.n_branch), j % 3, replace=False)
+    K = 1500
+    a = inst.alpha_schedule(K, alpha) * np.linspace(1.0, 0.3, K)  # with a step decay
+    for form in (FORM_F2, FORM_F1):
+        orc = oracle.solve(net, loads, outages=outs, K=K, alpha=a, form=form, history=True, opt=opt)
+        gpu = run_gpu(net, loads, outages=outs, K=K, alpha=a, form=form, history=True, opt=opt)  # AUTO
+        assert gpu["info"].path == dual.PATH_CLUSTER
+        assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+def test_optimizer_adam_config3_cluster16():
+    opt, alpha = OPTS["adam"]
+    net = inst.make_network(3)
+    K = 1000
+    a = inst.alpha_schedule(K, alpha)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, history=True, opt=opt)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, path=dual.PATH_CLUSTER, history=True, opt=opt)
+    assert gpu["info"].cluster_size == 16
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+def test_optimizer_rejected_off_the_cluster_path():
+    import torch
+    net = inst.make_network(0)
+    h = dual.DcopfDual(net, path=dual.PATH_BATCHED)
+    h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(np.tile(net.base_load[:, None], (1, 4)))).cuda())
+    with pytest.raises(dual.DcopfError):
+        h.set_optimizer(dual.OPT_ADAM, beta1=0.9, beta2=0.999, epsilon=1e-8)
+    with pytest.raises(dual.DcopfError):
+        h.set_optimizer(99)
+    h.close()
