@@ -50,6 +50,24 @@ WORKLOADS = {
     "config4b": (4, False, inst.CONFIG4_BATCH),
 }
 METRIC = "dual-ascent instance-iterations/sec"
+# ascent-step variants: (oracle/library variant id, hyperparameters, default step)
+OPTS = {
+    "plain": (0, {}, 1e-3),
+    "gdm": (1, {"rho": 0.9}, 1e-3),
+    "gdm_classic": (2, {"rho": 0.9}, 1e-3),
+    "adagrad": (3, {"eps": 1e-8}, 1.0),
+    "adam": (4, {"beta1": 0.9, "beta2": 0.999, "eps": 1e-8}, 0.1),
+}
+
+
+def opt_spec(args):
+    v, hp, a0 = OPTS[args.opt]
+    return dict(variant=v, **hp), (args.alpha if args.alpha is not None else a0)
+
+
+def gap_key(args):
+    _, alpha = opt_spec(args)
+    return f"{args.workload}/{args.form}" + ("" if args.opt == "plain" else f"/{args.opt}/{alpha:g}")
 UNIT = "instance-iterations/s"
 
 
@@ -65,6 +83,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap run (the workload's full K)")
+    ap.add_argument("--opt", default="plain", choices=sorted(OPTS),
+                    help="ascent-step variant (PAPER.md:245); non-plain variants run on the cluster path")
+    ap.add_argument("--alpha", type=float, default=None, help="constant step (default: the variant's)")
     return ap.parse_args()
 
 
@@ -139,7 +160,7 @@ def make_inputs(workload, lo, hi):
     return net, batch
 
 
-def cpu_oracle_rate(net, batch, form, cores, target_s=12.0):
+def cpu_oracle_rate(net, batch, form, cores, target_s=12.0, opt=None):
     """The oracle as it stands, timed on this host's cores over a bounded
     sample of the workload (instances x iterations), inst-it/s."""
     import oracle
@@ -151,11 +172,11 @@ def cpu_oracle_rate(net, batch, form, cores, target_s=12.0):
     # calibrate the iteration count to ~target_s of wall time
     K0 = 20
     t0 = time.perf_counter()
-    oracle.solve(net, loads, outages=outs, K=K0, alpha=inst.alpha_schedule(K0), form=form, threads=cores)
+    oracle.solve(net, loads, outages=outs, K=K0, alpha=inst.alpha_schedule(K0), form=form, threads=cores, opt=opt)
     dt = max(time.perf_counter() - t0, 1e-6)
     K = int(max(K0, min(200000, K0 * target_s / dt)))
     t0 = time.perf_counter()
-    oracle.solve(net, loads, outages=outs, K=K, alpha=inst.alpha_schedule(K), form=form, threads=cores)
+    oracle.solve(net, loads, outages=outs, K=K, alpha=inst.alpha_schedule(K), form=form, threads=cores, opt=opt)
     dt = time.perf_counter() - t0
     return n_inst * K / dt, f"{n_inst} instances x {K} iterations ({dt:.1f} s wall)"
 
@@ -163,7 +184,7 @@ def cpu_oracle_rate(net, batch, form, cores, target_s=12.0):
 def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, dev, rel=1e-3):
     import torch
     import torch.distributed as tdist
-    key = f"{args.workload}/{args.form}"
+    key = gap_key(args)
     try:
         ref = json.load(open(os.path.join(ROOT, "tests", "golden", "targets.json")))[key]
     except (OSError, KeyError):
@@ -227,7 +248,7 @@ def run_reference(args):
     a = inst.alpha_schedule(K_s)
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.solve(net, loads, outages=outs, K=K_s, alpha=a, form=form, threads=cores)
+        oracle.solve(net, loads, outages=outs, K=K_s, alpha=a, form=form, threads=cores, opt=opt_spec(args)[0])
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             per_step.append(dt)
@@ -275,14 +296,20 @@ def main():
     if config == 4:
         sw = np.zeros(net.n_branch, np.uint8)
         sw[net.n_tree:] = 1
+    ospec, alpha0 = opt_spec(args)
+    if args.opt != "plain":
+        path = dual.PATH_CLUSTER
     h = dual.DcopfDual(net, form=form, device=local, path=path, switchable=sw)
+    if args.opt != "plain":
+        h.set_optimizer(ospec["variant"], ospec.get("rho", 0.0), ospec.get("beta1", 0.0), ospec.get("beta2", 0.0),
+                        ospec.get("eps", 0.0))
     stream = torch.cuda.current_stream(dev)
     load_dev = torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev)
     outs_dev = None if batch.outages is None else torch.from_numpy(batch.outages).to(dev)
     h.set_instance_batch(load_dev, outs_dev, stream=stream)
     info = h.info()
     K, W = args.steps, args.warmup
-    alpha = inst.alpha_schedule(max(K, W, 1))
+    alpha = inst.alpha_schedule(max(K, W, 1), alpha0)
 
     def barrier():
         if world > 1:
@@ -379,7 +406,7 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            rate, sample = cpu_oracle_rate(net, batch, form, cores)
+            rate, sample = cpu_oracle_rate(net, batch, form, cores, opt=ospec)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -387,6 +414,7 @@ def main():
             "scaling": "strong" if B_total > 1 else "replicas",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE.json recipe)",
             "config": {"workload": args.workload, "form": args.form, "cost": "QP" if quad else "LP",
+                       "step": {"variant": args.opt, "alpha": alpha0, **OPTS[args.opt][1]},
                        "n_bus": net.n_bus, "n_branch": net.n_branch, "n_gen": net.n_gen,
                        "B_total": B_total, "B_per_gpu": B,
                        "path": {1: "batched-sweep", 2: "single", 3: "cluster"}[path],

@@ -412,7 +412,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
       const int a1 = std::min(nb, a0 + CH);
       for (int i = a0; i < a1; ++i) {
         RecA r{};
-        r.th = th_slot[i] * RB;
+        r.th = th_slot[i] * S.code_row_bytes;
         r.theta = net.theta[i];
         r.e0 = f1 ? (int)IA1.size() : (int)IA2.size();
         for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
@@ -447,14 +447,16 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
         r.row = br_slot[l] * BR;
         r.wpos = S.pos_br[l];
         r.obr = net.sw.empty() || net.sw[l] ? l : -1;
-        r.ts = th_slot[s] * RB;
-        r.tt = th_slot[t] * RB;
+        r.ts = th_slot[s] * S.code_row_bytes;
+        r.tt = th_slot[t] * S.code_row_bytes;
+        r.ths = net.theta[s];
+        r.tht = net.theta[t];
         r.b = net.b[l];
         r.F = net.F[l];
         if (!f1) {
           r.ls = lam_slot[s] * RB;
           r.lt = lam_slot[t] * RB;
-          r.fs = f_slot[l] * RB;
+          r.fs = f_slot[l] * S.code_row_bytes;
         }
         Bv.push_back(r);
       }
@@ -480,14 +482,16 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
           const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
           if (!f1) {
             RecIC2 x{};
-            x.f = f_slot[l] * RB;
+            x.f = f_slot[l] * S.code_row_bytes;
             x.br = l;
-            x.s = to ? 1.0 : -1.0;  // d/dlambda: +f* at the to bus, -f* at the from bus
+            x.sF = to ? net.F[l] : -net.F[l];  // d/dlambda: +f* at the to bus, -f* at the from bus
             IC2.push_back(x);
           } else {
             RecIC1 x{};
-            x.ts = th_slot[net.bs[l]] * RB;
-            x.tt = th_slot[net.bt[l]] * RB;
+            x.ts = th_slot[net.bs[l]] * S.code_row_bytes;
+            x.tt = th_slot[net.bt[l]] * S.code_row_bytes;
+            x.ths = net.theta[net.bs[l]];
+            x.tht = net.theta[net.bt[l]];
             x.br = net.sw.empty() || net.sw[l] ? l : -1;
             x.sb = to ? net.b[l] : -net.b[l];  // +phi at the to bus, -phi at the from bus
             IC1.push_back(x);
@@ -556,10 +560,10 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   off = al(off + S.n_lam_slots * RB + pad);
   S.off_dp = off;
   off = al(off + S.n_d_slots * RB + pad);
-  S.off_th = off;  // theta*_i rows
-  off = al(off + S.n_th_slots * RB + pad);
-  S.off_fc = off;  // f*_l rows (F2)
-  off = al(off + S.n_f_slots * RB + pad);
+  S.off_th = off;  // theta*_i code rows
+  off = al(off + S.n_th_slots * S.code_row_bytes);
+  S.off_fc = off;  // f*_l code rows (F2)
+  off = al(off + S.n_f_slots * S.code_row_bytes);
   // the per-warp dual-value partials [nw][64] are needed only at the end of a
   // sweep, when every pool is dead: they alias the pools
   S.off_red = S.off_brp;

@@ -35,17 +35,20 @@ enum ProgHeader {
 };
 constexpr int kProgHeaderBytes = 80;
 
-// All row / value fields are byte offsets into their shared-memory pool; the
-// minimiser values theta*_i and f*_l are kept per instance (one W-wide row).
+// All row / value fields are byte offsets into their shared-memory pool.  The
+// minimisers theta*_i and f*_l are kept as one signed byte per instance
+// (+1 / -1 / 0: the upper bound, the lower bound, the tie), a 64-byte "code
+// row" per entity; readers multiply by Theta or F, which reproduces the value
+// exactly (c * x is exact for c in {-1, 0, 1}).
 struct alignas(16) RecA { int e0, e1, th, pad; double theta, pad2; };   // bus of phase A
 struct alignas(16) RecIA2 { int row, br; double sb; };                   // F2: sb = to ? b : -b
 struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };      // F1: sb = to ? -b : b (br -1: never out)
-struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, wpos, obr; double b, F; };  // branch of phase B (wpos: nu' row;
-                                                                                      // obr: id if switchable, else -1)
+struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, wpos, obr; double b, F, ths, tht; };  // branch of phase B
+                          // (wpos: nu' row; obr: id if switchable, else -1; ths / tht: Theta of the endpoints)
 struct alignas(16) RecC { int wpos, ls, ds, g0, g1, e0, e1, pad; };     // bus of phase C (wpos: lambda' row)
 struct alignas(16) RecG { double c, lo, hi, a; };                         // generator
-struct alignas(16) RecIC2 { int f, br; double s; };                      // F2: s = to ? +1 : -1
-struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, pad2; };     // F1: sb = to ? b : -b (br -1: never out)
+struct alignas(16) RecIC2 { int f, br; double sF; };                     // F2: sF = to ? F : -F
+struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, ths, tht, pad2; };  // F1: sb = to ? b : -b (br -1: never out)
 
 // load-list entry kinds (top 2 bits of the packed entity word)
 enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
@@ -73,6 +76,7 @@ struct Schedule {
   // storage order of the state rows in HBM (positions) and its inverse, per kind
   std::vector<int> pos_lam, perm_lam, pos_d, perm_d, pos_br, perm_br;
   int row_bytes = 0;                        // lambda / d / nu row: 8 W
+  int code_row_bytes = 64;                  // theta* / f* code row: one byte per instance
   int n_br_slots = 0, n_lam_slots = 0, n_d_slots = 0, n_th_slots = 0, n_f_slots = 0;
   int br_row_bytes = 0;                     // 8 W (nu) or 16 W (mu+, mu-)
   int max_prog_bytes = 0;

@@ -126,6 +126,17 @@ __device__ __forceinline__ D2 ld2(const uint8_t *base, int off) {
 __device__ __forceinline__ void st2(double *p, double x, double y) {
   *reinterpret_cast<double2 *>(p) = make_double2(x, y);
 }
+// minimiser codes: one signed byte per instance (+1 / -1 / 0), a lane's two
+// instances in one 16-bit word; value = code * bound, exact for codes in {-1, 0, 1}
+__device__ __forceinline__ int code_of(bool up, bool down) { return up ? 1 : (down ? -1 : 0); }
+__device__ __forceinline__ void st_code2(uint8_t *p, int c0, int c1) {
+  *reinterpret_cast<unsigned short *>(p) = (unsigned short)((c0 & 0xff) | ((c1 & 0xff) << 8));
+}
+__device__ __forceinline__ D2 ld_code2(const uint8_t *base, int off, double x) {
+  const unsigned c = *reinterpret_cast<const unsigned short *>(base + off);
+  const int c0 = (int)(signed char)(c & 0xffu), c1 = (int)(signed char)(c >> 8);
+  return D2{(double)c0 * x, (double)c1 * x};
+}
 
 template <int FORM, bool EVAL, int NW, bool SOFT>
 #ifndef DCOPF_SWEEP_MAXREG
@@ -230,8 +241,8 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
   const uint8_t *brp = smem + a.off_brp + lofs;
   const uint8_t *lamp = smem + a.off_lamp + lofs;
   const uint8_t *dp = smem + a.off_dp + lofs;
-  uint8_t *thp = smem + a.off_th + lofs;  // theta*_i rows
-  uint8_t *fcp = smem + a.off_fc + lofs;  // f*_l rows (F2)
+  uint8_t *thp = smem + a.off_th + 2 * lane;  // theta*_i code rows
+  uint8_t *fcp = smem + a.off_fc + 2 * lane;  // f*_l code rows (F2)
   // Consumer warps are not stepped in lock-step: step g waits only for
   //   A-done(g-1): theta* of chunk g-1 (read by B) exists, and every warp has
   //                finished step g-2, so the theta* / f* slots this step
@@ -328,7 +339,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
           const bool nr = (bus != a.ref);
           const double t0 = (nr && w0 < 0.0) ? ra.theta : ((nr && w0 > 0.0) ? -ra.theta : 0.0);
           const double t1 = (nr && w1 < 0.0) ? ra.theta : ((nr && w1 > 0.0) ? -ra.theta : 0.0);
-          if (act) *reinterpret_cast<double2 *>(thp + ra.th) = make_double2(t0, t1);
+          if (act) st_code2(thp + ra.th, code_of(nr && w0 < 0.0, nr && w0 > 0.0), code_of(nr && w1 < 0.0, nr && w1 > 0.0));
           if (nr) {
             v0 += w0 * t0;
             v1 += w1 * t1;
@@ -352,7 +363,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
             if (o0) b0 = F0 = 0.0;
             if (o1) b1 = F1v = 0.0;
           }
-          const D2 ths = ld2(thp, r.ts), tht = ld2(thp, r.tt);
+          const D2 ths = ld_code2(thp, r.ts, r.ths), tht = ld_code2(thp, r.tt, r.tht);
           const double phi0 = b0 * (ths.x - tht.x);
           const double phi1 = b1 * (ths.y - tht.y);
           double* dst = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR);
@@ -362,7 +373,8 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
             // f* = -F if q > 0, +F if q < 0, 0 on a tie (an outaged lane has F = 0)
             const double f0 = (q0 > 0.0) ? -F0 : ((q0 < 0.0) ? F0 : 0.0);
             const double f1 = (q1 > 0.0) ? -F1v : ((q1 < 0.0) ? F1v : 0.0);
-            if (act) *reinterpret_cast<double2 *>(fcp + r.fs) = make_double2(f0, f1);
+            // code for C (an outaged lane stores the tie: its f* = +-0)
+            if (act) st_code2(fcp + r.fs, o0 ? 0 : code_of(q0 < 0.0, q0 > 0.0), o1 ? 0 : code_of(q1 < 0.0, q1 > 0.0));
             const double g0 = f0 - phi0, g1 = f1 - phi1;  // Kirchhoff residual
             v0 += q0 * f0;
             v1 += q1 * f1;
@@ -434,9 +446,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
             const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y) + r.e0;
             const int n = r.e1 - r.e0;
             auto acc = [&](const RecIC2 &x) {
-              const D2 f = ld2(fcp, x.f);
-              gl0 = gl0 + x.s * f.x;  // +f* at the to bus, -f* at the from bus ((-1)*f == -f exactly)
-              gl1 = gl1 + x.s * f.y;
+              const D2 f = ld_code2(fcp, x.f, x.sF);  // +-f* (c * (+-F) == +-(c * F) exactly)
+              gl0 = gl0 + f.x;  // +f* at the to bus, -f* at the from bus
+              gl1 = gl1 + f.y;
             };
 #pragma unroll
             for (int e = 0; e < 4; ++e)
@@ -453,7 +465,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
                 if (out_t(my_outs0, x.br)) sb0 = copysign(0.0, sb0);
                 if (out_t(my_outs1, x.br)) sb1 = copysign(0.0, sb1);
               }
-              const D2 ts = ld2(thp, x.ts), tt = ld2(thp, x.tt);
+              const D2 ts = ld_code2(thp, x.ts, x.ths), tt = ld_code2(thp, x.tt, x.tht);
               gl0 = gl0 + sb0 * (ts.x - tt.x);
               gl1 = gl1 + sb1 * (ts.y - tt.y);
             }

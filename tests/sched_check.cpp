@@ -86,8 +86,8 @@ int main(int argc, char **argv) {
     const RecIC2 *IC2 = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
     const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
     // the step's code writes land first (worst case for the concurrent readers)
-    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th / RB] = h[PH_A0] + j;
-    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs / RB] = h[PH_B0] + j;
+    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th / S.code_row_bytes] = h[PH_A0] + j;
+    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs / S.code_row_bytes] = h[PH_B0] + j;
     // A(c)
     for (int j = 0; j < h[PH_NA]; ++j) {
       int bus = h[PH_A0] + j;
@@ -113,8 +113,8 @@ int main(int argc, char **argv) {
       seenB[l]++;
       if (S.perm_br[Bv[j].wpos] != l) { printf("BAD B wpos\n"); ++bad; }
       want(brp, Bv[j].row / BR, l, "B br", c);
-      want(th, Bv[j].ts / RB, n.bs[l], "B th_s", c);
-      want(th, Bv[j].tt / RB, n.bt[l], "B th_t", c);
+      want(th, Bv[j].ts / S.code_row_bytes, n.bs[l], "B th_s", c);
+      want(th, Bv[j].tt / S.code_row_bytes, n.bt[l], "B th_t", c);
       if (!f1) {
         want(lamp, Bv[j].ls / RB, n.bs[l], "B lam_s", c);
         want(lamp, Bv[j].lt / RB, n.bt[l], "B lam_t", c);
@@ -132,11 +132,11 @@ int main(int argc, char **argv) {
         const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
         if ((f1 ? (IC1[e].br < 0 ? l : IC1[e].br) : IC2[e].br) != l) { printf("BAD C order\n"); ++bad; }
         if (!f1) {
-          want(fc, IC2[e].f / RB, l, "C f", c);
-          if (IC2[e].s != (to ? 1.0 : -1.0)) { printf("BAD C sign\n"); ++bad; }
+          want(fc, IC2[e].f / S.code_row_bytes, l, "C f", c);
+          if (IC2[e].sF != (to ? n.F[l] : -n.F[l])) { printf("BAD C sign\n"); ++bad; }
         } else {
-          want(th, IC1[e].ts / RB, n.bs[l], "C th_s", c);
-          want(th, IC1[e].tt / RB, n.bt[l], "C th_t", c);
+          want(th, IC1[e].ts / S.code_row_bytes, n.bs[l], "C th_s", c);
+          want(th, IC1[e].tt / S.code_row_bytes, n.bt[l], "C th_t", c);
           if (IC1[e].sb != (to ? n.b[l] : -n.b[l])) { printf("BAD C sign\n"); ++bad; }
         }
       }

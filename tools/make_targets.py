@@ -38,11 +38,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    ap.add_argument("--opt", default="plain", help="ascent-step variant (bench.py OPTS)")
+    ap.add_argument("--alpha", type=float, default=None)
+    ap.add_argument("--workloads", nargs="*", default=None)
+    ap.add_argument("--forms", nargs="*", default=["F2", "F1"])
     a = ap.parse_args()
     js = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    import bench
+    v, hp, a0 = bench.OPTS[a.opt]
+    alpha = a.alpha if a.alpha is not None else a0
+    opt = dict(variant=v, **hp)
     for wl, (config, quad) in WORKLOADS.items():
+        if a.workloads and wl not in a.workloads:
+            continue
         for form_name, form in (("F2", oracle.FORM_F2), ("F1", oracle.FORM_F1)):
-            key = f"{wl}/{form_name}"
+            if form_name not in a.forms:
+                continue
+            key = f"{wl}/{form_name}" + ("" if a.opt == "plain" else f"/{a.opt}/{alpha:g}")
             if a.only and key not in a.only:
                 continue
             net = inst.make_network(config, quadratic=quad)
@@ -54,9 +66,10 @@ def main():
                 ids = np.zeros(1, dtype=np.int64)
                 batch = inst.single_batch(net)
             t0 = time.time()
-            res = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K),
-                               form=form, threads=a.threads)
-            js[key] = {"K": K, "alpha": inst.ALPHA, "instance_ids": ids.tolist(), "best": res.best.tolist(),
+            res = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K, alpha),
+                               form=form, threads=a.threads, opt=opt)
+            js[key] = {"K": K, "alpha": alpha, "opt": {"name": a.opt, **opt},
+                       "instance_ids": ids.tolist(), "best": res.best.tolist(),
                        "bound": res.bound.tolist(), "status": res.status.tolist(),
                        "source": "oracle/dcopf_oracle.c via tools/make_targets.py"}
             print(key, f"{time.time() - t0:.1f}s", "best[:4] =", res.best[:4], flush=True)
