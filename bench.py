@@ -83,6 +83,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap run (the workload's full K)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank its own configs[4]-sized batch (default); strong: configs[4] split")
     ap.add_argument("--opt", default="plain", choices=sorted(OPTS),
                     help="ascent-step variant (PAPER.md:245); non-plain variants run on the cluster path")
     ap.add_argument("--alpha", type=float, default=None, help="constant step (default: the variant's)")
@@ -150,11 +152,12 @@ def dist_env():
     return rank, world, local
 
 
-def make_inputs(workload, lo, hi):
+def make_inputs(workload, lo, hi, total=inst.CONFIG4_BATCH):
     config, quad, _ = WORKLOADS[workload]
     net = inst.make_network(config, quadratic=quad)
     if config == 4:
-        batch = inst.config4_batch(net, range(lo, hi), variant="4b" if workload == "config4b" else "4")
+        batch = inst.config4_batch(net, range(lo, hi), variant="4b" if workload == "config4b" else "4",
+                                   total=max(total, hi))
     else:
         batch = inst.single_batch(net)
     return net, batch
@@ -283,8 +286,15 @@ def main():
     dev = torch.device("cuda", local)
     form = dual.FORM_F2 if args.form == "F2" else dual.FORM_F1
     config, quad, B_total = WORKLOADS[args.workload]
-    lo, hi = shard(B_total, rank, world) if B_total > 1 else (0, 1)
-    net, batch = make_inputs(args.workload, lo, hi)
+    if B_total > 1 and args.scaling == "weak":
+        # weak scaling (independent instances, no data-path collective): every
+        # rank iterates its own configs[4]-sized batch; rank r takes instances
+        # [r B, (r+1) B) of the seeded sweep (instance j's data depend only on j)
+        lo, hi = rank * B_total, (rank + 1) * B_total
+        B_total = B_total * world
+    else:
+        lo, hi = shard(B_total, rank, world) if B_total > 1 else (0, 1)
+    net, batch = make_inputs(args.workload, lo, hi, total=B_total)
     B = batch.B
     path = dual.PATH_BATCHED if B_total > 1 else dual.PATH_CLUSTER
     path = {"auto": path, "batched": dual.PATH_BATCHED, "single": dual.PATH_SINGLE,
@@ -348,7 +358,8 @@ def main():
     if world > 1 and B_total > 1:
         torch.cuda.synchronize()
         g0 = time.perf_counter()
-        gathered = gather_instance_results([bound, best, status], B_total)  # NCCL, once, off the hot loop
+        gathered = gather_instance_results([bound, best, status], B_total,  # NCCL, once, off the hot loop
+                                           sizes=[hi - lo] * world if args.scaling == "weak" else None)
         torch.cuda.synchronize()
         gather_ms = 1e3 * (time.perf_counter() - g0)
         assert gathered.shape == (3, B_total)
@@ -411,7 +422,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms_max / K, "higher_is_better": True,
-            "scaling": "strong" if B_total > 1 else "replicas",
+            "scaling": (args.scaling if B_total > 1 else "replicas"),
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE.json recipe)",
             "config": {"workload": args.workload, "form": args.form, "cost": "QP" if quad else "LP",
                        "step": {"variant": args.opt, "alpha": alpha0, **OPTS[args.opt][1]},

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <queue>
 #include <set>
+#include <type_traits>
 #include <string>
 
 namespace dcopf {
@@ -413,6 +414,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
       for (int i = a0; i < a1; ++i) {
         RecA r{};
         r.th = th_slot[i] * S.code_row_bytes;
+        r.bus = i;
         r.theta = net.theta[i];
         r.e0 = f1 ? (int)IA1.size() : (int)IA2.size();
         for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
@@ -501,6 +503,42 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
         Cv.push_back(r);
       }
     }
+    // ---- balance the step over the nw consumer warps: per phase, items in
+    // decreasing estimated cost go to the least-loaded warp (loads accumulate
+    // over A, B, C); each warp's items are then contiguous, and a table of
+    // [3][nw+1] offsets tells warp w its range.  A warp waits for every warp's
+    // A of the previous step, so the per-step maximum is what counts.
+    std::vector<long> load(nw, 0);
+    std::vector<uint16_t> wtab(3 * (nw + 1), 0);
+    auto balance = [&](auto &items, auto cost, int phase) {
+      const int n = (int)items.size();
+      std::vector<int> idx(n), own(n);
+      for (int x = 0; x < n; ++x) idx[x] = x;
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost(items[a]) > cost(items[b]); });
+      for (int x : idx) {
+        int w = 0;
+        for (int v = 1; v < nw; ++v)
+          if (load[v] < load[w]) w = v;
+        own[x] = w;
+        load[w] += cost(items[x]);
+      }
+      std::vector<int> ord(n);
+      for (int x = 0; x < n; ++x) ord[x] = x;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return own[a] < own[b]; });
+      typename std::remove_reference<decltype(items)>::type re(n);
+      for (int x = 0; x < n; ++x) re[x] = items[ord[x]];
+      items.swap(re);
+      uint16_t *t = wtab.data() + phase * (nw + 1);
+      for (int x = 0, w = 0; w <= nw; ++w) {
+        while (x < n && own[ord[x]] < w) ++x;
+        t[w] = (uint16_t)x;
+      }
+    };
+    const long kDeg = f1 ? 20 : 12;
+    balance(A, [&](const RecA &r) { return 30 + kDeg * (r.e1 - r.e0); }, 0);
+    balance(Bv, [&](const RecB &) { return 70L; }, 1);
+    balance(Cv, [&](const RecC &r) { return 35 + kDeg * (r.e1 - r.e0) + 25L * (r.g1 - r.g0); }, 2);
+
     std::vector<uint8_t> blk(kProgHeaderBytes, 0);
     int32_t hd[PH_COUNT] = {0};
     auto app = [&](const void *p, size_t n) {
@@ -519,8 +557,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     hd[PH_B0] = b0;
     // items are dealt round-robin to the nw consumer warps in the order A, B, C:
     // warp w starts B at (w - nA) mod nw and C at (w - nA - nB) mod nw
-    hd[PH_ROT_B] = (nw - (int)A.size() % nw) % nw;
-    hd[PH_ROT_C] = (nw - ((int)A.size() + (int)Bv.size()) % nw) % nw;
+    hd[PH_OFF_W] = app(wtab.data(), wtab.size() * sizeof(uint16_t));
     hd[PH_OFF_A] = app(A.data(), A.size() * sizeof(RecA));
     hd[PH_OFF_IA] = f1 ? app(IA1.data(), IA1.size() * sizeof(RecIA1)) : app(IA2.data(), IA2.size() * sizeof(RecIA2));
     hd[PH_OFF_B] = app(Bv.data(), Bv.size() * sizeof(RecB));

@@ -30,7 +30,7 @@ namespace dcopf {
 enum ProgHeader {
   PH_NA = 0, PH_NIA, PH_NB, PH_NC, PH_NIC, PH_NG, PH_A0, PH_B0,
   PH_OFF_A, PH_OFF_IA, PH_OFF_B, PH_OFF_C, PH_OFF_G, PH_OFF_IC, PH_BYTES, PH_PAD,
-  PH_ROT_B, PH_ROT_C, PH_PAD2, PH_PAD3,  // first B / C item index of warp 0 (round-robin over all items)
+  PH_ROT_B, PH_ROT_C, PH_OFF_W, PH_PAD3,  // (unused) ; byte offset of the per-warp item table
   PH_COUNT
 };
 constexpr int kProgHeaderBytes = 80;
@@ -40,7 +40,7 @@ constexpr int kProgHeaderBytes = 80;
 // (+1 / -1 / 0: the upper bound, the lower bound, the tie), a 64-byte "code
 // row" per entity; readers multiply by Theta or F, which reproduces the value
 // exactly (c * x is exact for c in {-1, 0, 1}).
-struct alignas(16) RecA { int e0, e1, th, pad; double theta, pad2; };   // bus of phase A
+struct alignas(16) RecA { int e0, e1, th, bus; double theta, pad2; };   // bus of phase A
 struct alignas(16) RecIA2 { int row, br; double sb; };                   // F2: sb = to ? b : -b
 struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };      // F1: sb = to ? -b : b (br -1: never out)
 struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, wpos, obr; double b, F, ths, tht; };  // branch of phase B

@@ -92,15 +92,19 @@ __device__ __forceinline__ void warp_arrive(uint64_t *bar, int lane) {
   __syncwarp();
   if (lane == 0) mbar_arrive(bar);
 }
+// try_wait suspend-time hint: a waiting warp sleeps in hardware until the phase
+// completes (or this many ns pass) instead of re-polling, so waiting warps do
+// not take issue slots from the working ones
+constexpr unsigned kSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   unsigned done = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs)
         : "memory");
   } while (!done);
 }
@@ -291,7 +295,8 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       const int4 h1 = *reinterpret_cast<const int4 *>(prog + 16);  // nIC nG a0 b0
       const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);  // offA offIA offB offC
       const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC bytes -
-      const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // rotB rotC
+      const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // - - offW -
+      const unsigned short *wt = reinterpret_cast<const unsigned short *>(prog + h4.z);  // [3][NW+1] item ranges
       const int nA = h0.x, nB = h0.z, nC = h0.w;
 
       if (a.debug_mode != 1) {  // (1: data movement only -- measurement)
@@ -299,9 +304,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       // ---------------- A(s): w_i, theta* codes ----------------
       {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
-        for (int j = warp; j < nA; j += NW) {
+        for (int j = wt[warp], je = wt[warp + 1]; j < je; ++j) {
           const RecA ra = A[j];
-          const int bus = h1.z + j;
+          const int bus = ra.bus;
           double w0 = 0.0, w1 = 0.0;
           if (FORM == kFormF2) {
             // incidence entries in ascending original branch id (the oracle's
@@ -350,11 +355,8 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       // ---------------- B(s-1): branches ----------------
       {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
-        int jb = warp + h4.x;
-        if (jb >= NW) jb -= NW;
-        for (int j = jb; j < nB; j += NW) {
+        for (int j = wt[NW + 1 + warp], je = wt[NW + 2 + warp]; j < je; ++j) {
           const RecB r = Bv[j];
-          const int l = h1.w + j;  // internal branch id (outage lists)
           double b0 = r.b, b1 = r.b, F0 = r.F, F1v = r.F;
           bool o0 = false, o1 = false;
           if (r.obr >= 0 && flagged(r.obr)) {  // obr < 0: branch never taken out
@@ -421,9 +423,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       {
         const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
         const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
-        int jc = warp + h4.y;
-        if (jc >= NW) jc -= NW;
-        for (int j = jc; j < nC; j += NW) {
+        for (int j = wt[2 * (NW + 1) + warp], je = wt[2 * (NW + 1) + warp + 1]; j < je; ++j) {
           const RecC r = Cv[j];
           const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
           double gl0 = -di.x, gl1 = -di.y;

@@ -25,7 +25,7 @@ def shard_sizes(B: int, world: int) -> List[int]:
     return [hi - lo for lo, hi in (shard(B, r, world) for r in range(world))]
 
 
-def gather_instance_results(rows: Sequence, B_total: int, group=None):
+def gather_instance_results(rows: Sequence, B_total: int, group=None, sizes=None):
     """All-gather per-instance result vectors.
 
     rows: list of equally-long 1-D tensors (this rank's shard, any dtype
@@ -37,7 +37,8 @@ def gather_instance_results(rows: Sequence, B_total: int, group=None):
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    sizes = shard_sizes(B_total, world)
+    sizes = list(sizes) if sizes is not None else shard_sizes(B_total, world)
+    assert sum(sizes) == B_total and len(sizes) == world
     n_local = sizes[rank]
     stacked = torch.stack([r.to(torch.float64) for r in rows])
     assert stacked.shape[1] == n_local, (stacked.shape, n_local)

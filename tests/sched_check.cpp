@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -86,11 +87,11 @@ int main(int argc, char **argv) {
     const RecIC2 *IC2 = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
     const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
     // the step's code writes land first (worst case for the concurrent readers)
-    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th / S.code_row_bytes] = h[PH_A0] + j;
-    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs / S.code_row_bytes] = h[PH_B0] + j;
+    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th / S.code_row_bytes] = A[j].bus;
+    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs / S.code_row_bytes] = S.perm_br[Bv[j].wpos];
     // A(c)
     for (int j = 0; j < h[PH_NA]; ++j) {
-      int bus = h[PH_A0] + j;
+      int bus = A[j].bus;
       seenA[bus]++;
       if (bus / S.CH != c) { printf("BAD A step\n"); ++bad; }
       if (A[j].e1 - A[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD A degree\n"); ++bad; }
@@ -109,9 +110,9 @@ int main(int argc, char **argv) {
     }
     // B(c-1)
     for (int j = 0; j < h[PH_NB]; ++j) {
-      int l = h[PH_B0] + j;
+      int l = S.perm_br[Bv[j].wpos];  // items are reordered for warp balance
       seenB[l]++;
-      if (S.perm_br[Bv[j].wpos] != l) { printf("BAD B wpos\n"); ++bad; }
+      if (std::max(n.bs[l], n.bt[l]) / S.CH != c - 1) { printf("BAD B step\n"); ++bad; }
       want(brp, Bv[j].row / BR, l, "B br", c);
       want(th, Bv[j].ts / S.code_row_bytes, n.bs[l], "B th_s", c);
       want(th, Bv[j].tt / S.code_row_bytes, n.bt[l], "B th_t", c);

@@ -71,3 +71,45 @@ def test_two_rank_gloo_gather_equals_unsharded(tmp_path):
     np.testing.assert_array_equal(g[0], ref.bound)
     np.testing.assert_array_equal(g[1], ref.best)
     np.testing.assert_array_equal(g[2], ref.status)
+
+
+def _worker_weak(rank, world, port, B, K, out_path):
+    """weak scaling: every rank its own B-instance batch = instances
+    [rank B, (rank+1) B) of the seeded config-4 sweep (bench.py --scaling weak)"""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2406_13191_b200 import instances as inst
+    from paper_2406_13191_b200.distributed import gather_instance_results
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    net = inst.tiny_network(40, 60, 8, seed=1)
+    lo, hi = rank * B, (rank + 1) * B
+    batch = inst.config4_batch(net, range(lo, hi), total=world * B)
+    r = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K, 3e-3))
+    g = gather_instance_results([torch.from_numpy(r.bound), torch.from_numpy(r.best)], world * B,
+                                sizes=[B] * world)
+    if rank == 0:
+        np.save(out_path, g.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_weak_scaling_gather(tmp_path):
+    """Each rank draws only its own instances; the gathered results equal one
+    process solving all 2B instances (instance data depend only on the id)."""
+    import oracle
+    from paper_2406_13191_b200 import instances as inst
+
+    B, K = 5, 150
+    out = str(tmp_path / "w.npy")
+    mp.spawn(_worker_weak, args=(2, _free_port(), B, K, out), nprocs=2, join=True)
+    g = np.load(out)
+    net = inst.tiny_network(40, 60, 8, seed=1)
+    batch = inst.config4_batch(net, range(2 * B))
+    ref = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K, 3e-3))
+    np.testing.assert_array_equal(g[0], ref.bound)
+    np.testing.assert_array_equal(g[1], ref.best)
