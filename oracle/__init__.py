@@ -26,6 +26,7 @@ OPT_PLAIN, OPT_GDM, OPT_GDM_CLASSIC, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2, 3, 4
 
 FORM_F2 = 0  # flow box (lambda, nu)
 FORM_F1 = 1  # limit rows (lambda, mu+, mu-)
+FORM_KVL = 2  # cycle basis (lambda, kappa), no angles
 DIVERGED = 1
 
 
@@ -55,7 +56,11 @@ def _load():
         lib.oracle_solve.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I]
         lib.oracle_solve.restype = I
         D = ctypes.c_double
-        lib.oracle_solve_opt.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I, I, D, D, D, D]
+        lib.oracle_solve_opt.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I, I, D, D, D, D, P]
+        lib.oracle_evaluate_kvl.argtypes = net + [P, L, P, P, I, P, P, P, P, P, P, P]
+        lib.oracle_evaluate_kvl.restype = I
+        lib.oracle_cycles.argtypes = net + [P, P, P, P, P, P, L]
+        lib.oracle_cycles.restype = I
         lib.oracle_solve_opt.restype = I
         lib.oracle_evaluate.argtypes = net + [I, L, P, P, I, P, P, P, P, P]
         lib.oracle_evaluate.restype = I
@@ -81,7 +86,13 @@ def _net_args(net, keep):
 
 
 def n_branch_mult(net, form):
+    if form == FORM_KVL:
+        return net.n_branch - net.n_bus + 1
     return net.n_branch * (2 if form == FORM_F1 else 1)
+
+
+def _sw(switchable):
+    return None if switchable is None else np.ascontiguousarray(switchable, dtype=np.uint8)
 
 
 @dataclass
@@ -95,7 +106,7 @@ class OracleResult:
 
 
 def solve(net, load, outages=None, K=0, alpha=None, form=FORM_F2, lam0=None, br0=None,
-          history=False, threads=1, opt=None) -> OracleResult:
+          history=False, threads=1, opt=None, switchable=None) -> OracleResult:
     """K projected ascent steps from y_0 = 0 (or the given warm start).
     opt: None (plain step) or dict(variant=OPT_*, rho=, beta1=, beta2=, eps=)."""
     lib = _load()
@@ -122,7 +133,7 @@ def solve(net, load, outages=None, K=0, alpha=None, form=FORM_F2, lam0=None, br0
     rc = lib.oracle_solve_opt(*_net_args(net, keep), form, B, _p(load), _p(outs), max_out, K, _p(alpha),
                               _p(lam), _p(br), _p(bound), _p(best), _p(status), _p(hist), int(warm),
                               int(threads), int(o["variant"]), float(o["rho"]), float(o["beta1"]),
-                              float(o["beta2"]), float(o["eps"]))
+                              float(o["beta2"]), float(o["eps"]), _p(_sw(switchable)))
     if rc != 0:
         raise ValueError("oracle_solve rejected its arguments")
     return OracleResult(lam, br, bound, best, status, hist)
@@ -174,3 +185,42 @@ def minimiser(net, load, lam, br, outages=None, form=FORM_F2):
     if rc != 0:
         raise ValueError("oracle_minimiser rejected its arguments")
     return p, fl, th
+
+
+def evaluate_kvl(net, load, lam, kap, outages=None, switchable=None):
+    """KVL form at given multipliers: (value[B], grad_lam[B][n_bus], grad_kap[B][nc], p[B][n_gen], f[B][n_l])."""
+    lib = _load()
+    load = np.ascontiguousarray(np.atleast_2d(load), dtype=np.float64)
+    B = load.shape[0]
+    nc = n_branch_mult(net, FORM_KVL)
+    lam = np.ascontiguousarray(np.atleast_2d(lam), dtype=np.float64)
+    kap = np.ascontiguousarray(np.atleast_2d(kap), dtype=np.float64).reshape(B, nc)
+    outs, max_out = None, 0
+    if outages is not None:
+        outs = np.ascontiguousarray(np.atleast_2d(outages), dtype=np.int32)
+        max_out = outs.shape[1]
+    val, gl, gk = np.zeros(B), np.zeros((B, net.n_bus)), np.zeros((B, nc))
+    p, f = np.zeros((B, net.n_gen)), np.zeros((B, net.n_branch))
+    keep = []
+    rc = lib.oracle_evaluate_kvl(*_net_args(net, keep), _p(_sw(switchable)), B, _p(load), _p(outs), max_out,
+                                 _p(lam), _p(kap), _p(val), _p(gl), _p(gk), _p(p), _p(f))
+    if rc != 0:
+        raise ValueError("oracle_evaluate_kvl rejected its arguments")
+    return val, gl, gk, p, f
+
+
+def cycles(net, switchable=None):
+    """The fundamental cycle basis (reading A-28): (def[nc], list of (branch ids, signs) per cycle)."""
+    lib = _load()
+    keep = []
+    nc = ctypes.c_int(0)
+    sw = _sw(switchable)
+    tot = lib.oracle_cycles(*_net_args(net, keep), _p(sw), ctypes.byref(nc), None, None, None, None, 0)
+    if tot < 0:
+        raise ValueError("network disconnected over never-switched branches")
+    d = np.zeros(nc.value, np.int32)
+    cp = np.zeros(nc.value + 1, np.int32)
+    cb = np.zeros(max(tot, 1), np.int32)
+    cs = np.zeros(max(tot, 1), np.int32)
+    lib.oracle_cycles(*_net_args(net, keep), _p(sw), ctypes.byref(nc), _p(d), _p(cp), _p(cb), _p(cs), tot)
+    return d, [(cb[cp[k]:cp[k + 1]], cs[cp[k]:cp[k + 1]]) for k in range(nc.value)]

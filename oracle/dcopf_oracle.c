@@ -64,6 +64,7 @@
 
 #define ORC_FORM_FLOW_BOX 0   /* F2: boxes p, f, theta; multipliers lambda, nu      */
 #define ORC_FORM_LIMIT_ROWS 1 /* F1: boxes p, theta; multipliers lambda, mu+, mu-   */
+#define ORC_FORM_CYCLE 2      /* KVL: boxes p, f; multipliers lambda (KCL), kappa (cycle KVL) */
 #define ORC_DIVERGED 1
 
 typedef struct {
@@ -251,11 +252,199 @@ static double opt_step(const orc_opt *o, double y, double g, double a, double *s
   }
 }
 
+/* ============================================================================
+ * Form KVL (reading A-28): the angle-free
+ * cycle-basis twin of the paper's PTDF constraint (Eq. 1:
+ * f = H(p - d)).  For a connected network, f is the PTDF flow of the
+ * injections iff KCL (G p - A^T f = d) holds and Kirchhoff's voltage law
+ * holds on every fundamental cycle k of a spanning tree:
+ *     sum_l C_kl x_l f_l = 0,   x_l = 1 / b_l,   C_kl in {0, +1, -1}.
+ * Dualising KCL (lambda) and KVL (kappa, free) leaves the boxes p, |f| <= F:
+ *     q_l    = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t)
+ *     f*_l   = -F if q > 0, +F if q < 0, 0 on a tie
+ *     g      = [sum_g a p*^2 + r p*] + [sum_l q_l f*_l] - [sum_i lambda_i d_i]
+ *     dg/dlambda = KCL residual (as F2),  dg/dkappa_k = sum_l C_kl (f*_l x_l).
+ * Spanning tree (reading A-28): breadth-first from the reference bus, buses
+ * in FIFO order, each bus's incident branches in ascending id, over branches
+ * with b > 0 that are never switched.  Cycle k belongs to the k-th non-tree
+ * branch l (ascending id): l traversed from s_l to t_l (+1), then the tree
+ * path from t_l back to s_l (+1 where a branch is traversed from its from bus
+ * to its to bus, -1 otherwise); entries kept in ascending branch id.  A
+ * branch with b = 0 (base or outaged) carries no flow (F_eff = 0, x = 0) and
+ * the cycle it defines is inactive (kappa_k not used, gradient 0).
+ * ========================================================================== */
+typedef struct {
+  int nc;
+  int *is_tree, *def;          /* [nl], [nc] */
+  int *cp, *cb, *cs;           /* cycle k: branches cb[cp[k]..cp[k+1]) ascending, signs cs */
+  int *bp, *bk, *bs;           /* branch l: cycles bk[bp[l]..bp[l+1]) ascending, signs bs */
+} orc_cyc;
+
+static void cyc_free(orc_cyc *Y) {
+  free(Y->is_tree); free(Y->def); free(Y->cp); free(Y->cb); free(Y->cs);
+  free(Y->bp); free(Y->bk); free(Y->bs);
+}
+
+/* returns 0, or -1 if the never-switched branches with b > 0 do not connect the buses */
+static int build_cycles(const orc_net *N, const unsigned char *sw, orc_cyc *Y) {
+  const int nb = N->n_bus, nl = N->n_branch;
+  int *deg = calloc((size_t)nb + 1, sizeof(int)), *ap = calloc((size_t)nb + 1, sizeof(int));
+  int *adj = malloc(sizeof(int) * (2 * (size_t)nl + 1));
+  int *parent = malloc(sizeof(int) * (nb + 1)), *pbr = malloc(sizeof(int) * (nb + 1));
+  int *depth = malloc(sizeof(int) * (nb + 1)), *queue = malloc(sizeof(int) * (nb + 1));
+  int *tmpb = malloc(sizeof(int) * (nb + 2)), *tmps = malloc(sizeof(int) * (nb + 2));
+  int i, l, k, head = 0, tail = 0, seen = 0, cap, tot = 0;
+  for (l = 0; l < nl; l++) { deg[N->br_from[l]]++; deg[N->br_to[l]]++; }
+  for (i = 0; i < nb; i++) ap[i + 1] = ap[i] + deg[i];
+  for (i = 0; i < nb; i++) deg[i] = 0;
+  for (l = 0; l < nl; l++) {                 /* ascending branch id per bus */
+    adj[ap[N->br_from[l]] + deg[N->br_from[l]]++] = l;
+    adj[ap[N->br_to[l]] + deg[N->br_to[l]]++] = l;
+  }
+  Y->is_tree = calloc((size_t)nl + 1, sizeof(int));
+  for (i = 0; i < nb; i++) parent[i] = -2;
+  parent[N->ref_bus] = -1; pbr[N->ref_bus] = -1; depth[N->ref_bus] = 0;
+  queue[tail++] = N->ref_bus; seen = 1;
+  while (head < tail) {
+    int u = queue[head++], e;
+    for (e = ap[u]; e < ap[u + 1]; e++) {
+      int m = adj[e], v = (N->br_from[m] == u) ? N->br_to[m] : N->br_from[m];
+      if (!(N->br_b[m] > 0.0) || (sw && sw[m]) || parent[v] != -2) continue;
+      parent[v] = u; pbr[v] = m; depth[v] = depth[u] + 1; Y->is_tree[m] = 1;
+      queue[tail++] = v; seen++;
+    }
+  }
+  Y->nc = nl - (nb - 1);
+  if (seen != nb || Y->nc < 0) {
+    free(deg); free(ap); free(adj); free(parent); free(pbr); free(depth); free(queue); free(tmpb); free(tmps);
+    free(Y->is_tree); Y->is_tree = NULL;
+    return -1;
+  }
+  cap = Y->nc * (nb + 1) + 1;
+  if (cap > 64 * nl + 1024) cap = 64 * nl + 1024;  /* grown below if needed */
+  Y->def = malloc(sizeof(int) * (Y->nc + 1));
+  Y->cp = malloc(sizeof(int) * (Y->nc + 2));
+  Y->cb = malloc(sizeof(int) * cap);
+  Y->cs = malloc(sizeof(int) * cap);
+  Y->cp[0] = 0;
+  for (k = 0, l = 0; l < nl; l++) {
+    int a, b, n = 0, x, y;
+    if (Y->is_tree[l]) continue;
+    Y->def[k] = l;
+    tmpb[n] = l; tmps[n] = 1; n++;            /* l from s to t */
+    a = N->br_to[l]; b = N->br_from[l];       /* tree path from t (a) back to s (b) */
+    while (a != b) {
+      if (depth[a] >= depth[b]) {               /* a climbs: traversed a -> parent(a) */
+        int m = pbr[a];
+        tmpb[n] = m; tmps[n] = (N->br_from[m] == a) ? 1 : -1; n++;
+        a = parent[a];
+      } else {                                  /* b climbs: traversed parent(b) -> b */
+        int m = pbr[b];
+        tmpb[n] = m; tmps[n] = (N->br_to[m] == b) ? 1 : -1; n++;
+        b = parent[b];
+      }
+    }
+    for (x = 1; x < n; x++)                     /* ascending branch id (insertion sort) */
+      for (y = x; y > 0 && tmpb[y - 1] > tmpb[y]; y--) {
+        int tb = tmpb[y], ts = tmps[y];
+        tmpb[y] = tmpb[y - 1]; tmps[y] = tmps[y - 1]; tmpb[y - 1] = tb; tmps[y - 1] = ts;
+      }
+    if (tot + n > cap) {
+      cap = 2 * (tot + n);
+      Y->cb = realloc(Y->cb, sizeof(int) * cap);
+      Y->cs = realloc(Y->cs, sizeof(int) * cap);
+    }
+    for (x = 0; x < n; x++) { Y->cb[tot + x] = tmpb[x]; Y->cs[tot + x] = tmps[x]; }
+    tot += n;
+    Y->cp[++k] = tot;
+  }
+  /* per-branch lists, ascending cycle index */
+  Y->bp = calloc((size_t)nl + 2, sizeof(int));
+  Y->bk = malloc(sizeof(int) * (tot + 1));
+  Y->bs = malloc(sizeof(int) * (tot + 1));
+  for (i = 0; i < tot; i++) Y->bp[Y->cb[i] + 1]++;
+  for (l = 0; l < nl; l++) Y->bp[l + 1] += Y->bp[l];
+  {
+    int *fill = calloc((size_t)nl + 1, sizeof(int));
+    for (k = 0; k < Y->nc; k++)
+      for (i = Y->cp[k]; i < Y->cp[k + 1]; i++) {
+        int m = Y->cb[i];
+        Y->bk[Y->bp[m] + fill[m]] = k;
+        Y->bs[Y->bp[m] + fill[m]] = Y->cs[i];
+        fill[m]++;
+      }
+    free(fill);
+  }
+  free(deg); free(ap); free(adj); free(parent); free(pbr); free(depth); free(queue); free(tmpb); free(tmps);
+  return 0;
+}
+
+/* value and gradient of the KVL form; kap[nc]; gradient in W->glam, W->gbr[nc] */
+static double evaluate_kvl(const orc_net *N, orc_work *W, const orc_cyc *Y, const double *d,
+                           const double *lam, const double *kap) {
+  const int nb = N->n_bus, nl = N->n_branch, ng = N->n_gen;
+  int i, g, l, k, e;
+  double s_gen = 0.0, s_br = 0.0, s_ld = 0.0;
+  /* (a) r_g */
+  for (g = 0; g < ng; g++) W->r[g] = N->gen_c[g] + lam[N->gen_bus[g]];
+  /* (b) q_l = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t); active cycles only */
+  for (l = 0; l < nl; l++) {
+    double x = (W->b[l] > 0.0) ? 1.0 / W->b[l] : 0.0, sum = 0.0;
+    for (e = Y->bp[l]; e < Y->bp[l + 1]; e++) {
+      k = Y->bk[e];
+      if (!(W->b[Y->def[k]] > 0.0)) continue;
+      sum = (Y->bs[e] > 0) ? sum + kap[k] : sum - kap[k];
+    }
+    W->q[l] = x * sum - (lam[N->br_from[l]] - lam[N->br_to[l]]);
+  }
+  /* (d) minimisers */
+  for (g = 0; g < ng; g++) {
+    double lo = N->gen_pmin[g], hi = N->gen_pmax[g], r = W->r[g];
+    if (N->gen_a && N->gen_a[g] > 0.0) {
+      double x = -r / (2.0 * N->gen_a[g]);
+      W->p[g] = (x < lo) ? lo : ((x > hi) ? hi : x);
+    } else if (r > 0.0) W->p[g] = lo;
+    else if (r < 0.0) W->p[g] = hi;
+    else W->p[g] = 0.5 * (lo + hi);
+  }
+  for (l = 0; l < nl; l++) {
+    double F = (W->b[l] > 0.0) ? W->F[l] : 0.0, q = W->q[l];
+    W->f[l] = (q > 0.0) ? -F : ((q < 0.0) ? F : 0.0);
+  }
+  /* (e) value */
+  for (g = 0; g < ng; g++) {
+    double t = W->r[g] * W->p[g];
+    if (N->gen_a && N->gen_a[g] > 0.0) t = N->gen_a[g] * W->p[g] * W->p[g] + t;
+    s_gen += t;
+  }
+  for (l = 0; l < nl; l++) s_br += W->q[l] * W->f[l];
+  for (i = 0; i < nb; i++) s_ld += lam[i] * d[i];
+  /* (g) gradient */
+  for (i = 0; i < nb; i++) W->glam[i] = -d[i];
+  for (g = 0; g < ng; g++) W->glam[N->gen_bus[g]] += W->p[g];
+  for (l = 0; l < nl; l++) {
+    W->glam[N->br_from[l]] -= W->f[l];
+    W->glam[N->br_to[l]] += W->f[l];
+  }
+  for (k = 0; k < Y->nc; k++) {
+    double acc = 0.0;
+    if (W->b[Y->def[k]] > 0.0)
+      for (e = Y->cp[k]; e < Y->cp[k + 1]; e++) {
+        int m = Y->cb[e];
+        double x = (W->b[m] > 0.0) ? 1.0 / W->b[m] : 0.0, t = W->f[m] * x;
+        acc = (Y->cs[e] > 0) ? acc + t : acc - t;
+      }
+    W->gbr[k] = acc;
+  }
+  return (s_gen + s_br) - s_ld;
+}
+
 static void run_instance(const orc_net *N, int form, const double *d, const int *out, int max_out,
                          long K, const double *alpha, double *lam, double *br, double *bound,
-                         double *best, int *status, double *hist, int warm, const orc_opt *opt) {
+                         double *best, int *status, double *hist, int warm, const orc_opt *opt,
+                         const orc_cyc *Y) {
   const int nb = N->n_bus, nl = N->n_branch;
-  const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * nl : nl;
+  const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * nl : ((form == ORC_FORM_CYCLE) ? Y->nc : nl);
   orc_work W;
   long k;
   int i, j, frozen = 0;
@@ -271,7 +460,7 @@ static void run_instance(const orc_net *N, int form, const double *d, const int 
   *best = -INFINITY;
   *status = 0;
   for (k = 0;; k++) {                            /* step 4: k = 0..K inclusive */
-    double g = evaluate(N, &W, form, d, lam, br);
+    double g = (form == ORC_FORM_CYCLE) ? evaluate_kvl(N, &W, Y, d, lam, br) : evaluate(N, &W, form, d, lam, br);
     int was_frozen = frozen;
     if (hist) hist[k] = g;
     if (!was_frozen) {                           /* (f) best = max(best, g) */
@@ -284,8 +473,8 @@ static void run_instance(const orc_net *N, int form, const double *d, const int 
       double a = alpha[k];
       if (opt->variant == ORC_OPT_ADAM) { b1t = b1t * opt->beta1; b2t = b2t * opt->beta2; }
       for (i = 0; i < nb; i++) lam[i] = opt_step(opt, lam[i], W.glam[i], a, &s1[i], &s2[i], b1t, b2t);
-      if (form == ORC_FORM_FLOW_BOX) {
-        for (j = 0; j < nl; j++) br[j] = opt_step(opt, br[j], W.gbr[j], a, &s1[nb + j], &s2[nb + j], b1t, b2t);
+      if (form == ORC_FORM_FLOW_BOX || form == ORC_FORM_CYCLE) {   /* nu / kappa: free */
+        for (j = 0; j < nbr; j++) br[j] = opt_step(opt, br[j], W.gbr[j], a, &s1[nb + j], &s2[nb + j], b1t, b2t);
       } else {
         for (j = 0; j < 2 * nl; j++) {
           double v = opt_step(opt, br[j], W.gbr[j], a, &s1[nb + j], &s2[nb + j], b1t, b2t);
@@ -324,23 +513,73 @@ static void run_instance(const orc_net *N, int form, const double *d, const int 
 int oracle_solve_opt(NET_ARGS, int form, long B, const double *load, const int *outages, int max_out,
                      long K, const double *alpha, double *lam, double *br, double *bound,
                      double *best, int *status, double *hist, int warm, int n_threads,
-                     int variant, double rho, double beta1, double beta2, double eps) {
+                     int variant, double rho, double beta1, double beta2, double eps,
+                     const unsigned char *switchable) {
   NET_INIT
   long j;
   orc_opt opt;
+  orc_cyc Y;
+  int nbr;
   opt.variant = variant; opt.rho = rho; opt.beta1 = beta1; opt.beta2 = beta2; opt.eps = eps;
+  memset(&Y, 0, sizeof Y);
   if (variant < ORC_OPT_PLAIN || variant > ORC_OPT_ADAM) return -1;
-  const int nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * n_branch : n_branch;
   if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0 || K < 0) return -1;
-  if (form != ORC_FORM_FLOW_BOX && form != ORC_FORM_LIMIT_ROWS) return -1;
+  if (form != ORC_FORM_FLOW_BOX && form != ORC_FORM_LIMIT_ROWS && form != ORC_FORM_CYCLE) return -1;
+  if (form == ORC_FORM_CYCLE && build_cycles(&N, switchable, &Y) != 0) return -2;
+  nbr = (form == ORC_FORM_LIMIT_ROWS) ? 2 * n_branch : ((form == ORC_FORM_CYCLE) ? Y.nc : n_branch);
   (void)n_threads;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(n_threads > 0 ? n_threads : 1)
   for (j = 0; j < B; j++) {
     run_instance(&N, form, load + j * (long)n_bus, outages ? outages + j * (long)max_out : NULL,
                  max_out, K, alpha, lam + j * (long)n_bus, br + j * (long)nbr, bound + j,
-                 best + j, status + j, hist ? hist + j * (K + 1) : NULL, warm, &opt);
+                 best + j, status + j, hist ? hist + j * (K + 1) : NULL, warm, &opt, &Y);
   }
+  if (form == ORC_FORM_CYCLE) cyc_free(&Y);
   return 0;
+}
+
+/* KVL form: value and gradient (kap[B][nc], grad_kap[B][nc]); minimiser p, f. */
+int oracle_evaluate_kvl(NET_ARGS, const unsigned char *switchable, long B, const double *load,
+                        const int *outages, int max_out, const double *lam, const double *kap,
+                        double *value, double *grad_lam, double *grad_kap, double *p, double *f) {
+  NET_INIT
+  long j;
+  orc_cyc Y;
+  if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0) return -1;
+  if (build_cycles(&N, switchable, &Y) != 0) return -2;
+  for (j = 0; j < B; j++) {
+    orc_work W;
+    work_alloc(&W, &N, ORC_FORM_FLOW_BOX);
+    apply_outages(&W, &N, outages ? outages + j * (long)max_out : NULL, max_out);
+    value[j] = evaluate_kvl(&N, &W, &Y, load + j * (long)n_bus, lam + j * (long)n_bus, kap + j * (long)Y.nc);
+    if (grad_lam) memcpy(grad_lam + j * (long)n_bus, W.glam, sizeof(double) * n_bus);
+    if (grad_kap) memcpy(grad_kap + j * (long)Y.nc, W.gbr, sizeof(double) * Y.nc);
+    if (p) memcpy(p + j * (long)n_gen, W.p, sizeof(double) * n_gen);
+    if (f) memcpy(f + j * (long)n_branch, W.f, sizeof(double) * n_branch);
+    work_free(&W);
+  }
+  cyc_free(&Y);
+  return 0;
+}
+
+/* The cycle basis (reading A-28): returns the number of entries (or -2 if
+ * disconnected); *nc = cycles; def[nc], cp[nc+1], cb/cs[entries] filled when
+ * cap >= entries. */
+int oracle_cycles(NET_ARGS, const unsigned char *switchable, int *nc, int *def, int *cp, int *cb, int *cs,
+                  long cap) {
+  NET_INIT
+  orc_cyc Y;
+  int k, tot;
+  if (build_cycles(&N, switchable, &Y) != 0) return -2;
+  *nc = Y.nc;
+  tot = Y.cp[Y.nc];
+  if (cap >= tot) {
+    for (k = 0; k < Y.nc; k++) def[k] = Y.def[k];
+    for (k = 0; k <= Y.nc; k++) cp[k] = Y.cp[k];
+    for (k = 0; k < tot; k++) { cb[k] = Y.cb[k]; cs[k] = Y.cs[k]; }
+  }
+  cyc_free(&Y);
+  return tot;
 }
 
 /* the plain projected step (the north_star path) */
@@ -350,7 +589,7 @@ int oracle_solve(NET_ARGS, int form, long B, const double *load, const int *outa
   return oracle_solve_opt(n_bus, n_branch, n_gen, ref_bus, br_from, br_to, br_b, br_fmax, theta_max,
                           gen_bus, gen_pmin, gen_pmax, gen_c, gen_a, form, B, load, outages, max_out, K,
                           alpha, lam, br, bound, best, status, hist, warm, n_threads,
-                          ORC_OPT_PLAIN, 0.0, 0.0, 0.0, 0.0);
+                          ORC_OPT_PLAIN, 0.0, 0.0, 0.0, 0.0, NULL);
 }
 
 /* Value and gradient at given multipliers (no step). */

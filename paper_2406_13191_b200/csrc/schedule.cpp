@@ -2,6 +2,7 @@
 #include "schedule.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <queue>
@@ -534,10 +535,13 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
         t[w] = (uint16_t)x;
       }
     };
-    const long kDeg = f1 ? 20 : 12;
-    balance(A, [&](const RecA &r) { return 30 + kDeg * (r.e1 - r.e0); }, 0);
-    balance(Bv, [&](const RecB &) { return 70L; }, 1);
-    balance(Cv, [&](const RecC &r) { return 35 + kDeg * (r.e1 - r.e0) + 25L * (r.g1 - r.g0); }, 2);
+    // estimated issue cost (instructions per warp) of an item
+    long cw[6] = {30, f1 ? 20 : 12, f1 ? 60 : 70, 35, f1 ? 20 : 12, 25};  // A0 Adeg B C0 Cdeg Cgen
+    if (const char *e = getenv("DCOPF_COST"))  // measurement only
+      sscanf(e, "%ld,%ld,%ld,%ld,%ld,%ld", &cw[0], &cw[1], &cw[2], &cw[3], &cw[4], &cw[5]);
+    balance(A, [&](const RecA &r) { return cw[0] + cw[1] * (r.e1 - r.e0); }, 0);
+    balance(Bv, [&](const RecB &) { return cw[2]; }, 1);
+    balance(Cv, [&](const RecC &r) { return cw[3] + cw[4] * (r.e1 - r.e0) + cw[5] * (r.g1 - r.g0); }, 2);
 
     std::vector<uint8_t> blk(kProgHeaderBytes, 0);
     int32_t hd[PH_COUNT] = {0};

@@ -579,3 +579,136 @@ def test_variants_weak_duality_and_convergence(form, opt, alpha):
     assert r.best[0] >= (0.98 if form == FORM_F2 else 0.95) * opt_val, r.best[0]
     if form == FORM_F1:
         assert np.all(r.br >= 0.0)
+
+
+# ---------------------------------------------------------------------------
+# KVL (cycle-basis) form, reading A-28: the sparse twin of the
+# paper's PTDF constraint (Eq. 1) with no angles
+
+
+def _cycle_matrix(net, switchable=None):
+    d, cyc = oracle.cycles(net, switchable)
+    C = np.zeros((len(d), net.n_branch))
+    for k, (bs, ss) in enumerate(cyc):
+        C[k, bs] = ss
+    return d, C
+
+
+@pytest.mark.parametrize("config", [0, 1])
+def test_kvl_cycle_basis_is_a_basis_of_closed_loops(config):
+    """n_l - n_b + 1 independent cycles; each is a closed walk (C A = 0: the
+    signed incidence around a loop cancels at every bus); its defining
+    non-tree branch appears with +1 and no other non-tree branch appears."""
+    net = inst.make_network(config)
+    d, C = _cycle_matrix(net)
+    A, _ = _incidence(net)
+    assert C.shape[0] == net.n_branch - net.n_bus + 1
+    assert np.all(C @ A == 0)
+    assert np.linalg.matrix_rank(C) == C.shape[0]
+    nontree = np.zeros(net.n_branch, bool)
+    nontree[d] = True
+    for k in range(len(d)):
+        assert C[k, d[k]] == 1
+        assert np.count_nonzero(C[k, nontree]) == 1
+
+
+def test_kvl_annihilates_dc_power_flow():
+    """DC power-flow flows f = diag(b) A theta satisfy sum_l C_kl f_l / b_l = 0
+    on every cycle (Kirchhoff's voltage law), and any vector in the null space
+    of C diag(1/b) with KCL is such a flow (dimension count)."""
+    net = inst.make_network(1)
+    _, C = _cycle_matrix(net)
+    inj = np.zeros(net.n_bus)
+    np.add.at(inj, net.gen_bus, net.gen_pmax * net.base_load.sum() / net.gen_pmax.sum())
+    inj -= net.base_load
+    f = inst.dc_flows(net.n_bus, net.ref_bus, net.br_from, net.br_to, net.br_b, inj)
+    assert np.max(np.abs(C @ (f / net.br_b))) <= 1e-9 * np.max(np.abs(f / net.br_b))
+
+
+def lagrangian_kvl(net, d, lam, kap, P, Fl, C, x):
+    """Eq. 3 for the KVL form: cost + lam^T(Gp - A^T f - d) + kap^T C diag(x) f."""
+    A, G = _incidence(net)
+    cost = P @ net.gen_c
+    if net.gen_a is not None:
+        cost = cost + (P * P) @ net.gen_a
+    kcl = P @ G.T - Fl @ A - d[None, :]
+    kvl = Fl @ (C @ np.diag(x)).T
+    return cost + kcl @ lam + kvl @ kap, kcl, kvl
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_kvl_value_equals_vertex_minimum(seed):
+    """The dual function = min of the Lagrangian over ALL vertices of the
+    p and f boxes (brute force, dense matrices); gradient = residuals there."""
+    net = inst.tiny_network(5, 8, 2, seed=seed)
+    _, C = _cycle_matrix(net)
+    x = 1.0 / net.br_b
+    rng = np.random.default_rng(seed + 10)
+    lam = rng.normal(0, 20, net.n_bus)
+    kap = rng.normal(0, 3, C.shape[0])
+    val, gl, gk, p, f = oracle.evaluate_kvl(net, net.base_load, lam, kap)
+    V = _vertices(np.r_[net.gen_pmin, -net.br_fmax], np.r_[net.gen_pmax, net.br_fmax])
+    L, kcl, kvl = lagrangian_kvl(net, net.base_load, lam, kap, V[:, :net.n_gen], V[:, net.n_gen:], C, x)
+    j = int(np.argmin(L))
+    assert abs(val[0] - L[j]) <= 1e-9 * max(1.0, abs(L[j]))
+    np.testing.assert_allclose(gl[0], kcl[j], atol=1e-9)
+    np.testing.assert_allclose(gk[0], kvl[j], atol=1e-9)
+
+
+def test_kvl_gradient_central_differences():
+    net = inst.make_network(0)
+    _, C = _cycle_matrix(net)
+    rng = np.random.default_rng(3)
+    lam = rng.normal(-30, 10, net.n_bus)
+    kap = rng.normal(0, 50, C.shape[0])
+    _, gl, gk, _, _ = oracle.evaluate_kvl(net, net.base_load, lam, kap)
+    h = 1e-6
+    for i in range(net.n_bus):
+        e = np.zeros(net.n_bus)
+        e[i] = h
+        fd = (oracle.evaluate_kvl(net, net.base_load, lam + e, kap)[0][0] -
+              oracle.evaluate_kvl(net, net.base_load, lam - e, kap)[0][0]) / (2 * h)
+        assert abs(fd - gl[0, i]) <= 1e-6
+    for k in range(C.shape[0]):
+        e = np.zeros(C.shape[0])
+        e[k] = h
+        fd = (oracle.evaluate_kvl(net, net.base_load, lam, kap + e)[0][0] -
+              oracle.evaluate_kvl(net, net.base_load, lam, kap - e)[0][0]) / (2 * h)
+        assert abs(fd - gk[0, k]) <= 1e-6
+
+
+@pytest.mark.parametrize("opt,alpha,tol", [(None, 1e-2, 0.01), (ADAM, 0.1, 0.01), (GDM, 1e-3, 0.01)])
+def test_kvl_weak_and_strong_duality_config0(opt, alpha, tol):
+    """Every iterate <= the LP optimum (no angle box in this form: the primal
+    is the paper's Eq. 1); Adam / GDM get within 1% (survey P-4: KVL is the
+    best-converging form)."""
+    net = inst.make_network(0)
+    _, opt_val = inst.primal_lp(net, net.base_load)
+    K = 20000
+    r = oracle.solve(net, net.base_load, K=K, alpha=inst.alpha_schedule(K, alpha), form=oracle.FORM_KVL,
+                     history=True, opt=opt)
+    assert np.all(r.hist[0] <= opt_val + 1e-9 * abs(opt_val))
+    assert r.best[0] >= (1 - tol) * opt_val, r.best[0]
+
+
+def test_kvl_outage_equals_branch_removed():
+    """An outaged (switchable, hence non-tree) branch drops its own cycle:
+    the run equals the network without that branch, bitwise."""
+    net = inst.make_network(1)
+    sw = np.zeros(net.n_branch, np.uint8)
+    sw[net.n_tree:] = 1
+    l = net.n_tree + 17
+    K = 300
+    a = inst.alpha_schedule(K, 0.05)
+    r = oracle.solve(net, net.base_load, outages=np.array([[l]]), K=K, alpha=a, form=oracle.FORM_KVL,
+                     switchable=sw, opt=ADAM)
+    keep = np.r_[0:l, l + 1:net.n_branch]
+    sub = inst.Network(**{**net.__dict__, "n_branch": net.n_branch - 1, "br_from": net.br_from[keep],
+                          "br_to": net.br_to[keep], "br_b": net.br_b[keep], "br_fmax": net.br_fmax[keep]})
+    r2 = oracle.solve(sub, net.base_load, K=K, alpha=a, form=oracle.FORM_KVL, switchable=sw[keep], opt=ADAM)
+    d, _ = _cycle_matrix(net, sw)
+    k = int(np.nonzero(d == l)[0][0])
+    assert r.br[0, k] == 0.0
+    np.testing.assert_array_equal(r.lam, r2.lam)
+    np.testing.assert_array_equal(np.delete(r.br[0], k), r2.br[0])
+    assert r.best[0] == r2.best[0]
