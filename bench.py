@@ -78,7 +78,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
-    ap.add_argument("--form", default="F2", choices=["F2", "F1"])
+    ap.add_argument("--form", default="F2", choices=["F2", "F1", "KVL"],
+                    help="F2 flow box (default), F1 limit rows, KVL cycle basis (cluster path)")
     ap.add_argument("--path", default="auto", choices=["auto", "batched", "single", "cluster"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -238,7 +239,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    form = 0 if args.form == "F2" else 1
+    form = {"F2": 0, "F1": 1, "KVL": 2}[args.form]
     _, _, B = WORKLOADS[args.workload]
     net, batch = make_inputs(args.workload, 0, B if B == 1 else min(B, 256))
     cores = os.cpu_count() or 1
@@ -284,7 +285,7 @@ def main():
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    form = dual.FORM_F2 if args.form == "F2" else dual.FORM_F1
+    form = {"F2": dual.FORM_F2, "F1": dual.FORM_F1, "KVL": dual.FORM_KVL}[args.form]
     config, quad, B_total = WORKLOADS[args.workload]
     if B_total > 1 and args.scaling == "weak":
         # weak scaling (independent instances, no data-path collective): every
@@ -307,7 +308,7 @@ def main():
         sw = np.zeros(net.n_branch, np.uint8)
         sw[net.n_tree:] = 1
     ospec, alpha0 = opt_spec(args)
-    if args.opt != "plain":
+    if args.opt != "plain" or form == dual.FORM_KVL:
         path = dual.PATH_CLUSTER
     h = dual.DcopfDual(net, form=form, device=local, path=path, switchable=sw)
     if args.opt != "plain":
@@ -403,7 +404,8 @@ def main():
         value = inst_it / (ms_max / 1e3)
         # algorithmic HBM bytes of the timed launch: K iterations (read + write
         # the multipliers, read the loads) + the final evaluation (reads only)
-        eval_read = 8 * (2 * net.n_bus + net.n_branch * (1 if form == dual.FORM_F2 else 2))
+        n_bm = (info.alg_bytes_per_inst_iter // 8 - 3 * net.n_bus) // 2  # branch-block multipliers per instance
+        eval_read = 8 * (2 * net.n_bus + n_bm)
         per_gpu_bytes = B * (info.alg_bytes_per_inst_iter * K + (eval_read if path == dual.PATH_BATCHED else 0))
         achieved = per_gpu_bytes / (ms / 1e3) / 1e9  # GB/s on this rank's kernel launches
         traffic = None  # DRAM bytes per launch, from the committed ncu capture (scaled to this launch)

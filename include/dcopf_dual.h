@@ -63,7 +63,19 @@ enum {
   DCOPF_ESTATE = -5     /* call out of order (e.g. iterate before set_instance_batch) */
 };
 
-enum { DCOPF_FORM_FLOW_BOX = 0 /* F2 */, DCOPF_FORM_LIMIT_ROWS = 1 /* F1 */ };
+enum {
+  DCOPF_FORM_FLOW_BOX = 0,   /* F2 */
+  DCOPF_FORM_LIMIT_ROWS = 1, /* F1 */
+  DCOPF_FORM_CYCLE = 2       /* KVL: angle-free cycle-basis twin of the paper's PTDF constraint
+                                (Eq. 1): boxes p, |f| <= F; KCL
+                                dualised with lambda, Kirchhoff's voltage law on the fundamental
+                                cycles of a canonical spanning tree (reading A-28) with
+                                free kappa[n_cycles], n_cycles = n_branch - n_bus + 1.  Cluster
+                                path only; the branch block of get/set_multipliers and evaluate is
+                                kappa[n_cycles][B] in canonical cycle order; outages must be
+                                switchable branches (the tree is built from the never-switchable
+                                ones) */
+};
 
 /* per-instance status: a diverged instance is frozen; the
  * others continue.  DIVERGED = g(y_k) non-finite or |g(y_k)| > 1e15; the step

@@ -35,7 +35,9 @@ struct ClHeader {
   int off_lam, off_d, off_br, off_th, off_fc, off_red;  // state arrays (bytes)
   int blob_bytes;               // records + header (copied from global)
   int off_s1l, off_s2l, off_s1b, off_s2b;  // optimiser state (lambda / branch), 0 if absent
-  int pad[7];
+  int nCy, cy0, off_Cy, off_CE, off_zero;   // KVL form: owned cycles, first one, records, a zero slot
+  int nCE;                                  // KVL form: cycle-term entries
+  int pad[1];
 };
 static_assert(sizeof(ClHeader) == 128, "ClHeader is 128 bytes");
 
@@ -47,6 +49,28 @@ struct alignas(16) ClC { int g0, g1, e0, e1; };                           // own
 struct alignas(8) ClIC2 { unsigned f; int sgn; };                         // F2: sgn = to ? +1 : -1
 struct alignas(16) ClIC1 { unsigned ts, tt; int br, pad; double sb, pad2; };  // F1: sb = to ? b : -b
 struct alignas(16) ClG { double c, lo, hi, a; };
+// KVL form (angle-free, cycle basis): phase B per owned branch, its cycle terms; phase C per owned cycle
+struct alignas(16) ClBk { unsigned ls, lt; int e0, e1; double x, F; int br, pad0, pad1, pad2; };  // x = 1/b
+struct alignas(16) ClBKe { unsigned kap; int sgn, dbr, pad; };  // kappa of a cycle containing the branch (dbr: its
+                                                                // defining branch, for outage masking)
+struct alignas(16) ClCy { int e0, e1, dbr, pad; };               // owned cycle
+struct alignas(16) ClCe { unsigned f; int pad; double sx; };    // f* of a cycle branch, sx = C_kl x_l
+
+// Fundamental cycle basis (reading A-28) in some branch numbering:
+// cycle k is defined by non-tree branch def[k]; its branches cb[cp[k]..cp[k+1])
+// (ascending ORIGINAL id) with signs cs.
+struct CycleBasis {
+  int nc = 0;
+  std::vector<int> def, cp, cb, cs;
+  std::vector<uint8_t> is_tree;
+};
+
+// The canonical basis of the network, in ORIGINAL branch ids: a breadth-first
+// tree from `ref` (FIFO bus order, each bus's incident branches in ascending
+// id) over branches with b > 0 that are never switched; non-tree branches in
+// ascending id.  Returns "" or an error (disconnected).
+std::string build_cycle_basis(int nb, int nl, int ref, const int *fr, const int *to, const double *b,
+                              const uint8_t *sw, CycleBasis *out);
 
 struct ClusterPlan {
   int C = 1;                          // CTAs per cluster
@@ -55,11 +79,15 @@ struct ClusterPlan {
   std::vector<uint8_t> blob;          // C blobs (header + records)
   std::vector<int> bus_lo, br_lo;     // [C+1] owned ranges (internal ids)
   int nb_max = 0, nl_max = 0;
+  std::vector<int> cyc_lo;            // KVL: [C+1] owned ranges of the internal cycle order
+  std::vector<int> cyc_perm;          // KVL: internal cycle index -> canonical cycle k
 };
 
 // Partition the internal network over C CTAs and lay out their shared memory.
 // Returns "" or an error (e.g. a partition does not fit max_smem).
 // nstate: optimiser state arrays per multiplier (0 plain, 1 GDM / AdaGrad, 2 Adam).
-std::string build_cluster_plan(const NetInternal &net, int C, int max_smem, int nstate, ClusterPlan *out);
+// cyc: the cycle basis in INTERNAL branch ids (KVL form only, else null).
+std::string build_cluster_plan(const NetInternal &net, int C, int max_smem, int nstate, ClusterPlan *out,
+                               const CycleBasis *cyc = nullptr);
 
 }  // namespace dcopf

@@ -45,6 +45,7 @@ struct ClusterArgs {
   long k_base;
   double *grad_lam, *grad_br, *value;  // EVAL outputs (instance-major) or null
   int n_bus, n_br;
+  int n_bm;                     // branch-block multipliers per instance: n_br (F2), 2 n_br (F1), n_cycles (KVL)
   // ascent-step variant (dcopf_dual.h DCOPF_OPT_*) and its persistent state
   int opt;
   double rho, beta1, beta2, eps;
@@ -160,7 +161,25 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
 #pragma unroll
   for (int j = 0; j < kMaxOut; ++j) o[j] = (j < nout) ? a.outs[b * nout + j] : -1;
   auto cvt = [&](unsigned x) { return cl_map(sbase + (x & ((1u << kClAddrShift) - 1)), x >> kClAddrShift); };
-  if (FORM == kFormF2) {
+  if (FORM == kFormKVL) {
+    const unsigned zero = cl_map(sbase + H.off_zero, rank);  // masked cycle terms read 0.0
+    if (tid == 0) reinterpret_cast<double *>(smem + H.off_zero)[0] = 0.0;
+    ClBKe *BK = reinterpret_cast<ClBKe *>(smem + H.off_IA);
+    for (int e = tid; e < H.nIA; e += nthr) BK[e].kap = is_out(o, nout, BK[e].dbr) ? zero : cvt(BK[e].kap);
+    ClBk *Bv = reinterpret_cast<ClBk *>(smem + H.off_B);
+    for (int j = tid; j < nB; j += nthr) {
+      Bv[j].ls = cvt(Bv[j].ls);
+      Bv[j].lt = cvt(Bv[j].lt);
+      if (is_out(o, nout, Bv[j].br)) Bv[j].x = Bv[j].F = 0.0;  // an outaged branch: b = F = 0 (A-16)
+    }
+    ClIC2 *IC = reinterpret_cast<ClIC2 *>(smem + H.off_IC);
+    for (int e = tid; e < H.nIC; e += nthr) IC[e].f = cvt(IC[e].f);
+    ClCy *Cy = reinterpret_cast<ClCy *>(smem + H.off_Cy);
+    for (int c = tid; c < H.nCy; c += nthr)
+      if (is_out(o, nout, Cy[c].dbr)) Cy[c].e1 = Cy[c].e0;  // its defining branch is out: no cycle
+    ClCe *CE = reinterpret_cast<ClCe *>(smem + H.off_CE);
+    for (int e = tid; e < H.nCE; e += nthr) CE[e].f = cvt(CE[e].f);
+  } else if (FORM == kFormF2) {
     ClIA2 *IA = reinterpret_cast<ClIA2 *>(smem + H.off_IA);
     ClIC2 *IC = reinterpret_cast<ClIC2 *>(smem + H.off_IC);
     for (int e = tid; e < H.nIA; e += nthr) {
@@ -183,7 +202,7 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
       }
     }
   }
-  {
+  if (FORM != kFormKVL) {
     ClB *Bv = reinterpret_cast<ClB *>(smem + H.off_B);
     for (int j = tid; j < nB; j += nthr) {
       Bv[j].ts = cvt(Bv[j].ts);
@@ -194,28 +213,31 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
     }
   }
   // ---- this CTA's state ------------------------------------------------------------
+  // branch-block multipliers of this CTA: nu / mu of its branches, or kappa of its cycles (KVL)
+  const size_t bm0 = b * (size_t)a.n_bm + (FORM == kFormKVL ? (size_t)H.cy0 : (size_t)H.br0 * BRW);
+  const int nbm = (FORM == kFormKVL) ? H.nCy : nB * BRW;
   const double *lam_g = a.lam + b * (size_t)a.n_bus + H.bus0;
-  const double *br_g = a.br + (b * (size_t)a.n_br + H.br0) * BRW;
+  const double *br_g = a.br + bm0;
   const double *d_g = a.d + b * (size_t)a.n_bus + H.bus0;
   for (int i = tid; i < nA; i += nthr) {
     lam_s[i] = lam_g[i];
     d_s[i] = d_g[i];
   }
-  for (int j = tid; j < nB * BRW; j += nthr) br_s[j] = br_g[j];
+  for (int j = tid; j < nbm; j += nthr) br_s[j] = br_g[j];
   // optimiser state (same layout as the multipliers)
   const bool ost = (MODE == kModeStep) && a.opt != DCOPF_OPT_PLAIN;
   const bool ost2 = ost && a.opt == DCOPF_OPT_ADAM;
   double *s1l = reinterpret_cast<double *>(smem + H.off_s1l), *s2l = reinterpret_cast<double *>(smem + H.off_s2l);
   double *s1b = reinterpret_cast<double *>(smem + H.off_s1b), *s2b = reinterpret_cast<double *>(smem + H.off_s2b);
   if (ost) {
-    const size_t ol = b * (size_t)a.n_bus + H.bus0, ob = (b * (size_t)a.n_br + H.br0) * BRW;
+    const size_t ol = b * (size_t)a.n_bus + H.bus0;
     for (int i = tid; i < nA; i += nthr) {
       s1l[i] = a.s1_lam[ol + i];
       if (ost2) s2l[i] = a.s2_lam[ol + i];
     }
-    for (int j = tid; j < nB * BRW; j += nthr) {
-      s1b[j] = a.s1_br[ob + j];
-      if (ost2) s2b[j] = a.s2_br[ob + j];
+    for (int j = tid; j < nbm; j += nthr) {
+      s1b[j] = a.s1_br[bm0 + j];
+      if (ost2) s2b[j] = a.s2_br[bm0 + j];
     }
   }
   double b1t = a.b1t, b2t = a.b2t;
@@ -264,7 +286,8 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
       b2t = b2t * a.beta2;
     }
     double val = 0.0;
-    // ---------------- A: w_i, theta*_i ----------------
+    // ---------------- A: w_i, theta*_i (not in the angle-free KVL form) ----------------
+    if (FORM != kFormKVL) {
     for (int i = tid; i < nA; i += nthr) {
       const ClA r = Ar[i];
       double w = 0.0;
@@ -289,8 +312,27 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
     }
     cl_sync();
     if (FORM == kFormF2 && k > 0) finish(k - 1);
+    }
     const bool step = (MODE == kModeStep) && (k < K) && !flag[0];
     // ---------------- B: branches ----------------
+    if (FORM == kFormKVL) {
+      // q_l = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t), cycles in ascending k
+      const ClBk *Bk = reinterpret_cast<const ClBk *>(smem + H.off_B);
+      const ClBKe *BK = reinterpret_cast<const ClBKe *>(smem + H.off_IA);
+      for (int j = tid; j < nB; j += nthr) {
+        const ClBk r = Bk[j];
+        double sum = 0.0;
+        for (int e = r.e0; e < r.e1; ++e) {
+          const ClBKe x = BK[e];
+          const double kv = cl_ld(x.kap);
+          sum = (x.sgn > 0) ? sum + kv : sum - kv;
+        }
+        const double q = r.x * sum - (cl_ld(r.ls) - cl_ld(r.lt));
+        const double f = (q > 0.0) ? -r.F : ((q < 0.0) ? r.F : 0.0);
+        fc_s[j] = f;
+        val += q * f;
+      }
+    } else
     for (int j = tid; j < nB; j += nthr) {
       const ClB r = Br[j];
       const double phi = r.b * (cl_ld(r.ts) - cl_ld(r.tt));
@@ -333,7 +375,7 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
         gl = gl + p;
         val += (G.a > 0.0) ? G.a * p * p + rc * p : rc * p;
       }
-      if (FORM == kFormF2) {
+      if (FORM == kFormF2 || FORM == kFormKVL) {
         const ClIC2 *IC = reinterpret_cast<const ClIC2 *>(smem + H.off_IC);
         for (int e = r.e0; e < r.e1; ++e) {
           const ClIC2 x = IC[e];
@@ -351,6 +393,22 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
       if (step) lam_s[i] = ost ? opt_step(a, li, gl, alpha, &s1l[i], &s2l[i], b1t, b2t) : li + alpha * gl;
       if (MODE == kModeEval) a.grad_lam[b * (size_t)a.n_bus + H.bus0 + i] = gl;
     }
+    if (FORM == kFormKVL) {
+      // d/dkappa_k = sum_l C_kl (f*_l x_l), branches in ascending id (f * (-x) == -(f x))
+      const ClCy *Cy = reinterpret_cast<const ClCy *>(smem + H.off_Cy);
+      const ClCe *CE = reinterpret_cast<const ClCe *>(smem + H.off_CE);
+      for (int c = tid; c < H.nCy; c += nthr) {
+        const ClCy r = Cy[c];
+        double acc = 0.0;
+        for (int e = r.e0; e < r.e1; ++e) {
+          const ClCe x = CE[e];
+          acc = acc + cl_ld(x.f) * x.sx;
+        }
+        const double kv = br_s[c];
+        if (step) br_s[c] = ost ? opt_step(a, kv, acc, alpha, &s1b[c], &s2b[c], b1t, b2t) : kv + alpha * acc;
+        if (MODE == kModeEval) a.grad_br[b * (size_t)a.n_bm + H.cy0 + c] = acc;
+      }
+    }
     // ---------------- this CTA's partial of g(y_k) ----------------
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
@@ -362,26 +420,26 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       if (lane == 0) red[0] = v;
     }
-    if (FORM == kFormF1 || k == K) {
-      cl_sync();  // F1: the next A reads lambda'; and every partial is published
+    if (FORM != kFormF2 || k == K) {
+      cl_sync();  // F1 / KVL: the next phase reads lambda' (kappa'); and every partial is published
       finish(k);
     }
   }
   // ---- results -----------------------------------------------------------------
   if (MODE == kModeStep) {
     double *lam_o = a.lam + b * (size_t)a.n_bus + H.bus0;
-    double *br_o = a.br + (b * (size_t)a.n_br + H.br0) * BRW;
+    double *br_o = a.br + bm0;
     for (int i = tid; i < nA; i += nthr) lam_o[i] = lam_s[i];
-    for (int j = tid; j < nB * BRW; j += nthr) br_o[j] = br_s[j];
+    for (int j = tid; j < nbm; j += nthr) br_o[j] = br_s[j];
     if (ost) {
-      const size_t ol = b * (size_t)a.n_bus + H.bus0, ob = (b * (size_t)a.n_br + H.br0) * BRW;
+      const size_t ol = b * (size_t)a.n_bus + H.bus0;
       for (int i = tid; i < nA; i += nthr) {
         a.s1_lam[ol + i] = s1l[i];
         if (ost2) a.s2_lam[ol + i] = s2l[i];
       }
-      for (int j = tid; j < nB * BRW; j += nthr) {
-        a.s1_br[ob + j] = s1b[j];
-        if (ost2) a.s2_br[ob + j] = s2b[j];
+      for (int j = tid; j < nbm; j += nthr) {
+        a.s1_br[bm0 + j] = s1b[j];
+        if (ost2) a.s2_br[bm0 + j] = s2b[j];
       }
     }
   }

@@ -79,6 +79,10 @@ struct dcopf_dual_s {
   dcopf_optimizer opt = {DCOPF_OPT_PLAIN, 0, 0.0, 0.0, 0.0, 0.0};
   double *os[4] = {nullptr, nullptr, nullptr, nullptr};  // s1_lam, s2_lam, s1_br, s2_br
   double b1t = 1.0, b2t = 1.0;                            // beta^t after the steps taken so far
+  // branch-block multipliers: entities x components (F2: n_br x 1, F1: n_br x 2, KVL: cycles x 1)
+  int n_bm_ent = 0, bm_C = 1;
+  CycleBasis cyc_orig, cyc_int;                 // KVL: canonical cycle basis (original / internal branch ids)
+  int *d_cyc_perm = nullptr, *d_cyc_inv = nullptr;  // KVL: internal cycle order <-> canonical k
   // cluster path: per-rank plan blobs
   ClusterPlan cplan;
   int cplan_C = 0;
@@ -384,6 +388,8 @@ struct Perms {
 Perms perms(dcopf_dual_t h) {
   if (h->path == DCOPF_PATH_BATCHED)
     return Perms{h->d_lam_perm_b, h->d_lam_inv_b, h->d_d_perm_b, h->d_br_perm_b, h->d_br_inv_b};
+  if (h->form == DCOPF_FORM_CYCLE)
+    return Perms{h->d_bus_perm, h->d_bus_inv, h->d_bus_perm, h->d_cyc_perm, h->d_cyc_inv};
   return Perms{h->d_bus_perm, h->d_bus_inv, h->d_bus_perm, h->d_br_perm, h->d_br_inv};
 }
 
@@ -414,8 +420,8 @@ int reset_opt_state(dcopf_dual_t h, cudaStream_t s) {
   h->b1t = h->b2t = 1.0;
   const int ns = opt_nstate(h);
   if (h->B == 0 || h->path != DCOPF_PATH_CLUSTER || ns == 0) return DCOPF_OK;
-  const size_t n[4] = {(size_t)h->B * h->n_bus, (size_t)h->B * h->n_bus, (size_t)h->B * h->n_br * brw(h->form),
-                       (size_t)h->B * h->n_br * brw(h->form)};
+  const size_t n[4] = {(size_t)h->B * h->n_bus, (size_t)h->B * h->n_bus, (size_t)h->B * h->n_bm_ent * h->bm_C,
+                       (size_t)h->B * h->n_bm_ent * h->bm_C};
   for (int x = 0; x < 4; ++x) {
     if (x == 1 || x == 3) {
       if (ns < 2) continue;
@@ -437,11 +443,15 @@ int configure_cluster(dcopf_dual_t h) {
   std::string err;
   for (; C <= 16; C *= 2) {
     ClusterPlan pl;
-    err = build_cluster_plan(h->ni, C, h->dev_smem, opt_nstate(h), &pl);
+    err = build_cluster_plan(h->ni, C, h->dev_smem, opt_nstate(h), &pl,
+                             h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr);
     if (!err.empty()) continue;
-    auto fn = (h->form == DCOPF_FORM_FLOW_BOX) ? k_cluster<kFormF2, kModeStep> : k_cluster<kFormF1, kModeStep>;
-    const void *fns[4] = {(const void *)k_cluster<kFormF2, kModeStep>, (const void *)k_cluster<kFormF2, kModeEval>,
-                          (const void *)k_cluster<kFormF1, kModeStep>, (const void *)k_cluster<kFormF1, kModeEval>};
+    auto fn = (h->form == DCOPF_FORM_FLOW_BOX)   ? k_cluster<kFormF2, kModeStep>
+              : (h->form == DCOPF_FORM_CYCLE) ? k_cluster<kFormKVL, kModeStep>
+                                              : k_cluster<kFormF1, kModeStep>;
+    const void *fns[6] = {(const void *)k_cluster<kFormF2, kModeStep>,  (const void *)k_cluster<kFormF2, kModeEval>,
+                          (const void *)k_cluster<kFormF1, kModeStep>,  (const void *)k_cluster<kFormF1, kModeEval>,
+                          (const void *)k_cluster<kFormKVL, kModeStep>, (const void *)k_cluster<kFormKVL, kModeEval>};
     for (const void *f : fns) {
       CK(h, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
       if (C > 8) CK(h, cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -469,6 +479,12 @@ int configure_cluster(dcopf_dual_t h) {
     h->cplan = pl;
     h->cplan_C = C;
     int rc = upload(h, &h->d_cblob, h->cplan.blob);
+    if (!rc && h->form == DCOPF_FORM_CYCLE) {  // state order of kappa: internal -> canonical k and back
+      std::vector<int> inv(h->n_bm_ent);
+      for (int x = 0; x < h->n_bm_ent; ++x) inv[h->cplan.cyc_perm[x]] = x;
+      rc = upload(h, &h->d_cyc_perm, h->cplan.cyc_perm);
+      if (!rc) rc = upload(h, &h->d_cyc_inv, inv);
+    }
     std::vector<uint8_t>().swap(h->cplan.blob);
     return rc;
   }
@@ -494,6 +510,7 @@ ClusterArgs cluster_args(dcopf_dual_t h) {
   a.k_base = h->k_base;
   a.n_bus = h->n_bus;
   a.n_br = h->n_br;
+  a.n_bm = h->n_bm_ent * h->bm_C;
   a.opt = h->opt.variant;
   a.rho = h->opt.momentum;
   a.beta1 = h->opt.beta1;
@@ -524,6 +541,7 @@ int launch_cluster(dcopf_dual_t h, const ClusterArgs &a, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (h->form == DCOPF_FORM_FLOW_BOX) CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormF2, MODE>, a));
+  else if (h->form == DCOPF_FORM_CYCLE) CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormKVL, MODE>, a));
   else CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormF1, MODE>, a));
   CK(h, cudaGetLastError());
   return DCOPF_OK;
@@ -638,6 +656,8 @@ void dcopf_dual_destroy(dcopf_dual_t h) {
   if (!h) return;
   cudaSetDevice(h->device);
   free_batch(h);
+  cudaFree(h->d_cyc_perm);
+  cudaFree(h->d_cyc_inv);
   int *ip[] = {h->d_bus_ptr, h->d_bus_inc, h->d_gen_ptr,    h->d_br_s,      h->d_br_t,    h->d_bus_perm,
                h->d_bus_inv, h->d_br_perm, h->d_br_inv,     h->d_prog_bytes, h->d_tx_bytes, h->d_ld_ptr,
                h->d_ld,      h->flag,      h->d_lam_perm_b, h->d_lam_inv_b, h->d_d_perm_b, h->d_br_perm_b,
@@ -662,7 +682,7 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   memset(&o, 0, sizeof o);
   o.precision = 64;
   if (opt) o = *opt;
-  if (o.form != DCOPF_FORM_FLOW_BOX && o.form != DCOPF_FORM_LIMIT_ROWS)
+  if (o.form != DCOPF_FORM_FLOW_BOX && o.form != DCOPF_FORM_LIMIT_ROWS && o.form != DCOPF_FORM_CYCLE)
     return fail(nullptr, DCOPF_EINVAL, "unknown form %d", o.form);
   if (o.precision != 64 && o.precision != 0)
     return fail(nullptr, DCOPF_EINVAL, "precision %d not supported (fp64 only)", o.precision);
@@ -766,6 +786,20 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
     delete h;
     return fail(nullptr, DCOPF_EINVAL, "%s", ierr.c_str());
   }
+  h->n_bm_ent = nl;
+  h->bm_C = (h->form == DCOPF_FORM_LIMIT_ROWS) ? 2 : 1;
+  if (h->form == DCOPF_FORM_CYCLE) {  // the canonical cycle basis (reading A-28), then internal branch ids
+    const std::string cerr = build_cycle_basis(nb, nl, net->ref_bus, fr.data(), to.data(), net->br_b,
+                                               net->br_switchable, &h->cyc_orig);
+    if (!cerr.empty()) {
+      delete h;
+      return fail(nullptr, DCOPF_ETOPOLOGY, "%s", cerr.c_str());
+    }
+    h->cyc_int = h->cyc_orig;
+    for (int &l : h->cyc_int.def) l = in.br_inv[l];
+    for (int &l : h->cyc_int.cb) l = in.br_inv[l];
+    h->n_bm_ent = h->cyc_orig.nc;
+  }
   h->bus_perm = in.bus_perm;
   h->bus_inv = in.bus_inv;
   h->br_perm = in.br_perm;
@@ -823,9 +857,16 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   int path = h->path_opt;
+  if (h->form == DCOPF_FORM_CYCLE && path != DCOPF_PATH_AUTO && path != DCOPF_PATH_CLUSTER)
+    return fail(h, DCOPF_EINVAL, "the KVL (cycle) form runs on the cluster path only");
   if (path == DCOPF_PATH_AUTO) {
-    path = (B <= h->single_max || h->opt.variant != DCOPF_OPT_PLAIN) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
-    if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) path = DCOPF_PATH_SINGLE;
+    path = (B <= h->single_max || h->opt.variant != DCOPF_OPT_PLAIN || h->form == DCOPF_FORM_CYCLE)
+               ? DCOPF_PATH_CLUSTER
+               : DCOPF_PATH_BATCHED;
+    if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) {
+      if (h->form == DCOPF_FORM_CYCLE) return DCOPF_EINVAL;  // (message set by configure_cluster)
+      path = DCOPF_PATH_SINGLE;
+    }
   }
   int W = 1;
   if (path == DCOPF_PATH_BATCHED) {
@@ -858,6 +899,9 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
       if (l < -1 || l >= h->n_br) return fail(h, DCOPF_EINVAL, "outage id %d out of range", l);
       if (l >= 0 && !h->switchable.empty() && !h->switchable[l])
         return fail(h, DCOPF_EINVAL, "branch %d is not switchable", l);
+      if (l >= 0 && h->form == DCOPF_FORM_CYCLE && h->cyc_orig.is_tree[l])
+        return fail(h, DCOPF_EINVAL, "branch %d is in the cycle-basis tree (KVL form): declare the switchable "
+                                     "branches (br_switchable) so the tree avoids them", l);
       outs_h[x] = l < 0 ? -1 : h->br_inv[l];
     }
   }
@@ -870,7 +914,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   h->B_pad = B_pad;
   h->max_out = max_out;
   h->cur = 0;
-  const size_t nlam = (size_t)B_pad * h->n_bus, nbr = (size_t)B_pad * h->n_br * brw(h->form);
+  const size_t nlam = (size_t)B_pad * h->n_bus, nbr = (size_t)B_pad * h->n_bm_ent * h->bm_C;
   if (!reuse) {
     const int nbuf = (path == DCOPF_PATH_BATCHED) ? 2 : 1;
     for (int i = 0; i < nbuf; ++i) {
@@ -981,7 +1025,7 @@ int dcopf_dual_get_multipliers(dcopf_dual_t h, double *lambda, double *branch, v
   const int cur = (h->path == DCOPF_PATH_BATCHED) ? h->cur : 0;
   const Perms pm = perms(h);
   int rc = export_ext(h, h->lam[cur], lambda, pm.lam_inv, h->n_bus, 1, s);
-  if (!rc) rc = export_ext(h, h->br[cur], branch, pm.br_inv, h->n_br, brw(h->form), s);
+  if (!rc) rc = export_ext(h, h->br[cur], branch, pm.br_inv, h->n_bm_ent, h->bm_C, s);
   return rc;
 }
 
@@ -991,7 +1035,7 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   const int cur = (h->path == DCOPF_PATH_BATCHED) ? h->cur : 0;
-  const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_br * brw(h->form);
+  const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_bm_ent * h->bm_C;
   double *tl = nullptr, *tb = nullptr;
   CK(h, cudaMalloc(&tl, std::max<size_t>(nlam, 1) * 8));
   cudaError_t e = cudaMalloc(&tb, std::max<size_t>(nbr, 1) * 8);
@@ -1002,7 +1046,7 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
   int rc = DCOPF_OK;
   const Perms pm = perms(h);
   if (lambda) rc = import_ext(h, lambda, tl, pm.lam_perm, h->n_bus, 1, s);
-  if (!rc && branch) rc = import_ext(h, branch, tb, pm.br_perm, h->n_br, brw(h->form), s);
+  if (!rc && branch) rc = import_ext(h, branch, tb, pm.br_perm, h->n_bm_ent, h->bm_C, s);
   if (!rc) {
     int bad = 0;
     cudaMemsetAsync(h->flag, 0, sizeof(int), s);
@@ -1039,7 +1083,7 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_br * brw(h->form);
+  const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_bm_ent * h->bm_C;
   if (!h->g_lam) CK(h, cudaMalloc(&h->g_lam, std::max<size_t>(nlam, 1) * 8));
   if (!h->g_br) CK(h, cudaMalloc(&h->g_br, std::max<size_t>(nbr, 1) * 8));
   int rc;
@@ -1067,7 +1111,7 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
   rc = copy_out(h, value, h->value, s);
   const Perms pm = perms(h);
   if (!rc) rc = export_ext(h, h->g_lam, grad_lambda, pm.lam_inv, h->n_bus, 1, s);
-  if (!rc) rc = export_ext(h, h->g_br, grad_branch, pm.br_inv, h->n_br, brw(h->form), s);
+  if (!rc) rc = export_ext(h, h->g_br, grad_branch, pm.br_inv, h->n_bm_ent, h->bm_C, s);
   return rc;
 }
 
@@ -1136,7 +1180,7 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
   info->n_branch = h->n_br;
   info->n_gen = h->n_gen;
   info->quadratic = h->quadratic;
-  info->alg_bytes_per_inst_iter = 8LL * (3LL * h->n_bus + (h->form == DCOPF_FORM_LIMIT_ROWS ? 4LL : 2LL) * h->n_br);
+  info->alg_bytes_per_inst_iter = 8LL * (3LL * h->n_bus + 2LL * h->n_bm_ent * h->bm_C);
   info->bandwidth = h->bandwidth;
   if (h->path == DCOPF_PATH_BATCHED) {
     info->smem_bytes = h->sch.total;

@@ -20,6 +20,7 @@ from . import _build
 
 FORM_F2 = 0  # DCOPF_FORM_FLOW_BOX
 FORM_F1 = 1  # DCOPF_FORM_LIMIT_ROWS
+FORM_KVL = 2  # DCOPF_FORM_CYCLE (cluster path only)
 PATH_AUTO, PATH_BATCHED, PATH_SINGLE, PATH_CLUSTER = 0, 1, 2, 3
 INST_OK, INST_DIVERGED = 0, 1
 OPT_PLAIN, OPT_GDM, OPT_GDM_CLASSIC, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2, 3, 4
@@ -176,6 +177,8 @@ class DcopfDual:
 
     @property
     def n_branch_mult(self):
+        if self.form == FORM_KVL:
+            return self.net.n_branch - self.net.n_bus + 1
         return self.net.n_branch * (2 if self.form == FORM_F1 else 1)
 
     # -- ABI calls ------------------------------------------------------------

@@ -442,3 +442,82 @@ def test_optimizer_rejected_off_the_cluster_path():
     with pytest.raises(dual.DcopfError):
         h.set_optimizer(99)
     h.close()
+
+
+# ---------------------------------------------------------------------------
+# KVL (cycle-basis) form, on the cluster path
+
+
+@pytest.mark.parametrize("name", ["plain"] + sorted(OPTS))
+def test_kvl_config0(name):
+    opt, alpha = OPTS[name] if name != "plain" else (None, 1e-2)
+    net = inst.make_network(0)
+    K = 3000
+    a = inst.alpha_schedule(K, alpha)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=oracle.FORM_KVL, history=True, opt=opt)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=dual.FORM_KVL, history=True, opt=opt, split=777)
+    assert gpu["info"].path == dual.PATH_CLUSTER
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("C", [1, 4, 16])
+def test_kvl_cluster_sizes_and_outages(C, monkeypatch):
+    monkeypatch.setenv("DCOPF_CLUSTER", str(C))
+    net = inst.tiny_network(600, 900, 150, seed=4)
+    sw = non_tree_switchable(net)
+    rng = np.random.default_rng(1)
+    B = 4
+    loads = net.base_load[None, :] * rng.uniform(0.8, 1.2, (B, net.n_bus))
+    outs = np.full((B, 3), -1, np.int32)
+    for j in range(1, B):
+        outs[j, :j] = rng.choice(np.arange(net.n_tree, net.n_branch), j, replace=False)
+    K = 500
+    opt, alpha = OPTS["adam"]
+    a = inst.alpha_schedule(K, alpha)
+    orc = oracle.solve(net, loads, outages=outs, K=K, alpha=a, form=oracle.FORM_KVL, history=True, opt=opt,
+                       switchable=sw)
+    gpu = run_gpu(net, loads, outages=outs, K=K, alpha=a, form=dual.FORM_KVL, history=True, opt=opt,
+                  switchable=sw)
+    assert gpu["info"].cluster_size == C
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+def test_kvl_config3_adam_and_evaluate():
+    net = inst.make_network(3)
+    K = 500
+    opt, alpha = OPTS["adam"]
+    a = inst.alpha_schedule(K, alpha)
+    orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=oracle.FORM_KVL, history=True, opt=opt)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=dual.FORM_KVL, history=True, opt=opt)
+    assert gpu["info"].cluster_size == 16
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+    # value and gradient at the reached point
+    import torch
+    dev = torch.device("cuda:0")
+    h = dual.DcopfDual(net, form=dual.FORM_KVL)
+    h.set_instance_batch(torch.from_numpy(net.base_load[:, None].copy()).to(dev))
+    h.set_multipliers(torch.from_numpy(orc.lam.T.copy()).to(dev), torch.from_numpy(orc.br.T.copy()).to(dev))
+    val = torch.empty(1, dtype=torch.float64, device=dev)
+    gl = torch.empty((net.n_bus, 1), dtype=torch.float64, device=dev)
+    gk = torch.empty((h.n_branch_mult, 1), dtype=torch.float64, device=dev)
+    h.evaluate(val, gl, gk)
+    ov, ogl, ogk, _, _ = oracle.evaluate_kvl(net, net.base_load, orc.lam, orc.br)
+    assert abs(float(val.cpu()[0]) - ov[0]) <= BOUND_RTOL * max(abs(ov[0]), cost_scale(net))
+    np.testing.assert_array_equal(gl.cpu().numpy()[:, 0], ogl[0])
+    np.testing.assert_array_equal(gk.cpu().numpy()[:, 0], ogk[0])
+    h.close()
+
+
+def test_kvl_rejects_tree_outage_and_other_paths():
+    import torch
+    net = inst.make_network(0)
+    with pytest.raises(dual.DcopfError):
+        h = dual.DcopfDual(net, form=dual.FORM_KVL, path=dual.PATH_BATCHED)
+        h.set_instance_batch(torch.from_numpy(np.tile(net.base_load[:, None], (1, 300))).cuda())
+    h = dual.DcopfDual(net, form=dual.FORM_KVL)   # no switchable mask: the tree may use any branch
+    d, _ = oracle.cycles(net)
+    tree = np.setdiff1d(np.arange(net.n_branch), d)
+    with pytest.raises(dual.DcopfError):
+        h.set_instance_batch(torch.from_numpy(net.base_load[:, None].copy()).cuda(),
+                             torch.tensor([[int(tree[0])]], dtype=torch.int32).cuda())
+    h.close()

@@ -51,7 +51,7 @@ def main():
     for wl, (config, quad) in WORKLOADS.items():
         if a.workloads and wl not in a.workloads:
             continue
-        for form_name, form in (("F2", oracle.FORM_F2), ("F1", oracle.FORM_F1)):
+        for form_name, form in (("F2", oracle.FORM_F2), ("F1", oracle.FORM_F1), ("KVL", oracle.FORM_KVL)):
             if form_name not in a.forms:
                 continue
             key = f"{wl}/{form_name}" + ("" if a.opt == "plain" else f"/{a.opt}/{alpha:g}")
@@ -66,8 +66,12 @@ def main():
                 ids = np.zeros(1, dtype=np.int64)
                 batch = inst.single_batch(net)
             t0 = time.time()
+            sw = None
+            if config == 4:  # only non-tree branches are ever taken out (bench.py passes the same mask)
+                sw = np.zeros(net.n_branch, np.uint8)
+                sw[net.n_tree:] = 1
             res = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K, alpha),
-                               form=form, threads=a.threads, opt=opt)
+                               form=form, threads=a.threads, opt=opt, switchable=sw)
             js[key] = {"K": K, "alpha": alpha, "opt": {"name": a.opt, **opt},
                        "instance_ids": ids.tolist(), "best": res.best.tolist(),
                        "bound": res.bound.tolist(), "status": res.status.tolist(),
