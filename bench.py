@@ -191,7 +191,7 @@ def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, 
     key = gap_key(args)
     try:
         ref = json.load(open(os.path.join(ROOT, "tests", "golden", "targets.json")))[key]
-    except (OSError, KeyError):
+    except (OSError, KeyError, ValueError):
         return {"unavailable": f"no oracle reference for {key} (run tools/make_targets.py)"}
     K = int(ref["K"])
     ids = np.asarray(ref["instance_ids"], dtype=np.int64)
@@ -229,9 +229,13 @@ def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, 
            "and schedule (tests/golden/targets.json)", "sampled_instances": n, "reached": reached,
            "max_hit_iteration": worst if world == 1 else None, "seconds": secs, "run_seconds_full_K": run_s,
            "reference_best_range": [float(best_ref.min()), float(best_ref.max())]}
-    opt = ref.get("primal_opt")
-    if opt is not None:
-        out["true_gap_at_K"] = ref.get("true_gap_at_K")
+    popt = ref.get("primal_opt")
+    if popt is not None and mine.any():  # (ii): the true gap of the GPU's best bound after K, vs the optimum
+        best = np.empty(batch.B)
+        h.get_bound(best=best)
+        b = float(best[ids[mine][0] - lo])
+        out["primal_opt"] = popt
+        out["true_gap_at_K"] = (popt - b) / abs(popt)
     return out
 
 

@@ -72,7 +72,10 @@ def main():
                 sw[net.n_tree:] = 1
             res = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K, alpha),
                                form=form, threads=a.threads, opt=opt, switchable=sw)
-            js[key] = {"K": K, "alpha": alpha, "opt": {"name": a.opt, **opt},
+            primal = None
+            if config != 4:  # the exact optimum (HiGHS; Kelley cutting planes for QP): true gap, (ii)
+                primal = (inst.primal_qp(net, net.base_load) if quad else inst.primal_lp(net, net.base_load))[1]
+            js[key] = {"K": K, "alpha": alpha, "opt": {"name": a.opt, **opt}, "primal_opt": primal,
                        "instance_ids": ids.tolist(), "best": res.best.tolist(),
                        "bound": res.bound.tolist(), "status": res.status.tolist(),
                        "source": "oracle/dcopf_oracle.c via tools/make_targets.py"}
