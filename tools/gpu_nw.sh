@@ -2,8 +2,6 @@ set -x
 run() { env "$@" python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e --no-gap --form ${FORM:-F2} > /tmp/o.txt 2>&1; grep '^{' /tmp/o.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$*', '%.4g' % d['value'], d['config']['kernel']['threads'], d['config']['kernel']['chunk'])" || tail -3 /tmp/o.txt; }
 L=paper_2406_13191_b200/lib
 for f in F2 F1; do
-for nw in 17 19 21; do
-FORM=$f run DCOPF_LIB=$L/libdcopf_dual_nw$nw.so DCOPF_SYNC=soft
-FORM=$f run DCOPF_LIB=$L/libdcopf_dual_nw$nw.so DCOPF_SYNC=hard
-done
+FORM=$f run X=1
+FORM=$f run DCOPF_LIB=$L/libdcopf_dual_nw15.so
 done
