@@ -511,17 +511,28 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     // A of the previous step, so the per-step maximum is what counts.
     std::vector<long> load(nw, 0);
     std::vector<uint16_t> wtab(3 * (nw + 1), 0);
+    // warps share the 4 SM sub-partitions (warp w on w % 4); the producer warp
+    // (index nw) mostly sleeps, so consumer warps on its sub-partition issue
+    // faster: their capacity is scaled by `sp` (DCOPF_SMSP_SPEED, measured)
+    std::vector<double> speed(nw, 1.0);
+    {
+      double sp = 1.0;  // measured: >1 does not help
+      if (const char *e = getenv("DCOPF_SMSP_SPEED")) sp = atof(e);
+      for (int w = 0; w < nw; ++w)
+        if (w % 4 == nw % 4) speed[w] = sp;
+    }
     auto balance = [&](auto &items, auto cost, int phase) {
       const int n = (int)items.size();
       std::vector<int> idx(n), own(n);
       for (int x = 0; x < n; ++x) idx[x] = x;
       std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost(items[a]) > cost(items[b]); });
       for (int x : idx) {
+        const long cx = cost(items[x]);
         int w = 0;
         for (int v = 1; v < nw; ++v)
-          if (load[v] < load[w]) w = v;
+          if ((load[v] + cx) / speed[v] < (load[w] + cx) / speed[w]) w = v;
         own[x] = w;
-        load[w] += cost(items[x]);
+        load[w] += cx;
       }
       std::vector<int> ord(n);
       for (int x = 0; x < n; ++x) ord[x] = x;

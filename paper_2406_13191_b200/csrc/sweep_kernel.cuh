@@ -96,6 +96,12 @@ __device__ __forceinline__ void warp_arrive(uint64_t *bar, int lane) {
 // completes (or this many ns pass) instead of re-polling, so waiting warps do
 // not take issue slots from the working ones
 constexpr unsigned kSuspendNs = 1000000;
+#ifndef DCOPF_BACKOFF_NS0
+#define DCOPF_BACKOFF_NS0 32
+#endif
+#ifndef DCOPF_BACKOFF_NSMAX
+#define DCOPF_BACKOFF_NSMAX 256
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   unsigned done = 0;
   do {
@@ -107,6 +113,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
         : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs)
         : "memory");
   } while (!done);
+}
+// consumer-to-consumer waits (A-done / B-done): test, then back off with
+// nanosleep so a waiting warp issues a handful of instructions instead of
+// re-polling (its SM sub-partition's other warps keep the issue slots)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, unsigned parity) {
+  unsigned done = 0, ns = DCOPF_BACKOFF_NS0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+    ns = ns < DCOPF_BACKOFF_NSMAX ? 2 * ns : ns;
+  }
 }
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
   asm volatile(
@@ -300,7 +324,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       const int nA = h0.x, nB = h0.z, nC = h0.w;
 
       if (a.debug_mode != 1) {  // (1: data movement only -- measurement)
-      if (SOFT && gs > 0) mbar_wait(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+      if (SOFT && gs > 0) mbar_wait_backoff(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       // ---------------- A(s): w_i, theta* codes ----------------
       {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
@@ -417,7 +441,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       }
       if (SOFT) {
         warp_arrive(&bdone[gs & 3], lane);
-        if (gs > 0) mbar_wait(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+        if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       }
       // ---------------- C(s-2): ready buses ----------------
       {
