@@ -81,7 +81,7 @@ enum {
  * others continue.  DIVERGED = g(y_k) non-finite or |g(y_k)| > 1e15; the step
  * of that iteration is still taken, no later step is (y frozen at y_{k+1}),
  * best keeps only valid values (reading A-23). */
-enum { DCOPF_INST_OK = 0, DCOPF_INST_DIVERGED = 1 };
+enum { DCOPF_INST_OK = 0, DCOPF_INST_DIVERGED = 1, DCOPF_INST_CONVERGED = 2 };
 
 /* kernel path selection */
 enum {
@@ -203,6 +203,16 @@ typedef struct {
   double epsilon;    /* AdaGrad / Adam guard (SPEC.md:359 suggests 1e-8) */
 } dcopf_optimizer;
 int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt);
+
+/* Per-instance stopping rule of Algorithm 1 ("if
+ * |gamma^(i+1) - gamma^(i)| < tolerance: Stop"): with tol > 0,
+ * an instance whose consecutive dual values within one iterate() call differ by
+ * less than tol gets status DCOPF_INST_CONVERGED and is frozen exactly like a
+ * diverged one (the step of the detecting iteration is taken, no later one;
+ * DESIGN.md reading A-29); the other instances of the batch go on.  tol = 0
+ * (default) disables it.  Persists until changed.  Errors: EINVAL (tol < 0 or
+ * not finite). */
+int dcopf_dual_set_stop(dcopf_dual_t h, double tol);
 
 /* Time to gap (BASELINE.json metric "time to 1e-3 gap"):
  * per-instance thresholds target[B] (host or device; NULL clears them).  The

@@ -28,6 +28,7 @@ FORM_F2 = 0  # flow box (lambda, nu)
 FORM_F1 = 1  # limit rows (lambda, mu+, mu-)
 FORM_KVL = 2  # cycle basis (lambda, kappa), no angles
 DIVERGED = 1
+CONVERGED = 2  # the stopping rule |g_k - g_{k-1}| < tol fired (Alg. 1)
 
 
 def build(force: bool = False) -> str:
@@ -56,7 +57,7 @@ def _load():
         lib.oracle_solve.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I]
         lib.oracle_solve.restype = I
         D = ctypes.c_double
-        lib.oracle_solve_opt.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I, I, D, D, D, D, P]
+        lib.oracle_solve_opt.argtypes = net + [I, L, P, P, I, L, P, P, P, P, P, P, P, I, I, I, D, D, D, D, P, D]
         lib.oracle_evaluate_kvl.argtypes = net + [P, L, P, P, I, P, P, P, P, P, P, P]
         lib.oracle_evaluate_kvl.restype = I
         lib.oracle_cycles.argtypes = net + [P, P, P, P, P, P, L]
@@ -106,7 +107,7 @@ class OracleResult:
 
 
 def solve(net, load, outages=None, K=0, alpha=None, form=FORM_F2, lam0=None, br0=None,
-          history=False, threads=1, opt=None, switchable=None) -> OracleResult:
+          history=False, threads=1, opt=None, switchable=None, tol=0.0) -> OracleResult:
     """K projected ascent steps from y_0 = 0 (or the given warm start).
     opt: None (plain step) or dict(variant=OPT_*, rho=, beta1=, beta2=, eps=)."""
     lib = _load()
@@ -133,7 +134,7 @@ def solve(net, load, outages=None, K=0, alpha=None, form=FORM_F2, lam0=None, br0
     rc = lib.oracle_solve_opt(*_net_args(net, keep), form, B, _p(load), _p(outs), max_out, K, _p(alpha),
                               _p(lam), _p(br), _p(bound), _p(best), _p(status), _p(hist), int(warm),
                               int(threads), int(o["variant"]), float(o["rho"]), float(o["beta1"]),
-                              float(o["beta2"]), float(o["eps"]), _p(_sw(switchable)))
+                              float(o["beta2"]), float(o["eps"]), _p(_sw(switchable)), float(tol))
     if rc != 0:
         raise ValueError("oracle_solve rejected its arguments")
     return OracleResult(lam, br, bound, best, status, hist)

@@ -66,6 +66,7 @@
 #define ORC_FORM_LIMIT_ROWS 1 /* F1: boxes p, theta; multipliers lambda, mu+, mu-   */
 #define ORC_FORM_CYCLE 2      /* KVL: boxes p, f; multipliers lambda (KCL), kappa (cycle KVL) */
 #define ORC_DIVERGED 1
+#define ORC_CONVERGED 2  /* stopping rule |g_k - g_{k-1}| < tol (Alg. 1) */
 
 typedef struct {
   int n_bus, n_branch, n_gen, ref_bus;
@@ -223,6 +224,7 @@ static int valid_bound(double g) { return isfinite(g) && fabs(g) <= 1e15; }
 typedef struct {
   int variant;
   double rho, beta1, beta2, eps;
+  double tol;  /* stopping rule (0: off) */
 } orc_opt;
 
 /* one coordinate of the ascent step (the variants above); s1, s2 = state */
@@ -449,6 +451,7 @@ static void run_instance(const orc_net *N, int form, const double *d, const int 
   long k;
   int i, j, frozen = 0;
   double b1t = 1.0, b2t = 1.0;                   /* beta1^t, beta2^t (Adam) */
+  double gprev = 0.0;                            /* g(y_{k-1}) for the stopping rule */
   double *s1 = calloc((size_t)(nb + nbr + 1), sizeof(double));   /* optimiser state, y order */
   double *s2 = calloc((size_t)(nb + nbr + 1), sizeof(double));
   work_alloc(&W, N, form);
@@ -464,9 +467,15 @@ static void run_instance(const orc_net *N, int form, const double *d, const int 
     int was_frozen = frozen;
     if (hist) hist[k] = g;
     if (!was_frozen) {                           /* (f) best = max(best, g) */
-      if (valid_bound(g)) { if (g > *best) *best = g; }
-      else { *status = ORC_DIVERGED; frozen = 1; }
+      if (valid_bound(g)) {
+        if (g > *best) *best = g;
+        /* Alg. 1 stopping rule: |gamma^(i+1) - gamma^(i)| < tol.
+         * Like divergence (reading A-23/A-29) the step of this iteration is
+         * still taken and every later one skipped. */
+        if (opt->tol > 0.0 && k > 0 && fabs(g - gprev) < opt->tol) { *status = ORC_CONVERGED; frozen = 1; }
+      } else { *status = ORC_DIVERGED; frozen = 1; }
     }
+    gprev = g;
     if (k == K) { *bound = g; break; }
     if (was_frozen) continue;
     {                                            /* (h) ascent step and projection */
@@ -514,13 +523,14 @@ int oracle_solve_opt(NET_ARGS, int form, long B, const double *load, const int *
                      long K, const double *alpha, double *lam, double *br, double *bound,
                      double *best, int *status, double *hist, int warm, int n_threads,
                      int variant, double rho, double beta1, double beta2, double eps,
-                     const unsigned char *switchable) {
+                     const unsigned char *switchable, double tol) {
   NET_INIT
   long j;
   orc_opt opt;
   orc_cyc Y;
   int nbr;
   opt.variant = variant; opt.rho = rho; opt.beta1 = beta1; opt.beta2 = beta2; opt.eps = eps;
+  opt.tol = tol;
   memset(&Y, 0, sizeof Y);
   if (variant < ORC_OPT_PLAIN || variant > ORC_OPT_ADAM) return -1;
   if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0 || K < 0) return -1;
@@ -589,7 +599,7 @@ int oracle_solve(NET_ARGS, int form, long B, const double *load, const int *outa
   return oracle_solve_opt(n_bus, n_branch, n_gen, ref_bus, br_from, br_to, br_b, br_fmax, theta_max,
                           gen_bus, gen_pmin, gen_pmax, gen_c, gen_a, form, B, load, outages, max_out, K,
                           alpha, lam, br, bound, best, status, hist, warm, n_threads,
-                          ORC_OPT_PLAIN, 0.0, 0.0, 0.0, 0.0, NULL);
+                          ORC_OPT_PLAIN, 0.0, 0.0, 0.0, 0.0, NULL, 0.0);
 }
 
 /* Value and gradient at given multipliers (no step). */

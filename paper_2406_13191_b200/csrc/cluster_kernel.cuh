@@ -52,6 +52,7 @@ struct ClusterArgs {
   double b1t, b2t;              // beta1^t, beta2^t at this launch's first step (Adam)
   double *s1_lam, *s2_lam;      // [b][n_bus] instance-major internal, or null
   double *s1_br, *s2_br;        // [b][n_br * BRW]
+  double tol;                   // stopping rule (0: off)
 };
 
 // One coordinate of the ascent step for the gradient-based-optimisation
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
   double b1t = a.b1t, b2t = a.b2t;
   if (tid == 0) flag[0] = (MODE != kModeEval) ? a.status[b] : 0;
   double best = (MODE != kModeEval) ? a.best[b] : 0.0;
+  double gprev = 0.0;  // g(y_{k-1}) within this call (stopping rule; warp 0 lane 0)
   __syncthreads();
   cl_sync();  // every CTA's shared memory is ready for remote reads
 
@@ -268,9 +270,14 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
             if (kk == K) a.bound[b] = g;
           }
           if (!frozen) {
-            if (valid_bound(g)) best = (g > best) ? g : best;
-            else frozen = 1;
+            if (valid_bound(g)) {
+              best = (g > best) ? g : best;
+              if (a.tol > 0.0 && kk > 0 && fabs(g - gprev) < a.tol) frozen = 2;  // Alg. 1 stopping rule
+            } else {
+              frozen = 1;
+            }
           }
+          gprev = g;
           if (rank == 0 && a.target && a.hit[b] < 0 && best >= a.target[b]) a.hit[b] = a.k_base + kk;
           flag[0] = frozen;
         }

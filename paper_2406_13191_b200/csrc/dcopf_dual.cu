@@ -60,6 +60,7 @@ struct dcopf_dual_s {
   double *target = nullptr;                           // time-to-gap thresholds [B_pad]
   long long *hit = nullptr;                           // first evaluation index reaching them [B_pad]
   bool has_target = false;
+  double tol = 0.0;                                   // stopping rule (set_stop)
   long k_base = 0;                                    // steps taken since set_instance_batch
   double *g_lam = nullptr, *g_br = nullptr;  // evaluate scratch (internal layout)
   double *scratch = nullptr;
@@ -518,6 +519,7 @@ ClusterArgs cluster_args(dcopf_dual_t h) {
   a.eps = h->opt.epsilon;
   a.b1t = h->b1t;
   a.b2t = h->b2t;
+  a.tol = h->tol;
   a.s1_lam = h->os[0];
   a.s2_lam = h->os[1];
   a.s1_br = h->os[2];
@@ -593,6 +595,7 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.off_th = sc.off_th;
   a.off_fc = sc.off_fc;
   a.soft = h->soft_sync;
+  a.tol = h->tol;
   if (const char *e = getenv("DCOPF_DEBUG_MODE")) a.debug_mode = atoi(e);  // measurement only
   return a;
 }
@@ -627,6 +630,7 @@ SingleArgs single_args(dcopf_dual_t h) {
   a.target = h->has_target ? h->target : nullptr;
   a.hit = h->hit;
   a.k_base = h->k_base;
+  a.tol = h->tol;
   return a;
 }
 
@@ -1140,6 +1144,13 @@ int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt) {
   int rc = reset_opt_state(h, nullptr);
   if (!rc) CK(h, cudaDeviceSynchronize());
   return rc;
+}
+
+int dcopf_dual_set_stop(dcopf_dual_t h, double tol) {
+  if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
+  if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(h, DCOPF_EINVAL, "tol must be finite and >= 0");
+  h->tol = tol;
+  return DCOPF_OK;
 }
 
 int dcopf_dual_set_target(dcopf_dual_t h, const double *target, void *cuda_stream) {

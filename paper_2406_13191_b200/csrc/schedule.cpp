@@ -594,8 +594,8 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   int off = 0;
   S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers
   off = al(off + 16 * S.S + 64);
-  S.off_frz = off;  // frozen flags [64] int, then running best [64] double
-  off = al(off + 4 * 64 + 8 * 64);
+  S.off_frz = off;  // frozen flags [64] int, then running best [64] and previous g [64] double
+  off = al(off + 4 * 64 + 2 * 8 * 64);
   S.off_obm = off;  // per-tile outage bitmap over branches
   off = al(off + 4 * ((nl + 31) / 32 + 1));
   S.off_outs = off;  // per-instance outage lists of the tile

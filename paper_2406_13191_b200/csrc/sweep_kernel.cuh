@@ -70,6 +70,7 @@ struct SweepArgs {
   int off_bar, off_red, off_frz, off_obm, off_outs, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th,
       off_fc;
   int soft;                         // 1: consumer warps drift by <= 1 step (pool_gap 2); 0: lock-step
+  double tol;                       // stopping rule (0: off)
   int debug_mode;                   // 0; 1 = data movement only; 2 = no row copies (measurement only)
 };
 
@@ -179,6 +180,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
   double *red = reinterpret_cast<double *>(smem + a.off_red);   // [NW][64]
   int *frz = reinterpret_cast<int *>(smem + a.off_frz);         // [64]
   double *bst = reinterpret_cast<double *>(smem + a.off_frz + 256);  // [64] running best (no registers held)
+  double *gpv = bst + 64;                                              // [64] previous g (stopping rule)
   unsigned *obm = reinterpret_cast<unsigned *>(smem + a.off_obm);
   int *outs_s = reinterpret_cast<int *>(smem + a.off_outs);     // [64][kMaxOut]
   constexpr int BRW = (FORM == kFormF2) ? 1 : 2;
@@ -541,16 +543,28 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
           a.bound[b1i] = g1;
         }
         double best0 = bst[2 * lane], best1 = bst[2 * lane + 1];
+        // (stopping rule: |g_k - g_{k-1}| < tol within this call; status 2)
+        const bool chk = a.tol > 0.0 && k > 0;
         if (!frz[2 * lane]) {
-          if (valid_bound(g0)) best0 = (g0 > best0) ? g0 : best0;
-          else frz[2 * lane] = 1;
+          if (valid_bound(g0)) {
+            best0 = (g0 > best0) ? g0 : best0;
+            if (chk && fabs(g0 - gpv[2 * lane]) < a.tol) frz[2 * lane] = 2;
+          } else {
+            frz[2 * lane] = 1;
+          }
         }
         if (!frz[2 * lane + 1]) {
-          if (valid_bound(g1)) best1 = (g1 > best1) ? g1 : best1;
-          else frz[2 * lane + 1] = 1;
+          if (valid_bound(g1)) {
+            best1 = (g1 > best1) ? g1 : best1;
+            if (chk && fabs(g1 - gpv[2 * lane + 1]) < a.tol) frz[2 * lane + 1] = 2;
+          } else {
+            frz[2 * lane + 1] = 1;
+          }
         }
         bst[2 * lane] = best0;
         bst[2 * lane + 1] = best1;
+        gpv[2 * lane] = g0;
+        gpv[2 * lane + 1] = g1;
         if (a.target) {  // time to gap: first evaluation whose running best reaches the target
           // (state kept in global memory, touched once per sweep: no registers held)
           if (a.hit[b0i] < 0 && best0 >= a.target[b0i]) a.hit[b0i] = a.k_base + k;

@@ -22,7 +22,7 @@ FORM_F2 = 0  # DCOPF_FORM_FLOW_BOX
 FORM_F1 = 1  # DCOPF_FORM_LIMIT_ROWS
 FORM_KVL = 2  # DCOPF_FORM_CYCLE (cluster path only)
 PATH_AUTO, PATH_BATCHED, PATH_SINGLE, PATH_CLUSTER = 0, 1, 2, 3
-INST_OK, INST_DIVERGED = 0, 1
+INST_OK, INST_DIVERGED, INST_CONVERGED = 0, 1, 2
 OPT_PLAIN, OPT_GDM, OPT_GDM_CLASSIC, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2, 3, 4
 ERRORS = {-1: "EINVAL", -2: "ETOPOLOGY", -3: "ECUDA", -4: "ENOMEM", -5: "ESTATE"}
 
@@ -67,7 +67,7 @@ class Optimizer(ctypes.Structure):
 
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",
            "dcopf_dual_get_bound", "dcopf_dual_get_multipliers", "dcopf_dual_set_multipliers",
-           "dcopf_dual_evaluate", "dcopf_dual_set_optimizer", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info",
+           "dcopf_dual_evaluate", "dcopf_dual_set_optimizer", "dcopf_dual_set_stop", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info",
            "dcopf_dual_last_error", "dcopf_dual_destroy"]
 
 _lib = None
@@ -92,6 +92,8 @@ def load_library(path: Optional[str] = None):
     lib.dcopf_dual_evaluate.argtypes = [P, P, P, P, P]
     if hasattr(lib, "dcopf_dual_set_optimizer"):
         lib.dcopf_dual_set_optimizer.argtypes = [P, ctypes.POINTER(Optimizer)]
+    if hasattr(lib, "dcopf_dual_set_stop"):
+        lib.dcopf_dual_set_stop.argtypes = [P, ctypes.c_double]
     if hasattr(lib, "dcopf_dual_set_target"):
         lib.dcopf_dual_set_target.argtypes = [P, P, P]
         lib.dcopf_dual_get_first_hit.argtypes = [P, P, P]
@@ -213,6 +215,10 @@ class DcopfDual:
         o = Optimizer()
         o.variant, o.momentum, o.beta1, o.beta2, o.epsilon = int(variant), momentum, beta1, beta2, epsilon
         self._check(self.lib.dcopf_dual_set_optimizer(self.h, ctypes.byref(o)))
+
+    def set_stop(self, tol=0.0):
+        """Algorithm 1's stopping rule |g_k - g_{k-1}| < tol per instance (0: off)."""
+        self._check(self.lib.dcopf_dual_set_stop(self.h, float(tol)))
 
     def set_target(self, target=None, stream=None):
         """Per-instance time-to-gap thresholds [B] (None clears them)."""

@@ -20,13 +20,15 @@ def cost_scale(net):
 
 
 def run_gpu(net, loads, outages=None, K=0, alpha=None, form=0, path=dual.PATH_AUTO, history=False,
-            lam0=None, br0=None, implied_theta=False, switchable=None, opt=None, split=None):
+            lam0=None, br0=None, implied_theta=False, switchable=None, opt=None, split=None, tol=0.0):
     """loads [B][n_bus] (instance-major, like the oracle); returns instance-major results."""
     import torch
     dev = torch.device("cuda:0")
     loads = np.atleast_2d(loads)
     B = loads.shape[0]
     h = dual.DcopfDual(net, form=form, path=path, implied_theta=implied_theta, switchable=switchable)
+    if tol:
+        h.set_stop(tol)
     if opt is not None:  # oracle-style dict(variant=, rho=, beta1=, beta2=, eps=)
         h.set_optimizer(opt.get("variant", 0), opt.get("rho", 0.0), opt.get("beta1", 0.0), opt.get("beta2", 0.0),
                         opt.get("eps", 0.0))

@@ -521,3 +521,26 @@ def test_kvl_rejects_tree_outage_and_other_paths():
         h.set_instance_batch(torch.from_numpy(net.base_load[:, None].copy()).cuda(),
                              torch.tensor([[int(tree[0])]], dtype=torch.int32).cuda())
     h.close()
+
+
+# ---------------------------------------------------------------------------
+# Algorithm 1's stopping rule per instance (reading A-29)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_stopping_rule_per_instance(path):
+    net = inst.tiny_network(23, 37, 30, seed=5)
+    rng = np.random.default_rng(4)
+    B = 9
+    loads = net.base_load[None, :] * rng.uniform(0.7, 1.3, (B, net.n_bus))
+    K = 2500
+    a = inst.alpha_schedule(K, 3e-3)
+    tol = 2e-3  # some instances stop, some do not
+    orc = oracle.solve(net, loads, K=K, alpha=a, history=True, tol=tol)
+    assert 0 < np.sum(orc.status == oracle.CONVERGED) < B
+    gpu = run_gpu(net, loads, K=K, alpha=a, path=path, history=True, tol=tol)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+    # split calls: the rule looks only within a call (its first evaluation
+    # re-evaluates the previous call's last point) -- same result here
+    gpu2 = run_gpu(net, loads, K=K, alpha=a, path=path, history=True, tol=tol, split=997)
+    np.testing.assert_array_equal(gpu2["status"], gpu["status"])

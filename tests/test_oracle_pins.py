@@ -712,3 +712,32 @@ def test_kvl_outage_equals_branch_removed():
     np.testing.assert_array_equal(r.lam, r2.lam)
     np.testing.assert_array_equal(np.delete(r.br[0], k), r2.br[0])
     assert r.best[0] == r2.best[0]
+
+
+# ---------------------------------------------------------------------------
+# Algorithm 1's stopping rule, reading A-29
+
+
+def test_stopping_rule_oracle():
+    """The instance stops at the first k >= 1 with |g_k - g_{k-1}| < tol (the
+    step of that iteration is still taken, A-29): its multipliers equal a run
+    of exactly k+1 steps, no earlier consecutive pair is within tol, and
+    tol = 0 changes nothing."""
+    net = inst.make_network(0, theta_mode="min")
+    K = 20000
+    a = inst.alpha_schedule(K, 0.1)
+    tol = 1e-4
+    r = oracle.solve(net, net.base_load, K=K, alpha=a, opt=ADAM, tol=tol, history=True)
+    full = oracle.solve(net, net.base_load, K=K, alpha=a, opt=ADAM, history=True)
+    assert r.status[0] == oracle.CONVERGED
+    d = np.abs(np.diff(full.hist[0]))
+    k = int(np.nonzero(d < tol)[0][0]) + 1
+    np.testing.assert_array_equal(r.hist[0, :k + 1], full.hist[0, :k + 1])
+    again = oracle.solve(net, net.base_load, K=k + 1, alpha=a, opt=ADAM)
+    np.testing.assert_array_equal(r.lam, again.lam)
+    np.testing.assert_array_equal(r.br, again.br)
+    assert np.all(r.hist[0, k + 1:] == r.hist[0, k + 1])      # frozen afterwards
+    z = oracle.solve(net, net.base_load, K=3000, alpha=a, opt=ADAM, tol=0.0)
+    z0 = oracle.solve(net, net.base_load, K=3000, alpha=a, opt=ADAM)
+    np.testing.assert_array_equal(z.lam, z0.lam)
+    assert z.status[0] == 0
