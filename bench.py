@@ -312,7 +312,7 @@ def main():
         sw = np.zeros(net.n_branch, np.uint8)
         sw[net.n_tree:] = 1
     ospec, alpha0 = opt_spec(args)
-    if args.opt != "plain" or form == dual.FORM_KVL:
+    if args.opt != "plain":
         path = dual.PATH_CLUSTER
     h = dual.DcopfDual(net, form=form, device=local, path=path, switchable=sw)
     if args.opt != "plain":

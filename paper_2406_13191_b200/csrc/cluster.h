@@ -56,15 +56,6 @@ struct alignas(16) ClBKe { unsigned kap; int sgn, dbr, pad; };  // kappa of a cy
 struct alignas(16) ClCy { int e0, e1, dbr, pad; };               // owned cycle
 struct alignas(16) ClCe { unsigned f; int pad; double sx; };    // f* of a cycle branch, sx = C_kl x_l
 
-// Fundamental cycle basis (reading A-28) in some branch numbering:
-// cycle k is defined by non-tree branch def[k]; its branches cb[cp[k]..cp[k+1])
-// (ascending ORIGINAL id) with signs cs.
-struct CycleBasis {
-  int nc = 0;
-  std::vector<int> def, cp, cb, cs;
-  std::vector<uint8_t> is_tree;
-};
-
 // The canonical basis of the network, in ORIGINAL branch ids: a breadth-first
 // tree from `ref` (FIFO bus order, each bus's incident branches in ascending
 // id) over branches with b > 0 that are never switched; non-tree branches in

@@ -323,7 +323,8 @@ int compile_schedule(dcopf_dual_t h, int W) {
     sc = Schedule();
     sc.ring_life = cd.second;
     sc.pool_gap = h->soft_sync ? 2 : 1;  // soft sync: consumer warps drift by up to one step
-    std::string err = build_schedule(h->ni, cd.first, P, W, kSweepWarps, &sc);
+    std::string err = build_schedule(h->ni, cd.first, P, W, kSweepWarps, &sc,
+                                     h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr);
     if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
     if (sc.total <= h->dev_smem) {
       ok = true;
@@ -349,7 +350,7 @@ int compile_schedule(dcopf_dual_t h, int W) {
   }
   // storage order of the batched state (per kind) in terms of original ids
   if (!rc) {
-    const int nb = h->n_bus, nl = h->n_br;
+    const int nb = h->n_bus, nl = h->n_bm_ent;  // branch-block rows: branches, or cycles (KVL)
     std::vector<int> lam_perm(nb), lam_inv(nb), d_perm(nb), br_perm(nl), br_inv(nl);
     for (int p = 0; p < nb; ++p) {
       lam_perm[p] = h->bus_perm[h->sch.perm_lam[p]];
@@ -357,7 +358,8 @@ int compile_schedule(dcopf_dual_t h, int W) {
       d_perm[p] = h->bus_perm[h->sch.perm_d[p]];
     }
     for (int p = 0; p < nl; ++p) {
-      br_perm[p] = h->br_perm[h->sch.perm_br[p]];
+      // KVL: the storage order lists canonical cycle indices directly
+      br_perm[p] = (h->form == DCOPF_FORM_CYCLE) ? h->sch.perm_br[p] : h->br_perm[h->sch.perm_br[p]];
       br_inv[br_perm[p]] = p;
     }
     if (!rc) rc = upload(h, &h->d_lam_perm_b, lam_perm);
@@ -365,7 +367,13 @@ int compile_schedule(dcopf_dual_t h, int W) {
     if (!rc) rc = upload(h, &h->d_d_perm_b, d_perm);
     if (!rc) rc = upload(h, &h->d_br_perm_b, br_perm);
     if (!rc) rc = upload(h, &h->d_br_inv_b, br_inv);
-    if (!rc) rc = upload(h, &h->d_br_pos_b, h->sch.pos_br);
+    if (h->form == DCOPF_FORM_CYCLE) {  // internal branch -> storage row of the cycle it defines (-1: tree)
+      std::vector<int> pos(h->n_br, -1);
+      for (int k = 0; k < h->cyc_int.nc; ++k) pos[h->cyc_int.def[k]] = h->sch.pos_br[k];
+      if (!rc) rc = upload(h, &h->d_br_pos_b, pos);
+    } else if (!rc) {
+      rc = upload(h, &h->d_br_pos_b, h->sch.pos_br);
+    }
   }
   if (rc) return rc;
   std::vector<uint8_t>().swap(h->sch.prog);  // device copy only
@@ -378,6 +386,8 @@ int compile_schedule(dcopf_dual_t h, int W) {
   if (!rc) rc = set_smem(h, k_sweep<kFormF2, true, kSweepWarps, true>, b);
   if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps, true>, b);
   if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps, true>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormKVL, false, kSweepWarps, true>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormKVL, true, kSweepWarps, true>, b);
   if (!rc) h->sched_W = W;
   return rc;
 }
@@ -569,6 +579,7 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.k_base = h->k_base;
   a.n_bus = h->n_bus;
   a.n_br = h->n_br;
+  a.n_brows = h->n_bm_ent;
   a.ref = h->ref_int;
   a.W = h->T;
   const Schedule &sc = h->sch;
@@ -607,6 +618,8 @@ int launch_sweep(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
   if (h->form == DCOPF_FORM_FLOW_BOX) {
     if (h->soft_sync) k_sweep<kFormF2, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);
     else k_sweep<kFormF2, EVAL, kSweepWarps, false><<<grid, threads, sm, s>>>(a);
+  } else if (h->form == DCOPF_FORM_CYCLE) {
+    k_sweep<kFormKVL, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);  // (soft sync only)
   } else {
     if (h->soft_sync) k_sweep<kFormF1, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);
     else k_sweep<kFormF1, EVAL, kSweepWarps, false><<<grid, threads, sm, s>>>(a);
@@ -861,12 +874,10 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   int path = h->path_opt;
-  if (h->form == DCOPF_FORM_CYCLE && path != DCOPF_PATH_AUTO && path != DCOPF_PATH_CLUSTER)
-    return fail(h, DCOPF_EINVAL, "the KVL (cycle) form runs on the cluster path only");
+  if (h->form == DCOPF_FORM_CYCLE && path == DCOPF_PATH_SINGLE)
+    return fail(h, DCOPF_EINVAL, "the KVL (cycle) form runs on the cluster and batched paths");
   if (path == DCOPF_PATH_AUTO) {
-    path = (B <= h->single_max || h->opt.variant != DCOPF_OPT_PLAIN || h->form == DCOPF_FORM_CYCLE)
-               ? DCOPF_PATH_CLUSTER
-               : DCOPF_PATH_BATCHED;
+    path = (B <= h->single_max || h->opt.variant != DCOPF_OPT_PLAIN) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
     if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) {
       if (h->form == DCOPF_FORM_CYCLE) return DCOPF_EINVAL;  // (message set by configure_cluster)
       path = DCOPF_PATH_SINGLE;
@@ -1063,6 +1074,10 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
         k_check_outaged<<<grid_for((size_t)h->B * h->max_out), 256, 0, s>>>(
             tb, h->outs, h->path == DCOPF_PATH_BATCHED ? h->d_br_pos_b : nullptr, h->max_out, h->B, h->n_br, h->T,
             h->flag);
+      // KVL, batched: kappa of a cycle whose defining branch is out stays 0 (phase B does not mask it)
+      if (h->form == DCOPF_FORM_CYCLE && h->path == DCOPF_PATH_BATCHED && h->max_out > 0)
+        k_check_outaged<<<grid_for((size_t)h->B * h->max_out), 256, 0, s>>>(
+            tb, h->outs, h->d_br_pos_b, h->max_out, h->B, h->n_bm_ent, h->T, h->flag);
     }
     cudaMemcpyAsync(&bad, h->flag, sizeof(int), cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);

@@ -219,11 +219,132 @@ int colour(std::vector<Interval> iv, std::vector<int> &slot) {
   return n;
 }
 
+// Storage order and slots of one kind of state row (see build_schedule):
+// rows with live range <= life go to a ring (one bulk copy per step), the
+// others to interval-coloured sticky slots after it.  Returns the ring count.
+int place_rows(int n, const std::vector<Interval> &iv, const std::vector<int> &first, int LIFE, std::vector<int> &pos,
+               std::vector<int> &perm, std::vector<int> &slot, int *ring, int *nslots) {
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return first[x] < first[y]; });
+    std::vector<int> rr, sticky;
+    for (int id : idx) (iv[id].hi - first[id] <= LIFE ? rr : sticky).push_back(id);
+    pos.assign(n, 0);
+    perm.assign(n, 0);
+    int p = 0;
+    for (int id : rr) { pos[id] = p; perm[p++] = id; }
+    for (int id : sticky) { pos[id] = p; perm[p++] = id; }
+    int R = 1;
+    for (size_t k = 0, j = 0; k < rr.size(); ++k) {  // j: oldest ring row still live at issue time of k
+      const int t = iv[rr[k]].lo;                   // issue time (first - P, clamped)
+      while (j < k && iv[rr[j]].hi < t) ++j;
+      R = std::max(R, (int)(k - j + 1));
+    }
+    for (size_t k = 0; k < rr.size(); ++k) slot[rr[k]] = (int)(k % R);
+    std::vector<Interval> siv;
+    for (int id : sticky) siv.push_back({iv[id].lo, iv[id].hi, id});
+    std::vector<int> sslot(n, 0);
+    const int ns = colour(siv, sslot);
+    for (int id : sticky) slot[id] = R + sslot[id];
+    *ring = R;
+    *nslots = R + ns;
+    return (int)rr.size();
+}
+
+// Per-step load lists over the three row kinds (ring runs + sticky rows).
+struct KindInfo {
+  int kind, n, nring, R, bytes;
+  const std::vector<int> *first, *pos, *perm, *slot;
+};
+void build_loads(Schedule &S, int nst, const KindInfo (&kinds)[3], std::vector<int> &row_bytes) {
+  S.ld_ptr.assign(nst + 1, 0);
+  S.ld.clear();
+  row_bytes.assign(nst, 0);
+  S.n_copies = 0;
+  S.n_sticky_copies = 0;
+  std::vector<std::vector<int4_t>> per(nst);
+  for (const KindInfo &K : kinds) {
+    for (int p0 = 0; p0 < K.nring;) {  // ring rows: positions [0, nring) sorted by first use
+      const int st = (*K.first)[(*K.perm)[p0]];
+      int p1 = p0;
+      while (p1 < K.nring && (*K.first)[(*K.perm)[p1]] == st) ++p1;
+      for (int q = p0; q < p1;) {  // split at the ring wrap
+        const int sl = q % K.R;
+        const int cnt = std::min(p1 - q, K.R - sl);
+        per[st].push_back({K.kind, q, cnt, sl});
+        q += cnt;
+      }
+      p0 = p1;
+    }
+    for (int p = K.nring; p < K.n; ++p) {  // sticky rows
+      const int id = (*K.perm)[p];
+      per[(*K.first)[id]].push_back({K.kind, p, 1, (*K.slot)[id]});
+      ++S.n_sticky_copies;
+    }
+  }
+  for (int st = 0; st < nst; ++st) {
+    for (const int4_t &x : per[st]) {
+      S.ld.push_back(x);
+      row_bytes[st] += x.c * kinds[x.a].bytes;
+    }
+    S.n_copies += (int)per[st].size();
+    S.ld_ptr[st + 1] = (int)S.ld.size();
+  }
+}
+
+// Shared-memory layout of the sweep kernel for a built schedule.
+void layout_smem(Schedule &S, int nl, int nw) {
+  const int RB = S.row_bytes, BR = S.br_row_bytes;
+  auto al = [](int x) { return (x + 127) & ~127; };
+  int off = 0;
+  S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers
+  off = al(off + 16 * S.S + 64);
+  S.off_frz = off;  // frozen flags [64] int, then running best [64] and previous g [64] double
+  off = al(off + 4 * 64 + 2 * 8 * 64);
+  S.off_obm = off;  // per-tile outage bitmap over branches
+  off = al(off + 4 * ((nl + 31) / 32 + 1));
+  S.off_outs = off;  // per-instance outage lists of the tile
+  off = al(off + 4 * 64 * 8);
+  S.off_prog = off;
+  off = al(off + S.S * al(S.max_prog_bytes));
+  // state / minimiser pools; lanes past the tile width read up to 512 - RB
+  // bytes past a pool's last slot
+  int pad = 512 - RB;
+  if (const char *e = getenv("DCOPF_POOL_PAD")) pad = atoi(e);  // measurement only
+  S.off_brp = off;
+  off = al(off + S.n_br_slots * BR + pad);
+  S.off_lamp = off;
+  off = al(off + S.n_lam_slots * RB + pad);
+  S.off_dp = off;
+  off = al(off + S.n_d_slots * RB + pad);
+  S.off_th = off;  // theta*_i code rows
+  off = al(off + S.n_th_slots * S.code_row_bytes);
+  S.off_fc = off;  // f*_l code rows (F2)
+  off = al(off + S.n_f_slots * S.code_row_bytes);
+  // the per-warp dual-value partials [nw][64] are needed only at the end of a
+  // sweep, when every pool is dead: they alias the pools
+  S.off_red = S.off_brp;
+  off = std::max(off, al(S.off_brp + 8 * 64 * nw));
+  if (getenv("DCOPF_RED_SEPARATE")) {  // measurement only
+    S.off_red = off;
+    off = al(off + 8 * 64 * nw);
+  }
+  S.total = off;
+}
+
+std::string build_schedule_kvl(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out,
+                               const CycleBasis &Y);
+
 }  // namespace
 
 size_t Schedule::smem_bytes(int) const { return (size_t)total; }
 
-std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out) {
+std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out,
+                           const CycleBasis *cyc) {
+  if (net.form == 2) {
+    if (!cyc) return "KVL form needs its cycle basis";
+    return build_schedule_kvl(net, CH, P, W, nw, out, *cyc);
+  }
   Schedule &S = *out;
   const int nb = net.nb, nl = net.nl;
   const bool f1 = net.form == 1;
@@ -320,31 +441,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   const int LIFE = S.ring_life;
   auto place = [&](int n, const std::vector<Interval> &iv, const std::vector<int> &first, std::vector<int> &pos,
                    std::vector<int> &perm, std::vector<int> &slot, int *ring, int *nslots) {
-    std::vector<int> idx(n);
-    for (int i = 0; i < n; ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return first[x] < first[y]; });
-    std::vector<int> rr, sticky;
-    for (int id : idx) (iv[id].hi - first[id] <= LIFE ? rr : sticky).push_back(id);
-    pos.assign(n, 0);
-    perm.assign(n, 0);
-    int p = 0;
-    for (int id : rr) { pos[id] = p; perm[p++] = id; }
-    for (int id : sticky) { pos[id] = p; perm[p++] = id; }
-    int R = 1;
-    for (size_t k = 0, j = 0; k < rr.size(); ++k) {  // j: oldest ring row still live at issue time of k
-      const int t = iv[rr[k]].lo;                   // issue time (first - P, clamped)
-      while (j < k && iv[rr[j]].hi < t) ++j;
-      R = std::max(R, (int)(k - j + 1));
-    }
-    for (size_t k = 0; k < rr.size(); ++k) slot[rr[k]] = (int)(k % R);
-    std::vector<Interval> siv;
-    for (int id : sticky) siv.push_back({iv[id].lo, iv[id].hi, id});
-    std::vector<int> sslot(n, 0);
-    const int ns = colour(siv, sslot);
-    for (int id : sticky) slot[id] = R + sslot[id];
-    *ring = R;
-    *nslots = R + ns;
-    return (int)rr.size();
+    return place_rows(n, iv, first, LIFE, pos, perm, slot, ring, nslots);
   };
   int ring_lam = 0, ring_d = 0, ring_br = 0;
   const int nr_lam = place(nb, iv_lam, lam_first, S.pos_lam, S.perm_lam, lam_slot, &ring_lam, &S.n_lam_slots);
@@ -355,47 +452,11 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   S.ring_br = ring_br;
 
   // ---- load lists: per step, ranges of rows (kind, first position, count, first slot) ----
-  S.ld_ptr.assign(nst + 1, 0);
-  S.ld.clear();
-  std::vector<int> row_bytes(nst, 0);
-  S.n_copies = 0;
-  S.n_sticky_copies = 0;
-  struct KindInfo {
-    int kind, n, nring, R, bytes;
-    const std::vector<int> *first, *pos, *perm, *slot;
-  };
+  std::vector<int> row_bytes;
   const KindInfo kinds[3] = {{LD_LAM, nb, nr_lam, ring_lam, RB, &lam_first, &S.pos_lam, &S.perm_lam, &lam_slot},
                              {LD_D, nb, nr_d, ring_d, RB, &d_first, &S.pos_d, &S.perm_d, &d_slot},
                              {LD_BR, nl, nr_br, ring_br, BR, &br_first, &S.pos_br, &S.perm_br, &br_slot}};
-  std::vector<std::vector<int4_t>> per(nst);
-  for (const KindInfo &K : kinds) {
-    // ring rows: positions [0, nring) sorted by first use -> one run per step
-    for (int p0 = 0; p0 < K.nring;) {
-      const int st = (*K.first)[(*K.perm)[p0]];
-      int p1 = p0;
-      while (p1 < K.nring && (*K.first)[(*K.perm)[p1]] == st) ++p1;
-      for (int q = p0; q < p1;) {  // split at the ring wrap
-        const int sl = q % K.R;
-        const int cnt = std::min(p1 - q, K.R - sl);
-        per[st].push_back({K.kind, q, cnt, sl});
-        q += cnt;
-      }
-      p0 = p1;
-    }
-    for (int p = K.nring; p < K.n; ++p) {  // sticky rows
-      const int id = (*K.perm)[p];
-      per[(*K.first)[id]].push_back({K.kind, p, 1, (*K.slot)[id]});
-      ++S.n_sticky_copies;
-    }
-  }
-  for (int st = 0; st < nst; ++st) {
-    for (const int4_t &x : per[st]) {
-      S.ld.push_back(x);
-      row_bytes[st] += x.c * (x.a == LD_BR ? BR : RB);
-    }
-    S.n_copies += (int)per[st].size();
-    S.ld_ptr[st + 1] = (int)S.ld.size();
-  }
+  build_loads(S, nst, kinds, row_bytes);
 
   // ---- program blocks, one per step ----
   S.prog.clear();
@@ -589,43 +650,235 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     S.tx_bytes[st] = S.prog_bytes[st] + row_bytes[st];
   }
 
-  // ---- shared-memory layout ----
-  auto al = [](int x) { return (x + 127) & ~127; };
-  int off = 0;
-  S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers
-  off = al(off + 16 * S.S + 64);
-  S.off_frz = off;  // frozen flags [64] int, then running best [64] and previous g [64] double
-  off = al(off + 4 * 64 + 2 * 8 * 64);
-  S.off_obm = off;  // per-tile outage bitmap over branches
-  off = al(off + 4 * ((nl + 31) / 32 + 1));
-  S.off_outs = off;  // per-instance outage lists of the tile
-  off = al(off + 4 * 64 * 8);
-  S.off_prog = off;
-  off = al(off + S.S * al(S.max_prog_bytes));
-  // state / minimiser pools; lanes past the tile width read up to 512 - RB
-  // bytes past a pool's last slot
-  int pad = 512 - RB;
-  if (const char *e = getenv("DCOPF_POOL_PAD")) pad = atoi(e);  // measurement only
-  S.off_brp = off;
-  off = al(off + S.n_br_slots * BR + pad);
-  S.off_lamp = off;
-  off = al(off + S.n_lam_slots * RB + pad);
-  S.off_dp = off;
-  off = al(off + S.n_d_slots * RB + pad);
-  S.off_th = off;  // theta*_i code rows
-  off = al(off + S.n_th_slots * S.code_row_bytes);
-  S.off_fc = off;  // f*_l code rows (F2)
-  off = al(off + S.n_f_slots * S.code_row_bytes);
-  // the per-warp dual-value partials [nw][64] are needed only at the end of a
-  // sweep, when every pool is dead: they alias the pools
-  S.off_red = S.off_brp;
-  off = std::max(off, al(S.off_brp + 8 * 64 * nw));
-  if (getenv("DCOPF_RED_SEPARATE")) {  // measurement only
-    S.off_red = off;
-    off = al(off + 8 * 64 * nw);
-  }
-  S.total = off;
+  layout_smem(S, nl, nw);
   return "";
 }
+
+namespace {
+
+// ============================================================================
+// KVL (cycle-basis) form on the batched path.  Steps s = 0..nch:
+//   B(s)     branches whose larger endpoint is in chunk s: q_l from the kappa
+//            of the cycles through l and lambda_s, lambda_t -> f* code, q f
+//   C(s-1)   buses whose last neighbour is in chunk s-1 (as F2): lambda'
+//   D(s-1)   cycles whose last branch is in chunk s-1: sum C x f* -> kappa'
+// Rows: lambda (B of incident branches .. C), d (C), kappa (first B of a
+// cycle branch .. D); f* codes: B .. last C / D reader.
+std::string build_schedule_kvl(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out,
+                               const CycleBasis &Y) {
+  Schedule &S = *out;
+  const int nb = net.nb, nl = net.nl, nc = Y.nc;
+  if (W < 2 || W > 64 || (W & 1)) return "tile width must be even in [2, 64]";
+  S.CH = CH;
+  S.P = P;
+  S.S = P + 1;
+  S.W = W;
+  S.nch = (nb + CH - 1) / CH;
+  S.nsteps = S.nch + 1;
+  S.row_bytes = 8 * W;
+  S.br_row_bytes = 8 * W;  // kappa rows
+  const int nch = S.nch, nst = S.nsteps, RB = S.row_bytes, CRB = S.code_row_bytes;
+  auto chunk = [&](int bus) { return bus / CH; };
+  std::vector<int> hi(nl);
+  for (int l = 0; l < nl; ++l) {
+    hi[l] = std::max(net.bs[l], net.bt[l]);
+    if (l > 0 && hi[l] < hi[l - 1]) return "internal branch order not sorted by larger endpoint";
+  }
+  auto stB = [&](int l) { return chunk(hi[l]); };
+  std::vector<int> rp(nb);
+  for (int i = 0; i < nb; ++i) rp[i] = i;
+  for (int l = 0; l < nl; ++l) {
+    rp[net.bs[l]] = std::max(rp[net.bs[l]], net.bt[l]);
+    rp[net.bt[l]] = std::max(rp[net.bt[l]], net.bs[l]);
+  }
+  auto stC = [&](int i) { return chunk(rp[i]) + 1; };
+  std::vector<int> stD(nc), firstK(nc);
+  std::vector<std::vector<std::pair<int, int>>> bcyc(nl);  // cycles through a branch, ascending k
+  for (int k = 0; k < nc; ++k) {
+    int mx = 0, mn = nst;
+    for (int e = Y.cp[k]; e < Y.cp[k + 1]; ++e) {
+      const int l = Y.cb[e];
+      mx = std::max(mx, stB(l));
+      mn = std::min(mn, stB(l));
+      bcyc[l].push_back({k, Y.cs[e]});
+    }
+    stD[k] = mx + 1;
+    firstK[k] = mn;
+  }
+  // ---- live ranges ----
+  std::vector<Interval> iv_lam(nb), iv_d(nb), iv_k(nc), iv_f(nl);
+  std::vector<int> lam_first(nb), d_first(nb);
+  for (int i = 0; i < nb; ++i) {
+    const int last = stC(i);
+    int first = last;
+    for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) first = std::min(first, stB(net.bus_inc[e] >> 1));
+    lam_first[i] = first;
+    iv_lam[i] = {std::max(0, first - P), last, i};
+    d_first[i] = last;
+    iv_d[i] = {std::max(0, last - P), last, i};
+  }
+  for (int k = 0; k < nc; ++k) iv_k[k] = {std::max(0, firstK[k] - P), stD[k], k};
+  for (int l = 0; l < nl; ++l) {
+    int last = std::max(stC(net.bs[l]), stC(net.bt[l]));
+    for (auto &kc : bcyc[l]) last = std::max(last, stD[kc.first]);
+    iv_f[l] = {stB(l), last + S.pool_gap - 1, l};
+  }
+  std::vector<int> lam_slot(nb), d_slot(nb), k_slot(nc), f_slot(nl);
+  S.n_th_slots = 0;
+  S.n_f_slots = colour(iv_f, f_slot);
+  const int LIFE = S.ring_life;
+  int ring_lam = 0, ring_d = 0, ring_k = 0;
+  const int nr_lam = place_rows(nb, iv_lam, lam_first, LIFE, S.pos_lam, S.perm_lam, lam_slot, &ring_lam, &S.n_lam_slots);
+  const int nr_d = place_rows(nb, iv_d, d_first, LIFE, S.pos_d, S.perm_d, d_slot, &ring_d, &S.n_d_slots);
+  const int nr_k = place_rows(nc, iv_k, firstK, LIFE, S.pos_br, S.perm_br, k_slot, &ring_k, &S.n_br_slots);
+  S.ring_lam = ring_lam;
+  S.ring_d = ring_d;
+  S.ring_br = ring_k;
+  std::vector<int> row_bytes;
+  const KindInfo kinds[3] = {{LD_LAM, nb, nr_lam, ring_lam, RB, &lam_first, &S.pos_lam, &S.perm_lam, &lam_slot},
+                             {LD_D, nb, nr_d, ring_d, RB, &d_first, &S.pos_d, &S.perm_d, &d_slot},
+                             {LD_BR, nc, nr_k, ring_k, RB, &firstK, &S.pos_br, &S.perm_br, &k_slot}};
+  build_loads(S, nst, kinds, row_bytes);
+  // items per step
+  std::vector<std::vector<int>> Cst(nst), Dst(nst);
+  for (int i = 0; i < nb; ++i) Cst[stC(i)].push_back(i);
+  for (int k = 0; k < nc; ++k) Dst[stD[k]].push_back(k);
+  // ---- program blocks ----
+  S.prog.clear();
+  S.prog_off.assign(nst, 0);
+  S.prog_bytes.assign(nst, 0);
+  S.tx_bytes.assign(nst, 0);
+  S.max_prog_bytes = 0;
+  const bool has_sw = !net.sw.empty();
+  for (int st = 0; st < nst; ++st) {
+    std::vector<RecBK> Bv;
+    std::vector<RecBKe> BKe;
+    if (st < nch) {
+      for (int l = 0; l < nl; ++l) {
+        if (stB(l) != st) continue;
+        RecBK r{};
+        r.ls = lam_slot[net.bs[l]] * RB;
+        r.lt = lam_slot[net.bt[l]] * RB;
+        r.fs = f_slot[l] * CRB;
+        r.obr = (!has_sw || net.sw[l]) ? l : -1;
+        r.x = (net.b[l] > 0.0) ? 1.0 / net.b[l] : 0.0;
+        r.F = (net.b[l] > 0.0) ? net.F[l] : 0.0;  // b = 0: an open circuit
+        r.e0 = (int)BKe.size();
+        for (auto &kc : bcyc[l])  // (a cycle whose defining branch has b = 0 is inactive: no term)
+          if (net.b[Y.def[kc.first]] > 0.0) BKe.push_back(RecBKe{k_slot[kc.first] * RB, kc.second});
+        r.e1 = (int)BKe.size();
+        Bv.push_back(r);
+      }
+    }
+    std::vector<RecC> Cv;
+    std::vector<RecG> G;
+    std::vector<RecIC2> IC;
+    for (int i : Cst[st]) {
+      RecC r{};
+      r.wpos = S.pos_lam[i];
+      r.ls = lam_slot[i] * RB;
+      r.ds = d_slot[i] * RB;
+      r.g0 = (int)G.size();
+      for (int g = net.gen_ptr[i]; g < net.gen_ptr[i + 1]; ++g) G.push_back(RecG{net.gc[g], net.glo[g], net.ghi[g], net.ga[g]});
+      r.g1 = (int)G.size();
+      r.e0 = (int)IC.size();
+      for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
+        const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
+        const double F = (net.b[l] > 0.0) ? net.F[l] : 0.0;
+        IC.push_back(RecIC2{f_slot[l] * CRB, l, to ? F : -F});
+      }
+      r.e1 = (int)IC.size();
+      Cv.push_back(r);
+    }
+    std::vector<RecD> Dv;
+    std::vector<RecDe> De;
+    for (int k : Dst[st]) {
+      RecD r{};
+      r.ks = k_slot[k] * RB;
+      r.wpos = S.pos_br[k];
+      const int dl = Y.def[k];
+      r.dbr = (!has_sw || net.sw[dl]) ? dl : -1;
+      r.e0 = (int)De.size();
+      if (net.b[dl] > 0.0)  // a b = 0 defining branch: no cycle (gradient 0)
+        for (int e = Y.cp[k]; e < Y.cp[k + 1]; ++e) {
+          const int m = Y.cb[e];
+          const double x = 1.0 / net.b[m], sx = (Y.cs[e] > 0) ? x : -x, F = net.F[m];
+          RecDe d{};
+          d.fs = f_slot[m] * CRB;
+          d.t[0] = (-F) * sx;  // (c F) sx for c = -1, 0, +1 (exact: the oracle's f x with the sign of C)
+          d.t[1] = (0.0 * F) * sx;
+          d.t[2] = F * sx;
+          De.push_back(d);
+        }
+      r.e1 = (int)De.size();
+      Dv.push_back(r);
+    }
+    // balance B, C, D over the warps (as build_schedule)
+    std::vector<long> load(nw, 0);
+    std::vector<uint16_t> wtab(3 * (nw + 1), 0);
+    auto balance = [&](auto &items, auto cost, int phase) {
+      const int n = (int)items.size();
+      std::vector<int> idx(n), own(n);
+      for (int x = 0; x < n; ++x) idx[x] = x;
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost(items[a]) > cost(items[b]); });
+      for (int x : idx) {
+        const long cx = cost(items[x]);
+        int w = 0;
+        for (int v = 1; v < nw; ++v)
+          if (load[v] < load[w]) w = v;
+        own[x] = w;
+        load[w] += cx;
+      }
+      std::vector<int> ord(n);
+      for (int x = 0; x < n; ++x) ord[x] = x;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return own[a] < own[b]; });
+      typename std::remove_reference<decltype(items)>::type re(n);
+      for (int x = 0; x < n; ++x) re[x] = items[ord[x]];
+      items.swap(re);
+      uint16_t *t = wtab.data() + phase * (nw + 1);
+      for (int x = 0, w = 0; w <= nw; ++w) {
+        while (x < n && own[ord[x]] < w) ++x;
+        t[w] = (uint16_t)x;
+      }
+    };
+    balance(Bv, [&](const RecBK &r) { return 50L + 10L * (r.e1 - r.e0); }, 0);
+    balance(Cv, [&](const RecC &r) { return 35L + 12L * (r.e1 - r.e0) + 25L * (r.g1 - r.g0); }, 1);
+    balance(Dv, [&](const RecD &r) { return 30L + 10L * (r.e1 - r.e0); }, 2);
+    std::vector<uint8_t> blk(kProgHeaderBytes, 0);
+    int32_t hd[PH_COUNT] = {0};
+    auto app = [&](const void *p, size_t n) {
+      size_t off = (blk.size() + 15) & ~size_t(15);
+      blk.resize(off + n);
+      if (n) memcpy(blk.data() + off, p, n);
+      return (int32_t)off;
+    };
+    hd[PH_NA] = (int)Dv.size();
+    hd[PH_NIA] = (int)De.size();
+    hd[PH_NB] = (int)Bv.size();
+    hd[PH_NC] = (int)Cv.size();
+    hd[PH_NIC] = (int)IC.size();
+    hd[PH_NG] = (int)G.size();
+    hd[PH_OFF_A] = app(Dv.data(), Dv.size() * sizeof(RecD));
+    hd[PH_OFF_IA] = app(De.data(), De.size() * sizeof(RecDe));
+    hd[PH_OFF_B] = app(Bv.data(), Bv.size() * sizeof(RecBK));
+    hd[PH_OFF_C] = app(Cv.data(), Cv.size() * sizeof(RecC));
+    hd[PH_OFF_G] = app(G.data(), G.size() * sizeof(RecG));
+    hd[PH_OFF_IC] = app(IC.data(), IC.size() * sizeof(RecIC2));
+    hd[PH_PAD] = app(BKe.data(), BKe.size() * sizeof(RecBKe));  // KVL: cycle terms of phase B
+    hd[PH_OFF_W] = app(wtab.data(), wtab.size() * sizeof(uint16_t));
+    blk.resize((blk.size() + 15) & ~size_t(15), 0);
+    hd[PH_BYTES] = (int32_t)blk.size();
+    memcpy(blk.data(), hd, sizeof hd);
+    S.prog_off[st] = (long long)S.prog.size();
+    S.prog_bytes[st] = (int)blk.size();
+    S.prog.insert(S.prog.end(), blk.begin(), blk.end());
+    S.max_prog_bytes = std::max(S.max_prog_bytes, (int)blk.size());
+    S.tx_bytes[st] = S.prog_bytes[st] + row_bytes[st];
+  }
+  layout_smem(S, nl, nw);
+  return "";
+}
+
+}  // namespace
 
 }  // namespace dcopf

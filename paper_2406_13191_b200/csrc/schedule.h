@@ -53,6 +53,23 @@ struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, ths, tht, pad2; };  
 // load-list entry kinds (top 2 bits of the packed entity word)
 enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
 
+// KVL form (batched path): phase B per branch with its cycle terms, phase D per cycle
+struct alignas(16) RecBK { int ls, lt, e0, e1, fs, obr, pad0, pad1; double x, F; };  // x = 1/b (0 if b = 0)
+struct alignas(8) RecBKe { int ks, sgn; };                                        // kappa slot of a cycle term
+struct alignas(16) RecD { int ks, wpos, e0, e1, dbr, pad0, pad1, pad2; };          // cycle: kappa slot, kappa' row,
+                                                                                  // dbr: defining branch if switchable
+struct alignas(16) RecDe { int fs, pad; double t[3]; };                           // f* code slot; t[c+1] = (c F) sx,
+                                                                                  // sx = C_kl x_l (exact table)
+
+// Fundamental cycle basis (reading A-28) in some branch numbering:
+// cycle k is defined by non-tree branch def[k]; its branches cb[cp[k]..cp[k+1])
+// (ascending ORIGINAL id) with signs cs.
+struct CycleBasis {
+  int nc = 0;
+  std::vector<int> def, cp, cb, cs;
+  std::vector<uint8_t> is_tree;
+};
+
 struct NetInternal {
   int nb, nl, ref, form;                   // internal numbering
   std::vector<int> bus_ptr, bus_inc;        // CSR, entries (l << 1) | is_to, ascending original id
@@ -116,6 +133,8 @@ std::vector<int> dfs_tree_order(int n, const std::vector<std::vector<int>> &adj,
 // Build the schedule for tiles of W instances (2 per lane); the sweep runs in
 // nch + 2 skewed steps: step s executes A(s), B(s-1) and C(s-2) between two
 // barriers.  Returns an empty string or an error message.
-std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out);
+// cyc: the cycle basis in INTERNAL branch ids (KVL form, net.form == 2), else null.
+std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out,
+                           const CycleBasis *cyc = nullptr);
 
 }  // namespace dcopf

@@ -61,6 +61,7 @@ struct SweepArgs {
   double *out_val;                  // EVAL: value [B_pad]
   double *g_lam, *g_br;             // EVAL: gradients (tile-major)
   int n_bus, n_br, ref, W;
+  int n_brows;                      // branch-block rows per tile: n_br (F2 / F1), n_cycles (KVL)
   const uint8_t *prog;
   const long long *prog_off;
   const int *prog_bytes, *tx_bytes;
@@ -229,7 +230,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       if (k > 0) named_bar(2, (NW + 1) * 32);  // sweep k-1 written and fenced
       const int par = (a.cur + (int)(k & 1)) & 1;
       const uint8_t *lam_src = reinterpret_cast<const uint8_t *>(par ? a.lam1 : a.lam0) + tile * (size_t)a.n_bus * RB;
-      const uint8_t *br_src = reinterpret_cast<const uint8_t *>(par ? a.br1 : a.br0) + tile * (size_t)a.n_br * BR;
+      const uint8_t *br_src = reinterpret_cast<const uint8_t *>(par ? a.br1 : a.br0) + tile * (size_t)a.n_brows * BR;
       const uint8_t *d_src = reinterpret_cast<const uint8_t *>(a.d) + tile * (size_t)a.n_bus * RB;
       for (int c = 0; c < nst; ++c) {
         const int st = pst;
@@ -299,7 +300,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
     const int par = (a.cur + (int)(k & 1)) & 1;
     uint8_t *lam_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_lam : (par ? a.lam0 : a.lam1)) + tile * (size_t)a.n_bus * RB +
                      lofs;
-    uint8_t *br_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_br : (par ? a.br0 : a.br1)) + tile * (size_t)a.n_br * BR +
+    uint8_t *br_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_br : (par ? a.br0 : a.br1)) + tile * (size_t)a.n_brows * BR +
                     lofs;
     const bool step0 = !EVAL && !last && !frz[2 * lane], step1 = !EVAL && !last && !frz[2 * lane + 1];
     const double alpha = (EVAL || last) ? 0.0 : a.alpha[k];
@@ -325,6 +326,136 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       const unsigned short *wt = reinterpret_cast<const unsigned short *>(prog + h4.z);  // [3][NW+1] item ranges
       const int nA = h0.x, nB = h0.z, nC = h0.w;
 
+      // ---------------- C: ready buses (F2 / F1: C(s-2), warp table 2; KVL: C(s-1), table 1) ----
+      auto phaseC = [&](int tbl) {
+        const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
+        const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
+        for (int j = wt[tbl * (NW + 1) + warp], je = wt[tbl * (NW + 1) + warp + 1]; j < je; ++j) {
+          const RecC r = Cv[j];
+          const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
+          double gl0 = -di.x, gl1 = -di.y;
+#pragma unroll 1
+          for (int gg = r.g0; gg < r.g1; ++gg) {  // mostly 0 or 1 generator
+            const RecG gr = G[gg];
+            const double r0 = gr.c + li.x, r1 = gr.c + li.y;
+            const double p0 = gen_minimiser(r0, gr.lo, gr.hi, gr.a), p1 = gen_minimiser(r1, gr.lo, gr.hi, gr.a);
+            gl0 = gl0 + p0;
+            gl1 = gl1 + p1;
+            if (gr.a > 0.0) {
+              v0 += gr.a * p0 * p0 + r0 * p0;
+              v1 += gr.a * p1 * p1 + r1 * p1;
+            } else {
+              v0 += r0 * p0;
+              v1 += r1 * p1;
+            }
+          }
+          if (FORM != kFormF1) {
+            const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y) + r.e0;
+            const int n = r.e1 - r.e0;
+            auto acc = [&](const RecIC2 &x) {
+              const D2 f = ld_code2(fcp, x.f, x.sF);  // +-f* (c * (+-F) == +-(c * F) exactly)
+              gl0 = gl0 + f.x;  // +f* at the to bus, -f* at the from bus
+              gl1 = gl1 + f.y;
+            };
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (e < n) acc(IC[e]);
+#pragma unroll 1
+            for (int e = 4; e < n; ++e) acc(IC[e]);
+          } else {
+            const RecIC1 *IC = reinterpret_cast<const RecIC1 *>(prog + h3.y);
+#pragma unroll 1
+            for (int e = r.e0; e < r.e1; ++e) {
+              const RecIC1 x = IC[e];
+              double sb0 = x.sb, sb1 = x.sb;
+              if (x.br >= 0 && flagged(x.br)) {
+                if (out_t(my_outs0, x.br)) sb0 = copysign(0.0, sb0);
+                if (out_t(my_outs1, x.br)) sb1 = copysign(0.0, sb1);
+              }
+              const D2 ts = ld_code2(thp, x.ts, x.ths), tt = ld_code2(thp, x.tt, x.tht);
+              gl0 = gl0 + sb0 * (ts.x - tt.x);
+              gl1 = gl1 + sb1 * (ts.y - tt.y);
+            }
+          }
+          v0 += -(li.x * di.x);
+          v1 += -(li.y * di.y);
+          if (write && act) {
+            double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.wpos * RB);
+            if (EVAL) st2(dst, gl0, gl1);
+            else st2(dst, (!CHK || step0) ? li.x + alpha * gl0 : li.x, (!CHK || step1) ? li.y + alpha * gl1 : li.y);
+          }
+        }
+      };
+      if constexpr (FORM == kFormKVL) {
+      if (a.debug_mode != 1) {
+      // f* codes of B(<= s-1) exist and every warp has finished step s-2
+      // (f* code slots are reused 2 steps after their last read)
+      if (SOFT && gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+      // ---------------- B(s): q_l = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t), f* ----------------
+      {
+        const RecBK *Bv = reinterpret_cast<const RecBK *>(prog + h2.z);
+        const RecBKe *BKe = reinterpret_cast<const RecBKe *>(prog + h3.w);
+        for (int j = wt[warp], je = wt[warp + 1]; j < je; ++j) {
+          const RecBK r = Bv[j];
+          double x0 = r.x, x1 = r.x, F0 = r.F, F1v = r.F;
+          bool o0 = false, o1 = false;
+          if (r.obr >= 0 && flagged(r.obr)) {  // an outaged lane: b = F = 0
+            o0 = out_t(my_outs0, r.obr);
+            o1 = out_t(my_outs1, r.obr);
+            if (o0) x0 = F0 = 0.0;
+            if (o1) x1 = F1v = 0.0;
+          }
+          double s0 = 0.0, s1 = 0.0;  // cycles in ascending k (the oracle's order)
+#pragma unroll 1
+          for (int e = r.e0; e < r.e1; ++e) {
+            const RecBKe t = BKe[e];
+            const D2 kv = ld2(brp, t.ks);
+            s0 = (t.sgn > 0) ? s0 + kv.x : s0 - kv.x;
+            s1 = (t.sgn > 0) ? s1 + kv.y : s1 - kv.y;
+          }
+          const D2 ls = ld2(lamp, r.ls), lt = ld2(lamp, r.lt);
+          const double q0 = x0 * s0 - (ls.x - lt.x), q1 = x1 * s1 - (ls.y - lt.y);
+          const double f0 = (q0 > 0.0) ? -F0 : ((q0 < 0.0) ? F0 : 0.0);
+          const double f1 = (q1 > 0.0) ? -F1v : ((q1 < 0.0) ? F1v : 0.0);
+          if (act) st_code2(fcp + r.fs, o0 ? 0 : code_of(q0 < 0.0, q0 > 0.0), o1 ? 0 : code_of(q1 < 0.0, q1 > 0.0));
+          v0 += q0 * f0;
+          v1 += q1 * f1;
+        }
+      }
+      if (SOFT) warp_arrive(&bdone[gs & 3], lane);
+      phaseC(1);
+      // ---------------- D(s-1): d/dkappa_k = sum_l C_kl x_l f*_l, kappa' ----------------
+      {
+        const RecD *Dv = reinterpret_cast<const RecD *>(prog + h2.x);
+        const RecDe *De = reinterpret_cast<const RecDe *>(prog + h2.y);
+        for (int j = wt[2 * (NW + 1) + warp], je = wt[2 * (NW + 1) + warp + 1]; j < je; ++j) {
+          const RecD r = Dv[j];
+          const D2 kv = ld2(brp, r.ks);
+          double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 1
+          for (int e = r.e0; e < r.e1; ++e) {
+            const RecDe d = De[e];
+            const unsigned c = *reinterpret_cast<const unsigned short *>(fcp + d.fs);
+            // index 0 / 1 / 2 for code -1 / 0 / +1 (lanes past the tile width read
+            // padding bytes: clamp so they never index outside the record)
+            const int c0 = (int)(signed char)(c & 0xffu), c1 = (int)(signed char)(c >> 8);
+            const int i0 = (c0 > 0) ? 2 : ((c0 < 0) ? 0 : 1), i1 = (c1 > 0) ? 2 : ((c1 < 0) ? 0 : 1);
+            acc0 = acc0 + d.t[i0];  // (c F) sx: the oracle's C_kl (f*_l x_l), exact
+            acc1 = acc1 + d.t[i1];
+          }
+          if (r.dbr >= 0 && flagged(r.dbr)) {  // defining branch out: no cycle, gradient 0
+            if (out_t(my_outs0, r.dbr)) acc0 = 0.0;
+            if (out_t(my_outs1, r.dbr)) acc1 = 0.0;
+          }
+          if (write && act) {
+            double *dst = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR);
+            if (EVAL) st2(dst, acc0, acc1);
+            else st2(dst, (!CHK || step0) ? kv.x + alpha * acc0 : kv.x, (!CHK || step1) ? kv.y + alpha * acc1 : kv.y);
+          }
+        }
+      }
+      }  // debug_mode
+      } else {
       if (a.debug_mode != 1) {  // (1: data movement only -- measurement)
       if (SOFT && gs > 0) mbar_wait_backoff(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       // ---------------- A(s): w_i, theta* codes ----------------
@@ -445,67 +576,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         warp_arrive(&bdone[gs & 3], lane);
         if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       }
-      // ---------------- C(s-2): ready buses ----------------
-      {
-        const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
-        const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
-        for (int j = wt[2 * (NW + 1) + warp], je = wt[2 * (NW + 1) + warp + 1]; j < je; ++j) {
-          const RecC r = Cv[j];
-          const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
-          double gl0 = -di.x, gl1 = -di.y;
-#pragma unroll 1
-          for (int gg = r.g0; gg < r.g1; ++gg) {  // mostly 0 or 1 generator
-            const RecG gr = G[gg];
-            const double r0 = gr.c + li.x, r1 = gr.c + li.y;
-            const double p0 = gen_minimiser(r0, gr.lo, gr.hi, gr.a), p1 = gen_minimiser(r1, gr.lo, gr.hi, gr.a);
-            gl0 = gl0 + p0;
-            gl1 = gl1 + p1;
-            if (gr.a > 0.0) {
-              v0 += gr.a * p0 * p0 + r0 * p0;
-              v1 += gr.a * p1 * p1 + r1 * p1;
-            } else {
-              v0 += r0 * p0;
-              v1 += r1 * p1;
-            }
-          }
-          if (FORM == kFormF2) {
-            const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y) + r.e0;
-            const int n = r.e1 - r.e0;
-            auto acc = [&](const RecIC2 &x) {
-              const D2 f = ld_code2(fcp, x.f, x.sF);  // +-f* (c * (+-F) == +-(c * F) exactly)
-              gl0 = gl0 + f.x;  // +f* at the to bus, -f* at the from bus
-              gl1 = gl1 + f.y;
-            };
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (e < n) acc(IC[e]);
-#pragma unroll 1
-            for (int e = 4; e < n; ++e) acc(IC[e]);
-          } else {
-            const RecIC1 *IC = reinterpret_cast<const RecIC1 *>(prog + h3.y);
-#pragma unroll 1
-            for (int e = r.e0; e < r.e1; ++e) {
-              const RecIC1 x = IC[e];
-              double sb0 = x.sb, sb1 = x.sb;
-              if (x.br >= 0 && flagged(x.br)) {
-                if (out_t(my_outs0, x.br)) sb0 = copysign(0.0, sb0);
-                if (out_t(my_outs1, x.br)) sb1 = copysign(0.0, sb1);
-              }
-              const D2 ts = ld_code2(thp, x.ts, x.ths), tt = ld_code2(thp, x.tt, x.tht);
-              gl0 = gl0 + sb0 * (ts.x - tt.x);
-              gl1 = gl1 + sb1 * (ts.y - tt.y);
-            }
-          }
-          v0 += -(li.x * di.x);
-          v1 += -(li.y * di.y);
-          if (write && act) {
-            double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.wpos * RB);
-            if (EVAL) st2(dst, gl0, gl1);
-            else st2(dst, (!CHK || step0) ? li.x + alpha * gl0 : li.x, (!CHK || step1) ? li.y + alpha * gl1 : li.y);
-          }
-        }
-      }
+      phaseC(2);
       }  // debug_mode
+      }  // FORM
       if (SOFT) {
         warp_arrive(&empty[st], lane);
       } else {  // lock-step mode: every warp finished the step

@@ -12,10 +12,108 @@
 #include <string>
 #include <vector>
 
+#include "../paper_2406_13191_b200/csrc/cluster.h"
 #include "../paper_2406_13191_b200/csrc/schedule.h"
 
 using namespace dcopf;
 
+
+// KVL replay: B(s) reads lambda / kappa rows and writes f* codes; C(s-1) and
+// D(s-1) read them; worst-case landing (writes of a step land first).
+static int check_kvl(const NetInternal &n, const Schedule &S, const CycleBasis &Y, int P) {
+  std::vector<int> brp(S.n_br_slots, -1), lamp(S.n_lam_slots, -1), dp(S.n_d_slots, -1), fc(S.n_f_slots, -1);
+  std::vector<int> seenB(n.nl, 0), seenC(n.nb, 0), seenD(Y.nc, 0);
+  const int RB = S.row_bytes, CRB = S.code_row_bytes;
+  int bad = 0;
+  auto issue = [&](int c) {
+    if (c >= S.nsteps) return;
+    for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
+      const int4_t x = S.ld[e];
+      std::vector<int> &pool = x.a == LD_LAM ? lamp : x.a == LD_D ? dp : brp;
+      const std::vector<int> &perm = x.a == LD_LAM ? S.perm_lam : x.a == LD_D ? S.perm_d : S.perm_br;
+      for (int r = 0; r < x.c; ++r) {
+        if (x.d + r >= (int)pool.size()) { printf("BAD slot range\n"); ++bad; continue; }
+        pool[x.d + r] = perm[x.b + r];
+      }
+    }
+  };
+  auto want = [&](std::vector<int> &pool, int slot, int ent, const char *what, int c) {
+    if (slot < 0 || slot >= (int)pool.size() || pool[slot] != ent) {
+      if (bad < 10) printf("BAD %s step %d slot %d want %d have %d\n", what, c, slot, ent,
+                           (slot >= 0 && slot < (int)pool.size()) ? pool[slot] : -9);
+      ++bad;
+    }
+  };
+  for (int c = 0; c <= P; ++c) issue(c);
+  for (int c = 0; c < S.nsteps; ++c) {
+    const uint8_t *pg = S.prog.data() + S.prog_off[c];
+    const int *h = reinterpret_cast<const int *>(pg);
+    const RecBK *Bv = reinterpret_cast<const RecBK *>(pg + h[PH_OFF_B]);
+    const RecBKe *BK = reinterpret_cast<const RecBKe *>(pg + h[PH_PAD]);
+    const RecC *Cv = reinterpret_cast<const RecC *>(pg + h[PH_OFF_C]);
+    const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
+    const RecD *Dv = reinterpret_cast<const RecD *>(pg + h[PH_OFF_A]);
+    const RecDe *De = reinterpret_cast<const RecDe *>(pg + h[PH_OFF_IA]);
+    // which branch is which record: match by lambda rows + f slot (B records carry no id)
+    std::vector<int> bl(h[PH_NB], -1);
+    for (int j = 0; j < h[PH_NB]; ++j) {
+      for (int l = 0; l < n.nl; ++l)
+        if (std::max(n.bs[l], n.bt[l]) / S.CH == c && !seenB[l] && lamp[Bv[j].ls / RB] == n.bs[l] &&
+            lamp[Bv[j].lt / RB] == n.bt[l] && (Bv[j].obr < 0 || Bv[j].obr == l)) {
+          bl[j] = l;
+          break;
+        }
+      if (bl[j] < 0) { printf("BAD B record %d at step %d\n", j, c); ++bad; continue; }
+      fc[Bv[j].fs / CRB] = bl[j];  // the step's code writes land first
+    }
+    for (int j = 0; j < h[PH_NB]; ++j) {
+      const int l = bl[j];
+      if (l < 0) continue;
+      seenB[l]++;
+      int cnt = 0;
+      for (int k = 0; k < Y.nc; ++k)
+        for (int e = Y.cp[k]; e < Y.cp[k + 1]; ++e)
+          if (Y.cb[e] == l && n.b[Y.def[k]] > 0.0) {
+            if (Bv[j].e0 + cnt >= Bv[j].e1) { printf("BAD B terms\n"); ++bad; break; }
+            want(brp, BK[Bv[j].e0 + cnt].ks / RB, k, "B kappa", c);
+            if (BK[Bv[j].e0 + cnt].sgn != Y.cs[e]) { printf("BAD B sign\n"); ++bad; }
+            ++cnt;
+          }
+      if (cnt != Bv[j].e1 - Bv[j].e0) { printf("BAD B term count\n"); ++bad; }
+    }
+    for (int j = 0; j < h[PH_NC]; ++j) {
+      const int bus = S.perm_lam[Cv[j].wpos];
+      seenC[bus]++;
+      want(lamp, Cv[j].ls / RB, bus, "C lam", c);
+      want(dp, Cv[j].ds / RB, bus, "C d", c);
+      if (Cv[j].e1 - Cv[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD C degree\n"); ++bad; }
+      for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
+        const int l = n.bus_inc[n.bus_ptr[bus] + e - Cv[j].e0] >> 1;
+        if (IC[e].br != l) { printf("BAD C order\n"); ++bad; }
+        want(fc, IC[e].f / CRB, l, "C f", c);
+      }
+    }
+    for (int j = 0; j < h[PH_NA]; ++j) {
+      const int k = S.perm_br[Dv[j].wpos];
+      seenD[k]++;
+      want(brp, Dv[j].ks / RB, k, "D kappa", c);
+      if (Dv[j].e1 - Dv[j].e0 != Y.cp[k + 1] - Y.cp[k]) { printf("BAD D length\n"); ++bad; continue; }
+      for (int e = Dv[j].e0; e < Dv[j].e1; ++e) {
+        const int q = Y.cp[k] + e - Dv[j].e0, l = Y.cb[q];
+        want(fc, De[e].fs / CRB, l, "D f", c);
+        const double sx = (Y.cs[q] > 0 ? 1.0 : -1.0) / n.b[l];
+        if (De[e].t[2] != n.F[l] * sx || De[e].t[0] != -n.F[l] * sx) { printf("BAD D coefficient\n"); ++bad; }
+      }
+    }
+    issue(c + P + 1);
+  }
+  for (int l = 0; l < n.nl; ++l) if (seenB[l] != 1) { printf("BAD cover br %d\n", l); ++bad; break; }
+  for (int i = 0; i < n.nb; ++i) if (seenC[i] != 1) { printf("BAD cover bus %d\n", i); ++bad; break; }
+  for (int k = 0; k < Y.nc; ++k) if (seenD[k] != 1) { printf("BAD cover cycle %d\n", k); ++bad; break; }
+  printf("chunks %d slots br %d lam %d d %d th %d f %d smem %d copies %d sticky %d bad %d\n", S.nch, S.n_br_slots,
+         S.n_lam_slots, S.n_d_slots, S.n_th_slots, S.n_f_slots, S.total, S.n_copies, S.n_sticky_copies, bad);
+  return bad ? 1 : 0;
+}
 
 int main(int argc, char **argv) {
   int nb, nl, ref, form, CH, P;
@@ -34,10 +132,20 @@ int main(int argc, char **argv) {
   const int W = argc > 2 ? atoi(argv[2]) : 32;
   if (argc > 3) S.ring_life = atoi(argv[3]);
   if (argc > 4) S.pool_gap = atoi(argv[4]);
-  std::string err = build_schedule(n, CH, P, W, 8, &S);
+  CycleBasis Y, Yi;
+  if (form == 2) {  // KVL: the canonical basis (every non-tree branch switchable for this check)
+    std::vector<uint8_t> none(nl, 0);
+    std::string e1 = build_cycle_basis(nb, nl, ref, fr.data(), to.data(), b.data(), none.data(), &Y);
+    if (!e1.empty()) { printf("ERR %s\n", e1.c_str()); return 1; }
+    Yi = Y;
+    for (int &l : Yi.def) l = in.br_inv[l];
+    for (int &l : Yi.cb) l = in.br_inv[l];
+  }
+  std::string err = build_schedule(n, CH, P, W, 8, &S, form == 2 ? &Yi : nullptr);
 
   if (!err.empty()) { printf("ERR %s\n", err.c_str()); return 1; }
   const bool f1 = n.form == 1;
+  if (form == 2) return check_kvl(n, S, Yi, P);
   std::vector<int> brp(S.n_br_slots, -1), lamp(S.n_lam_slots, -1), dp(S.n_d_slots, -1), th(S.n_th_slots, -1),
       fc(S.n_f_slots, -1);
   std::vector<int> seenA(n.nb, 0), seenB(n.nl, 0), seenC(n.nb, 0);

@@ -508,12 +508,12 @@ def test_kvl_config3_adam_and_evaluate():
     h.close()
 
 
-def test_kvl_rejects_tree_outage_and_other_paths():
+def test_kvl_rejects_tree_outage_and_single_path():
     import torch
     net = inst.make_network(0)
     with pytest.raises(dual.DcopfError):
-        h = dual.DcopfDual(net, form=dual.FORM_KVL, path=dual.PATH_BATCHED)
-        h.set_instance_batch(torch.from_numpy(np.tile(net.base_load[:, None], (1, 300))).cuda())
+        h = dual.DcopfDual(net, form=dual.FORM_KVL, path=dual.PATH_SINGLE)
+        h.set_instance_batch(torch.from_numpy(net.base_load[:, None].copy()).cuda())
     h = dual.DcopfDual(net, form=dual.FORM_KVL)   # no switchable mask: the tree may use any branch
     d, _ = oracle.cycles(net)
     tree = np.setdiff1d(np.arange(net.n_branch), d)
@@ -544,3 +544,78 @@ def test_stopping_rule_per_instance(path):
     # re-evaluates the previous call's last point) -- same result here
     gpu2 = run_gpu(net, loads, K=K, alpha=a, path=path, history=True, tol=tol, split=997)
     np.testing.assert_array_equal(gpu2["status"], gpu["status"])
+
+
+# KVL form on the batched path (sweep kernel)
+
+
+def test_kvl_batched_tiny_ragged():
+    net = inst.tiny_network(23, 37, 30, seed=5)
+    sw = non_tree_switchable(net)
+    rng = np.random.default_rng(9)
+    B = 37  # two tiles, ragged tail
+    loads = net.base_load[None, :] * rng.uniform(0.7, 1.3, (B, net.n_bus))
+    outs = np.full((B, 3), -1, np.int32)
+    for j in range(B):
+        if j % 4:
+            outs[j, :j % 4] = rng.choice(np.arange(net.n_tree, net.n_branch), j % 4, replace=False)
+    K = 700
+    a = inst.alpha_schedule(K, 4e-3) * np.linspace(1.0, 0.2, K)
+    orc = oracle.solve(net, loads, outages=outs, K=K, alpha=a, form=oracle.FORM_KVL, history=True, switchable=sw)
+    gpu = run_gpu(net, loads, outages=outs, K=K, alpha=a, form=dual.FORM_KVL, path=dual.PATH_BATCHED,
+                  history=True, switchable=sw)
+    assert gpu["info"].path == dual.PATH_BATCHED
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+def test_kvl_batched_config4_sampled():
+    net = inst.make_network(4)
+    sw = non_tree_switchable(net)
+    B = inst.CONFIG4_BATCH
+    K = 400
+    batch = inst.config4_batch(net, range(B))
+    a = inst.alpha_schedule(K, 1e-2)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=dual.FORM_KVL,
+                  path=dual.PATH_BATCHED, switchable=sw)
+    idx = np.array([0, 55, 4097, 8191])
+    orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=oracle.FORM_KVL,
+                       switchable=sw, threads=4)
+    assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)
+
+
+def test_kvl_batched_evaluate_at_random_points():
+    import torch
+    net = inst.tiny_network(40, 70, 9, seed=3)
+    sw = non_tree_switchable(net)
+    rng = np.random.default_rng(2)
+    B = 150
+    nc = net.n_branch - net.n_bus + 1
+    loads = net.base_load[None, :] * rng.uniform(0.8, 1.2, (B, net.n_bus))
+    outs = np.full((B, 1), -1, np.int32)
+    outs[::3, 0] = rng.choice(np.arange(net.n_tree, net.n_branch), len(outs[::3]))
+    lam = rng.normal(-30, 10, (B, net.n_bus))
+    kap = rng.normal(0, 20, (B, nc))
+    d, _ = oracle.cycles(net, sw)
+    for j in range(B):  # kappa of an inactive cycle must be 0 (set_multipliers checks it)
+        if outs[j, 0] >= 0:
+            kap[j, np.nonzero(d == outs[j, 0])[0]] = 0.0
+    dev = torch.device("cuda:0")
+    h = dual.DcopfDual(net, form=dual.FORM_KVL, path=dual.PATH_BATCHED, switchable=sw)
+    h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(loads.T)).to(dev), torch.from_numpy(outs).to(dev))
+    h.set_multipliers(torch.from_numpy(np.ascontiguousarray(lam.T)).to(dev),
+                      torch.from_numpy(np.ascontiguousarray(kap.T)).to(dev))
+    val = torch.empty(B, dtype=torch.float64, device=dev)
+    gl = torch.empty((net.n_bus, B), dtype=torch.float64, device=dev)
+    gk = torch.empty((nc, B), dtype=torch.float64, device=dev)
+    h.evaluate(val, gl, gk)
+    ov, ogl, ogk, _, _ = oracle.evaluate_kvl(net, loads, lam, kap, outages=outs, switchable=sw)
+    S = cost_scale(net)
+    assert np.all(np.abs(val.cpu().numpy() - ov) <= BOUND_RTOL * np.maximum(np.abs(ov), S))
+    np.testing.assert_array_equal(gl.cpu().numpy().T, ogl)
+    np.testing.assert_array_equal(gk.cpu().numpy().T, ogk)
+    bad = kap.copy()
+    j = int(np.nonzero(outs[:, 0] >= 0)[0][0])
+    bad[j, np.nonzero(d == outs[j, 0])[0]] = 1.0
+    with pytest.raises(dual.DcopfError):
+        h.set_multipliers(None, torch.from_numpy(np.ascontiguousarray(bad.T)).to(dev))
+    h.close()

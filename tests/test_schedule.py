@@ -19,7 +19,8 @@ EXE = "/tmp/dcopf_sched_check"
 @pytest.fixture(scope="module")
 def checker():
     src = [os.path.join(ROOT, "tests", "sched_check.cpp"),
-           os.path.join(ROOT, "paper_2406_13191_b200", "csrc", "schedule.cpp")]
+           os.path.join(ROOT, "paper_2406_13191_b200", "csrc", "schedule.cpp"),
+           os.path.join(ROOT, "paper_2406_13191_b200", "csrc", "cluster.cpp")]
     subprocess.check_call(["g++", "-O2", "-std=c++17", "-o", EXE] + src)
     return EXE
 
@@ -32,7 +33,7 @@ def run(checker, net, form, CH, P, order="dfs", W=32, life=4):
 
 
 @pytest.mark.parametrize("config", [0, 1, 3])
-@pytest.mark.parametrize("form", [0, 1])
+@pytest.mark.parametrize("form", [0, 1, 2])
 @pytest.mark.parametrize("CH,P,W,life", [(32, 2, 56, 4), (8, 1, 2, 0), (64, 3, 64, 6), (16, 2, 56, 2)])
 def test_schedule_slots_valid(checker, config, form, CH, P, W, life):
     net = inst.make_network(config)
@@ -48,7 +49,7 @@ def test_schedule_random_small(checker, seed):
     net = inst.tiny_network(nb, max(nl, nb - 1), 3, seed=seed) if nb > 1 else None
     if net is None:
         return
-    for form in (0, 1):
+    for form in (0, 1, 2):
         for CH, P, life in ((1, 1, 0), (3, 2, 2), (16, 1, 6)):
             rc, out = run(checker, net, form, CH, P, life=life)
             assert rc == 0, out
