@@ -569,14 +569,16 @@ def test_kvl_batched_tiny_ragged():
 
 
 def test_kvl_batched_config4_sampled():
+    """config 4 at its full K (5000) in the bench's launch configuration."""
     net = inst.make_network(4)
     sw = non_tree_switchable(net)
     B = inst.CONFIG4_BATCH
-    K = 400
+    K = inst.ITERS[4]
     batch = inst.config4_batch(net, range(B))
-    a = inst.alpha_schedule(K, 1e-2)
+    a = inst.alpha_schedule(K)
     gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=dual.FORM_KVL,
                   path=dual.PATH_BATCHED, switchable=sw)
+    assert gpu["info"].grid * gpu["info"].tile_width >= B and gpu["info"].grid <= 148
     idx = np.array([0, 55, 4097, 8191])
     orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=oracle.FORM_KVL,
                        switchable=sw, threads=4)
