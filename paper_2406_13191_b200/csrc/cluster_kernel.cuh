@@ -126,8 +126,13 @@ __device__ __forceinline__ double2 cl_ld2(unsigned addr) {
   return v;
 }
 
+#ifndef DCOPF_CLUSTER_THREADS
+#define DCOPF_CLUSTER_THREADS 1024
+#endif
+constexpr int kClusterThreads = DCOPF_CLUSTER_THREADS;
+
 template <int FORM, int MODE>
-__global__ void __launch_bounds__(1024, 1) k_cluster(const ClusterArgs a) {
+__global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int BRW = (FORM == kFormF2) ? 1 : 2;
   const unsigned rank = cl_rank(), C = cl_nrank();

@@ -474,7 +474,7 @@ int configure_cluster(dcopf_dual_t h) {
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(C);
-    cfg.blockDim = dim3(1024);
+    cfg.blockDim = dim3(kClusterThreads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.attrs = at;
     cfg.numAttrs = 1;
@@ -547,7 +547,7 @@ int launch_cluster(dcopf_dual_t h, const ClusterArgs &a, cudaStream_t s) {
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3((unsigned)(h->B * C));
-  cfg.blockDim = dim3(1024);
+  cfg.blockDim = dim3(kClusterThreads);
   cfg.dynamicSmemBytes = h->cplan.smem;
   cfg.stream = s;
   cfg.attrs = at;
@@ -1221,7 +1221,7 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
     info->tile_width = h->T;
   } else if (h->path == DCOPF_PATH_CLUSTER) {
     info->smem_bytes = h->cplan.smem;
-    info->threads_per_block = 1024;
+    info->threads_per_block = kClusterThreads;
     info->grid = (int)(h->B * h->cplan_C);
     info->state_on_chip = 1;
     info->tile_width = 1;
