@@ -621,3 +621,22 @@ def test_kvl_batched_evaluate_at_random_points():
     with pytest.raises(dual.DcopfError):
         h.set_multipliers(None, torch.from_numpy(np.ascontiguousarray(bad.T)).to(dev))
     h.close()
+
+
+@pytest.mark.parametrize("form", [FORM_F2, oracle.FORM_KVL])
+def test_batched_more_tiles_than_sms(form):
+    """B = 10 000 on the 2000-bus network: 64-wide tiles, 157 tiles on 148
+    SMs (a second wave of persistent CTAs); sampled instances vs the oracle."""
+    net = inst.make_network(1)
+    sw = non_tree_switchable(net)
+    B = 10000
+    batch = inst.config4_batch(net, range(B), total=B)
+    K = 60
+    a = inst.alpha_schedule(K, 1e-2)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, path=dual.PATH_BATCHED,
+                  switchable=sw)
+    assert gpu["info"].tile_width == 64 and gpu["info"].grid > 148
+    idx = np.array([0, 63, 64, 9407, 9999])
+    orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=form, switchable=sw,
+                       threads=4)
+    assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)
