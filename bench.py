@@ -233,9 +233,13 @@ def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, 
     if popt is not None and mine.any():  # (ii): the true gap of the GPU's best bound after K, vs the optimum
         best = np.empty(batch.B)
         h.get_bound(best=best)
-        b = float(best[ids[mine][0] - lo])
-        out["primal_opt"] = popt
-        out["true_gap_at_K"] = (popt - b) / abs(popt)
+        po = np.atleast_1d(np.asarray(popt, dtype=np.float64))
+        po = po[mine] if po.size == len(ids) else po[:1]
+        b = best[ids[mine] - lo][:po.size]
+        gaps = (po - b) / np.abs(po)
+        out["primal_opt"] = float(po[0]) if po.size == 1 else "per sampled instance (HiGHS)"
+        out["true_gap_at_K"] = float(gaps[0]) if po.size == 1 else {"median": float(np.median(gaps)),
+                                                                    "max": float(np.max(gaps))}
     return out
 
 
@@ -312,8 +316,6 @@ def main():
         sw = np.zeros(net.n_branch, np.uint8)
         sw[net.n_tree:] = 1
     ospec, alpha0 = opt_spec(args)
-    if args.opt != "plain":
-        path = dual.PATH_CLUSTER
     h = dual.DcopfDual(net, form=form, device=local, path=path, switchable=sw)
     if args.opt != "plain":
         h.set_optimizer(ospec["variant"], ospec.get("rho", 0.0), ospec.get("beta1", 0.0), ospec.get("beta2", 0.0),

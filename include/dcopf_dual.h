@@ -190,7 +190,9 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
  *                t = steps since the state was reset (b^t by repeated products)
  * Optimiser state starts at 0 and persists across iterate() calls; it is reset
  * by set_instance_batch() and by this call.  Variants other than PLAIN run on
- * the cluster path only (AUTO selects it for them; iterate() on another path
+ * the cluster path (state in shared memory) and the batched path (state rows
+ * in HBM beside the multipliers, read and written at the update: 1 or 2 more
+ * rows per multiplier and iteration); not on DCOPF_PATH_SINGLE (iterate()
  * fails with ESTATE).  Errors: EINVAL (unknown variant, rho/b1/b2 outside
  * [0, 1), eps < 0, or the cluster partition plus the optimiser state does not
  * fit shared memory). */

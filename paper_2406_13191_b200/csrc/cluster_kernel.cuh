@@ -55,39 +55,9 @@ struct ClusterArgs {
   double tol;                   // stopping rule (0: off)
 };
 
-// One coordinate of the ascent step for the gradient-based-optimisation
-// variants (Algorithm 1; the oracle's opt_step, same operation
-// order, no contraction).
 __device__ __forceinline__ double opt_step(const ClusterArgs &a, double y, double g, double al, double *s1,
                                            double *s2, double b1t, double b2t) {
-  switch (a.opt) {
-    case DCOPF_OPT_GDM: {
-      const double v = a.rho * *s1 + al * g;
-      *s1 = v;
-      y = y + v;
-      return y + al * g;
-    }
-    case DCOPF_OPT_GDM_CLASSIC: {
-      const double v = a.rho * *s1 + al * g;
-      *s1 = v;
-      return y + v;
-    }
-    case DCOPF_OPT_ADAGRAD: {
-      const double G = *s1 + g * g;
-      *s1 = G;
-      return y + (al * g) / (sqrt(G) + a.eps);
-    }
-    case DCOPF_OPT_ADAM: {
-      const double m = a.beta1 * *s1 + (1.0 - a.beta1) * g;
-      const double v = a.beta2 * *s2 + (1.0 - a.beta2) * (g * g);
-      *s1 = m;
-      *s2 = v;
-      const double mh = m / (1.0 - b1t), vh = v / (1.0 - b2t);
-      return y + (al * mh) / (sqrt(vh) + a.eps);
-    }
-    default:
-      return y + al * g;
-  }
+  return opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y, g, al, *s1, *s2, b1t, b2t);
 }
 
 __device__ __forceinline__ unsigned cl_rank() {

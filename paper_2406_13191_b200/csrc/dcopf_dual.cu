@@ -388,6 +388,9 @@ int compile_schedule(dcopf_dual_t h, int W) {
   if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps, true>, b);
   if (!rc) rc = set_smem(h, k_sweep<kFormKVL, false, kSweepWarps, true>, b);
   if (!rc) rc = set_smem(h, k_sweep<kFormKVL, true, kSweepWarps, true>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormF2, false, kSweepWarps, true, true>, b);  // optimiser variants
+  if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps, true, true>, b);
+  if (!rc) rc = set_smem(h, k_sweep<kFormKVL, false, kSweepWarps, true, true>, b);
   if (!rc) h->sched_W = W;
   return rc;
 }
@@ -430,9 +433,10 @@ int opt_nstate(dcopf_dual_t h) {
 int reset_opt_state(dcopf_dual_t h, cudaStream_t s) {
   h->b1t = h->b2t = 1.0;
   const int ns = opt_nstate(h);
-  if (h->B == 0 || h->path != DCOPF_PATH_CLUSTER || ns == 0) return DCOPF_OK;
-  const size_t n[4] = {(size_t)h->B * h->n_bus, (size_t)h->B * h->n_bus, (size_t)h->B * h->n_bm_ent * h->bm_C,
-                       (size_t)h->B * h->n_bm_ent * h->bm_C};
+  if (h->B == 0 || h->path == DCOPF_PATH_SINGLE || ns == 0) return DCOPF_OK;
+  // same layout as the multipliers (cluster: instance-major; batched: tile-major rows)
+  const size_t n[4] = {(size_t)h->B_pad * h->n_bus, (size_t)h->B_pad * h->n_bus,
+                       (size_t)h->B_pad * h->n_bm_ent * h->bm_C, (size_t)h->B_pad * h->n_bm_ent * h->bm_C};
   for (int x = 0; x < 4; ++x) {
     if (x == 1 || x == 3) {
       if (ns < 2) continue;
@@ -607,6 +611,17 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.off_fc = sc.off_fc;
   a.soft = h->soft_sync;
   a.tol = h->tol;
+  a.opt = h->opt.variant;
+  a.rho = h->opt.momentum;
+  a.beta1 = h->opt.beta1;
+  a.beta2 = h->opt.beta2;
+  a.eps = h->opt.epsilon;
+  a.b1t = h->b1t;
+  a.b2t = h->b2t;
+  a.s1_lam = h->os[0];
+  a.s2_lam = h->os[1];
+  a.s1_br = h->os[2];
+  a.s2_br = h->os[3];
   if (const char *e = getenv("DCOPF_DEBUG_MODE")) a.debug_mode = atoi(e);  // measurement only
   return a;
 }
@@ -615,6 +630,13 @@ template <bool EVAL>
 int launch_sweep(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
   const unsigned grid = (unsigned)(h->B_pad / h->T), threads = (kSweepWarps + 1) * 32;
   const size_t sm = h->sch.total;
+  if (!EVAL && h->opt.variant != DCOPF_OPT_PLAIN) {  // optimiser variants (soft step sync)
+    if (h->form == DCOPF_FORM_FLOW_BOX) k_sweep<kFormF2, false, kSweepWarps, true, true><<<grid, threads, sm, s>>>(a);
+    else if (h->form == DCOPF_FORM_CYCLE) k_sweep<kFormKVL, false, kSweepWarps, true, true><<<grid, threads, sm, s>>>(a);
+    else k_sweep<kFormF1, false, kSweepWarps, true, true><<<grid, threads, sm, s>>>(a);
+    CK(h, cudaGetLastError());
+    return DCOPF_OK;
+  }
   if (h->form == DCOPF_FORM_FLOW_BOX) {
     if (h->soft_sync) k_sweep<kFormF2, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);
     else k_sweep<kFormF2, EVAL, kSweepWarps, false><<<grid, threads, sm, s>>>(a);
@@ -877,7 +899,7 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   if (h->form == DCOPF_FORM_CYCLE && path == DCOPF_PATH_SINGLE)
     return fail(h, DCOPF_EINVAL, "the KVL (cycle) form runs on the cluster and batched paths");
   if (path == DCOPF_PATH_AUTO) {
-    path = (B <= h->single_max || h->opt.variant != DCOPF_OPT_PLAIN) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
+    path = (B <= h->single_max) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
     if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) {
       if (h->form == DCOPF_FORM_CYCLE) return DCOPF_EINVAL;  // (message set by configure_cluster)
       path = DCOPF_PATH_SINGLE;
@@ -979,8 +1001,8 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     if (rc) return rc;
     hist = h->scratch;
   }
-  if (h->opt.variant != DCOPF_OPT_PLAIN && h->path != DCOPF_PATH_CLUSTER)
-    return fail(h, DCOPF_ESTATE, "optimiser variants run on the cluster path only");
+  if (h->opt.variant != DCOPF_OPT_PLAIN && h->path == DCOPF_PATH_SINGLE)
+    return fail(h, DCOPF_ESTATE, "optimiser variants run on the cluster and batched paths");
   int rc = stage_alpha(h, K, alpha, s);
   if (rc) return rc;
   if (h->path == DCOPF_PATH_BATCHED) {
@@ -992,6 +1014,11 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     if (rc) return rc;
     h->cur = (int)((h->cur + K) & 1);
     h->k_base += (long)K;
+    if (h->opt.variant == DCOPF_OPT_ADAM)
+      for (int64_t k = 0; k < K; ++k) {  // the kernel's repeated products, continued
+        h->b1t = h->b1t * h->opt.beta1;
+        h->b2t = h->b2t * h->opt.beta2;
+      }
   } else if (h->path == DCOPF_PATH_SINGLE) {
     SingleArgs a = single_args(h);
     a.alpha = h->alpha_dev;
@@ -1143,9 +1170,8 @@ int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt) {
   auto unit = [](double x) { return std::isfinite(x) && x >= 0.0 && x < 1.0; };
   if (!unit(o.momentum) || !unit(o.beta1) || !unit(o.beta2) || !(o.epsilon >= 0.0) || !std::isfinite(o.epsilon))
     return fail(h, DCOPF_EINVAL, "momentum, beta1, beta2 must be in [0, 1) and epsilon finite >= 0");
-  if (h->B > 0 && h->path != DCOPF_PATH_CLUSTER && o.variant != DCOPF_OPT_PLAIN)
-    return fail(h, DCOPF_EINVAL, "optimiser variants run on the cluster path: set the optimiser before "
-                                 "set_instance_batch (AUTO then selects it) or use DCOPF_PATH_CLUSTER");
+  if (h->B > 0 && h->path == DCOPF_PATH_SINGLE && o.variant != DCOPF_OPT_PLAIN)
+    return fail(h, DCOPF_EINVAL, "optimiser variants run on the cluster and batched paths");
   CK(h, cudaSetDevice(h->device));
   const int ns_old = opt_nstate(h);
   h->opt = o;

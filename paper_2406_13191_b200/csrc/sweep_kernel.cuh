@@ -72,6 +72,11 @@ struct SweepArgs {
       off_fc;
   int soft;                         // 1: consumer warps drift by <= 1 step (pool_gap 2); 0: lock-step
   double tol;                       // stopping rule (0: off)
+  // ascent-step variant (OPT kernels): DCOPF_OPT_* and its state, stored like
+  // the multipliers (tile-major rows in storage order), updated in place
+  int opt;
+  double rho, beta1, beta2, eps, b1t, b2t;  // b1t, b2t: beta^t before this launch's first step
+  double *s1_lam, *s2_lam, *s1_br, *s2_br;
   int debug_mode;                   // 0; 1 = data movement only; 2 = no row copies (measurement only)
 };
 
@@ -168,7 +173,7 @@ __device__ __forceinline__ D2 ld_code2(const uint8_t *base, int off, double x) {
   return D2{(double)c0 * x, (double)c1 * x};
 }
 
-template <int FORM, bool EVAL, int NW, bool SOFT>
+template <int FORM, bool EVAL, int NW, bool SOFT, bool OPT = false>
 #ifndef DCOPF_SWEEP_MAXREG
 #define DCOPF_SWEEP_MAXREG 96  // 20 warps x 32 x 96 + allocation granularity fit the 64K register file
 #endif
@@ -272,6 +277,13 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
   const uint8_t *brp = smem + a.off_brp + lofs;
   const uint8_t *lamp = smem + a.off_lamp + lofs;
   const uint8_t *dp = smem + a.off_dp + lofs;
+  // optimiser state rows of this tile (OPT kernels)
+  uint8_t *os1l = OPT ? reinterpret_cast<uint8_t *>(a.s1_lam) + tile * (size_t)a.n_bus * RB + lofs : nullptr;
+  uint8_t *os2l = OPT ? reinterpret_cast<uint8_t *>(a.s2_lam) + tile * (size_t)a.n_bus * RB + lofs : nullptr;
+  uint8_t *os1b = OPT ? reinterpret_cast<uint8_t *>(a.s1_br) + tile * (size_t)a.n_brows * BR + lofs : nullptr;
+  uint8_t *os2b = OPT ? reinterpret_cast<uint8_t *>(a.s2_br) + tile * (size_t)a.n_brows * BR + lofs : nullptr;
+  const bool ost2 = OPT && a.opt == 4;  // Adam: two state arrays
+  double ob1t = a.b1t, ob2t = a.b2t;
   uint8_t *thp = smem + a.off_th + 2 * lane;  // theta*_i code rows
   uint8_t *fcp = smem + a.off_fc + 2 * lane;  // f*_l code rows (F2)
   // Consumer warps are not stepped in lock-step: step g waits only for
@@ -304,6 +316,23 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
                     lofs;
     const bool step0 = !EVAL && !last && !frz[2 * lane], step1 = !EVAL && !last && !frz[2 * lane + 1];
     const double alpha = (EVAL || last) ? 0.0 : a.alpha[k];
+    if (OPT && !EVAL && !last) {  // Adam's beta^t, t = steps since the state was reset
+      ob1t = ob1t * a.beta1;
+      ob2t = ob2t * a.beta2;
+    }
+    // optimiser-variant update of one row of the lane's two instances (the
+    // state row sits at the same offset of the state arrays)
+    auto ostep = [&](double y0, double y1, double g0, double g1, size_t off, bool lam_side, bool do0,
+                     bool do1) -> D2 {
+      double2 *p1 = reinterpret_cast<double2 *>((lam_side ? os1l : os1b) + off);
+      double2 *p2 = reinterpret_cast<double2 *>((lam_side ? os2l : os2b) + off);
+      double2 S1 = *p1, S2 = ost2 ? *p2 : make_double2(0.0, 0.0);
+      if (do0) y0 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y0, g0, alpha, S1.x, S2.x, ob1t, ob2t);
+      if (do1) y1 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y1, g1, alpha, S1.y, S2.y, ob1t, ob2t);
+      *p1 = S1;
+      if (ost2) *p2 = S2;
+      return D2{y0, y1};
+    };
     double v0 = 0.0, v1 = 0.0;
 
     // the step loop, instantiated twice: CHK = some instance of the tile is
@@ -381,8 +410,14 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
           v1 += -(li.y * di.y);
           if (write && act) {
             double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.wpos * RB);
-            if (EVAL) st2(dst, gl0, gl1);
-            else st2(dst, (!CHK || step0) ? li.x + alpha * gl0 : li.x, (!CHK || step1) ? li.y + alpha * gl1 : li.y);
+            if (EVAL) {
+              st2(dst, gl0, gl1);
+            } else if constexpr (OPT) {
+              const D2 y = ostep(li.x, li.y, gl0, gl1, (size_t)r.wpos * RB, true, !CHK || step0, !CHK || step1);
+              st2(dst, y.x, y.y);
+            } else {
+              st2(dst, (!CHK || step0) ? li.x + alpha * gl0 : li.x, (!CHK || step1) ? li.y + alpha * gl1 : li.y);
+            }
           }
         }
       };
@@ -449,8 +484,14 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
           }
           if (write && act) {
             double *dst = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR);
-            if (EVAL) st2(dst, acc0, acc1);
-            else st2(dst, (!CHK || step0) ? kv.x + alpha * acc0 : kv.x, (!CHK || step1) ? kv.y + alpha * acc1 : kv.y);
+            if (EVAL) {
+              st2(dst, acc0, acc1);
+            } else if constexpr (OPT) {
+              const D2 y = ostep(kv.x, kv.y, acc0, acc1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
+              st2(dst, y.x, y.y);
+            } else {
+              st2(dst, (!CHK || step0) ? kv.x + alpha * acc0 : kv.x, (!CHK || step1) ? kv.y + alpha * acc1 : kv.y);
+            }
           }
         }
       }
@@ -538,8 +579,14 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
             v0 += q0 * f0;
             v1 += q1 * f1;
             if (write && act) {
-              if (EVAL) st2(dst, g0, g1);
-              else st2(dst, (!CHK || step0) ? nu.x + alpha * g0 : nu.x, (!CHK || step1) ? nu.y + alpha * g1 : nu.y);
+              if (EVAL) {
+                st2(dst, g0, g1);
+              } else if constexpr (OPT) {
+                const D2 y = ostep(nu.x, nu.y, g0, g1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
+                st2(dst, y.x, y.y);
+              } else {
+                st2(dst, (!CHK || step0) ? nu.x + alpha * g0 : nu.x, (!CHK || step1) ? nu.y + alpha * g1 : nu.y);
+              }
             }
           } else {
             const D2 mp = ld2(brp, r.row), mm = ld2(brp, r.row + RB);
@@ -553,6 +600,19 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
                 st2(dst2, gm0, gm1);
               } else {
                 double p0 = mp.x, m0 = mm.x, p1 = mp.y, m1 = mm.y;
+                if constexpr (OPT) {
+                  const bool d0 = !CHK || step0, d1 = !CHK || step1;
+                  const D2 yp = ostep(mp.x, mp.y, gp0, gp1, (size_t)r.wpos * BR, false, d0, d1);
+                  const D2 ym = ostep(mm.x, mm.y, gm0, gm1, (size_t)r.wpos * BR + RB, false, d0, d1);
+                  if (d0) {
+                    p0 = (yp.x > 0.0) ? yp.x : 0.0;  // mu <- max(mu, 0)
+                    m0 = (ym.x > 0.0) ? ym.x : 0.0;
+                  }
+                  if (d1) {
+                    p1 = (yp.y > 0.0) ? yp.y : 0.0;
+                    m1 = (ym.y > 0.0) ? ym.y : 0.0;
+                  }
+                } else {
                 if (!CHK || step0) {
                   p0 = mp.x + alpha * gp0;
                   m0 = mm.x + alpha * gm0;
@@ -564,6 +624,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
                   m1 = mm.y + alpha * gm1;
                   p1 = (p1 > 0.0) ? p1 : 0.0;
                   m1 = (m1 > 0.0) ? m1 : 0.0;
+                }
                 }
                 st2(dst, p0, p1);
                 st2(dst2, m0, m1);

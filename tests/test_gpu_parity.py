@@ -416,9 +416,11 @@ def test_optimizer_variants_batch_with_outages(name):
     a = inst.alpha_schedule(K, alpha) * np.linspace(1.0, 0.3, K)  # with a step decay
     for form in (FORM_F2, FORM_F1):
         orc = oracle.solve(net, loads, outages=outs, K=K, alpha=a, form=form, history=True, opt=opt)
-        gpu = run_gpu(net, loads, outages=outs, K=K, alpha=a, form=form, history=True, opt=opt)  # AUTO
-        assert gpu["info"].path == dual.PATH_CLUSTER
-        assert_parity(net, gpu, orc, bitwise_multipliers=True)
+        for path in (dual.PATH_CLUSTER, dual.PATH_BATCHED):
+            gpu = run_gpu(net, loads, outages=outs, K=K, alpha=a, form=form, history=True, opt=opt, path=path,
+                          split=600)
+            assert gpu["info"].path == path
+            assert_parity(net, gpu, orc, bitwise_multipliers=True)
 
 
 def test_optimizer_adam_config3_cluster16():
@@ -432,10 +434,10 @@ def test_optimizer_adam_config3_cluster16():
     assert_parity(net, gpu, orc, bitwise_multipliers=True)
 
 
-def test_optimizer_rejected_off_the_cluster_path():
+def test_optimizer_rejected_on_the_single_path():
     import torch
     net = inst.make_network(0)
-    h = dual.DcopfDual(net, path=dual.PATH_BATCHED)
+    h = dual.DcopfDual(net, path=dual.PATH_SINGLE)
     h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(np.tile(net.base_load[:, None], (1, 4)))).cuda())
     with pytest.raises(dual.DcopfError):
         h.set_optimizer(dual.OPT_ADAM, beta1=0.9, beta2=0.999, epsilon=1e-8)
@@ -639,4 +641,22 @@ def test_batched_more_tiles_than_sms(form):
     idx = np.array([0, 63, 64, 9407, 9999])
     orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=form, switchable=sw,
                        threads=4)
+    assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("name", ["adam", "gdm"])
+def test_optimizer_batched_config4_kvl_sampled(name):
+    """KVL + an optimiser variant on the config-4 batch (variant 4b: feasible,
+    one load factor per instance), the bench's launch configuration."""
+    opt, alpha = OPTS[name]
+    net = inst.make_network(4)
+    sw = non_tree_switchable(net)
+    B = inst.CONFIG4_BATCH
+    batch = inst.config4_batch(net, range(B), variant="4b")
+    K = 300
+    a = inst.alpha_schedule(K, alpha if name == "adam" else 1e-3)
+    gpu = run_gpu(net, batch.load, K=K, alpha=a, form=dual.FORM_KVL, path=dual.PATH_BATCHED, switchable=sw,
+                  opt=opt)
+    idx = np.array([0, 77, 8191])
+    orc = oracle.solve(net, batch.load[idx], K=K, alpha=a, form=oracle.FORM_KVL, switchable=sw, opt=opt, threads=3)
     assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)

@@ -31,7 +31,7 @@ from paper_2406_13191_b200 import instances as inst  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "targets.json")
 WORKLOADS = {"config1": (1, False), "config2": (2, True), "config3": (3, False), "config3q": (3, True),
-             "config4": (4, False)}
+             "config4": (4, False), "config4b": (4, False)}
 
 
 def main():
@@ -61,7 +61,7 @@ def main():
             K = inst.ITERS[config]
             if config == 4:
                 ids = np.arange(0, inst.CONFIG4_BATCH, 128)
-                batch = inst.config4_batch(net, ids)
+                batch = inst.config4_batch(net, ids, variant="4b" if wl == "config4b" else "4")
             else:
                 ids = np.zeros(1, dtype=np.int64)
                 batch = inst.single_batch(net)
@@ -75,6 +75,8 @@ def main():
             primal = None
             if config != 4:  # the exact optimum (HiGHS; Kelley cutting planes for QP): true gap, (ii)
                 primal = (inst.primal_qp(net, net.base_load) if quad else inst.primal_lp(net, net.base_load))[1]
+            elif wl == "config4b":  # feasible instances: their LP optima (sampled)
+                primal = [inst.primal_lp(net, batch.load[r])[1] for r in range(len(ids))]
             js[key] = {"K": K, "alpha": alpha, "opt": {"name": a.opt, **opt}, "primal_opt": primal,
                        "instance_ids": ids.tolist(), "best": res.best.tolist(),
                        "bound": res.bound.tolist(), "status": res.status.tolist(),
