@@ -413,6 +413,10 @@ def main():
         n_bm = (info.alg_bytes_per_inst_iter // 8 - 3 * net.n_bus) // 2  # branch-block multipliers per instance
         eval_read = 8 * (2 * net.n_bus + n_bm)
         per_gpu_bytes = B * (info.alg_bytes_per_inst_iter * K + (eval_read if path == dual.PATH_BATCHED else 0))
+        if args.opt != "plain":  # the optimiser state rows (1 or 2 per multiplier) are read and written too
+            nstate = 2 if args.opt == "adam" else 1
+            n_bm = (info.alg_bytes_per_inst_iter // 8 - 3 * net.n_bus) // 2
+            per_gpu_bytes += B * K * nstate * 2 * 8 * (net.n_bus + n_bm)
         achieved = per_gpu_bytes / (ms / 1e3) / 1e9  # GB/s on this rank's kernel launches
         traffic = None  # DRAM bytes per launch, from the committed ncu capture (scaled to this launch)
         try:

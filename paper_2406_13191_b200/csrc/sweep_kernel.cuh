@@ -154,6 +154,9 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 struct D2 {
   double x, y;
 };
+struct OState {  // optimiser state of a lane's two instances (one row)
+  double2 s1, s2;
+};
 __device__ __forceinline__ D2 ld2(const uint8_t *base, int off) {
   const double2 v = *reinterpret_cast<const double2 *>(base + off);
   return D2{v.x, v.y};
@@ -322,15 +325,22 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
     }
     // optimiser-variant update of one row of the lane's two instances (the
     // state row sits at the same offset of the state arrays)
-    auto ostep = [&](double y0, double y1, double g0, double g1, size_t off, bool lam_side, bool do0,
+    // (oload issues the state loads at the start of an item so their latency
+    // overlaps the item's work; ostep updates and stores them)
+    auto oload = [&](size_t off, bool lam_side, bool on) -> OState {
+      OState o{make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+      if (on) {
+        o.s1 = *reinterpret_cast<const double2 *>((lam_side ? os1l : os1b) + off);
+        if (ost2) o.s2 = *reinterpret_cast<const double2 *>((lam_side ? os2l : os2b) + off);
+      }
+      return o;
+    };
+    auto ostep = [&](OState &o, double y0, double y1, double g0, double g1, size_t off, bool lam_side, bool do0,
                      bool do1) -> D2 {
-      double2 *p1 = reinterpret_cast<double2 *>((lam_side ? os1l : os1b) + off);
-      double2 *p2 = reinterpret_cast<double2 *>((lam_side ? os2l : os2b) + off);
-      double2 S1 = *p1, S2 = ost2 ? *p2 : make_double2(0.0, 0.0);
-      if (do0) y0 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y0, g0, alpha, S1.x, S2.x, ob1t, ob2t);
-      if (do1) y1 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y1, g1, alpha, S1.y, S2.y, ob1t, ob2t);
-      *p1 = S1;
-      if (ost2) *p2 = S2;
+      if (do0) y0 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y0, g0, alpha, o.s1.x, o.s2.x, ob1t, ob2t);
+      if (do1) y1 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y1, g1, alpha, o.s1.y, o.s2.y, ob1t, ob2t);
+      *reinterpret_cast<double2 *>((lam_side ? os1l : os1b) + off) = o.s1;
+      if (ost2) *reinterpret_cast<double2 *>((lam_side ? os2l : os2b) + off) = o.s2;
       return D2{y0, y1};
     };
     double v0 = 0.0, v1 = 0.0;
@@ -361,6 +371,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
         for (int j = wt[tbl * (NW + 1) + warp], je = wt[tbl * (NW + 1) + warp + 1]; j < je; ++j) {
           const RecC r = Cv[j];
+          OState ost = oload((size_t)r.wpos * RB, true, OPT && !EVAL && write && act);
           const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
           double gl0 = -di.x, gl1 = -di.y;
 #pragma unroll 1
@@ -413,7 +424,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
             if (EVAL) {
               st2(dst, gl0, gl1);
             } else if constexpr (OPT) {
-              const D2 y = ostep(li.x, li.y, gl0, gl1, (size_t)r.wpos * RB, true, !CHK || step0, !CHK || step1);
+              const D2 y = ostep(ost, li.x, li.y, gl0, gl1, (size_t)r.wpos * RB, true, !CHK || step0, !CHK || step1);
               st2(dst, y.x, y.y);
             } else {
               st2(dst, (!CHK || step0) ? li.x + alpha * gl0 : li.x, (!CHK || step1) ? li.y + alpha * gl1 : li.y);
@@ -465,6 +476,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         const RecDe *De = reinterpret_cast<const RecDe *>(prog + h2.y);
         for (int j = wt[2 * (NW + 1) + warp], je = wt[2 * (NW + 1) + warp + 1]; j < je; ++j) {
           const RecD r = Dv[j];
+          OState ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
           const D2 kv = ld2(brp, r.ks);
           double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll 1
@@ -487,7 +499,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
             if (EVAL) {
               st2(dst, acc0, acc1);
             } else if constexpr (OPT) {
-              const D2 y = ostep(kv.x, kv.y, acc0, acc1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
+              const D2 y = ostep(ost, kv.x, kv.y, acc0, acc1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
               st2(dst, y.x, y.y);
             } else {
               st2(dst, (!CHK || step0) ? kv.x + alpha * acc0 : kv.x, (!CHK || step1) ? kv.y + alpha * acc1 : kv.y);
@@ -555,6 +567,8 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
         for (int j = wt[NW + 1 + warp], je = wt[NW + 2 + warp]; j < je; ++j) {
           const RecB r = Bv[j];
+          OState ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
+          OState ost_m = oload((size_t)r.wpos * BR + RB, false, FORM == kFormF1 && OPT && !EVAL && write && act);
           double b0 = r.b, b1 = r.b, F0 = r.F, F1v = r.F;
           bool o0 = false, o1 = false;
           if (r.obr >= 0 && flagged(r.obr)) {  // obr < 0: branch never taken out
@@ -582,7 +596,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
               if (EVAL) {
                 st2(dst, g0, g1);
               } else if constexpr (OPT) {
-                const D2 y = ostep(nu.x, nu.y, g0, g1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
+                const D2 y = ostep(ost, nu.x, nu.y, g0, g1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
                 st2(dst, y.x, y.y);
               } else {
                 st2(dst, (!CHK || step0) ? nu.x + alpha * g0 : nu.x, (!CHK || step1) ? nu.y + alpha * g1 : nu.y);
@@ -602,8 +616,8 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
                 double p0 = mp.x, m0 = mm.x, p1 = mp.y, m1 = mm.y;
                 if constexpr (OPT) {
                   const bool d0 = !CHK || step0, d1 = !CHK || step1;
-                  const D2 yp = ostep(mp.x, mp.y, gp0, gp1, (size_t)r.wpos * BR, false, d0, d1);
-                  const D2 ym = ostep(mm.x, mm.y, gm0, gm1, (size_t)r.wpos * BR + RB, false, d0, d1);
+                  const D2 yp = ostep(ost, mp.x, mp.y, gp0, gp1, (size_t)r.wpos * BR, false, d0, d1);
+                  const D2 ym = ostep(ost_m, mm.x, mm.y, gm0, gm1, (size_t)r.wpos * BR + RB, false, d0, d1);
                   if (d0) {
                     p0 = (yp.x > 0.0) ? yp.x : 0.0;  // mu <- max(mu, 0)
                     m0 = (ym.x > 0.0) ? ym.x : 0.0;
