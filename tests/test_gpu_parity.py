@@ -295,6 +295,10 @@ def test_single_bus_no_branches(path):
                        gen_pmax=np.array([100.0]), gen_c=np.array([5.0]))
     gpu = run_gpu(net, np.array([[50.0]]), K=20, alpha=inst.alpha_schedule(20, 0.02), path=path)
     assert gpu["best"][0] == 250.0 and gpu["bound"][0] == 250.0
+    if path != dual.PATH_SINGLE:  # KVL: no branches, no cycles
+        gpu = run_gpu(net, np.array([[50.0]]), K=20, alpha=inst.alpha_schedule(20, 0.02), path=path,
+                      form=dual.FORM_KVL)
+        assert gpu["best"][0] == 250.0 and gpu["br"].shape[1] == 0
 
 
 def test_implied_theta_box_matches_generator():
