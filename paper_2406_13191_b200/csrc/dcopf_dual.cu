@@ -322,7 +322,7 @@ int compile_schedule(dcopf_dual_t h, int W) {
   for (auto &cd : cands) {
     sc = Schedule();
     sc.ring_life = cd.second;
-    sc.pool_gap = h->soft_sync ? 2 : 1;  // soft sync: consumer warps drift by up to one step
+    sc.pool_gap = h->soft_sync ? 3 : 1;  // soft sync: consumer warps drift by up to two steps
     std::string err = build_schedule(h->ni, cd.first, P, W, kSweepWarps, &sc,
                                      h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr);
     if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());

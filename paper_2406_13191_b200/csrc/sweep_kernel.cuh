@@ -289,14 +289,15 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
   double ob1t = a.b1t, ob2t = a.b2t;
   uint8_t *thp = smem + a.off_th + 2 * lane;  // theta*_i code rows
   uint8_t *fcp = smem + a.off_fc + 2 * lane;  // f*_l code rows (F2)
-  // Consumer warps are not stepped in lock-step: step g waits only for
-  //   A-done(g-1): theta* of chunk g-1 (read by B) exists, and every warp has
-  //                finished step g-2, so the theta* / f* slots this step
-  //                overwrites are dead (pool slots are reused only 2 steps
-  //                after their last read: schedule pool_gap = 2);
-  //   B-done(g-1): f* of the branches C reads exists;
-  //   full[stage]: the step's program block and rows have landed.
-  // A warp may therefore run up to one step ahead of the slowest one.
+  // Consumer warps are not stepped in lock-step.  In step g a warp waits on
+  //   full[stage]   before anything: the step's program block and rows landed;
+  //   A-done(g-1)   after its A(g) items, before B: the theta* codes of chunk
+  //                 g-1 exist (every warp finished A(g-1), hence step g-2);
+  //   B-done(g-1)   after its B items, before C: the f* codes C reads exist.
+  // A(g) itself waits on no warp: the theta* slots it writes were last read
+  // 3 or more steps earlier (schedule pool_gap = 3) and the A-done(g-2) wait of
+  // the previous step already guarantees every warp finished step g-3.  (KVL:
+  // B(g) likewise, then B-done(g-1) before C and D.)  Warps drift by <= 2 steps.
   unsigned gs = 0;  // global step counter (continues across sweeps; only gs mod 8 matters)
   const int nout = a.max_out;
   const int *my_outs0 = outs_s + (2 * lane) * kMaxOut, *my_outs1 = my_outs0 + kMaxOut;
@@ -434,9 +435,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       };
       if constexpr (FORM == kFormKVL) {
       if (a.debug_mode != 1) {
-      // f* codes of B(<= s-1) exist and every warp has finished step s-2
-      // (f* code slots are reused 2 steps after their last read)
-      if (SOFT && gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+      // B(s) needs no other warp: its rows come by TMA, and the f* code slots
+      // it writes were last read 3+ steps ago (pool_gap 3), by which time every
+      // warp has finished (this warp waited B-done(s-2) in the previous step)
       // ---------------- B(s): q_l = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t), f* ----------------
       {
         const RecBK *Bv = reinterpret_cast<const RecBK *>(prog + h2.z);
@@ -468,7 +469,10 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
           v1 += q1 * f1;
         }
       }
-      if (SOFT) warp_arrive(&bdone[gs & 3], lane);
+      if (SOFT) {  // C and D read the f* codes of B(<= s-1)
+        warp_arrive(&bdone[gs & 3], lane);
+        if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+      }
       phaseC(1);
       // ---------------- D(s-1): d/dkappa_k = sum_l C_kl x_l f*_l, kappa' ----------------
       {
@@ -510,7 +514,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       }  // debug_mode
       } else {
       if (a.debug_mode != 1) {  // (1: data movement only -- measurement)
-      if (SOFT && gs > 0) mbar_wait_backoff(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+      // A(s) needs no other warp: its rows come by TMA, and the theta* code
+      // slots it writes were last read 3+ steps ago (pool_gap 3), by which time
+      // every warp has finished (this warp waited A-done(s-2) in step s-1)
       // ---------------- A(s): w_i, theta* codes ----------------
       {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
@@ -561,7 +567,11 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
           }
         }
       }
-      if (SOFT) warp_arrive(&adone[gs & 3], lane);
+      if (SOFT) {  // B(s-1) reads the theta* codes of A(<= s-1); the f* slots it writes
+        // were last read 2+ steps ago, and A-done(s-1) implies every warp finished step s-2
+        warp_arrive(&adone[gs & 3], lane);
+        if (gs > 0) mbar_wait_backoff(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+      }
       // ---------------- B(s-1): branches ----------------
       {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
