@@ -53,6 +53,7 @@ struct ClusterArgs {
   double *s1_lam, *s2_lam;      // [b][n_bus] instance-major internal, or null
   double *s1_br, *s2_br;        // [b][n_br * BRW]
   double tol;                   // stopping rule (0: off)
+  int dbg;                      // measurement only: 1 = skip the phases' work (synchronisation floor)
 };
 
 __device__ __forceinline__ double opt_step(const ClusterArgs &a, double y, double g, double al, double *s1,
@@ -77,6 +78,11 @@ __device__ __forceinline__ unsigned cl_id() {
 }
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// (a cluster of one CTA needs only the block barrier)
+__device__ __forceinline__ void cl_sync(unsigned C) {
+  if (C == 1) __syncthreads();
+  else cl_sync();
 }
 __device__ __forceinline__ unsigned cl_map(unsigned local_addr, unsigned rank) {
   unsigned r;
@@ -261,8 +267,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
     __syncthreads();
   };
 
+  const int nAw = a.dbg ? 0 : nA, nBw = a.dbg ? 0 : nB, nCyw = a.dbg ? 0 : H.nCy;  // (dbg: measurement)
+  // the step of iteration k+1 is fetched during iteration k: every cluster
+  // barrier invalidates L1, so a load at the top of the iteration would cost
+  // an L2 round trip on the critical path each time
+  double alpha_next = (K > 0) ? a.alpha[0] : 0.0;
   for (long k = 0; k <= K; ++k) {
-    const double alpha = (k < K) ? a.alpha[k] : 0.0;
+    const double alpha = alpha_next;
+    if (k + 1 < K) alpha_next = a.alpha[k + 1];
     if (ost2 && k < K) {  // Adam's beta^t, t = steps since the state was reset
       b1t = b1t * a.beta1;
       b2t = b2t * a.beta2;
@@ -270,7 +282,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
     double val = 0.0;
     // ---------------- A: w_i, theta*_i (not in the angle-free KVL form) ----------------
     if (FORM != kFormKVL) {
-    for (int i = tid; i < nA; i += nthr) {
+    for (int i = tid; i < nAw; i += nthr) {
       const ClA r = Ar[i];
       double w = 0.0;
       if (FORM == kFormF2) {
@@ -292,7 +304,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
       th_s[i] = th;
       if (!isref) val += w * th;
     }
-    cl_sync();
+    cl_sync(C);
     if (FORM == kFormF2 && k > 0) finish(k - 1);
     }
     const bool step = (MODE == kModeStep) && (k < K) && !flag[0];
@@ -301,7 +313,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
       // q_l = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t), cycles in ascending k
       const ClBk *Bk = reinterpret_cast<const ClBk *>(smem + H.off_B);
       const ClBKe *BK = reinterpret_cast<const ClBKe *>(smem + H.off_IA);
-      for (int j = tid; j < nB; j += nthr) {
+      for (int j = tid; j < nBw; j += nthr) {
         const ClBk r = Bk[j];
         double sum = 0.0;
         for (int e = r.e0; e < r.e1; ++e) {
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
         val += q * f;
       }
     } else
-    for (int j = tid; j < nB; j += nthr) {
+    for (int j = tid; j < nBw; j += nthr) {
       const ClB r = Br[j];
       const double phi = r.b * (cl_ld(r.ts) - cl_ld(r.tt));
       if (FORM == kFormF2) {
@@ -344,9 +356,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
         }
       }
     }
-    cl_sync();
+    cl_sync(C);
     // ---------------- C: generators, d/dlambda, lambda' ----------------
-    for (int i = tid; i < nA; i += nthr) {
+    for (int i = tid; i < nAw; i += nthr) {
       const ClC r = Cr[i];
       const double li = lam_s[i], di = d_s[i];
       double gl = -di;
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
       // d/dkappa_k = sum_l C_kl (f*_l x_l), branches in ascending id (f * (-x) == -(f x))
       const ClCy *Cy = reinterpret_cast<const ClCy *>(smem + H.off_Cy);
       const ClCe *CE = reinterpret_cast<const ClCe *>(smem + H.off_CE);
-      for (int c = tid; c < H.nCy; c += nthr) {
+      for (int c = tid; c < nCyw; c += nthr) {
         const ClCy r = Cy[c];
         double acc = 0.0;
         for (int e = r.e0; e < r.e1; ++e) {
@@ -403,7 +415,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
       if (lane == 0) red[0] = v;
     }
     if (FORM != kFormF2 || k == K) {
-      cl_sync();  // F1 / KVL: the next phase reads lambda' (kappa'); and every partial is published
+      cl_sync(C);  // F1 / KVL: the next phase reads lambda' (kappa'); and every partial is published
       finish(k);
     }
   }
@@ -411,11 +423,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
   if (MODE == kModeStep) {
     double *lam_o = a.lam + b * (size_t)a.n_bus + H.bus0;
     double *br_o = a.br + bm0;
-    for (int i = tid; i < nA; i += nthr) lam_o[i] = lam_s[i];
+    for (int i = tid; i < nAw; i += nthr) lam_o[i] = lam_s[i];
     for (int j = tid; j < nbm; j += nthr) br_o[j] = br_s[j];
     if (ost) {
       const size_t ol = b * (size_t)a.n_bus + H.bus0;
-      for (int i = tid; i < nA; i += nthr) {
+      for (int i = tid; i < nAw; i += nthr) {
         a.s1_lam[ol + i] = s1l[i];
         if (ost2) a.s2_lam[ol + i] = s2l[i];
       }

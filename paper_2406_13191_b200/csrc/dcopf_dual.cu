@@ -534,6 +534,7 @@ ClusterArgs cluster_args(dcopf_dual_t h) {
   a.b1t = h->b1t;
   a.b2t = h->b2t;
   a.tol = h->tol;
+  if (const char *e = getenv("DCOPF_CLUSTER_DEBUG")) a.dbg = atoi(e);  // measurement only
   a.s1_lam = h->os[0];
   a.s2_lam = h->os[1];
   a.s1_br = h->os[2];
