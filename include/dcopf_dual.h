@@ -124,9 +124,13 @@ typedef struct {
   int32_t reserved[3];      /* zero */
 } dcopf_options;
 
-/* Create a handle: validates and copies the network, reorders buses
- * (reverse Cuthill-McKee) and builds the bus->branch incidence (CSR, entries
- * in ascending original branch id) and the generator map on the device.
+/* Create a handle: validates and copies the network, orders the buses
+ * internally (depth-first over a breadth-first spanning tree from the
+ * reference bus, smallest subtree first: neighbours stay close, which keeps
+ * the batched path's shared-memory window and the cluster path's cross-CTA
+ * traffic small), builds the bus->branch incidence (CSR, entries in
+ * ascending original branch id) and the generator map, and -- KVL form --
+ * the canonical cycle basis (reading A-28).
  * Errors: EINVAL (sizes, indices, self loops, negative b/F/Theta/a,
  * pmin > pmax, non-finite data, bad options), ETOPOLOGY (disconnected over
  * b > 0, or over never-switchable branches when br_switchable is given),
