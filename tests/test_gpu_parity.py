@@ -161,17 +161,20 @@ def test_large_network_batched_path(config, form):
 # checked on sampled instances; and a 64-instance cut checked everywhere
 
 
-def test_config4_full_batch_sampled():
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
+def test_config4_full_batch_sampled(form):
+    """config 4 at full K (5000) in the bench's launch configuration (8192
+    instances, 147 tiles of 56), sampled instances vs the oracle."""
     net = inst.make_network(4)
     B = inst.CONFIG4_BATCH
     K = inst.ITERS[4]
     batch = inst.config4_batch(net, range(B))
     a = inst.alpha_schedule(K)
-    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=FORM_F2,
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form,
                   path=dual.PATH_BATCHED, switchable=non_tree_switchable(net))
     assert gpu["info"].grid * gpu["info"].tile_width >= B and gpu["info"].grid <= 148
     idx = np.array([0, 31, 4097, 8191])
-    orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=FORM_F2,
+    orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=form,
                        threads=4)
     assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)
 
