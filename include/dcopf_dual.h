@@ -66,15 +66,27 @@ enum {
 enum {
   DCOPF_FORM_FLOW_BOX = 0,   /* F2 */
   DCOPF_FORM_LIMIT_ROWS = 1, /* F1 */
-  DCOPF_FORM_CYCLE = 2       /* KVL: angle-free cycle-basis twin of the paper's PTDF constraint
+  DCOPF_FORM_CYCLE = 2,      /* KVL: angle-free cycle-basis twin of the paper's PTDF constraint
                                 (Eq. 1): boxes p, |f| <= F; KCL
                                 dualised with lambda, Kirchhoff's voltage law on the fundamental
                                 cycles of a canonical spanning tree (reading A-28) with
-                                free kappa[n_cycles], n_cycles = n_branch - n_bus + 1.  Cluster
-                                path only; the branch block of get/set_multipliers and evaluate is
-                                kappa[n_cycles][B] in canonical cycle order; outages must be
+                                free kappa[n_cycles], n_cycles = n_branch - n_bus + 1.  Cluster and
+                                batched paths; the branch block of get/set_multipliers and evaluate
+                                is kappa[n_cycles][B] in canonical cycle order; outages must be
                                 switchable branches (the tree is built from the never-switchable
                                 ones) */
+  DCOPF_FORM_PTDF = 3        /* the paper's dense-PTDF problem literally (Eq. 1;
+                                SURVEY.md NEXT-4), for LOAD-ONLY batches on a fixed topology:
+                                  min a p^2 + c p  s.t.  1^T p = 1^T d (lambda, one per instance),
+                                  -F <= H_a (G p - d) <= F (mu+, mu- >= 0), pmin <= p <= pmax,
+                                H = Omega E (E^T Omega E)^{-1} with a zero slack column,
+                                built by the library at create (see dcopf_dual_get_ptdf).  Runs on
+                                DCOPF_PATH_DENSE only: per ascent step two fp64 GEMMs over the batch
+                                (tensor-core DMMA) with the inner minimiser, dual value, gradient and
+                                projected step fused into their epilogues.  Multiplier layouts:
+                                lambda[1][B]; branch block mu+[n_branch][B] followed by
+                                mu-[n_branch][B] (as F1).  Outages are rejected (EINVAL): one H_a
+                                serves the whole batch.  theta_max and br_switchable are ignored. */
 };
 
 /* per-instance status: a diverged instance is frozen; the
@@ -91,9 +103,11 @@ enum {
                              persistent launch for all K iterations: a TMA-fed sweep over a
                              host-compiled schedule of the network (DFS tree bus order) */
   DCOPF_PATH_SINGLE = 2,  /* one persistent CTA per instance running all K iterations on chip */
-  DCOPF_PATH_CLUSTER = 3  /* one thread-block cluster of up to 16 CTAs per instance, the network
+  DCOPF_PATH_CLUSTER = 3, /* one thread-block cluster of up to 16 CTAs per instance, the network
                              partitioned over the CTAs' shared memories (distributed shared
                              memory), all K iterations in one launch */
+  DCOPF_PATH_DENSE = 4    /* DCOPF_FORM_PTDF only (and AUTO resolves to it): batched fp64 GEMMs,
+                             3 launches per ascent step, batch padded to a multiple of 128 */
 };
 
 /* Network description.  Host pointers,
@@ -116,7 +130,7 @@ typedef struct {
 } dcopf_network_desc;
 
 typedef struct {
-  int32_t form;             /* DCOPF_FORM_FLOW_BOX (0) or DCOPF_FORM_LIMIT_ROWS (1) */
+  int32_t form;             /* DCOPF_FORM_* */
   int32_t precision;        /* 64 (fp64; the only mode in this build) */
   int32_t device;           /* CUDA device ordinal */
   int32_t path;             /* DCOPF_PATH_* */
@@ -259,6 +273,15 @@ typedef struct {
   int32_t cluster_size;           /* cluster path: CTAs per instance (1 otherwise) */
 } dcopf_info;
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info);
+
+/* DCOPF_FORM_PTDF: the PTDF matrix the handle iterates with, H_a[n_branch][n_bus]
+ * (row-major, original ids), into a host or device buffer.  The
+ * library builds it from a spanning tree and its fundamental cycles (reading
+ * A-28): H_a = T - C^T (C X C^T)^{-1} C X T, T the tree flows of "inject 1 at
+ * bus i, withdraw at the slack", C the signed cycle incidence, X = diag(1/b);
+ * a branch with b = 0 carries no flow (zero row).  Errors: EINVAL (another
+ * form, Ha NULL), ECUDA. */
+int dcopf_dual_get_ptdf(dcopf_dual_t h, double *Ha, void *cuda_stream);
 
 const char *dcopf_dual_last_error(dcopf_dual_t h); /* never NULL; h may be NULL (last create error) */
 void dcopf_dual_destroy(dcopf_dual_t h);           /* NULL is a no-op */

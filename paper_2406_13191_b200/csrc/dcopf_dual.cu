@@ -26,6 +26,7 @@
 #include "cluster.h"
 #include "cluster_kernel.cuh"
 #include "dual_kernels.cuh"
+#include "ptdf.h"
 #include "schedule.h"
 #include "sweep_kernel.cuh"
 
@@ -90,6 +91,8 @@ struct dcopf_dual_s {
   uint8_t *d_cblob = nullptr;
   int *d_lam_perm_b = nullptr, *d_lam_inv_b = nullptr, *d_d_perm_b = nullptr, *d_br_perm_b = nullptr,
       *d_br_inv_b = nullptr, *d_br_pos_b = nullptr;
+  // dense-PTDF form (DCOPF_FORM_PTDF): all of its state; the fields above stay unused
+  PtdfState *pt = nullptr;
 };
 
 namespace {
@@ -695,6 +698,7 @@ const char *dcopf_dual_last_error(dcopf_dual_t h) { return h ? h->err.c_str() : 
 void dcopf_dual_destroy(dcopf_dual_t h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  ptdf_destroy(h->pt);
   free_batch(h);
   cudaFree(h->d_cyc_perm);
   cudaFree(h->d_cyc_inv);
@@ -722,11 +726,14 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   memset(&o, 0, sizeof o);
   o.precision = 64;
   if (opt) o = *opt;
-  if (o.form != DCOPF_FORM_FLOW_BOX && o.form != DCOPF_FORM_LIMIT_ROWS && o.form != DCOPF_FORM_CYCLE)
+  if (o.form != DCOPF_FORM_FLOW_BOX && o.form != DCOPF_FORM_LIMIT_ROWS && o.form != DCOPF_FORM_CYCLE &&
+      o.form != DCOPF_FORM_PTDF)
     return fail(nullptr, DCOPF_EINVAL, "unknown form %d", o.form);
   if (o.precision != 64 && o.precision != 0)
     return fail(nullptr, DCOPF_EINVAL, "precision %d not supported (fp64 only)", o.precision);
-  if (o.path < 0 || o.path > 3) return fail(nullptr, DCOPF_EINVAL, "unknown path %d", o.path);
+  if (o.path < 0 || o.path > 4) return fail(nullptr, DCOPF_EINVAL, "unknown path %d", o.path);
+  if ((o.form == DCOPF_FORM_PTDF) != (o.path == DCOPF_PATH_DENSE) && o.path != DCOPF_PATH_AUTO)
+    return fail(nullptr, DCOPF_EINVAL, "the PTDF form runs on DCOPF_PATH_DENSE (and only it)");
   const int nb = net->n_bus, nl = net->n_branch, ng = net->n_gen;
   if (nb < 1 || nl < 0 || ng < 0) return fail(nullptr, DCOPF_EINVAL, "bad sizes n_bus=%d n_branch=%d n_gen=%d", nb, nl, ng);
   if (net->ref_bus < 0 || net->ref_bus >= nb) return fail(nullptr, DCOPF_EINVAL, "ref_bus %d out of range", net->ref_bus);
@@ -756,13 +763,32 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
     if (net->gen_a && (!(net->gen_a[g] >= 0.0) || !std::isfinite(net->gen_a[g])))
       return fail(nullptr, DCOPF_EINVAL, "generator %d quadratic cost must be finite and >= 0", g);
   }
-  if (net->theta_max)
+  if (net->theta_max && o.form != DCOPF_FORM_PTDF)
     for (int i = 0; i < nb; ++i)
       if (!(net->theta_max[i] >= 0.0) || !std::isfinite(net->theta_max[i]))
         return fail(nullptr, DCOPF_EINVAL, "theta_max[%d] must be finite and >= 0", i);
   std::vector<char> use(nl);
   for (int l = 0; l < nl; ++l) use[l] = net->br_b[l] > 0.0;
   if (!connected(nb, fr, to, use)) return fail(nullptr, DCOPF_ETOPOLOGY, "network is disconnected over branches with b > 0");
+  if (o.form == DCOPF_FORM_PTDF) {  // dense PTDF: its own state (ptdf.cu), no internal reordering
+    dcopf_dual_t h = new dcopf_dual_s();
+    h->device = o.device;
+    h->form = o.form;
+    h->path_opt = h->path = DCOPF_PATH_DENSE;
+    h->n_bus = nb;
+    h->n_br = nl;
+    h->n_gen = ng;
+    PtdfNetIn pn{nb, nl, ng, net->ref_bus, fr.data(), to.data(), net->br_b, net->br_fmax, net->gen_bus,
+                 net->gen_pmin, net->gen_pmax, net->gen_c, net->gen_a};
+    std::string perr;
+    const int prc = ptdf_create(pn, o.device, &h->pt, &perr);
+    if (prc) {
+      delete h;
+      return fail(nullptr, prc, "%s", perr.c_str());
+    }
+    *out = h;
+    return DCOPF_OK;
+  }
   if (net->br_switchable) {
     for (int l = 0; l < nl; ++l) use[l] = net->br_b[l] > 0.0 && !net->br_switchable[l];
     if (!connected(nb, fr, to, use))
@@ -896,6 +922,20 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
     return fail(h, DCOPF_EINVAL, "max_out must be in [0, %d] with a non-NULL outage array", kMaxOut);
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (h->pt) {
+    if (max_out > 0) {
+      std::vector<int32_t> raw((size_t)B * max_out);
+      CK(h, cudaMemcpy(raw.data(), outages, raw.size() * sizeof(int32_t), cudaMemcpyDefault));
+      for (int32_t l : raw)
+        if (l != -1)
+          return fail(h, DCOPF_EINVAL, "the PTDF form takes load-only batches (one H_a for the batch): no outages");
+    }
+    std::string perr;
+    const int prc = ptdf_set_batch(h->pt, B, load, s, &perr);
+    if (prc) return fail(h, prc, "%s", perr.c_str());
+    h->B = B;
+    return DCOPF_OK;
+  }
   int path = h->path_opt;
   if (h->form == DCOPF_FORM_CYCLE && path == DCOPF_PATH_SINGLE)
     return fail(h, DCOPF_EINVAL, "the KVL (cycle) form runs on the cluster and batched paths");
@@ -1006,7 +1046,11 @@ int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *h
     return fail(h, DCOPF_ESTATE, "optimiser variants run on the cluster and batched paths");
   int rc = stage_alpha(h, K, alpha, s);
   if (rc) return rc;
-  if (h->path == DCOPF_PATH_BATCHED) {
+  if (h->pt) {
+    std::string perr;
+    rc = ptdf_iterate(h->pt, K, h->alpha_dev, hist, s, &perr);
+    if (rc) return fail(h, rc, "%s", perr.c_str());
+  } else if (h->path == DCOPF_PATH_BATCHED) {
     SweepArgs a = sweep_args(h);
     a.alpha = h->alpha_dev;
     a.K = K;
@@ -1054,6 +1098,11 @@ int dcopf_dual_get_bound(dcopf_dual_t h, double *bound, double *best, int32_t *s
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (h->pt) {
+    std::string perr;
+    const int prc = ptdf_get_bound(h->pt, bound, best, status, s, &perr);
+    return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
+  }
   int rc = copy_out(h, bound, h->bound, s);
   if (!rc) rc = copy_out(h, best, h->best, s);
   if (!rc) rc = copy_out(h, status, h->status, s);
@@ -1065,6 +1114,11 @@ int dcopf_dual_get_multipliers(dcopf_dual_t h, double *lambda, double *branch, v
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (h->pt) {
+    std::string perr;
+    const int prc = ptdf_get_multipliers(h->pt, lambda, branch, s, &perr);
+    return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
+  }
   const int cur = (h->path == DCOPF_PATH_BATCHED) ? h->cur : 0;
   const Perms pm = perms(h);
   int rc = export_ext(h, h->lam[cur], lambda, pm.lam_inv, h->n_bus, 1, s);
@@ -1077,6 +1131,11 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (h->pt) {
+    std::string perr;
+    const int prc = ptdf_set_multipliers(h->pt, lambda, branch, s, &perr);
+    return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
+  }
   const int cur = (h->path == DCOPF_PATH_BATCHED) ? h->cur : 0;
   const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_bm_ent * h->bm_C;
   double *tl = nullptr, *tb = nullptr;
@@ -1130,6 +1189,11 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (h->pt) {
+    std::string perr;
+    const int prc = ptdf_evaluate(h->pt, value, grad_lambda, grad_branch, s, &perr);
+    return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
+  }
   const size_t nlam = (size_t)h->B_pad * h->n_bus, nbr = (size_t)h->B_pad * h->n_bm_ent * h->bm_C;
   if (!h->g_lam) CK(h, cudaMalloc(&h->g_lam, std::max<size_t>(nlam, 1) * 8));
   if (!h->g_br) CK(h, cudaMalloc(&h->g_br, std::max<size_t>(nbr, 1) * 8));
@@ -1174,6 +1238,12 @@ int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt) {
   if (h->B > 0 && h->path == DCOPF_PATH_SINGLE && o.variant != DCOPF_OPT_PLAIN)
     return fail(h, DCOPF_EINVAL, "optimiser variants run on the cluster and batched paths");
   CK(h, cudaSetDevice(h->device));
+  if (h->pt) {
+    h->opt = o;
+    std::string perr;
+    const int prc = ptdf_set_optimizer(h->pt, o, &perr);
+    return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
+  }
   const int ns_old = opt_nstate(h);
   h->opt = o;
   if (opt_nstate(h) != ns_old) {  // the shared-memory plan holds the state arrays: rebuild it
@@ -1192,6 +1262,7 @@ int dcopf_dual_set_stop(dcopf_dual_t h, double tol) {
   if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
   if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(h, DCOPF_EINVAL, "tol must be finite and >= 0");
   h->tol = tol;
+  if (h->pt) ptdf_set_stop(h->pt, tol);
   return DCOPF_OK;
 }
 
@@ -1200,6 +1271,11 @@ int dcopf_dual_set_target(dcopf_dual_t h, const double *target, void *cuda_strea
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (h->pt) {
+    std::string perr;
+    const int prc = ptdf_set_target(h->pt, target, s, &perr);
+    return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
+  }
   if (!target) {
     h->has_target = false;
     return DCOPF_OK;
@@ -1219,12 +1295,21 @@ int dcopf_dual_get_first_hit(dcopf_dual_t h, int64_t *hit, void *cuda_stream) {
   if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
   if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
   CK(h, cudaSetDevice(h->device));
+  if (h->pt) {
+    std::string perr;
+    const int prc = ptdf_get_first_hit(h->pt, hit, (cudaStream_t)cuda_stream, &perr);
+    return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
+  }
   return copy_out(h, reinterpret_cast<long long *>(hit), h->hit, (cudaStream_t)cuda_stream);
 }
 
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
   if (!h || !info) return fail(h, DCOPF_EINVAL, "null argument");
   memset(info, 0, sizeof *info);
+  if (h->pt) {
+    ptdf_info(h->pt, info);
+    return DCOPF_OK;
+  }
   info->B = h->B;
   info->B_padded = h->B_pad;
   info->path = h->path;
@@ -1263,6 +1348,16 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
   }
   if (h->path != DCOPF_PATH_CLUSTER) info->cluster_size = 1;
   return DCOPF_OK;
+}
+
+int dcopf_dual_get_ptdf(dcopf_dual_t h, double *Ha, void *cuda_stream) {
+  if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
+  if (!h->pt) return fail(h, DCOPF_EINVAL, "dcopf_dual_get_ptdf needs the PTDF form");
+  if (!Ha) return fail(h, DCOPF_EINVAL, "Ha is NULL");
+  CK(h, cudaSetDevice(h->device));
+  std::string perr;
+  const int prc = ptdf_get_matrix(h->pt, Ha, (cudaStream_t)cuda_stream, &perr);
+  return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,1192 @@
+// ptdf.cu -- dense-PTDF form of the dual: the paper's Eq. 1
+// with one shared H_a for a batch of load scenarios, iterated
+// as two fp64 GEMMs per ascent step on the tensor cores (DMMA, mma.sync
+// m8n8k4 f64: sm_100a's fp64 tensor-core instruction; tcgen05 has no fp64
+// kind) with the inner minimisation, the dual value, the gradient and the
+// projected step fused into the GEMM epilogues.  See ptdf.h for the algebra.
+#include "ptdf.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <thread>
+#include <vector>
+
+#include "cluster.h"
+
+namespace dcopf {
+namespace {
+
+// ---------------------------------------------------------------------------
+// GEMM tiling: C[M][N] = A[M][K] B[K][N], A row-major (K contiguous), B
+// row-major (N = instances contiguous).  128 x 128 x 16 CTA tiles, 8 warps as
+// 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 DMMA m8n8k4 tiles, a 4-stage
+// cp.async pipeline, padded shared-memory rows (conflict-free fragment
+// loads: A stride 20 doubles, B stride 132 doubles).  M, N, K are padded to
+// the tile sizes with zeros by the owner of each matrix.
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, NTHR = 256;
+constexpr int AST = BK + 4, BST = BN + 4;
+constexpr int A_STAGE = BM * AST, B_STAGE = BK * BST;  // doubles
+constexpr int GEMM_SMEM = STAGES * (A_STAGE + B_STAGE) * 8;
+
+enum { EPI_STORE = 0, EPI_GEN = 1, EPI_LINE_STEP = 2, EPI_LINE_EVAL = 3 };
+
+inline long up(long x, long m) { return (x + m - 1) / m * m; }
+
+struct GemmArgs {
+  const double *A;
+  long lda;
+  const double *Bm;
+  long ldb;
+  int M, N, K, group;
+  long ld;  // leading dimension of every [rows][B_pad] array (= B_pad) / of C for EPI_STORE
+  double *C;
+  // EPI_GEN (rows = generators)
+  const double *gc, *glo, *ghi, *ga;
+  int ng;
+  const double *lam;
+  double *P, *part_obj, *part_p;
+  // EPI_LINE (rows = lines)
+  const double *r, *F;
+  int nl;
+  double *mup, *mum, *nu, *part_line, *gp_out, *gm_out;
+  const int *status;
+  const double *alpha;
+  int k;
+  int opt;
+  double rho, beta1, beta2, eps, b1t, b2t;
+  double *s1p, *s2p, *s1m, *s2m;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double opt_step(const GemmArgs &g, double y, double gr, double al, double &s1,
+                                           double &s2) {
+  switch (g.opt) {
+    case 1: {  // GDM (Algorithm 1 as printed: velocity update, then gradient update; reading A-25)
+      const double v = g.rho * s1 + al * gr;
+      s1 = v;
+      y = y + v;
+      return y + al * gr;
+    }
+    case 2: {  // GDM-classic
+      const double v = g.rho * s1 + al * gr;
+      s1 = v;
+      return y + v;
+    }
+    case 3: {  // AdaGrad (reading A-26)
+      const double G = s1 + gr * gr;
+      s1 = G;
+      return y + (al * gr) / (sqrt(G) + g.eps);
+    }
+    case 4: {  // Adam (reading A-26)
+      const double m = g.beta1 * s1 + (1.0 - g.beta1) * gr;
+      const double v = g.beta2 * s2 + (1.0 - g.beta2) * (gr * gr);
+      s1 = m;
+      s2 = v;
+      const double mh = m / (1.0 - g.b1t), vh = v / (1.0 - g.b2t);
+      return y + (al * mh) / (sqrt(vh) + g.eps);
+    }
+    default:
+      return y + al * gr;
+  }
+}
+
+// one CTA per 128 x 128 output tile, grouped raster (`group` M-tiles per band,
+// M fastest inside a band) so concurrently running CTAs share A and B tiles in L2
+template <int EPI>
+__global__ void __launch_bounds__(NTHR, 1) k_dgemm(const GemmArgs g) {
+  extern __shared__ __align__(16) double sm[];
+  double *As = sm, *Bs = sm + STAGES * A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 2, wn = warp & 3;
+  const int nMt = g.M / BM, nNt = g.N / BN;
+  const int t = blockIdx.x, band = t / (g.group * nNt), first_m = band * g.group;
+  const int gs = min(nMt - first_m, g.group);
+  const int mt = first_m + (t % (g.group * nNt)) % gs, nt = (t % (g.group * nNt)) / gs;
+  const int m0 = mt * BM, n0 = nt * BN;
+  const int KT = g.K / BK;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double *as = As + stage * A_STAGE, *bs = Bs + stage * B_STAGE;
+#pragma unroll
+    for (int c = tid; c < BM * BK / 2; c += NTHR) {
+      const int row = c >> 3, ch = c & 7;
+      cp_async16(as + row * AST + ch * 2, g.A + (size_t)(m0 + row) * g.lda + k0 + ch * 2);
+    }
+#pragma unroll
+    for (int c = tid; c < BK * BN / 2; c += NTHR) {
+      const int row = c >> 6, ch = c & 63;
+      cp_async16(bs + row * BST + ch * 2, g.Bm + (size_t)(k0 + row) * g.ldb + n0 + ch * 2);
+    }
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();  // stage kt landed for every thread; stage kt-1 is free
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) load_stage(nk % STAGES, nk);
+    cp_async_commit();
+    const double *as = As + (kt % STAGES) * A_STAGE + (wm * 64 + (lane >> 2)) * AST + (lane & 3);
+    const double *bs = Bs + (kt % STAGES) * B_STAGE + (lane & 3) * BST + wn * 32 + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = as[i * 8 * AST + kk * 4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[kk * 4 * BST + j * 8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // pipeline buffers are free: the epilogue reuses them
+
+  // fragment (i, j, e) <-> row m0 + wm*64 + i*8 + lane/4, column n0 + wn*32 + j*8 + 2*(lane%4) + e
+  const int rbase = m0 + wm * 64 + (lane >> 2);
+  const int cbase = n0 + wn * 32 + 2 * (lane & 3);
+  if (EPI == EPI_STORE) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<double2 *>(g.C + (size_t)(rbase + i * 8) * g.ld + cbase + j * 8) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
+    return;
+  }
+  double s0[4][2], s1[4][2];  // per-column partial sums over this thread's 8 rows
+#pragma unroll
+  for (int j = 0; j < 4; ++j) s0[j][0] = s0[j][1] = s1[j][0] = s1[j][1] = 0.0;
+
+  if (EPI == EPI_GEN) {
+    double lamv[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 l2 = *reinterpret_cast<const double2 *>(g.lam + cbase + j * 8);
+      lamv[j][0] = l2.x;
+      lamv[j][1] = l2.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = rbase + i * 8;
+      const bool live = row < g.ng;
+      const double c = live ? g.gc[row] : 0.0, lo = live ? g.glo[row] : 0.0, hi = live ? g.ghi[row] : 0.0;
+      const double a = (live && g.ga) ? g.ga[row] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double pv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double q = (c + lamv[j][e]) + acc[i][j][e];  // q = c + lambda 1 + H_g^T nu
+          double p;
+          if (a > 0.0) {  // clip(-q / 2a) (reading A-6)
+            const double x = -q / (2.0 * a);
+            p = (x < lo) ? lo : ((x > hi) ? hi : x);
+          } else {        // bound selection, sign(0) -> midpoint (reading A-4)
+            p = (q > 0.0) ? lo : ((q < 0.0) ? hi : 0.5 * (lo + hi));
+          }
+          if (!live) p = 0.0;
+          pv[e] = p;
+          if (live) {
+            s0[j][e] += a * p * p + q * p;
+            s1[j][e] += p;
+          }
+        }
+        *reinterpret_cast<double2 *>(g.P + (size_t)row * g.ld + cbase + j * 8) = make_double2(pv[0], pv[1]);
+      }
+    }
+  } else {  // EPI_LINE_*
+    const double al = (EPI == EPI_LINE_STEP) ? g.alpha[g.k] : 0.0;
+    bool frozen[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      frozen[j][0] = (EPI == EPI_LINE_STEP) ? g.status[cbase + j * 8] != 0 : true;
+      frozen[j][1] = (EPI == EPI_LINE_STEP) ? g.status[cbase + j * 8 + 1] != 0 : true;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = rbase + i * 8;
+      if (row >= g.nl) continue;
+      const double F = g.F[row];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const size_t o = (size_t)row * g.ld + cbase + j * 8;
+        const double2 r2 = *reinterpret_cast<const double2 *>(g.r + o);
+        const double2 p2 = *reinterpret_cast<const double2 *>(g.mup + o);
+        const double2 m2 = *reinterpret_cast<const double2 *>(g.mum + o);
+        const double rv[2] = {r2.x, r2.y}, mp[2] = {p2.x, p2.y}, mm[2] = {m2.x, m2.y};
+        double gp[2], gm[2], np[2], nm[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double y = acc[i][j][e];
+          gp[e] = (y - rv[e]) - F;  // dg/dmu+ = H_g p* - r - F
+          gm[e] = (rv[e] - y) - F;  // dg/dmu- = r - H_g p* - F
+          s0[j][e] += mm[e] * (rv[e] - F) - mp[e] * (rv[e] + F);
+          np[e] = mp[e];
+          nm[e] = mm[e];
+        }
+        if (EPI == EPI_LINE_EVAL) {
+          if (g.gp_out) {
+            *reinterpret_cast<double2 *>(g.gp_out + o) = make_double2(gp[0], gp[1]);
+            *reinterpret_cast<double2 *>(g.gm_out + o) = make_double2(gm[0], gm[1]);
+          }
+        } else {
+          if (g.opt == 0) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (!frozen[j][e]) {
+                const double vp = mp[e] + al * gp[e], vm = mm[e] + al * gm[e];
+                np[e] = vp > 0.0 ? vp : 0.0;  // mu <- max(mu, 0)
+                nm[e] = vm > 0.0 ? vm : 0.0;
+              }
+          } else {
+            double2 a1 = *reinterpret_cast<const double2 *>(g.s1p + o);
+            double2 a2 = g.s2p ? *reinterpret_cast<const double2 *>(g.s2p + o) : make_double2(0.0, 0.0);
+            double2 b1 = *reinterpret_cast<const double2 *>(g.s1m + o);
+            double2 b2 = g.s2m ? *reinterpret_cast<const double2 *>(g.s2m + o) : make_double2(0.0, 0.0);
+            double sa1[2] = {a1.x, a1.y}, sa2[2] = {a2.x, a2.y}, sb1[2] = {b1.x, b1.y}, sb2[2] = {b2.x, b2.y};
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (!frozen[j][e]) {
+                const double vp = opt_step(g, mp[e], gp[e], al, sa1[e], sa2[e]);
+                const double vm = opt_step(g, mm[e], gm[e], al, sb1[e], sb2[e]);
+                np[e] = vp > 0.0 ? vp : 0.0;
+                nm[e] = vm > 0.0 ? vm : 0.0;
+              }
+            *reinterpret_cast<double2 *>(g.s1p + o) = make_double2(sa1[0], sa1[1]);
+            *reinterpret_cast<double2 *>(g.s1m + o) = make_double2(sb1[0], sb1[1]);
+            if (g.s2p) {
+              *reinterpret_cast<double2 *>(g.s2p + o) = make_double2(sa2[0], sa2[1]);
+              *reinterpret_cast<double2 *>(g.s2m + o) = make_double2(sb2[0], sb2[1]);
+            }
+          }
+          *reinterpret_cast<double2 *>(g.mup + o) = make_double2(np[0], np[1]);
+          *reinterpret_cast<double2 *>(g.mum + o) = make_double2(nm[0], nm[1]);
+          *reinterpret_cast<double2 *>(g.nu + o) = make_double2(np[0] - nm[0], np[1] - nm[1]);
+        }
+      }
+    }
+  }
+  // column sums: lanes with the same lane%4 hold the same columns (xor over lane/4),
+  // then the two M-warps through shared memory, fixed order (deterministic)
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        s0[j][e] += __shfl_xor_sync(0xffffffffu, s0[j][e], off);
+        if (EPI == EPI_GEN) s1[j][e] += __shfl_xor_sync(0xffffffffu, s1[j][e], off);
+      }
+  double *red = sm;  // [2 sums][2 wm][BN]
+  if (lane < 4) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 32 + j * 8 + 2 * lane + e;
+        red[wm * BN + col] = s0[j][e];
+        if (EPI == EPI_GEN) red[2 * BN + wm * BN + col] = s1[j][e];
+      }
+  }
+  __syncthreads();
+  if (tid < BN) {
+    const size_t o = (size_t)mt * g.ld + n0 + tid;
+    if (EPI == EPI_GEN) {
+      g.part_obj[o] = red[tid] + red[BN + tid];
+      g.part_p[o] = red[2 * BN + tid] + red[3 * BN + tid];
+    } else {
+      g.part_line[o] = red[tid] + red[BN + tid];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per instance: the dual value, grad lambda, bookkeeping and the lambda step
+struct FinArgs {
+  const double *part_obj, *part_p, *part_line;
+  int nMt1, nMt2;
+  long ld, B;
+  const double *D;
+  double *lam, *sl1, *sl2;
+  int *status;
+  double *best, *bound, *value, *gprev, *hist, *glam_out;
+  const double *alpha, *target;
+  long long *hit;
+  long long k_base;
+  int k, K, first;
+  double tol;
+  int opt;
+  double rho, beta1, beta2, eps, b1t, b2t;
+};
+
+__device__ __forceinline__ bool valid_bound(double g) { return isfinite(g) && fabs(g) <= 1e15; }
+
+template <bool EVAL>
+__global__ void k_finish(const FinArgs f) {
+  const long n = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= f.ld) return;
+  double so = 0.0, sp = 0.0, sl = 0.0;
+  for (int t = 0; t < f.nMt1; ++t) {
+    so += f.part_obj[(size_t)t * f.ld + n];
+    sp += f.part_p[(size_t)t * f.ld + n];
+  }
+  for (int t = 0; t < f.nMt2; ++t) sl += f.part_line[(size_t)t * f.ld + n];
+  const double lam = f.lam[n], D = f.D[n];
+  const double g = (so - lam * D) + sl;
+  const double gl = sp - D;  // dg/dlambda = 1^T p* - 1^T d
+  if (EVAL) {
+    f.value[n] = g;
+    if (f.glam_out) f.glam_out[n] = gl;
+    return;
+  }
+  if (f.hist && f.k < f.K && n < f.B) f.hist[(size_t)f.k * f.B + n] = g;
+  if (f.k == f.K) f.bound[n] = g;
+  int st = f.status[n];
+  const bool was = st != 0;
+  double best = f.best[n];
+  if (!was) {
+    if (valid_bound(g)) {
+      if (g > best) best = g;
+      if (f.tol > 0.0 && !f.first && fabs(g - f.gprev[n]) < f.tol) st = DCOPF_INST_CONVERGED;  // Alg. 1 stop
+    } else {
+      st = DCOPF_INST_DIVERGED;
+    }
+  }
+  f.gprev[n] = g;
+  f.best[n] = best;
+  f.status[n] = st;
+  if (f.target && f.hit[n] < 0 && best >= f.target[n]) f.hit[n] = f.k_base + f.k;
+  if (f.k < f.K && !was) {
+    const double al = f.alpha[f.k];
+    double s1 = f.sl1 ? f.sl1[n] : 0.0, s2 = f.sl2 ? f.sl2[n] : 0.0;
+    GemmArgs o;
+    o.opt = f.opt;
+    o.rho = f.rho;
+    o.beta1 = f.beta1;
+    o.beta2 = f.beta2;
+    o.eps = f.eps;
+    o.b1t = f.b1t;
+    o.b2t = f.b2t;
+    f.lam[n] = opt_step(o, lam, gl, al, s1, s2);  // lambda free: no projection
+    if (f.sl1) f.sl1[n] = s1;
+    if (f.sl2) f.sl2[n] = s2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// construction kernels (tree flows, cycle sums, H_a assembly, generator columns)
+struct TreeDev {
+  const int *tin, *tout;   // DFS entry / exit times per bus
+  const int *child;        // per branch: the deeper endpoint of a tree branch, -1 otherwise
+  const double *sig;       // per branch: +1 if the flow child -> parent runs from -> to, else -1
+};
+
+__device__ __forceinline__ double tflow(const TreeDev &T, const int *tin_bus, int l, int i) {
+  const int c = T.child[l];
+  if (c < 0) return 0.0;
+  const int ti = tin_bus[i];
+  return (T.tin[c] <= ti && ti < T.tout[c]) ? T.sig[l] : 0.0;
+}
+
+// S[k][i] = sum_{l in cycle k} C_kl x_l T[l][i]
+__global__ void k_cycle_tree(TreeDev T, const int *cp, const int *cb, const double *cs, const double *x, int nc,
+                             int nb, double *S, long lds) {
+  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (long)nc * nb) return;
+  const int k = (int)(id / nb), i = (int)(id % nb);
+  double s = 0.0;
+  for (int e = cp[k]; e < cp[k + 1]; ++e) {
+    const int l = cb[e];
+    s += cs[e] * x[l] * tflow(T, T.tin, l, i);
+  }
+  S[(size_t)k * lds + i] = s;
+}
+
+// H_a[l][i] = T[l][i] - sum_{k containing l} C_kl W[k][i]  (0 for an open branch, b = 0)
+__global__ void k_assemble(TreeDev T, const int *bp, const int *bk, const double *bs, const double *W, long ldw,
+                           const double *b, int nl, int nb, double *Ha, long ldh) {
+  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (long)nl * nb) return;
+  const int l = (int)(id / nb), i = (int)(id % nb);
+  double h = 0.0;
+  if (b[l] > 0.0) {
+    h = tflow(T, T.tin, l, i);
+    for (int e = bp[l]; e < bp[l + 1]; ++e) h -= bs[e] * W[(size_t)bk[e] * ldw + i];
+  }
+  Ha[(size_t)l * ldh + i] = h;
+}
+
+// HgT[g][l] = Hg[l][g] = H_a[l][bus(g)]
+__global__ void k_gen_cols(const double *Ha, long ldh, const int *gbus, int ng, int nl, double *HgT, long ldt,
+                           double *Hg, long ldg) {
+  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (long)ng * nl) return;
+  const int g = (int)(id / nl), l = (int)(id % nl);
+  const double v = Ha[(size_t)l * ldh + gbus[g]];
+  HgT[(size_t)g * ldt + l] = v;
+  Hg[(size_t)l * ldg + g] = v;
+}
+
+__global__ void k_colsum(const double *Dm, int nb, long ld, double *D) {
+  const long n = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= ld) return;
+  double s = 0.0;
+  for (int i = 0; i < nb; ++i) s += Dm[(size_t)i * ld + n];  // 1^T d, ascending bus
+  D[n] = s;
+}
+
+__global__ void k_fill(double *p, double v, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_sub(const double *a, const double *b, double *c, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    c[i] = a[i] - b[i];
+}
+
+// set_multipliers validation: finite, and mu >= 0 where `nonneg`
+__global__ void k_check(const double *p, size_t rows, long ld, long B, int nonneg, int *flag) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * B; i += (size_t)gridDim.x * blockDim.x) {
+    const double v = p[(i / B) * ld + i % B];
+    if (!isfinite(v) || (nonneg && v < 0.0)) *flag = 1;
+  }
+}
+
+int blocks_for(size_t n) { return (int)std::min<size_t>(std::max<size_t>((n + 255) / 256, 1), 148 * 64); }
+
+}  // namespace
+
+// ===========================================================================
+struct PtdfState {
+  int device = 0, nb = 0, nl = 0, ng = 0, nc = 0;
+  long nlp = 0, nlk = 0, ngp = 0, ngk = 0, nbk = 0;  // padded sizes (M: 128, K: 16)
+  int quadratic = 0;
+  int group = 8;
+  // network (device)
+  double *Ha = nullptr, *HgT = nullptr, *Hg = nullptr, *F = nullptr, *gc = nullptr, *glo = nullptr, *ghi = nullptr,
+         *ga = nullptr;
+  // batch
+  long B = 0, Bp = 0;
+  double *r = nullptr, *D = nullptr, *lam = nullptr, *mup = nullptr, *mum = nullptr, *nu = nullptr, *P = nullptr;
+  double *part_obj = nullptr, *part_p = nullptr, *part_line = nullptr;
+  double *best = nullptr, *bound = nullptr, *value = nullptr, *gprev = nullptr, *target = nullptr;
+  double *gp = nullptr, *gm = nullptr, *glam = nullptr;
+  int *status = nullptr, *flag = nullptr;
+  long long *hit = nullptr;
+  bool has_target = false;
+  long long k_base = 0;
+  double tol = 0.0;
+  dcopf_optimizer opt = {DCOPF_OPT_PLAIN, 0, 0.0, 0.0, 0.0, 0.0};
+  double b1t = 1.0, b2t = 1.0;
+  double *os[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // s1p s2p s1m s2m sl1 sl2
+  double *scratch = nullptr;
+  size_t scratch_bytes = 0;
+};
+
+namespace {
+
+#define PCK(call)                                                                                           \
+  do {                                                                                                      \
+    cudaError_t e_ = (call);                                                                                \
+    if (e_ != cudaSuccess) {                                                                                \
+      *err = std::string(#call) + " failed: " + cudaGetErrorString(e_);                                     \
+      return e_ == cudaErrorMemoryAllocation ? DCOPF_ENOMEM : DCOPF_ECUDA;                                  \
+    }                                                                                                       \
+  } while (0)
+
+int dalloc(double **p, size_t n, std::string *err) {
+  cudaFree(*p);
+  *p = nullptr;
+  PCK(cudaMalloc(p, std::max<size_t>(n, 1) * 8));
+  PCK(cudaMemset(*p, 0, std::max<size_t>(n, 1) * 8));
+  return DCOPF_OK;
+}
+
+bool is_dev(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <int EPI>
+int launch_gemm(const GemmArgs &g, cudaStream_t s, std::string *err) {
+  if (g.M == 0 || g.N == 0) return DCOPF_OK;
+  const int tiles = (g.M / BM) * (g.N / BN);
+  k_dgemm<EPI><<<tiles, NTHR, GEMM_SMEM, s>>>(g);
+  PCK(cudaGetLastError());
+  return DCOPF_OK;
+}
+
+int set_gemm_attrs(std::string *err) {
+  PCK(cudaFuncSetAttribute(k_dgemm<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+  PCK(cudaFuncSetAttribute(k_dgemm<EPI_GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+  PCK(cudaFuncSetAttribute(k_dgemm<EPI_LINE_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+  PCK(cudaFuncSetAttribute(k_dgemm<EPI_LINE_EVAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+  return DCOPF_OK;
+}
+
+GemmArgs plain_gemm(const double *A, long lda, const double *Bm, long ldb, double *C, long ldc, long M, long N,
+                    long K, int group) {
+  GemmArgs g;
+  memset(&g, 0, sizeof g);
+  g.A = A;
+  g.lda = lda;
+  g.Bm = Bm;
+  g.ldb = ldb;
+  g.C = C;
+  g.ld = ldc;
+  g.M = (int)M;
+  g.N = (int)N;
+  g.K = (int)K;
+  g.group = group;
+  return g;
+}
+
+// Host: Cholesky M = L L^T (row-major lower) and X = L^{-1}; returns false if not SPD.
+bool chol_inverse(std::vector<double> &M, int n, std::vector<double> *Linv) {
+  for (int j = 0; j < n; ++j) {
+    double *Lj = &M[(size_t)j * n];
+    for (int i = j; i < n; ++i) {
+      double *Li = &M[(size_t)i * n];
+      double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      int k = 0;
+      for (; k + 4 <= j; k += 4) {
+        s0 += Li[k] * Lj[k];
+        s1 += Li[k + 1] * Lj[k + 1];
+        s2 += Li[k + 2] * Lj[k + 2];
+        s3 += Li[k + 3] * Lj[k + 3];
+      }
+      for (; k < j; ++k) s0 += Li[k] * Lj[k];
+      const double v = Li[j] - ((s0 + s1) + (s2 + s3));
+      if (i == j) {
+        if (!(v > 0.0)) return false;
+        Lj[j] = std::sqrt(v);
+      } else {
+        Li[j] = v / Lj[j];
+      }
+    }
+  }
+  // L^{-1}: column j solves L x = e_j; columns are independent (threads)
+  Linv->assign((size_t)n * n, 0.0);
+  std::vector<double> &X = *Linv;
+  const int nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  auto work = [&](int t0) {
+    std::vector<double> x(n);
+    for (int j = t0; j < n; j += nt) {
+      x[j] = 1.0 / M[(size_t)j * n + j];
+      for (int i = j + 1; i < n; ++i) {
+        const double *Li = &M[(size_t)i * n];
+        double s = 0.0;
+        for (int k = j; k < i; ++k) s += Li[k] * x[k];
+        x[i] = -s / Li[i];
+      }
+      for (int i = j; i < n; ++i) X[(size_t)i * n + j] = x[i];
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) th.emplace_back(work, t);
+  for (auto &t : th) t.join();
+  return true;
+}
+
+int ensure_scratch(PtdfState *st, size_t bytes, std::string *err) {
+  if (st->scratch_bytes >= bytes) return DCOPF_OK;
+  cudaFree(st->scratch);
+  st->scratch = nullptr;
+  st->scratch_bytes = 0;
+  PCK(cudaMalloc(&st->scratch, bytes));
+  st->scratch_bytes = bytes;
+  return DCOPF_OK;
+}
+
+void free_batch(PtdfState *st) {
+  double **dp[] = {&st->r,     &st->D,      &st->lam,    &st->mup,   &st->mum,   &st->nu,     &st->P,
+                   &st->part_obj, &st->part_p, &st->part_line, &st->best, &st->bound, &st->value, &st->gprev,
+                   &st->target, &st->gp,    &st->gm,     &st->glam,  &st->os[0], &st->os[1], &st->os[2],
+                   &st->os[3],  &st->os[4], &st->os[5]};
+  for (double **p : dp) {
+    cudaFree(*p);
+    *p = nullptr;
+  }
+  cudaFree(st->status);
+  cudaFree(st->hit);
+  st->status = nullptr;
+  st->hit = nullptr;
+  st->B = st->Bp = 0;
+}
+
+int nstate(const dcopf_optimizer &o) {
+  return o.variant == DCOPF_OPT_ADAM ? 2 : (o.variant == DCOPF_OPT_PLAIN ? 0 : 1);
+}
+
+int reset_opt(PtdfState *st, std::string *err) {
+  for (double *&p : st->os) {
+    cudaFree(p);
+    p = nullptr;
+  }
+  st->b1t = st->b2t = 1.0;
+  const int ns = nstate(st->opt);
+  if (st->Bp == 0 || ns == 0) return DCOPF_OK;
+  const size_t nm = (size_t)st->nlp * st->Bp;
+  int rc = dalloc(&st->os[0], nm, err);
+  if (!rc) rc = dalloc(&st->os[2], nm, err);
+  if (!rc) rc = dalloc(&st->os[4], st->Bp, err);
+  if (!rc && ns == 2) rc = dalloc(&st->os[1], nm, err);
+  if (!rc && ns == 2) rc = dalloc(&st->os[3], nm, err);
+  if (!rc && ns == 2) rc = dalloc(&st->os[5], st->Bp, err);
+  return rc;
+}
+
+GemmArgs gen_args(PtdfState *st) {
+  GemmArgs g = plain_gemm(st->HgT, st->nlk, st->nu, st->Bp, nullptr, st->Bp, st->ngp, st->Bp, st->nlk, st->group);
+  g.gc = st->gc;
+  g.glo = st->glo;
+  g.ghi = st->ghi;
+  g.ga = st->quadratic ? st->ga : nullptr;
+  g.ng = st->ng;
+  g.lam = st->lam;
+  g.P = st->P;
+  g.part_obj = st->part_obj;
+  g.part_p = st->part_p;
+  return g;
+}
+
+GemmArgs line_args(PtdfState *st) {
+  GemmArgs g = plain_gemm(st->Hg, st->ngk, st->P, st->Bp, nullptr, st->Bp, st->nlp, st->Bp, st->ngk, st->group);
+  g.r = st->r;
+  g.F = st->F;
+  g.nl = st->nl;
+  g.mup = st->mup;
+  g.mum = st->mum;
+  g.nu = st->nu;
+  g.part_line = st->part_line;
+  g.status = st->status;
+  g.opt = st->opt.variant;
+  g.rho = st->opt.momentum;
+  g.beta1 = st->opt.beta1;
+  g.beta2 = st->opt.beta2;
+  g.eps = st->opt.epsilon;
+  g.s1p = st->os[0];
+  g.s2p = st->os[1];
+  g.s1m = st->os[2];
+  g.s2m = st->os[3];
+  return g;
+}
+
+FinArgs fin_args(PtdfState *st) {
+  FinArgs f;
+  memset(&f, 0, sizeof f);
+  f.part_obj = st->part_obj;
+  f.part_p = st->part_p;
+  f.part_line = st->part_line;
+  f.nMt1 = (int)(st->ngp / BM);
+  f.nMt2 = (int)(st->nlp / BM);
+  f.ld = st->Bp;
+  f.B = st->B;
+  f.D = st->D;
+  f.lam = st->lam;
+  f.sl1 = st->os[4];
+  f.sl2 = st->os[5];
+  f.status = st->status;
+  f.best = st->best;
+  f.bound = st->bound;
+  f.value = st->value;
+  f.gprev = st->gprev;
+  f.opt = st->opt.variant;
+  f.rho = st->opt.momentum;
+  f.beta1 = st->opt.beta1;
+  f.beta2 = st->opt.beta2;
+  f.eps = st->opt.epsilon;
+  f.tol = st->tol;
+  return f;
+}
+
+// rows x B (ld Bp, device) <-> rows x B (ld B, host or device)
+int copy_rows_out(PtdfState *st, double *dst, const double *src, long rows, cudaStream_t s, std::string *err) {
+  if (!dst || rows == 0) return DCOPF_OK;
+  PCK(cudaMemcpy2DAsync(dst, st->B * 8, src, st->Bp * 8, st->B * 8, rows, cudaMemcpyDefault, s));
+  if (!is_dev(dst)) PCK(cudaStreamSynchronize(s));
+  return DCOPF_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+int ptdf_create(const PtdfNetIn &net, int device, PtdfState **out, std::string *err) {
+  *out = nullptr;
+  CycleBasis cb;
+  std::string e = build_cycle_basis(net.nb, net.nl, net.ref, net.fr, net.to, net.b, nullptr, &cb);
+  if (!e.empty()) {
+    *err = e;
+    return DCOPF_ETOPOLOGY;
+  }
+  PtdfState *st = new PtdfState();
+  st->device = device;
+  st->nb = net.nb;
+  st->nl = net.nl;
+  st->ng = net.ng;
+  if (net.a)
+    for (int g = 0; g < net.ng; ++g) st->quadratic |= net.a[g] > 0.0;
+  if (const char *ev = getenv("DCOPF_PTDF_GROUP")) st->group = std::max(1, atoi(ev));
+  st->nlp = up(net.nl, BM);
+  st->nlk = up(net.nl, BK);
+  st->ngp = up(net.ng, BM);
+  st->ngk = up(net.ng, BK);
+  st->nbk = up(net.nb, BK);
+  auto fail = [&](int rc) {
+    ptdf_destroy(st);
+    return rc;
+  };
+
+  // ---- tree: parent / child per branch, DFS times ----
+  const int nb = net.nb, nl = net.nl;
+  std::vector<std::vector<int>> adj(nb);
+  for (int l = 0; l < nl; ++l)
+    if (cb.is_tree[l]) {
+      adj[net.fr[l]].push_back(l);
+      adj[net.to[l]].push_back(l);
+    }
+  std::vector<int> tin(nb, 0), tout(nb, 0), child(nl, -1);
+  std::vector<double> sig(nl, 0.0);
+  {
+    std::vector<int> parent(nb, -1), it(nb, 0), stack{net.ref};
+    std::vector<char> seen(nb, 0);
+    seen[net.ref] = 1;
+    int clock = 0;
+    tin[net.ref] = clock++;
+    while (!stack.empty()) {
+      const int u = stack.back();
+      if (it[u] < (int)adj[u].size()) {
+        const int l = adj[u][it[u]++];
+        const int v = net.fr[l] == u ? net.to[l] : net.fr[l];
+        if (seen[v]) continue;
+        seen[v] = 1;
+        parent[v] = u;
+        child[l] = v;
+        sig[l] = (net.fr[l] == v) ? 1.0 : -1.0;  // flow v -> u (towards the slack) runs from -> to?
+        tin[v] = clock++;
+        stack.push_back(v);
+      } else {
+        tout[u] = clock;
+        stack.pop_back();
+      }
+    }
+  }
+  // ---- cycles of the branches with b > 0 (the others carry no flow) ----
+  std::vector<int> ccp{0}, ccb;
+  std::vector<double> ccs;
+  for (int k = 0; k < cb.nc; ++k) {
+    if (!(net.b[cb.def[k]] > 0.0)) continue;
+    for (int x = cb.cp[k]; x < cb.cp[k + 1]; ++x) {
+      ccb.push_back(cb.cb[x]);
+      ccs.push_back((double)cb.cs[x]);
+    }
+    ccp.push_back((int)ccb.size());
+  }
+  const int nc = (int)ccp.size() - 1;
+  st->nc = nc;
+  std::vector<double> x(nl, 0.0);
+  for (int l = 0; l < nl; ++l) x[l] = net.b[l] > 0.0 ? 1.0 / net.b[l] : 0.0;
+  // branch -> (cycle, sign) lists, ascending cycle
+  std::vector<int> bp(nl + 1, 0), bk;
+  std::vector<double> bsg;
+  {
+    std::vector<std::vector<std::pair<int, double>>> per(nl);
+    for (int k = 0; k < nc; ++k)
+      for (int q = ccp[k]; q < ccp[k + 1]; ++q) per[ccb[q]].push_back({k, ccs[q]});
+    for (int l = 0; l < nl; ++l) {
+      for (auto &pr : per[l]) {
+        bk.push_back(pr.first);
+        bsg.push_back(pr.second);
+      }
+      bp[l + 1] = (int)bk.size();
+    }
+  }
+  // ---- M = C X C^T, Cholesky, L^{-1} (host) ----
+  std::vector<double> Linv;
+  if (nc > 0) {
+    std::vector<double> M((size_t)nc * nc, 0.0);
+    for (int l = 0; l < nl; ++l)
+      for (int u = bp[l]; u < bp[l + 1]; ++u)
+        for (int v = bp[l]; v < bp[l + 1]; ++v)
+          M[(size_t)bk[u] * nc + bk[v]] += bsg[u] * bsg[v] * x[l];
+    if (!chol_inverse(M, nc, &Linv)) {
+      *err = "PTDF: the cycle matrix C X C^T is not positive definite";
+      return fail(DCOPF_EINVAL);
+    }
+  }
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) {
+    *err = std::string("cudaSetDevice: ") + cudaGetErrorString(ce);
+    return fail(DCOPF_ECUDA);
+  }
+  if (int arc = set_gemm_attrs(err)) return fail(arc);
+  // ---- device: S = C X T, W = L^{-T} (L^{-1} S), H_a = T - C^T W ----
+  int *d_tin = nullptr, *d_tout = nullptr, *d_child = nullptr, *d_cp = nullptr, *d_cb = nullptr, *d_bp = nullptr,
+      *d_bk = nullptr, *d_gbus = nullptr;
+  double *d_sig = nullptr, *d_cs = nullptr, *d_x = nullptr, *d_bs = nullptr, *d_b = nullptr, *d_S = nullptr,
+         *d_V = nullptr, *d_W = nullptr, *d_L = nullptr, *d_LT = nullptr;
+  int rc = DCOPF_OK;
+  auto upi = [&](int **d, const std::vector<int> &v) {
+    if (rc) return;
+    if (cudaMalloc(d, std::max<size_t>(v.size(), 1) * 4) != cudaSuccess ||
+        (!v.empty() && cudaMemcpy(*d, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)) {
+      *err = "PTDF: device upload failed";
+      rc = DCOPF_ENOMEM;
+    }
+  };
+  auto upd = [&](double **d, const std::vector<double> &v) {
+    if (rc) return;
+    if (cudaMalloc(d, std::max<size_t>(v.size(), 1) * 8) != cudaSuccess ||
+        (!v.empty() && cudaMemcpy(*d, v.data(), v.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)) {
+      *err = "PTDF: device upload failed";
+      rc = DCOPF_ENOMEM;
+    }
+  };
+  std::vector<int> gbus(net.gen_bus, net.gen_bus + net.ng);
+  upi(&d_tin, tin);
+  upi(&d_tout, tout);
+  upi(&d_child, child);
+  upi(&d_cp, ccp);
+  upi(&d_cb, ccb);
+  upi(&d_bp, bp);
+  upi(&d_bk, bk);
+  upi(&d_gbus, gbus);
+  upd(&d_sig, sig);
+  upd(&d_cs, ccs);
+  upd(&d_x, x);
+  upd(&d_bs, bsg);
+  upd(&d_b, std::vector<double>(net.b, net.b + nl));
+  const long ncp = up(std::max(nc, 1), BM), nck = up(std::max(nc, 1), BK), nbN = up(nb, BN);
+  if (!rc) rc = dalloc(&st->Ha, (size_t)st->nlp * st->nbk, err);
+  if (!rc) rc = dalloc(&d_W, (size_t)ncp * nbN, err);
+  TreeDev T{d_tin, d_tout, d_child, d_sig};
+  if (!rc && nc > 0) {
+    rc = dalloc(&d_S, (size_t)ncp * nbN, err);
+    if (!rc) rc = dalloc(&d_V, (size_t)ncp * nbN, err);
+    std::vector<double> Lp((size_t)ncp * nck, 0.0), LTp((size_t)ncp * nck, 0.0);
+    for (int i = 0; i < nc; ++i)
+      for (int j = 0; j < nc; ++j) {
+        Lp[(size_t)i * nck + j] = Linv[(size_t)i * nc + j];
+        LTp[(size_t)i * nck + j] = Linv[(size_t)j * nc + i];
+      }
+    upd(&d_L, Lp);
+    upd(&d_LT, LTp);
+    if (!rc) {
+      k_cycle_tree<<<blocks_for((size_t)nc * nb), 256>>>(T, d_cp, d_cb, d_cs, d_x, nc, nb, d_S, nbN);
+      rc = launch_gemm<EPI_STORE>(plain_gemm(d_L, nck, d_S, nbN, d_V, nbN, ncp, nbN, nck, st->group), nullptr, err);
+    }
+    // the rows of V beyond nc are zero (zero rows of L^{-1}); K of the second product is nck
+    if (!rc)
+      rc = launch_gemm<EPI_STORE>(plain_gemm(d_LT, nck, d_V, nbN, d_W, nbN, ncp, nbN, nck, st->group), nullptr, err);
+  }
+  if (!rc) {
+    k_assemble<<<blocks_for((size_t)nl * nb), 256>>>(T, d_bp, d_bk, d_bs, d_W, nbN, d_b, nl, nb, st->Ha, st->nbk);
+    if (!rc) rc = dalloc(&st->HgT, (size_t)st->ngp * st->nlk, err);
+    if (!rc) rc = dalloc(&st->Hg, (size_t)st->nlp * st->ngk, err);
+    if (!rc)
+      k_gen_cols<<<blocks_for((size_t)net.ng * nl), 256>>>(st->Ha, st->nbk, d_gbus, net.ng, nl, st->HgT, st->nlk,
+                                                           st->Hg, st->ngk);
+    ce = cudaDeviceSynchronize();
+    if (!rc && ce != cudaSuccess) {
+      *err = std::string("PTDF construction: ") + cudaGetErrorString(ce);
+      rc = DCOPF_ECUDA;
+    }
+  }
+  int *ip[] = {d_tin, d_tout, d_child, d_cp, d_cb, d_bp, d_bk, d_gbus};
+  for (int *p : ip) cudaFree(p);
+  double *dp[] = {d_sig, d_cs, d_x, d_bs, d_b, d_S, d_V, d_W, d_L, d_LT};
+  for (double *p : dp) cudaFree(p);
+  if (rc) return fail(rc);
+  // ---- generators and limits ----
+  auto padv = [&](const double *src, int n, long np) {
+    std::vector<double> v(np, 0.0);
+    if (src) std::copy(src, src + n, v.begin());
+    return v;
+  };
+  upd(&st->F, padv(net.F, nl, st->nlp));
+  upd(&st->gc, padv(net.c, net.ng, st->ngp));
+  upd(&st->glo, padv(net.lo, net.ng, st->ngp));
+  upd(&st->ghi, padv(net.hi, net.ng, st->ngp));
+  upd(&st->ga, padv(net.a, net.ng, st->ngp));
+  if (rc) return fail(rc);
+  ce = cudaMalloc(&st->flag, sizeof(int));
+  if (ce != cudaSuccess) {
+    *err = "cudaMalloc failed";
+    return fail(DCOPF_ENOMEM);
+  }
+  *out = st;
+  return DCOPF_OK;
+}
+
+void ptdf_destroy(PtdfState *st) {
+  if (!st) return;
+  cudaSetDevice(st->device);
+  free_batch(st);
+  double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch};
+  for (double *p : dp) cudaFree(p);
+  cudaFree(st->flag);
+  delete st;
+}
+
+int64_t ptdf_batch(const PtdfState *st) { return st->B; }
+
+int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s, std::string *err) {
+  const long Bp = up(B, BN);
+  const bool reuse = st->B > 0 && st->Bp == Bp;
+  if (!reuse) {
+    free_batch(st);
+    const size_t nm = (size_t)st->nlp * Bp;
+    int rc = DCOPF_OK;
+    double **rows_l[] = {&st->r, &st->mup, &st->mum, &st->nu};
+    for (double **p : rows_l)
+      if (!rc) rc = dalloc(p, nm, err);
+    if (!rc) rc = dalloc(&st->P, (size_t)st->ngp * Bp, err);
+    if (!rc) rc = dalloc(&st->part_obj, (size_t)(st->ngp / BM) * Bp, err);
+    if (!rc) rc = dalloc(&st->part_p, (size_t)(st->ngp / BM) * Bp, err);
+    if (!rc) rc = dalloc(&st->part_line, (size_t)(st->nlp / BM) * Bp, err);
+    double **vec[] = {&st->D, &st->lam, &st->best, &st->bound, &st->value, &st->gprev, &st->target, &st->glam};
+    for (double **p : vec)
+      if (!rc) rc = dalloc(p, Bp, err);
+    if (rc) return rc;
+    PCK(cudaMalloc(&st->status, Bp * 4));
+    PCK(cudaMalloc(&st->hit, Bp * 8));
+  }
+  st->B = B;
+  st->Bp = Bp;
+  // loads: [n_bus][B] -> Dm [nbk][Bp] (zero padded), r = H_a Dm, D = 1^T d
+  const size_t dm = (size_t)st->nbk * Bp;
+  int rc = ensure_scratch(st, dm * 8, err);
+  if (rc) return rc;
+  PCK(cudaMemsetAsync(st->scratch, 0, dm * 8, s));
+  PCK(cudaMemcpy2DAsync(st->scratch, Bp * 8, load, B * 8, B * 8, st->nb, cudaMemcpyDefault, s));
+  rc = launch_gemm<EPI_STORE>(plain_gemm(st->Ha, st->nbk, st->scratch, Bp, st->r, Bp, st->nlp, Bp, st->nbk, st->group),
+                              s, err);
+  if (rc) return rc;
+  k_colsum<<<blocks_for(Bp), 256, 0, s>>>(st->scratch, st->nb, Bp, st->D);
+  const size_t nm = (size_t)st->nlp * Bp;
+  k_fill<<<blocks_for(nm), 256, 0, s>>>(st->mup, 0.0, nm);
+  k_fill<<<blocks_for(nm), 256, 0, s>>>(st->mum, 0.0, nm);
+  k_fill<<<blocks_for(nm), 256, 0, s>>>(st->nu, 0.0, nm);
+  k_fill<<<blocks_for(Bp), 256, 0, s>>>(st->lam, 0.0, Bp);
+  k_fill<<<blocks_for(Bp), 256, 0, s>>>(st->best, -std::numeric_limits<double>::infinity(), Bp);
+  k_fill<<<blocks_for(Bp), 256, 0, s>>>(st->bound, std::numeric_limits<double>::quiet_NaN(), Bp);
+  PCK(cudaMemsetAsync(st->status, 0, Bp * 4, s));
+  PCK(cudaMemsetAsync(st->hit, 0xff, Bp * 8, s));
+  PCK(cudaGetLastError());
+  st->has_target = false;
+  st->k_base = 0;
+  PCK(cudaStreamSynchronize(s));  // the load scratch is reused by the next call
+  return reset_opt(st, err);
+}
+
+int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist, cudaStream_t s, std::string *err) {
+  GemmArgs g1 = gen_args(st), g2 = line_args(st);
+  g2.alpha = alpha_dev;
+  FinArgs f = fin_args(st);
+  f.alpha = alpha_dev;
+  f.hist = hist;
+  f.K = (int)K;
+  f.k_base = st->k_base;
+  f.target = st->has_target ? st->target : nullptr;
+  f.hit = st->hit;
+  const int fb = blocks_for(st->Bp);
+  for (int64_t k = 0; k <= K; ++k) {
+    int rc = launch_gemm<EPI_GEN>(g1, s, err);
+    if (rc) return rc;
+    const bool step = k < K;
+    if (step && st->opt.variant == DCOPF_OPT_ADAM) {  // beta^t by repeated products (reading A-26)
+      st->b1t = st->b1t * st->opt.beta1;
+      st->b2t = st->b2t * st->opt.beta2;
+    }
+    g2.k = (int)k;
+    g2.b1t = f.b1t = st->b1t;
+    g2.b2t = f.b2t = st->b2t;
+    if (step) {
+      rc = launch_gemm<EPI_LINE_STEP>(g2, s, err);
+    } else {  // the final evaluation at y_K: the value's line terms only, no step
+      rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
+    }
+    if (rc) return rc;
+    f.k = (int)k;
+    f.first = k == 0;
+    k_finish<false><<<fb, 256, 0, s>>>(f);
+    PCK(cudaGetLastError());
+  }
+  st->k_base += K;
+  return DCOPF_OK;
+}
+
+int ptdf_get_bound(PtdfState *st, double *bound, double *best, int32_t *status, cudaStream_t s, std::string *err) {
+  const size_t n = st->B;
+  if (bound) PCK(cudaMemcpyAsync(bound, st->bound, n * 8, cudaMemcpyDefault, s));
+  if (best) PCK(cudaMemcpyAsync(best, st->best, n * 8, cudaMemcpyDefault, s));
+  if (status) PCK(cudaMemcpyAsync(status, st->status, n * 4, cudaMemcpyDefault, s));
+  if ((bound && !is_dev(bound)) || (best && !is_dev(best)) || (status && !is_dev(status)))
+    PCK(cudaStreamSynchronize(s));
+  return DCOPF_OK;
+}
+
+int ptdf_get_multipliers(PtdfState *st, double *lambda, double *branch, cudaStream_t s, std::string *err) {
+  int rc = copy_rows_out(st, lambda, st->lam, 1, s, err);
+  if (!rc) rc = copy_rows_out(st, branch, st->mup, st->nl, s, err);
+  if (!rc && branch) rc = copy_rows_out(st, branch + (size_t)st->nl * st->B, st->mum, st->nl, s, err);
+  return rc;
+}
+
+int ptdf_set_multipliers(PtdfState *st, const double *lambda, const double *branch, cudaStream_t s,
+                         std::string *err) {
+  const size_t nm = (size_t)st->nlp * st->Bp;
+  // stage into scratch: [lambda Bp][mu+ nlp x Bp][mu- nlp x Bp], validate, then commit
+  int rc = ensure_scratch(st, (2 * nm + st->Bp) * 8, err);
+  if (rc) return rc;
+  double *tl = st->scratch, *tp = tl + st->Bp, *tm = tp + nm;
+  PCK(cudaMemsetAsync(st->scratch, 0, (2 * nm + st->Bp) * 8, s));
+  if (lambda) PCK(cudaMemcpyAsync(tl, lambda, st->B * 8, cudaMemcpyDefault, s));
+  if (branch && st->nl > 0) {
+    PCK(cudaMemcpy2DAsync(tp, st->Bp * 8, branch, st->B * 8, st->B * 8, st->nl, cudaMemcpyDefault, s));
+    PCK(cudaMemcpy2DAsync(tm, st->Bp * 8, branch + (size_t)st->nl * st->B, st->B * 8, st->B * 8, st->nl,
+                          cudaMemcpyDefault, s));
+  }
+  PCK(cudaMemsetAsync(st->flag, 0, sizeof(int), s));
+  if (lambda) k_check<<<blocks_for(st->B), 256, 0, s>>>(tl, 1, st->Bp, st->B, 0, st->flag);
+  if (branch && st->nl > 0) k_check<<<blocks_for(2 * nm), 256, 0, s>>>(tp, 2 * st->nlp, st->Bp, st->B, 1, st->flag);
+  int bad = 0;
+  PCK(cudaMemcpyAsync(&bad, st->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  PCK(cudaStreamSynchronize(s));
+  if (bad) {
+    *err = "multipliers must be finite and mu >= 0 (SPEC.md:239)";
+    return DCOPF_EINVAL;
+  }
+  if (lambda) PCK(cudaMemcpyAsync(st->lam, tl, st->B * 8, cudaMemcpyDeviceToDevice, s));
+  if (branch) {
+    PCK(cudaMemcpyAsync(st->mup, tp, nm * 8, cudaMemcpyDeviceToDevice, s));
+    PCK(cudaMemcpyAsync(st->mum, tm, nm * 8, cudaMemcpyDeviceToDevice, s));
+    k_sub<<<blocks_for(nm), 256, 0, s>>>(st->mup, st->mum, st->nu, nm);
+  }
+  PCK(cudaStreamSynchronize(s));
+  return DCOPF_OK;
+}
+
+int ptdf_evaluate(PtdfState *st, double *value, double *grad_lambda, double *grad_branch, cudaStream_t s,
+                  std::string *err) {
+  int rc = DCOPF_OK;
+  if (!st->gp) rc = dalloc(&st->gp, (size_t)st->nlp * st->Bp, err);
+  if (!rc && !st->gm) rc = dalloc(&st->gm, (size_t)st->nlp * st->Bp, err);
+  if (!rc) rc = launch_gemm<EPI_GEN>(gen_args(st), s, err);
+  if (rc) return rc;
+  GemmArgs g2 = line_args(st);
+  g2.gp_out = st->gp;
+  g2.gm_out = st->gm;
+  rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
+  if (rc) return rc;
+  FinArgs f = fin_args(st);
+  f.glam_out = st->glam;
+  k_finish<true><<<blocks_for(st->Bp), 256, 0, s>>>(f);
+  PCK(cudaGetLastError());
+  if (value) PCK(cudaMemcpyAsync(value, st->value, st->B * 8, cudaMemcpyDefault, s));
+  rc = copy_rows_out(st, grad_lambda, st->glam, 1, s, err);
+  if (!rc) rc = copy_rows_out(st, grad_branch, st->gp, st->nl, s, err);
+  if (!rc && grad_branch) rc = copy_rows_out(st, grad_branch + (size_t)st->nl * st->B, st->gm, st->nl, s, err);
+  if (!rc) PCK(cudaStreamSynchronize(s));
+  return rc;
+}
+
+int ptdf_set_optimizer(PtdfState *st, const dcopf_optimizer &o, std::string *err) {
+  st->opt = o;
+  int rc = reset_opt(st, err);
+  if (!rc) PCK(cudaDeviceSynchronize());
+  return rc;
+}
+
+void ptdf_set_stop(PtdfState *st, double tol) { st->tol = tol; }
+
+int ptdf_set_target(PtdfState *st, const double *target, cudaStream_t s, std::string *err) {
+  if (!target) {
+    st->has_target = false;
+    return DCOPF_OK;
+  }
+  std::vector<double> t(st->Bp, std::numeric_limits<double>::infinity());
+  PCK(cudaMemcpyAsync(t.data(), target, st->B * 8, cudaMemcpyDefault, s));
+  PCK(cudaStreamSynchronize(s));
+  for (long b = 0; b < st->B; ++b)
+    if (std::isnan(t[b])) {
+      *err = "target is NaN";
+      return DCOPF_EINVAL;
+    }
+  PCK(cudaMemcpyAsync(st->target, t.data(), st->Bp * 8, cudaMemcpyHostToDevice, s));
+  PCK(cudaStreamSynchronize(s));
+  st->has_target = true;
+  return DCOPF_OK;
+}
+
+int ptdf_get_first_hit(PtdfState *st, int64_t *hit, cudaStream_t s, std::string *err) {
+  if (!hit) return DCOPF_OK;
+  PCK(cudaMemcpyAsync(hit, st->hit, st->B * 8, cudaMemcpyDefault, s));
+  if (!is_dev(hit)) PCK(cudaStreamSynchronize(s));
+  return DCOPF_OK;
+}
+
+int ptdf_get_matrix(PtdfState *st, double *Ha, cudaStream_t s, std::string *err) {
+  if (!Ha || st->nl == 0) return DCOPF_OK;
+  PCK(cudaMemcpy2DAsync(Ha, (size_t)st->nb * 8, st->Ha, st->nbk * 8, (size_t)st->nb * 8, st->nl, cudaMemcpyDefault,
+                        s));
+  PCK(cudaStreamSynchronize(s));
+  return DCOPF_OK;
+}
+
+void ptdf_info(const PtdfState *st, dcopf_info *info) {
+  info->B = st->B;
+  info->B_padded = st->Bp;
+  info->path = DCOPF_PATH_DENSE;
+  info->form = DCOPF_FORM_PTDF;
+  info->n_bus = st->nb;
+  info->n_branch = st->nl;
+  info->n_gen = st->ng;
+  info->quadratic = st->quadratic;
+  // per instance-iteration, algorithmic: the two GEMMs' shares of H_g (read once per
+  // iteration for the whole batch, so ~0 per instance) + nu, p*, r, mu+-, nu rows
+  info->alg_bytes_per_inst_iter = 8LL * (2LL * st->nl + 2LL * st->ng + 6LL * st->nl);
+  info->smem_bytes = GEMM_SMEM;
+  info->threads_per_block = NTHR;
+  info->grid = (int)((st->nlp / BM) * (st->Bp / BN));
+  info->launches_per_iter = 3;
+  info->tile_width = BN;
+  info->cluster_size = 1;
+}
+
+}  // namespace dcopf

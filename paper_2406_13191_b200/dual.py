@@ -20,8 +20,9 @@ from . import _build
 
 FORM_F2 = 0  # DCOPF_FORM_FLOW_BOX
 FORM_F1 = 1  # DCOPF_FORM_LIMIT_ROWS
-FORM_KVL = 2  # DCOPF_FORM_CYCLE (cluster path only)
-PATH_AUTO, PATH_BATCHED, PATH_SINGLE, PATH_CLUSTER = 0, 1, 2, 3
+FORM_KVL = 2  # DCOPF_FORM_CYCLE (cluster and batched paths)
+FORM_PTDF = 3  # DCOPF_FORM_PTDF: the paper's dense-PTDF Eq. 1, load-only batches (dense path)
+PATH_AUTO, PATH_BATCHED, PATH_SINGLE, PATH_CLUSTER, PATH_DENSE = 0, 1, 2, 3, 4
 INST_OK, INST_DIVERGED, INST_CONVERGED = 0, 1, 2
 OPT_PLAIN, OPT_GDM, OPT_GDM_CLASSIC, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2, 3, 4
 ERRORS = {-1: "EINVAL", -2: "ETOPOLOGY", -3: "ECUDA", -4: "ENOMEM", -5: "ESTATE"}
@@ -67,7 +68,7 @@ class Optimizer(ctypes.Structure):
 
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",
            "dcopf_dual_get_bound", "dcopf_dual_get_multipliers", "dcopf_dual_set_multipliers",
-           "dcopf_dual_evaluate", "dcopf_dual_set_optimizer", "dcopf_dual_set_stop", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info",
+           "dcopf_dual_evaluate", "dcopf_dual_set_optimizer", "dcopf_dual_set_stop", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info", "dcopf_dual_get_ptdf",
            "dcopf_dual_last_error", "dcopf_dual_destroy"]
 
 _lib = None
@@ -98,6 +99,8 @@ def load_library(path: Optional[str] = None):
         lib.dcopf_dual_set_target.argtypes = [P, P, P]
         lib.dcopf_dual_get_first_hit.argtypes = [P, P, P]
     lib.dcopf_dual_get_info.argtypes = [P, ctypes.POINTER(Info)]
+    if hasattr(lib, "dcopf_dual_get_ptdf"):
+        lib.dcopf_dual_get_ptdf.argtypes = [P, P, P]
     lib.dcopf_dual_last_error.argtypes = [P]
     lib.dcopf_dual_last_error.restype = ctypes.c_char_p
     lib.dcopf_dual_destroy.argtypes = [P]
@@ -181,7 +184,12 @@ class DcopfDual:
     def n_branch_mult(self):
         if self.form == FORM_KVL:
             return self.net.n_branch - self.net.n_bus + 1
-        return self.net.n_branch * (2 if self.form == FORM_F1 else 1)
+        return self.net.n_branch * (2 if self.form in (FORM_F1, FORM_PTDF) else 1)
+
+    @property
+    def n_lambda(self):
+        """Rows of the lambda block: one per bus, one per instance for the PTDF form."""
+        return 1 if self.form == FORM_PTDF else self.net.n_bus
 
     # -- ABI calls ------------------------------------------------------------
     def set_instance_batch(self, load, outages=None, stream=None):
@@ -231,6 +239,13 @@ class DcopfDual:
         self._check(self.lib.dcopf_dual_get_first_hit(self.h, _ptr(hit), _stream(stream)))
         return hit
 
+    def get_ptdf(self, Ha=None, stream=None):
+        """PTDF form: the library's H_a [n_branch][n_bus]."""
+        if Ha is None:
+            Ha = np.empty((self.net.n_branch, self.net.n_bus))
+        self._check(self.lib.dcopf_dual_get_ptdf(self.h, _ptr(Ha), _stream(stream)))
+        return Ha
+
     def info(self) -> Info:
         inf = Info()
         self._check(self.lib.dcopf_dual_get_info(self.h, ctypes.byref(inf)))
@@ -242,7 +257,7 @@ class DcopfDual:
         bound, best = np.empty(B), np.empty(B)
         status = np.empty(B, dtype=np.int32)
         self.get_bound(bound, best, status)
-        lam = np.empty((self.net.n_bus, B))
+        lam = np.empty((self.n_lambda, B))
         br = np.empty((self.n_branch_mult, B))
         self.get_multipliers(lam, br)
         return bound, best, status, lam, br

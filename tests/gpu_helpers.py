@@ -49,7 +49,7 @@ def run_gpu(net, loads, outages=None, K=0, alpha=None, form=0, path=dual.PATH_AU
     bound = torch.empty(B, dtype=torch.float64, device=dev)
     best = torch.empty(B, dtype=torch.float64, device=dev)
     status = torch.empty(B, dtype=torch.int32, device=dev)
-    lam = torch.empty((net.n_bus, B), dtype=torch.float64, device=dev)
+    lam = torch.empty((h.n_lambda, B), dtype=torch.float64, device=dev)
     br = torch.empty((nbr, B), dtype=torch.float64, device=dev)
     h.get_bound(bound, best, status)
     h.get_multipliers(lam, br)

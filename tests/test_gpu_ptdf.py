@@ -1,0 +1,272 @@
+"""GPU parity of the dense-PTDF form (DCOPF_FORM_PTDF on DCOPF_PATH_DENSE;
+SURVEY.md NEXT-4) against the numpy oracle oracle/ptdf.py, at the north_star
+tolerances (1e-9 relative on the bound, reading A-17; 1e-8 normalised max-abs
+on the multipliers, reading A-18).
+
+Not bitwise: the GPU sums the PTDF products in DMMA tile order and builds H_a
+by the cycle method, the oracle uses numpy's matmul and solve (reading A-30).
+The library's H_a is also checked on its own against Kirchhoff's laws.
+"""
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import ptdf as P
+from paper_2406_13191_b200 import dual
+from paper_2406_13191_b200 import instances as inst
+
+from gpu_helpers import BOUND_RTOL, MULT_TOL, assert_parity, cost_scale, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+ADAM = dict(variant=P.OPT_ADAM, beta1=0.9, beta2=0.999, eps=1e-8)
+GDM = dict(variant=P.OPT_GDM, rho=0.9)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    dual.load_library()
+
+
+def _orc(net, loads, K, alpha, Ha=None, **kw):
+    r = P.solve(net, loads, K, alpha, Ha=Ha, history=True, **kw)
+    return SimpleNamespace(lam=r.lam[:, None], br=r.mu, bound=r.bound, best=r.best, status=r.status, hist=r.hist)
+
+
+def _gpu(net, loads, K, alpha, **kw):
+    return run_gpu(net, loads, K=K, alpha=alpha, form=dual.FORM_PTDF, path=dual.PATH_DENSE, history=True, **kw)
+
+
+def _lib_ptdf(net):
+    h = dual.DcopfDual(net, form=dual.FORM_PTDF, path=dual.PATH_DENSE)
+    H = h.get_ptdf()
+    h.close()
+    return H
+
+
+def _scaled_loads(net, B, seed):
+    rng = np.random.default_rng(seed)
+    return net.base_load[None, :] * rng.uniform(0.85, 1.15, (B, 1))
+
+
+def _with_open_branch(net):
+    b = net.br_b.copy()
+    b[net.n_tree + 1] = 0.0   # a non-tree branch with b = 0 (open circuit)
+    return inst.Network(**{**net.__dict__, "br_b": b})
+
+
+# ---------------------------------------------------------------------------
+# the PTDF matrix
+
+
+@pytest.mark.parametrize("which", ["config0", "config1", "radial", "open_branch", "multi_gen"])
+def test_ptdf_matrix(which):
+    if which == "config0":
+        net = inst.make_network(0)
+    elif which == "config1":
+        net = inst.make_network(1)
+    elif which == "radial":
+        net = inst.tiny_network(40, 39, 6, 3)
+    elif which == "open_branch":
+        net = _with_open_branch(inst.tiny_network(30, 50, 8, 5))
+    else:
+        net = inst.tiny_network(23, 40, 30, 9)
+    H = _lib_ptdf(net)
+    Ho = P.ptdf(net)
+    assert np.max(np.abs(H - Ho)) <= 1e-11 * max(1.0, np.max(np.abs(Ho)))
+    # on its own: zero slack column, KCL (E^T H = I - e_ref 1^T over b > 0), KVL on the C oracle's cycles
+    assert np.all(H[:, net.ref_bus] == 0.0)
+    E = P.incidence(net) * (net.br_b > 0)[:, None]
+    want = np.eye(net.n_bus)
+    want[net.ref_bus, :] -= 1.0
+    assert np.max(np.abs(E.T @ H - want)) <= 1e-10
+    assert np.all(H[net.br_b == 0.0] == 0.0)
+    _, cyc = oracle.cycles(net)
+    for br, sg in cyc:
+        if np.all(net.br_b[br] > 0):
+            assert np.max(np.abs((sg[:, None] * H[br] / net.br_b[br][:, None]).sum(0))) <= 1e-11
+
+
+# ---------------------------------------------------------------------------
+# the iteration
+
+
+def test_config0_full_K():
+    net = inst.make_network(0)
+    K = inst.ITERS[0]
+    a = inst.alpha_schedule(K)
+    gpu = _gpu(net, net.base_load[None], K, a)
+    orc = _orc(net, net.base_load[None], K, a)
+    assert_parity(net, gpu, orc)
+    info = gpu["info"]
+    assert info.path == dual.PATH_DENSE and info.form == dual.FORM_PTDF
+
+
+@pytest.mark.parametrize("B", [1, 130, 300])
+def test_config1_batch_ragged(B):
+    """Several 128-instance tiles and a ragged tail; M tiles over 3200 lines / 540 generators."""
+    net = inst.make_network(1)
+    Ha = P.ptdf(net)
+    K = 200
+    a = inst.alpha_schedule(K)
+    loads = _scaled_loads(net, B, 11)
+    gpu = _gpu(net, loads, K, a)
+    idx = np.unique(np.r_[0, B - 1, np.linspace(0, B - 1, 6).astype(int)])
+    orc = _orc(net, loads[idx], K, a, Ha=Ha)
+    assert_parity(net, gpu, orc, idx=idx)
+
+
+def test_quadratic_config2_network():
+    net = inst.make_network(2, quadratic=True)
+    K = 60
+    a = inst.alpha_schedule(K, 0.05)
+    loads = _scaled_loads(net, 3, 5)
+    gpu = _gpu(net, loads, K, a)
+    orc = _orc(net, loads, K, a)
+    assert_parity(net, gpu, orc)
+
+
+@pytest.mark.parametrize("opt,alpha", [(ADAM, 0.05), (GDM, 1e-3),
+                                       (dict(variant=P.OPT_GDM_CLASSIC, rho=0.5), 1e-3),
+                                       (dict(variant=P.OPT_ADAGRAD, eps=1e-8), 0.5)])
+def test_optimizers(opt, alpha):
+    net = inst.tiny_network(60, 95, 14, 21)
+    K = 400
+    a = inst.alpha_schedule(K, alpha)
+    loads = _scaled_loads(net, 140, 3)
+    gpu = _gpu(net, loads, K, a, opt=opt, split=150)
+    orc = _orc(net, loads, K, a, opt=opt)
+    assert_parity(net, gpu, orc)
+
+
+def test_divergence_and_stopping_rule():
+    net = inst.tiny_network(14, 19, 5, 0)
+    loads = _scaled_loads(net, 3, 1)
+    K = 40
+    a = np.full(K, 1e16)
+    gpu = _gpu(net, loads, K, a)
+    orc = _orc(net, loads, K, a)
+    assert np.all(orc.status == P.DIVERGED)
+    np.testing.assert_array_equal(gpu["status"], orc.status)
+    np.testing.assert_array_equal(np.isfinite(gpu["best"]), np.isfinite(orc.best))
+    # stopping rule: the tolerance fires mid-run for some instances only
+    K = 300
+    a = inst.alpha_schedule(K)
+    full = _orc(net, loads, K, a)
+    tol = float(np.median(np.abs(np.diff(full.hist[0])))) * 0.5
+    gpu = _gpu(net, loads, K, a, tol=tol)
+    orc = _orc(net, loads, K, a, tol=tol)
+    assert np.any(orc.status == P.CONVERGED)
+    assert_parity(net, gpu, orc, check_hist=False)
+
+
+def test_evaluate_at_random_point_and_warm_start():
+    import torch
+    net = inst.make_network(1)
+    Ha = P.ptdf(net)
+    B = 5
+    rng = np.random.default_rng(8)
+    loads = _scaled_loads(net, B, 2)
+    lam = rng.normal(0, 20, B)
+    mu = np.abs(rng.normal(0, 5, (B, 2 * net.n_branch))) * (rng.random((B, 2 * net.n_branch)) < 0.3)
+    h = dual.DcopfDual(net, form=dual.FORM_PTDF)
+    dev = torch.device("cuda:0")
+    h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(loads.T)).to(dev))
+    h.set_multipliers(np.ascontiguousarray(lam[None, :]), np.ascontiguousarray(mu.T))
+    val = np.empty(B)
+    gl = np.empty((1, B))
+    gb = np.empty((2 * net.n_branch, B))
+    h.evaluate(val, gl, gb)
+    ev = P.evaluate(net, Ha, loads, lam, mu[:, :net.n_branch], mu[:, net.n_branch:])
+    S = cost_scale(net)
+    assert np.all(np.abs(val - ev.value) <= BOUND_RTOL * np.maximum(np.abs(ev.value), S))
+    gmu = np.concatenate([ev.g_mup, ev.g_mum], axis=1)
+    sc = max(1.0, np.max(np.abs(gmu)))
+    assert np.max(np.abs(gb.T - gmu)) <= 1e-11 * sc
+    assert np.max(np.abs(gl[0] - ev.g_lam)) <= 1e-11 * max(1.0, np.max(np.abs(ev.g_lam)))
+    # warm start: 50 steps from that point
+    K = 50
+    a = inst.alpha_schedule(K)
+    h.iterate(K, a)
+    bound, best, status, l2, b2 = h.results_numpy()
+    r = P.solve(net, loads, K, a, Ha=Ha, lam0=lam, mu0=mu)
+    assert np.all(np.abs(bound - r.bound) <= BOUND_RTOL * np.maximum(np.abs(r.bound), S))
+    y_g = np.concatenate([l2.T, b2.T], axis=1)
+    y_o = np.concatenate([r.lam[:, None], r.mu], axis=1)
+    assert np.max(np.abs(y_g - y_o) / np.maximum(1.0, np.abs(y_o).max(axis=1, keepdims=True))) <= MULT_TOL
+    # mu < 0 in a warm start is rejected
+    bad = mu.copy()
+    bad[0, 3] = -1.0
+    with pytest.raises(dual.DcopfError):
+        h.set_multipliers(None, np.ascontiguousarray(bad.T))
+    h.close()
+
+
+def test_first_hit():
+    import torch
+    net = inst.make_network(0)
+    K = 2000
+    a = inst.alpha_schedule(K)
+    orc = P.solve(net, net.base_load[None], K, a, history=True)
+    run = np.maximum.accumulate(orc.hist[0])
+    target = run[K // 2] - 1e-9 * abs(run[K // 2])
+    want = int(np.argmax(run >= target))
+    h = dual.DcopfDual(net, form=dual.FORM_PTDF)
+    h.set_instance_batch(np.ascontiguousarray(net.base_load[:, None]))
+    h.set_target(np.array([target]))
+    h.iterate(700, a[:700])
+    h.iterate(K - 700, a[700:])
+    assert int(h.get_first_hit()[0]) == want
+    h.close()
+
+
+def test_edge_cases():
+    # single bus (no branch), a radial network (no cycle), one instance
+    one = inst.Network(n_bus=1, n_branch=0, n_gen=2, ref_bus=0, br_from=np.zeros(0, np.int32),
+                       br_to=np.zeros(0, np.int32), br_b=np.zeros(0), br_fmax=np.zeros(0),
+                       theta_max=np.zeros(1), gen_bus=np.zeros(2, np.int32), gen_pmin=np.zeros(2),
+                       gen_pmax=np.array([1.0, 2.0]), gen_c=np.array([10.0, 20.0]), base_load=np.array([1.5]))
+    for net in (one, inst.tiny_network(40, 39, 6, 3), _with_open_branch(inst.tiny_network(30, 50, 8, 5))):
+        K = 300
+        a = inst.alpha_schedule(K, 0.01)
+        loads = _scaled_loads(net, 2, 4)
+        gpu = _gpu(net, loads, K, a)
+        orc = _orc(net, loads, K, a)
+        assert_parity(net, gpu, orc)
+
+
+def test_rejects_outages_and_wrong_path():
+    net = inst.make_network(0)
+    h = dual.DcopfDual(net, form=dual.FORM_PTDF)
+    with pytest.raises(dual.DcopfError):
+        h.set_instance_batch(np.ascontiguousarray(net.base_load[:, None]), np.array([[3]], np.int32))
+    h.set_instance_batch(np.ascontiguousarray(net.base_load[:, None]), np.array([[-1]], np.int32))
+    h.close()
+    with pytest.raises(dual.DcopfError):
+        dual.DcopfDual(net, form=dual.FORM_PTDF, path=dual.PATH_BATCHED)
+    with pytest.raises(dual.DcopfError):
+        dual.DcopfDual(net, form=dual.FORM_F2, path=dual.PATH_DENSE)
+
+
+# ---------------------------------------------------------------------------
+# the bench configuration: config 4b (8192 load scenarios of the 10 000-bus
+# network, one factor each), sampled instances against the oracle
+
+
+def test_config4b_full_size_sampled():
+    import torch
+    net = inst.make_network(3)
+    ids = np.arange(inst.CONFIG4_BATCH)
+    batch = inst.config4_batch(net, ids, variant="4b")
+    K = 6
+    a = inst.alpha_schedule(K)
+    gpu = _gpu(net, batch.load, K, a)
+    idx = np.array([0, 1, 127, 128, 4095, 8191])
+    orc = _orc(net, batch.load[idx], K, a)
+    assert_parity(net, gpu, orc, idx=idx)
+    assert gpu["info"].B_padded == inst.CONFIG4_BATCH
