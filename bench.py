@@ -14,7 +14,12 @@ not counted as work, so the reported rate is conservative).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload config4|config4b|config0|config1|config2|config3|config3q]
-                  [--form F2|F1]
+                  [--form F2|F1|KVL|PTDF]
+
+--form PTDF runs the paper's dense-PTDF Eq. 1 on the dense
+path (two fused fp64 DMMA GEMMs per step); it takes load-only batches, so its
+workload is config4b (or a single-instance config); its roofline is the fp64
+tensor-core peak measured live (cuBLAS DGEMM through torch.matmul).
 
 Multi-GPU: launched by torchrun; one process per GPU; the instances are
 sharded with no communication in the loop; one NCCL all_gather of the
@@ -78,9 +83,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
-    ap.add_argument("--form", default="F2", choices=["F2", "F1", "KVL"],
-                    help="F2 flow box (default), F1 limit rows, KVL cycle basis (cluster path)")
-    ap.add_argument("--path", default="auto", choices=["auto", "batched", "single", "cluster"])
+    ap.add_argument("--form", default="F2", choices=["F2", "F1", "KVL", "PTDF"],
+                    help="F2 flow box (default), F1 limit rows, KVL cycle basis, PTDF dense (load-only batches)")
+    ap.add_argument("--path", default="auto", choices=["auto", "batched", "single", "cluster", "dense"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap run (the workload's full K)")
@@ -162,6 +167,47 @@ def make_inputs(workload, lo, hi, total=inst.CONFIG4_BATCH):
     else:
         batch = inst.single_batch(net)
     return net, batch
+
+
+def fp64_peak_tflops(dev):
+    """The fp64 tensor-core roofline for the PTDF form, measured here: cuBLAS
+    DGEMM 8192^3 through torch.matmul, best of 5 (MEASURED_PEAKS.json has no
+    fp64 entry and B200_PROFILING.md no fp64 fallback)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        a @ b
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del a, b
+    return 2.0 * n ** 3 / (best / 1e3) / 1e12
+
+
+def ptdf_oracle_rate(net, batch, cores, target_s=12.0, opt=None):
+    """oracle/ptdf.py (numpy, BLAS threads = the host's cores) on a bounded
+    sample: a few instances x K steps, H_a built outside the timed part."""
+    from oracle import ptdf as P
+    Ha = P.ptdf(net)
+    n_inst = min(batch.B, 16)
+    loads = batch.load[np.linspace(0, batch.B - 1, n_inst).astype(int)]
+    K0 = 3
+    t0 = time.perf_counter()
+    P.solve(net, loads, K0, inst.alpha_schedule(K0), Ha=Ha, opt=opt)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    K = int(max(K0, min(100000, K0 * target_s / dt)))
+    t0 = time.perf_counter()
+    P.solve(net, loads, K, inst.alpha_schedule(K), Ha=Ha, opt=opt)
+    dt = time.perf_counter() - t0
+    return n_inst * K / dt, f"{n_inst} instances x {K} iterations ({dt:.1f} s wall), numpy BLAS, H_a precomputed"
 
 
 def cpu_oracle_rate(net, batch, form, cores, target_s=12.0, opt=None):
@@ -247,7 +293,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    form = {"F2": 0, "F1": 1, "KVL": 2}[args.form]
+    form = {"F2": 0, "F1": 1, "KVL": 2, "PTDF": 3}[args.form]
     _, _, B = WORKLOADS[args.workload]
     net, batch = make_inputs(args.workload, 0, B if B == 1 else min(B, 256))
     cores = os.cpu_count() or 1
@@ -258,15 +304,27 @@ def run_reference(args):
     outs = None if batch.outages is None else batch.outages[:n_inst]
     K_s = 50 if net.n_bus > 1000 else 2000
     a = inst.alpha_schedule(K_s)
+    Ha = None
+    if form == 3:
+        from oracle import ptdf as P
+        Ha = P.ptdf(net)
+        n_inst = min(batch.B, 16)
+        loads = batch.load[:n_inst]
+        K_s = 5 if net.n_bus > 1000 else 2000
+        a = inst.alpha_schedule(K_s)
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.solve(net, loads, outages=outs, K=K_s, alpha=a, form=form, threads=cores, opt=opt_spec(args)[0])
+        if form == 3:
+            P.solve(net, loads, K_s, a, Ha=Ha, opt=opt_spec(args)[0])
+        else:
+            oracle.solve(net, loads, outages=outs, K=K_s, alpha=a, form=form, threads=cores, opt=opt_spec(args)[0])
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             per_step.append(dt)
     T = sum(per_step)
     value = n_inst * K_s * args.steps / T
-    sample = f"{n_inst} instances x {K_s} iterations per step, oracle/dcopf_oracle.c OpenMP over instances"
+    sample = (f"{n_inst} instances x {K_s} iterations per step, "
+              + ("oracle/ptdf.py numpy BLAS" if form == 3 else "oracle/dcopf_oracle.c OpenMP over instances"))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -293,8 +351,10 @@ def main():
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    form = {"F2": dual.FORM_F2, "F1": dual.FORM_F1, "KVL": dual.FORM_KVL}[args.form]
+    form = {"F2": dual.FORM_F2, "F1": dual.FORM_F1, "KVL": dual.FORM_KVL, "PTDF": dual.FORM_PTDF}[args.form]
     config, quad, B_total = WORKLOADS[args.workload]
+    if form == dual.FORM_PTDF and args.workload == "config4":
+        raise SystemExit("--form PTDF takes load-only batches: use --workload config4b (config 4 has outages)")
     if B_total > 1 and args.scaling == "weak":
         # weak scaling (independent instances, no data-path collective): every
         # rank iterates its own configs[4]-sized batch; rank r takes instances
@@ -306,13 +366,15 @@ def main():
     net, batch = make_inputs(args.workload, lo, hi, total=B_total)
     B = batch.B
     path = dual.PATH_BATCHED if B_total > 1 else dual.PATH_CLUSTER
+    if form == dual.FORM_PTDF:
+        path = dual.PATH_DENSE
     path = {"auto": path, "batched": dual.PATH_BATCHED, "single": dual.PATH_SINGLE,
-            "cluster": dual.PATH_CLUSTER}[args.path]
+            "cluster": dual.PATH_CLUSTER, "dense": dual.PATH_DENSE}[args.path]
 
     # config 4 takes branches out among the non-tree ones only: declaring that
     # lets the library skip the outage test on the (never switched) tree
     sw = None
-    if config == 4:
+    if config == 4 and form != dual.FORM_PTDF:
         sw = np.zeros(net.n_branch, np.uint8)
         sw[net.n_tree:] = 1
     ospec, alpha0 = opt_spec(args)
@@ -407,6 +469,9 @@ def main():
                "d2h_bytes_per_call": int(d2h), "steps_per_call": K,
                "timed": "set_instance_batch(host pinned) + iterate(K) + get_bound(host), wall clock, max over ranks"}
 
+    dense = form == dual.FORM_PTDF
+    if rank == 0 and dense:
+        peak_t = fp64_peak_tflops(dev)
     if rank == 0:
         peak, peak_src = peaks()
         inst_it = B_total * K
@@ -429,10 +494,23 @@ def main():
                 traffic = ent["dram_over_alg"] * per_gpu_bytes
         except Exception:
             pass
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src}
+        if dense:  # two GEMMs per step, 2 n_l n_g flops each per instance (the final evaluation not counted)
+            flops = 4.0 * net.n_branch * net.n_gen * B * K
+            ach_t = flops / (ms / 1e3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach_t, "peak": peak_t, "unit": "TFLOP/s", "frac": ach_t / peak_t,
+                    "traffic": None, "alg_flops_per_inst_iter": 4 * net.n_branch * net.n_gen,
+                    "peak_source": "measured live: cuBLAS DGEMM 8192^3 via torch.matmul, best of 5 (fp64)",
+                    "kernel": "the whole step (2 fused DMMA GEMMs + the per-instance finisher)"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            rate, sample = cpu_oracle_rate(net, batch, form, cores, opt=ospec)
+            if dense:
+                rate, sample = ptdf_oracle_rate(net, batch, cores, opt=ospec)
+            else:
+                rate, sample = cpu_oracle_rate(net, batch, form, cores, opt=ospec)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -443,7 +521,7 @@ def main():
                        "step": {"variant": args.opt, "alpha": alpha0, **OPTS[args.opt][1]},
                        "n_bus": net.n_bus, "n_branch": net.n_branch, "n_gen": net.n_gen,
                        "B_total": B_total, "B_per_gpu": B,
-                       "path": {1: "batched-sweep", 2: "single", 3: "cluster"}[path],
+                       "path": {1: "batched-sweep", 2: "single", 3: "cluster", 4: "dense-gemm"}[path],
                        "cluster_size": info.cluster_size,
                        "kernel": {"grid": info.grid, "threads": info.threads_per_block, "smem": info.smem_bytes,
                                   "chunk": info.chunk, "tile_width": info.tile_width,
@@ -454,15 +532,16 @@ def main():
                        "l2": ("inputs larger than L2: state %.2f GB per GPU" %
                               ((info.B_padded * (2 * net.n_bus + 2 * net.n_branch * (1 if form == 0 else 2)
                                                  + net.n_bus) * 8) / 1e9))
-                       if B_total > 1 else "state on chip (single instance)",
-                       "timed_launches": f"1 persistent launch: {K} iterations + final evaluation"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src},
+                       if B_total > 1 and not dense else ("H_g %.2f GB read twice per step" %
+                                                            (2 * 8 * net.n_branch * net.n_gen / 1e9)
+                                                            if dense else "state on chip (single instance)"),
+                       "timed_launches": (f"{3 * (K + 1)} launches: 3 per step ({K} steps) + the final evaluation"
+                                          if dense else f"1 persistent launch: {K} iterations + final evaluation")},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "time_to_gap": ttg,
             "e2e": e2e,
-            "gpu_launches": 1,
+            "gpu_launches": 3 * (K + 1) if dense else 1,
             "clocks": clk,
             "gather_ms": gather_ms,
         }

@@ -583,7 +583,7 @@ int oracle_cycles(NET_ARGS, const unsigned char *switchable, int *nc, int *def, 
   if (build_cycles(&N, switchable, &Y) != 0) return -2;
   *nc = Y.nc;
   tot = Y.cp[Y.nc];
-  if (cap >= tot) {
+  if (cap >= tot && cp != NULL) {   /* cp == NULL: size query only (also when there is no cycle) */
     for (k = 0; k < Y.nc; k++) def[k] = Y.def[k];
     for (k = 0; k <= Y.nc; k++) cp[k] = Y.cp[k];
     for (k = 0; k < tot; k++) { cb[k] = Y.cb[k]; cs[k] = Y.cs[k]; }

@@ -420,45 +420,45 @@ __device__ __forceinline__ double tflow(const TreeDev &T, const int *tin_bus, in
 // S[k][i] = sum_{l in cycle k} C_kl x_l T[l][i]
 __global__ void k_cycle_tree(TreeDev T, const int *cp, const int *cb, const double *cs, const double *x, int nc,
                              int nb, double *S, long lds) {
-  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= (long)nc * nb) return;
-  const int k = (int)(id / nb), i = (int)(id % nb);
-  double s = 0.0;
-  for (int e = cp[k]; e < cp[k + 1]; ++e) {
-    const int l = cb[e];
-    s += cs[e] * x[l] * tflow(T, T.tin, l, i);
+  for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < (long)nc * nb; id += (long)gridDim.x * blockDim.x) {
+    const int k = (int)(id / nb), i = (int)(id % nb);
+    double s = 0.0;
+    for (int e = cp[k]; e < cp[k + 1]; ++e) {
+      const int l = cb[e];
+      s += cs[e] * x[l] * tflow(T, T.tin, l, i);
+    }
+    S[(size_t)k * lds + i] = s;
   }
-  S[(size_t)k * lds + i] = s;
 }
 
 // H_a[l][i] = T[l][i] - sum_{k containing l} C_kl W[k][i]  (0 for an open branch, b = 0)
 __global__ void k_assemble(TreeDev T, const int *bp, const int *bk, const double *bs, const double *W, long ldw,
                            const double *b, int nl, int nb, double *Ha, long ldh) {
-  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= (long)nl * nb) return;
-  const int l = (int)(id / nb), i = (int)(id % nb);
-  double h = 0.0;
-  if (b[l] > 0.0) {
-    h = tflow(T, T.tin, l, i);
-    for (int e = bp[l]; e < bp[l + 1]; ++e) h -= bs[e] * W[(size_t)bk[e] * ldw + i];
+  for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < (long)nl * nb; id += (long)gridDim.x * blockDim.x) {
+    const int l = (int)(id / nb), i = (int)(id % nb);
+    double h = 0.0;
+    if (b[l] > 0.0) {
+      h = tflow(T, T.tin, l, i);
+      for (int e = bp[l]; e < bp[l + 1]; ++e) h -= bs[e] * W[(size_t)bk[e] * ldw + i];
+    }
+    Ha[(size_t)l * ldh + i] = h;
   }
-  Ha[(size_t)l * ldh + i] = h;
 }
 
 // HgT[g][l] = Hg[l][g] = H_a[l][bus(g)]
 __global__ void k_gen_cols(const double *Ha, long ldh, const int *gbus, int ng, int nl, double *HgT, long ldt,
                            double *Hg, long ldg) {
-  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= (long)ng * nl) return;
-  const int g = (int)(id / nl), l = (int)(id % nl);
-  const double v = Ha[(size_t)l * ldh + gbus[g]];
-  HgT[(size_t)g * ldt + l] = v;
-  Hg[(size_t)l * ldg + g] = v;
+  for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < (long)ng * nl; id += (long)gridDim.x * blockDim.x) {
+    const int g = (int)(id / nl), l = (int)(id % nl);
+    const double v = Ha[(size_t)l * ldh + gbus[g]];
+    HgT[(size_t)g * ldt + l] = v;
+    Hg[(size_t)l * ldg + g] = v;
+  }
 }
 
 __global__ void k_colsum(const double *Dm, int nb, long ld, double *D) {
   const long n = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= ld) return;
+  if (n >= ld) return;  // (launched with ld threads)
   double s = 0.0;
   for (int i = 0; i < nb; ++i) s += Dm[(size_t)i * ld + n];  // 1^T d, ascending bus
   D[n] = s;

@@ -122,9 +122,12 @@ def test_config1_batch_ragged(B):
 
 
 def test_quadratic_config2_network():
+    """alpha = 1e-3 (reading A-9): the trajectory is well conditioned (a 1e-15
+    perturbation of H_a stays at 1e-16 relative after 60 steps; at alpha = 0.05
+    one instance amplifies it to 3e-7, reading A-30)."""
     net = inst.make_network(2, quadratic=True)
-    K = 60
-    a = inst.alpha_schedule(K, 0.05)
+    K = 200
+    a = inst.alpha_schedule(K)
     loads = _scaled_loads(net, 3, 5)
     gpu = _gpu(net, loads, K, a)
     orc = _orc(net, loads, K, a)
@@ -154,14 +157,19 @@ def test_divergence_and_stopping_rule():
     assert np.all(orc.status == P.DIVERGED)
     np.testing.assert_array_equal(gpu["status"], orc.status)
     np.testing.assert_array_equal(np.isfinite(gpu["best"]), np.isfinite(orc.best))
-    # stopping rule: the tolerance fires mid-run for some instances only
+    # stopping rule: a tolerance between the smallest and the second smallest
+    # per-instance min |g_k - g_{k-1}| fires for exactly one instance; no
+    # difference lies within 1e-6 (relative) of it, far above the GPU/oracle gap
     K = 300
     a = inst.alpha_schedule(K)
     full = _orc(net, loads, K, a)
-    tol = float(np.median(np.abs(np.diff(full.hist[0])))) * 0.5
+    d = np.abs(np.diff(full.hist, axis=1))
+    m = np.sort(d.min(axis=1))
+    tol = float(np.sqrt(m[0] * m[1]))
+    assert m[1] / m[0] > 1.01 and np.min(np.abs(d / tol - 1.0)) > 1e-6
     gpu = _gpu(net, loads, K, a, tol=tol)
     orc = _orc(net, loads, K, a, tol=tol)
-    assert np.any(orc.status == P.CONVERGED)
+    assert np.sum(orc.status == P.CONVERGED) == 1
     assert_parity(net, gpu, orc, check_hist=False)
 
 

@@ -10,6 +10,11 @@ best reaches (1 - 1e-3) of it (on the sign-aware side).  Config 4 uses the
 deterministic sample of every 128th instance (64 instances), as SURVEY.md
 §8(d) prescribes for the oracle at that size.
 
+Form PTDF (oracle/ptdf.py): config 4b only (load-only batch),
+16 sampled instances (every 512th); the true gap is taken against the LP
+optimum of Eq. 1 itself, i.e. without an angle box (HiGHS on B-theta with
+Theta = inf, which never touches H).
+
 Calls only oracle/ and the seeded input generator; nothing here comes from
 the CUDA path.
 
@@ -51,14 +56,35 @@ def main():
     for wl, (config, quad) in WORKLOADS.items():
         if a.workloads and wl not in a.workloads:
             continue
-        for form_name, form in (("F2", oracle.FORM_F2), ("F1", oracle.FORM_F1), ("KVL", oracle.FORM_KVL)):
+        for form_name, form in (("F2", oracle.FORM_F2), ("F1", oracle.FORM_F1), ("KVL", oracle.FORM_KVL),
+                                ("PTDF", None)):
             if form_name not in a.forms:
                 continue
             key = f"{wl}/{form_name}" + ("" if a.opt == "plain" else f"/{a.opt}/{alpha:g}")
             if a.only and key not in a.only:
                 continue
+            if form_name == "PTDF" and wl != "config4b":
+                continue
             net = inst.make_network(config, quadratic=quad)
             K = inst.ITERS[config]
+            if form_name == "PTDF":
+                import dataclasses
+                from oracle import ptdf as P
+                ids = np.arange(0, inst.CONFIG4_BATCH, 512)
+                batch = inst.config4_batch(net, ids, variant="4b")
+                t0 = time.time()
+                res = P.solve(net, batch.load, K, inst.alpha_schedule(K, alpha), opt=opt)
+                th = np.full(net.n_bus, 1e6)
+                th[net.ref_bus] = 0.0
+                nob = dataclasses.replace(net, theta_max=th)
+                primal = [inst.primal_lp(nob, batch.load[r])[1] for r in range(len(ids))]
+                js[key] = {"K": K, "alpha": alpha, "opt": {"name": a.opt, **opt}, "primal_opt": primal,
+                           "primal_note": "LP optimum of Eq. 1 (no angle box)",
+                           "instance_ids": ids.tolist(), "best": res.best.tolist(), "bound": res.bound.tolist(),
+                           "status": res.status.tolist(), "source": "oracle/ptdf.py via tools/make_targets.py"}
+                print(key, f"{time.time() - t0:.1f}s", "best[:4] =", res.best[:4], flush=True)
+                json.dump(js, open(OUT, "w"), indent=0)
+                continue
             if config == 4:
                 ids = np.arange(0, inst.CONFIG4_BATCH, 128)
                 batch = inst.config4_batch(net, ids, variant="4b" if wl == "config4b" else "4")
