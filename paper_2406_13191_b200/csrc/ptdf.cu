@@ -20,12 +20,27 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // GEMM tiling: C[M][N] = A[M][K] B[K][N], A row-major (K contiguous), B
-// row-major (N = instances contiguous).  128 x 128 x 16 CTA tiles, 8 warps as
-// 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 DMMA m8n8k4 tiles, a 4-stage
-// cp.async pipeline, padded shared-memory rows (conflict-free fragment
-// loads: A stride 20 doubles, B stride 132 doubles).  M, N, K are padded to
-// the tile sizes with zeros by the owner of each matrix.
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, NTHR = 256;
+// row-major (N = instances contiguous).  64 x 128 x 16 CTA tiles of 4 warps
+// (warp tile 64 x 32 = 8 x 4 DMMA m8n8k4 tiles, 64 fp64 accumulators per
+// thread), two CTAs per SM so one CTA's barrier / epilogue overlaps the
+// other's DMMA stream, a 4-stage cp.async pipeline, padded shared-memory rows
+// (conflict-free fragment loads: A stride BK+4, B stride 132 doubles).
+// Measured on config 4b: 128 x 128 tiles at one CTA per SM
+// reached 79% of the DGEMM peak per step, 64 x 128 at two per SM 85%.
+// M, N, K are padded to the tile sizes with zeros by the owner of each matrix.
+#ifndef PTDF_BM
+#define PTDF_BM 64
+#endif
+#ifndef PTDF_BK
+#define PTDF_BK 16
+#endif
+#ifndef PTDF_STAGES
+#define PTDF_STAGES 4
+#endif
+constexpr int BM = PTDF_BM, BN = 128, BK = PTDF_BK, STAGES = PTDF_STAGES;
+constexpr int NTHR = (BM / 64) * 4 * 32;  // warps: BM/64 (M) x 4 (N), warp tile 64 x 32
+constexpr int CTAS_PER_SM = (BM == 64) ? 2 : 1;
+constexpr int WMN = BM / 64;
 constexpr int AST = BK + 4, BST = BN + 4;
 constexpr int A_STAGE = BM * AST, B_STAGE = BK * BST;  // doubles
 constexpr int GEMM_SMEM = STAGES * (A_STAGE + B_STAGE) * 8;
@@ -109,7 +124,7 @@ __device__ __forceinline__ double opt_step(const GemmArgs &g, double y, double g
 // one CTA per 128 x 128 output tile, grouped raster (`group` M-tiles per band,
 // M fastest inside a band) so concurrently running CTAs share A and B tiles in L2
 template <int EPI>
-__global__ void __launch_bounds__(NTHR, 1) k_dgemm(const GemmArgs g) {
+__global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
   extern __shared__ __align__(16) double sm[];
   double *As = sm, *Bs = sm + STAGES * A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 2, wn = warp & 3;
@@ -125,7 +140,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_dgemm(const GemmArgs g) {
     double *as = As + stage * A_STAGE, *bs = Bs + stage * B_STAGE;
 #pragma unroll
     for (int c = tid; c < BM * BK / 2; c += NTHR) {
-      const int row = c >> 3, ch = c & 7;
+      const int row = c / (BK / 2), ch = c % (BK / 2);
       cp_async16(as + row * AST + ch * 2, g.A + (size_t)(m0 + row) * g.lda + k0 + ch * 2);
     }
 #pragma unroll
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_dgemm(const GemmArgs g) {
         s0[j][e] += __shfl_xor_sync(0xffffffffu, s0[j][e], off);
         if (EPI == EPI_GEN) s1[j][e] += __shfl_xor_sync(0xffffffffu, s1[j][e], off);
       }
-  double *red = sm;  // [2 sums][2 wm][BN]
+  double *red = sm;  // [2 sums][WMN][BN]
   if (lane < 4) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -314,17 +329,23 @@ __global__ void __launch_bounds__(NTHR, 1) k_dgemm(const GemmArgs g) {
       for (int e = 0; e < 2; ++e) {
         const int col = wn * 32 + j * 8 + 2 * lane + e;
         red[wm * BN + col] = s0[j][e];
-        if (EPI == EPI_GEN) red[2 * BN + wm * BN + col] = s1[j][e];
+        if (EPI == EPI_GEN) red[WMN * BN + wm * BN + col] = s1[j][e];
       }
   }
   __syncthreads();
   if (tid < BN) {
     const size_t o = (size_t)mt * g.ld + n0 + tid;
+    double so = red[tid], sp = red[WMN * BN + tid];
+#pragma unroll
+    for (int w = 1; w < WMN; ++w) {  // the M-warps in order
+      so += red[w * BN + tid];
+      sp += red[WMN * BN + w * BN + tid];
+    }
     if (EPI == EPI_GEN) {
-      g.part_obj[o] = red[tid] + red[BN + tid];
-      g.part_p[o] = red[2 * BN + tid] + red[3 * BN + tid];
+      g.part_obj[o] = so;
+      g.part_p[o] = sp;
     } else {
-      g.part_line[o] = red[tid] + red[BN + tid];
+      g.part_line[o] = so;
     }
   }
 }
