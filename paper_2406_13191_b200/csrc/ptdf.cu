@@ -55,6 +55,7 @@ struct GemmArgs {
   const double *Bm;
   long ldb;
   int M, N, K, group;
+  int noff;  // first column of this launch (a launch covers columns [noff, noff + N))
   long ld;  // leading dimension of every [rows][B_pad] array (= B_pad) / of C for EPI_STORE
   double *C;
   // EPI_GEN (rows = generators)
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
   const int t = blockIdx.x, band = t / (g.group * nNt), first_m = band * g.group;
   const int gs = min(nMt - first_m, g.group);
   const int mt = first_m + (t % (g.group * nNt)) % gs, nt = (t % (g.group * nNt)) / gs;
-  const int m0 = mt * BM, n0 = nt * BN;
+  const int m0 = mt * BM, n0 = g.noff + nt * BN;
   const int KT = g.K / BK;
 
   auto load_stage = [&](int stage, int kt) {
@@ -356,6 +357,7 @@ struct FinArgs {
   const double *part_obj, *part_p, *part_line;
   int nMt1, nMt2;
   long ld, B;
+  long n0, n1;  // instances [n0, n1) of this launch
   const double *D;
   double *lam, *sl1, *sl2;
   int *status;
@@ -373,8 +375,8 @@ __device__ __forceinline__ bool valid_bound(double g) { return isfinite(g) && fa
 
 template <bool EVAL>
 __global__ void k_finish(const FinArgs f) {
-  const long n = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= f.ld) return;
+  const long n = f.n0 + (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= f.n1) return;
   double so = 0.0, sp = 0.0, sl = 0.0;
   for (int t = 0; t < f.nMt1; ++t) {
     so += f.part_obj[(size_t)t * f.ld + n];
@@ -532,6 +534,11 @@ struct PtdfState {
   double *os[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // s1p s2p s1m s2m sl1 sl2
   double *scratch = nullptr;
   size_t scratch_bytes = 0;
+  // iterate(): the batch's column blocks in `nsplit` groups on their own streams,
+  // so one group's GEMM tail overlaps the other's (instances are independent)
+  int nsplit = 2;
+  cudaStream_t sub[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -738,6 +745,8 @@ FinArgs fin_args(PtdfState *st) {
   f.nMt2 = (int)(st->nlp / BM);
   f.ld = st->Bp;
   f.B = st->B;
+  f.n0 = 0;
+  f.n1 = st->Bp;
   f.D = st->D;
   f.lam = st->lam;
   f.sl1 = st->os[4];
@@ -783,6 +792,7 @@ int ptdf_create(const PtdfNetIn &net, int device, PtdfState **out, std::string *
   if (net.a)
     for (int g = 0; g < net.ng; ++g) st->quadratic |= net.a[g] > 0.0;
   if (const char *ev = getenv("DCOPF_PTDF_GROUP")) st->group = std::max(1, atoi(ev));
+  if (const char *ev = getenv("DCOPF_PTDF_SPLIT")) st->nsplit = std::max(1, std::min(2, atoi(ev)));  // measurement
   st->nlp = up(net.nl, BM);
   st->nlk = up(net.nl, BK);
   st->ngp = up(net.ng, BM);
@@ -980,6 +990,11 @@ void ptdf_destroy(PtdfState *st) {
   free_batch(st);
   double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch};
   for (double *p : dp) cudaFree(p);
+  for (int c = 0; c < 2; ++c) {
+    if (st->sub[c]) cudaStreamDestroy(st->sub[c]);
+    if (st->ev_join[c]) cudaEventDestroy(st->ev_join[c]);
+  }
+  if (st->ev_fork) cudaEventDestroy(st->ev_fork);
   cudaFree(st->flag);
   delete st;
 }
@@ -1045,29 +1060,63 @@ int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist
   f.k_base = st->k_base;
   f.target = st->has_target ? st->target : nullptr;
   f.hit = st->hit;
-  const int fb = blocks_for(st->Bp);
+  // column groups: nsplit contiguous ranges of whole N tiles, one stream each
+  const int ntiles = (int)(st->Bp / BN);
+  const int ns = std::max(1, std::min(st->nsplit, ntiles));
+  if (ns > 1 && !st->ev_fork) {
+    for (int c = 0; c < 2; ++c) {
+      PCK(cudaStreamCreateWithFlags(&st->sub[c], cudaStreamNonBlocking));
+      PCK(cudaEventCreateWithFlags(&st->ev_join[c], cudaEventDisableTiming));
+    }
+    PCK(cudaEventCreateWithFlags(&st->ev_fork, cudaEventDisableTiming));
+  }
+  GemmArgs G1[2], G2[2];
+  FinArgs Fc[2];
+  cudaStream_t ss[2] = {s, s};
+  for (int c = 0; c < ns; ++c) {
+    const int t0 = ntiles * c / ns, t1 = ntiles * (c + 1) / ns;
+    G1[c] = g1;
+    G2[c] = g2;
+    Fc[c] = f;
+    G1[c].noff = G2[c].noff = t0 * BN;
+    G1[c].N = G2[c].N = (t1 - t0) * BN;
+    Fc[c].n0 = (long)t0 * BN;
+    Fc[c].n1 = (long)t1 * BN;
+    if (ns > 1) ss[c] = st->sub[c];
+  }
+  if (ns > 1) {
+    PCK(cudaEventRecord(st->ev_fork, s));
+    for (int c = 0; c < ns; ++c) PCK(cudaStreamWaitEvent(st->sub[c], st->ev_fork, 0));
+  }
   for (int64_t k = 0; k <= K; ++k) {
-    int rc = launch_gemm<EPI_GEN>(g1, s, err);
-    if (rc) return rc;
     const bool step = k < K;
     if (step && st->opt.variant == DCOPF_OPT_ADAM) {  // beta^t by repeated products (reading A-26)
       st->b1t = st->b1t * st->opt.beta1;
       st->b2t = st->b2t * st->opt.beta2;
     }
-    g2.k = (int)k;
-    g2.b1t = f.b1t = st->b1t;
-    g2.b2t = f.b2t = st->b2t;
-    if (step) {
-      rc = launch_gemm<EPI_LINE_STEP>(g2, s, err);
-    } else {  // the final evaluation at y_K: the value's line terms only, no step
-      rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
+    for (int c = 0; c < ns; ++c) {
+      int rc = launch_gemm<EPI_GEN>(G1[c], ss[c], err);
+      if (rc) return rc;
+      G2[c].k = (int)k;
+      G2[c].b1t = Fc[c].b1t = st->b1t;
+      G2[c].b2t = Fc[c].b2t = st->b2t;
+      if (step) {
+        rc = launch_gemm<EPI_LINE_STEP>(G2[c], ss[c], err);
+      } else {  // the final evaluation at y_K: the value's line terms only, no step
+        rc = launch_gemm<EPI_LINE_EVAL>(G2[c], ss[c], err);
+      }
+      if (rc) return rc;
+      Fc[c].k = (int)k;
+      Fc[c].first = k == 0;
+      k_finish<false><<<blocks_for(Fc[c].n1 - Fc[c].n0), 256, 0, ss[c]>>>(Fc[c]);
+      PCK(cudaGetLastError());
     }
-    if (rc) return rc;
-    f.k = (int)k;
-    f.first = k == 0;
-    k_finish<false><<<fb, 256, 0, s>>>(f);
-    PCK(cudaGetLastError());
   }
+  if (ns > 1)
+    for (int c = 0; c < ns; ++c) {
+      PCK(cudaEventRecord(st->ev_join[c], st->sub[c]));
+      PCK(cudaStreamWaitEvent(s, st->ev_join[c], 0));
+    }
   st->k_base += K;
   return DCOPF_OK;
 }
