@@ -250,6 +250,20 @@ int dcopf_dual_set_target(dcopf_dual_t h, const double *target, void *cuda_strea
 /* hit[B] (int64): the first evaluation index reaching the target, or -1. */
 int dcopf_dual_get_first_hit(dcopf_dual_t h, int64_t *hit, void *cuda_stream);
 
+/* Batch compaction (the branch-and-bound use of the bound,
+ * PAPER.md:25, 63): drops every instance whose status is DIVERGED or CONVERGED
+ * and packs the remaining (OK) instances, in their current order, into a
+ * smaller batch -- fewer tiles / clusters / CTAs per later iterate() call.
+ * Each kept instance keeps its multipliers, optimiser state, best, target and
+ * first hit, loads and outages, so its later results are bitwise those of an
+ * uncompacted run.  kept[j] (host or device, capacity = B before the call, or
+ * NULL) receives the pre-compaction index of new instance j; *n_kept (or NULL)
+ * their number.  Afterwards every call sees the packed batch (B = n_kept):
+ * read the retiring instances' results BEFORE compacting.  If no instance is
+ * frozen, or none is OK, the batch is left as it is (n_kept = B, resp. 0).
+ * Not for the PTDF form (EINVAL).  Errors: ESTATE (no batch), ENOMEM, ECUDA. */
+int dcopf_dual_compact(dcopf_dual_t h, int64_t *kept, int64_t *n_kept, void *cuda_stream);
+
 /* Static facts about the handle, for reporting. */
 typedef struct {
   int64_t B;                      /* instances loaded (0 before set_instance_batch) */

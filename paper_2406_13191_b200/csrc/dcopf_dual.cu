@@ -1350,6 +1350,106 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
   return DCOPF_OK;
 }
 
+int dcopf_dual_compact(dcopf_dual_t h, int64_t *kept, int64_t *n_kept, void *cuda_stream) {
+  if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
+  if (h->B == 0) return fail(h, DCOPF_ESTATE, "no batch loaded");
+  if (h->pt) return fail(h, DCOPF_EINVAL, "compaction runs on the sparse forms' paths");
+  CK(h, cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  std::vector<int32_t> st(h->B);
+  CK(h, cudaMemcpyAsync(st.data(), h->status, h->B * 4, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  std::vector<long long> act;
+  for (long b = 0; b < h->B; ++b)
+    if (st[b] == DCOPF_INST_OK) act.push_back(b);
+  const long nk = (long)act.size();
+  if (n_kept) *n_kept = nk;
+  if (nk == 0 || nk == h->B) {  // nothing to drop, or nothing left: the batch stays as it is
+    if (kept && nk > 0) {
+      std::vector<int64_t> id(act.begin(), act.end());
+      CK(h, cudaMemcpyAsync(kept, id.data(), nk * 8, cudaMemcpyDefault, s));
+      CK(h, cudaStreamSynchronize(s));
+    }
+    return DCOPF_OK;
+  }
+  const int T = h->T;
+  const long B_pad = (nk + T - 1) / T * T;
+  std::vector<long long> slot(B_pad, -1);
+  std::copy(act.begin(), act.end(), slot.begin());
+  long long *d_slot = nullptr;
+  CK(h, cudaMalloc(&d_slot, B_pad * 8));
+  int rc = DCOPF_OK;
+  std::vector<void *> old;  // freed after the gathers have run
+  auto done = [&](int code) {
+    cudaStreamSynchronize(s);
+    for (void *p : old) cudaFree(p);
+    cudaFree(d_slot);
+    return code;
+  };
+  if (cudaMemcpyAsync(d_slot, slot.data(), B_pad * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return done(fail(h, DCOPF_ECUDA, "compact: slot upload failed"));
+  // tile-major state: multipliers (current buffer), loads, optimiser state
+  const int rows_br = h->n_bm_ent * h->bm_C;
+  struct TA {
+    double **p;
+    int rows;
+  } tiles[] = {{&h->lam[h->cur], h->n_bus}, {&h->br[h->cur], rows_br}, {&h->load, h->n_bus},
+               {&h->os[0], h->n_bus},       {&h->os[1], h->n_bus},      {&h->os[2], rows_br},
+               {&h->os[3], rows_br}};
+  for (auto &ta : tiles) {
+    if (!*ta.p) continue;
+    double *nw = nullptr;
+    if (cudaMalloc(&nw, std::max<size_t>((size_t)B_pad * ta.rows, 1) * 8) != cudaSuccess)
+      return done(fail(h, DCOPF_ENOMEM, "compact: cudaMalloc failed"));
+    k_gather_tiles<<<grid_for((size_t)B_pad * ta.rows), 256, 0, s>>>(*ta.p, nw, ta.rows, T, d_slot, B_pad);
+    old.push_back(*ta.p);
+    *ta.p = nw;
+  }
+  // per-instance rows: bound, best, status, target, hit, outages
+  auto gd = [&](double **p, double fill) -> int {
+    double *nw = nullptr;
+    if (cudaMalloc(&nw, B_pad * 8) != cudaSuccess) return fail(h, DCOPF_ENOMEM, "compact: cudaMalloc failed");
+    k_gather_rows<double><<<grid_for(B_pad), 256, 0, s>>>(*p, nw, 1, d_slot, B_pad, fill);
+    old.push_back(*p);
+    *p = nw;
+    return (int)DCOPF_OK;
+  };
+  const double inf = std::numeric_limits<double>::infinity();
+  if (!rc) rc = gd(&h->bound, std::numeric_limits<double>::quiet_NaN());
+  if (!rc) rc = gd(&h->best, -inf);
+  if (!rc) rc = gd(&h->target, inf);
+  if (!rc) {
+    int *ns = nullptr, *no = nullptr;
+    long long *nh = nullptr;
+    const size_t wo = std::max<size_t>((size_t)B_pad * h->max_out, 1);
+    if (cudaMalloc(&ns, B_pad * 4) != cudaSuccess || cudaMalloc(&nh, B_pad * 8) != cudaSuccess ||
+        cudaMalloc(&no, wo * 4) != cudaSuccess)
+      return done(fail(h, DCOPF_ENOMEM, "compact: cudaMalloc failed"));
+    k_gather_rows<int><<<grid_for(B_pad), 256, 0, s>>>(h->status, ns, 1, d_slot, B_pad, 0);
+    k_gather_rows<long long><<<grid_for(B_pad), 256, 0, s>>>(h->hit, nh, 1, d_slot, B_pad, -1LL);
+    if (h->max_out > 0) k_gather_rows<int><<<grid_for(wo), 256, 0, s>>>(h->outs, no, h->max_out, d_slot, B_pad, -1);
+    old.push_back(h->status);
+    old.push_back(h->hit);
+    old.push_back(h->outs);
+    h->status = ns;
+    h->hit = nh;
+    h->outs = no;
+  }
+  // scratch sized for the old batch stays valid (larger); value / gradients are recomputed
+  if (!rc && cudaGetLastError() != cudaSuccess) rc = fail(h, DCOPF_ECUDA, "compact: kernel launch failed");
+  if (!rc && kept) {
+    std::vector<int64_t> id(act.begin(), act.end());
+    if (cudaMemcpyAsync(kept, id.data(), nk * 8, cudaMemcpyDefault, s) != cudaSuccess)
+      rc = fail(h, DCOPF_ECUDA, "compact: kept copy failed");
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess && !rc) rc = fail(h, DCOPF_ECUDA, "compact: synchronize failed");
+  if (!rc) {
+    h->B = nk;
+    h->B_pad = B_pad;
+  }
+  return done(rc);
+}
+
 int dcopf_dual_get_ptdf(dcopf_dual_t h, double *Ha, void *cuda_stream) {
   if (!h) return fail(nullptr, DCOPF_EINVAL, "null handle");
   if (!h->pt) return fail(h, DCOPF_EINVAL, "dcopf_dual_get_ptdf needs the PTDF form");

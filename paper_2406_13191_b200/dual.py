@@ -68,7 +68,7 @@ class Optimizer(ctypes.Structure):
 
 SYMBOLS = ["dcopf_dual_create", "dcopf_dual_set_instance_batch", "dcopf_dual_iterate",
            "dcopf_dual_get_bound", "dcopf_dual_get_multipliers", "dcopf_dual_set_multipliers",
-           "dcopf_dual_evaluate", "dcopf_dual_set_optimizer", "dcopf_dual_set_stop", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info", "dcopf_dual_get_ptdf",
+           "dcopf_dual_evaluate", "dcopf_dual_set_optimizer", "dcopf_dual_set_stop", "dcopf_dual_set_target", "dcopf_dual_get_first_hit", "dcopf_dual_get_info", "dcopf_dual_get_ptdf", "dcopf_dual_compact",
            "dcopf_dual_last_error", "dcopf_dual_destroy"]
 
 _lib = None
@@ -101,6 +101,8 @@ def load_library(path: Optional[str] = None):
     lib.dcopf_dual_get_info.argtypes = [P, ctypes.POINTER(Info)]
     if hasattr(lib, "dcopf_dual_get_ptdf"):
         lib.dcopf_dual_get_ptdf.argtypes = [P, P, P]
+    if hasattr(lib, "dcopf_dual_compact"):
+        lib.dcopf_dual_compact.argtypes = [P, P, P, P]
     lib.dcopf_dual_last_error.argtypes = [P]
     lib.dcopf_dual_last_error.restype = ctypes.c_char_p
     lib.dcopf_dual_destroy.argtypes = [P]
@@ -238,6 +240,16 @@ class DcopfDual:
             hit = np.empty(self.B, dtype=np.int64)
         self._check(self.lib.dcopf_dual_get_first_hit(self.h, _ptr(hit), _stream(stream)))
         return hit
+
+    def compact(self, stream=None):
+        """Drop the frozen (DIVERGED / CONVERGED) instances; returns the
+        pre-compaction indices of the kept ones (their new order)."""
+        kept = np.empty(self.B, dtype=np.int64)
+        n = ctypes.c_int64(0)
+        self._check(self.lib.dcopf_dual_compact(self.h, _ptr(kept), ctypes.byref(n), _stream(stream)))
+        if 0 < n.value < self.B:
+            self.B = int(n.value)
+        return kept[:n.value].copy()
 
     def get_ptdf(self, Ha=None, stream=None):
         """PTDF form: the library's H_a [n_branch][n_bus]."""
