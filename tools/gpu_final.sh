@@ -13,3 +13,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --cs
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -c 1 -o gpurun_out/final/ncu_k_sweep_config4_F2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-gap > /dev/null 2>&1; echo n1=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -c 1 -o gpurun_out/final/ncu_k_sweep_config4_KVL python bench.py --form KVL --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-gap > /dev/null 2>&1; echo n2=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cluster -c 1 -o gpurun_out/final/ncu_k_cluster_config3_F2 python bench.py --workload config3 --steps 100 --warmup 400 --no-cpu-baseline --no-e2e --no-gap > /dev/null 2>&1; echo n3=$?
+python bench.py --workload config4b --form PTDF --steps 30 --warmup 3 --no-gap > gpurun_out/final/bench_config4b_PTDF.json 2> gpurun_out/final/bench_config4b_PTDF.err; echo b_ptdf=$?
+python bench.py --workload config4b --steps 100 --warmup 10 --no-cpu-baseline > gpurun_out/final/bench_config4b_F2.json 2>&1; echo b4b=$?
