@@ -122,6 +122,16 @@ __device__ __forceinline__ double opt_step(const GemmArgs &g, double y, double g
   }
 }
 
+// p* = argmin over [lo, hi] of a p^2 + q p: clip(-q / 2a) (reading A-6), else
+// bound selection with sign(0) -> midpoint (reading A-4)
+__device__ __forceinline__ double minimiser(double q, double lo, double hi, double a) {
+  if (a > 0.0) {
+    const double x = -q / (2.0 * a);
+    return (x < lo) ? lo : ((x > hi) ? hi : x);
+  }
+  return (q > 0.0) ? lo : ((q < 0.0) ? hi : 0.5 * (lo + hi));
+}
+
 // one CTA per 128 x 128 output tile, grouped raster (`group` M-tiles per band,
 // M fastest inside a band) so concurrently running CTAs share A and B tiles in L2
 template <int EPI>
@@ -222,13 +232,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const double q = (c + lamv[j][e]) + acc[i][j][e];  // q = c + lambda 1 + H_g^T nu
-          double p;
-          if (a > 0.0) {  // clip(-q / 2a) (reading A-6)
-            const double x = -q / (2.0 * a);
-            p = (x < lo) ? lo : ((x > hi) ? hi : x);
-          } else {        // bound selection, sign(0) -> midpoint (reading A-4)
-            p = (q > 0.0) ? lo : ((q < 0.0) ? hi : 0.5 * (lo + hi));
-          }
+          double p = minimiser(q, lo, hi, a);
           if (!live) p = 0.0;
           pv[e] = p;
           if (live) {
@@ -349,6 +353,142 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
       g.part_line[o] = so;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Skinny batches (B <= 16, e.g. one large instance): the two products are
+// matrix-vector shaped, so they are HBM-bound reads of H_g, not tensor work.
+// k_gemv_part: out[s][m][b] = sum_{k in chunk s} A[k][m] X[k][b] with A
+// row-major over m (coalesced double2 per thread), X[k][0..NB) broadcast to
+// the block; the epilogue kernels sum the S chunks in order (deterministic).
+// GEMM1 uses A = H_g [n_l][n_g] (m = generator), GEMM2 A = H_g^T (m = line).
+constexpr int VT = 256;  // threads per block of the skinny kernels
+
+template <int NB>
+__global__ void __launch_bounds__(VT) k_gemv_part(const double *__restrict__ A, long lda, int M, int K,
+                                                  const double *__restrict__ X, long ldx, int S,
+                                                  double *__restrict__ out, long Mp) {
+  const int nMb = (M + 2 * VT - 1) / (2 * VT);
+  const int mb = blockIdx.x % nMb, sidx = blockIdx.x / nMb;
+  const int m = (mb * VT + threadIdx.x) * 2;
+  const int kc = (K + S - 1) / S, k0 = sidx * kc, k1 = min(K, k0 + kc);
+  double acc0[NB], acc1[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.0;
+  if (m < M) {
+    for (int k = k0; k < k1; ++k) {
+      const double2 a = *reinterpret_cast<const double2 *>(A + (size_t)k * lda + m);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const double x = X[(size_t)k * ldx + b];
+        acc0[b] += a.x * x;
+        acc1[b] += a.y * x;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      out[((size_t)sidx * Mp + m) * NB + b] = acc0[b];
+      out[((size_t)sidx * Mp + m + 1) * NB + b] = acc1[b];
+    }
+  }
+}
+
+// block sums of v[NB] in a fixed order -> part[blockIdx][b] (ld = B_pad)
+template <int NB>
+__device__ __forceinline__ void block_sums(double (&v)[NB], double *part, long ld, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v[b] += __shfl_xor_sync(0xffffffffu, v[b], off);
+    if (lane == 0) red[warp * NB + b] = v[b];
+  }
+  __syncthreads();
+  if (threadIdx.x < NB) {
+    double t = 0.0;
+    for (int w = 0; w < VT / 32; ++w) t += red[w * NB + threadIdx.x];
+    part[(size_t)blockIdx.x * ld + threadIdx.x] = t;
+  }
+}
+
+// GEMM1 epilogue, one thread per generator row g < ngk
+template <int NB>
+__global__ void __launch_bounds__(VT) k_gen_epi(const GemmArgs g, const double *__restrict__ q_part, int S, long Mp) {
+  __shared__ double red[VT / 32 * NB];
+  const int row = blockIdx.x * VT + threadIdx.x;
+  const bool live = row < g.ng;
+  double so[NB], sp[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) so[b] = sp[b] = 0.0;
+  if (row < Mp) {
+    const double c = live ? g.gc[row] : 0.0, lo = live ? g.glo[row] : 0.0, hi = live ? g.ghi[row] : 0.0;
+    const double a = (live && g.ga) ? g.ga[row] : 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double Q = 0.0;
+      for (int x = 0; x < S; ++x) Q += q_part[((size_t)x * Mp + row) * NB + b];
+      const double q = (c + g.lam[b]) + Q;  // q = c + lambda 1 + H_g^T nu
+      const double p = live ? minimiser(q, lo, hi, a) : 0.0;
+      g.P[(size_t)row * g.ld + b] = p;
+      if (live) {
+        so[b] += a * p * p + q * p;
+        sp[b] += p;
+      }
+    }
+  }
+  block_sums<NB>(so, g.part_obj, g.ld, red);
+  __syncthreads();
+  block_sums<NB>(sp, g.part_p, g.ld, red);
+}
+
+// GEMM2 epilogue, one thread per line row l < nl: gradient, value terms, projected step
+template <int NB, bool STEP>
+__global__ void __launch_bounds__(VT) k_line_epi(const GemmArgs g, const double *__restrict__ y_part, int S, long Mp) {
+  __shared__ double red[VT / 32 * NB];
+  const int row = blockIdx.x * VT + threadIdx.x;
+  double sv[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) sv[b] = 0.0;
+  if (row < g.nl) {
+    const double F = g.F[row];
+    const double al = STEP ? g.alpha[g.k] : 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double y = 0.0;
+      for (int x = 0; x < S; ++x) y += y_part[((size_t)x * Mp + row) * NB + b];
+      const size_t o = (size_t)row * g.ld + b;
+      const double r = g.r[o], mp = g.mup[o], mm = g.mum[o];
+      const double gp = (y - r) - F, gm = (r - y) - F;
+      sv[b] += mm * (r - F) - mp * (r + F);
+      if (!STEP) {
+        if (g.gp_out) {
+          g.gp_out[o] = gp;
+          g.gm_out[o] = gm;
+        }
+      } else if (g.status[b] == 0) {
+        double vp, vm;
+        if (g.opt == 0) {
+          vp = mp + al * gp;
+          vm = mm + al * gm;
+        } else {
+          double a1 = g.s1p[o], a2 = g.s2p ? g.s2p[o] : 0.0, b1 = g.s1m[o], b2 = g.s2m ? g.s2m[o] : 0.0;
+          vp = opt_step(g, mp, gp, al, a1, a2);
+          vm = opt_step(g, mm, gm, al, b1, b2);
+          g.s1p[o] = a1;
+          g.s1m[o] = b1;
+          if (g.s2p) {
+            g.s2p[o] = a2;
+            g.s2m[o] = b2;
+          }
+        }
+        const double np = vp > 0.0 ? vp : 0.0, nm = vm > 0.0 ? vm : 0.0;  // mu <- max(mu, 0)
+        g.mup[o] = np;
+        g.mum[o] = nm;
+        g.nu[o] = np - nm;
+      }
+    }
+  }
+  block_sums<NB>(sv, g.part_line, g.ld, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -537,6 +677,9 @@ struct PtdfState {
   // iterate(): the batch's column blocks in `nsplit` groups on their own streams,
   // so one group's GEMM tail overlaps the other's (instances are independent)
   int nsplit = 2;
+  // skinny batches (B <= 16): matrix-vector kernels; nbv = instance columns computed (0: GEMM mode)
+  int nbv = 0, S1 = 1, S2 = 1;
+  double *qpart = nullptr, *ypart = nullptr;
   cudaStream_t sub[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
 };
@@ -773,6 +916,51 @@ int copy_rows_out(PtdfState *st, double *dst, const double *src, long rows, cuda
   return DCOPF_OK;
 }
 
+template <int NB>
+int skinny_pass_t(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, cudaStream_t s,
+                  std::string *err) {
+  const int ng = st->ng, nl = st->nl;
+  if (ng > 0) {
+    const int nMb = (ng + 2 * VT - 1) / (2 * VT);
+    if (nl > 0)
+      k_gemv_part<NB><<<nMb * st->S1, VT, 0, s>>>(st->Hg, st->ngk, ng, nl, st->nu, st->Bp, st->S1, st->qpart,
+                                                  st->ngk);
+    k_gen_epi<NB><<<(int)((st->ngk + VT - 1) / VT), VT, 0, s>>>(g1, st->qpart, nl > 0 ? st->S1 : 0, st->ngk);
+  }
+  if (nl > 0) {
+    const int nMb = (nl + 2 * VT - 1) / (2 * VT);
+    if (ng > 0)
+      k_gemv_part<NB><<<nMb * st->S2, VT, 0, s>>>(st->HgT, st->nlk, nl, ng, st->P, st->Bp, st->S2, st->ypart,
+                                                  st->nlk);
+    const int eb = (nl + VT - 1) / VT, S = ng > 0 ? st->S2 : 0;
+    if (step)
+      k_line_epi<NB, true><<<eb, VT, 0, s>>>(g2, st->ypart, S, st->nlk);
+    else
+      k_line_epi<NB, false><<<eb, VT, 0, s>>>(g2, st->ypart, S, st->nlk);
+  }
+  PCK(cudaGetLastError());
+  return DCOPF_OK;
+}
+
+int skinny_pass(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, cudaStream_t s, std::string *err) {
+  switch (st->nbv) {
+    case 1: return skinny_pass_t<1>(st, g1, g2, step, s, err);
+    case 2: return skinny_pass_t<2>(st, g1, g2, step, s, err);
+    case 4: return skinny_pass_t<4>(st, g1, g2, step, s, err);
+    case 8: return skinny_pass_t<8>(st, g1, g2, step, s, err);
+    default: return skinny_pass_t<16>(st, g1, g2, step, s, err);
+  }
+}
+
+// partial-sum tiles the finisher reads: GEMM tiles, or the skinny epilogue blocks
+void fin_tiles(const PtdfState *st, FinArgs *f) {
+  if (st->nbv) {
+    f->nMt1 = st->ng > 0 ? (int)((st->ngk + VT - 1) / VT) : 0;
+    f->nMt2 = (st->nl + VT - 1) / VT;
+    f->n1 = st->B;
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -988,7 +1176,7 @@ void ptdf_destroy(PtdfState *st) {
   if (!st) return;
   cudaSetDevice(st->device);
   free_batch(st);
-  double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch};
+  double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch, st->qpart, st->ypart};
   for (double *p : dp) cudaFree(p);
   for (int c = 0; c < 2; ++c) {
     if (st->sub[c]) cudaStreamDestroy(st->sub[c]);
@@ -1024,6 +1212,19 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
   }
   st->B = B;
   st->Bp = Bp;
+  // skinny mode for B <= 16 (DCOPF_PTDF_SKINNY=0 forces the GEMMs; measurement)
+  st->nbv = 0;
+  const char *sk = getenv("DCOPF_PTDF_SKINNY");
+  if (B <= 16 && !(sk && atoi(sk) == 0)) {
+    st->nbv = B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : (B <= 8 ? 8 : 16)));
+    const int target = 4 * 148;
+    const int nMb1 = std::max(1, (st->ng + 2 * VT - 1) / (2 * VT)), nMb2 = std::max(1, (st->nl + 2 * VT - 1) / (2 * VT));
+    st->S1 = std::max(1, std::min(std::max(st->nl, 1), target / nMb1));
+    st->S2 = std::max(1, std::min(std::max(st->ng, 1), target / nMb2));
+    int rc0 = dalloc(&st->qpart, (size_t)st->S1 * st->ngk * 16, err);
+    if (!rc0) rc0 = dalloc(&st->ypart, (size_t)st->S2 * st->nlk * 16, err);
+    if (rc0) return rc0;
+  }
   // loads: [n_bus][B] -> Dm [nbk][Bp] (zero padded), r = H_a Dm, D = 1^T d
   const size_t dm = (size_t)st->nbk * Bp;
   int rc = ensure_scratch(st, dm * 8, err);
@@ -1060,6 +1261,27 @@ int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist
   f.k_base = st->k_base;
   f.target = st->has_target ? st->target : nullptr;
   f.hit = st->hit;
+  if (st->nbv) {  // skinny batch: matrix-vector passes on the caller's stream
+    fin_tiles(st, &f);
+    for (int64_t k = 0; k <= K; ++k) {
+      const bool step = k < K;
+      if (step && st->opt.variant == DCOPF_OPT_ADAM) {  // beta^t by repeated products (reading A-26)
+        st->b1t = st->b1t * st->opt.beta1;
+        st->b2t = st->b2t * st->opt.beta2;
+      }
+      g2.k = (int)k;
+      g2.b1t = f.b1t = st->b1t;
+      g2.b2t = f.b2t = st->b2t;
+      int rc = skinny_pass(st, g1, g2, step, s, err);
+      if (rc) return rc;
+      f.k = (int)k;
+      f.first = k == 0;
+      k_finish<false><<<1, 256, 0, s>>>(f);
+      PCK(cudaGetLastError());
+    }
+    st->k_base += K;
+    return DCOPF_OK;
+  }
   // column groups: nsplit contiguous ranges of whole N tiles, one stream each
   const int ntiles = (int)(st->Bp / BN);
   const int ns = std::max(1, std::min(st->nsplit, ntiles));
@@ -1177,14 +1399,19 @@ int ptdf_evaluate(PtdfState *st, double *value, double *grad_lambda, double *gra
   int rc = DCOPF_OK;
   if (!st->gp) rc = dalloc(&st->gp, (size_t)st->nlp * st->Bp, err);
   if (!rc && !st->gm) rc = dalloc(&st->gm, (size_t)st->nlp * st->Bp, err);
-  if (!rc) rc = launch_gemm<EPI_GEN>(gen_args(st), s, err);
   if (rc) return rc;
   GemmArgs g2 = line_args(st);
   g2.gp_out = st->gp;
   g2.gm_out = st->gm;
-  rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
+  if (st->nbv) {
+    rc = skinny_pass(st, gen_args(st), g2, false, s, err);
+  } else {
+    rc = launch_gemm<EPI_GEN>(gen_args(st), s, err);
+    if (!rc) rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
+  }
   if (rc) return rc;
   FinArgs f = fin_args(st);
+  fin_tiles(st, &f);
   f.glam_out = st->glam;
   k_finish<true><<<blocks_for(st->Bp), 256, 0, s>>>(f);
   PCK(cudaGetLastError());

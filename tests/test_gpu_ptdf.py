@@ -96,7 +96,11 @@ def test_ptdf_matrix(which):
 # the iteration
 
 
-def test_config0_full_K():
+@pytest.mark.parametrize("skinny", ["1", "0"])
+def test_config0_full_K(skinny, monkeypatch):
+    """B = 1: the matrix-vector kernels (skinny mode, default for B <= 16) and,
+    forced, the GEMM kernels on a 128-column tile."""
+    monkeypatch.setenv("DCOPF_PTDF_SKINNY", skinny)
     net = inst.make_network(0)
     K = inst.ITERS[0]
     a = inst.alpha_schedule(K)
@@ -105,6 +109,33 @@ def test_config0_full_K():
     assert_parity(net, gpu, orc)
     info = gpu["info"]
     assert info.path == dual.PATH_DENSE and info.form == dual.FORM_PTDF
+
+
+def _no_flow_lines(net, Ha, loads):
+    """Lines that carry no flow in any instance of the batch: zero H_g row, and
+    the load flow r = H_a d and the limit F at rounding level (reading A-30).
+    Their gradient is rounding noise, which Adam / AdaGrad rescale to O(alpha)
+    steps, so their mu walk differently on the two sides; they never reach the
+    bound (zero H_g row, r + F ~ 0)."""
+    Hg = Ha[:, net.gen_bus]
+    r = np.abs(loads @ Ha.T).max(axis=0)
+    m = (np.abs(Hg).max(axis=1) < 1e-12) & (r < 1e-9) & (net.br_fmax < 1e-9)
+    return np.r_[m, m]
+
+
+@pytest.mark.parametrize("B", [1, 3, 9, 16])
+def test_skinny_batches_config1_adam(B):
+    """Skinny mode at every column count class (1, 4, 16 columns computed), Adam."""
+    net = inst.make_network(1)
+    Ha = P.ptdf(net)
+    K = 300
+    a = inst.alpha_schedule(K, 0.1)
+    loads = _scaled_loads(net, B, 17)
+    gpu = _gpu(net, loads, K, a, opt=ADAM, split=120)
+    orc = _orc(net, loads, K, a, Ha=Ha, opt=ADAM)
+    noflow = _no_flow_lines(net, Ha, loads)
+    assert 0 < noflow.sum() < 0.05 * noflow.size
+    assert_parity(net, gpu, orc, br_mask=~noflow)
 
 
 @pytest.mark.parametrize("B", [1, 130, 300])
