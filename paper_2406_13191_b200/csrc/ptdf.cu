@@ -357,109 +357,148 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
 
 // ---------------------------------------------------------------------------
 // Skinny batches (B <= 16, e.g. one large instance): the two products are
-// matrix-vector shaped, so they are HBM-bound reads of H_g, not tensor work.
-// k_gemv_part: out[s][m][b] = sum_{k in chunk s} A[k][m] X[k][b] with A
-// row-major over m (coalesced double2 per thread), X[k][0..NB) broadcast to
-// the block; the epilogue kernels sum the S chunks in order (deterministic).
-// GEMM1 uses A = H_g [n_l][n_g] (m = generator), GEMM2 A = H_g^T (m = line).
-constexpr int VT = 256;  // threads per block of the skinny kernels
+// matrix-vector shaped, i.e. HBM-bound reads of H_g (254 MB at config 3), not
+// tensor work.  One warp per row, coalesced double2 loads along the row, the
+// vector in a compact [K][NB] copy (nu_c, p_c: L1/L2 resident), a fixed xor
+// tree for the dot product, and the epilogue fused: GEMM1 rows are generators
+// (A = H_g^T, row g, K = n_l), GEMM2 rows are lines (A = H_g, row l, K = n_g).
+// Each block writes its partial sums per instance to part[block][b] (ld NB).
+constexpr int VT = 512, VW = VT / 32;   // threads and warps per block
+constexpr int WPR_G = 4, WPR_L = 1;      // warps per row: GEMM1 rows are 100 KB (config 3), GEMM2 rows 20 KB
 
 template <int NB>
-__global__ void __launch_bounds__(VT) k_gemv_part(const double *__restrict__ A, long lda, int M, int K,
-                                                  const double *__restrict__ X, long ldx, int S,
-                                                  double *__restrict__ out, long Mp) {
-  const int nMb = (M + 2 * VT - 1) / (2 * VT);
-  const int mb = blockIdx.x % nMb, sidx = blockIdx.x / nMb;
-  const int m = (mb * VT + threadIdx.x) * 2;
-  const int kc = (K + S - 1) / S, k0 = sidx * kc, k1 = min(K, k0 + kc);
-  double acc0[NB], acc1[NB];
+__device__ __forceinline__ void warp_dot(const double *__restrict__ row, const double *__restrict__ xc, int k0,
+                                         int K, double (&acc)[NB]) {
+  const int lane = threadIdx.x & 31;
+  // four independent accumulator sets (k strides of 64, 4 deep) keep four
+  // row loads in flight per lane; combined in a fixed order
+  double part[4][NB];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.0;
-  if (m < M) {
-    for (int k = k0; k < k1; ++k) {
-      const double2 a = *reinterpret_cast<const double2 *>(A + (size_t)k * lda + m);
+  for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const double x = X[(size_t)k * ldx + b];
-        acc0[b] += a.x * x;
-        acc1[b] += a.y * x;
-      }
-    }
+    for (int b = 0; b < NB; ++b) part[u][b] = 0.0;
+  int k = k0 + 2 * lane;
+  for (; k + 192 < K; k += 256) {
+    double2 a[4];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      out[((size_t)sidx * Mp + m) * NB + b] = acc0[b];
-      out[((size_t)sidx * Mp + m + 1) * NB + b] = acc1[b];
+    for (int u = 0; u < 4; ++u) a[u] = *reinterpret_cast<const double2 *>(row + k + 64 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int kk = k + 64 * u;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) part[u][b] += a[u].x * xc[kk * NB + b] + a[u].y * xc[(kk + 1) * NB + b];
     }
   }
+  for (int u = 0; k < K; k += 64, ++u) {
+    const double2 a = *reinterpret_cast<const double2 *>(row + k);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) part[u & 3][b] += a.x * xc[k * NB + b] + a.y * xc[(k + 1) * NB + b];
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = (part[0][b] + part[1][b]) + (part[2][b] + part[3][b]);
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
 }
 
-// block sums of v[NB] in a fixed order -> part[blockIdx][b] (ld = B_pad)
+// block partial sums: per-warp values red[warp][b] summed in warp order
 template <int NB>
-__device__ __forceinline__ void block_sums(double (&v)[NB], double *part, long ld, double *red) {
+__device__ __forceinline__ void block_part(double *red, const double (&v)[NB], double *part) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane < NB) {
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v[b] += __shfl_xor_sync(0xffffffffu, v[b], off);
-    if (lane == 0) red[warp * NB + b] = v[b];
+    for (int b = 0; b < NB; ++b)
+      if (b == lane) red[warp * NB + b] = v[b];
   }
   __syncthreads();
   if (threadIdx.x < NB) {
     double t = 0.0;
-    for (int w = 0; w < VT / 32; ++w) t += red[w * NB + threadIdx.x];
-    part[(size_t)blockIdx.x * ld + threadIdx.x] = t;
+    for (int w = 0; w < VW; ++w) t += red[w * NB + threadIdx.x];
+    part[(size_t)blockIdx.x * NB + threadIdx.x] = t;
   }
 }
 
-// GEMM1 epilogue, one thread per generator row g < ngk
+// the row's K range split over WPR warps (64-aligned); their dot products are
+// combined in warp order through shared memory (deterministic)
+template <int NB, int WPR>
+__device__ __forceinline__ void row_dot(const GemmArgs &g, int row, bool live, const double *__restrict__ xc,
+                                        double (*rp)[NB], double (&acc)[NB]) {
+  const int warp = threadIdx.x >> 5, q = warp % WPR;
+  const int Kq = ((g.K + WPR * 64 - 1) / (WPR * 64)) * 64;
+  const int k0 = q * Kq, k1 = min(g.K, k0 + Kq);
+  double a[NB];
+  if (live) warp_dot<NB>(g.A + (size_t)row * g.lda, xc, k0, k1, a);
+  else
+#pragma unroll
+    for (int b = 0; b < NB; ++b) a[b] = 0.0;
+  if (WPR > 1) {
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) rp[warp][b] = a[b];
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double t = rp[warp - q][b];
+      for (int j = 1; j < WPR; ++j) t += rp[warp - q + j][b];
+      acc[b] = t;
+    }
+  } else {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = a[b];
+  }
+}
+
 template <int NB>
-__global__ void __launch_bounds__(VT) k_gen_epi(const GemmArgs g, const double *__restrict__ q_part, int S, long Mp) {
-  __shared__ double red[VT / 32 * NB];
-  const int row = blockIdx.x * VT + threadIdx.x;
+__global__ void __launch_bounds__(VT) k_gen_row(const GemmArgs g, const double *__restrict__ nuc,
+                                                double *__restrict__ pc) {
+  __shared__ double red[2][VW * NB];
+  __shared__ double rp[VW][NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * (VW / WPR_G) + warp / WPR_G;
   const bool live = row < g.ng;
-  double so[NB], sp[NB];
+  double so[NB], sp[NB], acc[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) so[b] = sp[b] = 0.0;
-  if (row < Mp) {
-    const double c = live ? g.gc[row] : 0.0, lo = live ? g.glo[row] : 0.0, hi = live ? g.ghi[row] : 0.0;
-    const double a = (live && g.ga) ? g.ga[row] : 0.0;
+  row_dot<NB, WPR_G>(g, row, live, nuc, rp, acc);  // (H_g^T nu)_g
+  if (live && warp % WPR_G == 0) {
+    const double c = g.gc[row], lo = g.glo[row], hi = g.ghi[row], a = g.ga ? g.ga[row] : 0.0;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      double Q = 0.0;
-      for (int x = 0; x < S; ++x) Q += q_part[((size_t)x * Mp + row) * NB + b];
-      const double q = (c + g.lam[b]) + Q;  // q = c + lambda 1 + H_g^T nu
-      const double p = live ? minimiser(q, lo, hi, a) : 0.0;
-      g.P[(size_t)row * g.ld + b] = p;
-      if (live) {
-        so[b] += a * p * p + q * p;
-        sp[b] += p;
-      }
+      const double q = (c + g.lam[b]) + acc[b];
+      const double p = minimiser(q, lo, hi, a);
+      if (lane == b) pc[(size_t)row * NB + b] = p;
+      so[b] += a * p * p + q * p;
+      sp[b] += p;
     }
   }
-  block_sums<NB>(so, g.part_obj, g.ld, red);
-  __syncthreads();
-  block_sums<NB>(sp, g.part_p, g.ld, red);
+  block_part<NB>(red[0], so, g.part_obj);
+  block_part<NB>(red[1], sp, g.part_p);
 }
 
-// GEMM2 epilogue, one thread per line row l < nl: gradient, value terms, projected step
 template <int NB, bool STEP>
-__global__ void __launch_bounds__(VT) k_line_epi(const GemmArgs g, const double *__restrict__ y_part, int S, long Mp) {
-  __shared__ double red[VT / 32 * NB];
-  const int row = blockIdx.x * VT + threadIdx.x;
-  double sv[NB];
+__global__ void __launch_bounds__(VT) k_line_row(const GemmArgs g, const double *__restrict__ pcv,
+                                                 double *__restrict__ nuc) {
+  __shared__ double red[VW * NB];
+  __shared__ double rp[VW][NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * (VW / WPR_L) + warp / WPR_L;
+  const bool live = row < g.nl;
+  double sv[NB], acc[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) sv[b] = 0.0;
-  if (row < g.nl) {
-    const double F = g.F[row];
+  row_dot<NB, WPR_L>(g, row, live, pcv, rp, acc);  // (H_g p*)_l
+  if (live && warp % WPR_L == 0) {
     const double al = STEP ? g.alpha[g.k] : 0.0;
+    const double F = g.F[row];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      double y = 0.0;
-      for (int x = 0; x < S; ++x) y += y_part[((size_t)x * Mp + row) * NB + b];
       const size_t o = (size_t)row * g.ld + b;
+      const double y = acc[b];
       const double r = g.r[o], mp = g.mup[o], mm = g.mum[o];
-      const double gp = (y - r) - F, gm = (r - y) - F;
       sv[b] += mm * (r - F) - mp * (r + F);
+      if (lane != b) continue;  // lane b owns instance b of this row
+      const double gp = (y - r) - F, gm = (r - y) - F;
       if (!STEP) {
         if (g.gp_out) {
           g.gp_out[o] = gp;
@@ -485,10 +524,17 @@ __global__ void __launch_bounds__(VT) k_line_epi(const GemmArgs g, const double 
         g.mup[o] = np;
         g.mum[o] = nm;
         g.nu[o] = np - nm;
+        nuc[(size_t)row * NB + b] = np - nm;
       }
     }
   }
-  block_sums<NB>(sv, g.part_line, g.ld, red);
+  block_part<NB>(red, sv, g.part_line);
+}
+
+// compact copy nu_c[l][b] = nu[l][b] (after set_batch / set_multipliers)
+__global__ void k_compact_nu(const double *nu, long ld, int nl, int NB, double *nuc) {
+  for (long x = (long)blockIdx.x * blockDim.x + threadIdx.x; x < (long)nl * NB; x += (long)gridDim.x * blockDim.x)
+    nuc[x] = nu[(x / NB) * ld + x % NB];
 }
 
 // ---------------------------------------------------------------------------
@@ -514,15 +560,7 @@ struct FinArgs {
 __device__ __forceinline__ bool valid_bound(double g) { return isfinite(g) && fabs(g) <= 1e15; }
 
 template <bool EVAL>
-__global__ void k_finish(const FinArgs f) {
-  const long n = f.n0 + (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= f.n1) return;
-  double so = 0.0, sp = 0.0, sl = 0.0;
-  for (int t = 0; t < f.nMt1; ++t) {
-    so += f.part_obj[(size_t)t * f.ld + n];
-    sp += f.part_p[(size_t)t * f.ld + n];
-  }
-  for (int t = 0; t < f.nMt2; ++t) sl += f.part_line[(size_t)t * f.ld + n];
+__device__ __forceinline__ void finish_one(const FinArgs &f, long n, double so, double sp, double sl) {
   const double lam = f.lam[n], D = f.D[n];
   const double g = (so - lam * D) + sl;
   const double gl = sp - D;  // dg/dlambda = 1^T p* - 1^T d
@@ -563,6 +601,44 @@ __global__ void k_finish(const FinArgs f) {
     if (f.sl1) f.sl1[n] = s1;
     if (f.sl2) f.sl2[n] = s2;
   }
+}
+
+// GEMM mode: one thread per instance sums its tiles' partials in tile order
+template <bool EVAL>
+__global__ void k_finish(const FinArgs f) {
+  const long n = f.n0 + (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= f.n1) return;
+  double so = 0.0, sp = 0.0, sl = 0.0;
+  for (int t = 0; t < f.nMt1; ++t) {
+    so += f.part_obj[(size_t)t * f.ld + n];
+    sp += f.part_p[(size_t)t * f.ld + n];
+  }
+  for (int t = 0; t < f.nMt2; ++t) sl += f.part_line[(size_t)t * f.ld + n];
+  finish_one<EVAL>(f, n, so, sp, sl);
+}
+
+// skinny mode: one block per instance, its (many) block partials summed by a
+// fixed strided split + tree (deterministic)
+template <bool EVAL>
+__global__ void __launch_bounds__(256) k_finish_blk(const FinArgs f) {
+  __shared__ double red[3][256];
+  const long n = f.n0 + blockIdx.x;
+  double so = 0.0, sp = 0.0, sl = 0.0;
+  for (int t = threadIdx.x; t < f.nMt1; t += 256) {
+    so += f.part_obj[(size_t)t * f.ld + n];
+    sp += f.part_p[(size_t)t * f.ld + n];
+  }
+  for (int t = threadIdx.x; t < f.nMt2; t += 256) sl += f.part_line[(size_t)t * f.ld + n];
+  red[0][threadIdx.x] = so;
+  red[1][threadIdx.x] = sp;
+  red[2][threadIdx.x] = sl;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int c = 0; c < 3; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) finish_one<EVAL>(f, n, red[0][0], red[1][0], red[2][0]);
 }
 
 // ---------------------------------------------------------------------------
@@ -678,8 +754,8 @@ struct PtdfState {
   // so one group's GEMM tail overlaps the other's (instances are independent)
   int nsplit = 2;
   // skinny batches (B <= 16): matrix-vector kernels; nbv = instance columns computed (0: GEMM mode)
-  int nbv = 0, S1 = 1, S2 = 1;
-  double *qpart = nullptr, *ypart = nullptr;
+  int nbv = 0;
+  double *nuc = nullptr, *pcv = nullptr, *sp_obj = nullptr, *sp_p = nullptr, *sp_line = nullptr;
   cudaStream_t sub[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
 };
@@ -916,27 +992,28 @@ int copy_rows_out(PtdfState *st, double *dst, const double *src, long rows, cuda
   return DCOPF_OK;
 }
 
+int skinny_blocks_g(int rows) { return std::max(1, (rows + VW / WPR_G - 1) / (VW / WPR_G)); }
+int skinny_blocks_l(int rows) { return std::max(1, (rows + VW / WPR_L - 1) / (VW / WPR_L)); }
+
 template <int NB>
 int skinny_pass_t(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, cudaStream_t s,
                   std::string *err) {
-  const int ng = st->ng, nl = st->nl;
-  if (ng > 0) {
-    const int nMb = (ng + 2 * VT - 1) / (2 * VT);
-    if (nl > 0)
-      k_gemv_part<NB><<<nMb * st->S1, VT, 0, s>>>(st->Hg, st->ngk, ng, nl, st->nu, st->Bp, st->S1, st->qpart,
-                                                  st->ngk);
-    k_gen_epi<NB><<<(int)((st->ngk + VT - 1) / VT), VT, 0, s>>>(g1, st->qpart, nl > 0 ? st->S1 : 0, st->ngk);
-  }
-  if (nl > 0) {
-    const int nMb = (nl + 2 * VT - 1) / (2 * VT);
-    if (ng > 0)
-      k_gemv_part<NB><<<nMb * st->S2, VT, 0, s>>>(st->HgT, st->nlk, nl, ng, st->P, st->Bp, st->S2, st->ypart,
-                                                  st->nlk);
-    const int eb = (nl + VT - 1) / VT, S = ng > 0 ? st->S2 : 0;
+  GemmArgs a = g1, b = g2;
+  a.A = st->HgT;  // row g of H_g^T, K = n_l
+  a.lda = st->nlk;
+  a.K = st->nl;
+  a.part_obj = st->sp_obj;
+  a.part_p = st->sp_p;
+  b.A = st->Hg;   // row l of H_g, K = n_g
+  b.lda = st->ngk;
+  b.K = st->ng;
+  b.part_line = st->sp_line;
+  if (st->ng > 0) k_gen_row<NB><<<skinny_blocks_g(st->ng), VT, 0, s>>>(a, st->nuc, st->pcv);
+  if (st->nl > 0) {
     if (step)
-      k_line_epi<NB, true><<<eb, VT, 0, s>>>(g2, st->ypart, S, st->nlk);
+      k_line_row<NB, true><<<skinny_blocks_l(st->nl), VT, 0, s>>>(b, st->pcv, st->nuc);
     else
-      k_line_epi<NB, false><<<eb, VT, 0, s>>>(g2, st->ypart, S, st->nlk);
+      k_line_row<NB, false><<<skinny_blocks_l(st->nl), VT, 0, s>>>(b, st->pcv, st->nuc);
   }
   PCK(cudaGetLastError());
   return DCOPF_OK;
@@ -952,13 +1029,25 @@ int skinny_pass(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step
   }
 }
 
-// partial-sum tiles the finisher reads: GEMM tiles, or the skinny epilogue blocks
+// skinny mode: the finisher reads the per-block partials [block][NB]
 void fin_tiles(const PtdfState *st, FinArgs *f) {
   if (st->nbv) {
-    f->nMt1 = st->ng > 0 ? (int)((st->ngk + VT - 1) / VT) : 0;
-    f->nMt2 = (st->nl + VT - 1) / VT;
+    f->part_obj = st->sp_obj;
+    f->part_p = st->sp_p;
+    f->part_line = st->sp_line;
+    f->nMt1 = st->ng > 0 ? skinny_blocks_g(st->ng) : 0;
+    f->nMt2 = st->nl > 0 ? skinny_blocks_l(st->nl) : 0;
+    f->ld = st->nbv;
+    f->n0 = 0;
     f->n1 = st->B;
   }
+}
+
+int skinny_sync_nu(PtdfState *st, cudaStream_t s, std::string *err) {
+  if (!st->nbv || st->nl == 0) return DCOPF_OK;
+  k_compact_nu<<<blocks_for((size_t)st->nl * st->nbv), 256, 0, s>>>(st->nu, st->Bp, st->nl, st->nbv, st->nuc);
+  PCK(cudaGetLastError());
+  return DCOPF_OK;
 }
 
 }  // namespace
@@ -1176,7 +1265,8 @@ void ptdf_destroy(PtdfState *st) {
   if (!st) return;
   cudaSetDevice(st->device);
   free_batch(st);
-  double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch, st->qpart, st->ypart};
+  double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch, st->nuc, st->pcv,
+                  st->sp_obj, st->sp_p, st->sp_line};
   for (double *p : dp) cudaFree(p);
   for (int c = 0; c < 2; ++c) {
     if (st->sub[c]) cudaStreamDestroy(st->sub[c]);
@@ -1217,12 +1307,12 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
   const char *sk = getenv("DCOPF_PTDF_SKINNY");
   if (B <= 16 && !(sk && atoi(sk) == 0)) {
     st->nbv = B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : (B <= 8 ? 8 : 16)));
-    const int target = 4 * 148;
-    const int nMb1 = std::max(1, (st->ng + 2 * VT - 1) / (2 * VT)), nMb2 = std::max(1, (st->nl + 2 * VT - 1) / (2 * VT));
-    st->S1 = std::max(1, std::min(std::max(st->nl, 1), target / nMb1));
-    st->S2 = std::max(1, std::min(std::max(st->ng, 1), target / nMb2));
-    int rc0 = dalloc(&st->qpart, (size_t)st->S1 * st->ngk * 16, err);
-    if (!rc0) rc0 = dalloc(&st->ypart, (size_t)st->S2 * st->nlk * 16, err);
+    // compact vectors padded to the row padding (the double2 loads read one past an odd K)
+    int rc0 = dalloc(&st->nuc, (size_t)st->nlk * 16 + 16, err);
+    if (!rc0) rc0 = dalloc(&st->pcv, (size_t)st->ngk * 16 + 16, err);
+    if (!rc0) rc0 = dalloc(&st->sp_obj, (size_t)skinny_blocks_g(st->ng) * 16, err);
+    if (!rc0) rc0 = dalloc(&st->sp_p, (size_t)skinny_blocks_g(st->ng) * 16, err);
+    if (!rc0) rc0 = dalloc(&st->sp_line, (size_t)skinny_blocks_l(st->nl) * 16, err);
     if (rc0) return rc0;
   }
   // loads: [n_bus][B] -> Dm [nbk][Bp] (zero padded), r = H_a Dm, D = 1^T d
@@ -1276,7 +1366,7 @@ int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist
       if (rc) return rc;
       f.k = (int)k;
       f.first = k == 0;
-      k_finish<false><<<1, 256, 0, s>>>(f);
+      k_finish_blk<false><<<(int)st->B, 256, 0, s>>>(f);
       PCK(cudaGetLastError());
     }
     st->k_base += K;
@@ -1389,6 +1479,7 @@ int ptdf_set_multipliers(PtdfState *st, const double *lambda, const double *bran
     PCK(cudaMemcpyAsync(st->mup, tp, nm * 8, cudaMemcpyDeviceToDevice, s));
     PCK(cudaMemcpyAsync(st->mum, tm, nm * 8, cudaMemcpyDeviceToDevice, s));
     k_sub<<<blocks_for(nm), 256, 0, s>>>(st->mup, st->mum, st->nu, nm);
+    if (int rc2 = skinny_sync_nu(st, s, err)) return rc2;
   }
   PCK(cudaStreamSynchronize(s));
   return DCOPF_OK;
@@ -1413,7 +1504,10 @@ int ptdf_evaluate(PtdfState *st, double *value, double *grad_lambda, double *gra
   FinArgs f = fin_args(st);
   fin_tiles(st, &f);
   f.glam_out = st->glam;
-  k_finish<true><<<blocks_for(st->Bp), 256, 0, s>>>(f);
+  if (st->nbv)
+    k_finish_blk<true><<<(int)st->B, 256, 0, s>>>(f);
+  else
+    k_finish<true><<<blocks_for(st->Bp), 256, 0, s>>>(f);
   PCK(cudaGetLastError());
   if (value) PCK(cudaMemcpyAsync(value, st->value, st->B * 8, cudaMemcpyDefault, s));
   rc = copy_rows_out(st, grad_lambda, st->glam, 1, s, err);
