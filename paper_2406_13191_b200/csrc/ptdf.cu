@@ -356,188 +356,6 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
 }
 
 // ---------------------------------------------------------------------------
-// Skinny batches (B <= 16, e.g. one large instance): the two products are
-// matrix-vector shaped, i.e. HBM-bound reads of H_g (254 MB at config 3), not
-// tensor work.  One warp per row, coalesced double2 loads along the row, the
-// vector in a compact [K][NB] copy (nu_c, p_c: L1/L2 resident), a fixed xor
-// tree for the dot product, and the epilogue fused: GEMM1 rows are generators
-// (A = H_g^T, row g, K = n_l), GEMM2 rows are lines (A = H_g, row l, K = n_g).
-// Each block writes its partial sums per instance to part[block][b] (ld NB).
-constexpr int VT = 512, VW = VT / 32;   // threads and warps per block
-constexpr int WPR_G = 4, WPR_L = 1;      // warps per row: GEMM1 rows are 100 KB (config 3), GEMM2 rows 20 KB
-
-template <int NB>
-__device__ __forceinline__ void warp_dot(const double *__restrict__ row, const double *__restrict__ xc, int k0,
-                                         int K, double (&acc)[NB]) {
-  const int lane = threadIdx.x & 31;
-  // four independent accumulator sets (k strides of 64, 4 deep) keep four
-  // row loads in flight per lane; combined in a fixed order
-  double part[4][NB];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) part[u][b] = 0.0;
-  int k = k0 + 2 * lane;
-  for (; k + 192 < K; k += 256) {
-    double2 a[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = *reinterpret_cast<const double2 *>(row + k + 64 * u);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int kk = k + 64 * u;
-#pragma unroll
-      for (int b = 0; b < NB; ++b) part[u][b] += a[u].x * xc[kk * NB + b] + a[u].y * xc[(kk + 1) * NB + b];
-    }
-  }
-  for (int u = 0; k < K; k += 64, ++u) {
-    const double2 a = *reinterpret_cast<const double2 *>(row + k);
-#pragma unroll
-    for (int b = 0; b < NB; ++b) part[u & 3][b] += a.x * xc[k * NB + b] + a.y * xc[(k + 1) * NB + b];
-  }
-#pragma unroll
-  for (int b = 0; b < NB; ++b) acc[b] = (part[0][b] + part[1][b]) + (part[2][b] + part[3][b]);
-#pragma unroll
-  for (int b = 0; b < NB; ++b)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
-}
-
-// block partial sums: per-warp values red[warp][b] summed in warp order
-template <int NB>
-__device__ __forceinline__ void block_part(double *red, const double (&v)[NB], double *part) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane < NB) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-      if (b == lane) red[warp * NB + b] = v[b];
-  }
-  __syncthreads();
-  if (threadIdx.x < NB) {
-    double t = 0.0;
-    for (int w = 0; w < VW; ++w) t += red[w * NB + threadIdx.x];
-    part[(size_t)blockIdx.x * NB + threadIdx.x] = t;
-  }
-}
-
-// the row's K range split over WPR warps (64-aligned); their dot products are
-// combined in warp order through shared memory (deterministic)
-template <int NB, int WPR>
-__device__ __forceinline__ void row_dot(const GemmArgs &g, int row, bool live, const double *__restrict__ xc,
-                                        double (*rp)[NB], double (&acc)[NB]) {
-  const int warp = threadIdx.x >> 5, q = warp % WPR;
-  const int Kq = ((g.K + WPR * 64 - 1) / (WPR * 64)) * 64;
-  const int k0 = q * Kq, k1 = min(g.K, k0 + Kq);
-  double a[NB];
-  if (live) warp_dot<NB>(g.A + (size_t)row * g.lda, xc, k0, k1, a);
-  else
-#pragma unroll
-    for (int b = 0; b < NB; ++b) a[b] = 0.0;
-  if (WPR > 1) {
-    if ((threadIdx.x & 31) == 0)
-#pragma unroll
-      for (int b = 0; b < NB; ++b) rp[warp][b] = a[b];
-    __syncthreads();
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      double t = rp[warp - q][b];
-      for (int j = 1; j < WPR; ++j) t += rp[warp - q + j][b];
-      acc[b] = t;
-    }
-  } else {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) acc[b] = a[b];
-  }
-}
-
-template <int NB>
-__global__ void __launch_bounds__(VT) k_gen_row(const GemmArgs g, const double *__restrict__ nuc,
-                                                double *__restrict__ pc) {
-  __shared__ double red[2][VW * NB];
-  __shared__ double rp[VW][NB];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int row = blockIdx.x * (VW / WPR_G) + warp / WPR_G;
-  const bool live = row < g.ng;
-  double so[NB], sp[NB], acc[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b) so[b] = sp[b] = 0.0;
-  row_dot<NB, WPR_G>(g, row, live, nuc, rp, acc);  // (H_g^T nu)_g
-  if (live && warp % WPR_G == 0) {
-    const double c = g.gc[row], lo = g.glo[row], hi = g.ghi[row], a = g.ga ? g.ga[row] : 0.0;
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const double q = (c + g.lam[b]) + acc[b];
-      const double p = minimiser(q, lo, hi, a);
-      if (lane == b) pc[(size_t)row * NB + b] = p;
-      so[b] += a * p * p + q * p;
-      sp[b] += p;
-    }
-  }
-  block_part<NB>(red[0], so, g.part_obj);
-  block_part<NB>(red[1], sp, g.part_p);
-}
-
-template <int NB, bool STEP>
-__global__ void __launch_bounds__(VT) k_line_row(const GemmArgs g, const double *__restrict__ pcv,
-                                                 double *__restrict__ nuc) {
-  __shared__ double red[VW * NB];
-  __shared__ double rp[VW][NB];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int row = blockIdx.x * (VW / WPR_L) + warp / WPR_L;
-  const bool live = row < g.nl;
-  double sv[NB], acc[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b) sv[b] = 0.0;
-  row_dot<NB, WPR_L>(g, row, live, pcv, rp, acc);  // (H_g p*)_l
-  if (live && warp % WPR_L == 0) {
-    const double al = STEP ? g.alpha[g.k] : 0.0;
-    const double F = g.F[row];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const size_t o = (size_t)row * g.ld + b;
-      const double y = acc[b];
-      const double r = g.r[o], mp = g.mup[o], mm = g.mum[o];
-      sv[b] += mm * (r - F) - mp * (r + F);
-      if (lane != b) continue;  // lane b owns instance b of this row
-      const double gp = (y - r) - F, gm = (r - y) - F;
-      if (!STEP) {
-        if (g.gp_out) {
-          g.gp_out[o] = gp;
-          g.gm_out[o] = gm;
-        }
-      } else if (g.status[b] == 0) {
-        double vp, vm;
-        if (g.opt == 0) {
-          vp = mp + al * gp;
-          vm = mm + al * gm;
-        } else {
-          double a1 = g.s1p[o], a2 = g.s2p ? g.s2p[o] : 0.0, b1 = g.s1m[o], b2 = g.s2m ? g.s2m[o] : 0.0;
-          vp = opt_step(g, mp, gp, al, a1, a2);
-          vm = opt_step(g, mm, gm, al, b1, b2);
-          g.s1p[o] = a1;
-          g.s1m[o] = b1;
-          if (g.s2p) {
-            g.s2p[o] = a2;
-            g.s2m[o] = b2;
-          }
-        }
-        const double np = vp > 0.0 ? vp : 0.0, nm = vm > 0.0 ? vm : 0.0;  // mu <- max(mu, 0)
-        g.mup[o] = np;
-        g.mum[o] = nm;
-        g.nu[o] = np - nm;
-        nuc[(size_t)row * NB + b] = np - nm;
-      }
-    }
-  }
-  block_part<NB>(red, sv, g.part_line);
-}
-
-// compact copy nu_c[l][b] = nu[l][b] (after set_batch / set_multipliers)
-__global__ void k_compact_nu(const double *nu, long ld, int nl, int NB, double *nuc) {
-  for (long x = (long)blockIdx.x * blockDim.x + threadIdx.x; x < (long)nl * NB; x += (long)gridDim.x * blockDim.x)
-    nuc[x] = nu[(x / NB) * ld + x % NB];
-}
-
-// ---------------------------------------------------------------------------
 // per instance: the dual value, grad lambda, bookkeeping and the lambda step
 struct FinArgs {
   const double *part_obj, *part_p, *part_line;
@@ -639,6 +457,232 @@ __global__ void __launch_bounds__(256) k_finish_blk(const FinArgs f) {
     __syncthreads();
   }
   if (threadIdx.x == 0) finish_one<EVAL>(f, n, red[0][0], red[1][0], red[2][0]);
+}
+
+// ---------------------------------------------------------------------------
+// Skinny batches (B <= 16, e.g. one large instance): the two products are
+// matrix-vector shaped, i.e. HBM-bound reads of H_g (254 MB at config 3), not
+// tensor work.  One warp per row, coalesced double2 loads along the row, the
+// vector in a compact [K][NB] copy (nu_c, p_c: L1/L2 resident), a fixed xor
+// tree for the dot product, and the epilogue fused: GEMM1 rows are generators
+// (A = H_g^T, row g, K = n_l), GEMM2 rows are lines (A = H_g, row l, K = n_g).
+// Each block writes its partial sums per instance to part[block][b] (ld NB).
+constexpr int VT = 512, VW = VT / 32;   // threads and warps per block
+#ifndef PTDF_DU
+#define PTDF_DU 1
+#endif
+#ifndef PTDF_WPR_G
+#define PTDF_WPR_G 4
+#endif
+#ifndef PTDF_WPR_L
+#define PTDF_WPR_L 1
+#endif
+constexpr int WPR_G = PTDF_WPR_G, WPR_L = PTDF_WPR_L;  // warps per row: GEMM1 rows are 100 KB (config 3), GEMM2 rows 20 KB
+
+template <int NB>
+__device__ __forceinline__ void warp_dot(const double *__restrict__ row, const double *__restrict__ xc, int k0,
+                                         int K, double (&acc)[NB]) {
+  const int lane = threadIdx.x & 31;
+  // DU independent accumulator sets (k strides of 64, DU deep) keep DU row
+  // loads in flight per lane; combined in a fixed order
+  constexpr int DU = PTDF_DU;
+  double part[DU][NB];
+#pragma unroll
+  for (int u = 0; u < DU; ++u)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) part[u][b] = 0.0;
+  int k = k0 + 2 * lane;
+  for (; k + 64 * (DU - 1) < K; k += 64 * DU) {
+    double2 a[DU];
+#pragma unroll
+    for (int u = 0; u < DU; ++u) a[u] = *reinterpret_cast<const double2 *>(row + k + 64 * u);
+#pragma unroll
+    for (int u = 0; u < DU; ++u) {
+      const int kk = k + 64 * u;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) part[u][b] += a[u].x * xc[kk * NB + b] + a[u].y * xc[(kk + 1) * NB + b];
+    }
+  }
+  for (int u = 0; k < K; k += 64, ++u) {
+    const double2 a = *reinterpret_cast<const double2 *>(row + k);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) part[u % DU][b] += a.x * xc[k * NB + b] + a.y * xc[(k + 1) * NB + b];
+  }
+#pragma unroll
+  for (int u = 1; u < DU; ++u)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) part[0][b] += part[u][b];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = part[0][b];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
+}
+
+// block partial sums: per-warp values red[warp][b] summed in warp order
+template <int NB>
+__device__ __forceinline__ void block_part(double *red, const double (&v)[NB], double *part) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane < NB) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (b == lane) red[warp * NB + b] = v[b];
+  }
+  __syncthreads();
+  if (threadIdx.x < NB) {
+    double t = 0.0;
+    for (int w = 0; w < VW; ++w) t += red[w * NB + threadIdx.x];
+    part[(size_t)blockIdx.x * NB + threadIdx.x] = t;
+  }
+}
+
+// the row's K range split over WPR warps (64-aligned); their dot products are
+// combined in warp order through shared memory (deterministic)
+template <int NB, int WPR>
+__device__ __forceinline__ void row_dot(const GemmArgs &g, int row, bool live, const double *__restrict__ xc,
+                                        double (*rp)[NB], double (&acc)[NB]) {
+  const int warp = threadIdx.x >> 5, q = warp % WPR;
+  const int Kq = ((g.K + WPR * 64 - 1) / (WPR * 64)) * 64;
+  const int k0 = q * Kq, k1 = min(g.K, k0 + Kq);
+  double a[NB];
+  if (live) warp_dot<NB>(g.A + (size_t)row * g.lda, xc, k0, k1, a);
+  else
+#pragma unroll
+    for (int b = 0; b < NB; ++b) a[b] = 0.0;
+  if (WPR > 1) {
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) rp[warp][b] = a[b];
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double t = rp[warp - q][b];
+      for (int j = 1; j < WPR; ++j) t += rp[warp - q + j][b];
+      acc[b] = t;
+    }
+  } else {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = a[b];
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(VT) k_gen_row(const GemmArgs g, const double *__restrict__ nuc,
+                                                double *__restrict__ pc) {
+  __shared__ double red[2][VW * NB];
+  __shared__ double rp[VW][NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * (VW / WPR_G) + warp / WPR_G;
+  const bool live = row < g.ng;
+  double so[NB], sp[NB], acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) so[b] = sp[b] = 0.0;
+  row_dot<NB, WPR_G>(g, row, live, nuc, rp, acc);  // (H_g^T nu)_g
+  if (live && warp % WPR_G == 0) {
+    const double c = g.gc[row], lo = g.glo[row], hi = g.ghi[row], a = g.ga ? g.ga[row] : 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double q = (c + g.lam[b]) + acc[b];
+      const double p = minimiser(q, lo, hi, a);
+      if (lane == b) pc[(size_t)row * NB + b] = p;
+      so[b] += a * p * p + q * p;
+      sp[b] += p;
+    }
+  }
+  block_part<NB>(red[0], so, g.part_obj);
+  block_part<NB>(red[1], sp, g.part_p);
+}
+
+// the last block to finish (atomic ticket) sums every block's partials per
+// instance in a fixed order and runs the per-instance finisher: no extra launch
+template <int NB, bool STEP, bool FEVAL>
+__global__ void __launch_bounds__(VT) k_line_row(const GemmArgs g, const double *__restrict__ pcv,
+                                                 double *__restrict__ nuc, const FinArgs f, unsigned *ticket) {
+  __shared__ double red[VW * NB];
+  __shared__ double fred[3][VT];
+  __shared__ bool last;
+  __shared__ double rp[VW][NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * (VW / WPR_L) + warp / WPR_L;
+  const bool live = row < g.nl;
+  double sv[NB], acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) sv[b] = 0.0;
+  row_dot<NB, WPR_L>(g, row, live, pcv, rp, acc);  // (H_g p*)_l
+  if (live && warp % WPR_L == 0) {
+    const double al = STEP ? g.alpha[g.k] : 0.0;
+    const double F = g.F[row];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const size_t o = (size_t)row * g.ld + b;
+      const double y = acc[b];
+      const double r = g.r[o], mp = g.mup[o], mm = g.mum[o];
+      sv[b] += mm * (r - F) - mp * (r + F);
+      if (lane != b) continue;  // lane b owns instance b of this row
+      const double gp = (y - r) - F, gm = (r - y) - F;
+      if (!STEP) {
+        if (g.gp_out) {
+          g.gp_out[o] = gp;
+          g.gm_out[o] = gm;
+        }
+      } else if (g.status[b] == 0) {
+        double vp, vm;
+        if (g.opt == 0) {
+          vp = mp + al * gp;
+          vm = mm + al * gm;
+        } else {
+          double a1 = g.s1p[o], a2 = g.s2p ? g.s2p[o] : 0.0, b1 = g.s1m[o], b2 = g.s2m ? g.s2m[o] : 0.0;
+          vp = opt_step(g, mp, gp, al, a1, a2);
+          vm = opt_step(g, mm, gm, al, b1, b2);
+          g.s1p[o] = a1;
+          g.s1m[o] = b1;
+          if (g.s2p) {
+            g.s2p[o] = a2;
+            g.s2m[o] = b2;
+          }
+        }
+        const double np = vp > 0.0 ? vp : 0.0, nm = vm > 0.0 ? vm : 0.0;  // mu <- max(mu, 0)
+        g.mup[o] = np;
+        g.mum[o] = nm;
+        g.nu[o] = np - nm;
+        nuc[(size_t)row * NB + b] = np - nm;
+      }
+    }
+  }
+  block_part<NB>(red, sv, g.part_line);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (long n = f.n0; n < f.n1; ++n) {
+    double so = 0.0, sp = 0.0, sl = 0.0;
+    for (int t = threadIdx.x; t < f.nMt1; t += VT) {
+      so += __ldcg(f.part_obj + (size_t)t * f.ld + n);
+      sp += __ldcg(f.part_p + (size_t)t * f.ld + n);
+    }
+    for (int t = threadIdx.x; t < f.nMt2; t += VT) sl += __ldcg(f.part_line + (size_t)t * f.ld + n);
+    fred[0][threadIdx.x] = so;
+    fred[1][threadIdx.x] = sp;
+    fred[2][threadIdx.x] = sl;
+    __syncthreads();
+    for (int w = VT / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w)
+        for (int c = 0; c < 3; ++c) fred[c][threadIdx.x] += fred[c][threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) finish_one<FEVAL>(f, n, fred[0][0], fred[1][0], fred[2][0]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *ticket = 0u;  // ready for the next launch
+}
+
+// compact copy nu_c[l][b] = nu[l][b] (after set_batch / set_multipliers)
+__global__ void k_compact_nu(const double *nu, long ld, int nl, int NB, double *nuc) {
+  for (long x = (long)blockIdx.x * blockDim.x + threadIdx.x; x < (long)nl * NB; x += (long)gridDim.x * blockDim.x)
+    nuc[x] = nu[(x / NB) * ld + x % NB];
 }
 
 // ---------------------------------------------------------------------------
@@ -756,6 +800,7 @@ struct PtdfState {
   // skinny batches (B <= 16): matrix-vector kernels; nbv = instance columns computed (0: GEMM mode)
   int nbv = 0;
   double *nuc = nullptr, *pcv = nullptr, *sp_obj = nullptr, *sp_p = nullptr, *sp_line = nullptr;
+  unsigned *ticket = nullptr;  // last-block ticket of the skinny line kernel (zero between launches)
   cudaStream_t sub[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
 };
@@ -996,8 +1041,8 @@ int skinny_blocks_g(int rows) { return std::max(1, (rows + VW / WPR_G - 1) / (VW
 int skinny_blocks_l(int rows) { return std::max(1, (rows + VW / WPR_L - 1) / (VW / WPR_L)); }
 
 template <int NB>
-int skinny_pass_t(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, cudaStream_t s,
-                  std::string *err) {
+int skinny_pass_t(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, const FinArgs &f, bool feval,
+                  cudaStream_t s, std::string *err) {
   GemmArgs a = g1, b = g2;
   a.A = st->HgT;  // row g of H_g^T, K = n_l
   a.lda = st->nlk;
@@ -1009,23 +1054,31 @@ int skinny_pass_t(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool st
   b.K = st->ng;
   b.part_line = st->sp_line;
   if (st->ng > 0) k_gen_row<NB><<<skinny_blocks_g(st->ng), VT, 0, s>>>(a, st->nuc, st->pcv);
-  if (st->nl > 0) {
+  const int lb = skinny_blocks_l(st->nl);
+  if (st->nl > 0) {  // the line kernel's last block runs the finisher
     if (step)
-      k_line_row<NB, true><<<skinny_blocks_l(st->nl), VT, 0, s>>>(b, st->pcv, st->nuc);
+      k_line_row<NB, true, false><<<lb, VT, 0, s>>>(b, st->pcv, st->nuc, f, st->ticket);
+    else if (!feval)
+      k_line_row<NB, false, false><<<lb, VT, 0, s>>>(b, st->pcv, st->nuc, f, st->ticket);
     else
-      k_line_row<NB, false><<<skinny_blocks_l(st->nl), VT, 0, s>>>(b, st->pcv, st->nuc);
+      k_line_row<NB, false, true><<<lb, VT, 0, s>>>(b, st->pcv, st->nuc, f, st->ticket);
+  } else if (feval) {
+    k_finish_blk<true><<<(int)st->B, 256, 0, s>>>(f);
+  } else {
+    k_finish_blk<false><<<(int)st->B, 256, 0, s>>>(f);
   }
   PCK(cudaGetLastError());
   return DCOPF_OK;
 }
 
-int skinny_pass(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, cudaStream_t s, std::string *err) {
+int skinny_pass(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, const FinArgs &f, bool feval,
+                cudaStream_t s, std::string *err) {
   switch (st->nbv) {
-    case 1: return skinny_pass_t<1>(st, g1, g2, step, s, err);
-    case 2: return skinny_pass_t<2>(st, g1, g2, step, s, err);
-    case 4: return skinny_pass_t<4>(st, g1, g2, step, s, err);
-    case 8: return skinny_pass_t<8>(st, g1, g2, step, s, err);
-    default: return skinny_pass_t<16>(st, g1, g2, step, s, err);
+    case 1: return skinny_pass_t<1>(st, g1, g2, step, f, feval, s, err);
+    case 2: return skinny_pass_t<2>(st, g1, g2, step, f, feval, s, err);
+    case 4: return skinny_pass_t<4>(st, g1, g2, step, f, feval, s, err);
+    case 8: return skinny_pass_t<8>(st, g1, g2, step, f, feval, s, err);
+    default: return skinny_pass_t<16>(st, g1, g2, step, f, feval, s, err);
   }
 }
 
@@ -1274,6 +1327,7 @@ void ptdf_destroy(PtdfState *st) {
   }
   if (st->ev_fork) cudaEventDestroy(st->ev_fork);
   cudaFree(st->flag);
+  cudaFree(st->ticket);
   delete st;
 }
 
@@ -1313,6 +1367,10 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
     if (!rc0) rc0 = dalloc(&st->sp_obj, (size_t)skinny_blocks_g(st->ng) * 16, err);
     if (!rc0) rc0 = dalloc(&st->sp_p, (size_t)skinny_blocks_g(st->ng) * 16, err);
     if (!rc0) rc0 = dalloc(&st->sp_line, (size_t)skinny_blocks_l(st->nl) * 16, err);
+    if (!rc0 && !st->ticket) {
+      PCK(cudaMalloc(&st->ticket, sizeof(unsigned)));
+      PCK(cudaMemset(st->ticket, 0, sizeof(unsigned)));
+    }
     if (rc0) return rc0;
   }
   // loads: [n_bus][B] -> Dm [nbk][Bp] (zero padded), r = H_a Dm, D = 1^T d
@@ -1362,12 +1420,10 @@ int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist
       g2.k = (int)k;
       g2.b1t = f.b1t = st->b1t;
       g2.b2t = f.b2t = st->b2t;
-      int rc = skinny_pass(st, g1, g2, step, s, err);
-      if (rc) return rc;
       f.k = (int)k;
       f.first = k == 0;
-      k_finish_blk<false><<<(int)st->B, 256, 0, s>>>(f);
-      PCK(cudaGetLastError());
+      int rc = skinny_pass(st, g1, g2, step, f, false, s, err);
+      if (rc) return rc;
     }
     st->k_base += K;
     return DCOPF_OK;
@@ -1494,20 +1550,17 @@ int ptdf_evaluate(PtdfState *st, double *value, double *grad_lambda, double *gra
   GemmArgs g2 = line_args(st);
   g2.gp_out = st->gp;
   g2.gm_out = st->gm;
-  if (st->nbv) {
-    rc = skinny_pass(st, gen_args(st), g2, false, s, err);
-  } else {
-    rc = launch_gemm<EPI_GEN>(gen_args(st), s, err);
-    if (!rc) rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
-  }
-  if (rc) return rc;
   FinArgs f = fin_args(st);
   fin_tiles(st, &f);
   f.glam_out = st->glam;
-  if (st->nbv)
-    k_finish_blk<true><<<(int)st->B, 256, 0, s>>>(f);
-  else
-    k_finish<true><<<blocks_for(st->Bp), 256, 0, s>>>(f);
+  if (st->nbv) {
+    rc = skinny_pass(st, gen_args(st), g2, false, f, true, s, err);
+  } else {
+    rc = launch_gemm<EPI_GEN>(gen_args(st), s, err);
+    if (!rc) rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
+    if (!rc) k_finish<true><<<blocks_for(st->Bp), 256, 0, s>>>(f);
+  }
+  if (rc) return rc;
   PCK(cudaGetLastError());
   if (value) PCK(cudaMemcpyAsync(value, st->value, st->B * 8, cudaMemcpyDefault, s));
   rc = copy_rows_out(st, grad_lambda, st->glam, 1, s, err);

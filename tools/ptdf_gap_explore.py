@@ -22,8 +22,8 @@ if quad:
 else:
     opt = inst.primal_lp(dataclasses.replace(net, theta_max=th), net.base_load)[1]
 print("opt", opt, "(%.1fs)" % (time.time() - t0), flush=True)
-K = 5000
-marks = [50, 100, 200, 500, 1000, 2000, 5000]
+K = int(__import__("os").environ.get("PTDF_K", "5000"))
+marks = [m for m in [50, 100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000] if m <= K]
 h = dual.DcopfDual(net, form=dual.FORM_PTDF)
 ld = np.ascontiguousarray(net.base_load[:, None])
 for name, var, kw, alphas in [("adam", dual.OPT_ADAM, dict(beta1=0.9, beta2=0.999, epsilon=1e-8), [0.01, 0.1, 1.0, 10.0]),
