@@ -106,16 +106,18 @@ class PtdfEval:
     p: np.ndarray         # [B][n_g]
 
 
-def evaluate(net, Ha, load, lam, mup, mum) -> PtdfEval:
-    """Dual value and gradient at (lambda[B], mu+[B][n_l], mu-[B][n_l])."""
+def evaluate(net, Ha, load, lam, mup, mum, _pre=None) -> PtdfEval:
+    """Dual value and gradient at (lambda[B], mu+[B][n_l], mu-[B][n_l]).
+    _pre: (H_g, 1^T d, H_a d) already formed for this net and load (solve()
+    forms them once; the same expressions, so the same values)."""
     load = np.atleast_2d(np.asarray(load, dtype=np.float64))
     lam = np.asarray(lam, dtype=np.float64).reshape(-1)
     mup = np.atleast_2d(np.asarray(mup, dtype=np.float64))
     mum = np.atleast_2d(np.asarray(mum, dtype=np.float64))
-    Hg = Ha[:, net.gen_bus]                     # H_a G  [n_l][n_g]
+    if _pre is None:
+        _pre = _constants(net, Ha, load)
+    Hg, D, r = _pre                             # H_a G [n_l][n_g], 1^T d [B], H_a d [B][n_l]
     F = np.asarray(net.br_fmax, dtype=np.float64)
-    D = load.sum(axis=1)                        # 1^T d
-    r = load @ Ha.T                             # H_a d  [B][n_l]
     q = net.gen_c[None, :] + lam[:, None] + (mup - mum) @ Hg
     p = minimiser(net, q)
     a = _gen_a(net)
@@ -123,6 +125,11 @@ def evaluate(net, Ha, load, lam, mup, mum) -> PtdfEval:
     value = obj.sum(axis=1) - lam * D - (mup * (r + F)).sum(axis=1) + (mum * (r - F)).sum(axis=1)
     y = p @ Hg.T                                # H_g p*  [B][n_l]
     return PtdfEval(value, p.sum(axis=1) - D, y - r - F, r - y - F, p)
+
+
+def _constants(net, Ha, load):
+    """The parts of the dual function that do not depend on the multipliers."""
+    return Ha[:, net.gen_bus], load.sum(axis=1), load @ Ha.T
 
 
 def _valid(g):
@@ -190,8 +197,9 @@ def solve(net, load, K, alpha, Ha=None, lam0=None, mu0=None, opt=None, tol=0.0,
     gprev = np.zeros(B)
     hist = np.zeros((B, K + 1)) if history else None
     bound = np.zeros(B)
+    pre = _constants(net, Ha, load)
     for k in range(K + 1):
-        ev = evaluate(net, Ha, load, lam, mu[:, :nl], mu[:, nl:])
+        ev = evaluate(net, Ha, load, lam, mu[:, :nl], mu[:, nl:], _pre=pre)
         g = ev.value
         if hist is not None:
             hist[:, k] = g
