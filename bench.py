@@ -72,7 +72,8 @@ def opt_spec(args):
 
 def gap_key(args):
     _, alpha = opt_spec(args)
-    return f"{args.workload}/{args.form}" + ("" if args.opt == "plain" else f"/{args.opt}/{alpha:g}")
+    return (f"{args.workload}/{args.form}" + ("" if args.opt == "plain" else f"/{args.opt}/{alpha:g}")
+            + (f"/{args.decay}" if args.decay else ""))
 UNIT = "instance-iterations/s"
 
 
@@ -93,7 +94,8 @@ def parse():
                     help="weak: each rank its own configs[4]-sized batch (default); strong: configs[4] split")
     ap.add_argument("--opt", default="plain", choices=sorted(OPTS),
                     help="ascent-step variant (PAPER.md:245); non-plain variants run on the cluster path")
-    ap.add_argument("--alpha", type=float, default=None, help="constant step (default: the variant's)")
+    ap.add_argument("--alpha", type=float, default=None, help="step (default: the variant's)")
+    ap.add_argument("--decay", default=None, help="step decay: inv:T (alpha/(1+k/T)) or step:F:N (alpha F^floor(k/N))")
     return ap.parse_args()
 
 
@@ -249,7 +251,7 @@ def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, 
     target[ids[mine] - lo] = best_ref[mine] - rel * np.abs(best_ref[mine])
     h.set_instance_batch(load_dev, outs_dev, stream=stream)
     h.set_target(target, stream=stream)
-    alpha = inst.alpha_schedule(K, float(ref["alpha"]))
+    alpha = inst.alpha_schedule(K, float(ref["alpha"]), ref.get("decay"))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
@@ -388,7 +390,7 @@ def main():
     h.set_instance_batch(load_dev, outs_dev, stream=stream)
     info = h.info()
     K, W = args.steps, args.warmup
-    alpha = inst.alpha_schedule(max(K, W, 1), alpha0)
+    alpha = inst.alpha_schedule(max(K, W, 1), alpha0, args.decay)
 
     def barrier():
         if world > 1:
@@ -470,7 +472,7 @@ def main():
                "timed": "set_instance_batch(host pinned) + iterate(K) + get_bound(host), wall clock, max over ranks"}
 
     dense = form == dual.FORM_PTDF
-    if rank == 0 and dense:
+    if rank == 0 and dense and B > 16:
         peak_t = fp64_peak_tflops(dev)
     if rank == 0:
         peak, peak_src = peaks()
@@ -497,7 +499,13 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src}
-        if dense:  # two GEMMs per step, 2 n_l n_g flops each per instance (the final evaluation not counted)
+        if dense and B <= 16:  # skinny batch: two matrix-vector passes, H_g read twice per step (HBM-bound)
+            per_step = 16.0 * net.n_branch * net.n_gen + 8.0 * B * (7 * net.n_branch + 2 * net.n_gen)
+            ach = per_step * K / (ms / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": None, "alg_bytes_per_step": per_step, "peak_source": peak_src,
+                    "kernel": "the whole step (2 matrix-vector kernels reading H_g, epilogues, fused finisher)"}
+        elif dense:  # two GEMMs per step, 2 n_l n_g flops each per instance (the final evaluation not counted)
             flops = 4.0 * net.n_branch * net.n_gen * B * K
             ach_t = flops / (ms / 1e3) / 1e12
             roof = {"bound": "tensor", "achieved": ach_t, "peak": peak_t, "unit": "TFLOP/s", "frac": ach_t / peak_t,
@@ -518,7 +526,7 @@ def main():
             "scaling": (args.scaling if B_total > 1 else "replicas"),
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE.json recipe)",
             "config": {"workload": args.workload, "form": args.form, "cost": "QP" if quad else "LP",
-                       "step": {"variant": args.opt, "alpha": alpha0, **OPTS[args.opt][1]},
+                       "step": {"variant": args.opt, "alpha": alpha0, "decay": args.decay, **OPTS[args.opt][1]},
                        "n_bus": net.n_bus, "n_branch": net.n_branch, "n_gen": net.n_gen,
                        "B_total": B_total, "B_per_gpu": B,
                        "path": {1: "batched-sweep", 2: "single", 3: "cluster", 4: "dense-gemm"}[path],
@@ -535,13 +543,14 @@ def main():
                        if B_total > 1 and not dense else ("H_g %.2f GB read twice per step" %
                                                             (2 * 8 * net.n_branch * net.n_gen / 1e9)
                                                             if dense else "state on chip (single instance)"),
-                       "timed_launches": (f"{3 * (K + 1)} launches: 3 per step ({K} steps) + the final evaluation"
+                       "timed_launches": (f"{(2 if B <= 16 else 3) * (K + 1)} launches: {2 if B <= 16 else 3} per step "
+                                          f"({K} steps) + the final evaluation"
                                           if dense else f"1 persistent launch: {K} iterations + final evaluation")},
             "roofline": roof,
             "cpu_baseline": cpu,
             "time_to_gap": ttg,
             "e2e": e2e,
-            "gpu_launches": 3 * (K + 1) if dense else 1,
+            "gpu_launches": ((2 if B <= 16 else 3) * (K + 1)) if dense else 1,
             "clocks": clk,
             "gather_ms": gather_ms,
         }

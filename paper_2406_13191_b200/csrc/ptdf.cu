@@ -1630,6 +1630,13 @@ void ptdf_info(const PtdfState *st, dcopf_info *info) {
   info->grid = (int)((st->nlp / BM) * (st->Bp / BN));
   info->launches_per_iter = 3;
   info->tile_width = BN;
+  if (st->nbv) {  // skinny batch: warp-per-row matrix-vector kernels (grid of the line kernel)
+    info->smem_bytes = 0;
+    info->threads_per_block = VT;
+    info->grid = skinny_blocks_l(st->nl);
+    info->launches_per_iter = 2;
+    info->tile_width = st->nbv;
+  }
   info->cluster_size = 1;
 }
 

@@ -293,9 +293,19 @@ def config4_batch(net: Network, ids, seed: int = 0, variant: str = "4",
     return Batch(load=load, outages=(outs if variant == "4" else None), instance_ids=ids)
 
 
-def alpha_schedule(K: int, alpha: float = ALPHA) -> np.ndarray:
-    """Explicit step array (reading A-9): both sides consume identical values."""
-    return np.full(int(K), float(alpha), dtype=np.float64)
+def alpha_schedule(K: int, alpha: float = ALPHA, decay: Optional[str] = None) -> np.ndarray:
+    """Explicit step array (reading A-9): both sides consume identical values.
+    decay (the paper's step decay; reading A-26): None = constant,
+    "inv:T" = alpha / (1 + k/T), "step:F:N" = alpha * F^floor(k/N)."""
+    k = np.arange(int(K), dtype=np.float64)
+    if not decay:
+        return np.full(int(K), float(alpha), dtype=np.float64)
+    kind, *par = decay.split(":")
+    if kind == "inv":
+        return float(alpha) / (1.0 + k / float(par[0]))
+    if kind == "step":
+        return float(alpha) * float(par[0]) ** np.floor(k / float(par[1]))
+    raise ValueError(f"unknown decay {decay!r}")
 
 
 # ----------------------------------------------------------------------------

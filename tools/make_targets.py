@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--workloads", nargs="*", default=None)
     ap.add_argument("--forms", nargs="*", default=["F2", "F1"])
+    ap.add_argument("--decay", default=None, help="step decay (instances.alpha_schedule)")
+    ap.add_argument("--K", type=int, default=None, help="override the workload's K")
     a = ap.parse_args()
     js = json.load(open(OUT)) if os.path.exists(OUT) else {}
     import bench
@@ -60,25 +62,31 @@ def main():
                                 ("PTDF", None)):
             if form_name not in a.forms:
                 continue
-            key = f"{wl}/{form_name}" + ("" if a.opt == "plain" else f"/{a.opt}/{alpha:g}")
+            key = (f"{wl}/{form_name}" + ("" if a.opt == "plain" else f"/{a.opt}/{alpha:g}")
+                   + (f"/{a.decay}" if a.decay else ""))
             if a.only and key not in a.only:
                 continue
-            if form_name == "PTDF" and wl != "config4b":
+            if form_name == "PTDF" and wl not in ("config4b", "config1", "config3"):
                 continue
             net = inst.make_network(config, quadratic=quad)
-            K = inst.ITERS[config]
+            K = a.K or inst.ITERS[config]
             if form_name == "PTDF":
                 import dataclasses
                 from oracle import ptdf as P
-                ids = np.arange(0, inst.CONFIG4_BATCH, 512)
-                batch = inst.config4_batch(net, ids, variant="4b")
+                if config == 4:
+                    ids = np.arange(0, inst.CONFIG4_BATCH, 512)
+                    batch = inst.config4_batch(net, ids, variant="4b")
+                else:
+                    ids = np.zeros(1, dtype=np.int64)
+                    batch = inst.single_batch(net)
                 t0 = time.time()
-                res = P.solve(net, batch.load, K, inst.alpha_schedule(K, alpha), opt=opt)
+                res = P.solve(net, batch.load, K, inst.alpha_schedule(K, alpha, a.decay), opt=opt)
                 th = np.full(net.n_bus, 1e6)
                 th[net.ref_bus] = 0.0
                 nob = dataclasses.replace(net, theta_max=th)
                 primal = [inst.primal_lp(nob, batch.load[r])[1] for r in range(len(ids))]
-                js[key] = {"K": K, "alpha": alpha, "opt": {"name": a.opt, **opt}, "primal_opt": primal,
+                js[key] = {"K": K, "alpha": alpha, "decay": a.decay, "opt": {"name": a.opt, **opt},
+                           "primal_opt": primal if config == 4 else primal[0],
                            "primal_note": "LP optimum of Eq. 1 (no angle box)",
                            "instance_ids": ids.tolist(), "best": res.best.tolist(), "bound": res.bound.tolist(),
                            "status": res.status.tolist(), "source": "oracle/ptdf.py via tools/make_targets.py"}
@@ -96,7 +104,7 @@ def main():
             if config == 4:  # only non-tree branches are ever taken out (bench.py passes the same mask)
                 sw = np.zeros(net.n_branch, np.uint8)
                 sw[net.n_tree:] = 1
-            res = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K, alpha),
+            res = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=inst.alpha_schedule(K, alpha, a.decay),
                                form=form, threads=a.threads, opt=opt, switchable=sw)
             primal = None
             if config != 4:  # the exact optimum (HiGHS; Kelley cutting planes for QP): true gap, (ii)
