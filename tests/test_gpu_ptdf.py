@@ -309,3 +309,15 @@ def test_config4b_full_size_sampled():
     orc = _orc(net, batch.load[idx], K, a)
     assert_parity(net, gpu, orc, idx=idx)
     assert gpu["info"].B_padded == inst.CONFIG4_BATCH
+
+
+def test_decay_schedule_single_instance():
+    """The schedule that gives the fastest time to gap on one instance (Adam,
+    alpha_k = 5 / (1 + k/200)): skinny mode against the oracle."""
+    net = inst.make_network(0)
+    K = 2000
+    a = inst.alpha_schedule(K, 5.0, "inv:200")
+    loads = _scaled_loads(net, 2, 23)
+    gpu = _gpu(net, loads, K, a, opt=ADAM, split=700)
+    orc = _orc(net, loads, K, a, opt=ADAM)
+    assert_parity(net, gpu, orc, br_mask=~_no_flow_lines(net, P.ptdf(net), loads))

@@ -741,3 +741,16 @@ def test_stopping_rule_oracle():
     z0 = oracle.solve(net, net.base_load, K=3000, alpha=a, opt=ADAM)
     np.testing.assert_array_equal(z.lam, z0.lam)
     assert z.status[0] == 0
+
+
+def test_alpha_schedule_decays():
+    """The explicit step arrays (reading A-9) with the paper's step decay
+    (PAPER.md:348): constant, alpha/(1 + k/T), alpha F^floor(k/N)."""
+    a = inst.alpha_schedule(6, 2.0)
+    assert np.all(a == 2.0)
+    a = inst.alpha_schedule(5, 5.0, "inv:200")
+    np.testing.assert_allclose(a, 5.0 / (1.0 + np.arange(5) / 200.0), rtol=0, atol=0)
+    a = inst.alpha_schedule(7, 2.0, "step:0.5:3")
+    np.testing.assert_array_equal(a, [2, 2, 2, 1, 1, 1, 0.5])
+    with pytest.raises(ValueError):
+        inst.alpha_schedule(3, 1.0, "cosine:1")
