@@ -4,8 +4,9 @@ on B200, in dual-ascent instance-iterations per second (BASELINE.json metric).
 
 Default workload = BASELINE.json configs[4]: the 10000-bus / 12700-branch /
 2500-generator network, 8192 load-scenario / line-switching instances, linear
-cost, form F2, sharded contiguously over the ranks (fixed total batch:
-"scaling": "strong").
+cost, form F2.  Multi-GPU default "scaling": "weak" -- every rank iterates its
+own configs[4]-sized batch (rank r: instances [8192 r, 8192 (r+1)) of the seeded
+sweep); --scaling strong splits one 8192-instance batch instead.
 
 A "step" is one ascent iteration (S1-S4) over the rank's whole batch.  The
 timed region is one dcopf_dual_iterate(K) call = ONE persistent kernel launch
@@ -19,7 +20,10 @@ not counted as work, so the reported rate is conservative).
 --form PTDF runs the paper's dense-PTDF Eq. 1 on the dense
 path (two fused fp64 DMMA GEMMs per step); it takes load-only batches, so its
 workload is config4b (or a single-instance config); its roofline is the fp64
-tensor-core peak measured live (cuBLAS DGEMM through torch.matmul).
+tensor-core peak measured live (cuBLAS DGEMM through torch.matmul), or HBM for
+batches of <= 16 instances (matrix-vector kernels).  --decay inv:T | step:F:N
+gives the paper's step decay (e.g. config 3, PTDF, --opt adam --alpha 5
+--decay inv:200: the fastest time to a 1e-3 gap measured).
 
 Multi-GPU: launched by torchrun; one process per GPU; the instances are
 sharded with no communication in the loop; one NCCL all_gather of the
