@@ -512,8 +512,16 @@ def main():
         elif dense:  # two GEMMs per step, 2 n_l n_g flops each per instance (the final evaluation not counted)
             flops = 4.0 * net.n_branch * net.n_gen * B * K
             ach_t = flops / (ms / 1e3) / 1e12
+            traffic_t = None  # DRAM bytes of the timed launches, from the committed ncu launch list
+            try:
+                pk = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))["config4b/PTDF"]["per_kernel"]
+                if args.workload == "config4b" and B == inst.CONFIG4_BATCH:
+                    traffic_t = K * sum(v["dram_read"] + v["dram_write"] for v in pk.values())
+            except Exception:
+                pass
             roof = {"bound": "tensor", "achieved": ach_t, "peak": peak_t, "unit": "TFLOP/s", "frac": ach_t / peak_t,
-                    "traffic": None, "alg_flops_per_inst_iter": 4 * net.n_branch * net.n_gen,
+                    "traffic": traffic_t, "traffic_note": "DRAM bytes (ncu) of K steps: GEMM1 + GEMM2 + finisher",
+                    "alg_flops_per_inst_iter": 4 * net.n_branch * net.n_gen,
                     "peak_source": "measured live: cuBLAS DGEMM 8192^3 via torch.matmul, best of 5 (fp64)",
                     "kernel": "the whole step (2 fused DMMA GEMMs + the per-instance finisher)"}
         cpu = None
