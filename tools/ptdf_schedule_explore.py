@@ -12,10 +12,14 @@ from paper_2406_13191_b200 import dual, instances as inst
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
-net = inst.make_network(cfg)
+qp = len(sys.argv) > 3 and sys.argv[3] == "qp"
+net = inst.make_network(cfg, quadratic=qp)
 th = np.full(net.n_bus, 1e6)
 th[net.ref_bus] = 0.0
-opt = inst.primal_lp(dataclasses.replace(net, theta_max=th), net.base_load)[1]
+if qp:  # Kelley cutting planes: the optimum to ~1e-10 (its upper bound is used)
+    opt = inst.primal_qp(dataclasses.replace(net, theta_max=th), net.base_load)[2]
+else:
+    opt = inst.primal_lp(dataclasses.replace(net, theta_max=th), net.base_load)[1]
 print("config", cfg, "opt", opt, flush=True)
 k = np.arange(K, dtype=np.float64)
 S = {
