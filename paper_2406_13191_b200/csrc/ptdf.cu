@@ -468,12 +468,6 @@ __global__ void __launch_bounds__(256) k_finish_blk(const FinArgs f) {
 // (A = H_g^T, row g, K = n_l), GEMM2 rows are lines (A = H_g, row l, K = n_g).
 // Each block writes its partial sums per instance to part[block][b] (ld NB).
 constexpr int VT = 512, VW = VT / 32;   // threads and warps per block
-#ifndef PTDF_GEN_MINB
-#define PTDF_GEN_MINB 1
-#endif
-#ifndef PTDF_LINE_MINB
-#define PTDF_LINE_MINB 1
-#endif
 #ifndef PTDF_DU
 #define PTDF_DU 1
 #endif
@@ -484,6 +478,11 @@ constexpr int VT = 512, VW = VT / 32;   // threads and warps per block
 #define PTDF_WPR_L 1
 #endif
 constexpr int WPR_G = PTDF_WPR_G, WPR_L = PTDF_WPR_L;  // warps per row: GEMM1 rows are 100 KB (config 3), GEMM2 rows 20 KB
+
+// resident blocks per SM the register budget is sized for: 3 (<= 42 registers)
+// for 1-2 columns -- measured: 116 us/it at 3 blocks vs 118 at 2 and 134 at 1 on
+// one config-3 instance -- fewer where the per-column state would spill
+constexpr int skinny_minb(int nb) { return nb <= 2 ? 3 : (nb <= 4 ? 2 : 1); }
 
 template <int NB>
 __device__ __forceinline__ void warp_dot(const double *__restrict__ row, const double *__restrict__ xc, int k0,
@@ -574,7 +573,7 @@ __device__ __forceinline__ void row_dot(const GemmArgs &g, int row, bool live, c
 }
 
 template <int NB>
-__global__ void __launch_bounds__(VT, PTDF_GEN_MINB) k_gen_row(const GemmArgs g, const double *__restrict__ nuc,
+__global__ void __launch_bounds__(VT, skinny_minb(NB)) k_gen_row(const GemmArgs g, const double *__restrict__ nuc,
                                                 double *__restrict__ pc) {
   __shared__ double red[2][VW * NB];
   __shared__ double rp[VW][NB];
@@ -603,7 +602,7 @@ __global__ void __launch_bounds__(VT, PTDF_GEN_MINB) k_gen_row(const GemmArgs g,
 // the last block to finish (atomic ticket) sums every block's partials per
 // instance in a fixed order and runs the per-instance finisher: no extra launch
 template <int NB, bool STEP, bool FEVAL>
-__global__ void __launch_bounds__(VT, PTDF_LINE_MINB) k_line_row(const GemmArgs g, const double *__restrict__ pcv,
+__global__ void __launch_bounds__(VT, skinny_minb(NB)) k_line_row(const GemmArgs g, const double *__restrict__ pcv,
                                                  double *__restrict__ nuc, const FinArgs f, unsigned *ticket) {
   __shared__ double red[VW * NB];
   __shared__ double fred[3][VT];
