@@ -472,7 +472,7 @@ constexpr int VT = 512, VW = VT / 32;   // threads and warps per block
 #define PTDF_DU 1
 #endif
 #ifndef PTDF_WPR_G
-#define PTDF_WPR_G 4
+#define PTDF_WPR_G 2
 #endif
 #ifndef PTDF_WPR_L
 #define PTDF_WPR_L 1
@@ -500,18 +500,29 @@ __device__ __forceinline__ void warp_dot(const double *__restrict__ row, const d
   for (; k + 64 * (DU - 1) < K; k += 64 * DU) {
     double2 a[DU];
 #pragma unroll
-    for (int u = 0; u < DU; ++u) a[u] = *reinterpret_cast<const double2 *>(row + k + 64 * u);
+    for (int u = 0; u < DU; ++u) a[u] = __ldcs(reinterpret_cast<const double2 *>(row + k + 64 * u));
 #pragma unroll
     for (int u = 0; u < DU; ++u) {
       const int kk = k + 64 * u;
 #pragma unroll
-      for (int b = 0; b < NB; ++b) part[u][b] += a[u].x * xc[kk * NB + b] + a[u].y * xc[(kk + 1) * NB + b];
+      if (NB == 1) {  // the vector pair in one 16-byte load
+        const double2 x = *reinterpret_cast<const double2 *>(xc + kk);
+        part[u][0] += a[u].x * x.x + a[u].y * x.y;
+      } else {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) part[u][b] += a[u].x * xc[kk * NB + b] + a[u].y * xc[(kk + 1) * NB + b];
+      }
     }
   }
   for (int u = 0; k < K; k += 64, ++u) {
-    const double2 a = *reinterpret_cast<const double2 *>(row + k);
+    const double2 a = __ldcs(reinterpret_cast<const double2 *>(row + k));
+    if (NB == 1) {
+      const double2 x = *reinterpret_cast<const double2 *>(xc + k);
+      part[u % DU][0] += a.x * x.x + a.y * x.y;
+    } else {
 #pragma unroll
-    for (int b = 0; b < NB; ++b) part[u % DU][b] += a.x * xc[k * NB + b] + a.y * xc[(k + 1) * NB + b];
+      for (int b = 0; b < NB; ++b) part[u % DU][b] += a.x * xc[k * NB + b] + a.y * xc[(k + 1) * NB + b];
+    }
   }
 #pragma unroll
   for (int u = 1; u < DU; ++u)
