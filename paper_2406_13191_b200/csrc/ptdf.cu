@@ -468,6 +468,9 @@ __global__ void __launch_bounds__(256) k_finish_blk(const FinArgs f) {
 // (A = H_g^T, row g, K = n_l), GEMM2 rows are lines (A = H_g, row l, K = n_g).
 // Each block writes its partial sums per instance to part[block][b] (ld NB).
 constexpr int VT = 512, VW = VT / 32;   // threads and warps per block
+#ifndef PTDF_LINE_CAP
+#define PTDF_LINE_CAP (148 * 3)
+#endif
 #ifndef PTDF_DU
 #define PTDF_DU 1
 #endif
@@ -620,11 +623,16 @@ __global__ void __launch_bounds__(VT, skinny_minb(NB)) k_line_row(const GemmArgs
   __shared__ bool last;
   __shared__ double rp[VW][NB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int row = blockIdx.x * (VW / WPR_L) + warp / WPR_L;
-  const bool live = row < g.nl;
   double sv[NB], acc[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) sv[b] = 0.0;
+  // grid-stride over row groups (the grid is capped at the resident blocks, so
+  // the rows spread evenly over the SMs instead of a ragged second wave)
+  constexpr int RPB = VW / WPR_L;
+  const int iters = (g.nl + gridDim.x * RPB - 1) / (gridDim.x * RPB);
+  for (int it = 0; it < iters; ++it) {
+  const int row = (it * gridDim.x + blockIdx.x) * RPB + warp / WPR_L;
+  const bool live = row < g.nl;
   row_dot<NB, WPR_L>(g, row, live, pcv, rp, acc);  // (H_g p*)_l
   if (live && warp % WPR_L == 0) {
     const double al = STEP ? g.alpha[g.k] : 0.0;
@@ -666,6 +674,7 @@ __global__ void __launch_bounds__(VT, skinny_minb(NB)) k_line_row(const GemmArgs
       }
     }
   }
+  }  // rows
   block_part<NB>(red, sv, g.part_line);
   __threadfence();
   __syncthreads();
@@ -1054,7 +1063,9 @@ int copy_rows_out(PtdfState *st, double *dst, const double *src, long rows, cuda
 }
 
 int skinny_blocks_g(int rows) { return std::max(1, (rows + VW / WPR_G - 1) / (VW / WPR_G)); }
-int skinny_blocks_l(int rows) { return std::max(1, (rows + VW / WPR_L - 1) / (VW / WPR_L)); }
+int skinny_blocks_l(int rows) {  // capped at the blocks resident on 148 SMs (the kernel strides over rows)
+  return std::max(1, std::min((rows + VW / WPR_L - 1) / (VW / WPR_L), PTDF_LINE_CAP));
+}
 
 template <int NB>
 int skinny_pass_t(PtdfState *st, const GemmArgs &g1, const GemmArgs &g2, bool step, const FinArgs &f, bool feval,
