@@ -321,3 +321,37 @@ def test_decay_schedule_single_instance():
     gpu = _gpu(net, loads, K, a, opt=ADAM, split=700)
     orc = _orc(net, loads, K, a, opt=ADAM)
     assert_parity(net, gpu, orc, br_mask=~_no_flow_lines(net, P.ptdf(net), loads))
+
+
+def test_evaluate_gemm_mode_and_rejections():
+    """evaluate() on the GEMM kernels (B > 16) against the oracle; set_multipliers
+    rejects NaN and mu < 0; compaction is not offered for the PTDF form."""
+    import torch
+    net = inst.make_network(0)
+    Ha = P.ptdf(net)
+    B = 40
+    rng = np.random.default_rng(31)
+    loads = _scaled_loads(net, B, 9)
+    lam = rng.normal(0, 20, B)
+    mu = np.abs(rng.normal(0, 5, (B, 2 * net.n_branch)))
+    h = dual.DcopfDual(net, form=dual.FORM_PTDF)
+    h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(loads.T)).to("cuda:0"))
+    h.set_multipliers(np.ascontiguousarray(lam[None, :]), np.ascontiguousarray(mu.T))
+    val, gl, gb = np.empty(B), np.empty((1, B)), np.empty((2 * net.n_branch, B))
+    h.evaluate(val, gl, gb)
+    ev = P.evaluate(net, Ha, loads, lam, mu[:, :net.n_branch], mu[:, net.n_branch:])
+    S = cost_scale(net)
+    assert np.all(np.abs(val - ev.value) <= BOUND_RTOL * np.maximum(np.abs(ev.value), S))
+    assert np.max(np.abs(gb.T - np.concatenate([ev.g_mup, ev.g_mum], axis=1))) <= 1e-11 * max(1.0, np.abs(gb).max())
+    assert np.max(np.abs(gl[0] - ev.g_lam)) <= 1e-11 * max(1.0, np.abs(ev.g_lam).max())
+    bad = mu.copy()
+    bad[3, 2] = np.nan
+    with pytest.raises(dual.DcopfError):
+        h.set_multipliers(None, np.ascontiguousarray(bad.T))
+    with pytest.raises(dual.DcopfError):
+        h.compact()
+    # the matrix into a device buffer equals the host copy
+    Hd = torch.empty((net.n_branch, net.n_bus), dtype=torch.float64, device="cuda:0")
+    h.get_ptdf(Hd)
+    np.testing.assert_array_equal(Hd.cpu().numpy(), h.get_ptdf())
+    h.close()
