@@ -56,6 +56,8 @@ struct GemmArgs {
   long ldb;
   int M, N, K, group;
   int noff;  // first column of this launch (a launch covers columns [noff, noff + N))
+  int ktps;          // split-K (EPI_STORE, gridDim.y splits): k-tiles per split (0: all)
+  long c_split;      // ... and the distance between the splits' C blocks
   long ld;  // leading dimension of every [rows][B_pad] array (= B_pad) / of C for EPI_STORE
   double *C;
   // EPI_GEN (rows = generators)
@@ -144,10 +146,12 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
   const int gs = min(nMt - first_m, g.group);
   const int mt = first_m + (t % (g.group * nNt)) % gs, nt = (t % (g.group * nNt)) / gs;
   const int m0 = mt * BM, n0 = g.noff + nt * BN;
-  const int KT = g.K / BK;
+  // split-K (gridDim.y > 1, EPI_STORE only): this CTA's k-tile range
+  const int KT0 = g.ktps ? blockIdx.y * g.ktps : 0;
+  const int KT = g.ktps ? min(g.K / BK - KT0, g.ktps) : g.K / BK;
 
   auto load_stage = [&](int stage, int kt) {
-    const int k0 = kt * BK;
+    const int k0 = (KT0 + kt) * BK;
     double *as = As + stage * A_STAGE, *bs = Bs + stage * B_STAGE;
 #pragma unroll
     for (int c = tid; c < BM * BK / 2; c += NTHR) {
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        *reinterpret_cast<double2 *>(g.C + (size_t)(rbase + i * 8) * g.ld + cbase + j * 8) =
+        *reinterpret_cast<double2 *>(g.C + blockIdx.y * g.c_split + (size_t)(rbase + i * 8) * g.ld + cbase + j * 8) =
             make_double2(acc[i][j][0], acc[i][j][1]);
     return;
   }
@@ -457,6 +461,34 @@ __global__ void __launch_bounds__(256) k_finish_blk(const FinArgs f) {
     __syncthreads();
   }
   if (threadIdx.x == 0) finish_one<EVAL>(f, n, red[0][0], red[1][0], red[2][0]);
+}
+
+// ---------------------------------------------------------------------------
+// Medium batches: GEMM1 (K = n_l) split over K when its tiles cannot fill the
+// GPU; this kernel sums the splits' Q blocks in split order and applies the
+// GEMM1 epilogue -- one thread per column, the 64 rows of an M tile in order.
+__global__ void __launch_bounds__(BN) k_gen_reduce(const GemmArgs g, const double *__restrict__ Qs, int S,
+                                                   long split) {
+  const int mt = blockIdx.x, n = g.noff + blockIdx.y * BN + threadIdx.x;
+  double so = 0.0, sp = 0.0;
+  const double lam = g.lam[n];
+  for (int r = 0; r < BM; ++r) {
+    const int row = mt * BM + r;
+    const bool live = row < g.ng;
+    double Q = 0.0;
+    for (int x = 0; x < S; ++x) Q += Qs[x * split + (size_t)row * g.ld + n];
+    double p = 0.0;
+    if (live) {
+      const double a = g.ga ? g.ga[row] : 0.0;
+      const double q = (g.gc[row] + lam) + Q;  // q = c + lambda 1 + H_g^T nu
+      p = minimiser(q, g.glo[row], g.ghi[row], a);
+      so += a * p * p + q * p;
+      sp += p;
+    }
+    g.P[(size_t)row * g.ld + n] = p;
+  }
+  g.part_obj[(size_t)mt * g.ld + n] = so;
+  g.part_p[(size_t)mt * g.ld + n] = sp;
 }
 
 // ---------------------------------------------------------------------------
@@ -826,6 +858,10 @@ struct PtdfState {
   int nbv = 0;
   double *nuc = nullptr, *pcv = nullptr, *sp_obj = nullptr, *sp_p = nullptr, *sp_line = nullptr;
   unsigned *ticket = nullptr;  // last-block ticket of the skinny line kernel (zero between launches)
+  // medium batches: split-K scratch of GEMM1 ([S][n_g pad][B_pad]), CTA slots of the GPU
+  double *qsplit = nullptr;
+  size_t qsplit_n = 0;
+  int n_slots = 296;
   cudaStream_t sub[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
 };
@@ -863,7 +899,8 @@ template <int EPI>
 int launch_gemm(const GemmArgs &g, cudaStream_t s, std::string *err) {
   if (g.M == 0 || g.N == 0) return DCOPF_OK;
   const int tiles = (g.M / BM) * (g.N / BN);
-  k_dgemm<EPI><<<tiles, NTHR, GEMM_SMEM, s>>>(g);
+  const int splits = (EPI == EPI_STORE && g.ktps) ? (g.K / BK + g.ktps - 1) / g.ktps : 1;
+  k_dgemm<EPI><<<dim3(tiles, splits), NTHR, GEMM_SMEM, s>>>(g);
   PCK(cudaGetLastError());
   return DCOPF_OK;
 }
@@ -1123,6 +1160,41 @@ void fin_tiles(const PtdfState *st, FinArgs *f) {
   }
 }
 
+// GEMM1 of one launch: fused epilogue, or -- when its tiles cannot fill the
+// GPU (medium batches) -- split over K into scratch + k_gen_reduce
+// (ncon: launches of this shape running concurrently, one per column group)
+int launch_gen(PtdfState *st, const GemmArgs &g1, cudaStream_t s, std::string *err, int ncon = 1) {
+  if (g1.M == 0 || g1.N == 0) return DCOPF_OK;
+  const int tiles = (g1.M / BM) * (g1.N / BN), ktiles = g1.K / BK;
+  int S = 1;
+  const char *ev = getenv("DCOPF_PTDF_SPLITK");  // measurement: 0 disables
+  // measured on config 3: B = 128 1.67 -> 0.91 ms/it, B = 512 +13%, B = 1024 (320 tiles) better unsplit
+  if (tiles * ncon < st->n_slots && ktiles >= 32 && !(ev && atoi(ev) == 0))
+    S = std::min((2 * st->n_slots + tiles * ncon - 1) / (tiles * ncon), ktiles / 16);
+  if (S <= 1) return launch_gemm<EPI_GEN>(g1, s, err);
+  GemmArgs gs = g1;
+  gs.ktps = (ktiles + S - 1) / S;
+  S = (ktiles + gs.ktps - 1) / gs.ktps;
+  const long split = (long)st->ngp * st->Bp;
+  // sized once for the most splits any launch of this batch can use, so the two
+  // column groups of iterate() (two streams) never see it reallocated
+  const size_t need = (size_t)std::max(1, ktiles / 16) * split;
+  if (st->qsplit_n < need) {
+    cudaFree(st->qsplit);
+    st->qsplit = nullptr;
+    st->qsplit_n = 0;
+    PCK(cudaMalloc(&st->qsplit, need * 8));
+    st->qsplit_n = need;
+  }
+  gs.C = st->qsplit;
+  gs.c_split = split;
+  int rc = launch_gemm<EPI_STORE>(gs, s, err);
+  if (rc) return rc;
+  k_gen_reduce<<<dim3(g1.M / BM, g1.N / BN), BN, 0, s>>>(g1, st->qsplit, S, split);
+  PCK(cudaGetLastError());
+  return DCOPF_OK;
+}
+
 int skinny_sync_nu(PtdfState *st, cudaStream_t s, std::string *err) {
   if (!st->nbv || st->nl == 0) return DCOPF_OK;
   k_compact_nu<<<blocks_for((size_t)st->nl * st->nbv), 256, 0, s>>>(st->nu, st->Bp, st->nl, st->nbv, st->nuc);
@@ -1243,6 +1315,11 @@ int ptdf_create(const PtdfNetIn &net, int device, PtdfState **out, std::string *
     return fail(DCOPF_ECUDA);
   }
   if (int arc = set_gemm_attrs(err)) return fail(arc);
+  {
+    int nsm = 148;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess)
+      st->n_slots = CTAS_PER_SM * nsm;
+  }
   // ---- device: S = C X T, W = L^{-T} (L^{-1} S), H_a = T - C^T W ----
   int *d_tin = nullptr, *d_tout = nullptr, *d_child = nullptr, *d_cp = nullptr, *d_cb = nullptr, *d_bp = nullptr,
       *d_bk = nullptr, *d_gbus = nullptr;
@@ -1346,7 +1423,7 @@ void ptdf_destroy(PtdfState *st) {
   cudaSetDevice(st->device);
   free_batch(st);
   double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch, st->nuc, st->pcv,
-                  st->sp_obj, st->sp_p, st->sp_line};
+                  st->sp_obj, st->sp_p, st->sp_line, st->qsplit};
   for (double *p : dp) cudaFree(p);
   for (int c = 0; c < 2; ++c) {
     if (st->sub[c]) cudaStreamDestroy(st->sub[c]);
@@ -1490,7 +1567,7 @@ int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist
       st->b2t = st->b2t * st->opt.beta2;
     }
     for (int c = 0; c < ns; ++c) {
-      int rc = launch_gemm<EPI_GEN>(G1[c], ss[c], err);
+      int rc = launch_gen(st, G1[c], ss[c], err, ns);
       if (rc) return rc;
       G2[c].k = (int)k;
       G2[c].b1t = Fc[c].b1t = st->b1t;
@@ -1583,7 +1660,7 @@ int ptdf_evaluate(PtdfState *st, double *value, double *grad_lambda, double *gra
   if (st->nbv) {
     rc = skinny_pass(st, gen_args(st), g2, false, f, true, s, err);
   } else {
-    rc = launch_gemm<EPI_GEN>(gen_args(st), s, err);
+    rc = launch_gen(st, gen_args(st), s, err);
     if (!rc) rc = launch_gemm<EPI_LINE_EVAL>(g2, s, err);
     if (!rc) k_finish<true><<<blocks_for(st->Bp), 256, 0, s>>>(f);
   }
