@@ -281,6 +281,9 @@ def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, 
            "and schedule (tests/golden/targets.json)", "sampled_instances": n, "reached": reached,
            "max_hit_iteration": worst if world == 1 else None, "seconds": secs, "run_seconds_full_K": run_s,
            "reference_best_range": [float(best_ref.min()), float(best_ref.max())]}
+    if np.all(best_ref[mine] == 0.0):
+        out["note"] = ("degenerate reference: the oracle's best bound after K steps is g(y_0) = 0 (this form and step "
+                       "never rise above the starting bound here, DESIGN.md §6b), so the target is met at evaluation 0")
     popt = ref.get("primal_opt")
     if popt is not None and mine.any():  # (ii): the true gap of the GPU's best bound after K, vs the optimum
         best = np.empty(batch.B)
