@@ -519,7 +519,8 @@ def main():
             try:
                 pk = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))["config4b/PTDF"]["per_kernel"]
                 if args.workload == "config4b" and B == inst.CONFIG4_BATCH:
-                    traffic_t = K * sum(v["dram_read"] + v["dram_write"] for v in pk.values())
+                    # per step: every kernel once per column group (two groups on two streams)
+                    traffic_t = K * 2 * sum(v["dram_read"] + v["dram_write"] for v in pk.values())
             except Exception:
                 pass
             roof = {"bound": "tensor", "achieved": ach_t, "peak": peak_t, "unit": "TFLOP/s", "frac": ach_t / peak_t,

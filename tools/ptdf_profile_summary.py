@@ -16,6 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 SRC = os.path.join(ROOT, "gpurun_out", "ptdf")
 NL, NG, B = 12700, 2500, 8192
+CHUNKS = 2  # iterate() runs the batch as two column groups on two streams: one launch covers B / 2
 
 
 def main():
@@ -44,7 +45,7 @@ def main():
         wr = sum(x["dram__bytes_write.sum"] for x in ms) / len(ms)
         e = {"launches": len(ms), "gpu_time_ms": round(t, 4), "dram_read": rd, "dram_write": wr}
         if "GEMM" in label:
-            e["fp64_tflops"] = round(2.0 * NL * NG * B / (t / 1e3) / 1e12, 2)
+            e["fp64_tflops"] = round(2.0 * NL * NG * (B / CHUNKS) / (t / 1e3) / 1e12, 2)
         out[label] = e
     rep = os.path.join(SRC, "ncu_dgemm.ncu-rep")
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
@@ -83,7 +84,7 @@ def main():
         + "\n".join(txt) + "\n")
     summ = json.load(open(os.path.join(PROF, "ncu_summary.json")))
     summ["config4b/PTDF"] = {"per_kernel": out, "tag": "r1_ptdf_ncu_dgemm",
-                             "alg_flops_per_gemm": 2 * NL * NG * B,
+                             "alg_flops_per_gemm_launch": 2 * NL * NG * B // CHUNKS,
                              "note": "ncu launch list (serialised, cold) of bench.py --workload config4b --form PTDF; "
                                      "the bench line's rate is the whole step over CUDA events"}
     json.dump(summ, open(os.path.join(PROF, "ncu_summary.json"), "w"), indent=1)
