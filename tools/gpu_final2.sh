@@ -10,5 +10,6 @@ python bench.py --form KVL --no-cpu-baseline > gpurun_out/final2/bench_config4_K
 python bench.py --workload config3 --steps 2000 --warmup 100 --no-cpu-baseline > gpurun_out/final2/bench_config3_F2.json 2>&1
 python bench.py --workload config3 --form KVL --opt adam --alpha 0.1 --steps 2000 --warmup 100 --no-cpu-baseline > gpurun_out/final2/bench_config3_KVL_adam.json 2>&1
 python bench.py --workload config3 --form PTDF --opt adam --alpha 5 --decay inv:200 --steps 2000 --warmup 100 > gpurun_out/final2/bench_config3_PTDF_adam_inv200.json 2>&1
-python bench.py --workload config4b --form PTDF --steps 30 --warmup 3 --no-gap > gpurun_out/final2/bench_config4b_PTDF.json 2>&1
+python bench.py --workload config4b --form PTDF --steps 30 --warmup 3 > gpurun_out/final2/bench_config4b_PTDF.json 2>&1
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/final2/bench_reference.json 2>&1
+python bench.py --workload config4b --form PTDF --opt adam --alpha 5 --decay inv:200 --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/final2/bench_config4b_PTDF_adam_inv200.json 2>&1
