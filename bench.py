@@ -21,7 +21,7 @@ not counted as work, so the reported rate is conservative).
 path (two fused fp64 DMMA GEMMs per step); it takes load-only batches, so its
 workload is config4b (or a single-instance config); its roofline is the fp64
 tensor-core peak measured live (cuBLAS DGEMM through torch.matmul), or HBM for
-batches of <= 16 instances (matrix-vector kernels).  --decay inv:T | step:F:N
+batches of <= 4 instances (matrix-vector kernels).  --decay inv:T | step:F:N
 gives the paper's step decay (e.g. config 3, PTDF, --opt adam --alpha 5
 --decay inv:200: the fastest time to a 1e-3 gap measured).
 
@@ -479,7 +479,7 @@ def main():
                "timed": "set_instance_batch(host pinned) + iterate(K) + get_bound(host), wall clock, max over ranks"}
 
     dense = form == dual.FORM_PTDF
-    if rank == 0 and dense and B > 16:
+    if rank == 0 and dense and B > 4:
         peak_t = fp64_peak_tflops(dev)
     if rank == 0:
         peak, peak_src = peaks()
@@ -506,7 +506,7 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src}
-        if dense and B <= 16:  # skinny batch: two matrix-vector passes, H_g read twice per step (HBM-bound)
+        if dense and B <= 4:  # skinny batch: two matrix-vector passes, H_g read twice per step (HBM-bound)
             per_step = 16.0 * net.n_branch * net.n_gen + 8.0 * B * (7 * net.n_branch + 2 * net.n_gen)
             ach = per_step * K / (ms / 1e3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
@@ -559,14 +559,14 @@ def main():
                        if B_total > 1 and not dense else ("H_g %.2f GB read twice per step" %
                                                             (2 * 8 * net.n_branch * net.n_gen / 1e9)
                                                             if dense else "state on chip (single instance)"),
-                       "timed_launches": (f"{(2 if B <= 16 else 3) * (K + 1)} launches: {2 if B <= 16 else 3} per step "
+                       "timed_launches": (f"{(2 if B <= 4 else 3) * (K + 1)} launches: {2 if B <= 4 else 3} per step "
                                           f"({K} steps) + the final evaluation"
                                           if dense else f"1 persistent launch: {K} iterations + final evaluation")},
             "roofline": roof,
             "cpu_baseline": cpu,
             "time_to_gap": ttg,
             "e2e": e2e,
-            "gpu_launches": ((2 if B <= 16 else 3) * (K + 1)) if dense else 1,
+            "gpu_launches": ((2 if B <= 4 else 3) * (K + 1)) if dense else 1,
             "clocks": clk,
             "gather_ms": gather_ms,
         }

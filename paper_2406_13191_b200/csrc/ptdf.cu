@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(BN) k_gen_reduce(const GemmArgs g, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// Skinny batches (B <= 16, e.g. one large instance): the two products are
+// Skinny batches (B <= 4, e.g. one large instance): the two products are
 // matrix-vector shaped, i.e. HBM-bound reads of H_g (254 MB at config 3), not
 // tensor work.  One warp per row, coalesced double2 loads along the row, the
 // vector in a compact [K][NB] copy (nu_c, p_c: L1/L2 resident), a fixed xor
@@ -962,7 +962,7 @@ struct PtdfState {
   // iterate(): the batch's column blocks in `nsplit` groups on their own streams,
   // so one group's GEMM tail overlaps the other's (instances are independent)
   int nsplit = 2;
-  // skinny batches (B <= 16): matrix-vector kernels; nbv = instance columns computed (0: GEMM mode)
+  // skinny batches (B <= 4): matrix-vector kernels; nbv = instance columns computed (0: GEMM mode)
   int nbv = 0;
   double *nuc = nullptr, *pcv = nullptr, *sp_obj = nullptr, *sp_p = nullptr, *sp_line = nullptr;
   unsigned *ticket = nullptr;  // last-block ticket of the skinny line kernel (zero between launches)
@@ -1568,10 +1568,12 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
   }
   st->B = B;
   st->Bp = Bp;
-  // skinny mode for B <= 16 (DCOPF_PTDF_SKINNY=0 forces the GEMMs; measurement)
+  // skinny mode for B <= 4 (DCOPF_PTDF_SKINNY=0 forces the GEMMs; measurement).  Measured on
+  // config 3 (us per step): skinny 100 / 208 / 624 / 2369 at B = 1 / 2 / 4 / 8, the split-K
+  // GEMMs a flat 934 for any B <= 128
   st->nbv = 0;
   const char *sk = getenv("DCOPF_PTDF_SKINNY");
-  if (B <= 16 && !(sk && atoi(sk) == 0)) {
+  if (B <= 4 && !(sk && atoi(sk) == 0)) {
     st->nbv = B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : (B <= 8 ? 8 : 16)));
     // compact vectors padded to the row padding (the double2 loads read one past an odd K)
     int rc0 = dalloc(&st->nuc, (size_t)st->nlk * 16 + 16, err);
