@@ -625,7 +625,7 @@ constexpr int WPR_G = PTDF_WPR_G, WPR_L = PTDF_WPR_L;  // warps per row: GEMM1 r
 // resident blocks per SM the register budget is sized for: 3 (<= 42 registers)
 // for 1-2 columns -- measured: 116 us/it at 3 blocks vs 118 at 2 and 134 at 1 on
 // one config-3 instance -- fewer where the per-column state would spill
-constexpr int skinny_minb(int nb) { return nb <= 2 ? 3 : (nb <= 4 ? 2 : 1); }
+constexpr int skinny_minb(int nb) { return nb <= 1 ? 3 : (nb <= 4 ? 2 : 1); }
 
 template <int NB>
 __device__ __forceinline__ void warp_dot(const double *__restrict__ row, const double *__restrict__ xc, int k0,
@@ -651,9 +651,14 @@ __device__ __forceinline__ void warp_dot(const double *__restrict__ row, const d
       if (NB == 1) {  // the vector pair in one 16-byte load
         const double2 x = *reinterpret_cast<const double2 *>(xc + kk);
         part[u][0] += a[u].x * x.x + a[u].y * x.y;
-      } else {
+      } else {  // the two vector rows as 16-byte loads (NB even)
 #pragma unroll
-        for (int b = 0; b < NB; ++b) part[u][b] += a[u].x * xc[kk * NB + b] + a[u].y * xc[(kk + 1) * NB + b];
+        for (int b = 0; b < NB; b += 2) {
+          const double2 x0 = *reinterpret_cast<const double2 *>(xc + kk * NB + b);
+          const double2 x1 = *reinterpret_cast<const double2 *>(xc + (kk + 1) * NB + b);
+          part[u][b] += a[u].x * x0.x + a[u].y * x1.x;
+          part[u][b + 1] += a[u].x * x0.y + a[u].y * x1.y;
+        }
       }
     }
   }
@@ -1569,8 +1574,8 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
   st->B = B;
   st->Bp = Bp;
   // skinny mode for B <= 4 (DCOPF_PTDF_SKINNY=0 forces the GEMMs; measurement).  Measured on
-  // config 3 (us per step): skinny 100 / 208 / 624 / 2369 at B = 1 / 2 / 4 / 8, the split-K
-  // GEMMs a flat 934 for any B <= 128
+  // config 3 (us per step): skinny 100 / 157 / 379 at B = 1 / 2 / 4 (2369 at B = 8), the
+  // split-K GEMMs a flat 934 for any B <= 128
   st->nbv = 0;
   const char *sk = getenv("DCOPF_PTDF_SKINNY");
   if (B <= 4 && !(sk && atoi(sk) == 0)) {
