@@ -317,7 +317,7 @@ int compile_schedule(dcopf_dual_t h, int W) {
     const int life = getenv("DCOPF_RING_LIFE") ? atoi(getenv("DCOPF_RING_LIFE")) : 4;
     cands.push_back({std::max(1, atoi(e)), life});
   }
-  const int chs[] = {32, 24, 20, 16, 14, 12, 10, 8, 6, 4, 2, 1}, lifes[] = {6, 4, 2};
+  const int chs[] = {32, 28, 26, 24, 22, 20, 16, 14, 12, 10, 8, 6, 4, 2, 1}, lifes[] = {6, 4, 2};
   for (int ch : chs)
     for (int life : lifes) cands.push_back({ch, life});
   Schedule sc;
