@@ -303,7 +303,8 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
 }
 
 // Compile + upload the sweep schedule for tile width W: the chunk starts at
-// DCOPF_CHUNK (default 32) and halves until the kernel's shared memory fits.
+// the largest of the candidate chunks (40 .. 1 buses; DCOPF_CHUNK to force one) and ring
+// lives whose kernel shared memory fits (config 4: F2 26, KVL 36, F1 16 buses).
 int compile_schedule(dcopf_dual_t h, int W) {
   if (h->sched_W == W) return DCOPF_OK;
   h->soft_sync = 1;  // measured faster for both forms at 19 consumer warps
@@ -317,7 +318,7 @@ int compile_schedule(dcopf_dual_t h, int W) {
     const int life = getenv("DCOPF_RING_LIFE") ? atoi(getenv("DCOPF_RING_LIFE")) : 4;
     cands.push_back({std::max(1, atoi(e)), life});
   }
-  const int chs[] = {32, 28, 26, 24, 22, 20, 16, 14, 12, 10, 8, 6, 4, 2, 1}, lifes[] = {6, 4, 2};
+  const int chs[] = {40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1}, lifes[] = {6, 4, 2};
   for (int ch : chs)
     for (int life : lifes) cands.push_back({ch, life});
   Schedule sc;
