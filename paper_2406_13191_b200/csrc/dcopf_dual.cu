@@ -303,22 +303,26 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
 }
 
 // Compile + upload the sweep schedule for tile width W: the chunk starts at
-// the largest of the candidate chunks (40 .. 1 buses; DCOPF_CHUNK to force one) and ring
-// lives whose kernel shared memory fits (config 4: F2 26, KVL 36, F1 16 buses).
+// the largest of the candidate chunks (48 .. 1 buses; DCOPF_CHUNK to force one) and ring
+// lives whose kernel shared memory fits (config 4: F2 26, KVL 48, F1 16 buses).
 int compile_schedule(dcopf_dual_t h, int W) {
   if (h->sched_W == W) return DCOPF_OK;
   h->soft_sync = 1;  // measured faster for both forms at 19 consumer warps
   if (const char *e = getenv("DCOPF_SYNC")) h->soft_sync = std::string(e) == "soft";
   // search (chunk, ring life) from large to small until the kernel's shared
   // memory fits: larger chunks mean fewer steps, longer ring lives fewer copies
-  int P = 2;
+  // program-block stages in flight: 2, except KVL, whose steps are shorter and
+  // whose shared memory is better spent on larger chunks (measured on config 4:
+  // KVL 1.17e7 at P = 2 / 36-row chunks, 1.21e7 at P = 1 / 48; F2 and F1 best at 2)
+  int P = (h->form == DCOPF_FORM_CYCLE) ? 1 : 2;
   if (const char *e = getenv("DCOPF_PREFETCH")) P = std::max(1, atoi(e));
   std::vector<std::pair<int, int>> cands;
   if (const char *e = getenv("DCOPF_CHUNK")) {
     const int life = getenv("DCOPF_RING_LIFE") ? atoi(getenv("DCOPF_RING_LIFE")) : 4;
     cands.push_back({std::max(1, atoi(e)), life});
   }
-  const int chs[] = {40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1}, lifes[] = {6, 4, 2};
+  const int chs[] = {48, 40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1},
+            lifes[] = {6, 4, 2};
   for (int ch : chs)
     for (int life : lifes) cands.push_back({ch, life});
   Schedule sc;
