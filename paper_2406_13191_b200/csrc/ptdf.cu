@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
   // tile the next tile's stage is awaited (one barrier per tile) before its
   // first fragments are loaded -- no shared-memory latency after the barrier.
   constexpr int KK = BK / 4;
+  static_assert(STAGES >= 3, "the double-buffered main loop waits for stage kt+1 one tile early");
   double fa[2][8], fb[2][4];
   auto ld_frag = [&](int buf, int stage, int kk) {
     const double *as = As + stage * A_STAGE + (wm * 64 + (lane >> 2)) * AST + (lane & 3) + kk * 4;
