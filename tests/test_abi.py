@@ -75,3 +75,38 @@ def test_validation_errors(lib):
 def test_last_error_null_handle(lib):
     msg = lib.dcopf_dual_last_error(None)
     assert isinstance(msg, bytes)
+
+
+def test_binding_constants_match_header():
+    """The ctypes binding's enum values and struct layouts are the header's."""
+    hdr = open(os.path.join(ROOT, "include", "dcopf_dual.h")).read()
+    vals = {k: int(v) for k, v in re.findall(r"\b(DCOPF_[A-Z_0-9]+)\s*=\s*(-?\d+)", hdr)}
+    assert vals["DCOPF_FORM_FLOW_BOX"] == dual.FORM_F2
+    assert vals["DCOPF_FORM_LIMIT_ROWS"] == dual.FORM_F1
+    assert vals["DCOPF_FORM_CYCLE"] == dual.FORM_KVL
+    assert vals["DCOPF_FORM_PTDF"] == dual.FORM_PTDF
+    assert (vals["DCOPF_PATH_AUTO"], vals["DCOPF_PATH_BATCHED"], vals["DCOPF_PATH_SINGLE"], vals["DCOPF_PATH_CLUSTER"],
+            vals["DCOPF_PATH_DENSE"]) == (dual.PATH_AUTO, dual.PATH_BATCHED, dual.PATH_SINGLE, dual.PATH_CLUSTER,
+                                          dual.PATH_DENSE)
+    assert (vals["DCOPF_INST_OK"], vals["DCOPF_INST_DIVERGED"], vals["DCOPF_INST_CONVERGED"]) == (
+        dual.INST_OK, dual.INST_DIVERGED, dual.INST_CONVERGED)
+    assert (vals["DCOPF_OPT_PLAIN"], vals["DCOPF_OPT_GDM"], vals["DCOPF_OPT_GDM_CLASSIC"], vals["DCOPF_OPT_ADAGRAD"],
+            vals["DCOPF_OPT_ADAM"]) == (dual.OPT_PLAIN, dual.OPT_GDM, dual.OPT_GDM_CLASSIC, dual.OPT_ADAGRAD,
+                                        dual.OPT_ADAM)
+    for k, v in vals.items():
+        if k in ("DCOPF_OK", "DCOPF_EINVAL", "DCOPF_ETOPOLOGY", "DCOPF_ECUDA", "DCOPF_ENOMEM", "DCOPF_ESTATE"):
+            assert v == 0 or dual.ERRORS[v] == k[len("DCOPF_"):]
+
+
+def test_binding_struct_sizes_match_c(tmp_path):
+    """sizeof of every ABI struct as the C compiler lays it out == the ctypes mirror."""
+    import subprocess
+    src = tmp_path / "sizes.c"
+    src.write_text('#include <stdio.h>\n#include "dcopf_dual.h"\nint main(void){printf("%zu %zu %zu %zu",'
+                   'sizeof(dcopf_network_desc),sizeof(dcopf_options),sizeof(dcopf_optimizer),sizeof(dcopf_info));'
+                   'return 0;}\n')
+    exe = tmp_path / "sizes"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert got == [ctypes.sizeof(dual.NetworkDesc), ctypes.sizeof(dual.Options), ctypes.sizeof(dual.Optimizer),
+                   ctypes.sizeof(dual.Info)]
