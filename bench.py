@@ -100,6 +100,11 @@ def parse():
                     help="ascent-step variant (PAPER.md:245); non-plain variants run on the cluster path")
     ap.add_argument("--alpha", type=float, default=None, help="step (default: the variant's)")
     ap.add_argument("--decay", default=None, help="step decay: inv:T (alpha/(1+k/T)) or step:F:N (alpha F^floor(k/N))")
+    ap.add_argument("--tile", default=None,
+                    help="V,C: batched path tiling (instances per lane, parts per tile); default: the library's choice")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="instances of the config4/config4b sweep (default 8192 = configs[4]); e.g. 1024 = one "
+                         "rank's shard of the literal 8-GPU split measured on one GPU")
     return ap.parse_args()
 
 
@@ -362,6 +367,8 @@ def main():
     dev = torch.device("cuda", local)
     form = {"F2": dual.FORM_F2, "F1": dual.FORM_F1, "KVL": dual.FORM_KVL, "PTDF": dual.FORM_PTDF}[args.form]
     config, quad, B_total = WORKLOADS[args.workload]
+    if args.batch is not None and B_total > 1:
+        B_total = int(args.batch)
     if form == dual.FORM_PTDF and args.workload == "config4":
         raise SystemExit("--form PTDF takes load-only batches: use --workload config4b (config 4 has outages)")
     if B_total > 1 and args.scaling == "weak":
@@ -387,7 +394,8 @@ def main():
         sw = np.zeros(net.n_branch, np.uint8)
         sw[net.n_tree:] = 1
     ospec, alpha0 = opt_spec(args)
-    h = dual.DcopfDual(net, form=form, device=local, path=path, switchable=sw)
+    tv, tc = (int(x) for x in args.tile.split(",")) if args.tile else (0, 0)
+    h = dual.DcopfDual(net, form=form, device=local, path=path, switchable=sw, lane_instances=tv, tile_parts=tc)
     if args.opt != "plain":
         h.set_optimizer(ospec["variant"], ospec.get("rho", 0.0), ospec.get("beta1", 0.0), ospec.get("beta2", 0.0),
                         ospec.get("eps", 0.0))
@@ -547,6 +555,8 @@ def main():
                        "B_total": B_total, "B_per_gpu": B,
                        "path": {1: "batched-sweep", 2: "single", 3: "cluster", 4: "dense-gemm"}[path],
                        "cluster_size": info.cluster_size,
+                       "tile": {"lane_instances": info.lane_instances, "parts": info.tile_parts,
+                                "halo_items": info.halo_items, "steps_per_sweep": info.steps_per_sweep},
                        "kernel": {"grid": info.grid, "threads": info.threads_per_block, "smem": info.smem_bytes,
                                   "chunk": info.chunk, "tile_width": info.tile_width,
                                   "copies_per_sweep": info.copies_per_sweep, "ring_life": info.ring_life,

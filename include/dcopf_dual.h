@@ -135,7 +135,11 @@ typedef struct {
   int32_t device;           /* CUDA device ordinal */
   int32_t path;             /* DCOPF_PATH_* */
   int32_t single_max_batch; /* AUTO threshold; <= 0 means 128 */
-  int32_t reserved[3];      /* zero */
+  int32_t tile_parts;       /* batched path, forms F2 / KVL: CTAs per instance tile (1..16), each
+                               sweeping a contiguous part of the network; 0 = chosen per batch */
+  int32_t lane_instances;   /* batched path, forms F2 / KVL: instances per lane, 2 or 4; 0 = chosen
+                               per batch (F1: always 2, one part) */
+  int32_t reserved[1];      /* zero */
 } dcopf_options;
 
 /* Create a handle: validates and copies the network, orders the buses
@@ -285,6 +289,11 @@ typedef struct {
   int32_t copies_per_sweep;       /* batched path: bulk copies per tile per iteration */
   int32_t ring_life;              /* batched path: rows live <= this many steps use the rings */
   int32_t cluster_size;           /* cluster path: CTAs per instance (1 otherwise) */
+  int32_t tile_parts;             /* batched path: CTAs per instance tile (each sweeps a part of the
+                                     network; the tile's parts meet once per iteration) */
+  int32_t lane_instances;         /* batched path: instances per lane (2 or 4) */
+  int32_t halo_items;             /* batched path: codes recomputed per sweep by the parts of a tile */
+  int32_t steps_per_sweep;        /* batched path: pipeline steps of the longest part */
 } dcopf_info;
 int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info);
 

@@ -34,14 +34,18 @@ using namespace dcopf;
 
 static thread_local std::string g_create_error;
 
-#ifndef DCOPF_SWEEP_WARPS
-#define DCOPF_SWEEP_WARPS 19
-#endif
-static const int kSweepWarps = DCOPF_SWEEP_WARPS;  // consumer warps of k_sweep (+1 producer warp = 20 warps, 640 threads)
+// consumer warps of k_sweep (+1 producer warp): 2 instances per lane 19 (640
+// threads, 96 registers), 4 per lane 15 (512 threads, 128 registers)
+constexpr int kSweepWarps2 = 19;
+constexpr int kSweepWarps4 = 15;
+inline int sweep_warps(int V) { return V == 4 ? kSweepWarps4 : kSweepWarps2; }
 
 struct dcopf_dual_s {
   std::string err;
   int device = 0, form = 0, path_opt = 0, single_max = 128, n_sm = 148, dev_smem = 0;
+  int opt_parts = 0, opt_lane = 0;
+  bool implied_box = false;
+  int force_cluster_C = 0;          // configure_cluster: only this cluster size (0: the smallest that fits)         // theta_max was NULL: the library computed the angle box  // dcopf_options tile_parts / lane_instances (0 = chosen per batch)
   int n_bus = 0, n_br = 0, n_gen = 0, ref_int = 0, quadratic = 0, bandwidth = 0;
   std::vector<int> bus_perm, bus_inv, br_perm, br_inv;  // perm: internal -> original
   std::vector<uint8_t> switchable;                      // original ids; empty = all
@@ -69,11 +73,16 @@ struct dcopf_dual_s {
   double *alpha_dev = nullptr, *alpha_pin = nullptr;  // schedule alpha[K]: device + pinned staging
   size_t alpha_cap = 0;
   cudaEvent_t alpha_ev = nullptr;                     // staging reusable once this fired
-  // compiled sweep schedule of the batched path (for tile width sched_W)
+  // compiled sweep schedule of the batched path (for tile width sched_W,
+  // sched_V instances per lane, sched_C parts per tile)
   Schedule sch;
-  int sched_W = 0;
-  int soft_sync = 0;  // k_sweep step synchronisation (see sweep_kernel.cuh); DCOPF_SYNC=soft|hard
+  int sched_W = 0, sched_V = 0, sched_C = 0;
+  int tile_V = 2, tile_C = 1;  // loaded batch: instances per lane, parts (CTAs) per tile
   uint8_t *d_prog = nullptr;
+  int *d_part_step0 = nullptr;
+  unsigned *d_tile_sync = nullptr;  // split tiles: per-tile arrival counters
+  double *d_part_val = nullptr;     // split tiles: per-part partial dual values [2][tiles][C][W]
+  size_t tile_sync_cap = 0, part_val_cap = 0;
   long long *d_prog_off = nullptr;
   int *d_prog_bytes = nullptr, *d_tx_bytes = nullptr, *d_ld_ptr = nullptr, *d_ld = nullptr;
   // batched path state layout: storage position <-> original id, per kind
@@ -302,50 +311,48 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
   return DCOPF_OK;
 }
 
-// Compile + upload the sweep schedule for tile width W: the chunk starts at
-// the largest of the candidate chunks (48 .. 1 buses; DCOPF_CHUNK to force one) and ring
-// lives whose kernel shared memory fits (config 4: F2 26, KVL 48, F1 16 buses).
-int compile_schedule(dcopf_dual_t h, int W) {
-  if (h->sched_W == W) return DCOPF_OK;
-  h->soft_sync = 1;  // measured faster for both forms at 19 consumer warps
-  if (const char *e = getenv("DCOPF_SYNC")) h->soft_sync = std::string(e) == "soft";
-  // search (chunk, ring life) from large to small until the kernel's shared
-  // memory fits: larger chunks mean fewer steps, longer ring lives fewer copies
+// Compile + upload the sweep schedule for tiles of W instances, V per lane,
+// swept by C parts: the chunk starts at the largest of the candidate chunks
+// (48 .. 1 buses) and ring lives whose kernel shared memory fits.  F2 and KVL
+// use the split-tile compiler (split_schedule.cpp; C = 1 is the unsplit
+// sweep), F1 the unsplit one (schedule.cpp; V = 2, C = 1).
+int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
+  if (h->sched_W == W && h->sched_V == V && h->sched_C == C) return DCOPF_OK;
   // program-block stages in flight: 2, except KVL, whose steps are shorter and
   // whose shared memory is better spent on larger chunks (measured on config 4:
   // KVL 1.17e7 at P = 2 / 36-row chunks, 1.21e7 at P = 1 / 48; F2 and F1 best at 2)
-  int P = (h->form == DCOPF_FORM_CYCLE) ? 1 : 2;
-  if (const char *e = getenv("DCOPF_PREFETCH")) P = std::max(1, atoi(e));
-  std::vector<std::pair<int, int>> cands;
-  if (const char *e = getenv("DCOPF_CHUNK")) {
-    const int life = getenv("DCOPF_RING_LIFE") ? atoi(getenv("DCOPF_RING_LIFE")) : 4;
-    cands.push_back({std::max(1, atoi(e)), life});
-  }
+  const int P = (h->form == DCOPF_FORM_CYCLE) ? 1 : 2;
+  const int nw = sweep_warps(V);
   const int chs[] = {48, 40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1},
             lifes[] = {6, 4, 2};
-  for (int ch : chs)
-    for (int life : lifes) cands.push_back({ch, life});
   Schedule sc;
   bool ok = false;
-  for (auto &cd : cands) {
-    sc = Schedule();
-    sc.ring_life = cd.second;
-    sc.pool_gap = h->soft_sync ? 3 : 1;  // soft sync: consumer warps drift by up to two steps
-    std::string err = build_schedule(h->ni, cd.first, P, W, kSweepWarps, &sc,
-                                     h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr);
-    if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
-    if (sc.total <= h->dev_smem) {
-      ok = true;
-      break;
+  for (int ch : chs) {
+    for (int life : lifes) {
+      sc = Schedule();
+      sc.ring_life = life;
+      sc.pool_gap = 3;  // soft step sync: consumer warps drift by up to two steps
+      const CycleBasis *cy = h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr;
+      const std::string err = (h->form == DCOPF_FORM_LIMIT_ROWS)
+                                  ? build_schedule(h->ni, ch, P, W, nw, &sc, cy)
+                                  : build_schedule_split(h->ni, ch, P, W, V, nw, C, {}, &sc, cy);
+      if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
+      if (sc.total <= h->dev_smem) {
+        ok = true;
+        break;
+      }
     }
+    if (ok) break;
   }
   if (!ok) return fail(h, DCOPF_EINVAL, "batched schedule does not fit shared memory; use the single path");
+  h->sched_W = h->sched_V = h->sched_C = 0;  // (invalid until every upload succeeded)
   h->sch = sc;
   int rc = upload(h, &h->d_prog, h->sch.prog);
   if (!rc) rc = upload(h, &h->d_prog_off, h->sch.prog_off);
   if (!rc) rc = upload(h, &h->d_prog_bytes, h->sch.prog_bytes);
   if (!rc) rc = upload(h, &h->d_tx_bytes, h->sch.tx_bytes);
   if (!rc) rc = upload(h, &h->d_ld_ptr, h->sch.ld_ptr);
+  if (!rc) rc = upload(h, &h->d_part_step0, h->sch.part_step0);
   if (!rc) {
     std::vector<int> ld(4 * h->sch.ld.size());
     for (size_t x = 0; x < h->sch.ld.size(); ++x) {
@@ -385,22 +392,60 @@ int compile_schedule(dcopf_dual_t h, int W) {
   }
   if (rc) return rc;
   std::vector<uint8_t>().swap(h->sch.prog);  // device copy only
-  const int b = h->sch.total;
-  if (!rc) rc = set_smem(h, k_sweep<kFormF2, false, kSweepWarps, false>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF2, true, kSweepWarps, false>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps, false>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps, false>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF2, false, kSweepWarps, true>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF2, true, kSweepWarps, true>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps, true>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF1, true, kSweepWarps, true>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormKVL, false, kSweepWarps, true>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormKVL, true, kSweepWarps, true>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormF2, false, kSweepWarps, true, true>, b);  // optimiser variants
-  if (!rc) rc = set_smem(h, k_sweep<kFormF1, false, kSweepWarps, true, true>, b);
-  if (!rc) rc = set_smem(h, k_sweep<kFormKVL, false, kSweepWarps, true, true>, b);
-  if (!rc) h->sched_W = W;
-  return rc;
+  h->sched_W = W;
+  h->sched_V = V;
+  h->sched_C = C;
+  return DCOPF_OK;
+}
+
+// Tile configuration of the batched path for B instances: V instances per
+// lane, W per tile, C parts (CTAs) per tile.  A warp instruction costs one
+// issue slot whatever its lane count, and an item's instructions are mostly
+// per warp (record decode, addressing, loop control) with the fp64 work per
+// instance: an item costs ~87 + 30 V issue slots (measured SASS mix, DESIGN.md
+// §5.1).  A CTA's sweep therefore costs ~(87 + 30 V) / C per item of the
+// network (plus the halo items of a split tile), whatever W is; the batch is
+// covered in ONE wave of tiles x C <= n_sm CTAs at the cheapest (V, C).  F1
+// is unsplit (V = 2, C = 1).  Batches too large for one wave use V = 4, C = 1
+// and W = 128 (several waves of whole-network tiles).
+void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out) {
+  const long nsm = h->n_sm;
+  if (h->form == DCOPF_FORM_LIMIT_ROWS) {
+    *V_out = 2;
+    *C_out = 1;
+    *W_out = (int)std::min<int64_t>(64, 2 * ((B + 2LL * nsm - 1) / (2LL * nsm)));
+    return;
+  }
+  double best = 1e300;
+  int bV = 4, bW = 128, bC = 1;
+  for (int V : {2, 4})
+    for (int C = 1; C <= 16; ++C) {
+      if ((h->opt_lane && V != h->opt_lane) || (h->opt_parts && C != h->opt_parts)) continue;
+      if (!h->opt_parts && C > 1 && h->n_bus < 64 * C) break;  // parts of >= 64 buses (halo stays small)
+      if (C > h->n_bus) break;
+      const long maxt = nsm / C;
+      if (maxt < 1) break;
+      long W = (B + maxt - 1) / maxt;
+      W = std::max<long>(V, (W + V - 1) / V * V);
+      if (W > 32L * V) continue;
+      const double halo = 1.0 + 0.02 * (C - 1);  // halo items of a split tile (measured ~1-2% per cut)
+      const double cost = (87.0 + 30.0 * V) / C * halo;
+      if (cost < best - 1e-9) {
+        best = cost;
+        bV = V;
+        bW = (int)W;
+        bC = C;
+      }
+    }
+  if (best == 1e300) {  // more than one wave (or a forced configuration that cannot cover B in one)
+    bV = h->opt_lane ? h->opt_lane : 4;
+    bC = h->opt_parts ? h->opt_parts : 1;
+    const long maxt = std::max<long>(1, nsm / bC);
+    bW = (int)std::min<long>(32L * bV, std::max<long>(bV, ((B + maxt - 1) / maxt + bV - 1) / bV * bV));
+  }
+  *V_out = bV;
+  *W_out = bW;
+  *C_out = bC;
 }
 
 // state-layout permutations of the current path (storage position <-> original id)
@@ -413,20 +458,6 @@ Perms perms(dcopf_dual_t h) {
   if (h->form == DCOPF_FORM_CYCLE)
     return Perms{h->d_bus_perm, h->d_bus_inv, h->d_bus_perm, h->d_cyc_perm, h->d_cyc_inv};
   return Perms{h->d_bus_perm, h->d_bus_inv, h->d_bus_perm, h->d_br_perm, h->d_br_inv};
-}
-
-int configure_single(dcopf_dual_t h) {
-  int rc = DCOPF_OK;
-  const int b = h->smem_single;
-  if (!rc) rc = set_smem(h, k_single<kFormF2, true, kModeStep>, b);
-  if (!rc) rc = set_smem(h, k_single<kFormF2, true, kModeEval>, b);
-  if (!rc) rc = set_smem(h, k_single<kFormF2, false, kModeStep>, b);
-  if (!rc) rc = set_smem(h, k_single<kFormF2, false, kModeEval>, b);
-  if (!rc) rc = set_smem(h, k_single<kFormF1, true, kModeStep>, b);
-  if (!rc) rc = set_smem(h, k_single<kFormF1, true, kModeEval>, b);
-  if (!rc) rc = set_smem(h, k_single<kFormF1, false, kModeStep>, b);
-  if (!rc) rc = set_smem(h, k_single<kFormF1, false, kModeEval>, b);
-  return rc;
 }
 
 int opt_nstate(dcopf_dual_t h) {
@@ -462,9 +493,11 @@ int configure_cluster(dcopf_dual_t h) {
   if (h->cplan_C) return DCOPF_OK;
   int C = 1;
   while (C < 16 && (long)h->n_bus > 640L * C) C *= 2;
-  if (const char *e = getenv("DCOPF_CLUSTER")) C = std::max(1, std::min(16, atoi(e)));
+  if (h->opt_parts) C = h->opt_parts;  // dcopf_options.tile_parts: the cluster size
+  if (h->force_cluster_C) C = h->force_cluster_C;
   std::string err;
   for (; C <= 16; C *= 2) {
+    if (h->force_cluster_C && C != h->force_cluster_C) break;
     ClusterPlan pl;
     err = build_cluster_plan(h->ni, C, h->dev_smem, opt_nstate(h), &pl,
                              h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr);
@@ -565,9 +598,13 @@ int launch_cluster(dcopf_dual_t h, const ClusterArgs &a, cudaStream_t s) {
   cfg.stream = s;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (h->form == DCOPF_FORM_FLOW_BOX) CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormF2, MODE>, a));
-  else if (h->form == DCOPF_FORM_CYCLE) CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormKVL, MODE>, a));
-  else CK(h, cudaLaunchKernelEx(&cfg, k_cluster<kFormF1, MODE>, a));
+  // (the dynamic shared-memory limit is per function and shared by every
+  // handle: set it for this handle's plan right before its launch)
+  auto fn = (h->form == DCOPF_FORM_FLOW_BOX) ? k_cluster<kFormF2, MODE>
+            : (h->form == DCOPF_FORM_CYCLE)  ? k_cluster<kFormKVL, MODE>
+                                             : k_cluster<kFormF1, MODE>;
+  CK(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cplan.smem));
+  CK(h, cudaLaunchKernelEx(&cfg, fn, a));
   CK(h, cudaGetLastError());
   return DCOPF_OK;
 }
@@ -602,7 +639,6 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.tx_bytes = h->d_tx_bytes;
   a.ld_ptr = h->d_ld_ptr;
   a.ld = reinterpret_cast<const int4 *>(h->d_ld);
-  a.nsteps = sc.nsteps;
   a.S = sc.S;
   a.row_bytes = sc.row_bytes;
   a.br_row_bytes = sc.br_row_bytes;
@@ -618,7 +654,12 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.off_dp = sc.off_dp;
   a.off_th = sc.off_th;
   a.off_fc = sc.off_fc;
-  a.soft = h->soft_sync;
+  a.parts = h->tile_C;
+  a.part_step0 = h->d_part_step0;
+  a.tile_sync = h->d_tile_sync;
+  a.part_val = h->d_part_val;
+  a.tiles = (int)(h->B_pad / h->T);
+  a.soft = 1;
   a.tol = h->tol;
   a.opt = h->opt.variant;
   a.rho = h->opt.momentum;
@@ -631,32 +672,49 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.s2_lam = h->os[1];
   a.s1_br = h->os[2];
   a.s2_br = h->os[3];
-  if (const char *e = getenv("DCOPF_DEBUG_MODE")) a.debug_mode = atoi(e);  // measurement only
   return a;
+}
+
+// one k_sweep launch: the kernel's dynamic shared-memory limit is set for
+// THIS handle's schedule right before the launch (the attribute is per
+// function and shared by every handle of the process); a split tile (C > 1)
+// is a cooperative launch, so the tile's CTAs are co-resident for the
+// once-per-sweep meeting of its parts, whose counters are zeroed first
+template <int FORM, bool EVAL, bool OPT, int V>
+int launch_sweep_t(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
+  constexpr int NW = V == 4 ? kSweepWarps4 : kSweepWarps2;
+  auto fn = k_sweep<FORM, EVAL, NW, true, OPT, V>;
+  const int sm = h->sch.total;
+  CK(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  const int C = h->tile_C;
+  if (C > 1) CK(h, cudaMemsetAsync(h->d_tile_sync, 0, (size_t)a.tiles * sizeof(unsigned), s));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.gridDim = dim3((unsigned)(a.tiles * C));
+  cfg.blockDim = dim3((NW + 1) * 32);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = (C > 1) ? 1 : 0;
+  CK(h, cudaLaunchKernelEx(&cfg, fn, a));
+  return DCOPF_OK;
 }
 
 template <bool EVAL>
 int launch_sweep(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
-  const unsigned grid = (unsigned)(h->B_pad / h->T), threads = (kSweepWarps + 1) * 32;
-  const size_t sm = h->sch.total;
-  if (!EVAL && h->opt.variant != DCOPF_OPT_PLAIN) {  // optimiser variants (soft step sync)
-    if (h->form == DCOPF_FORM_FLOW_BOX) k_sweep<kFormF2, false, kSweepWarps, true, true><<<grid, threads, sm, s>>>(a);
-    else if (h->form == DCOPF_FORM_CYCLE) k_sweep<kFormKVL, false, kSweepWarps, true, true><<<grid, threads, sm, s>>>(a);
-    else k_sweep<kFormF1, false, kSweepWarps, true, true><<<grid, threads, sm, s>>>(a);
-    CK(h, cudaGetLastError());
-    return DCOPF_OK;
-  }
+  const bool opt = !EVAL && h->opt.variant != DCOPF_OPT_PLAIN;  // optimiser variants
+  const bool v4 = h->tile_V == 4;
   if (h->form == DCOPF_FORM_FLOW_BOX) {
-    if (h->soft_sync) k_sweep<kFormF2, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);
-    else k_sweep<kFormF2, EVAL, kSweepWarps, false><<<grid, threads, sm, s>>>(a);
-  } else if (h->form == DCOPF_FORM_CYCLE) {
-    k_sweep<kFormKVL, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);  // (soft sync only)
-  } else {
-    if (h->soft_sync) k_sweep<kFormF1, EVAL, kSweepWarps, true><<<grid, threads, sm, s>>>(a);
-    else k_sweep<kFormF1, EVAL, kSweepWarps, false><<<grid, threads, sm, s>>>(a);
+    if (v4) return opt ? launch_sweep_t<kFormF2, false, true, 4>(h, a, s) : launch_sweep_t<kFormF2, EVAL, false, 4>(h, a, s);
+    return opt ? launch_sweep_t<kFormF2, false, true, 2>(h, a, s) : launch_sweep_t<kFormF2, EVAL, false, 2>(h, a, s);
   }
-  CK(h, cudaGetLastError());
-  return DCOPF_OK;
+  if (h->form == DCOPF_FORM_CYCLE) {
+    if (v4) return opt ? launch_sweep_t<kFormKVL, false, true, 4>(h, a, s) : launch_sweep_t<kFormKVL, EVAL, false, 4>(h, a, s);
+    return opt ? launch_sweep_t<kFormKVL, false, true, 2>(h, a, s) : launch_sweep_t<kFormKVL, EVAL, false, 2>(h, a, s);
+  }
+  return opt ? launch_sweep_t<kFormF1, false, true, 2>(h, a, s) : launch_sweep_t<kFormF1, EVAL, false, 2>(h, a, s);
 }
 
 SingleArgs single_args(dcopf_dual_t h) {
@@ -680,6 +738,7 @@ SingleArgs single_args(dcopf_dual_t h) {
 
 template <int FORM, bool SM, int MODE>
 int launch_single_t(dcopf_dual_t h, const SingleArgs &a, cudaStream_t s) {
+  CK(h, cudaFuncSetAttribute(k_single<FORM, SM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_single));
   k_single<FORM, SM, MODE><<<(unsigned)h->B, 1024, h->smem_single, s>>>(dev_net(h), a);
   CK(h, cudaGetLastError());
   return DCOPF_OK;
@@ -717,6 +776,9 @@ void dcopf_dual_destroy(dcopf_dual_t h) {
   for (double *p : dp) cudaFree(p);
   cudaFree(h->d_prog);
   cudaFree(h->d_prog_off);
+  cudaFree(h->d_part_step0);
+  cudaFree(h->d_tile_sync);
+  cudaFree(h->d_part_val);
   cudaFree(h->d_cblob);
   cudaFreeHost(h->alpha_pin);
   if (h->alpha_ev) cudaEventDestroy(h->alpha_ev);
@@ -737,6 +799,11 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   if (o.precision != 64 && o.precision != 0)
     return fail(nullptr, DCOPF_EINVAL, "precision %d not supported (fp64 only)", o.precision);
   if (o.path < 0 || o.path > 4) return fail(nullptr, DCOPF_EINVAL, "unknown path %d", o.path);
+  if (o.tile_parts < 0 || o.tile_parts > 16) return fail(nullptr, DCOPF_EINVAL, "tile_parts must be in [0, 16]");
+  if (o.lane_instances != 0 && o.lane_instances != 2 && o.lane_instances != 4)
+    return fail(nullptr, DCOPF_EINVAL, "lane_instances must be 0, 2 or 4");
+  if (o.tile_parts & (o.tile_parts - 1) && o.path == DCOPF_PATH_CLUSTER)
+    return fail(nullptr, DCOPF_EINVAL, "cluster path: tile_parts (CTAs per instance) must be a power of two");
   if ((o.form == DCOPF_FORM_PTDF) != (o.path == DCOPF_PATH_DENSE) && o.path != DCOPF_PATH_AUTO)
     return fail(nullptr, DCOPF_EINVAL, "the PTDF form runs on DCOPF_PATH_DENSE (and only it)");
   const int nb = net->n_bus, nl = net->n_branch, ng = net->n_gen;
@@ -839,12 +906,15 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   h->form = o.form;
   h->path_opt = o.path;
   h->single_max = o.single_max_batch > 0 ? o.single_max_batch : 128;
+  h->opt_parts = o.tile_parts;
+  h->opt_lane = o.lane_instances;
   h->n_bus = nb;
   h->n_br = nl;
   h->n_gen = ng;
   if (net->gen_a)
     for (int g = 0; g < ng; ++g) h->quadratic |= net->gen_a[g] > 0.0;
   if (net->br_switchable) h->switchable.assign(net->br_switchable, net->br_switchable + nl);
+  h->implied_box = net->theta_max == nullptr;
 
   // ---- internal numbering: bus order, branch order, CSR, generator map ----
   const char *ord = getenv("DCOPF_ORDER");
@@ -944,34 +1014,9 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   int path = h->path_opt;
   if (h->form == DCOPF_FORM_CYCLE && path == DCOPF_PATH_SINGLE)
     return fail(h, DCOPF_EINVAL, "the KVL (cycle) form runs on the cluster and batched paths");
-  if (path == DCOPF_PATH_AUTO) {
-    path = (B <= h->single_max) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
-    if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) {
-      if (h->form == DCOPF_FORM_CYCLE) return DCOPF_EINVAL;  // (message set by configure_cluster)
-      path = DCOPF_PATH_SINGLE;
-    }
-  }
-  int W = 1;
-  if (path == DCOPF_PATH_BATCHED) {
-    // tile width: even, <= 64, so that #tiles ~ #SMs (one CTA per SM)
-    W = (int)std::min<int64_t>(64, 2 * ((B + 2LL * h->n_sm - 1) / (2LL * h->n_sm)));
-    if (const char *ev = getenv("DCOPF_TILE_W")) W = std::max(2, std::min(64, atoi(ev) & ~1));
-    int rc = compile_schedule(h, W);
-    if (rc) return rc;
-  } else if (path == DCOPF_PATH_CLUSTER) {
-    int rc = configure_cluster(h);
-    if (rc) return rc;
-  } else {
-    const size_t ss_state = single_smem(h->n_bus, h->n_br, h->form, true);
-    const size_t ss_nostate = single_smem(h->n_bus, h->n_br, h->form, false);
-    if (ss_nostate > (size_t)h->dev_smem)
-      return fail(h, DCOPF_EINVAL, "single path needs %zu B shared memory (> %d)", ss_nostate, h->dev_smem);
-    h->single_smem = ss_state <= (size_t)h->dev_smem;
-    h->smem_single = (int)(h->single_smem ? ss_state : ss_nostate);
-    int rc = configure_single(h);
-    if (rc) return rc;
-  }
-  // outages: validate on the host, convert to internal ids
+  // outages: validate on the host and convert to internal ids BEFORE anything
+  // of the loaded batch (schedule, path, state) is touched, so a rejected call
+  // leaves the handle as it was
   std::vector<int> outs_h;
   if (max_out > 0) {
     std::vector<int32_t> raw((size_t)B * max_out);
@@ -982,18 +1027,56 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
       if (l < -1 || l >= h->n_br) return fail(h, DCOPF_EINVAL, "outage id %d out of range", l);
       if (l >= 0 && !h->switchable.empty() && !h->switchable[l])
         return fail(h, DCOPF_EINVAL, "branch %d is not switchable", l);
+      if (l >= 0 && h->implied_box && h->switchable.empty() && h->form != DCOPF_FORM_CYCLE)
+        return fail(h, DCOPF_EINVAL,
+                    "outage of branch %d with an implied angle box over ALL branches (theta_max and "
+                    "br_switchable NULL): the box would not be valid for that instance -- declare the "
+                    "switchable branches (br_switchable) or pass theta_max", l);
       if (l >= 0 && h->form == DCOPF_FORM_CYCLE && h->cyc_orig.is_tree[l])
         return fail(h, DCOPF_EINVAL, "branch %d is in the cycle-basis tree (KVL form): declare the switchable "
                                      "branches (br_switchable) so the tree avoids them", l);
       outs_h[x] = l < 0 ? -1 : h->br_inv[l];
     }
   }
+  if (path == DCOPF_PATH_AUTO) {
+    path = (B <= h->single_max) ? DCOPF_PATH_CLUSTER : DCOPF_PATH_BATCHED;
+    if (path == DCOPF_PATH_CLUSTER && configure_cluster(h) != DCOPF_OK) {
+      if (h->form == DCOPF_FORM_CYCLE) return DCOPF_EINVAL;  // (message set by configure_cluster)
+      path = DCOPF_PATH_SINGLE;
+    }
+  }
+  int W = 1, tV = 2, tC = 1;
+  if (path == DCOPF_PATH_BATCHED) {
+    if (h->form == DCOPF_FORM_LIMIT_ROWS && (h->opt_parts > 1 || h->opt_lane == 4))
+      return fail(h, DCOPF_EINVAL, "form F1 runs unsplit tiles of 2 instances per lane on the batched path");
+    choose_tiles(h, B, &tV, &W, &tC);
+    // a failed compile leaves sched_* invalid: the old batch (if any) is
+    // dropped below before anything can use the new schedule with it
+    int rc = compile_schedule(h, W, tV, tC);
+    if (rc) {
+      free_batch(h);
+      return rc;
+    }
+  } else if (path == DCOPF_PATH_CLUSTER) {
+    int rc = configure_cluster(h);
+    if (rc) return rc;
+  } else {
+    const size_t ss_state = single_smem(h->n_bus, h->n_br, h->form, true);
+    const size_t ss_nostate = single_smem(h->n_bus, h->n_br, h->form, false);
+    if (ss_nostate > (size_t)h->dev_smem)
+      return fail(h, DCOPF_EINVAL, "single path needs %zu B shared memory (> %d)", ss_nostate, h->dev_smem);
+    h->single_smem = ss_state <= (size_t)h->dev_smem;
+    h->smem_single = (int)(h->single_smem ? ss_state : ss_nostate);
+  }
   const int64_t B_pad = (B + W - 1) / W * W;
-  const bool reuse = h->lam[0] && h->B_pad == B_pad && h->T == W && h->path == path && h->max_out == max_out;
+  const bool reuse = h->lam[0] && h->B_pad == B_pad && h->T == W && h->path == path && h->max_out == max_out &&
+                     h->tile_V == tV && h->tile_C == tC;
   if (!reuse) free_batch(h);
   h->path = path;
   h->B = B;
   h->T = W;
+  h->tile_V = tV;
+  h->tile_C = tC;
   h->B_pad = B_pad;
   h->max_out = max_out;
   h->cur = 0;
@@ -1012,6 +1095,23 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
     CK(h, cudaMalloc(&h->outs, std::max<size_t>((size_t)B_pad * max_out, 1) * 4));
     CK(h, cudaMalloc(&h->target, B_pad * 8));
     CK(h, cudaMalloc(&h->hit, B_pad * 8));
+  }
+  if (path == DCOPF_PATH_BATCHED && tC > 1) {  // split tiles: the parts' meeting place
+    const size_t tiles = (size_t)(B_pad / W), nsync = tiles, nval = 2 * tiles * tC * W;
+    if (h->tile_sync_cap < nsync) {
+      cudaFree(h->d_tile_sync);
+      h->d_tile_sync = nullptr;
+      h->tile_sync_cap = 0;
+      CK(h, cudaMalloc(&h->d_tile_sync, nsync * sizeof(unsigned)));
+      h->tile_sync_cap = nsync;
+    }
+    if (h->part_val_cap < nval) {
+      cudaFree(h->d_part_val);
+      h->d_part_val = nullptr;
+      h->part_val_cap = 0;
+      CK(h, cudaMalloc(&h->d_part_val, nval * sizeof(double)));
+      h->part_val_cap = nval;
+    }
   }
   h->has_target = false;
   h->k_base = 0;
@@ -1240,6 +1340,11 @@ int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt) {
   auto unit = [](double x) { return std::isfinite(x) && x >= 0.0 && x < 1.0; };
   if (!unit(o.momentum) || !unit(o.beta1) || !unit(o.beta2) || !(o.epsilon >= 0.0) || !std::isfinite(o.epsilon))
     return fail(h, DCOPF_EINVAL, "momentum, beta1, beta2 must be in [0, 1) and epsilon finite >= 0");
+  // AdaGrad / Adam divide by sqrt(state) + eps, and the state is exactly 0 at
+  // the start (and stays 0 on a coordinate whose gradient is 0, e.g. an
+  // outaged branch): eps = 0 would give 0/0
+  if ((o.variant == DCOPF_OPT_ADAGRAD || o.variant == DCOPF_OPT_ADAM) && !(o.epsilon > 0.0))
+    return fail(h, DCOPF_EINVAL, "AdaGrad and Adam need epsilon > 0 (SPEC.md:359 suggests 1e-8)");
   if (h->B > 0 && h->path == DCOPF_PATH_SINGLE && o.variant != DCOPF_OPT_PLAIN)
     return fail(h, DCOPF_EINVAL, "optimiser variants run on the cluster and batched paths");
   CK(h, cudaSetDevice(h->device));
@@ -1250,12 +1355,24 @@ int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt) {
     return prc ? fail(h, prc, "%s", perr.c_str()) : DCOPF_OK;
   }
   const int ns_old = opt_nstate(h);
+  const dcopf_optimizer o_old = h->opt;
   h->opt = o;
   if (opt_nstate(h) != ns_old) {  // the shared-memory plan holds the state arrays: rebuild it
+    const int C_old = h->cplan_C;
+    const ClusterPlan plan_old = h->cplan;
     h->cplan_C = 0;
     if (h->B > 0 && h->path == DCOPF_PATH_CLUSTER) {
+      // keep the loaded batch's cluster size: the partition (and the KVL
+      // storage order of kappa, cluster.cpp) depends on it
+      h->force_cluster_C = C_old;
       int rc = configure_cluster(h);
-      if (rc) return rc;
+      h->force_cluster_C = 0;
+      if (rc) {  // the variant is not taken: the handle stays as it was
+        h->opt = o_old;
+        h->cplan = plan_old;
+        h->cplan_C = C_old;
+        return rc;
+      }
     }
   }
   int rc = reset_opt_state(h, nullptr);
@@ -1327,8 +1444,17 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
   info->bandwidth = h->bandwidth;
   if (h->path == DCOPF_PATH_BATCHED) {
     info->smem_bytes = h->sch.total;
-    info->threads_per_block = (kSweepWarps + 1) * 32;
-    info->grid = (int)(h->B_pad / h->T);
+    info->threads_per_block = (sweep_warps(h->tile_V) + 1) * 32;
+    info->grid = (int)(h->B_pad / h->T) * h->tile_C;
+    info->tile_parts = h->tile_C;
+    info->lane_instances = h->tile_V;
+    info->halo_items = h->sch.halo_a + h->sch.halo_b;
+    {
+      int mx = 0;
+      for (int p = 0; p + 1 < (int)h->sch.part_step0.size(); ++p)
+        mx = std::max(mx, h->sch.part_step0[p + 1] - h->sch.part_step0[p]);
+      info->steps_per_sweep = mx;
+    }
     info->launches_per_iter = 0;
     info->chunk = h->sch.CH;
     info->ring_bus = h->sch.n_lam_slots;

@@ -1,5 +1,6 @@
 // schedule.cpp -- see schedule.h.
 #include "schedule.h"
+#include "schedule_detail.h"
 
 #include <algorithm>
 #include <cstdio>
@@ -186,11 +187,7 @@ std::string internalize(int nb, int nl, int ng, int ref, const int *fr, const in
   return "";
 }
 
-namespace {
-
-struct Interval {
-  int lo, hi, id;
-};
+namespace detail {
 
 // greedy interval colouring; returns #colours, slot[id]
 int colour(std::vector<Interval> iv, std::vector<int> &slot) {
@@ -299,17 +296,19 @@ void layout_smem(Schedule &S, int nl, int nw) {
   int off = 0;
   S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers
   off = al(off + 16 * S.S + 64);
-  S.off_frz = off;  // frozen flags [64] int, then running best [64] and previous g [64] double
-  off = al(off + 4 * 64 + 2 * 8 * 64);
+  const int TS = 32 * S.V;  // per-tile instance slots (a lane's instances are below 32 V)
+  S.off_frz = off;  // frozen flags [TS] int, then running best and previous g [TS] double
+  off = al(off + 4 * TS + 2 * 8 * TS);
   S.off_obm = off;  // per-tile outage bitmap over branches
   off = al(off + 4 * ((nl + 31) / 32 + 1));
   S.off_outs = off;  // per-instance outage lists of the tile
-  off = al(off + 4 * 64 * 8);
+  off = al(off + 4 * TS * 8);
   S.off_prog = off;
   off = al(off + S.S * al(S.max_prog_bytes));
-  // state / minimiser pools; lanes past the tile width read up to 512 - RB
-  // bytes past a pool's last slot
-  int pad = 512 - RB;
+  // state / minimiser pools; lanes past the tile width read past a pool's
+  // last slot: lane l reads 16 bytes at 16 l (and, 4 instances per lane, at
+  // 4 W + 16 l) of a row of 8 W bytes
+  int pad = std::max(0, 512 + (S.V == 4 ? 4 * S.W : 0) - RB);
   if (const char *e = getenv("DCOPF_POOL_PAD")) pad = atoi(e);  // measurement only
   S.off_brp = off;
   off = al(off + S.n_br_slots * BR + pad);
@@ -321,20 +320,20 @@ void layout_smem(Schedule &S, int nl, int nw) {
   off = al(off + S.n_th_slots * S.code_row_bytes);
   S.off_fc = off;  // f*_l code rows (F2)
   off = al(off + S.n_f_slots * S.code_row_bytes);
-  // the per-warp dual-value partials [nw][64] are needed only at the end of a
-  // sweep, when every pool is dead: they alias the pools
+  // the per-warp dual-value partials [nw][TS] are needed only at the end of
+  // a sweep, when every pool is dead: they alias the pools
   S.off_red = S.off_brp;
-  off = std::max(off, al(S.off_brp + 8 * 64 * nw));
-  if (getenv("DCOPF_RED_SEPARATE")) {  // measurement only
-    S.off_red = off;
-    off = al(off + 8 * 64 * nw);
-  }
+  off = std::max(off, al(S.off_brp + 8 * TS * nw));
   S.total = off;
 }
 
+}  // namespace detail
+
+using namespace detail;
+
+namespace {
 std::string build_schedule_kvl(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out,
                                const CycleBasis &Y);
-
 }  // namespace
 
 size_t Schedule::smem_bytes(int) const { return (size_t)total; }
@@ -357,6 +356,9 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
   S.nsteps = S.nch + 2;
   S.row_bytes = 8 * W;
   S.br_row_bytes = f1 ? 16 * W : 8 * W;
+  S.V = 2;
+  S.C = 1;
+  S.part_bus0 = {0, nb};
   const int nch = S.nch, nst = S.nsteps, RB = S.row_bytes, BR = S.br_row_bytes;
   auto chunk = [&](int bus) { return bus / CH; };
   std::vector<int> hi(nl), lo(nl);
@@ -477,6 +479,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
         RecA r{};
         r.th = th_slot[i] * S.code_row_bytes;
         r.bus = i;
+        r.flags = (i == net.ref) ? kAFlagRef : 0;
         r.theta = net.theta[i];
         r.e0 = f1 ? (int)IA1.size() : (int)IA2.size();
         for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
@@ -650,6 +653,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     S.tx_bytes[st] = S.prog_bytes[st] + row_bytes[st];
   }
 
+  S.part_step0 = {0, nst};
   layout_smem(S, nl, nw);
   return "";
 }
@@ -677,6 +681,9 @@ std::string build_schedule_kvl(const NetInternal &net, int CH, int P, int W, int
   S.nsteps = S.nch + 1;
   S.row_bytes = 8 * W;
   S.br_row_bytes = 8 * W;  // kappa rows
+  S.V = 2;
+  S.C = 1;
+  S.part_bus0 = {0, nb};
   const int nch = S.nch, nst = S.nsteps, RB = S.row_bytes, CRB = S.code_row_bytes;
   auto chunk = [&](int bus) { return bus / CH; };
   std::vector<int> hi(nl);
@@ -761,6 +768,7 @@ std::string build_schedule_kvl(const NetInternal &net, int CH, int P, int W, int
         r.lt = lam_slot[net.bt[l]] * RB;
         r.fs = f_slot[l] * CRB;
         r.obr = (!has_sw || net.sw[l]) ? l : -1;
+        r.br = l;
         r.x = (net.b[l] > 0.0) ? 1.0 / net.b[l] : 0.0;
         r.F = (net.b[l] > 0.0) ? net.F[l] : 0.0;  // b = 0: an open circuit
         r.e0 = (int)BKe.size();
@@ -875,6 +883,7 @@ std::string build_schedule_kvl(const NetInternal &net, int CH, int P, int W, int
     S.max_prog_bytes = std::max(S.max_prog_bytes, (int)blk.size());
     S.tx_bytes[st] = S.prog_bytes[st] + row_bytes[st];
   }
+  S.part_step0 = {0, nst};
   layout_smem(S, nl, nw);
   return "";
 }

@@ -40,11 +40,16 @@ constexpr int kProgHeaderBytes = 80;
 // (+1 / -1 / 0: the upper bound, the lower bound, the tie), a 64-byte "code
 // row" per entity; readers multiply by Theta or F, which reproduces the value
 // exactly (c * x is exact for c in {-1, 0, 1}).
-struct alignas(16) RecA { int e0, e1, th, bus; double theta, pad2; };   // bus of phase A
+struct alignas(16) RecA { int e0, e1, th, bus; double theta; int flags, pad; };  // bus of phase A
+// RecA.flags: kAFlagRef = the reference bus (theta* = 0), kAFlagHalo = a halo bus of a split tile
+// (theta* code only: the bus is owned by another part of the tile, which counts its value)
+enum { kAFlagRef = 1, kAFlagHalo = 2 };
 struct alignas(16) RecIA2 { int row, br; double sb; };                   // F2: sb = to ? b : -b
 struct alignas(16) RecIA1 { int row, br, ls, lt; double sb, pad; };      // F1: sb = to ? -b : b (br -1: never out)
 struct alignas(16) RecB { int row, ls, lt, ts, tt, fs, wpos, obr; double b, F, ths, tht; };  // branch of phase B
                           // (wpos: nu' row; obr: id if switchable, else -1; ths / tht: Theta of the endpoints)
+                          // wpos < 0: a "lite" halo branch of a split tile (branch -1 - wpos, owned by the
+                          // next part): f* code only -- no theta* codes, no value, no write
 struct alignas(16) RecC { int wpos, ls, ds, g0, g1, e0, e1, pad; };     // bus of phase C (wpos: lambda' row)
 struct alignas(16) RecG { double c, lo, hi, a; };                         // generator
 struct alignas(16) RecIC2 { int f, br; double sF; };                     // F2: sF = to ? F : -F
@@ -54,7 +59,8 @@ struct alignas(16) RecIC1 { int ts, tt, br, pad; double sb, ths, tht, pad2; };  
 enum { LD_LAM = 0, LD_D = 1, LD_BR = 2 };
 
 // KVL form (batched path): phase B per branch with its cycle terms, phase D per cycle
-struct alignas(16) RecBK { int ls, lt, e0, e1, fs, obr, pad0, pad1; double x, F; };  // x = 1/b (0 if b = 0)
+struct alignas(16) RecBK { int ls, lt, e0, e1, fs, obr, halo, br; double x, F; };  // x = 1/b (0 if b = 0)
+                          // halo = 1: a branch of another part (f* code only, no value); br: internal id
 struct alignas(8) RecBKe { int ks, sgn; };                                        // kappa slot of a cycle term
 struct alignas(16) RecD { int ks, wpos, e0, e1, dbr, pad0, pad1, pad2; };          // cycle: kappa slot, kappa' row,
                                                                                   // dbr: defining branch if switchable
@@ -84,8 +90,15 @@ struct int4_t {
   int a, b, c, d;  // load entry: kind, first storage position, row count, first slot
 };
 
+constexpr int kMaxTileW = 128;  // instances per tile: 32 lanes x up to 4 instances
+
 struct Schedule {
   int CH = 0, P = 0, S = 0, W = 0, nch = 0, nsteps = 0;
+  int V = 2;                                // instances per lane (2: W <= 64; 4: W <= 128)
+  int C = 1;                                // parts (CTAs) per tile: each sweeps its own bus range
+  std::vector<int> part_step0;              // [C+1] first global step of each part
+  std::vector<int> part_bus0;               // [C+1] internal bus range owned by each part
+  int halo_a = 0, halo_b = 0;               // halo items over all parts (recomputed codes)
   int ring_life = 6;                        // rows live <= this many steps go to the rings
   int pool_gap = 1;                         // theta* / f* pool slots are reused only pool_gap steps after
                                             // their last read (2: consumer warps may drift by one step)
@@ -93,7 +106,7 @@ struct Schedule {
   // storage order of the state rows in HBM (positions) and its inverse, per kind
   std::vector<int> pos_lam, perm_lam, pos_d, perm_d, pos_br, perm_br;
   int row_bytes = 0;                        // lambda / d / nu row: 8 W
-  int code_row_bytes = 64;                  // theta* / f* code row: one byte per instance
+  int code_row_bytes = 64;                  // theta* / f* code row: one byte per instance (32 V)
   int n_br_slots = 0, n_lam_slots = 0, n_d_slots = 0, n_th_slots = 0, n_f_slots = 0;
   int br_row_bytes = 0;                     // 8 W (nu) or 16 W (mu+, mu-)
   int max_prog_bytes = 0;
@@ -136,5 +149,17 @@ std::vector<int> dfs_tree_order(int n, const std::vector<std::vector<int>> &adj,
 // cyc: the cycle basis in INTERNAL branch ids (KVL form, net.form == 2), else null.
 std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out,
                            const CycleBasis *cyc = nullptr);
+
+// Split-tile schedule (forms F2 and KVL): each tile of W instances (V per
+// lane) is swept by C CTAs ("parts"), part p owning the internal buses
+// [cuts[p], cuts[p+1]) and the branches (KVL: also the cycles) whose larger
+// endpoint it owns.  A part recomputes, from the y_k rows in HBM, the few
+// minimiser codes it needs from the neighbouring parts (halo theta* / f*
+// codes: the same arithmetic on the same inputs, so bitwise the owner's), and
+// writes only the multipliers it owns.  The parts' steps are concatenated
+// (part_step0); every part has the same shared-memory layout.  C = 1 is the
+// unsplit sweep.  cuts empty = balanced by estimated cost.
+std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, int V, int nw, int C,
+                                 std::vector<int> cuts, Schedule *out, const CycleBasis *cyc = nullptr);
 
 }  // namespace dcopf

@@ -1,18 +1,23 @@
 // sweep_kernel.cuh -- the batched path: one persistent, warp-specialised,
 // TMA-fed sweep kernel per dcopf_dual_iterate() call (sm_100a).
 //
-// Layout: instances are grouped in tiles of W (even, <= 64) -- the tile width
-// is chosen per batch so the number of tiles is about the SM count -- and
+// Layout: instances are grouped in tiles of W (a multiple of V <= 32 V) and
 // every per-instance array is tile-major [tile][entity][W] (F1 mu:
 // [tile][branch][2][W]).  A row (one entity of one tile) is 8 W contiguous
-// bytes.  Lane l of a warp owns instances 2l and 2l+1 of its tile, so every
-// shared-memory / global access of a row is one 16-byte vector per lane and
-// every topology record is a warp-uniform broadcast shared by 2*32 instances.
+// bytes.  Lane l of a warp owns V instances of its tile: 2l and 2l+1 (V = 2),
+// plus W/2 + 2l and W/2 + 2l + 1 (V = 4), so every shared-memory / global
+// access of a row is one (V = 2) or two (V = 4) 16-byte vectors per lane, and
+// every topology record is a warp-uniform broadcast shared by 32 V instances.
+// The issue cost of an item (record decode, addressing, loop control) is per
+// warp, so V = 4 halves it per instance; only the fp64 arithmetic scales
+// with V.
 //
-// One CTA = one tile, for all K iterations (instances never interact: no grid
-// synchronisation, one launch per call).  Each iteration is a sweep over a
-// host-compiled schedule (schedule.h) of nch chunks in nch+2 skewed steps;
-// step s runs, between two barriers,
+// A tile is swept by C CTAs ("parts", split_schedule.cpp), part p owning a
+// contiguous range of the network (C = 1: the whole network).  Instances
+// never interact: there is no grid synchronisation, only the tile's parts
+// meet once per sweep (below).  Each iteration is a sweep over the part's
+// host-compiled steps (schedule.h); for F2 / F1 step s runs, between
+// barriers,
 //     A(s)    buses of chunk s: w_i over the incidence -> theta* codes
 //     B(s-1)  branches whose larger endpoint is in chunk s-1: q_l, f* codes,
 //             phi_l, Kirchhoff (F2) / limit (F1) residual, nu' / mu' -> HBM
@@ -24,8 +29,19 @@
 // cp.async.bulk (TMA 1-D bulk copies) P steps ahead, synchronised by
 // full/empty mbarriers.  Every HBM byte of the iteration is read once and
 // written once: the traffic is the algorithmic 8 (3 n_b + 2 n_l) B per
-// instance-iteration (F2).  Between sweeps the pipeline drains (y_{k+1} rows
-// are read by TMA in sweep k+1, so writers fence generic -> async proxy).
+// instance-iteration (F2), plus the few halo rows of a split tile.  Between
+// sweeps the pipeline drains (y_{k+1} rows are read by TMA in sweep k+1, so
+// writers fence generic -> async proxy).
+//
+// Split tiles (C > 1): halo items recompute the codes a part reads but does
+// not own (RecA kAFlagHalo, RecB wpos < 0, RecBK halo) and count nothing
+// toward the value.  At the end of a sweep every part publishes its partial
+// dual value of each instance, arrives on the tile's counter in global
+// memory (release) and waits for all C arrivals (acquire); then every part
+// sums the C partials in part order, so all parts take the same best /
+// divergence / stopping decisions, and the y_{k+1} rows each part wrote are
+// visible to the other parts' TMA copies of sweep k+1.  The launch is
+// cooperative: all CTAs are co-resident.
 //
 // Outages (F2): an outaged branch's nu is held at exactly zero (it starts at
 // 0 and its gradient f* - phi is +-0), so b nu vanishes in phase A without a
@@ -67,10 +83,16 @@ struct SweepArgs {
   const int *prog_bytes, *tx_bytes;
   const int *ld_ptr;
   const int4 *ld;                   // load entries {kind, first storage position, rows, first slot}
-  int nsteps, S, row_bytes, br_row_bytes;
+  int S, row_bytes, br_row_bytes;
   int off_bar, off_red, off_frz, off_obm, off_outs, off_prog, prog_stride, off_brp, off_lamp, off_dp, off_th,
       off_fc;
-  int soft;                         // 1: consumer warps drift by <= 1 step (pool_gap 2); 0: lock-step
+  // split tiles
+  int parts;                        // C: CTAs per tile (blockIdx.x = tile * C + part)
+  const int *part_step0;            // [C+1] first global step of each part
+  unsigned *tile_sync;              // [tiles] arrival counters, zero at launch (C > 1)
+  double *part_val;                 // [2][tiles][C][W] partial dual values (C > 1)
+  int tiles;
+  int soft;                         // 1: consumer warps drift by <= 2 steps (pool_gap 3); 0: lock-step
   double tol;                       // stopping rule (0: off)
   // ascent-step variant (OPT kernels): DCOPF_OPT_* and its state, stored like
   // the multipliers (tile-major rows in storage order), updated in place
@@ -103,12 +125,6 @@ __device__ __forceinline__ void warp_arrive(uint64_t *bar, int lane) {
 // completes (or this many ns pass) instead of re-polling, so waiting warps do
 // not take issue slots from the working ones
 constexpr unsigned kSuspendNs = 1000000;
-#ifndef DCOPF_BACKOFF_NS0
-#define DCOPF_BACKOFF_NS0 32
-#endif
-#ifndef DCOPF_BACKOFF_NSMAX
-#define DCOPF_BACKOFF_NSMAX 256
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   unsigned done = 0;
   do {
@@ -125,7 +141,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
 // nanosleep so a waiting warp issues a handful of instructions instead of
 // re-polling (its SM sub-partition's other warps keep the issue slots)
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, unsigned parity) {
-  unsigned done = 0, ns = DCOPF_BACKOFF_NS0;
+  unsigned done = 0, ns = 32;
   for (;;) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -136,7 +152,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, unsigned parity
         : "memory");
     if (done) return;
     __nanosleep(ns);
-    ns = ns < DCOPF_BACKOFF_NSMAX ? 2 * ns : ns;
+    ns = ns < 256 ? 2 * ns : ns;
   }
 }
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
@@ -149,59 +165,115 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
-// the two instances of a lane
-struct D2 {
-  double x, y;
+// the V instances of a lane
+template <int V>
+struct DV {
+  double v[V];
 };
-struct OState {  // optimiser state of a lane's two instances (one row)
-  double2 s1, s2;
+template <int V>
+struct OState {  // optimiser state of a lane's instances (one row)
+  double s1[V], s2[V];
 };
-__device__ __forceinline__ D2 ld2(const uint8_t *base, int off) {
-  const double2 v = *reinterpret_cast<const double2 *>(base + off);
-  return D2{v.x, v.y};
+// row loads / stores: instances 2l, 2l+1 at byte 16 l of the row (folded into
+// the base pointer), instances W/2 + 2l, W/2 + 2l + 1 hb = 4 W bytes further
+template <int V>
+__device__ __forceinline__ DV<V> ldv(const uint8_t *base, int off, int hb) {
+  DV<V> r;
+  const double2 a = *reinterpret_cast<const double2 *>(base + off);
+  r.v[0] = a.x;
+  r.v[1] = a.y;
+  if constexpr (V == 4) {
+    const double2 b = *reinterpret_cast<const double2 *>(base + off + hb);
+    r.v[2] = b.x;
+    r.v[3] = b.y;
+  }
+  return r;
 }
-__device__ __forceinline__ void st2(double *p, double x, double y) {
-  *reinterpret_cast<double2 *>(p) = make_double2(x, y);
+template <int V>
+__device__ __forceinline__ void stv(void *p, const double (&x)[V], int hb) {
+  *reinterpret_cast<double2 *>(p) = make_double2(x[0], x[1]);
+  if constexpr (V == 4) *reinterpret_cast<double2 *>(reinterpret_cast<uint8_t *>(p) + hb) = make_double2(x[2], x[3]);
 }
-// minimiser codes: one signed byte per instance (+1 / -1 / 0), a lane's two
-// instances in one 16-bit word; value = code * bound, exact for codes in {-1, 0, 1}
+// minimiser codes: one signed byte per instance (+1 / -1 / 0), a lane's V
+// instances in one 2- or 4-byte word at byte V l of the code row (folded into
+// the base pointer); value = code * bound, exact for codes in {-1, 0, 1}
 __device__ __forceinline__ int code_of(bool up, bool down) { return up ? 1 : (down ? -1 : 0); }
-__device__ __forceinline__ void st_code2(uint8_t *p, int c0, int c1) {
-  *reinterpret_cast<unsigned short *>(p) = (unsigned short)((c0 & 0xff) | ((c1 & 0xff) << 8));
+template <int V>
+__device__ __forceinline__ void st_codes(uint8_t *p, const int (&c)[V]) {
+  if constexpr (V == 2) {
+    *reinterpret_cast<unsigned short *>(p) = (unsigned short)((c[0] & 0xff) | ((c[1] & 0xff) << 8));
+  } else {
+    *reinterpret_cast<unsigned *>(p) =
+        (unsigned)(c[0] & 0xff) | ((unsigned)(c[1] & 0xff) << 8) | ((unsigned)(c[2] & 0xff) << 16) |
+        ((unsigned)(c[3] & 0xff) << 24);
+  }
 }
-__device__ __forceinline__ D2 ld_code2(const uint8_t *base, int off, double x) {
-  const unsigned c = *reinterpret_cast<const unsigned short *>(base + off);
-  const int c0 = (int)(signed char)(c & 0xffu), c1 = (int)(signed char)(c >> 8);
-  return D2{(double)c0 * x, (double)c1 * x};
+template <int V>
+__device__ __forceinline__ void ld_codes(const uint8_t *base, int off, int (&c)[V]) {
+  if constexpr (V == 2) {
+    const unsigned u = *reinterpret_cast<const unsigned short *>(base + off);
+    c[0] = (int)(signed char)(u & 0xffu);
+    c[1] = (int)(signed char)(u >> 8);
+  } else {
+    const unsigned u = *reinterpret_cast<const unsigned *>(base + off);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = (int)(signed char)((u >> (8 * j)) & 0xffu);
+  }
+}
+template <int V>
+__device__ __forceinline__ DV<V> ld_code(const uint8_t *base, int off, double x) {
+  int c[V];
+  ld_codes<V>(base, off, c);
+  DV<V> r;
+#pragma unroll
+  for (int j = 0; j < V; ++j) r.v[j] = (double)c[j] * x;
+  return r;
 }
 
-template <int FORM, bool EVAL, int NW, bool SOFT, bool OPT = false>
 #ifndef DCOPF_SWEEP_MAXREG
 #define DCOPF_SWEEP_MAXREG 96  // 20 warps x 32 x 96 + allocation granularity fit the 64K register file
 #endif
-__global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
+// registers per thread: (NW + 1) warps share the 64K register file
+template <int NW>
+struct SweepRegs {
+  static constexpr int value = (NW + 1) * 32 * 128 <= 65536 ? 128 : DCOPF_SWEEP_MAXREG;
+};
+
+template <int FORM, bool EVAL, int NW, bool SOFT, bool OPT, int V>
+__global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + a.off_bar);
   uint64_t *empty = full + a.S;
   uint64_t *adone = empty + a.S;  // [4] all consumer threads finished phase A of step g (slot g & 3)
   uint64_t *bdone = adone + 4;    // [4] ... phase B of step g
-  double *red = reinterpret_cast<double *>(smem + a.off_red);   // [NW][64]
-  int *frz = reinterpret_cast<int *>(smem + a.off_frz);         // [64]
-  double *bst = reinterpret_cast<double *>(smem + a.off_frz + 256);  // [64] running best (no registers held)
-  double *gpv = bst + 64;                                              // [64] previous g (stopping rule)
+  constexpr int TS = 32 * V;  // per-tile instance slots (schedule.cpp layout_smem)
+  double *red = reinterpret_cast<double *>(smem + a.off_red);   // [NW][TS]
+  int *frz = reinterpret_cast<int *>(smem + a.off_frz);         // [TS]
+  double *bst = reinterpret_cast<double *>(smem + a.off_frz + 4 * TS);  // [TS] running best
+  double *gpv = bst + TS;                                                // [TS] previous g
   unsigned *obm = reinterpret_cast<unsigned *>(smem + a.off_obm);
-  int *outs_s = reinterpret_cast<int *>(smem + a.off_outs);     // [64][kMaxOut]
-  constexpr int BRW = (FORM == kFormF2) ? 1 : 2;
+  int *outs_s = reinterpret_cast<int *>(smem + a.off_outs);     // [TS][kMaxOut]
   constexpr int CT = NW * 32;
+  static_assert(V == 2 || V == 4, "2 or 4 instances per lane");
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int W = a.W, L = W >> 1;
+  const int W = a.W, L = W / V, hW = W >> 1, hb = 4 * W;
   const bool act = lane < L;
-  const size_t tile = blockIdx.x;
+  const int C = a.parts;
+  const int part = (int)(blockIdx.x % (unsigned)C);
+  const size_t tile = blockIdx.x / (unsigned)C;
   const long ib = (long)tile * W;          // first instance of the tile
-  const int S = a.S, nst = a.nsteps;
+  const int S = a.S;
+  const int s0 = a.part_step0[part], s1 = a.part_step0[part + 1];
   const long K = EVAL ? 0 : a.K;
+  // instance (within the tile) of this lane's j-th value
+  auto inst = [&](int j) { return (j < 2) ? 2 * lane + j : hW + 2 * lane + (j - 2); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -215,16 +287,16 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int x = threadIdx.x; x < (a.n_br + 31) / 32; x += blockDim.x) obm[x] = 0u;
-  for (int t = threadIdx.x; t < 64; t += blockDim.x) {
+  for (int t = threadIdx.x; t < TS; t += blockDim.x) {
     frz[t] = (!EVAL && t < W) ? a.status[ib + t] : 0;
     bst[t] = (!EVAL && t < W) ? a.best[ib + t] : 0.0;
   }
-  for (int x = threadIdx.x; x < 64 * kMaxOut; x += blockDim.x) {
+  for (int x = threadIdx.x; x < TS * kMaxOut; x += blockDim.x) {
     const int t = x / kMaxOut, j = x % kMaxOut;
     outs_s[x] = (t < W && j < a.max_out) ? a.outs[(ib + t) * a.max_out + j] : -1;
   }
   __syncthreads();
-  for (int x = threadIdx.x; x < 64 * kMaxOut; x += blockDim.x)
+  for (int x = threadIdx.x; x < TS * kMaxOut; x += blockDim.x)
     if (outs_s[x] >= 0) atomicOr(&obm[outs_s[x] >> 5], 1u << (outs_s[x] & 31));
   __syncthreads();
 
@@ -235,12 +307,15 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
     unsigned pph = 0;      // its use parity
     bool pused = false;    // every stage used at least once
     for (long k = 0; k <= K; ++k) {
-      if (k > 0) named_bar(2, (NW + 1) * 32);  // sweep k-1 written and fenced
+      if (k > 0) {
+        named_bar(2, (NW + 1) * 32);  // sweep k-1 written and fenced (all parts of the tile)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       const int par = (a.cur + (int)(k & 1)) & 1;
       const uint8_t *lam_src = reinterpret_cast<const uint8_t *>(par ? a.lam1 : a.lam0) + tile * (size_t)a.n_bus * RB;
       const uint8_t *br_src = reinterpret_cast<const uint8_t *>(par ? a.br1 : a.br0) + tile * (size_t)a.n_brows * BR;
       const uint8_t *d_src = reinterpret_cast<const uint8_t *>(a.d) + tile * (size_t)a.n_bus * RB;
-      for (int c = 0; c < nst; ++c) {
+      for (int c = s0; c < s1; ++c) {
         const int st = pst;
         const unsigned pu = pph;  // parity of this use of stage st
         if (++pst == S) {
@@ -274,8 +349,7 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
 
   // =========================== consumers ===========================
   const int RB = a.row_bytes, BR = a.br_row_bytes;
-  // lanes past the tile width (W < 64) read the pools' tail padding and never
-  // store (mirroring lane 0 instead would put them in lane 0's banks)
+  // lanes past the tile width read the pools' tail padding and never store
   const int lofs = lane * 16;
   const uint8_t *brp = smem + a.off_brp + lofs;
   const uint8_t *lamp = smem + a.off_lamp + lofs;
@@ -287,8 +361,8 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
   uint8_t *os2b = OPT ? reinterpret_cast<uint8_t *>(a.s2_br) + tile * (size_t)a.n_brows * BR + lofs : nullptr;
   const bool ost2 = OPT && a.opt == 4;  // Adam: two state arrays
   double ob1t = a.b1t, ob2t = a.b2t;
-  uint8_t *thp = smem + a.off_th + 2 * lane;  // theta*_i code rows
-  uint8_t *fcp = smem + a.off_fc + 2 * lane;  // f*_l code rows (F2)
+  uint8_t *thp = smem + a.off_th + V * lane;  // theta*_i code rows
+  uint8_t *fcp = smem + a.off_fc + V * lane;  // f*_l code rows (F2)
   // Consumer warps are not stepped in lock-step.  In step g a warp waits on
   //   full[stage]   before anything: the step's program block and rows landed;
   //   A-done(g-1)   after its A(g) items, before B: the theta* codes of chunk
@@ -300,7 +374,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
   // B(g) likewise, then B-done(g-1) before C and D.)  Warps drift by <= 2 steps.
   unsigned gs = 0;  // global step counter (continues across sweeps; only gs mod 8 matters)
   const int nout = a.max_out;
-  const int *my_outs0 = outs_s + (2 * lane) * kMaxOut, *my_outs1 = my_outs0 + kMaxOut;
+  const int *my_outs[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) my_outs[j] = outs_s + inst(j) * kMaxOut;
   auto flagged = [&](int l) { return (obm[l >> 5] >> (l & 31)) & 1u; };
   auto out_t = [&](const int *lst, int l) {
     bool r = false;
@@ -318,39 +394,55 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
                      lofs;
     uint8_t *br_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_br : (par ? a.br0 : a.br1)) + tile * (size_t)a.n_brows * BR +
                     lofs;
-    const bool step0 = !EVAL && !last && !frz[2 * lane], step1 = !EVAL && !last && !frz[2 * lane + 1];
+    bool stp[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) stp[j] = !EVAL && !last && !frz[inst(j)];
     const double alpha = (EVAL || last) ? 0.0 : a.alpha[k];
     if (OPT && !EVAL && !last) {  // Adam's beta^t, t = steps since the state was reset
       ob1t = ob1t * a.beta1;
       ob2t = ob2t * a.beta2;
     }
-    // optimiser-variant update of one row of the lane's two instances (the
-    // state row sits at the same offset of the state arrays)
-    // (oload issues the state loads at the start of an item so their latency
-    // overlaps the item's work; ostep updates and stores them)
-    auto oload = [&](size_t off, bool lam_side, bool on) -> OState {
-      OState o{make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    // optimiser-variant update of one row of the lane's instances (the state
+    // row sits at the same offset of the state arrays); oload issues the
+    // state loads at the start of an item so their latency overlaps the item's
+    // work, ostep updates and stores them
+    auto oload = [&](size_t off, bool lam_side, bool on) -> OState<V> {
+      OState<V> o;
+#pragma unroll
+      for (int j = 0; j < V; ++j) o.s1[j] = o.s2[j] = 0.0;
       if (on) {
-        o.s1 = *reinterpret_cast<const double2 *>((lam_side ? os1l : os1b) + off);
-        if (ost2) o.s2 = *reinterpret_cast<const double2 *>((lam_side ? os2l : os2b) + off);
+        const DV<V> x = ldv<V>((lam_side ? os1l : os1b), (int)off, hb);
+#pragma unroll
+        for (int j = 0; j < V; ++j) o.s1[j] = x.v[j];
+        if (ost2) {
+          const DV<V> y = ldv<V>((lam_side ? os2l : os2b), (int)off, hb);
+#pragma unroll
+          for (int j = 0; j < V; ++j) o.s2[j] = y.v[j];
+        }
       }
       return o;
     };
-    auto ostep = [&](OState &o, double y0, double y1, double g0, double g1, size_t off, bool lam_side, bool do0,
-                     bool do1) -> D2 {
-      if (do0) y0 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y0, g0, alpha, o.s1.x, o.s2.x, ob1t, ob2t);
-      if (do1) y1 = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y1, g1, alpha, o.s1.y, o.s2.y, ob1t, ob2t);
-      *reinterpret_cast<double2 *>((lam_side ? os1l : os1b) + off) = o.s1;
-      if (ost2) *reinterpret_cast<double2 *>((lam_side ? os2l : os2b) + off) = o.s2;
-      return D2{y0, y1};
+    // y[j] <- update (only where do_[j]); state stored back
+    auto ostep = [&](OState<V> &o, double (&y)[V], const double (&g)[V], size_t off, bool lam_side,
+                     const bool (&do_)[V]) {
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        if (do_[j]) y[j] = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y[j], g[j], alpha, o.s1[j], o.s2[j], ob1t, ob2t);
+      stv<V>((lam_side ? os1l : os1b) + off, o.s1, hb);
+      if (ost2) stv<V>((lam_side ? os2l : os2b) + off, o.s2, hb);
     };
-    double v0 = 0.0, v1 = 0.0;
+    double v[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) v[j] = 0.0;
 
     // the step loop, instantiated twice: CHK = some instance of the tile is
-    // frozen (diverged) and its state must be carried over unchanged
+    // frozen (diverged / converged) and its state must be carried over unchanged
     auto run_steps = [&](auto chk_tag) {
     constexpr bool CHK = decltype(chk_tag)::value;
-    for (int c = 0; c < nst; ++c) {
+    bool dos[V];  // the step is taken for instance j
+#pragma unroll
+    for (int j = 0; j < V; ++j) dos[j] = !CHK || stp[j];
+    for (int c = s0; c < s1; ++c) {
       const int st = cst;
       mbar_wait(&full[st], cph);
       if (++cst == S) {
@@ -358,13 +450,10 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         cph ^= 1u;
       }
       const uint8_t *prog = smem + a.off_prog + st * a.prog_stride;
-      const int4 h0 = *reinterpret_cast<const int4 *>(prog);       // nA nIA nB nC
-      const int4 h1 = *reinterpret_cast<const int4 *>(prog + 16);  // nIC nG a0 b0
       const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);  // offA offIA offB offC
       const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC bytes -
       const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // - - offW -
       const unsigned short *wt = reinterpret_cast<const unsigned short *>(prog + h4.z);  // [3][NW+1] item ranges
-      const int nA = h0.x, nB = h0.z, nC = h0.w;
 
       // ---------------- C: ready buses (F2 / F1: C(s-2), warp table 2; KVL: C(s-1), table 1) ----
       auto phaseC = [&](int tbl) {
@@ -372,31 +461,30 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
         for (int j = wt[tbl * (NW + 1) + warp], je = wt[tbl * (NW + 1) + warp + 1]; j < je; ++j) {
           const RecC r = Cv[j];
-          OState ost = oload((size_t)r.wpos * RB, true, OPT && !EVAL && write && act);
-          const D2 li = ld2(lamp, r.ls), di = ld2(dp, r.ds);
-          double gl0 = -di.x, gl1 = -di.y;
+          OState<V> ost = oload((size_t)r.wpos * RB, true, OPT && !EVAL && write && act);
+          const DV<V> li = ldv<V>(lamp, r.ls, hb), di = ldv<V>(dp, r.ds, hb);
+          double gl[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) gl[q] = -di.v[q];
 #pragma unroll 1
           for (int gg = r.g0; gg < r.g1; ++gg) {  // mostly 0 or 1 generator
             const RecG gr = G[gg];
-            const double r0 = gr.c + li.x, r1 = gr.c + li.y;
-            const double p0 = gen_minimiser(r0, gr.lo, gr.hi, gr.a), p1 = gen_minimiser(r1, gr.lo, gr.hi, gr.a);
-            gl0 = gl0 + p0;
-            gl1 = gl1 + p1;
-            if (gr.a > 0.0) {
-              v0 += gr.a * p0 * p0 + r0 * p0;
-              v1 += gr.a * p1 * p1 + r1 * p1;
-            } else {
-              v0 += r0 * p0;
-              v1 += r1 * p1;
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              const double rr = gr.c + li.v[q];
+              const double p = gen_minimiser(rr, gr.lo, gr.hi, gr.a);
+              gl[q] = gl[q] + p;
+              if (gr.a > 0.0) v[q] += gr.a * p * p + rr * p;
+              else v[q] += rr * p;
             }
           }
           if (FORM != kFormF1) {
             const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y) + r.e0;
             const int n = r.e1 - r.e0;
             auto acc = [&](const RecIC2 &x) {
-              const D2 f = ld_code2(fcp, x.f, x.sF);  // +-f* (c * (+-F) == +-(c * F) exactly)
-              gl0 = gl0 + f.x;  // +f* at the to bus, -f* at the from bus
-              gl1 = gl1 + f.y;
+              const DV<V> f = ld_code<V>(fcp, x.f, x.sF);  // +-f* (c * (+-F) == +-(c * F) exactly)
+#pragma unroll
+              for (int q = 0; q < V; ++q) gl[q] = gl[q] + f.v[q];  // +f* at the to bus, -f* at the from bus
             };
 #pragma unroll
             for (int e = 0; e < 4; ++e)
@@ -408,27 +496,36 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
 #pragma unroll 1
             for (int e = r.e0; e < r.e1; ++e) {
               const RecIC1 x = IC[e];
-              double sb0 = x.sb, sb1 = x.sb;
+              double sb[V];
+#pragma unroll
+              for (int q = 0; q < V; ++q) sb[q] = x.sb;
               if (x.br >= 0 && flagged(x.br)) {
-                if (out_t(my_outs0, x.br)) sb0 = copysign(0.0, sb0);
-                if (out_t(my_outs1, x.br)) sb1 = copysign(0.0, sb1);
+#pragma unroll
+                for (int q = 0; q < V; ++q)
+                  if (out_t(my_outs[q], x.br)) sb[q] = copysign(0.0, sb[q]);
               }
-              const D2 ts = ld_code2(thp, x.ts, x.ths), tt = ld_code2(thp, x.tt, x.tht);
-              gl0 = gl0 + sb0 * (ts.x - tt.x);
-              gl1 = gl1 + sb1 * (ts.y - tt.y);
+              const DV<V> ts = ld_code<V>(thp, x.ts, x.ths), tt = ld_code<V>(thp, x.tt, x.tht);
+#pragma unroll
+              for (int q = 0; q < V; ++q) gl[q] = gl[q] + sb[q] * (ts.v[q] - tt.v[q]);
             }
           }
-          v0 += -(li.x * di.x);
-          v1 += -(li.y * di.y);
+#pragma unroll
+          for (int q = 0; q < V; ++q) v[q] += -(li.v[q] * di.v[q]);
           if (write && act) {
-            double *dst = reinterpret_cast<double *>(lam_o + (size_t)r.wpos * RB);
+            uint8_t *dst = lam_o + (size_t)r.wpos * RB;
             if (EVAL) {
-              st2(dst, gl0, gl1);
+              stv<V>(dst, gl, hb);
             } else if constexpr (OPT) {
-              const D2 y = ostep(ost, li.x, li.y, gl0, gl1, (size_t)r.wpos * RB, true, !CHK || step0, !CHK || step1);
-              st2(dst, y.x, y.y);
+              double y[V];
+#pragma unroll
+              for (int q = 0; q < V; ++q) y[q] = li.v[q];
+              ostep(ost, y, gl, (size_t)r.wpos * RB, true, dos);
+              stv<V>(dst, y, hb);
             } else {
-              st2(dst, (!CHK || step0) ? li.x + alpha * gl0 : li.x, (!CHK || step1) ? li.y + alpha * gl1 : li.y);
+              double y[V];
+#pragma unroll
+              for (int q = 0; q < V; ++q) y[q] = dos[q] ? li.v[q] + alpha * gl[q] : li.v[q];
+              stv<V>(dst, y, hb);
             }
           }
         }
@@ -441,32 +538,44 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       // ---------------- B(s): q_l = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t), f* ----------------
       {
         const RecBK *Bv = reinterpret_cast<const RecBK *>(prog + h2.z);
-        const RecBKe *BKe = reinterpret_cast<const RecBKe *>(prog + h3.w);
+        const RecBKe *BKe = reinterpret_cast<const RecBKe *>(prog + *reinterpret_cast<const int *>(prog + 4 * PH_PAD));
         for (int j = wt[warp], je = wt[warp + 1]; j < je; ++j) {
           const RecBK r = Bv[j];
-          double x0 = r.x, x1 = r.x, F0 = r.F, F1v = r.F;
-          bool o0 = false, o1 = false;
-          if (r.obr >= 0 && flagged(r.obr)) {  // an outaged lane: b = F = 0
-            o0 = out_t(my_outs0, r.obr);
-            o1 = out_t(my_outs1, r.obr);
-            if (o0) x0 = F0 = 0.0;
-            if (o1) x1 = F1v = 0.0;
+          double x[V], F[V];
+          bool o[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            x[q] = r.x;
+            F[q] = r.F;
+            o[q] = false;
           }
-          double s0 = 0.0, s1 = 0.0;  // cycles in ascending k (the oracle's order)
+          if (r.obr >= 0 && flagged(r.obr)) {  // an outaged lane: b = F = 0
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              o[q] = out_t(my_outs[q], r.obr);
+              if (o[q]) x[q] = F[q] = 0.0;
+            }
+          }
+          double s[V];  // cycles in ascending k (the oracle's order)
+#pragma unroll
+          for (int q = 0; q < V; ++q) s[q] = 0.0;
 #pragma unroll 1
           for (int e = r.e0; e < r.e1; ++e) {
             const RecBKe t = BKe[e];
-            const D2 kv = ld2(brp, t.ks);
-            s0 = (t.sgn > 0) ? s0 + kv.x : s0 - kv.x;
-            s1 = (t.sgn > 0) ? s1 + kv.y : s1 - kv.y;
+            const DV<V> kv = ldv<V>(brp, t.ks, hb);
+#pragma unroll
+            for (int q = 0; q < V; ++q) s[q] = (t.sgn > 0) ? s[q] + kv.v[q] : s[q] - kv.v[q];
           }
-          const D2 ls = ld2(lamp, r.ls), lt = ld2(lamp, r.lt);
-          const double q0 = x0 * s0 - (ls.x - lt.x), q1 = x1 * s1 - (ls.y - lt.y);
-          const double f0 = (q0 > 0.0) ? -F0 : ((q0 < 0.0) ? F0 : 0.0);
-          const double f1 = (q1 > 0.0) ? -F1v : ((q1 < 0.0) ? F1v : 0.0);
-          if (act) st_code2(fcp + r.fs, o0 ? 0 : code_of(q0 < 0.0, q0 > 0.0), o1 ? 0 : code_of(q1 < 0.0, q1 > 0.0));
-          v0 += q0 * f0;
-          v1 += q1 * f1;
+          const DV<V> ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+          int cd[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            const double qq = x[q] * s[q] - (ls.v[q] - lt.v[q]);
+            const double f = (qq > 0.0) ? -F[q] : ((qq < 0.0) ? F[q] : 0.0);
+            cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
+            if (!r.halo) v[q] += qq * f;
+          }
+          if (act) st_codes<V>(fcp + r.fs, cd);
         }
       }
       if (SOFT) {  // C and D read the f* codes of B(<= s-1)
@@ -480,33 +589,44 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         const RecDe *De = reinterpret_cast<const RecDe *>(prog + h2.y);
         for (int j = wt[2 * (NW + 1) + warp], je = wt[2 * (NW + 1) + warp + 1]; j < je; ++j) {
           const RecD r = Dv[j];
-          OState ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
-          const D2 kv = ld2(brp, r.ks);
-          double acc0 = 0.0, acc1 = 0.0;
+          OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
+          const DV<V> kv = ldv<V>(brp, r.ks, hb);
+          double acc[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = 0.0;
 #pragma unroll 1
           for (int e = r.e0; e < r.e1; ++e) {
             const RecDe d = De[e];
-            const unsigned c = *reinterpret_cast<const unsigned short *>(fcp + d.fs);
+            int cd[V];
+            ld_codes<V>(fcp, d.fs, cd);
             // index 0 / 1 / 2 for code -1 / 0 / +1 (lanes past the tile width read
             // padding bytes: clamp so they never index outside the record)
-            const int c0 = (int)(signed char)(c & 0xffu), c1 = (int)(signed char)(c >> 8);
-            const int i0 = (c0 > 0) ? 2 : ((c0 < 0) ? 0 : 1), i1 = (c1 > 0) ? 2 : ((c1 < 0) ? 0 : 1);
-            acc0 = acc0 + d.t[i0];  // (c F) sx: the oracle's C_kl (f*_l x_l), exact
-            acc1 = acc1 + d.t[i1];
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              const int i = (cd[q] > 0) ? 2 : ((cd[q] < 0) ? 0 : 1);
+              acc[q] = acc[q] + d.t[i];  // (c F) sx: the oracle's C_kl (f*_l x_l), exact
+            }
           }
           if (r.dbr >= 0 && flagged(r.dbr)) {  // defining branch out: no cycle, gradient 0
-            if (out_t(my_outs0, r.dbr)) acc0 = 0.0;
-            if (out_t(my_outs1, r.dbr)) acc1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < V; ++q)
+              if (out_t(my_outs[q], r.dbr)) acc[q] = 0.0;
           }
           if (write && act) {
-            double *dst = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR);
+            uint8_t *dst = br_o + (size_t)r.wpos * BR;
             if (EVAL) {
-              st2(dst, acc0, acc1);
+              stv<V>(dst, acc, hb);
             } else if constexpr (OPT) {
-              const D2 y = ostep(ost, kv.x, kv.y, acc0, acc1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
-              st2(dst, y.x, y.y);
+              double y[V];
+#pragma unroll
+              for (int q = 0; q < V; ++q) y[q] = kv.v[q];
+              ostep(ost, y, acc, (size_t)r.wpos * BR, false, dos);
+              stv<V>(dst, y, hb);
             } else {
-              st2(dst, (!CHK || step0) ? kv.x + alpha * acc0 : kv.x, (!CHK || step1) ? kv.y + alpha * acc1 : kv.y);
+              double y[V];
+#pragma unroll
+              for (int q = 0; q < V; ++q) y[q] = dos[q] ? kv.v[q] + alpha * acc[q] : kv.v[q];
+              stv<V>(dst, y, hb);
             }
           }
         }
@@ -522,8 +642,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
         for (int j = wt[warp], je = wt[warp + 1]; j < je; ++j) {
           const RecA ra = A[j];
-          const int bus = ra.bus;
-          double w0 = 0.0, w1 = 0.0;
+          double w[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) w[q] = 0.0;
           if (FORM == kFormF2) {
             // incidence entries in ascending original branch id (the oracle's
             // order); degree <= 4 for ~97% of buses: a fixed 4-way body with
@@ -531,9 +652,9 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
             const RecIA2 *IA = reinterpret_cast<const RecIA2 *>(prog + h2.y) + ra.e0;
             const int n = ra.e1 - ra.e0;
             auto acc = [&](const RecIA2 &r) {
-              const D2 nu = ld2(brp, r.row);
-              w0 = w0 + r.sb * nu.x;  // w_s += -(b nu), w_t += b nu (outaged: nu == 0)
-              w1 = w1 + r.sb * nu.y;
+              const DV<V> nu = ldv<V>(brp, r.row, hb);
+#pragma unroll
+              for (int q = 0; q < V; ++q) w[q] = w[q] + r.sb * nu.v[q];  // w_s += -(b nu), w_t += b nu (outaged: nu == 0)
             };
 #pragma unroll
             for (int e = 0; e < 4; ++e)
@@ -545,26 +666,32 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
 #pragma unroll 1
             for (int e = ra.e0; e < ra.e1; ++e) {
               const RecIA1 r = IA[e];
-              double sb0 = r.sb, sb1 = r.sb;
+              double sb[V];
+#pragma unroll
+              for (int q = 0; q < V; ++q) sb[q] = r.sb;
               if (r.br >= 0 && flagged(r.br)) {  // br < 0: branch never taken out
-                if (out_t(my_outs0, r.br)) sb0 = copysign(0.0, sb0);
-                if (out_t(my_outs1, r.br)) sb1 = copysign(0.0, sb1);
+#pragma unroll
+                for (int q = 0; q < V; ++q)
+                  if (out_t(my_outs[q], r.br)) sb[q] = copysign(0.0, sb[q]);
               }
-              const D2 mp = ld2(brp, r.row), mm = ld2(brp, r.row + RB);
-              const D2 ls = ld2(lamp, r.ls), lt = ld2(lamp, r.lt);
-              w0 = w0 + sb0 * ((mp.x - mm.x) - (ls.x - lt.x));  // w_s += u, w_t -= u
-              w1 = w1 + sb1 * ((mp.y - mm.y) - (ls.y - lt.y));
+              const DV<V> mp = ldv<V>(brp, r.row, hb), mm = ldv<V>(brp, r.row + RB, hb);
+              const DV<V> ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+#pragma unroll
+              for (int q = 0; q < V; ++q)
+                w[q] = w[q] + sb[q] * ((mp.v[q] - mm.v[q]) - (ls.v[q] - lt.v[q]));  // w_s += u, w_t -= u
             }
           }
           // theta* = -Theta if w > 0, +Theta if w < 0, 0 on a tie and at the reference bus
-          const bool nr = (bus != a.ref);
-          const double t0 = (nr && w0 < 0.0) ? ra.theta : ((nr && w0 > 0.0) ? -ra.theta : 0.0);
-          const double t1 = (nr && w1 < 0.0) ? ra.theta : ((nr && w1 > 0.0) ? -ra.theta : 0.0);
-          if (act) st_code2(thp + ra.th, code_of(nr && w0 < 0.0, nr && w0 > 0.0), code_of(nr && w1 < 0.0, nr && w1 > 0.0));
-          if (nr) {
-            v0 += w0 * t0;
-            v1 += w1 * t1;
+          const bool nr = !(ra.flags & kAFlagRef);
+          const bool val = nr && !(ra.flags & kAFlagHalo);  // a halo bus: code only
+          int cd[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            const double t = (nr && w[q] < 0.0) ? ra.theta : ((nr && w[q] > 0.0) ? -ra.theta : 0.0);
+            cd[q] = code_of(nr && w[q] < 0.0, nr && w[q] > 0.0);
+            if (val) v[q] += w[q] * t;
           }
+          if (act) st_codes<V>(thp + ra.th, cd);
         }
       }
       if (SOFT) {  // B(s-1) reads the theta* codes of A(<= s-1); the f* slots it writes
@@ -577,81 +704,118 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
         for (int j = wt[NW + 1 + warp], je = wt[NW + 2 + warp]; j < je; ++j) {
           const RecB r = Bv[j];
-          OState ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
-          OState ost_m = oload((size_t)r.wpos * BR + RB, false, FORM == kFormF1 && OPT && !EVAL && write && act);
-          double b0 = r.b, b1 = r.b, F0 = r.F, F1v = r.F;
-          bool o0 = false, o1 = false;
-          if (r.obr >= 0 && flagged(r.obr)) {  // obr < 0: branch never taken out
-            o0 = out_t(my_outs0, r.obr);
-            o1 = out_t(my_outs1, r.obr);
-            if (o0) b0 = F0 = 0.0;
-            if (o1) b1 = F1v = 0.0;
+          double b[V], F[V];
+          bool o[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            b[q] = r.b;
+            F[q] = r.F;
+            o[q] = false;
           }
-          const D2 ths = ld_code2(thp, r.ts, r.ths), tht = ld_code2(thp, r.tt, r.tht);
-          const double phi0 = b0 * (ths.x - tht.x);
-          const double phi1 = b1 * (ths.y - tht.y);
-          double* dst = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR);
+          if (r.obr >= 0 && flagged(r.obr)) {  // obr < 0: branch never taken out
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              o[q] = out_t(my_outs[q], r.obr);
+              if (o[q]) b[q] = F[q] = 0.0;
+            }
+          }
+          if (FORM == kFormF2 && r.wpos < 0) {
+            // lite halo branch (split tiles): its f* code for this part's C items
+            const DV<V> nu = ldv<V>(brp, r.row, hb), ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+            int cd[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              const double qq = nu.v[q] - (ls.v[q] - lt.v[q]);
+              cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
+            }
+            if (act) st_codes<V>(fcp + r.fs, cd);
+            continue;
+          }
+          OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
+          OState<V> ost_m = oload((size_t)r.wpos * BR + RB, false, FORM == kFormF1 && OPT && !EVAL && write && act);
+          const DV<V> ths = ld_code<V>(thp, r.ts, r.ths), tht = ld_code<V>(thp, r.tt, r.tht);
+          double phi[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) phi[q] = b[q] * (ths.v[q] - tht.v[q]);
+          uint8_t *dst = br_o + (size_t)r.wpos * BR;
           if (FORM == kFormF2) {
-            const D2 nu = ld2(brp, r.row), ls = ld2(lamp, r.ls), lt = ld2(lamp, r.lt);
-            const double q0 = nu.x - (ls.x - lt.x), q1 = nu.y - (ls.y - lt.y);
-            // f* = -F if q > 0, +F if q < 0, 0 on a tie (an outaged lane has F = 0)
-            const double f0 = (q0 > 0.0) ? -F0 : ((q0 < 0.0) ? F0 : 0.0);
-            const double f1 = (q1 > 0.0) ? -F1v : ((q1 < 0.0) ? F1v : 0.0);
-            // code for C (an outaged lane stores the tie: its f* = +-0)
-            if (act) st_code2(fcp + r.fs, o0 ? 0 : code_of(q0 < 0.0, q0 > 0.0), o1 ? 0 : code_of(q1 < 0.0, q1 > 0.0));
-            const double g0 = f0 - phi0, g1 = f1 - phi1;  // Kirchhoff residual
-            v0 += q0 * f0;
-            v1 += q1 * f1;
+            const DV<V> nu = ldv<V>(brp, r.row, hb), ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+            double g[V];
+            int cd[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              const double qq = nu.v[q] - (ls.v[q] - lt.v[q]);
+              // f* = -F if q > 0, +F if q < 0, 0 on a tie (an outaged lane has F = 0)
+              const double f = (qq > 0.0) ? -F[q] : ((qq < 0.0) ? F[q] : 0.0);
+              // code for C (an outaged lane stores the tie: its f* = +-0)
+              cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
+              g[q] = f - phi[q];  // Kirchhoff residual
+              v[q] += qq * f;
+            }
+            if (act) st_codes<V>(fcp + r.fs, cd);
             if (write && act) {
               if (EVAL) {
-                st2(dst, g0, g1);
+                stv<V>(dst, g, hb);
               } else if constexpr (OPT) {
-                const D2 y = ostep(ost, nu.x, nu.y, g0, g1, (size_t)r.wpos * BR, false, !CHK || step0, !CHK || step1);
-                st2(dst, y.x, y.y);
+                double y[V];
+#pragma unroll
+                for (int q = 0; q < V; ++q) y[q] = nu.v[q];
+                ostep(ost, y, g, (size_t)r.wpos * BR, false, dos);
+                stv<V>(dst, y, hb);
               } else {
-                st2(dst, (!CHK || step0) ? nu.x + alpha * g0 : nu.x, (!CHK || step1) ? nu.y + alpha * g1 : nu.y);
+                double y[V];
+#pragma unroll
+                for (int q = 0; q < V; ++q) y[q] = dos[q] ? nu.v[q] + alpha * g[q] : nu.v[q];
+                stv<V>(dst, y, hb);
               }
             }
           } else {
-            const D2 mp = ld2(brp, r.row), mm = ld2(brp, r.row + RB);
-            const double gp0 = phi0 - F0, gm0 = -phi0 - F0, gp1 = phi1 - F1v, gm1 = -phi1 - F1v;
-            v0 += -(F0 * (mp.x + mm.x));
-            v1 += -(F1v * (mp.y + mm.y));
+            const DV<V> mp = ldv<V>(brp, r.row, hb), mm = ldv<V>(brp, r.row + RB, hb);
+            double gp[V], gm[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              gp[q] = phi[q] - F[q];
+              gm[q] = -phi[q] - F[q];
+              v[q] += -(F[q] * (mp.v[q] + mm.v[q]));
+            }
             if (write && act) {
-              double* dst2 = reinterpret_cast<double *>(br_o + (size_t)r.wpos * BR + RB);
+              uint8_t *dst2 = br_o + (size_t)r.wpos * BR + RB;
               if (EVAL) {
-                st2(dst, gp0, gp1);
-                st2(dst2, gm0, gm1);
+                stv<V>(dst, gp, hb);
+                stv<V>(dst2, gm, hb);
               } else {
-                double p0 = mp.x, m0 = mm.x, p1 = mp.y, m1 = mm.y;
+                double pp[V], mq[V];
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                  pp[q] = mp.v[q];
+                  mq[q] = mm.v[q];
+                }
                 if constexpr (OPT) {
-                  const bool d0 = !CHK || step0, d1 = !CHK || step1;
-                  const D2 yp = ostep(ost, mp.x, mp.y, gp0, gp1, (size_t)r.wpos * BR, false, d0, d1);
-                  const D2 ym = ostep(ost_m, mm.x, mm.y, gm0, gm1, (size_t)r.wpos * BR + RB, false, d0, d1);
-                  if (d0) {
-                    p0 = (yp.x > 0.0) ? yp.x : 0.0;  // mu <- max(mu, 0)
-                    m0 = (ym.x > 0.0) ? ym.x : 0.0;
+                  double yp[V], ym[V];
+#pragma unroll
+                  for (int q = 0; q < V; ++q) {
+                    yp[q] = mp.v[q];
+                    ym[q] = mm.v[q];
                   }
-                  if (d1) {
-                    p1 = (yp.y > 0.0) ? yp.y : 0.0;
-                    m1 = (ym.y > 0.0) ? ym.y : 0.0;
-                  }
+                  ostep(ost, yp, gp, (size_t)r.wpos * BR, false, dos);
+                  ostep(ost_m, ym, gm, (size_t)r.wpos * BR + RB, false, dos);
+#pragma unroll
+                  for (int q = 0; q < V; ++q)
+                    if (dos[q]) {
+                      pp[q] = (yp[q] > 0.0) ? yp[q] : 0.0;  // mu <- max(mu, 0)
+                      mq[q] = (ym[q] > 0.0) ? ym[q] : 0.0;
+                    }
                 } else {
-                if (!CHK || step0) {
-                  p0 = mp.x + alpha * gp0;
-                  m0 = mm.x + alpha * gm0;
-                  p0 = (p0 > 0.0) ? p0 : 0.0;  // mu <- max(mu, 0)
-                  m0 = (m0 > 0.0) ? m0 : 0.0;
+#pragma unroll
+                  for (int q = 0; q < V; ++q)
+                    if (dos[q]) {
+                      const double p0 = mp.v[q] + alpha * gp[q], m0 = mm.v[q] + alpha * gm[q];
+                      pp[q] = (p0 > 0.0) ? p0 : 0.0;  // mu <- max(mu, 0)
+                      mq[q] = (m0 > 0.0) ? m0 : 0.0;
+                    }
                 }
-                if (!CHK || step1) {
-                  p1 = mp.y + alpha * gp1;
-                  m1 = mm.y + alpha * gm1;
-                  p1 = (p1 > 0.0) ? p1 : 0.0;
-                  m1 = (m1 > 0.0) ? m1 : 0.0;
-                }
-                }
-                st2(dst, p0, p1);
-                st2(dst2, m0, m1);
+                stv<V>(dst, pp, hb);
+                stv<V>(dst2, mq, hb);
               }
             }
           }
@@ -673,78 +837,86 @@ __global__ void __maxnreg__(DCOPF_SWEEP_MAXREG) k_sweep(const SweepArgs a) {
       ++gs;
     }
     };
-    const bool anyf = __any_sync(0xffffffffu, (frz[2 * lane] | frz[2 * lane + 1]) != 0);
+    bool anyf_l = false;
+#pragma unroll
+    for (int j = 0; j < V; ++j) anyf_l |= frz[inst(j)] != 0;
+    const bool anyf = __any_sync(0xffffffffu, anyf_l);
     if (anyf) run_steps(std::integral_constant<bool, true>{});
     else run_steps(std::integral_constant<bool, false>{});
     // ---------------- dual value, best, status ----------------
     named_bar(1, CT);  // every warp is past the sweep's last step: the pools red aliases are dead
-    red[warp * 64 + 2 * lane] = v0;
-    red[warp * 64 + 2 * lane + 1] = v1;
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[warp * TS + inst(j)] = v[j];
     named_bar(1, CT);
+    double g[V];
     if (warp == 0 && act) {
-      double g0 = 0.0, g1 = 0.0;
-      for (int w = 0; w < NW; ++w) {
-        g0 += red[w * 64 + 2 * lane];
-        g1 += red[w * 64 + 2 * lane + 1];
-      }
-      const long b0i = ib + 2 * lane, b1i = b0i + 1;
-      if (EVAL) {
-        a.out_val[b0i] = g0;
-        a.out_val[b1i] = g1;
-      } else {
-        if (!last && a.hist) {
-          if (b0i < a.B) a.hist[(size_t)k * a.B + b0i] = g0;
-          if (b1i < a.B) a.hist[(size_t)k * a.B + b1i] = g1;
-        }
-        if (last) {
-          a.bound[b0i] = g0;
-          a.bound[b1i] = g1;
-        }
-        double best0 = bst[2 * lane], best1 = bst[2 * lane + 1];
-        // (stopping rule: |g_k - g_{k-1}| < tol within this call; status 2)
-        const bool chk = a.tol > 0.0 && k > 0;
-        if (!frz[2 * lane]) {
-          if (valid_bound(g0)) {
-            best0 = (g0 > best0) ? g0 : best0;
-            if (chk && fabs(g0 - gpv[2 * lane]) < a.tol) frz[2 * lane] = 2;
-          } else {
-            frz[2 * lane] = 1;
-          }
-        }
-        if (!frz[2 * lane + 1]) {
-          if (valid_bound(g1)) {
-            best1 = (g1 > best1) ? g1 : best1;
-            if (chk && fabs(g1 - gpv[2 * lane + 1]) < a.tol) frz[2 * lane + 1] = 2;
-          } else {
-            frz[2 * lane + 1] = 1;
-          }
-        }
-        bst[2 * lane] = best0;
-        bst[2 * lane + 1] = best1;
-        gpv[2 * lane] = g0;
-        gpv[2 * lane + 1] = g1;
-        if (a.target) {  // time to gap: first evaluation whose running best reaches the target
-          // (state kept in global memory, touched once per sweep: no registers held)
-          if (a.hit[b0i] < 0 && best0 >= a.target[b0i]) a.hit[b0i] = a.k_base + k;
-          if (a.hit[b1i] < 0 && best1 >= a.target[b1i]) a.hit[b1i] = a.k_base + k;
-        }
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += red[w * TS + inst(j)];
+        g[j] = s;
+        if (C > 1) a.part_val[((size_t)((k & 1) * a.tiles + tile) * C + part) * W + inst(j)] = s;
       }
     }
-    if (!last) {
-      // y_{k+1} rows must be visible to the async proxy before the producer
-      // issues sweep k+1's bulk copies
-      __threadfence();
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      named_bar(2, (NW + 1) * 32);
-    } else {
+    if (!last || C > 1) __threadfence();  // y_{k+1} rows (and the partials) visible device-wide
+    if (!last) asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and to the TMA copies of sweep k+1
+    if (C > 1) {
+      // the tile's parts meet: arrive (release) and wait for all C (acquire)
       named_bar(1, CT);
+      if (threadIdx.x == 0) {
+        atomicAdd(&a.tile_sync[tile], 1u);
+        const unsigned want = (unsigned)C * (unsigned)(k + 1);
+        while (ld_acquire_gpu(&a.tile_sync[tile]) < want) __nanosleep(64);
+      }
+      named_bar(1, CT);
+      if (warp == 0 && act) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          double s = 0.0;  // the parts' partials in part order: the same sum on every part
+          for (int p = 0; p < C; ++p) s += __ldcg(&a.part_val[((size_t)((k & 1) * a.tiles + tile) * C + p) * W + inst(j)]);
+          g[j] = s;
+        }
+      }
     }
+    if (warp == 0 && act) {
+      const bool out = part == 0;  // every part takes the same decisions; part 0 writes the outputs
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int t = inst(j);
+        const long bi = ib + t;
+        if (EVAL) {
+          if (out) a.out_val[bi] = g[j];
+        } else {
+          if (out && !last && a.hist && bi < a.B) a.hist[(size_t)k * a.B + bi] = g[j];
+          if (out && last) a.bound[bi] = g[j];
+          double best = bst[t];
+          // (stopping rule: |g_k - g_{k-1}| < tol within this call; status 2)
+          const bool chk = a.tol > 0.0 && k > 0;
+          if (!frz[t]) {
+            if (valid_bound(g[j])) {
+              best = (g[j] > best) ? g[j] : best;
+              if (chk && fabs(g[j] - gpv[t]) < a.tol) frz[t] = 2;
+            } else {
+              frz[t] = 1;
+            }
+          }
+          bst[t] = best;
+          gpv[t] = g[j];
+          // time to gap: first evaluation whose running best reaches the target
+          // (state kept in global memory, touched once per sweep: no registers held)
+          if (out && a.target && a.hit[bi] < 0 && best >= a.target[bi]) a.hit[bi] = a.k_base + k;
+        }
+      }
+    }
+    if (!last) named_bar(2, (NW + 1) * 32);  // the producer may start sweep k+1
+    else named_bar(1, CT);
   }
-  if (!EVAL && warp == 0 && act) {
-    a.best[ib + 2 * lane] = bst[2 * lane];
-    a.best[ib + 2 * lane + 1] = bst[2 * lane + 1];
-    a.status[ib + 2 * lane] = frz[2 * lane];
-    a.status[ib + 2 * lane + 1] = frz[2 * lane + 1];
+  if (!EVAL && warp == 0 && act && part == 0) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      a.best[ib + inst(j)] = bst[inst(j)];
+      a.status[ib + inst(j)] = frz[inst(j)];
+    }
   }
 }
 

@@ -45,7 +45,7 @@ class NetworkDesc(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("form", ctypes.c_int32), ("precision", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("path", ctypes.c_int32), ("single_max_batch", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("tile_parts", ctypes.c_int32), ("lane_instances", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class Info(ctypes.Structure):
@@ -58,7 +58,9 @@ class Info(ctypes.Structure):
                 ("state_on_chip", ctypes.c_int32), ("chunk", ctypes.c_int32),
                 ("ring_bus", ctypes.c_int32), ("ring_branch", ctypes.c_int32), ("tile_width", ctypes.c_int32),
                 ("copies_per_sweep", ctypes.c_int32), ("ring_life", ctypes.c_int32),
-                ("cluster_size", ctypes.c_int32)]
+                ("cluster_size", ctypes.c_int32), ("tile_parts", ctypes.c_int32),
+                ("lane_instances", ctypes.c_int32), ("halo_items", ctypes.c_int32),
+                ("steps_per_sweep", ctypes.c_int32)]
 
 
 class Optimizer(ctypes.Structure):
@@ -138,7 +140,8 @@ class DcopfDual:
     """One library handle: a network + (after set_instance_batch) a batch."""
 
     def __init__(self, net, form: int = FORM_F2, device: int = 0, path: int = PATH_AUTO,
-                 single_max_batch: int = 0, switchable=None, implied_theta: bool = False):
+                 single_max_batch: int = 0, switchable=None, implied_theta: bool = False,
+                 tile_parts: int = 0, lane_instances: int = 0):
         self.lib = load_library()
         self._keep = []
         k = lambda a, dt: (self._keep.append(np.ascontiguousarray(a, dtype=dt)) or self._keep[-1])
@@ -157,6 +160,7 @@ class DcopfDual:
         d.br_switchable = None if switchable is None else _ptr(k(switchable, np.uint8))
         o = Options()
         o.form, o.precision, o.device, o.path, o.single_max_batch = form, 64, device, path, single_max_batch
+        o.tile_parts, o.lane_instances = tile_parts, lane_instances
         h = ctypes.c_void_p()
         rc = self.lib.dcopf_dual_create(ctypes.byref(d), ctypes.byref(o), ctypes.byref(h))
         if rc != 0:

@@ -20,13 +20,17 @@ def cost_scale(net):
 
 
 def run_gpu(net, loads, outages=None, K=0, alpha=None, form=0, path=dual.PATH_AUTO, history=False,
-            lam0=None, br0=None, implied_theta=False, switchable=None, opt=None, split=None, tol=0.0):
-    """loads [B][n_bus] (instance-major, like the oracle); returns instance-major results."""
+            lam0=None, br0=None, implied_theta=False, switchable=None, opt=None, split=None, tol=0.0,
+            tile_parts=0, lane_instances=0):
+    """loads [B][n_bus] (instance-major, like the oracle); returns instance-major results.
+    tile_parts / lane_instances: dcopf_options (batched path: CTAs per tile and
+    instances per lane; cluster path: CTAs per cluster); 0 = the library's choice."""
     import torch
     dev = torch.device("cuda:0")
     loads = np.atleast_2d(loads)
     B = loads.shape[0]
-    h = dual.DcopfDual(net, form=form, path=path, implied_theta=implied_theta, switchable=switchable)
+    h = dual.DcopfDual(net, form=form, path=path, implied_theta=implied_theta, switchable=switchable,
+                       tile_parts=tile_parts, lane_instances=lane_instances)
     if tol:
         h.set_stop(tol)
     if opt is not None:  # oracle-style dict(variant=, rho=, beta1=, beta2=, eps=)

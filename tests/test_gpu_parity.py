@@ -116,15 +116,14 @@ def _oracle_full_K(config, quad, form):
 
 @pytest.mark.parametrize("C", [1, 2, 4, 8, 16])
 @pytest.mark.parametrize("form", [FORM_F2, FORM_F1])
-def test_cluster_sizes_bitwise(C, form, monkeypatch):
+def test_cluster_sizes_bitwise(C, form):
     """Every cluster size (1..16 CTAs, the partition changes) gives the same
     bits: the per-entity order never depends on the partition."""
-    monkeypatch.setenv("DCOPF_CLUSTER", str(C))
     net = inst.tiny_network(600, 900, 150, seed=3)  # fits one CTA (C = 1) as well
     K = 400
     a = inst.alpha_schedule(K, 1e-2)
     orc = oracle.solve(net, net.base_load, K=K, alpha=a, form=form, history=True)
-    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=dual.PATH_CLUSTER, history=True)
+    gpu = run_gpu(net, net.base_load, K=K, alpha=a, form=form, path=dual.PATH_CLUSTER, history=True, tile_parts=C)
     assert gpu["info"].cluster_size == C
     assert_parity(net, gpu, orc, bitwise_multipliers=True)
 
@@ -275,18 +274,27 @@ def test_divergence_isolated(path):
 
 
 def test_sharding_invariance_and_determinism():
-    """Instances never interact: 64 at once == 2 x 32 (bitwise), reruns bitwise."""
+    """Instances never interact: 64 at once == 2 x 32 == 32 x 2 (multipliers and
+    status bitwise; the dual value is a fixed-order sum per tiling, so across
+    tilings it agrees to rounding order), and reruns are bitwise."""
     net = inst.make_network(4)
     batch = inst.config4_batch(net, range(64))
     K = 60
-    a = inst.alpha_schedule(K)
+    a = inst.alpha_schedule(K, 1e-2)
     full = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, path=dual.PATH_BATCHED)
     again = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, path=dual.PATH_BATCHED)
     lo = run_gpu(net, batch.load[:32], outages=batch.outages[:32], K=K, alpha=a, path=dual.PATH_BATCHED)
     hi = run_gpu(net, batch.load[32:], outages=batch.outages[32:], K=K, alpha=a, path=dual.PATH_BATCHED)
+    pairs = [run_gpu(net, batch.load[j:j + 2], outages=batch.outages[j:j + 2], K=K, alpha=a,
+                     path=dual.PATH_BATCHED) for j in range(0, 64, 2)]
     for key in ("bound", "best", "lam", "br", "status"):
         np.testing.assert_array_equal(full[key], again[key])
-        np.testing.assert_array_equal(full[key], np.concatenate([lo[key], hi[key]]))
+    for parts in ([lo, hi], pairs):
+        for key in ("lam", "br", "status"):
+            np.testing.assert_array_equal(full[key], np.concatenate([p[key] for p in parts]))
+        for key in ("bound", "best"):
+            np.testing.assert_allclose(full[key], np.concatenate([p[key] for p in parts]), rtol=1e-12,
+                                       atol=1e-12 * cost_scale(net))
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -470,8 +478,7 @@ def test_kvl_config0(name):
 
 
 @pytest.mark.parametrize("C", [1, 4, 16])
-def test_kvl_cluster_sizes_and_outages(C, monkeypatch):
-    monkeypatch.setenv("DCOPF_CLUSTER", str(C))
+def test_kvl_cluster_sizes_and_outages(C):
     net = inst.tiny_network(600, 900, 150, seed=4)
     sw = non_tree_switchable(net)
     rng = np.random.default_rng(1)
@@ -486,7 +493,7 @@ def test_kvl_cluster_sizes_and_outages(C, monkeypatch):
     orc = oracle.solve(net, loads, outages=outs, K=K, alpha=a, form=oracle.FORM_KVL, history=True, opt=opt,
                        switchable=sw)
     gpu = run_gpu(net, loads, outages=outs, K=K, alpha=a, form=dual.FORM_KVL, history=True, opt=opt,
-                  switchable=sw)
+                  switchable=sw, tile_parts=C)
     assert gpu["info"].cluster_size == C
     assert_parity(net, gpu, orc, bitwise_multipliers=True)
 
@@ -643,7 +650,7 @@ def test_batched_more_tiles_than_sms(form):
     K = 60
     a = inst.alpha_schedule(K, 1e-2)
     gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, path=dual.PATH_BATCHED,
-                  switchable=sw)
+                  switchable=sw, tile_parts=1, lane_instances=2)
     assert gpu["info"].tile_width == 64 and gpu["info"].grid > 148
     idx = np.array([0, 63, 64, 9407, 9999])
     orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=form, switchable=sw,
@@ -667,3 +674,87 @@ def test_optimizer_batched_config4_kvl_sampled(name):
     idx = np.array([0, 77, 8191])
     orc = oracle.solve(net, batch.load[idx], K=K, alpha=a, form=oracle.FORM_KVL, switchable=sw, opt=opt, threads=3)
     assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)
+
+
+# ---------------------------------------------------------------------------
+# split tiles (split_schedule.cpp): a tile swept by C CTAs, V instances per
+# lane; every (V, C) gives the oracle's multipliers bitwise
+
+
+@pytest.mark.parametrize("form", [FORM_F2, oracle.FORM_KVL])
+@pytest.mark.parametrize("V,C", [(2, 1), (4, 1), (2, 3), (4, 2), (4, 7), (4, 16)])
+def test_split_tiles_bitwise(form, V, C):
+    """2000-bus network, 150 config-4-style instances (per-bus load factors,
+    0-3 non-tree outages, ragged last tile) at every tiling: owned items, halo
+    recomputation and the once-per-sweep meeting of the parts."""
+    net = inst.make_network(1)
+    sw = non_tree_switchable(net)
+    B = 150
+    batch = inst.config4_batch(net, range(B), total=B)
+    K = 120
+    a = inst.alpha_schedule(K, 1e-2) * np.linspace(1.0, 0.3, K)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, path=dual.PATH_BATCHED,
+                  switchable=sw, history=True, tile_parts=C, lane_instances=V)
+    info = gpu["info"]
+    assert (info.tile_parts, info.lane_instances) == (C, V)
+    assert info.grid == C * -(-B // info.tile_width)
+    orc = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, switchable=sw,
+                       history=True, threads=8)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("form", [FORM_F2, oracle.FORM_KVL])
+@pytest.mark.parametrize("B", [1024, 2048, 4096])
+def test_strong_scaling_shards_sampled(form, B):
+    """The per-GPU shards of the literal config-4 split (8192 over 8 / 4 / 2
+    GPUs) in the library's own tiling (4 instances per lane, 16 / 8 / 4 parts),
+    full K = 5000, sampled instances vs the oracle."""
+    net = inst.make_network(4)
+    sw = non_tree_switchable(net)
+    K = inst.ITERS[4]
+    batch = inst.config4_batch(net, range(B))
+    a = inst.alpha_schedule(K)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, form=form, path=dual.PATH_BATCHED,
+                  switchable=sw)
+    info = gpu["info"]
+    assert info.grid <= 148 and info.tile_parts > 1
+    idx = np.array([0, 1, B // 2 + 3, B - 1])
+    orc = oracle.solve(net, batch.load[idx], outages=batch.outages[idx], K=K, alpha=a, form=form, switchable=sw,
+                       threads=4)
+    assert_parity(net, gpu, orc, idx=idx, bitwise_multipliers=True)
+
+
+@pytest.mark.parametrize("V,C", [(4, 2), (4, 16)])
+def test_split_tiles_optimizer_and_evaluate(V, C):
+    """Adam on split tiles (state rows of owned entities only) and the
+    evaluate-only kernel (gradients written by the owning part)."""
+    import torch
+    net = inst.make_network(1)
+    sw = non_tree_switchable(net)
+    B = 64
+    batch = inst.config4_batch(net, range(B), total=B)
+    K = 150
+    opt, alpha = OPTS["adam"]
+    a = inst.alpha_schedule(K, alpha)
+    gpu = run_gpu(net, batch.load, outages=batch.outages, K=K, alpha=a, path=dual.PATH_BATCHED, switchable=sw,
+                  opt=opt, history=True, tile_parts=C, lane_instances=V)
+    orc = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=a, switchable=sw, opt=opt, history=True,
+                       threads=8)
+    assert_parity(net, gpu, orc, bitwise_multipliers=True)
+    # evaluate at the oracle's final multipliers
+    dev = torch.device("cuda:0")
+    h = dual.DcopfDual(net, path=dual.PATH_BATCHED, switchable=sw, tile_parts=C, lane_instances=V)
+    h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev),
+                         torch.from_numpy(batch.outages).to(dev))
+    h.set_multipliers(torch.from_numpy(np.ascontiguousarray(orc.lam.T)).to(dev),
+                      torch.from_numpy(np.ascontiguousarray(orc.br.T)).to(dev))
+    val = torch.empty(B, dtype=torch.float64, device=dev)
+    gl = torch.empty((net.n_bus, B), dtype=torch.float64, device=dev)
+    gb = torch.empty((net.n_branch, B), dtype=torch.float64, device=dev)
+    h.evaluate(val, gl, gb)
+    ov, ogl, ogb = oracle.evaluate(net, batch.load, orc.lam, orc.br, outages=batch.outages)[:3]
+    S = cost_scale(net)
+    assert np.all(np.abs(val.cpu().numpy() - ov) <= BOUND_RTOL * np.maximum(np.abs(ov), S))
+    np.testing.assert_array_equal(gl.cpu().numpy().T, ogl)
+    np.testing.assert_array_equal(gb.cpu().numpy().T, ogb)
+    h.close()

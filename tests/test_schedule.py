@@ -20,15 +20,19 @@ EXE = "/tmp/dcopf_sched_check"
 def checker():
     src = [os.path.join(ROOT, "tests", "sched_check.cpp"),
            os.path.join(ROOT, "paper_2406_13191_b200", "csrc", "schedule.cpp"),
+           os.path.join(ROOT, "paper_2406_13191_b200", "csrc", "split_schedule.cpp"),
            os.path.join(ROOT, "paper_2406_13191_b200", "csrc", "cluster.cpp")]
     subprocess.check_call(["g++", "-O2", "-std=c++17", "-o", EXE] + src)
     return EXE
 
 
-def run(checker, net, form, CH, P, order="dfs", W=32, life=4):
+def run(checker, net, form, CH, P, order="dfs", W=32, life=4, V=None, C=None, gap=3):
     lines = [f"{net.n_bus} {net.n_branch} {net.ref_bus} {form} {CH} {P}"]
     lines += [f"{a} {b}" for a, b in zip(net.br_from, net.br_to)]
-    res = subprocess.run([checker, order, str(W), str(life)], input="\n".join(lines) + "\n", capture_output=True, text=True)
+    args = [checker, order, str(W), str(life)]
+    if V is not None:  # the split-tile compiler (V instances per lane, C parts per tile)
+        args += [str(gap), str(V), str(C)]
+    res = subprocess.run(args, input="\n".join(lines) + "\n", capture_output=True, text=True)
     return res.returncode, res.stdout
 
 
@@ -70,3 +74,47 @@ def test_dfs_order_keeps_smem_small(checker):
         assert rc == 0 and smem <= 220 * 1024 and copies * factor < net.n_bus * 2 + net.n_branch, out
     rc, out = run(checker, net, 0, 16, 2, order="rcm", W=56, life=2)
     assert int(out.split("smem ")[1].split()[0]) > 227 * 1024, out
+
+
+# ---- split tiles (split_schedule.cpp): forms F2 (0) and KVL (2) -------------
+@pytest.mark.parametrize("config", [0, 1, 3])
+@pytest.mark.parametrize("form", [0, 2])
+@pytest.mark.parametrize("CH,P,W,life,V,C", [(26, 2, 56, 2, 2, 1), (10, 2, 112, 2, 4, 2), (10, 2, 112, 2, 4, 4),
+                                             (24, 2, 58, 2, 2, 8), (10, 1, 116, 2, 4, 16), (3, 2, 8, 0, 4, 3)])
+def test_split_schedule_valid(checker, config, form, CH, P, W, life, V, C):
+    """Every part's slot reads see the expected row / code, codes are read only
+    in a later step than the one writing them and rewritten only pool_gap steps
+    after their last read, and the owned items of the parts cover every bus,
+    branch and cycle exactly once (halo items recompute the rest)."""
+    net = inst.make_network(config)
+    if C > net.n_bus:
+        pytest.skip("more parts than buses")
+    rc, out = run(checker, net, form, CH, P, W=W, life=life, V=V, C=C)
+    assert rc == 0 and " bad 0" in out, out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_split_schedule_random_small(checker, seed):
+    rng = np.random.default_rng(100 + seed)
+    nb = int(rng.integers(2, 60))
+    nl = int(rng.integers(nb - 1, 3 * nb))
+    net = inst.tiny_network(nb, max(nl, nb - 1), 3, seed=seed)
+    for form in (0, 2):
+        for CH, P, life, V, C in ((1, 1, 0, 2, 2), (3, 2, 2, 4, 3), (16, 1, 6, 4, min(nb, 7))):
+            rc, out = run(checker, net, form, CH, P, life=life, W=8 * V, V=V, C=C)
+            assert rc == 0 and " bad 0" in out, out
+
+
+def test_split_halo_is_small_and_fits(checker):
+    """Config-3 network at the config-4 tilings the library picks (8192 instances:
+    4 per lane, 112-instance tiles over 2 parts; 1024: 116 over 16 parts): the
+    shared memory fits and the recomputed halo items are a few percent of the
+    ~32 700 items of a sweep."""
+    exe = checker
+    net = inst.make_network(3)
+    for form, CH, P, W, V, C, max_halo in ((0, 10, 2, 112, 4, 2, 40), (0, 10, 2, 116, 4, 16, 400),
+                                           (2, 22, 1, 112, 4, 2, 40), (2, 22, 1, 116, 4, 16, 400)):
+        rc, out = run(exe, net, form, CH, P, W=W, life=2, V=V, C=C)
+        smem = int(out.split("smem ")[1].split()[0])
+        halo = int(out.split("halo ")[1].split()[0])
+        assert rc == 0 and smem <= 227 * 1024 and halo <= max_halo, out
