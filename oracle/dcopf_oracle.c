@@ -533,6 +533,9 @@ int oracle_solve_opt(NET_ARGS, int form, long B, const double *load, const int *
   opt.tol = tol;
   memset(&Y, 0, sizeof Y);
   if (variant < ORC_OPT_PLAIN || variant > ORC_OPT_ADAM) return -1;
+  /* AdaGrad / Adam divide by sqrt(state) + eps with the state 0 at the start
+   * (SPEC.md:359 gives eps = 1e-8): eps <= 0 would divide 0 by 0 */
+  if ((variant == ORC_OPT_ADAGRAD || variant == ORC_OPT_ADAM) && !(eps > 0.0)) return -1;
   if (n_bus <= 0 || n_branch < 0 || n_gen < 0 || B < 0 || K < 0) return -1;
   if (form != ORC_FORM_FLOW_BOX && form != ORC_FORM_LIMIT_ROWS && form != ORC_FORM_CYCLE) return -1;
   if (form == ORC_FORM_CYCLE && build_cycles(&N, switchable, &Y) != 0) return -2;

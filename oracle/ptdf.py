@@ -186,6 +186,8 @@ def solve(net, load, K, alpha, Ha=None, lam0=None, mu0=None, opt=None, tol=0.0,
     assert alpha.shape[0] >= K
     o = dict(variant=OPT_PLAIN, rho=0.0, beta1=0.0, beta2=0.0, eps=0.0)
     o.update(opt or {})
+    if o["variant"] in (OPT_ADAGRAD, OPT_ADAM) and not o["eps"] > 0.0:
+        raise ValueError("AdaGrad / Adam need eps > 0 (SPEC.md:359: 1e-8): the state starts at 0")
     lam = np.zeros(B) if lam0 is None else np.array(lam0, dtype=np.float64).reshape(B)
     mu = np.zeros((B, 2 * nl)) if mu0 is None else np.array(mu0, dtype=np.float64).reshape(B, 2 * nl)
     sl1, sl2 = np.zeros(B), np.zeros(B)               # optimiser state (lambda)
