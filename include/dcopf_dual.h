@@ -99,9 +99,11 @@ enum { DCOPF_INST_OK = 0, DCOPF_INST_DIVERGED = 1, DCOPF_INST_CONVERGED = 2 };
 enum {
   DCOPF_PATH_AUTO = 0,    /* CLUSTER when B <= single_max_batch (SINGLE if the partition does
                              not fit), else BATCHED */
-  DCOPF_PATH_BATCHED = 1, /* tiles of W <= 64 instances (2 per lane), one CTA per tile, one
-                             persistent launch for all K iterations: a TMA-fed sweep over a
-                             host-compiled schedule of the network (DFS tree bus order) */
+  DCOPF_PATH_BATCHED = 1, /* tiles of W <= 32 V instances (V = 2 or 4 per lane), each tile swept by
+                             C = 1..16 CTAs over contiguous parts of the network (DFS tree bus
+                             order), one persistent (cooperative when C > 1) launch for all K
+                             iterations: a TMA-fed sweep over a host-compiled schedule; V, W, C
+                             chosen per batch so the launch is one wave on the SMs */
   DCOPF_PATH_SINGLE = 2,  /* one persistent CTA per instance running all K iterations on chip */
   DCOPF_PATH_CLUSTER = 3, /* one thread-block cluster of up to 16 CTAs per instance, the network
                              partitioned over the CTAs' shared memories (distributed shared
@@ -136,7 +138,10 @@ typedef struct {
   int32_t path;             /* DCOPF_PATH_* */
   int32_t single_max_batch; /* AUTO threshold; <= 0 means 128 */
   int32_t tile_parts;       /* batched path, forms F2 / KVL: CTAs per instance tile (1..16), each
-                               sweeping a contiguous part of the network; 0 = chosen per batch */
+                               sweeping a contiguous part of the network; cluster path: CTAs per
+                               instance cluster (1, 2, 4, 8, 16); 0 = chosen per batch / network.
+                               (SURVEY.md §8(b) also lists a "deterministic" flag: every path is
+                               deterministic, so it is not an option -- DESIGN.md reading A-31) */
   int32_t lane_instances;   /* batched path, forms F2 / KVL: instances per lane, 2 or 4; 0 = chosen
                                per batch (F1: always 2, one part) */
   int32_t reserved[1];      /* zero */
@@ -175,12 +180,23 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
 int dcopf_dual_iterate(dcopf_dual_t h, int64_t K, const double *alpha, double *history,
                        void *cuda_stream);
 
-/* bound[B] = g(y) at the last evaluation, best[B], status[B]; any may be NULL. */
+/* bound[B] = g(y) at the last evaluation, best[B], status[B]; any may be NULL.
+ * The bound is the dual value of Eq. 7b at the current
+ * multipliers: a valid lower bound on the optimum of Eq. 1 (weak duality,
+ * PAPER.md:135; Remarks 1-2) for any lambda, nu and mu >= 0;
+ * best is the running maximum over the iterates (Algorithm 1's gamma,
+ * PAPER.md:265).  Layout: instance b at index b (original batch order).
+ * Errors: ESTATE (no batch), ECUDA. */
 int dcopf_dual_get_bound(dcopf_dual_t h, double *bound, double *best, int32_t *status,
                          void *cuda_stream);
 
-/* lambda[n_bus][B]; branch: F2 nu[n_branch][B]; F1 mu+[n_branch][B] followed
- * by mu-[n_branch][B].  Either may be NULL. */
+/* The multipliers y_K after the last iterate() (Eq. 3: lambda
+ * for the power balance rows, and for the branch rows nu (F2, Kirchhoff
+ * f = diag(b) A theta), mu+ / mu- >= 0 (F1 and PTDF, the limit rows of Eq. 2,
+ * PAPER.md:111-118) or kappa (KVL)): lambda[n_bus][B] (PTDF: [1][B]); branch:
+ * F2 nu[n_branch][B]; F1 / PTDF mu+[n_branch][B] followed by mu-[n_branch][B];
+ * KVL kappa[n_cycles][B].  Original numbering, instance-contiguous.  Either
+ * may be NULL.  Errors: ESTATE (no batch), ECUDA. */
 int dcopf_dual_get_multipliers(dcopf_dual_t h, double *lambda, double *branch, void *cuda_stream);
 
 /* Warm start / checkpoint restore: same layouts as get_multipliers.  Any
@@ -194,8 +210,12 @@ int dcopf_dual_set_multipliers(dcopf_dual_t h, const double *lambda, const doubl
                                void *cuda_stream);
 
 /* Value and gradient at the current multipliers, no step and no change to
- * best/status: value[B], grad_lambda[n_bus][B], grad_branch (layout of
- * get_multipliers; for F1 the unprojected d g / d mu).  Any may be NULL. */
+ * best/status: value[B] = g(y) (Eq. 7b), grad_lambda[n_bus][B]
+ * and grad_branch = the constraint residuals at the inner minimiser (the
+ * gradient of the dual function, PAPER.md:245 and Alg. 1 PAPER.md:255-256 with
+ * the sign of Eq. 7b, reading A-5), in the layout of
+ * get_multipliers; for F1 the unprojected d g / d mu.  Any may be NULL.
+ * Errors: ESTATE (no batch), ECUDA, ENOMEM. */
 int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, double *grad_branch,
                         void *cuda_stream);
 
@@ -308,6 +328,17 @@ int dcopf_dual_get_ptdf(dcopf_dual_t h, double *Ha, void *cuda_stream);
 
 const char *dcopf_dual_last_error(dcopf_dual_t h); /* never NULL; h may be NULL (last create error) */
 void dcopf_dual_destroy(dcopf_dual_t h);           /* NULL is a no-op */
+
+/* Measurement-only environment variables (read by the library; never needed
+ * for correct results, each selects among variants that are all
+ * parity-tested; DESIGN.md §6 records what they measured):
+ *   DCOPF_PTDF_SKINNY=0|1   dense path: force the GEMM or the matrix-vector kernels
+ *   DCOPF_PTDF_SPLITK=0     dense path: disable the split-K GEMM1 for medium batches
+ *   DCOPF_PTDF_GROUP=n, DCOPF_PTDF_SPLIT=1|2   dense path: column-group size / stream split
+ *   DCOPF_CLUSTER_DEBUG=n   cluster path: skip phases (synchronisation floor, timing only;
+ *                           results are NOT the dual iteration when set)
+ * The batched path's tiling is an option (dcopf_options tile_parts / lane_instances), not
+ * an environment variable. */
 
 #ifdef __cplusplus
 }

@@ -36,8 +36,14 @@ static thread_local std::string g_create_error;
 
 // consumer warps of k_sweep (+1 producer warp): 2 instances per lane 19 (640
 // threads, 96 registers), 4 per lane 15 (512 threads, 128 registers)
-constexpr int kSweepWarps2 = 19;
-constexpr int kSweepWarps4 = 15;
+#ifndef DCOPF_SWEEP_WARPS2
+#define DCOPF_SWEEP_WARPS2 19
+#endif
+constexpr int kSweepWarps2 = DCOPF_SWEEP_WARPS2;
+#ifndef DCOPF_SWEEP_WARPS4
+#define DCOPF_SWEEP_WARPS4 15
+#endif
+constexpr int kSweepWarps4 = DCOPF_SWEEP_WARPS4;
 inline int sweep_warps(int V) { return V == 4 ? kSweepWarps4 : kSweepWarps2; }
 
 struct dcopf_dual_s {
@@ -321,7 +327,10 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
   // program-block stages in flight: 2, except KVL, whose steps are shorter and
   // whose shared memory is better spent on larger chunks (measured on config 4:
   // KVL 1.17e7 at P = 2 / 36-row chunks, 1.21e7 at P = 1 / 48; F2 and F1 best at 2)
-  const int P = (h->form == DCOPF_FORM_CYCLE) ? 1 : 2;
+#ifndef DCOPF_PREFETCH_F2
+#define DCOPF_PREFETCH_F2 2
+#endif
+  const int P = (h->form == DCOPF_FORM_CYCLE) ? 1 : (h->form == DCOPF_FORM_FLOW_BOX ? DCOPF_PREFETCH_F2 : 2);
   const int nw = sweep_warps(V);
   const int chs[] = {48, 40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1},
             lifes[] = {6, 4, 2};
@@ -333,7 +342,12 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
       sc.ring_life = life;
       sc.pool_gap = 3;  // soft step sync: consumer warps drift by up to two steps
       const CycleBasis *cy = h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr;
-      const std::string err = (h->form == DCOPF_FORM_LIMIT_ROWS)
+#ifdef DCOPF_UNSPLIT_BUILDER  // measurement: the unsplit compiler for F2 / KVL (V = 2, C = 1)
+      const bool unsplit = h->form == DCOPF_FORM_LIMIT_ROWS || (V == 2 && C == 1);
+#else
+      const bool unsplit = h->form == DCOPF_FORM_LIMIT_ROWS;
+#endif
+      const std::string err = unsplit
                                   ? build_schedule(h->ni, ch, P, W, nw, &sc, cy)
                                   : build_schedule_split(h->ni, ch, P, W, V, nw, C, {}, &sc, cy);
       if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
@@ -655,7 +669,7 @@ SweepArgs sweep_args(dcopf_dual_t h) {
   a.off_th = sc.off_th;
   a.off_fc = sc.off_fc;
   a.parts = h->tile_C;
-  a.part_step0 = h->d_part_step0;
+  for (int p = 0; p <= h->tile_C && p < (int)sc.part_step0.size(); ++p) a.part_step0[p] = sc.part_step0[p];
   a.tile_sync = h->d_tile_sync;
   a.part_val = h->d_part_val;
   a.tiles = (int)(h->B_pad / h->T);
@@ -917,11 +931,10 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   h->implied_box = net->theta_max == nullptr;
 
   // ---- internal numbering: bus order, branch order, CSR, generator map ----
-  const char *ord = getenv("DCOPF_ORDER");
   Internalized in;
   const std::string ierr = internalize(nb, nl, ng, net->ref_bus, fr.data(), to.data(), net->br_b, net->br_fmax,
                                        theta.data(), net->gen_bus, net->gen_pmin, net->gen_pmax, net->gen_c,
-                                       net->gen_a, net->br_switchable, h->form, ord && std::string(ord) == "rcm",
+                                       net->gen_a, net->br_switchable, h->form, /*rcm=*/false,
                                        &in);
   if (!ierr.empty()) {
     delete h;

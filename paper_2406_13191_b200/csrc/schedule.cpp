@@ -294,8 +294,8 @@ void layout_smem(Schedule &S, int nl, int nw) {
   const int RB = S.row_bytes, BR = S.br_row_bytes;
   auto al = [](int x) { return (x + 127) & ~127; };
   int off = 0;
-  S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers
-  off = al(off + 16 * S.S + 64);
+  S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers, then the part's step range (2 int)
+  off = al(off + 16 * S.S + 64 + 16);
   const int TS = 32 * S.V;  // per-tile instance slots (a lane's instances are below 32 V)
   S.off_frz = off;  // frozen flags [TS] int, then running best and previous g [TS] double
   off = al(off + 4 * TS + 2 * 8 * TS);
@@ -308,8 +308,7 @@ void layout_smem(Schedule &S, int nl, int nw) {
   // state / minimiser pools; lanes past the tile width read past a pool's
   // last slot: lane l reads 16 bytes at 16 l (and, 4 instances per lane, at
   // 4 W + 16 l) of a row of 8 W bytes
-  int pad = std::max(0, 512 + (S.V == 4 ? 4 * S.W : 0) - RB);
-  if (const char *e = getenv("DCOPF_POOL_PAD")) pad = atoi(e);  // measurement only
+  const int pad = std::max(0, 512 + (S.V == 4 ? 4 * S.W : 0) - RB);
   S.off_brp = off;
   off = al(off + S.n_br_slots * BR + pad);
   S.off_lamp = off;
@@ -575,16 +574,6 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     // A of the previous step, so the per-step maximum is what counts.
     std::vector<long> load(nw, 0);
     std::vector<uint16_t> wtab(3 * (nw + 1), 0);
-    // warps share the 4 SM sub-partitions (warp w on w % 4); the producer warp
-    // (index nw) mostly sleeps, so consumer warps on its sub-partition issue
-    // faster: their capacity is scaled by `sp` (DCOPF_SMSP_SPEED, measured)
-    std::vector<double> speed(nw, 1.0);
-    {
-      double sp = 1.0;  // measured: >1 does not help
-      if (const char *e = getenv("DCOPF_SMSP_SPEED")) sp = atof(e);
-      for (int w = 0; w < nw; ++w)
-        if (w % 4 == nw % 4) speed[w] = sp;
-    }
     auto balance = [&](auto &items, auto cost, int phase) {
       const int n = (int)items.size();
       std::vector<int> idx(n), own(n);
@@ -594,7 +583,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
         const long cx = cost(items[x]);
         int w = 0;
         for (int v = 1; v < nw; ++v)
-          if ((load[v] + cx) / speed[v] < (load[w] + cx) / speed[w]) w = v;
+          if (load[v] < load[w]) w = v;
         own[x] = w;
         load[w] += cx;
       }
@@ -611,9 +600,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
       }
     };
     // estimated issue cost (instructions per warp) of an item
-    long cw[6] = {30, f1 ? 20 : 12, f1 ? 60 : 70, 35, f1 ? 20 : 12, 25};  // A0 Adeg B C0 Cdeg Cgen
-    if (const char *e = getenv("DCOPF_COST"))  // measurement only
-      sscanf(e, "%ld,%ld,%ld,%ld,%ld,%ld", &cw[0], &cw[1], &cw[2], &cw[3], &cw[4], &cw[5]);
+    const long cw[6] = {30, f1 ? 20 : 12, f1 ? 60 : 70, 35, f1 ? 20 : 12, 25};  // A0 Adeg B C0 Cdeg Cgen
     balance(A, [&](const RecA &r) { return cw[0] + cw[1] * (r.e1 - r.e0); }, 0);
     balance(Bv, [&](const RecB &) { return cw[2]; }, 1);
     balance(Cv, [&](const RecC &r) { return cw[3] + cw[4] * (r.e1 - r.e0) + cw[5] * (r.g1 - r.g0); }, 2);
@@ -636,7 +623,7 @@ std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw,
     hd[PH_B0] = b0;
     // items are dealt round-robin to the nw consumer warps in the order A, B, C:
     // warp w starts B at (w - nA) mod nw and C at (w - nA - nB) mod nw
-    hd[PH_OFF_W] = app(wtab.data(), wtab.size() * sizeof(uint16_t));
+    hd[PH_OFF_W] = app(detail::warp_rows(wtab, nw).data(), 16 * (size_t)nw);
     hd[PH_OFF_A] = app(A.data(), A.size() * sizeof(RecA));
     hd[PH_OFF_IA] = f1 ? app(IA1.data(), IA1.size() * sizeof(RecIA1)) : app(IA2.data(), IA2.size() * sizeof(RecIA2));
     hd[PH_OFF_B] = app(Bv.data(), Bv.size() * sizeof(RecB));
@@ -873,7 +860,7 @@ std::string build_schedule_kvl(const NetInternal &net, int CH, int P, int W, int
     hd[PH_OFF_G] = app(G.data(), G.size() * sizeof(RecG));
     hd[PH_OFF_IC] = app(IC.data(), IC.size() * sizeof(RecIC2));
     hd[PH_PAD] = app(BKe.data(), BKe.size() * sizeof(RecBKe));  // KVL: cycle terms of phase B
-    hd[PH_OFF_W] = app(wtab.data(), wtab.size() * sizeof(uint16_t));
+    hd[PH_OFF_W] = app(detail::warp_rows(wtab, nw).data(), 16 * (size_t)nw);
     blk.resize((blk.size() + 15) & ~size_t(15), 0);
     hd[PH_BYTES] = (int32_t)blk.size();
     memcpy(blk.data(), hd, sizeof hd);

@@ -91,6 +91,7 @@ struct int4_t {
 };
 
 constexpr int kMaxTileW = 128;  // instances per tile: 32 lanes x up to 4 instances
+constexpr int kMaxParts = 16;   // parts (CTAs) per split tile
 
 struct Schedule {
   int CH = 0, P = 0, S = 0, W = 0, nch = 0, nsteps = 0;

@@ -511,7 +511,7 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
         hd[PH_NC] = (int)Cv.size();
         hd[PH_NIC] = (int)IC.size();
         hd[PH_NG] = (int)G.size();
-        hd[PH_OFF_W] = app(wtab.data(), wtab.size() * sizeof(uint16_t));
+        hd[PH_OFF_W] = app(detail::warp_rows(wtab, nw).data(), 16 * (size_t)nw);
         hd[PH_OFF_A] = app(A.data(), A.size() * sizeof(RecA));
         hd[PH_OFF_IA] = app(IA.data(), IA.size() * sizeof(RecIA2));
         hd[PH_OFF_B] = app(Bv.data(), Bv.size() * sizeof(RecB));
@@ -578,7 +578,7 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
         hd[PH_OFF_G] = app(G.data(), G.size() * sizeof(RecG));
         hd[PH_OFF_IC] = app(IC.data(), IC.size() * sizeof(RecIC2));
         hd[PH_PAD] = app(BKe.data(), BKe.size() * sizeof(RecBKe));  // KVL: cycle terms of phase B
-        hd[PH_OFF_W] = app(wtab.data(), wtab.size() * sizeof(uint16_t));
+        hd[PH_OFF_W] = app(detail::warp_rows(wtab, nw).data(), 16 * (size_t)nw);
       }
       blk.resize((blk.size() + 15) & ~size_t(15), 0);
       hd[PH_BYTES] = (int32_t)blk.size();

@@ -88,7 +88,8 @@ struct SweepArgs {
       off_fc;
   // split tiles
   int parts;                        // C: CTAs per tile (blockIdx.x = tile * C + part)
-  const int *part_step0;            // [C+1] first global step of each part
+  int part_step0[kMaxParts + 1];    // first global step of each part (kernel parameter space: the
+                                    // per-step loop bound is a constant-bank operand, never spilled)
   unsigned *tile_sync;              // [tiles] arrival counters, zero at launch (C > 1)
   double *part_val;                 // [2][tiles][C][W] partial dual values (C > 1)
   int tiles;
@@ -141,6 +142,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
 // nanosleep so a waiting warp issues a handful of instructions instead of
 // re-polling (its SM sub-partition's other warps keep the issue slots)
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, unsigned parity) {
+#ifdef DCOPF_CW_SUSPEND
+  mbar_wait(bar, parity);
+  return;
+#endif
   unsigned done = 0, ns = 32;
   for (;;) {
     asm volatile(
@@ -170,6 +175,19 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+// branch-free select (selp.f64): the bound selections below differ per lane,
+// and written as nested conditionals nvcc may compile them into divergent
+// branches (BSSY / BSYNC around both paths) instead of selects
+__device__ __forceinline__ double sel(bool p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r)
+      : "d"(a), "d"(b), "r"((unsigned)p));
+  return r;
+}
+// x on "up", -x on "down", 0 otherwise (x >= 0: the upper / lower box bound)
+__device__ __forceinline__ double bound_sel(bool up, bool down, double x) { return sel(up, x, sel(down, -x, 0.0)); }
 
 // the V instances of a lane
 template <int V>
@@ -236,13 +254,13 @@ __device__ __forceinline__ DV<V> ld_code(const uint8_t *base, int off, double x)
   return r;
 }
 
-#ifndef DCOPF_SWEEP_MAXREG
-#define DCOPF_SWEEP_MAXREG 96  // 20 warps x 32 x 96 + allocation granularity fit the 64K register file
-#endif
 // registers per thread: (NW + 1) warps share the 64K register file
 template <int NW>
-struct SweepRegs {
-  static constexpr int value = (NW + 1) * 32 * 128 <= 65536 ? 128 : DCOPF_SWEEP_MAXREG;
+struct SweepRegs {  // the largest multiple of 8 registers with which NW + 1 warps fit the register
+  // file: 16K registers per SM sub-partition, warps spread round-robin over the 4
+  static constexpr int per_smsp = (NW + 1 + 3) / 4;
+  static constexpr int r = 16384 / (per_smsp * 32) / 8 * 8;
+  static constexpr int value = r > 168 ? 168 : r;
 };
 
 template <int FORM, bool EVAL, int NW, bool SOFT, bool OPT, int V>
@@ -265,35 +283,44 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int W = a.W, L = W / V, hW = W >> 1, hb = 4 * W;
   const bool act = lane < L;
+  // the tile, the part and the part's step range are recomputed where they
+  // are used (per sweep) or read from shared memory (per step) instead of
+  // being held in registers across the step loop: at this register budget
+  // they are what ptxas spills first, and a spilled loop bound or stage
+  // address is a round trip to L1/L2 per step on the critical path
   const int C = a.parts;
-  const int part = (int)(blockIdx.x % (unsigned)C);
-  const size_t tile = blockIdx.x / (unsigned)C;
-  const long ib = (long)tile * W;          // first instance of the tile
+#define DCOPF_PART ((int)(blockIdx.x % (unsigned)a.parts))
+#define DCOPF_TILE ((size_t)(blockIdx.x / (unsigned)a.parts))
   const int S = a.S;
-  const int s0 = a.part_step0[part], s1 = a.part_step0[part + 1];
+  int *s_rng = reinterpret_cast<int *>(bdone + 4);  // [2] the part's first step, last step + 1
+#define DCOPF_S0 (*(volatile int *)&s_rng[0])
+#define DCOPF_S1 (*(volatile int *)&s_rng[1])
   const long K = EVAL ? 0 : a.K;
   // instance (within the tile) of this lane's j-th value
   auto inst = [&](int j) { return (j < 2) ? 2 * lane + j : hW + 2 * lane + (j - 2); };
 
   if (threadIdx.x == 0) {
+    s_rng[0] = a.part_step0[DCOPF_PART];
+    s_rng[1] = a.part_step0[DCOPF_PART + 1];
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], SOFT ? NW : 1);  // soft: one arrival per consumer warp
+      mbar_init(&empty[s], SOFT ? CT : 1);  // soft: one arrival per consumer thread
     }
-    for (int s = 0; s < 4; ++s) {
-      mbar_init(&adone[s], NW);
-      mbar_init(&bdone[s], NW);
+    for (int s = 0; s < 4; ++s) {  // (every consumer thread arrives: no __syncwarp before one lane's arrive)
+      mbar_init(&adone[s], CT);
+      mbar_init(&bdone[s], CT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int x = threadIdx.x; x < (a.n_br + 31) / 32; x += blockDim.x) obm[x] = 0u;
   for (int t = threadIdx.x; t < TS; t += blockDim.x) {
+    const long ib = (long)DCOPF_TILE * W;  // first instance of the tile
     frz[t] = (!EVAL && t < W) ? a.status[ib + t] : 0;
     bst[t] = (!EVAL && t < W) ? a.best[ib + t] : 0.0;
   }
   for (int x = threadIdx.x; x < TS * kMaxOut; x += blockDim.x) {
     const int t = x / kMaxOut, j = x % kMaxOut;
-    outs_s[x] = (t < W && j < a.max_out) ? a.outs[(ib + t) * a.max_out + j] : -1;
+    outs_s[x] = (t < W && j < a.max_out) ? a.outs[((long)DCOPF_TILE * W + t) * a.max_out + j] : -1;
   }
   __syncthreads();
   for (int x = threadIdx.x; x < TS * kMaxOut; x += blockDim.x)
@@ -312,10 +339,11 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       const int par = (a.cur + (int)(k & 1)) & 1;
+      const size_t tile = DCOPF_TILE;
       const uint8_t *lam_src = reinterpret_cast<const uint8_t *>(par ? a.lam1 : a.lam0) + tile * (size_t)a.n_bus * RB;
       const uint8_t *br_src = reinterpret_cast<const uint8_t *>(par ? a.br1 : a.br0) + tile * (size_t)a.n_brows * BR;
       const uint8_t *d_src = reinterpret_cast<const uint8_t *>(a.d) + tile * (size_t)a.n_bus * RB;
-      for (int c = s0; c < s1; ++c) {
+      for (int c = DCOPF_S0; c < DCOPF_S1; ++c) {
         const int st = pst;
         const unsigned pu = pph;  // parity of this use of stage st
         if (++pst == S) {
@@ -355,10 +383,11 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   const uint8_t *lamp = smem + a.off_lamp + lofs;
   const uint8_t *dp = smem + a.off_dp + lofs;
   // optimiser state rows of this tile (OPT kernels)
-  uint8_t *os1l = OPT ? reinterpret_cast<uint8_t *>(a.s1_lam) + tile * (size_t)a.n_bus * RB + lofs : nullptr;
-  uint8_t *os2l = OPT ? reinterpret_cast<uint8_t *>(a.s2_lam) + tile * (size_t)a.n_bus * RB + lofs : nullptr;
-  uint8_t *os1b = OPT ? reinterpret_cast<uint8_t *>(a.s1_br) + tile * (size_t)a.n_brows * BR + lofs : nullptr;
-  uint8_t *os2b = OPT ? reinterpret_cast<uint8_t *>(a.s2_br) + tile * (size_t)a.n_brows * BR + lofs : nullptr;
+  const size_t tile0 = OPT ? DCOPF_TILE : 0;
+  uint8_t *os1l = OPT ? reinterpret_cast<uint8_t *>(a.s1_lam) + tile0 * (size_t)a.n_bus * RB + lofs : nullptr;
+  uint8_t *os2l = OPT ? reinterpret_cast<uint8_t *>(a.s2_lam) + tile0 * (size_t)a.n_bus * RB + lofs : nullptr;
+  uint8_t *os1b = OPT ? reinterpret_cast<uint8_t *>(a.s1_br) + tile0 * (size_t)a.n_brows * BR + lofs : nullptr;
+  uint8_t *os2b = OPT ? reinterpret_cast<uint8_t *>(a.s2_br) + tile0 * (size_t)a.n_brows * BR + lofs : nullptr;
   const bool ost2 = OPT && a.opt == 4;  // Adam: two state arrays
   double ob1t = a.b1t, ob2t = a.b2t;
   uint8_t *thp = smem + a.off_th + V * lane;  // theta*_i code rows
@@ -374,9 +403,9 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   // B(g) likewise, then B-done(g-1) before C and D.)  Warps drift by <= 2 steps.
   unsigned gs = 0;  // global step counter (continues across sweeps; only gs mod 8 matters)
   const int nout = a.max_out;
-  const int *my_outs[V];
-#pragma unroll
-  for (int j = 0; j < V; ++j) my_outs[j] = outs_s + inst(j) * kMaxOut;
+  // (a lane's outage lists: outs_s + inst(q) * kMaxOut, formed at the rare use
+  // sites -- outaged branches only -- rather than held in registers)
+#define my_outs(q) (outs_s + inst(q) * kMaxOut)
   auto flagged = [&](int l) { return (obm[l >> 5] >> (l & 31)) & 1u; };
   auto out_t = [&](const int *lst, int l) {
     bool r = false;
@@ -390,10 +419,10 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     const bool last = (k == K);
     const bool write = EVAL || !last;
     const int par = (a.cur + (int)(k & 1)) & 1;
-    uint8_t *lam_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_lam : (par ? a.lam0 : a.lam1)) + tile * (size_t)a.n_bus * RB +
-                     lofs;
-    uint8_t *br_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_br : (par ? a.br0 : a.br1)) + tile * (size_t)a.n_brows * BR +
-                    lofs;
+    uint8_t *lam_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_lam : (par ? a.lam0 : a.lam1)) +
+                     DCOPF_TILE * (size_t)a.n_bus * RB + lofs;
+    uint8_t *br_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_br : (par ? a.br0 : a.br1)) +
+                    DCOPF_TILE * (size_t)a.n_brows * BR + lofs;
     bool stp[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) stp[j] = !EVAL && !last && !frz[inst(j)];
@@ -442,7 +471,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     bool dos[V];  // the step is taken for instance j
 #pragma unroll
     for (int j = 0; j < V; ++j) dos[j] = !CHK || stp[j];
-    for (int c = s0; c < s1; ++c) {
+    for (int c = DCOPF_S0; c < DCOPF_S1; ++c) {
       const int st = cst;
       mbar_wait(&full[st], cph);
       if (++cst == S) {
@@ -453,13 +482,16 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);  // offA offIA offB offC
       const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC bytes -
       const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // - - offW -
-      const unsigned short *wt = reinterpret_cast<const unsigned short *>(prog + h4.z);  // [3][NW+1] item ranges
+      // this warp's item ranges of the step's three phases, one 16-byte load
+      const uint4 wr = *reinterpret_cast<const uint4 *>(prog + h4.z + 16 * warp);
+      auto rng0 = [](unsigned x) { return (int)(x & 0xffffu); };
+      auto rng1 = [](unsigned x) { return (int)(x >> 16); };
 
       // ---------------- C: ready buses (F2 / F1: C(s-2), warp table 2; KVL: C(s-1), table 1) ----
-      auto phaseC = [&](int tbl) {
+      auto phaseC = [&](unsigned tr) {
         const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
         const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
-        for (int j = wt[tbl * (NW + 1) + warp], je = wt[tbl * (NW + 1) + warp + 1]; j < je; ++j) {
+        for (int j = rng0(tr), je = rng1(tr); j < je; ++j) {
           const RecC r = Cv[j];
           OState<V> ost = oload((size_t)r.wpos * RB, true, OPT && !EVAL && write && act);
           const DV<V> li = ldv<V>(lamp, r.ls, hb), di = ldv<V>(dp, r.ds, hb);
@@ -470,12 +502,24 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           for (int gg = r.g0; gg < r.g1; ++gg) {  // mostly 0 or 1 generator
             const RecG gr = G[gg];
 #pragma unroll
-            for (int q = 0; q < V; ++q) {
-              const double rr = gr.c + li.v[q];
-              const double p = gen_minimiser(rr, gr.lo, gr.hi, gr.a);
-              gl[q] = gl[q] + p;
-              if (gr.a > 0.0) v[q] += gr.a * p * p + rr * p;
-              else v[q] += rr * p;
+            if (gr.a > 0.0) {  // (warp-uniform: one generator record per warp)
+#pragma unroll
+              for (int q = 0; q < V; ++q) {
+                const double rr = gr.c + li.v[q];
+                const double x = -rr / (2.0 * gr.a);
+                const double p = sel(x < gr.lo, gr.lo, sel(x > gr.hi, gr.hi, x));  // clip(-r / (2a), lo, hi)
+                gl[q] = gl[q] + p;
+                v[q] += gr.a * p * p + rr * p;
+              }
+            } else {
+              const double mid = 0.5 * (gr.lo + gr.hi);
+#pragma unroll
+              for (int q = 0; q < V; ++q) {
+                const double rr = gr.c + li.v[q];
+                const double p = sel(rr > 0.0, gr.lo, sel(rr < 0.0, gr.hi, mid));  // bound selection, tie -> midpoint
+                gl[q] = gl[q] + p;
+                v[q] += rr * p;
+              }
             }
           }
           if (FORM != kFormF1) {
@@ -502,7 +546,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
               if (x.br >= 0 && flagged(x.br)) {
 #pragma unroll
                 for (int q = 0; q < V; ++q)
-                  if (out_t(my_outs[q], x.br)) sb[q] = copysign(0.0, sb[q]);
+                  if (out_t(my_outs(q), x.br)) sb[q] = copysign(0.0, sb[q]);
               }
               const DV<V> ts = ld_code<V>(thp, x.ts, x.ths), tt = ld_code<V>(thp, x.tt, x.tht);
 #pragma unroll
@@ -539,7 +583,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       {
         const RecBK *Bv = reinterpret_cast<const RecBK *>(prog + h2.z);
         const RecBKe *BKe = reinterpret_cast<const RecBKe *>(prog + *reinterpret_cast<const int *>(prog + 4 * PH_PAD));
-        for (int j = wt[warp], je = wt[warp + 1]; j < je; ++j) {
+        for (int j = rng0(wr.x), je = rng1(wr.x); j < je; ++j) {
           const RecBK r = Bv[j];
           double x[V], F[V];
           bool o[V];
@@ -552,7 +596,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           if (r.obr >= 0 && flagged(r.obr)) {  // an outaged lane: b = F = 0
 #pragma unroll
             for (int q = 0; q < V; ++q) {
-              o[q] = out_t(my_outs[q], r.obr);
+              o[q] = out_t(my_outs(q), r.obr);
               if (o[q]) x[q] = F[q] = 0.0;
             }
           }
@@ -571,7 +615,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #pragma unroll
           for (int q = 0; q < V; ++q) {
             const double qq = x[q] * s[q] - (ls.v[q] - lt.v[q]);
-            const double f = (qq > 0.0) ? -F[q] : ((qq < 0.0) ? F[q] : 0.0);
+            const double f = bound_sel(qq < 0.0, qq > 0.0, F[q]);  // -F if q > 0, +F if q < 0, 0 on a tie
             cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
             if (!r.halo) v[q] += qq * f;
           }
@@ -579,15 +623,15 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         }
       }
       if (SOFT) {  // C and D read the f* codes of B(<= s-1)
-        warp_arrive(&bdone[gs & 3], lane);
+        mbar_arrive(&bdone[gs & 3]);
         if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       }
-      phaseC(1);
+      phaseC(wr.y);
       // ---------------- D(s-1): d/dkappa_k = sum_l C_kl x_l f*_l, kappa' ----------------
       {
         const RecD *Dv = reinterpret_cast<const RecD *>(prog + h2.x);
         const RecDe *De = reinterpret_cast<const RecDe *>(prog + h2.y);
-        for (int j = wt[2 * (NW + 1) + warp], je = wt[2 * (NW + 1) + warp + 1]; j < je; ++j) {
+        for (int j = rng0(wr.z), je = rng1(wr.z); j < je; ++j) {
           const RecD r = Dv[j];
           OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
           const DV<V> kv = ldv<V>(brp, r.ks, hb);
@@ -610,7 +654,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           if (r.dbr >= 0 && flagged(r.dbr)) {  // defining branch out: no cycle, gradient 0
 #pragma unroll
             for (int q = 0; q < V; ++q)
-              if (out_t(my_outs[q], r.dbr)) acc[q] = 0.0;
+              if (out_t(my_outs(q), r.dbr)) acc[q] = 0.0;
           }
           if (write && act) {
             uint8_t *dst = br_o + (size_t)r.wpos * BR;
@@ -640,7 +684,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       // ---------------- A(s): w_i, theta* codes ----------------
       {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
-        for (int j = wt[warp], je = wt[warp + 1]; j < je; ++j) {
+        for (int j = rng0(wr.x), je = rng1(wr.x); j < je; ++j) {
           const RecA ra = A[j];
           double w[V];
 #pragma unroll
@@ -672,7 +716,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
               if (r.br >= 0 && flagged(r.br)) {  // br < 0: branch never taken out
 #pragma unroll
                 for (int q = 0; q < V; ++q)
-                  if (out_t(my_outs[q], r.br)) sb[q] = copysign(0.0, sb[q]);
+                  if (out_t(my_outs(q), r.br)) sb[q] = copysign(0.0, sb[q]);
               }
               const DV<V> mp = ldv<V>(brp, r.row, hb), mm = ldv<V>(brp, r.row + RB, hb);
               const DV<V> ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
@@ -687,7 +731,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           int cd[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) {
-            const double t = (nr && w[q] < 0.0) ? ra.theta : ((nr && w[q] > 0.0) ? -ra.theta : 0.0);
+            const double t = bound_sel(nr && w[q] < 0.0, nr && w[q] > 0.0, ra.theta);
             cd[q] = code_of(nr && w[q] < 0.0, nr && w[q] > 0.0);
             if (val) v[q] += w[q] * t;
           }
@@ -696,13 +740,13 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       }
       if (SOFT) {  // B(s-1) reads the theta* codes of A(<= s-1); the f* slots it writes
         // were last read 2+ steps ago, and A-done(s-1) implies every warp finished step s-2
-        warp_arrive(&adone[gs & 3], lane);
+        mbar_arrive(&adone[gs & 3]);
         if (gs > 0) mbar_wait_backoff(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       }
       // ---------------- B(s-1): branches ----------------
       {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
-        for (int j = wt[NW + 1 + warp], je = wt[NW + 2 + warp]; j < je; ++j) {
+        for (int j = rng0(wr.y), je = rng1(wr.y); j < je; ++j) {
           const RecB r = Bv[j];
           double b[V], F[V];
           bool o[V];
@@ -715,7 +759,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           if (r.obr >= 0 && flagged(r.obr)) {  // obr < 0: branch never taken out
 #pragma unroll
             for (int q = 0; q < V; ++q) {
-              o[q] = out_t(my_outs[q], r.obr);
+              o[q] = out_t(my_outs(q), r.obr);
               if (o[q]) b[q] = F[q] = 0.0;
             }
           }
@@ -746,7 +790,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             for (int q = 0; q < V; ++q) {
               const double qq = nu.v[q] - (ls.v[q] - lt.v[q]);
               // f* = -F if q > 0, +F if q < 0, 0 on a tie (an outaged lane has F = 0)
-              const double f = (qq > 0.0) ? -F[q] : ((qq < 0.0) ? F[q] : 0.0);
+              const double f = bound_sel(qq < 0.0, qq > 0.0, F[q]);
               // code for C (an outaged lane stores the tie: its f* = +-0)
               cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
               g[q] = f - phi[q];  // Kirchhoff residual
@@ -802,16 +846,16 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #pragma unroll
                   for (int q = 0; q < V; ++q)
                     if (dos[q]) {
-                      pp[q] = (yp[q] > 0.0) ? yp[q] : 0.0;  // mu <- max(mu, 0)
-                      mq[q] = (ym[q] > 0.0) ? ym[q] : 0.0;
+                      pp[q] = sel(yp[q] > 0.0, yp[q], 0.0);  // mu <- max(mu, 0)
+                      mq[q] = sel(ym[q] > 0.0, ym[q], 0.0);
                     }
                 } else {
 #pragma unroll
                   for (int q = 0; q < V; ++q)
                     if (dos[q]) {
                       const double p0 = mp.v[q] + alpha * gp[q], m0 = mm.v[q] + alpha * gm[q];
-                      pp[q] = (p0 > 0.0) ? p0 : 0.0;  // mu <- max(mu, 0)
-                      mq[q] = (m0 > 0.0) ? m0 : 0.0;
+                      pp[q] = sel(p0 > 0.0, p0, 0.0);  // mu <- max(mu, 0)
+                      mq[q] = sel(m0 > 0.0, m0, 0.0);
                     }
                 }
                 stv<V>(dst, pp, hb);
@@ -822,14 +866,14 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         }
       }
       if (SOFT) {
-        warp_arrive(&bdone[gs & 3], lane);
+        mbar_arrive(&bdone[gs & 3]);
         if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       }
-      phaseC(2);
+      phaseC(wr.z);
       }  // debug_mode
       }  // FORM
       if (SOFT) {
-        warp_arrive(&empty[st], lane);
+        mbar_arrive(&empty[st]);
       } else {  // lock-step mode: every warp finished the step
         named_bar(1, CT);
         if (threadIdx.x == 0) mbar_arrive(&empty[st]);
@@ -849,6 +893,9 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     for (int j = 0; j < V; ++j) red[warp * TS + inst(j)] = v[j];
     named_bar(1, CT);
     double g[V];
+    const int part = DCOPF_PART;
+    const size_t tile = DCOPF_TILE;
+    const long ib = (long)tile * W;
     if (warp == 0 && act) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
@@ -911,7 +958,8 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     if (!last) named_bar(2, (NW + 1) * 32);  // the producer may start sweep k+1
     else named_bar(1, CT);
   }
-  if (!EVAL && warp == 0 && act && part == 0) {
+  if (!EVAL && warp == 0 && act && DCOPF_PART == 0) {
+    const long ib = (long)DCOPF_TILE * W;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       a.best[ib + inst(j)] = bst[inst(j)];
@@ -919,5 +967,11 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     }
   }
 }
+
+#undef my_outs
+#undef DCOPF_S0
+#undef DCOPF_S1
+#undef DCOPF_PART
+#undef DCOPF_TILE
 
 }  // namespace dcopf
