@@ -86,6 +86,7 @@ struct dcopf_dual_s {
   int tile_V = 2, tile_C = 1;  // loaded batch: instances per lane, parts (CTAs) per tile
   uint8_t *d_prog = nullptr;
   int *d_part_step0 = nullptr;
+  std::vector<int> hpos_lam, hpos_d, hpos_br;  // batched layout: storage row of each original entity (host)
   unsigned *d_tile_sync = nullptr;  // split tiles: per-tile arrival counters
   double *d_part_val = nullptr;     // split tiles: per-part partial dual values [2][tiles][C][W]
   size_t tile_sync_cap = 0, part_val_cap = 0;
@@ -391,6 +392,10 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
       br_perm[p] = (h->form == DCOPF_FORM_CYCLE) ? h->sch.perm_br[p] : h->br_perm[h->sch.perm_br[p]];
       br_inv[br_perm[p]] = p;
     }
+    h->hpos_lam = lam_inv;
+    h->hpos_d.assign(nb, 0);
+    for (int p = 0; p < nb; ++p) h->hpos_d[d_perm[p]] = p;
+    h->hpos_br = br_inv;
     if (!rc) rc = upload(h, &h->d_lam_perm_b, lam_perm);
     if (!rc) rc = upload(h, &h->d_lam_inv_b, lam_inv);
     if (!rc) rc = upload(h, &h->d_d_perm_b, d_perm);
@@ -1516,11 +1521,41 @@ int dcopf_dual_compact(dcopf_dual_t h, int64_t *kept, int64_t *n_kept, void *cud
     }
     return DCOPF_OK;
   }
-  const int T = h->T;
+  // the kept instances' tiling: the batched path picks V, W, C again for the
+  // smaller batch (a shrinking branch-and-bound batch keeps the SMs busy) and
+  // moves every tile-major array into the new layout in one gather
+  const int T_old = h->T;
+  int T = T_old, nV = h->tile_V, nC = h->tile_C;
+  std::vector<int> map_lam, map_d, map_br;  // new storage row -> old storage row (identity if unchanged)
+  if (h->path == DCOPF_PATH_BATCHED) {
+    choose_tiles(h, nk, &nV, &T, &nC);
+    const std::vector<int> old_lam = h->hpos_lam, old_d = h->hpos_d, old_br = h->hpos_br;
+    if (T != T_old || nV != h->tile_V || nC != h->tile_C) {
+      if (int rc0 = compile_schedule(h, T, nV, nC)) {  // (the batch cannot be kept in either layout)
+        free_batch(h);
+        return rc0;
+      }
+    }
+    auto mk = [](const std::vector<int> &oldp, const std::vector<int> &newp) {
+      std::vector<int> m(newp.size());
+      for (size_t e = 0; e < newp.size(); ++e) m[newp[e]] = oldp[e];
+      return m;
+    };
+    map_lam = mk(old_lam, h->hpos_lam);
+    map_d = mk(old_d, h->hpos_d);
+    map_br = mk(old_br, h->hpos_br);
+  } else {
+    map_lam.resize(h->n_bus);
+    map_d.resize(h->n_bus);
+    map_br.resize(h->n_bm_ent);
+    for (int x = 0; x < h->n_bus; ++x) map_lam[x] = map_d[x] = x;
+    for (int x = 0; x < h->n_bm_ent; ++x) map_br[x] = x;
+  }
   const long B_pad = (nk + T - 1) / T * T;
   std::vector<long long> slot(B_pad, -1);
   std::copy(act.begin(), act.end(), slot.begin());
   long long *d_slot = nullptr;
+  int *d_map = nullptr;
   CK(h, cudaMalloc(&d_slot, B_pad * 8));
   int rc = DCOPF_OK;
   std::vector<void *> old;  // freed after the gathers have run
@@ -1528,26 +1563,68 @@ int dcopf_dual_compact(dcopf_dual_t h, int64_t *kept, int64_t *n_kept, void *cud
     cudaStreamSynchronize(s);
     for (void *p : old) cudaFree(p);
     cudaFree(d_slot);
+    cudaFree(d_map);
     return code;
   };
   if (cudaMemcpyAsync(d_slot, slot.data(), B_pad * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return done(fail(h, DCOPF_ECUDA, "compact: slot upload failed"));
+  // row maps on the device: [lambda | d | branch block]
+  std::vector<int> maps(map_lam);
+  maps.insert(maps.end(), map_d.begin(), map_d.end());
+  maps.insert(maps.end(), map_br.begin(), map_br.end());
+  if (cudaMalloc(&d_map, maps.size() * sizeof(int)) != cudaSuccess ||
+      cudaMemcpyAsync(d_map, maps.data(), maps.size() * sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return done(fail(h, DCOPF_ENOMEM, "compact: map upload failed"));
+  const int *m_lam = d_map, *m_d = d_map + map_lam.size(), *m_br = d_map + map_lam.size() + map_d.size();
   // tile-major state: multipliers (current buffer), loads, optimiser state
-  const int rows_br = h->n_bm_ent * h->bm_C;
+  const int nbr_ent = h->n_bm_ent;
   struct TA {
     double **p;
-    int rows;
-  } tiles[] = {{&h->lam[h->cur], h->n_bus}, {&h->br[h->cur], rows_br}, {&h->load, h->n_bus},
-               {&h->os[0], h->n_bus},       {&h->os[1], h->n_bus},      {&h->os[2], rows_br},
-               {&h->os[3], rows_br}};
+    int rows, comps;
+    const int *map;
+  } tiles[] = {{&h->lam[h->cur], h->n_bus, 1, m_lam}, {&h->br[h->cur], nbr_ent, h->bm_C, m_br},
+               {&h->load, h->n_bus, 1, m_d},           {&h->os[0], h->n_bus, 1, m_lam},
+               {&h->os[1], h->n_bus, 1, m_lam},         {&h->os[2], nbr_ent, h->bm_C, m_br},
+               {&h->os[3], nbr_ent, h->bm_C, m_br}};
   for (auto &ta : tiles) {
     if (!*ta.p) continue;
     double *nw = nullptr;
-    if (cudaMalloc(&nw, std::max<size_t>((size_t)B_pad * ta.rows, 1) * 8) != cudaSuccess)
+    if (cudaMalloc(&nw, std::max<size_t>((size_t)B_pad * ta.rows * ta.comps, 1) * 8) != cudaSuccess)
       return done(fail(h, DCOPF_ENOMEM, "compact: cudaMalloc failed"));
-    k_gather_tiles<<<grid_for((size_t)B_pad * ta.rows), 256, 0, s>>>(*ta.p, nw, ta.rows, T, d_slot, B_pad);
+    k_retile<<<grid_for((size_t)B_pad * ta.rows * ta.comps), 256, 0, s>>>(*ta.p, nw, ta.map, ta.rows, ta.comps, T_old,
+                                                                          T, d_slot, B_pad);
     old.push_back(*ta.p);
     *ta.p = nw;
+  }
+  if (h->path == DCOPF_PATH_BATCHED) {  // the ping-pong partners: contents dead, sized for the new batch
+    const int o = 1 - h->cur;
+    double *nl = nullptr, *nb = nullptr;
+    if (cudaMalloc(&nl, std::max<size_t>((size_t)B_pad * h->n_bus, 1) * 8) != cudaSuccess ||
+        cudaMalloc(&nb, std::max<size_t>((size_t)B_pad * nbr_ent * h->bm_C, 1) * 8) != cudaSuccess)
+      return done(fail(h, DCOPF_ENOMEM, "compact: cudaMalloc failed"));
+    old.push_back(h->lam[o]);
+    old.push_back(h->br[o]);
+    h->lam[o] = nl;
+    h->br[o] = nb;
+    if (nC > 1) {  // split tiles: the parts' meeting place
+      const size_t tl = (size_t)(B_pad / T), nval = 2 * tl * nC * T;
+      if (h->tile_sync_cap < tl) {
+        cudaFree(h->d_tile_sync);
+        h->d_tile_sync = nullptr;
+        h->tile_sync_cap = 0;
+        if (cudaMalloc(&h->d_tile_sync, tl * sizeof(unsigned)) != cudaSuccess)
+          return done(fail(h, DCOPF_ENOMEM, "compact: cudaMalloc failed"));
+        h->tile_sync_cap = tl;
+      }
+      if (h->part_val_cap < nval) {
+        cudaFree(h->d_part_val);
+        h->d_part_val = nullptr;
+        h->part_val_cap = 0;
+        if (cudaMalloc(&h->d_part_val, nval * sizeof(double)) != cudaSuccess)
+          return done(fail(h, DCOPF_ENOMEM, "compact: cudaMalloc failed"));
+        h->part_val_cap = nval;
+      }
+    }
   }
   // per-instance rows: bound, best, status, target, hit, outages
   auto gd = [&](double **p, double fill) -> int {
@@ -1590,6 +1667,9 @@ int dcopf_dual_compact(dcopf_dual_t h, int64_t *kept, int64_t *n_kept, void *cud
   if (!rc) {
     h->B = nk;
     h->B_pad = B_pad;
+    h->T = T;
+    h->tile_V = nV;
+    h->tile_C = nC;
   }
   return done(rc);
 }

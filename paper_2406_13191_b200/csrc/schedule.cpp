@@ -294,8 +294,10 @@ void layout_smem(Schedule &S, int nl, int nw) {
   const int RB = S.row_bytes, BR = S.br_row_bytes;
   auto al = [](int x) { return (x + 127) & ~127; };
   int off = 0;
-  S.off_bar = off;  // full[S], empty[S], A-done[4], B-done[4] mbarriers, then the part's step range (2 int)
-  off = al(off + 16 * S.S + 64 + 16);
+  // full[S], empty[S], A-done[4], B-done[4] mbarriers, then the part's step
+  // range (2 int, padded to 16 bytes), then per stage 4 item counters
+  S.off_bar = off;
+  off = al(off + 16 * S.S + 64 + 16 + 16 * S.S);
   const int TS = 32 * S.V;  // per-tile instance slots (a lane's instances are below 32 V)
   S.off_frz = off;  // frozen flags [TS] int, then running best and previous g [TS] double
   off = al(off + 4 * TS + 2 * 8 * TS);

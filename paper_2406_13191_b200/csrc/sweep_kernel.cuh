@@ -122,6 +122,9 @@ __device__ __forceinline__ void warp_arrive(uint64_t *bar, int lane) {
   __syncwarp();
   if (lane == 0) mbar_arrive(bar);
 }
+#ifndef DCOPF_L2_AHEAD
+#define DCOPF_L2_AHEAD 0  // steps ahead of the copies at which a step's rows are prefetched into L2 (0: off)
+#endif
 // try_wait suspend-time hint: a waiting warp sleeps in hardware until the phase
 // completes (or this many ns pass) instead of re-polling, so waiting warps do
 // not take issue slots from the working ones
@@ -167,6 +170,9 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void l2_prefetch(const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -188,6 +194,22 @@ __device__ __forceinline__ double sel(bool p, double a, double b) {
 }
 // x on "up", -x on "down", 0 otherwise (x >= 0: the upper / lower box bound)
 __device__ __forceinline__ double bound_sel(bool up, bool down, double x) { return sel(up, x, sel(down, -x, 0.0)); }
+// the flow-box minimiser and its code from the sign of q in one go (shared
+// predicates): f = +F, code +1 if q < 0; f = -F (nF), code -1 if q > 0; else 0
+// (a NaN q is a tie, as in the oracle's comparisons)
+__device__ __forceinline__ double flow_min(double q, double F, double nF, int &code) {
+  double f;
+  asm("{\n\t.reg .pred pu, pd;\n\t.reg .f64 t;\n\t"
+      "setp.lt.f64 pu, %2, 0d0000000000000000;\n\t"
+      "setp.gt.f64 pd, %2, 0d0000000000000000;\n\t"
+      "selp.f64 t, %4, 0d0000000000000000, pd;\n\t"
+      "selp.f64 %0, %3, t, pu;\n\t"
+      "selp.s32 %1, -1, 0, pd;\n\t"
+      "selp.s32 %1, 1, %1, pu;\n\t}"
+      : "=d"(f), "=r"(code)
+      : "d"(q), "d"(F), "d"(nF));
+  return f;
+}
 
 // the V instances of a lane
 template <int V>
@@ -293,6 +315,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #define DCOPF_TILE ((size_t)(blockIdx.x / (unsigned)a.parts))
   const int S = a.S;
   int *s_rng = reinterpret_cast<int *>(bdone + 4);  // [2] the part's first step, last step + 1
+  unsigned *icnt = reinterpret_cast<unsigned *>(s_rng + 4);  // [S][4] dynamic item counters (per stage, phase)
 #define DCOPF_S0 (*(volatile int *)&s_rng[0])
 #define DCOPF_S1 (*(volatile int *)&s_rng[1])
   const long K = EVAL ? 0 : a.K;
@@ -352,6 +375,10 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         }
         if (pused) mbar_wait(&empty[st], pu ^ 1u);  // previous use of the stage released
         if (pst == 0) pused = true;
+#ifdef DCOPF_DYNAMIC
+        if (lane < 4) icnt[4 * st + lane] = 0u;  // ordered before lane 0's release-arrive by __syncwarp
+        __syncwarp();
+#endif
         if (lane == 0) {
           mbar_arrive_expect_tx(&full[st], (unsigned)(a.debug_mode == 2 ? a.prog_bytes[c] : a.tx_bytes[c]));
           tma_load_1d(smem + a.off_prog + st * a.prog_stride, a.prog + a.prog_off[c], (unsigned)a.prog_bytes[c],
@@ -370,6 +397,20 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           else
             tma_load_1d(smem + a.off_brp + x.w * BR, br_src + (size_t)x.y * BR, x.z * BR, &full[st]);
         }
+#if DCOPF_L2_AHEAD > 0
+        // the rows of step c + DCOPF_L2_AHEAD (same sweep: y_k, final) are
+        // pulled into L2 now, so their TMA copies P steps before use hit L2
+        // instead of HBM (shared memory bounds the copy lead P, not L2)
+        if (c + DCOPF_L2_AHEAD < DCOPF_S1) {
+          const int c2 = c + DCOPF_L2_AHEAD;
+          for (int e = a.ld_ptr[c2] + lane, e2 = a.ld_ptr[c2 + 1]; e < e2; e += 32) {
+            const int4 x = a.ld[e];
+            if (x.x == LD_LAM) l2_prefetch(lam_src + (size_t)x.y * RB, x.z * RB);
+            else if (x.x == LD_D) l2_prefetch(d_src + (size_t)x.y * RB, x.z * RB);
+            else l2_prefetch(br_src + (size_t)x.y * BR, x.z * BR);
+          }
+        }
+#endif
       }
     }
     return;
@@ -479,6 +520,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         cph ^= 1u;
       }
       const uint8_t *prog = smem + a.off_prog + st * a.prog_stride;
+      const int4 h0 = *reinterpret_cast<const int4 *>(prog);       // nA nIA nB nC (KVL: nD nDe nB nC)
       const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);  // offA offIA offB offC
       const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC bytes -
       const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // - - offW -
@@ -486,12 +528,29 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       const uint4 wr = *reinterpret_cast<const uint4 *>(prog + h4.z + 16 * warp);
       auto rng0 = [](unsigned x) { return (int)(x & 0xffffu); };
       auto rng1 = [](unsigned x) { return (int)(x >> 16); };
+      unsigned *cnt_st = icnt + 4 * st;
+      (void)h0;
+      (void)cnt_st;
+#ifdef DCOPF_DYNAMIC
+      // items are taken from a per-phase counter (one shared-memory atomic per
+      // item, issued while the previous item runs) instead of the static
+      // per-warp ranges: no warp waits at the phase barrier for a straggler
+      auto grab = [&](int ph) {
+        const int t = (lane == 0) ? (int)atomicAdd(&cnt_st[ph], 1u) : 0;
+        return __shfl_sync(0xffffffffu, t, 0);
+      };
+#define ITEM_LOOP(ph, r, n)                                                                  \
+  for (int j = grab(ph), t_ = 0; j < (n); j = __shfl_sync(0xffffffffu, t_, 0))              \
+    if ((t_ = (lane == 0) ? (int)atomicAdd(&cnt_st[ph], 1u) : 0), true)
+#else
+#define ITEM_LOOP(ph, r, n) for (int j = rng0(r), je = rng1(r); j < je; ++j)
+#endif
 
       // ---------------- C: ready buses (F2 / F1: C(s-2), warp table 2; KVL: C(s-1), table 1) ----
-      auto phaseC = [&](unsigned tr) {
+      auto phaseC = [&](unsigned tr, int ph) {
         const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
         const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
-        for (int j = rng0(tr), je = rng1(tr); j < je; ++j) {
+        ITEM_LOOP(ph, tr, h0.w) {
           const RecC r = Cv[j];
           OState<V> ost = oload((size_t)r.wpos * RB, true, OPT && !EVAL && write && act);
           const DV<V> li = ldv<V>(lamp, r.ls, hb), di = ldv<V>(dp, r.ds, hb);
@@ -583,8 +642,8 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       {
         const RecBK *Bv = reinterpret_cast<const RecBK *>(prog + h2.z);
         const RecBKe *BKe = reinterpret_cast<const RecBKe *>(prog + *reinterpret_cast<const int *>(prog + 4 * PH_PAD));
-        for (int j = rng0(wr.x), je = rng1(wr.x); j < je; ++j) {
-          const RecBK r = Bv[j];
+        auto bkitem = [&](const RecBK &r, auto out_tag) {
+          constexpr bool OUT = decltype(out_tag)::value;
           double x[V], F[V];
           bool o[V];
 #pragma unroll
@@ -593,7 +652,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             F[q] = r.F;
             o[q] = false;
           }
-          if (r.obr >= 0 && flagged(r.obr)) {  // an outaged lane: b = F = 0
+          if constexpr (OUT) {  // an outaged lane: b = F = 0
 #pragma unroll
             for (int q = 0; q < V; ++q) {
               o[q] = out_t(my_outs(q), r.obr);
@@ -615,23 +674,29 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #pragma unroll
           for (int q = 0; q < V; ++q) {
             const double qq = x[q] * s[q] - (ls.v[q] - lt.v[q]);
-            const double f = bound_sel(qq < 0.0, qq > 0.0, F[q]);  // -F if q > 0, +F if q < 0, 0 on a tie
-            cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
+            int c;
+            const double f = flow_min(qq, F[q], -F[q], c);  // -F if q > 0, +F if q < 0, 0 on a tie
+            cd[q] = (OUT && o[q]) ? 0 : c;
             if (!r.halo) v[q] += qq * f;
           }
           if (act) st_codes<V>(fcp + r.fs, cd);
+        };
+        ITEM_LOOP(0, wr.x, h0.z) {
+          const RecBK r = Bv[j];
+          if (r.obr >= 0 && flagged(r.obr)) bkitem(r, std::integral_constant<bool, true>{});
+          else bkitem(r, std::integral_constant<bool, false>{});
         }
       }
       if (SOFT) {  // C and D read the f* codes of B(<= s-1)
         mbar_arrive(&bdone[gs & 3]);
         if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       }
-      phaseC(wr.y);
+      phaseC(wr.y, 1);
       // ---------------- D(s-1): d/dkappa_k = sum_l C_kl x_l f*_l, kappa' ----------------
       {
         const RecD *Dv = reinterpret_cast<const RecD *>(prog + h2.x);
         const RecDe *De = reinterpret_cast<const RecDe *>(prog + h2.y);
-        for (int j = rng0(wr.z), je = rng1(wr.z); j < je; ++j) {
+        ITEM_LOOP(2, wr.z, h0.x) {
           const RecD r = Dv[j];
           OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
           const DV<V> kv = ldv<V>(brp, r.ks, hb);
@@ -684,7 +749,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       // ---------------- A(s): w_i, theta* codes ----------------
       {
         const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
-        for (int j = rng0(wr.x), je = rng1(wr.x); j < je; ++j) {
+        ITEM_LOOP(0, wr.x, h0.x) {
           const RecA ra = A[j];
           double w[V];
 #pragma unroll
@@ -726,14 +791,18 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             }
           }
           // theta* = -Theta if w > 0, +Theta if w < 0, 0 on a tie and at the reference bus
-          const bool nr = !(ra.flags & kAFlagRef);
-          const bool val = nr && !(ra.flags & kAFlagHalo);  // a halo bus: code only
           int cd[V];
+          if (ra.flags & kAFlagRef) {  // (warp-uniform)
 #pragma unroll
-          for (int q = 0; q < V; ++q) {
-            const double t = bound_sel(nr && w[q] < 0.0, nr && w[q] > 0.0, ra.theta);
-            cd[q] = code_of(nr && w[q] < 0.0, nr && w[q] > 0.0);
-            if (val) v[q] += w[q] * t;
+            for (int q = 0; q < V; ++q) cd[q] = 0;
+          } else {
+            const bool val = !(ra.flags & kAFlagHalo);  // a halo bus: code only
+            const double nth = -ra.theta;
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              const double t = flow_min(w[q], ra.theta, nth, cd[q]);
+              if (val) v[q] += w[q] * t;
+            }
           }
           if (act) st_codes<V>(thp + ra.th, cd);
         }
@@ -746,8 +815,10 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       // ---------------- B(s-1): branches ----------------
       {
         const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
-        for (int j = rng0(wr.y), je = rng1(wr.y); j < je; ++j) {
-          const RecB r = Bv[j];
+        // one branch; OUT: some instance of the tile has it out (per-lane b = F
+        // = 0), else the warp-uniform fast path with no per-lane outage state
+        auto bitem = [&](const RecB &r, auto out_tag) {
+          constexpr bool OUT = decltype(out_tag)::value;
           double b[V], F[V];
           bool o[V];
 #pragma unroll
@@ -756,7 +827,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             F[q] = r.F;
             o[q] = false;
           }
-          if (r.obr >= 0 && flagged(r.obr)) {  // obr < 0: branch never taken out
+          if constexpr (OUT) {
 #pragma unroll
             for (int q = 0; q < V; ++q) {
               o[q] = out_t(my_outs(q), r.obr);
@@ -773,7 +844,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
               cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
             }
             if (act) st_codes<V>(fcp + r.fs, cd);
-            continue;
+            return;
           }
           OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
           OState<V> ost_m = oload((size_t)r.wpos * BR + RB, false, FORM == kFormF1 && OPT && !EVAL && write && act);
@@ -789,10 +860,11 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #pragma unroll
             for (int q = 0; q < V; ++q) {
               const double qq = nu.v[q] - (ls.v[q] - lt.v[q]);
-              // f* = -F if q > 0, +F if q < 0, 0 on a tie (an outaged lane has F = 0)
-              const double f = bound_sel(qq < 0.0, qq > 0.0, F[q]);
+              // f* = -F if q > 0, +F if q < 0, 0 on a tie (an outaged lane has F = 0);
               // code for C (an outaged lane stores the tie: its f* = +-0)
-              cd[q] = o[q] ? 0 : code_of(qq < 0.0, qq > 0.0);
+              int c;
+              const double f = flow_min(qq, F[q], -F[q], c);
+              cd[q] = (OUT && o[q]) ? 0 : c;
               g[q] = f - phi[q];  // Kirchhoff residual
               v[q] += qq * f;
             }
@@ -863,13 +935,18 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
               }
             }
           }
+        };
+        ITEM_LOOP(1, wr.y, h0.z) {
+          const RecB r = Bv[j];
+          if (r.obr >= 0 && flagged(r.obr)) bitem(r, std::integral_constant<bool, true>{});  // (obr < 0: never out)
+          else bitem(r, std::integral_constant<bool, false>{});
         }
       }
       if (SOFT) {
         mbar_arrive(&bdone[gs & 3]);
         if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
       }
-      phaseC(wr.z);
+      phaseC(wr.z, 2);
       }  // debug_mode
       }  // FORM
       if (SOFT) {
@@ -969,6 +1046,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 }
 
 #undef my_outs
+#undef ITEM_LOOP
 #undef DCOPF_S0
 #undef DCOPF_S1
 #undef DCOPF_PART

@@ -84,3 +84,57 @@ def test_compaction_no_op_cases():
     kept = h.compact()           # nothing left: the batch stays, n_kept = 0
     assert len(kept) == 0 and h.info().B == 10
     h.close()
+
+
+@pytest.mark.parametrize("form", [dual.FORM_F2, dual.FORM_KVL])
+def test_compaction_retiles_split_batch(form):
+    """A branch-and-bound-style shrink on the 10k-bus network: 2048 instances
+    (4 per lane, 8 parts per tile) compacted to about half are re-tiled (the
+    library picks 16 parts per tile for the smaller batch), so the kept
+    instances still fill the SMs.  Multipliers, status and first hits stay
+    bitwise those of the uncompacted run; the dual value is a fixed-order sum
+    per tiling, so across the re-tiling bound / best agree to rounding order."""
+    net = inst.make_network(4)
+    sw = np.zeros(net.n_branch, np.uint8)
+    sw[net.n_tree:] = 1
+    B = 2048
+    batch = inst.config4_batch(net, range(B), variant="4b")
+    K1, K2 = 40, 30
+    alpha = inst.alpha_schedule(K1 + K2, 1e-2)
+    probe = dual.DcopfDual(net, form=form, path=dual.PATH_BATCHED, switchable=sw)
+    probe.set_instance_batch(np.ascontiguousarray(batch.load.T))
+    hist = np.empty((K1, B))
+    probe.iterate(K1, alpha[:K1], hist)
+    info0 = probe.info()
+    probe.close()
+    d = np.abs(np.diff(hist, axis=0)).min(axis=0)
+    tol = float(np.quantile(d, 0.5))
+
+    def run(compact):
+        h = dual.DcopfDual(net, form=form, path=dual.PATH_BATCHED, switchable=sw)
+        h.set_stop(tol)
+        h.set_instance_batch(np.ascontiguousarray(batch.load.T))
+        h.iterate(K1, alpha[:K1])
+        kept = np.arange(B)
+        info = h.info()
+        if compact:
+            kept = h.compact()
+            info = h.info()
+        h.iterate(K2, alpha[K1:])
+        bound, best, status, lam, br = h.results_numpy()
+        hit = h.get_first_hit()
+        h.close()
+        return kept, info, dict(bound=bound, best=best, status=status, lam=lam, br=br, hit=hit)
+
+    _, _, ref = run(False)
+    kept, info, got = run(True)
+    assert 0 < len(kept) < B
+    assert info.tile_parts != info0.tile_parts  # re-tiled
+    assert info.grid * info.tile_width >= len(kept) * info.tile_parts and info.grid <= 148
+    assert info.grid > 148 // 2, "the compacted batch should still fill most SMs"
+    for k in ("status", "hit"):
+        np.testing.assert_array_equal(got[k], ref[k][kept], err_msg=k)
+    np.testing.assert_array_equal(got["lam"], ref["lam"][:, kept])
+    np.testing.assert_array_equal(got["br"], ref["br"][:, kept])
+    for k in ("bound", "best"):
+        np.testing.assert_allclose(got[k], ref[k][kept], rtol=1e-12, atol=1e-9, err_msg=k)
