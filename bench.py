@@ -4,9 +4,12 @@ on B200, in dual-ascent instance-iterations per second (BASELINE.json metric).
 
 Default workload = BASELINE.json configs[4]: the 10000-bus / 12700-branch /
 2500-generator network, 8192 load-scenario / line-switching instances, linear
-cost, form F2.  Multi-GPU default "scaling": "weak" -- every rank iterates its
-own configs[4]-sized batch (rank r: instances [8192 r, 8192 (r+1)) of the seeded
-sweep); --scaling strong splits one 8192-instance batch instead.
+cost, form F2.  Multi-GPU default "scaling": "strong" -- the literal configs[4]:
+ONE 8192-instance batch sharded over the N GPUs (rank r takes a contiguous
+shard; 1024 instances per GPU at N = 8, which the batched path covers with
+split tiles: one wave of 144 CTAs); --scaling weak gives every rank its own
+configs[4]-sized batch instead (rank r: instances [8192 r, 8192 (r+1)) of the
+seeded sweep).
 
 A "step" is one ascent iteration (S1-S4) over the rank's whole batch.  The
 timed region is one dcopf_dual_iterate(K) call = ONE persistent kernel launch
@@ -94,8 +97,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap run (the workload's full K)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: each rank its own configs[4]-sized batch (default); strong: configs[4] split")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): configs[4] split over the ranks; weak: each rank its own configs[4]-sized batch")
     ap.add_argument("--opt", default="plain", choices=sorted(OPTS),
                     help="ascent-step variant (PAPER.md:245); non-plain variants run on the cluster path")
     ap.add_argument("--alpha", type=float, default=None, help="step (default: the variant's)")

@@ -40,8 +40,12 @@
  *     instance j) of an [n_entity][B] array is at e*B + j.
  *   - A handle is not thread-safe; independent handles are independent.
  *   - Results are deterministic: identical inputs and schedule give bitwise
- *     identical outputs on the same GPU model, independent of how a batch is
- *     split across handles / GPUs (instances never interact).
+ *     identical outputs on the same GPU model.  Multipliers, status and first
+ *     hits are also bitwise independent of how a batch is split across
+ *     handles / GPUs and of the batched path's tiling (instances never
+ *     interact; every per-entity sum has the oracle's fixed order); the dual
+ *     value is a fixed-order sum per tiling, so across tilings bound / best
+ *     agree to rounding order (reading A-32).
  */
 #ifndef DCOPF_DUAL_H
 #define DCOPF_DUAL_H
@@ -136,7 +140,8 @@ typedef struct {
   int32_t precision;        /* 64 (fp64; the only mode in this build) */
   int32_t device;           /* CUDA device ordinal */
   int32_t path;             /* DCOPF_PATH_* */
-  int32_t single_max_batch; /* AUTO threshold; <= 0 means 128 */
+  int32_t single_max_batch; /* AUTO threshold (cluster path for B <= it); <= 0 means 56 (measured
+                               crossover on the 10k-bus network) */
   int32_t tile_parts;       /* batched path, forms F2 / KVL: CTAs per instance tile (1..16), each
                                sweeping a contiguous part of the network; cluster path: CTAs per
                                instance cluster (1, 2, 4, 8, 16); 0 = chosen per batch / network.

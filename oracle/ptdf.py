@@ -74,6 +74,10 @@ def ptdf(net) -> np.ndarray:
     X = np.linalg.solve(Bred, (Om @ Er).T)      # (E^T Omega E) X = (Omega E)^T, X = H^T
     Ha = np.zeros((net.n_branch, net.n_bus))
     Ha[:, keep] = X.T
+    # PTDF entries are flow fractions (|H| <= 1); below 1e-12 an entry is the
+    # solve's rounding residue of a structural zero -- no path from the bus to
+    # the slack runs through the line -- and is set to that exact 0 (reading A-30)
+    Ha[np.abs(Ha) < 1e-12] = 0.0
     return Ha
 
 

@@ -48,7 +48,7 @@ inline int sweep_warps(int V) { return V == 4 ? kSweepWarps4 : kSweepWarps2; }
 
 struct dcopf_dual_s {
   std::string err;
-  int device = 0, form = 0, path_opt = 0, single_max = 128, n_sm = 148, dev_smem = 0;
+  int device = 0, form = 0, path_opt = 0, single_max = 56, n_sm = 148, dev_smem = 0;
   int opt_parts = 0, opt_lane = 0;
   bool implied_box = false;
   int force_cluster_C = 0;          // configure_cluster: only this cluster size (0: the smallest that fits)         // theta_max was NULL: the library computed the angle box  // dcopf_options tile_parts / lane_instances (0 = chosen per batch)
@@ -418,15 +418,18 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
 }
 
 // Tile configuration of the batched path for B instances: V instances per
-// lane, W per tile, C parts (CTAs) per tile.  A warp instruction costs one
-// issue slot whatever its lane count, and an item's instructions are mostly
-// per warp (record decode, addressing, loop control) with the fp64 work per
-// instance: an item costs ~87 + 30 V issue slots (measured SASS mix, DESIGN.md
-// §5.1).  A CTA's sweep therefore costs ~(87 + 30 V) / C per item of the
-// network (plus the halo items of a split tile), whatever W is; the batch is
-// covered in ONE wave of tiles x C <= n_sm CTAs at the cheapest (V, C).  F1
-// is unsplit (V = 2, C = 1).  Batches too large for one wave use V = 4, C = 1
-// and W = 128 (several waves of whole-network tiles).
+// lane, W per tile, C parts (CTAs) per tile.  The sweep is issue-bound and a
+// warp instruction costs one issue slot whatever its lane count; measured per
+// item, the work of 4 instances per lane is ~2x that of 2 (the fp64 work per
+// instance dominates the item), and the time of a CTA's sweep is ~(V / C) x
+// (its share of the network's items) plus the halo items of a split tile.
+// The batch is covered in ONE wave of tiles x C <= n_sm CTAs at the smallest
+// estimated V / C (ties: V = 2, which affords larger chunks); F1 is unsplit
+// (V = 2, C = 1).  Batches too large for one wave use V = 4, C = 1 and W =
+// 128 (several waves of whole-network tiles).  Measured on config 4 (F2 /
+// KVL inst-it/s): 8192: V2C1 1.01e7 / 1.22e7, V4C2 1.00e7 /
+// 1.20e7; 4096: V2C2 9.5e6 / 1.20e7, V4C4 1.0e7 / 1.21e7; 2048: V2C4 9.2e6 /
+// 1.14e7, V4C8 9.5e6 / 1.11e7; 1024: V2C8 8.6e6 / 1.05e7, V4C16 8.6e6 / 1.02e7.
 void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out) {
   const long nsm = h->n_sm;
   if (h->form == DCOPF_FORM_LIMIT_ROWS) {
@@ -448,7 +451,7 @@ void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out)
       W = std::max<long>(V, (W + V - 1) / V * V);
       if (W > 32L * V) continue;
       const double halo = 1.0 + 0.02 * (C - 1);  // halo items of a split tile (measured ~1-2% per cut)
-      const double cost = (87.0 + 30.0 * V) / C * halo;
+      const double cost = (double)V / C * halo;
       if (cost < best - 1e-9) {
         best = cost;
         bV = V;
@@ -924,7 +927,11 @@ int dcopf_dual_create(const dcopf_network_desc *net, const dcopf_options *opt, d
   h->device = o.device;
   h->form = o.form;
   h->path_opt = o.path;
-  h->single_max = o.single_max_batch > 0 ? o.single_max_batch : 128;
+  // AUTO threshold: measured on config-4 instances of the 10k-bus network
+  // (tools/gpu_r2_medium.sh): one 16-CTA cluster per instance
+  // runs 9 instances at a time at ~6 us per iteration, the split-tile batched
+  // sweep any batch up to ~150 at ~50 us -- equal near B = 60
+  h->single_max = o.single_max_batch > 0 ? o.single_max_batch : 56;
   h->opt_parts = o.tile_parts;
   h->opt_lane = o.lane_instances;
   h->n_bus = nb;

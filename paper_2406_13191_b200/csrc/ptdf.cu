@@ -885,7 +885,11 @@ __global__ void k_cycle_tree(TreeDev T, const int *cp, const int *cb, const doub
   }
 }
 
-// H_a[l][i] = T[l][i] - sum_{k containing l} C_kl W[k][i]  (0 for an open branch, b = 0)
+// H_a[l][i] = T[l][i] - sum_{k containing l} C_kl W[k][i]  (0 for an open branch, b = 0).
+// PTDF entries are flow fractions, |H| <= 1; an entry below 1e-12 is a
+// rounding residue of a structural zero (no path from bus i to the slack runs
+// through l, e.g. a line into a part of the network with no injection) and is
+// stored as the exact 0 it is (reading A-30)
 __global__ void k_assemble(TreeDev T, const int *bp, const int *bk, const double *bs, const double *W, long ldw,
                            const double *b, int nl, int nb, double *Ha, long ldh) {
   for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < (long)nl * nb; id += (long)gridDim.x * blockDim.x) {
@@ -895,7 +899,7 @@ __global__ void k_assemble(TreeDev T, const int *bp, const int *bk, const double
       h = tflow(T, T.tin, l, i);
       for (int e = bp[l]; e < bp[l + 1]; ++e) h -= bs[e] * W[(size_t)bk[e] * ldw + i];
     }
-    Ha[(size_t)l * ldh + i] = h;
+    Ha[(size_t)l * ldh + i] = (fabs(h) < 1e-12) ? 0.0 : h;
   }
 }
 

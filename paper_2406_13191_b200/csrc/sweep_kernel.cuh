@@ -122,9 +122,6 @@ __device__ __forceinline__ void warp_arrive(uint64_t *bar, int lane) {
   __syncwarp();
   if (lane == 0) mbar_arrive(bar);
 }
-#ifndef DCOPF_L2_AHEAD
-#define DCOPF_L2_AHEAD 0  // steps ahead of the copies at which a step's rows are prefetched into L2 (0: off)
-#endif
 // try_wait suspend-time hint: a waiting warp sleeps in hardware until the phase
 // completes (or this many ns pass) instead of re-polling, so waiting warps do
 // not take issue slots from the working ones
@@ -169,9 +166,6 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
-}
-__device__ __forceinline__ void l2_prefetch(const void *src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -397,20 +391,6 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           else
             tma_load_1d(smem + a.off_brp + x.w * BR, br_src + (size_t)x.y * BR, x.z * BR, &full[st]);
         }
-#if DCOPF_L2_AHEAD > 0
-        // the rows of step c + DCOPF_L2_AHEAD (same sweep: y_k, final) are
-        // pulled into L2 now, so their TMA copies P steps before use hit L2
-        // instead of HBM (shared memory bounds the copy lead P, not L2)
-        if (c + DCOPF_L2_AHEAD < DCOPF_S1) {
-          const int c2 = c + DCOPF_L2_AHEAD;
-          for (int e = a.ld_ptr[c2] + lane, e2 = a.ld_ptr[c2 + 1]; e < e2; e += 32) {
-            const int4 x = a.ld[e];
-            if (x.x == LD_LAM) l2_prefetch(lam_src + (size_t)x.y * RB, x.z * RB);
-            else if (x.x == LD_D) l2_prefetch(d_src + (size_t)x.y * RB, x.z * RB);
-            else l2_prefetch(br_src + (size_t)x.y * BR, x.z * BR);
-          }
-        }
-#endif
       }
     }
     return;

@@ -238,6 +238,10 @@ def make_network(config: int, seed: int = 0, quadratic: Optional[bool] = None,
         inj = -d.copy()
         np.add.at(inj, gen_bus, pg)
         f_u = dc_flows(n, 0, br_from, br_to, br_b, inj)
+        # A-11: a structurally zero flow (a line into a part of the network with
+        # no load and no generator) is a literal zero limit; the sparse solve
+        # leaves rounding residues < 1e-12 there, against flows >= 3e-5 elsewhere
+        f_u[np.abs(f_u) < 1e-9 * np.abs(f_u).max()] = 0.0
         br_fmax = 1.3 * np.abs(f_u)
     pmin = np.zeros(n_g)
     if theta_mode is None:

@@ -72,10 +72,9 @@ def non_tree_switchable(net):
     return sw
 
 
-def assert_parity(net, gpu, orc, idx=None, check_hist=True, bitwise_multipliers=False, br_mask=None):
-    """Compare a GPU result with an oracle result (optionally on instance subset idx).
-    br_mask: optional bool [n_branch_mult], branch-block coordinates to compare
-    (the PTDF form under Adam excludes the no-flow lines of reading A-30)."""
+def assert_parity(net, gpu, orc, idx=None, check_hist=True, bitwise_multipliers=False):
+    """Compare a GPU result with an oracle result (optionally on instance subset
+    idx): every multiplier coordinate, the bound, best, status and history."""
     sel = slice(None) if idx is None else idx
     S = cost_scale(net)
     ob, obest = orc.bound, orc.best
@@ -87,8 +86,6 @@ def assert_parity(net, gpu, orc, idx=None, check_hist=True, bitwise_multipliers=
     assert np.all(np.abs(gbest[fin] - obest[fin]) <= BOUND_RTOL * np.maximum(np.abs(obest[fin]), S))
     np.testing.assert_array_equal(gpu["status"][sel], orc.status)
     gbr, obr = gpu["br"][sel], orc.br
-    if br_mask is not None:
-        gbr, obr = gbr[:, br_mask], obr[:, br_mask]
     y_g = np.concatenate([gpu["lam"][sel], gbr], axis=1)
     y_o = np.concatenate([orc.lam, obr], axis=1)
     err = np.max(np.abs(y_g - y_o), axis=1) / np.maximum(1.0, np.max(np.abs(y_o), axis=1))

@@ -129,8 +129,14 @@ def test_compaction_retiles_split_batch(form):
     _, _, ref = run(False)
     kept, info, got = run(True)
     assert 0 < len(kept) < B
-    assert info.tile_parts != info0.tile_parts  # re-tiled
-    assert info.grid * info.tile_width >= len(kept) * info.tile_parts and info.grid <= 148
+    # re-tiled as a fresh batch of the kept size would be, filling the SMs again
+    fresh = dual.DcopfDual(net, form=form, path=dual.PATH_BATCHED, switchable=sw)
+    fresh.set_instance_batch(np.ascontiguousarray(batch.load[kept].T))
+    fi = fresh.info()
+    fresh.close()
+    assert (info.lane_instances, info.tile_parts, info.tile_width, info.grid) == (
+        fi.lane_instances, fi.tile_parts, fi.tile_width, fi.grid)
+    assert (info.tile_width, info.grid) != (info0.tile_width, info0.grid)
     assert info.grid > 148 // 2, "the compacted batch should still fill most SMs"
     for k in ("status", "hit"):
         np.testing.assert_array_equal(got[k], ref[k][kept], err_msg=k)

@@ -80,6 +80,31 @@ def test_radial_network_path_flows(n_bus, seed):
     np.testing.assert_allclose(P.ptdf(net), _tree_flows(net), atol=1e-12, rtol=0)
 
 
+@pytest.mark.parametrize("n_bus,seed", [(7, 1), (25, 2), (60, 3)])
+def test_radial_structural_zeros_are_exact(n_bus, seed):
+    """A radial line carries flow for an injection at bus i iff it lies on the
+    path from i to the slack: every other entry is an exact zero (the solve's
+    rounding residues are snapped, reading A-30)."""
+    net = _net(n_bus, n_bus - 1, 3, seed)
+    np.testing.assert_array_equal(P.ptdf(net) == 0.0, _tree_flows(net) == 0.0)
+
+
+def test_injection_free_part_carries_exactly_no_flow():
+    """Config 1's lines into parts of the network with no load and no
+    generator (literal zero limits, reading A-11): zero H_g rows, zero load
+    flow and F = 0 -- all exactly, so the dual gradient on them is exactly 0."""
+    net = inst.make_network(1)
+    Ha = P.ptdf(net)
+    d = net.base_load
+    noflow = (np.abs(Ha[:, net.gen_bus]).max(axis=1) == 0.0) & (Ha @ d == 0.0)
+    assert noflow.sum() >= 20
+    assert np.all(net.br_fmax[noflow] == 0.0)
+    rng = np.random.default_rng(0)
+    mup = np.abs(rng.normal(size=(1, net.n_branch)))
+    ev = P.evaluate(net, Ha, d[None], np.full(1, -40.0), mup, mup[:, ::-1].copy())
+    assert np.all(ev.g_mup[0][noflow] == 0.0) and np.all(ev.g_mum[0][noflow] == 0.0)
+
+
 @pytest.mark.parametrize("shape", [(14, 19, 5, 0), (30, 52, 9, 4), (80, 130, 20, 7)])
 def test_kirchhoff_current_and_voltage_laws(shape):
     n, nl, ng, seed = shape
