@@ -142,13 +142,13 @@ typedef struct {
   int32_t path;             /* DCOPF_PATH_* */
   int32_t single_max_batch; /* AUTO threshold (cluster path for B <= it); <= 0 means 56 (measured
                                crossover on the 10k-bus network) */
-  int32_t tile_parts;       /* batched path, forms F2 / KVL: CTAs per instance tile (1..16), each
+  int32_t tile_parts;       /* batched path: CTAs per instance tile (1..16), each
                                sweeping a contiguous part of the network; cluster path: CTAs per
                                instance cluster (1, 2, 4, 8, 16); 0 = chosen per batch / network.
                                (SURVEY.md §8(b) also lists a "deterministic" flag: every path is
                                deterministic, so it is not an option -- DESIGN.md reading A-31) */
-  int32_t lane_instances;   /* batched path, forms F2 / KVL: instances per lane, 2 or 4; 0 = chosen
-                               per batch (F1: always 2, one part) */
+  int32_t lane_instances;   /* batched path: instances per lane, 2 or 4 (F1: 2); 0 = chosen per
+                               batch */
   int32_t reserved[1];      /* zero */
 } dcopf_options;
 

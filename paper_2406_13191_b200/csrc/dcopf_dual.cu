@@ -44,7 +44,10 @@ constexpr int kSweepWarps2 = DCOPF_SWEEP_WARPS2;
 #define DCOPF_SWEEP_WARPS4 15
 #endif
 constexpr int kSweepWarps4 = DCOPF_SWEEP_WARPS4;
-inline int sweep_warps(int V) { return V == 4 ? kSweepWarps4 : kSweepWarps2; }
+// (the optimiser variants spill a little at 96 registers with 19 warps, and
+// are still faster than with 15 warps at 128 registers: 2.9e6 vs 3.1e6
+// inst-it/s for KVL + Adam on config 4b -- latency hiding wins)
+inline int sweep_warps(int V, bool /*opt*/) { return V == 4 ? kSweepWarps4 : kSweepWarps2; }
 
 struct dcopf_dual_s {
   std::string err;
@@ -82,7 +85,7 @@ struct dcopf_dual_s {
   // compiled sweep schedule of the batched path (for tile width sched_W,
   // sched_V instances per lane, sched_C parts per tile)
   Schedule sch;
-  int sched_W = 0, sched_V = 0, sched_C = 0;
+  int sched_W = 0, sched_V = 0, sched_C = 0, sched_nw = 0;
   int tile_V = 2, tile_C = 1;  // loaded batch: instances per lane, parts (CTAs) per tile
   uint8_t *d_prog = nullptr;
   int *d_part_step0 = nullptr;
@@ -320,11 +323,16 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
 
 // Compile + upload the sweep schedule for tiles of W instances, V per lane,
 // swept by C parts: the chunk starts at the largest of the candidate chunks
-// (48 .. 1 buses) and ring lives whose kernel shared memory fits.  F2 and KVL
-// use the split-tile compiler (split_schedule.cpp; C = 1 is the unsplit
-// sweep), F1 the unsplit one (schedule.cpp; V = 2, C = 1).
+// (48 .. 1 buses) and ring lives whose kernel shared memory fits; the
+// split-tile compiler (split_schedule.cpp; C = 1 is the unsplit sweep).
 int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
-  if (h->sched_W == W && h->sched_V == V && h->sched_C == C) return DCOPF_OK;
+  const int nw = sweep_warps(V, h->opt.variant != DCOPF_OPT_PLAIN);
+  if (h->sched_W == W && h->sched_V == V && h->sched_C == C && h->sched_nw == nw) return DCOPF_OK;
+  // the same tiling for another warp count (an optimiser variant switched on
+  // or off with a batch loaded): keep the chunk and ring life, so the storage
+  // order of the loaded state -- which depends only on them -- stays valid
+  const bool keep_layout = h->sched_W == W && h->sched_V == V && h->sched_C == C && h->B > 0;
+  const int keep_ch = h->sch.CH, keep_life = h->sch.ring_life;
   // program-block stages in flight: 2, except KVL, whose steps are shorter and
   // whose shared memory is better spent on larger chunks (measured on config 4:
   // KVL 1.17e7 at P = 2 / 36-row chunks, 1.21e7 at P = 1 / 48; F2 and F1 best at 2)
@@ -332,25 +340,19 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
 #define DCOPF_PREFETCH_F2 2
 #endif
   const int P = (h->form == DCOPF_FORM_CYCLE) ? 1 : (h->form == DCOPF_FORM_FLOW_BOX ? DCOPF_PREFETCH_F2 : 2);
-  const int nw = sweep_warps(V);
   const int chs[] = {48, 40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1},
             lifes[] = {6, 4, 2};
   Schedule sc;
   bool ok = false;
   for (int ch : chs) {
+    if (keep_layout && ch != keep_ch) continue;
     for (int life : lifes) {
+      if (keep_layout && life != keep_life) continue;
       sc = Schedule();
       sc.ring_life = life;
       sc.pool_gap = 3;  // soft step sync: consumer warps drift by up to two steps
       const CycleBasis *cy = h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr;
-#ifdef DCOPF_UNSPLIT_BUILDER  // measurement: the unsplit compiler for F2 / KVL (V = 2, C = 1)
-      const bool unsplit = h->form == DCOPF_FORM_LIMIT_ROWS || (V == 2 && C == 1);
-#else
-      const bool unsplit = h->form == DCOPF_FORM_LIMIT_ROWS;
-#endif
-      const std::string err = unsplit
-                                  ? build_schedule(h->ni, ch, P, W, nw, &sc, cy)
-                                  : build_schedule_split(h->ni, ch, P, W, V, nw, C, {}, &sc, cy);
+      const std::string err = build_schedule_split(h->ni, ch, P, W, V, nw, C, {}, &sc, cy);
       if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
       if (sc.total <= h->dev_smem) {
         ok = true;
@@ -360,7 +362,7 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
     if (ok) break;
   }
   if (!ok) return fail(h, DCOPF_EINVAL, "batched schedule does not fit shared memory; use the single path");
-  h->sched_W = h->sched_V = h->sched_C = 0;  // (invalid until every upload succeeded)
+  h->sched_W = h->sched_V = h->sched_C = h->sched_nw = 0;  // (invalid until every upload succeeded)
   h->sch = sc;
   int rc = upload(h, &h->d_prog, h->sch.prog);
   if (!rc) rc = upload(h, &h->d_prog_off, h->sch.prog_off);
@@ -414,6 +416,7 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
   h->sched_W = W;
   h->sched_V = V;
   h->sched_C = C;
+  h->sched_nw = nw;
   return DCOPF_OK;
 }
 
@@ -424,24 +427,19 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
 // instance dominates the item), and the time of a CTA's sweep is ~(V / C) x
 // (its share of the network's items) plus the halo items of a split tile.
 // The batch is covered in ONE wave of tiles x C <= n_sm CTAs at the smallest
-// estimated V / C (ties: V = 2, which affords larger chunks); F1 is unsplit
-// (V = 2, C = 1).  Batches too large for one wave use V = 4, C = 1 and W =
+// estimated V / C (ties: V = 2, which affords larger chunks); F1 always runs
+// V = 2 (its mu rows are twice as wide).  Batches too large for one wave use V = 4, C = 1 and W =
 // 128 (several waves of whole-network tiles).  Measured on config 4 (F2 /
 // KVL inst-it/s): 8192: V2C1 1.01e7 / 1.22e7, V4C2 1.00e7 /
 // 1.20e7; 4096: V2C2 9.5e6 / 1.20e7, V4C4 1.0e7 / 1.21e7; 2048: V2C4 9.2e6 /
 // 1.14e7, V4C8 9.5e6 / 1.11e7; 1024: V2C8 8.6e6 / 1.05e7, V4C16 8.6e6 / 1.02e7.
 void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out) {
   const long nsm = h->n_sm;
-  if (h->form == DCOPF_FORM_LIMIT_ROWS) {
-    *V_out = 2;
-    *C_out = 1;
-    *W_out = (int)std::min<int64_t>(64, 2 * ((B + 2LL * nsm - 1) / (2LL * nsm)));
-    return;
-  }
   double best = 1e300;
   int bV = 4, bW = 128, bC = 1;
   for (int V : {2, 4})
     for (int C = 1; C <= 16; ++C) {
+      if (V == 4 && h->form == DCOPF_FORM_LIMIT_ROWS) break;  // F1: 2 per lane (its mu rows are twice as wide)
       if ((h->opt_lane && V != h->opt_lane) || (h->opt_parts && C != h->opt_parts)) continue;
       if (!h->opt_parts && C > 1 && h->n_bus < 64 * C) break;  // parts of >= 64 buses (halo stays small)
       if (C > h->n_bus) break;
@@ -460,7 +458,7 @@ void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out)
       }
     }
   if (best == 1e300) {  // more than one wave (or a forced configuration that cannot cover B in one)
-    bV = h->opt_lane ? h->opt_lane : 4;
+    bV = h->opt_lane ? h->opt_lane : (h->form == DCOPF_FORM_LIMIT_ROWS ? 2 : 4);
     bC = h->opt_parts ? h->opt_parts : 1;
     const long maxt = std::max<long>(1, nsm / bC);
     bW = (int)std::min<long>(32L * bV, std::max<long>(bV, ((B + maxt - 1) / maxt + bV - 1) / bV * bV));
@@ -702,9 +700,8 @@ SweepArgs sweep_args(dcopf_dual_t h) {
 // function and shared by every handle of the process); a split tile (C > 1)
 // is a cooperative launch, so the tile's CTAs are co-resident for the
 // once-per-sweep meeting of its parts, whose counters are zeroed first
-template <int FORM, bool EVAL, bool OPT, int V>
+template <int FORM, bool EVAL, bool OPT, int V, int NW>
 int launch_sweep_t(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
-  constexpr int NW = V == 4 ? kSweepWarps4 : kSweepWarps2;
   auto fn = k_sweep<FORM, EVAL, NW, true, OPT, V>;
   const int sm = h->sch.total;
   CK(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -726,17 +723,20 @@ int launch_sweep_t(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
 
 template <bool EVAL>
 int launch_sweep(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
+  constexpr int N2 = kSweepWarps2, N4 = kSweepWarps4;
   const bool opt = !EVAL && h->opt.variant != DCOPF_OPT_PLAIN;  // optimiser variants
   const bool v4 = h->tile_V == 4;
+  if (h->sched_nw != sweep_warps(h->tile_V, h->opt.variant != DCOPF_OPT_PLAIN))
+    return fail(h, DCOPF_ESTATE, "batched schedule compiled for another warp count");
   if (h->form == DCOPF_FORM_FLOW_BOX) {
-    if (v4) return opt ? launch_sweep_t<kFormF2, false, true, 4>(h, a, s) : launch_sweep_t<kFormF2, EVAL, false, 4>(h, a, s);
-    return opt ? launch_sweep_t<kFormF2, false, true, 2>(h, a, s) : launch_sweep_t<kFormF2, EVAL, false, 2>(h, a, s);
+    if (v4) return opt ? launch_sweep_t<kFormF2, false, true, 4, N4>(h, a, s) : launch_sweep_t<kFormF2, EVAL, false, 4, N4>(h, a, s);
+    return opt ? launch_sweep_t<kFormF2, false, true, 2, N2>(h, a, s) : launch_sweep_t<kFormF2, EVAL, false, 2, N2>(h, a, s);
   }
   if (h->form == DCOPF_FORM_CYCLE) {
-    if (v4) return opt ? launch_sweep_t<kFormKVL, false, true, 4>(h, a, s) : launch_sweep_t<kFormKVL, EVAL, false, 4>(h, a, s);
-    return opt ? launch_sweep_t<kFormKVL, false, true, 2>(h, a, s) : launch_sweep_t<kFormKVL, EVAL, false, 2>(h, a, s);
+    if (v4) return opt ? launch_sweep_t<kFormKVL, false, true, 4, N4>(h, a, s) : launch_sweep_t<kFormKVL, EVAL, false, 4, N4>(h, a, s);
+    return opt ? launch_sweep_t<kFormKVL, false, true, 2, N2>(h, a, s) : launch_sweep_t<kFormKVL, EVAL, false, 2, N2>(h, a, s);
   }
-  return opt ? launch_sweep_t<kFormF1, false, true, 2>(h, a, s) : launch_sweep_t<kFormF1, EVAL, false, 2>(h, a, s);
+  return opt ? launch_sweep_t<kFormF1, false, true, 2, N2>(h, a, s) : launch_sweep_t<kFormF1, EVAL, false, 2, N2>(h, a, s);
 }
 
 SingleArgs single_args(dcopf_dual_t h) {
@@ -1072,8 +1072,8 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
   }
   int W = 1, tV = 2, tC = 1;
   if (path == DCOPF_PATH_BATCHED) {
-    if (h->form == DCOPF_FORM_LIMIT_ROWS && (h->opt_parts > 1 || h->opt_lane == 4))
-      return fail(h, DCOPF_EINVAL, "form F1 runs unsplit tiles of 2 instances per lane on the batched path");
+    if (h->form == DCOPF_FORM_LIMIT_ROWS && h->opt_lane == 4)
+      return fail(h, DCOPF_EINVAL, "form F1 runs 2 instances per lane on the batched path");
     choose_tiles(h, B, &tV, &W, &tC);
     // a failed compile leaves sched_* invalid: the old batch (if any) is
     // dropped below before anything can use the new schedule with it
@@ -1400,6 +1400,13 @@ int dcopf_dual_set_optimizer(dcopf_dual_t h, const dcopf_optimizer *opt) {
       }
     }
   }
+  if (h->B > 0 && h->path == DCOPF_PATH_BATCHED) {  // the sweep's warp count follows the variant
+    int rc = compile_schedule(h, h->T, h->tile_V, h->tile_C);
+    if (rc) {
+      h->opt = o_old;
+      return rc;
+    }
+  }
   int rc = reset_opt_state(h, nullptr);
   if (!rc) CK(h, cudaDeviceSynchronize());
   return rc;
@@ -1469,7 +1476,7 @@ int dcopf_dual_get_info(dcopf_dual_t h, dcopf_info *info) {
   info->bandwidth = h->bandwidth;
   if (h->path == DCOPF_PATH_BATCHED) {
     info->smem_bytes = h->sch.total;
-    info->threads_per_block = (sweep_warps(h->tile_V) + 1) * 32;
+    info->threads_per_block = (h->sched_nw + 1) * 32;
     info->grid = (int)(h->B_pad / h->T) * h->tile_C;
     info->tile_parts = h->tile_C;
     info->lane_instances = h->tile_V;

@@ -1,19 +1,22 @@
-// schedule.h -- host-side compiler of the batched path's sweep schedule.
+// schedule.h -- host-side compiler of the batched path's sweep schedule
+// (schedule.cpp: internal numbering and the shared helpers; split_schedule.cpp:
+// the compiler).
 //
-// The batched kernel (pipe_kernel.cuh) sweeps each 32-instance tile once per
-// iteration in chunks of CH buses (internal order).  For every chunk this
+// The batched kernel (sweep_kernel.cuh) sweeps each tile of W instances once
+// per iteration, split over C parts (CTAs), each part in chunks of CH buses of
+// its own range of the internal (DFS tree) order.  For every step this
 // compiler emits
-//   * a "program" block: the bus / branch / ready-bus lists of the chunk's
-//     three phases with every topology constant and every shared-memory slot
-//     index they touch, laid out contiguously so one TMA bulk copy brings it
-//     on chip;
-//   * a load list: the state rows (lambda, d, nu or mu) whose first use is in
-//     this chunk, each with the shared-memory slot it is copied to.
-// Slots are assigned by greedy interval colouring over each row's live range
-// [first use - P, last use] in chunks (P = prefetch depth), so a slot is only
-// reloaded after its previous occupant's last reader finished; the number of
-// slots is the maximum overlap, which the bus order (DFS over a BFS spanning
-// tree, smallest subtree first) keeps small.
+//   * a "program" block: the item lists of the step's phases with every
+//     topology constant and every shared-memory slot index they touch, laid
+//     out contiguously so one TMA bulk copy brings it on chip;
+//   * a load list: the state rows (lambda, d, nu / mu / kappa) whose first use
+//     is in this step, each with the shared-memory slot it is copied to.
+// Slots are assigned over each row's live range [first use - P, last use] in
+// steps (P = prefetch depth): a ring for the short-lived rows (stored in HBM
+// in load order, one bulk copy per run) and interval colouring for the rest,
+// so a slot is only reloaded after its previous occupant's last reader
+// finished; the number of slots is the maximum overlap, which the bus order
+// (DFS over a BFS spanning tree, smallest subtree first) keeps small.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -144,14 +147,7 @@ std::string internalize(int nb, int nl, int ng, int ref, const int *fr, const in
 // visited smallest subtree first (keeps the live re-read window small).
 std::vector<int> dfs_tree_order(int n, const std::vector<std::vector<int>> &adj, int root);
 
-// Build the schedule for tiles of W instances (2 per lane); the sweep runs in
-// nch + 2 skewed steps: step s executes A(s), B(s-1) and C(s-2) between two
-// barriers.  Returns an empty string or an error message.
-// cyc: the cycle basis in INTERNAL branch ids (KVL form, net.form == 2), else null.
-std::string build_schedule(const NetInternal &net, int CH, int P, int W, int nw, Schedule *out,
-                           const CycleBasis *cyc = nullptr);
-
-// Split-tile schedule (forms F2 and KVL): each tile of W instances (V per
+// The sweep schedule (forms F2, F1 and KVL): each tile of W instances (V per
 // lane) is swept by C CTAs ("parts"), part p owning the internal buses
 // [cuts[p], cuts[p+1]) and the branches (KVL: also the cycles) whose larger
 // endpoint it owns.  A part recomputes, from the y_k rows in HBM, the few

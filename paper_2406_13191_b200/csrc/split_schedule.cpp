@@ -1,5 +1,5 @@
 // split_schedule.cpp -- the split-tile sweep schedule of the batched path
-// (schedule.h build_schedule_split; forms F2 and KVL).
+// (schedule.h build_schedule_split; forms F2, F1 and KVL).
 //
 // A tile of W instances is swept by C CTAs ("parts").  Part p owns the
 // internal buses [cuts[p], cuts[p+1]) (a contiguous range of the DFS tree
@@ -12,6 +12,8 @@
 // code -- and contribute nothing to the dual value:
 //   F2   halo A(j): theta*_j of a lower-part endpoint j of an owned branch;
 //        lite B(l): f*_l of a branch from an owned bus to a higher part
+//   F1   halo A(j): theta*_j of every bus of another part adjacent to an owned
+//        bus (read by B of owned branches and by C, whose d/dlambda uses phi)
 //   KVL  halo B(l): f*_l of a branch from an owned bus to a higher part (read
 //        by C) or of a lower-part branch of an owned cycle (read by D)
 // Rows the part owns are stored in HBM in its load order inside its segment
@@ -80,10 +82,10 @@ long bus_cost_f2(const NetInternal &n, int i) {
 std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, int V, int nw, int C,
                                  std::vector<int> cuts, Schedule *out, const CycleBasis *cyc) {
   Schedule &S = *out;
-  const bool kvl = net.form == 2;
-  if (net.form == 1) return "split schedule: forms F2 and KVL only";
+  const bool kvl = net.form == 2, f1 = net.form == 1;
   if (kvl && !cyc) return "KVL form needs its cycle basis";
   if (V != 2 && V != 4) return "instances per lane must be 2 or 4";
+  if (f1 && V != 2) return "form F1 runs 2 instances per lane";
   if (W < V || W > 32 * V || W % V) return "tile width must be a multiple of V in [V, 32 V]";
   const int nb = net.nb, nl = net.nl, nc = kvl ? cyc->nc : 0;
   const int nrow[3] = {nb, nb, kvl ? nc : nl};
@@ -110,10 +112,11 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
   // ---- part boundaries: balanced by estimated cost ----
   if (cuts.empty()) {
     std::vector<long> cost(nb, 0);
-    for (int i = 0; i < nb; ++i) cost[i] = kvl ? (35 + 12L * (net.bus_ptr[i + 1] - net.bus_ptr[i]) +
-                                                  25L * (net.gen_ptr[i + 1] - net.gen_ptr[i]))
-                                               : bus_cost_f2(net, i);
-    for (int l = 0; l < nl; ++l) cost[hi[l]] += kvl ? 50 + 10L * (long)bcyc[l].size() : 70;
+    for (int i = 0; i < nb; ++i) {
+      const long deg = net.bus_ptr[i + 1] - net.bus_ptr[i], gens = net.gen_ptr[i + 1] - net.gen_ptr[i];
+      cost[i] = kvl ? 35 + 12 * deg + 25 * gens : (f1 ? 65 + 40 * deg + 25 * gens : bus_cost_f2(net, i));
+    }
+    for (int l = 0; l < nl; ++l) cost[hi[l]] += kvl ? 50 + 10L * (long)bcyc[l].size() : (f1 ? 60 : 70);
     if (kvl)
       for (int k = 0; k < nc; ++k) cost[cyc_hi[k]] += 30 + 10L * (cyc->cp[k + 1] - cyc->cp[k]);
     const long tot = std::accumulate(cost.begin(), cost.end(), 0L);
@@ -136,7 +139,7 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
   S.V = V;
   S.C = C;
   S.row_bytes = 8 * W;
-  S.br_row_bytes = 8 * W;
+  S.br_row_bytes = f1 ? 16 * W : 8 * W;  // F1: mu+ then mu- in one row
   S.code_row_bytes = 32 * V;
   S.part_bus0 = cuts;
   const int RB = S.row_bytes, BR = S.br_row_bytes, CRB = S.code_row_bytes, LIFE = S.ring_life, GAP = S.pool_gap;
@@ -175,7 +178,7 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
     std::vector<int> bchunk(nl, -1), bhalo(nl, 0);
     for (int l = 0; l < nl; ++l) {
       if (own(hi[l])) bchunk[l] = chunk(hi[l]);
-      else if (own(lo[l])) {  // hi in a higher part: f* read by C(lo) here
+      else if (own(lo[l]) && !f1) {  // hi in a higher part: f* read by C(lo) here (F1 writes no f* code)
         bchunk[l] = chunk(lo[l]);
         bhalo[l] = 1;
       }
@@ -192,11 +195,21 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
           }
         }
       }
-    // ---- A (F2): owned buses at their chunk; halo theta* of lower endpoints
+    // ---- A (F2 / F1): owned buses at their chunk; halo theta* of lower
+    // endpoints of owned branches (read by B), and (F1) of every neighbour of an
+    // owned bus in another part (read by C: F1's d/dlambda uses phi from the
+    // theta* codes) -- at the earliest chunk of an owned neighbour
     if (!kvl) {
       std::vector<int> hstep(nb, INT_MAX);
-      for (int l = 0; l < nl; ++l)
-        if (own(hi[l]) && lo[l] < b0) hstep[lo[l]] = std::min(hstep[lo[l]], chunk(hi[l]));
+      for (int l = 0; l < nl; ++l) {
+        if (!f1) {
+          if (own(hi[l]) && lo[l] < b0) hstep[lo[l]] = std::min(hstep[lo[l]], chunk(hi[l]));
+        } else {
+          const int s_ = net.bs[l], t_ = net.bt[l];
+          if (own(s_) && !own(t_)) hstep[t_] = std::min(hstep[t_], chunk(s_));
+          if (own(t_) && !own(s_)) hstep[s_] = std::min(hstep[s_], chunk(t_));
+        }
+      }
       for (int i = 0; i < nb; ++i) {
         int s = -1, h = 0;
         if (own(i)) s = chunk(i);
@@ -207,7 +220,14 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
         }
         if (s < 0) continue;
         Pt.A[s].push_back({i, h});
-        for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) Pt.use[K_BR][net.bus_inc[e] >> 1].at(s);
+        for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
+          const int l = net.bus_inc[e] >> 1;
+          Pt.use[K_BR][l].at(s);
+          if (f1) {  // u_l = b ((mu+ - mu-) - (lambda_s - lambda_t))
+            Pt.use[K_LAM][net.bs[l]].at(s);
+            Pt.use[K_LAM][net.bt[l]].at(s);
+          }
+        }
         Pt.th[i].w = s;
       }
     }
@@ -217,8 +237,10 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
       const int s = bchunk[l] + off_B;
       Pt.B[s].push_back({l, bhalo[l]});
       if (bhalo[l]) ++S.halo_b;
-      Pt.use[K_LAM][net.bs[l]].at(s);
-      Pt.use[K_LAM][net.bt[l]].at(s);
+      if (!f1) {
+        Pt.use[K_LAM][net.bs[l]].at(s);
+        Pt.use[K_LAM][net.bt[l]].at(s);
+      }
       if (!kvl) {
         Pt.use[K_BR][l].at(s);
         if (!bhalo[l]) {  // phi needs theta* at both endpoints
@@ -229,7 +251,7 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
         for (auto &kc : bcyc[l])
           if (net.b[cyc->def[kc.first]] > 0.0) Pt.use[K_BR][kc.first].at(s);
       }
-      Pt.fc[l].w = s;
+      if (!f1) Pt.fc[l].w = s;
     }
     // ---- C: owned buses after every incident branch's code
     for (int i = b0; i < b1; ++i) {
@@ -241,7 +263,12 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
       Pt.use[K_D][i].at(s);
       for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
         const int l = net.bus_inc[e] >> 1;
-        Pt.fc[l].last = std::max(Pt.fc[l].last, s);
+        if (!f1) {
+          Pt.fc[l].last = std::max(Pt.fc[l].last, s);
+        } else {  // phi_l from the theta* codes of both endpoints
+          Pt.th[net.bs[l]].last = std::max(Pt.th[net.bs[l]].last, s);
+          Pt.th[net.bt[l]].last = std::max(Pt.th[net.bt[l]].last, s);
+        }
       }
     }
     // ---- D (KVL): owned cycles after their last branch
@@ -441,6 +468,7 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
       std::vector<RecC> Cv;
       std::vector<RecG> G;
       std::vector<RecIC2> IC;
+      std::vector<RecIC1> IC1;
       for (auto &it : Pt.Cc[st]) {
         const int i = it.first;
         RecC r{};
@@ -451,18 +479,30 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
         for (int g = net.gen_ptr[i]; g < net.gen_ptr[i + 1]; ++g)
           G.push_back(RecG{net.gc[g], net.glo[g], net.ghi[g], net.ga[g]});
         r.g1 = (int)G.size();
-        r.e0 = (int)IC.size();
+        r.e0 = f1 ? (int)IC1.size() : (int)IC.size();
         for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
           const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
+          if (f1) {
+            RecIC1 x{};
+            x.ts = Pt.th_slot[net.bs[l]] * CRB;
+            x.tt = Pt.th_slot[net.bt[l]] * CRB;
+            x.ths = net.theta[net.bs[l]];
+            x.tht = net.theta[net.bt[l]];
+            x.br = !has_sw || net.sw[l] ? l : -1;
+            x.sb = to ? net.b[l] : -net.b[l];  // +phi at the to bus, -phi at the from bus
+            IC1.push_back(x);
+            continue;
+          }
           const double F = (!kvl || net.b[l] > 0.0) ? net.F[l] : 0.0;  // KVL: b = 0 is an open circuit
           IC.push_back(RecIC2{Pt.f_slot[l] * CRB, l, to ? F : -F});
         }
-        r.e1 = (int)IC.size();
+        r.e1 = f1 ? (int)IC1.size() : (int)IC.size();
         Cv.push_back(r);
       }
       if (!kvl) {
         std::vector<RecA> A;
         std::vector<RecIA2> IA;
+        std::vector<RecIA1> IA1;
         for (auto &it : Pt.A[st]) {
           const int i = it.first;
           RecA r{};
@@ -470,16 +510,26 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
           r.bus = i;
           r.flags = (i == net.ref ? kAFlagRef : 0) | (it.second ? kAFlagHalo : 0);
           r.theta = net.theta[i];
-          r.e0 = (int)IA.size();
+          r.e0 = f1 ? (int)IA1.size() : (int)IA.size();
           for (int e = net.bus_ptr[i]; e < net.bus_ptr[i + 1]; ++e) {
             const int l = net.bus_inc[e] >> 1, to = net.bus_inc[e] & 1;
+            if (f1) {
+              RecIA1 x{};
+              x.row = Pt.slot[K_BR][l] * BR;
+              x.br = !has_sw || net.sw[l] ? l : -1;
+              x.ls = lam_sl(net.bs[l]);
+              x.lt = lam_sl(net.bt[l]);
+              x.sb = to ? -net.b[l] : net.b[l];  // w_s += u ; w_t -= u
+              IA1.push_back(x);
+              continue;
+            }
             RecIA2 x{};
             x.row = Pt.slot[K_BR][l] * BR;
             x.br = l;
             x.sb = to ? net.b[l] : -net.b[l];  // w_s += -(b nu) ; w_t += b nu
             IA.push_back(x);
           }
-          r.e1 = (int)IA.size();
+          r.e1 = f1 ? (int)IA1.size() : (int)IA.size();
           A.push_back(r);
         }
         std::vector<RecB> Bv;
@@ -489,9 +539,11 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
           r.row = Pt.slot[K_BR][l] * BR;
           r.wpos = it.second ? -1 - l : S.pos_br[l];
           r.obr = !has_sw || net.sw[l] ? l : -1;
-          r.ls = lam_sl(s_);
-          r.lt = lam_sl(t_);
-          r.fs = Pt.f_slot[l] * CRB;
+          if (!f1) {
+            r.ls = lam_sl(s_);
+            r.lt = lam_sl(t_);
+            r.fs = Pt.f_slot[l] * CRB;
+          }
           if (!it.second) {
             r.ts = Pt.th_slot[s_] * CRB;
             r.tt = Pt.th_slot[t_] * CRB;
@@ -502,22 +554,23 @@ std::string build_schedule_split(const NetInternal &net, int CH, int P, int W, i
           r.F = net.F[l];
           Bv.push_back(r);
         }
-        balance(A, [&](const RecA &r) { return 30L + 12L * (r.e1 - r.e0); }, 0);
-        balance(Bv, [&](const RecB &r) { return r.wpos < 0 ? 40L : 70L; }, 1);
-        balance(Cv, [&](const RecC &r) { return 35L + 12L * (r.e1 - r.e0) + 25L * (r.g1 - r.g0); }, 2);
+        const long cdeg = f1 ? 20L : 12L;
+        balance(A, [&](const RecA &r) { return 30L + cdeg * (r.e1 - r.e0); }, 0);
+        balance(Bv, [&](const RecB &r) { return r.wpos < 0 ? 40L : (f1 ? 60L : 70L); }, 1);
+        balance(Cv, [&](const RecC &r) { return 35L + cdeg * (r.e1 - r.e0) + 25L * (r.g1 - r.g0); }, 2);
         hd[PH_NA] = (int)A.size();
-        hd[PH_NIA] = (int)IA.size();
+        hd[PH_NIA] = f1 ? (int)IA1.size() : (int)IA.size();
         hd[PH_NB] = (int)Bv.size();
         hd[PH_NC] = (int)Cv.size();
-        hd[PH_NIC] = (int)IC.size();
+        hd[PH_NIC] = f1 ? (int)IC1.size() : (int)IC.size();
         hd[PH_NG] = (int)G.size();
         hd[PH_OFF_W] = app(detail::warp_rows(wtab, nw).data(), 16 * (size_t)nw);
         hd[PH_OFF_A] = app(A.data(), A.size() * sizeof(RecA));
-        hd[PH_OFF_IA] = app(IA.data(), IA.size() * sizeof(RecIA2));
+        hd[PH_OFF_IA] = f1 ? app(IA1.data(), IA1.size() * sizeof(RecIA1)) : app(IA.data(), IA.size() * sizeof(RecIA2));
         hd[PH_OFF_B] = app(Bv.data(), Bv.size() * sizeof(RecB));
         hd[PH_OFF_C] = app(Cv.data(), Cv.size() * sizeof(RecC));
         hd[PH_OFF_G] = app(G.data(), G.size() * sizeof(RecG));
-        hd[PH_OFF_IC] = app(IC.data(), IC.size() * sizeof(RecIC2));
+        hd[PH_OFF_IC] = f1 ? app(IC1.data(), IC1.size() * sizeof(RecIC1)) : app(IC.data(), IC.size() * sizeof(RecIC2));
       } else {
         std::vector<RecBK> Bv;
         std::vector<RecBKe> BKe;

@@ -160,6 +160,45 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, unsigned parity
     ns = ns < 256 ? 2 * ns : ns;
   }
 }
+// (the same operations on 32-bit shared addresses, precomputed once per kernel)
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(kSuspendNs)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_wait_backoff(unsigned bar, unsigned parity) {
+  unsigned done = 0, ns = 32;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+    ns = ns < 256 ? 2 * ns : ns;
+  }
+}
+__device__ __forceinline__ void tma_load_1d(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -214,8 +253,61 @@ template <int V>
 struct OState {  // optimiser state of a lane's instances (one row)
   double s1[V], s2[V];
 };
+// Shared memory is addressed by 32-bit shared-window addresses held in
+// registers (`sa` arguments) and read / written with explicit ld.shared /
+// st.shared: from generic pointers into the dynamic shared array nvcc
+// re-derives the window base (S2UR SR_CgaCtaId + ULEA) at many accesses of the
+// item loops, and the S2UR latency stalled ~5% of the warps' time.  The asm is
+// volatile (never moved across the mbarrier waits, which are volatile asm).
+__device__ __forceinline__ double2 lds_f64x2(unsigned sa) {
+  return *reinterpret_cast<const double2 *>(__cvta_shared_to_generic((size_t)sa));
+}
+__device__ __forceinline__ uint4 lds_u32x4(unsigned sa) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(sa));
+  return r;
+}
+__device__ __forceinline__ uint2 lds_u32x2(unsigned sa) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(sa));
+  return r;
+}
+__device__ __forceinline__ unsigned lds_u16(unsigned sa) {
+  return *reinterpret_cast<const unsigned short *>(__cvta_shared_to_generic((size_t)sa));
+}
+__device__ __forceinline__ unsigned lds_u32(unsigned sa) {
+  return *reinterpret_cast<const unsigned *>(__cvta_shared_to_generic((size_t)sa));
+}
+__device__ __forceinline__ void sts_u16(unsigned sa, unsigned v) {
+  *reinterpret_cast<unsigned short *>(__cvta_shared_to_generic((size_t)sa)) = (unsigned short)v;
+}
+__device__ __forceinline__ void sts_u32(unsigned sa, unsigned v) {
+  *reinterpret_cast<unsigned *>(__cvta_shared_to_generic((size_t)sa)) = v;
+}
+// a program-block record by value: a plain load through a generic pointer
+// formed from the 32-bit shared address (the compiler folds the conversion
+// back into shared loads of just the fields used, with the window base kept
+// in a uniform register)
+template <class T>
+__device__ __forceinline__ T lds_rec(unsigned sa) {
+  return *reinterpret_cast<const T *>(__cvta_shared_to_generic((size_t)sa));
+}
+
 // row loads / stores: instances 2l, 2l+1 at byte 16 l of the row (folded into
-// the base pointer), instances W/2 + 2l, W/2 + 2l + 1 hb = 4 W bytes further
+// the base address), instances W/2 + 2l, W/2 + 2l + 1 hb = 4 W bytes further
+template <int V>
+__device__ __forceinline__ DV<V> ldsv(unsigned base, int off, int hb) {
+  DV<V> r;
+  const double2 a = lds_f64x2(base + off);
+  r.v[0] = a.x;
+  r.v[1] = a.y;
+  if constexpr (V == 4) {
+    const double2 b = lds_f64x2(base + off + hb);
+    r.v[2] = b.x;
+    r.v[3] = b.y;
+  }
+  return r;
+}
 template <int V>
 __device__ __forceinline__ DV<V> ldv(const uint8_t *base, int off, int hb) {
   DV<V> r;
@@ -239,29 +331,28 @@ __device__ __forceinline__ void stv(void *p, const double (&x)[V], int hb) {
 // the base pointer); value = code * bound, exact for codes in {-1, 0, 1}
 __device__ __forceinline__ int code_of(bool up, bool down) { return up ? 1 : (down ? -1 : 0); }
 template <int V>
-__device__ __forceinline__ void st_codes(uint8_t *p, const int (&c)[V]) {
+__device__ __forceinline__ void st_codes(unsigned sa, const int (&c)[V]) {
   if constexpr (V == 2) {
-    *reinterpret_cast<unsigned short *>(p) = (unsigned short)((c[0] & 0xff) | ((c[1] & 0xff) << 8));
+    sts_u16(sa, (unsigned)((c[0] & 0xff) | ((c[1] & 0xff) << 8)));
   } else {
-    *reinterpret_cast<unsigned *>(p) =
-        (unsigned)(c[0] & 0xff) | ((unsigned)(c[1] & 0xff) << 8) | ((unsigned)(c[2] & 0xff) << 16) |
-        ((unsigned)(c[3] & 0xff) << 24);
+    sts_u32(sa, (unsigned)(c[0] & 0xff) | ((unsigned)(c[1] & 0xff) << 8) | ((unsigned)(c[2] & 0xff) << 16) |
+                    ((unsigned)(c[3] & 0xff) << 24));
   }
 }
 template <int V>
-__device__ __forceinline__ void ld_codes(const uint8_t *base, int off, int (&c)[V]) {
+__device__ __forceinline__ void ld_codes(unsigned base, int off, int (&c)[V]) {
   if constexpr (V == 2) {
-    const unsigned u = *reinterpret_cast<const unsigned short *>(base + off);
+    const unsigned u = lds_u16(base + off);
     c[0] = (int)(signed char)(u & 0xffu);
     c[1] = (int)(signed char)(u >> 8);
   } else {
-    const unsigned u = *reinterpret_cast<const unsigned *>(base + off);
+    const unsigned u = lds_u32(base + off);
 #pragma unroll
     for (int j = 0; j < 4; ++j) c[j] = (int)(signed char)((u >> (8 * j)) & 0xffu);
   }
 }
 template <int V>
-__device__ __forceinline__ DV<V> ld_code(const uint8_t *base, int off, double x) {
+__device__ __forceinline__ DV<V> ld_code(unsigned base, int off, double x) {
   int c[V];
   ld_codes<V>(base, off, c);
   DV<V> r;
@@ -286,6 +377,9 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   uint64_t *empty = full + a.S;
   uint64_t *adone = empty + a.S;  // [4] all consumer threads finished phase A of step g (slot g & 3)
   uint64_t *bdone = adone + 4;    // [4] ... phase B of step g
+  const unsigned sbase = smem_u32(smem);  // 32-bit shared addresses of the pools and barriers
+  const unsigned full_sa = sbase + a.off_bar, empty_sa = full_sa + 8 * a.S, adone_sa = empty_sa + 8 * a.S,
+                 bdone_sa = adone_sa + 32;
   constexpr int TS = 32 * V;  // per-tile instance slots (schedule.cpp layout_smem)
   double *red = reinterpret_cast<double *>(smem + a.off_red);   // [NW][TS]
   int *frz = reinterpret_cast<int *>(smem + a.off_frz);         // [TS]
@@ -309,9 +403,8 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #define DCOPF_TILE ((size_t)(blockIdx.x / (unsigned)a.parts))
   const int S = a.S;
   int *s_rng = reinterpret_cast<int *>(bdone + 4);  // [2] the part's first step, last step + 1
-  unsigned *icnt = reinterpret_cast<unsigned *>(s_rng + 4);  // [S][4] dynamic item counters (per stage, phase)
-#define DCOPF_S0 (*(volatile int *)&s_rng[0])
-#define DCOPF_S1 (*(volatile int *)&s_rng[1])
+#define DCOPF_S0 ((int)lds_u32(bdone_sa + 32))
+#define DCOPF_S1 ((int)lds_u32(bdone_sa + 36))
   const long K = EVAL ? 0 : a.K;
   // instance (within the tile) of this lane's j-th value
   auto inst = [&](int j) { return (j < 2) ? 2 * lane + j : hW + 2 * lane + (j - 2); };
@@ -367,16 +460,12 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           pst = 0;
           pph ^= 1u;
         }
-        if (pused) mbar_wait(&empty[st], pu ^ 1u);  // previous use of the stage released
+        if (pused) mbar_wait(empty_sa + 8 * st, pu ^ 1u);  // previous use of the stage released
         if (pst == 0) pused = true;
-#ifdef DCOPF_DYNAMIC
-        if (lane < 4) icnt[4 * st + lane] = 0u;  // ordered before lane 0's release-arrive by __syncwarp
-        __syncwarp();
-#endif
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[st], (unsigned)(a.debug_mode == 2 ? a.prog_bytes[c] : a.tx_bytes[c]));
-          tma_load_1d(smem + a.off_prog + st * a.prog_stride, a.prog + a.prog_off[c], (unsigned)a.prog_bytes[c],
-                      &full[st]);
+          mbar_arrive_expect_tx(full_sa + 8 * st, (unsigned)(a.debug_mode == 2 ? a.prog_bytes[c] : a.tx_bytes[c]));
+          tma_load_1d(sbase + a.off_prog + st * a.prog_stride, a.prog + a.prog_off[c], (unsigned)a.prog_bytes[c],
+                      full_sa + 8 * st);
         }
         __syncwarp();
         // each entry is one bulk copy of `rows` consecutive rows (storage
@@ -385,11 +474,11 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         for (int e = a.ld_ptr[c] + lane; e < e1; e += 32) {
           const int4 x = a.ld[e];
           if (x.x == LD_LAM)
-            tma_load_1d(smem + a.off_lamp + x.w * RB, lam_src + (size_t)x.y * RB, x.z * RB, &full[st]);
+            tma_load_1d(sbase + a.off_lamp + x.w * RB, lam_src + (size_t)x.y * RB, x.z * RB, full_sa + 8 * st);
           else if (x.x == LD_D)
-            tma_load_1d(smem + a.off_dp + x.w * RB, d_src + (size_t)x.y * RB, x.z * RB, &full[st]);
+            tma_load_1d(sbase + a.off_dp + x.w * RB, d_src + (size_t)x.y * RB, x.z * RB, full_sa + 8 * st);
           else
-            tma_load_1d(smem + a.off_brp + x.w * BR, br_src + (size_t)x.y * BR, x.z * BR, &full[st]);
+            tma_load_1d(sbase + a.off_brp + x.w * BR, br_src + (size_t)x.y * BR, x.z * BR, full_sa + 8 * st);
         }
       }
     }
@@ -400,9 +489,9 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   const int RB = a.row_bytes, BR = a.br_row_bytes;
   // lanes past the tile width read the pools' tail padding and never store
   const int lofs = lane * 16;
-  const uint8_t *brp = smem + a.off_brp + lofs;
-  const uint8_t *lamp = smem + a.off_lamp + lofs;
-  const uint8_t *dp = smem + a.off_dp + lofs;
+  const unsigned brp = sbase + a.off_brp + lofs;
+  const unsigned lamp = sbase + a.off_lamp + lofs;
+  const unsigned dp = sbase + a.off_dp + lofs;
   // optimiser state rows of this tile (OPT kernels)
   const size_t tile0 = OPT ? DCOPF_TILE : 0;
   uint8_t *os1l = OPT ? reinterpret_cast<uint8_t *>(a.s1_lam) + tile0 * (size_t)a.n_bus * RB + lofs : nullptr;
@@ -411,8 +500,8 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   uint8_t *os2b = OPT ? reinterpret_cast<uint8_t *>(a.s2_br) + tile0 * (size_t)a.n_brows * BR + lofs : nullptr;
   const bool ost2 = OPT && a.opt == 4;  // Adam: two state arrays
   double ob1t = a.b1t, ob2t = a.b2t;
-  uint8_t *thp = smem + a.off_th + V * lane;  // theta*_i code rows
-  uint8_t *fcp = smem + a.off_fc + V * lane;  // f*_l code rows (F2)
+  const unsigned thp = sbase + a.off_th + V * lane;  // theta*_i code rows
+  const unsigned fcp = sbase + a.off_fc + V * lane;  // f*_l code rows (F2)
   // Consumer warps are not stepped in lock-step.  In step g a warp waits on
   //   full[stage]   before anything: the step's program block and rows landed;
   //   A-done(g-1)   after its A(g) items, before B: the theta* codes of chunk
@@ -494,52 +583,37 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     for (int j = 0; j < V; ++j) dos[j] = !CHK || stp[j];
     for (int c = DCOPF_S0; c < DCOPF_S1; ++c) {
       const int st = cst;
-      mbar_wait(&full[st], cph);
+      mbar_wait(full_sa + 8 * st, cph);
       if (++cst == S) {
         cst = 0;
         cph ^= 1u;
       }
-      const uint8_t *prog = smem + a.off_prog + st * a.prog_stride;
-      const int4 h0 = *reinterpret_cast<const int4 *>(prog);       // nA nIA nB nC (KVL: nD nDe nB nC)
-      const int4 h2 = *reinterpret_cast<const int4 *>(prog + 32);  // offA offIA offB offC
-      const int4 h3 = *reinterpret_cast<const int4 *>(prog + 48);  // offG offIC bytes -
-      const int4 h4 = *reinterpret_cast<const int4 *>(prog + 64);  // - - offW -
+      const unsigned prog = sbase + a.off_prog + st * a.prog_stride;
+      const int4 h0 = lds_rec<int4>(prog);       // nA nIA nB nC (KVL: nD nDe nB nC)
+      const int4 h2 = lds_rec<int4>(prog + 32);  // offA offIA offB offC
+      const int4 h3 = lds_rec<int4>(prog + 48);  // offG offIC bytes PH_PAD (KVL: cycle terms of B)
+      const int4 h4 = lds_rec<int4>(prog + 64);  // - - offW -
       // this warp's item ranges of the step's three phases, one 16-byte load
-      const uint4 wr = *reinterpret_cast<const uint4 *>(prog + h4.z + 16 * warp);
+      const uint4 wr = lds_u32x4(prog + h4.z + 16 * warp);
       auto rng0 = [](unsigned x) { return (int)(x & 0xffffu); };
       auto rng1 = [](unsigned x) { return (int)(x >> 16); };
-      unsigned *cnt_st = icnt + 4 * st;
-      (void)h0;
-      (void)cnt_st;
-#ifdef DCOPF_DYNAMIC
-      // items are taken from a per-phase counter (one shared-memory atomic per
-      // item, issued while the previous item runs) instead of the static
-      // per-warp ranges: no warp waits at the phase barrier for a straggler
-      auto grab = [&](int ph) {
-        const int t = (lane == 0) ? (int)atomicAdd(&cnt_st[ph], 1u) : 0;
-        return __shfl_sync(0xffffffffu, t, 0);
-      };
-#define ITEM_LOOP(ph, r, n)                                                                  \
-  for (int j = grab(ph), t_ = 0; j < (n); j = __shfl_sync(0xffffffffu, t_, 0))              \
-    if ((t_ = (lane == 0) ? (int)atomicAdd(&cnt_st[ph], 1u) : 0), true)
-#else
+      // (the phase index argument is unused: items come from static LPT ranges;
+      // dynamic grabbing by a shared-memory counter was measured 10% slower)
 #define ITEM_LOOP(ph, r, n) for (int j = rng0(r), je = rng1(r); j < je; ++j)
-#endif
 
       // ---------------- C: ready buses (F2 / F1: C(s-2), warp table 2; KVL: C(s-1), table 1) ----
       auto phaseC = [&](unsigned tr, int ph) {
-        const RecC *Cv = reinterpret_cast<const RecC *>(prog + h2.w);
-        const RecG *G = reinterpret_cast<const RecG *>(prog + h3.x);
+        const unsigned Cv = prog + h2.w, G = prog + h3.x;
         ITEM_LOOP(ph, tr, h0.w) {
-          const RecC r = Cv[j];
+          const RecC r = lds_rec<RecC>(Cv + j * (unsigned)sizeof(RecC));
           OState<V> ost = oload((size_t)r.wpos * RB, true, OPT && !EVAL && write && act);
-          const DV<V> li = ldv<V>(lamp, r.ls, hb), di = ldv<V>(dp, r.ds, hb);
+          const DV<V> li = ldsv<V>(lamp, r.ls, hb), di = ldsv<V>(dp, r.ds, hb);
           double gl[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) gl[q] = -di.v[q];
 #pragma unroll 1
           for (int gg = r.g0; gg < r.g1; ++gg) {  // mostly 0 or 1 generator
-            const RecG gr = G[gg];
+            const RecG gr = lds_rec<RecG>(G + gg * (unsigned)sizeof(RecG));
 #pragma unroll
             if (gr.a > 0.0) {  // (warp-uniform: one generator record per warp)
 #pragma unroll
@@ -562,7 +636,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             }
           }
           if (FORM != kFormF1) {
-            const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(prog + h3.y) + r.e0;
+            const unsigned IC = prog + h3.y + r.e0 * (unsigned)sizeof(RecIC2);
             const int n = r.e1 - r.e0;
             auto acc = [&](const RecIC2 &x) {
               const DV<V> f = ld_code<V>(fcp, x.f, x.sF);  // +-f* (c * (+-F) == +-(c * F) exactly)
@@ -571,14 +645,14 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             };
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (e < n) acc(IC[e]);
+              if (e < n) acc(lds_rec<RecIC2>(IC + e * (unsigned)sizeof(RecIC2)));
 #pragma unroll 1
-            for (int e = 4; e < n; ++e) acc(IC[e]);
+            for (int e = 4; e < n; ++e) acc(lds_rec<RecIC2>(IC + e * (unsigned)sizeof(RecIC2)));
           } else {
-            const RecIC1 *IC = reinterpret_cast<const RecIC1 *>(prog + h3.y);
+            const unsigned IC = prog + h3.y;
 #pragma unroll 1
             for (int e = r.e0; e < r.e1; ++e) {
-              const RecIC1 x = IC[e];
+              const RecIC1 x = lds_rec<RecIC1>(IC + e * (unsigned)sizeof(RecIC1));
               double sb[V];
 #pragma unroll
               for (int q = 0; q < V; ++q) sb[q] = x.sb;
@@ -620,8 +694,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       // warp has finished (this warp waited B-done(s-2) in the previous step)
       // ---------------- B(s): q_l = x_l (sum_k C_kl kappa_k) - (lambda_s - lambda_t), f* ----------------
       {
-        const RecBK *Bv = reinterpret_cast<const RecBK *>(prog + h2.z);
-        const RecBKe *BKe = reinterpret_cast<const RecBKe *>(prog + *reinterpret_cast<const int *>(prog + 4 * PH_PAD));
+        const unsigned Bv = prog + h2.z, BKe = prog + h3.w;
         auto bkitem = [&](const RecBK &r, auto out_tag) {
           constexpr bool OUT = decltype(out_tag)::value;
           double x[V], F[V];
@@ -644,12 +717,12 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           for (int q = 0; q < V; ++q) s[q] = 0.0;
 #pragma unroll 1
           for (int e = r.e0; e < r.e1; ++e) {
-            const RecBKe t = BKe[e];
-            const DV<V> kv = ldv<V>(brp, t.ks, hb);
+            const RecBKe t = lds_rec<RecBKe>(BKe + e * (unsigned)sizeof(RecBKe));
+            const DV<V> kv = ldsv<V>(brp, t.ks, hb);
 #pragma unroll
             for (int q = 0; q < V; ++q) s[q] = (t.sgn > 0) ? s[q] + kv.v[q] : s[q] - kv.v[q];
           }
-          const DV<V> ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+          const DV<V> ls = ldsv<V>(lamp, r.ls, hb), lt = ldsv<V>(lamp, r.lt, hb);
           int cd[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) {
@@ -662,30 +735,29 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           if (act) st_codes<V>(fcp + r.fs, cd);
         };
         ITEM_LOOP(0, wr.x, h0.z) {
-          const RecBK r = Bv[j];
+          const RecBK r = lds_rec<RecBK>(Bv + j * (unsigned)sizeof(RecBK));
           if (r.obr >= 0 && flagged(r.obr)) bkitem(r, std::integral_constant<bool, true>{});
           else bkitem(r, std::integral_constant<bool, false>{});
         }
       }
       if (SOFT) {  // C and D read the f* codes of B(<= s-1)
-        mbar_arrive(&bdone[gs & 3]);
-        if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+        mbar_arrive(bdone_sa + 8 * (gs & 3));
+        if (gs > 0) mbar_wait_backoff(bdone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
       }
       phaseC(wr.y, 1);
       // ---------------- D(s-1): d/dkappa_k = sum_l C_kl x_l f*_l, kappa' ----------------
       {
-        const RecD *Dv = reinterpret_cast<const RecD *>(prog + h2.x);
-        const RecDe *De = reinterpret_cast<const RecDe *>(prog + h2.y);
+        const unsigned Dv = prog + h2.x, De = prog + h2.y;
         ITEM_LOOP(2, wr.z, h0.x) {
-          const RecD r = Dv[j];
+          const RecD r = lds_rec<RecD>(Dv + j * (unsigned)sizeof(RecD));
           OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
-          const DV<V> kv = ldv<V>(brp, r.ks, hb);
+          const DV<V> kv = ldsv<V>(brp, r.ks, hb);
           double acc[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) acc[q] = 0.0;
 #pragma unroll 1
           for (int e = r.e0; e < r.e1; ++e) {
-            const RecDe d = De[e];
+            const RecDe d = lds_rec<RecDe>(De + e * (unsigned)sizeof(RecDe));
             int cd[V];
             ld_codes<V>(fcp, d.fs, cd);
             // index 0 / 1 / 2 for code -1 / 0 / +1 (lanes past the tile width read
@@ -728,9 +800,9 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       // every warp has finished (this warp waited A-done(s-2) in step s-1)
       // ---------------- A(s): w_i, theta* codes ----------------
       {
-        const RecA *A = reinterpret_cast<const RecA *>(prog + h2.x);
+        const unsigned A = prog + h2.x;
         ITEM_LOOP(0, wr.x, h0.x) {
-          const RecA ra = A[j];
+          const RecA ra = lds_rec<RecA>(A + j * (unsigned)sizeof(RecA));
           double w[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) w[q] = 0.0;
@@ -738,23 +810,23 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             // incidence entries in ascending original branch id (the oracle's
             // order); degree <= 4 for ~97% of buses: a fixed 4-way body with
             // warp-uniform guards instead of a counted loop, the rest in a tail
-            const RecIA2 *IA = reinterpret_cast<const RecIA2 *>(prog + h2.y) + ra.e0;
+            const unsigned IA = prog + h2.y + ra.e0 * (unsigned)sizeof(RecIA2);
             const int n = ra.e1 - ra.e0;
             auto acc = [&](const RecIA2 &r) {
-              const DV<V> nu = ldv<V>(brp, r.row, hb);
+              const DV<V> nu = ldsv<V>(brp, r.row, hb);
 #pragma unroll
               for (int q = 0; q < V; ++q) w[q] = w[q] + r.sb * nu.v[q];  // w_s += -(b nu), w_t += b nu (outaged: nu == 0)
             };
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (e < n) acc(IA[e]);
+              if (e < n) acc(lds_rec<RecIA2>(IA + e * (unsigned)sizeof(RecIA2)));
 #pragma unroll 1
-            for (int e = 4; e < n; ++e) acc(IA[e]);
+            for (int e = 4; e < n; ++e) acc(lds_rec<RecIA2>(IA + e * (unsigned)sizeof(RecIA2)));
           } else {
-            const RecIA1 *IA = reinterpret_cast<const RecIA1 *>(prog + h2.y);
+            const unsigned IA = prog + h2.y;
 #pragma unroll 1
             for (int e = ra.e0; e < ra.e1; ++e) {
-              const RecIA1 r = IA[e];
+              const RecIA1 r = lds_rec<RecIA1>(IA + e * (unsigned)sizeof(RecIA1));
               double sb[V];
 #pragma unroll
               for (int q = 0; q < V; ++q) sb[q] = r.sb;
@@ -763,8 +835,8 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
                 for (int q = 0; q < V; ++q)
                   if (out_t(my_outs(q), r.br)) sb[q] = copysign(0.0, sb[q]);
               }
-              const DV<V> mp = ldv<V>(brp, r.row, hb), mm = ldv<V>(brp, r.row + RB, hb);
-              const DV<V> ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+              const DV<V> mp = ldsv<V>(brp, r.row, hb), mm = ldsv<V>(brp, r.row + RB, hb);
+              const DV<V> ls = ldsv<V>(lamp, r.ls, hb), lt = ldsv<V>(lamp, r.lt, hb);
 #pragma unroll
               for (int q = 0; q < V; ++q)
                 w[q] = w[q] + sb[q] * ((mp.v[q] - mm.v[q]) - (ls.v[q] - lt.v[q]));  // w_s += u, w_t -= u
@@ -789,12 +861,12 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       }
       if (SOFT) {  // B(s-1) reads the theta* codes of A(<= s-1); the f* slots it writes
         // were last read 2+ steps ago, and A-done(s-1) implies every warp finished step s-2
-        mbar_arrive(&adone[gs & 3]);
-        if (gs > 0) mbar_wait_backoff(&adone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+        mbar_arrive(adone_sa + 8 * (gs & 3));
+        if (gs > 0) mbar_wait_backoff(adone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
       }
       // ---------------- B(s-1): branches ----------------
       {
-        const RecB *Bv = reinterpret_cast<const RecB *>(prog + h2.z);
+        const unsigned Bv = prog + h2.z;
         // one branch; OUT: some instance of the tile has it out (per-lane b = F
         // = 0), else the warp-uniform fast path with no per-lane outage state
         auto bitem = [&](const RecB &r, auto out_tag) {
@@ -816,7 +888,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           }
           if (FORM == kFormF2 && r.wpos < 0) {
             // lite halo branch (split tiles): its f* code for this part's C items
-            const DV<V> nu = ldv<V>(brp, r.row, hb), ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+            const DV<V> nu = ldsv<V>(brp, r.row, hb), ls = ldsv<V>(lamp, r.ls, hb), lt = ldsv<V>(lamp, r.lt, hb);
             int cd[V];
 #pragma unroll
             for (int q = 0; q < V; ++q) {
@@ -834,7 +906,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           for (int q = 0; q < V; ++q) phi[q] = b[q] * (ths.v[q] - tht.v[q]);
           uint8_t *dst = br_o + (size_t)r.wpos * BR;
           if (FORM == kFormF2) {
-            const DV<V> nu = ldv<V>(brp, r.row, hb), ls = ldv<V>(lamp, r.ls, hb), lt = ldv<V>(lamp, r.lt, hb);
+            const DV<V> nu = ldsv<V>(brp, r.row, hb), ls = ldsv<V>(lamp, r.ls, hb), lt = ldsv<V>(lamp, r.lt, hb);
             double g[V];
             int cd[V];
 #pragma unroll
@@ -866,7 +938,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
               }
             }
           } else {
-            const DV<V> mp = ldv<V>(brp, r.row, hb), mm = ldv<V>(brp, r.row + RB, hb);
+            const DV<V> mp = ldsv<V>(brp, r.row, hb), mm = ldsv<V>(brp, r.row + RB, hb);
             double gp[V], gm[V];
 #pragma unroll
             for (int q = 0; q < V; ++q) {
@@ -917,23 +989,23 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           }
         };
         ITEM_LOOP(1, wr.y, h0.z) {
-          const RecB r = Bv[j];
+          const RecB r = lds_rec<RecB>(Bv + j * (unsigned)sizeof(RecB));
           if (r.obr >= 0 && flagged(r.obr)) bitem(r, std::integral_constant<bool, true>{});  // (obr < 0: never out)
           else bitem(r, std::integral_constant<bool, false>{});
         }
       }
       if (SOFT) {
-        mbar_arrive(&bdone[gs & 3]);
-        if (gs > 0) mbar_wait_backoff(&bdone[(gs - 1) & 3], ((gs - 1) >> 2) & 1u);
+        mbar_arrive(bdone_sa + 8 * (gs & 3));
+        if (gs > 0) mbar_wait_backoff(bdone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
       }
       phaseC(wr.z, 2);
       }  // debug_mode
       }  // FORM
       if (SOFT) {
-        mbar_arrive(&empty[st]);
+        mbar_arrive(empty_sa + 8 * st);
       } else {  // lock-step mode: every warp finished the step
         named_bar(1, CT);
-        if (threadIdx.x == 0) mbar_arrive(&empty[st]);
+        if (threadIdx.x == 0) mbar_arrive(empty_sa + 8 * st);
       }
       ++gs;
     }

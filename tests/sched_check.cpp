@@ -1,10 +1,11 @@
-// Host-only checker of the batched sweep schedule (paper_2406_13191_b200/csrc/schedule.cpp):
-// replays the producer/consumer order of k_pipe with worst-case (instant) TMA
-// landing and verifies that every shared-memory slot read holds the row or
-// code the program expects, and that every bus / branch is visited exactly
-// once per phase.  Input on stdin: nb nl ref form CH P, then nl lines "s t"
-// (internal ids, branches sorted by larger endpoint), then per bus its
-// incident branch list "deg l0 to0 l1 to1 ...".
+// Host-only checker of the batched sweep schedule (paper_2406_13191_b200/csrc/split_schedule.cpp):
+// replays every part's producer/consumer order of k_sweep with worst-case
+// (instant) TMA landing and verifies that every shared-memory slot read holds
+// the row or code the program expects, that codes are read only in a later
+// step than the one writing them, and that the owned items cover every bus /
+// branch / cycle exactly once per phase.  Input on stdin: nb nl ref form CH P,
+// then nl lines "s t" (original ids).  Arguments: order(dfs|rcm) W life
+// [pool_gap [V C]].
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -18,103 +19,6 @@
 using namespace dcopf;
 
 
-// KVL replay: B(s) reads lambda / kappa rows and writes f* codes; C(s-1) and
-// D(s-1) read them; worst-case landing (writes of a step land first).
-static int check_kvl(const NetInternal &n, const Schedule &S, const CycleBasis &Y, int P) {
-  std::vector<int> brp(S.n_br_slots, -1), lamp(S.n_lam_slots, -1), dp(S.n_d_slots, -1), fc(S.n_f_slots, -1);
-  std::vector<int> seenB(n.nl, 0), seenC(n.nb, 0), seenD(Y.nc, 0);
-  const int RB = S.row_bytes, CRB = S.code_row_bytes;
-  int bad = 0;
-  auto issue = [&](int c) {
-    if (c >= S.nsteps) return;
-    for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
-      const int4_t x = S.ld[e];
-      std::vector<int> &pool = x.a == LD_LAM ? lamp : x.a == LD_D ? dp : brp;
-      const std::vector<int> &perm = x.a == LD_LAM ? S.perm_lam : x.a == LD_D ? S.perm_d : S.perm_br;
-      for (int r = 0; r < x.c; ++r) {
-        if (x.d + r >= (int)pool.size()) { printf("BAD slot range\n"); ++bad; continue; }
-        pool[x.d + r] = perm[x.b + r];
-      }
-    }
-  };
-  auto want = [&](std::vector<int> &pool, int slot, int ent, const char *what, int c) {
-    if (slot < 0 || slot >= (int)pool.size() || pool[slot] != ent) {
-      if (bad < 10) printf("BAD %s step %d slot %d want %d have %d\n", what, c, slot, ent,
-                           (slot >= 0 && slot < (int)pool.size()) ? pool[slot] : -9);
-      ++bad;
-    }
-  };
-  for (int c = 0; c <= P; ++c) issue(c);
-  for (int c = 0; c < S.nsteps; ++c) {
-    const uint8_t *pg = S.prog.data() + S.prog_off[c];
-    const int *h = reinterpret_cast<const int *>(pg);
-    const RecBK *Bv = reinterpret_cast<const RecBK *>(pg + h[PH_OFF_B]);
-    const RecBKe *BK = reinterpret_cast<const RecBKe *>(pg + h[PH_PAD]);
-    const RecC *Cv = reinterpret_cast<const RecC *>(pg + h[PH_OFF_C]);
-    const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
-    const RecD *Dv = reinterpret_cast<const RecD *>(pg + h[PH_OFF_A]);
-    const RecDe *De = reinterpret_cast<const RecDe *>(pg + h[PH_OFF_IA]);
-    // which branch is which record: match by lambda rows + f slot (B records carry no id)
-    std::vector<int> bl(h[PH_NB], -1);
-    for (int j = 0; j < h[PH_NB]; ++j) {
-      for (int l = 0; l < n.nl; ++l)
-        if (std::max(n.bs[l], n.bt[l]) / S.CH == c && !seenB[l] && lamp[Bv[j].ls / RB] == n.bs[l] &&
-            lamp[Bv[j].lt / RB] == n.bt[l] && (Bv[j].obr < 0 || Bv[j].obr == l)) {
-          bl[j] = l;
-          break;
-        }
-      if (bl[j] < 0) { printf("BAD B record %d at step %d\n", j, c); ++bad; continue; }
-      fc[Bv[j].fs / CRB] = bl[j];  // the step's code writes land first
-    }
-    for (int j = 0; j < h[PH_NB]; ++j) {
-      const int l = bl[j];
-      if (l < 0) continue;
-      seenB[l]++;
-      int cnt = 0;
-      for (int k = 0; k < Y.nc; ++k)
-        for (int e = Y.cp[k]; e < Y.cp[k + 1]; ++e)
-          if (Y.cb[e] == l && n.b[Y.def[k]] > 0.0) {
-            if (Bv[j].e0 + cnt >= Bv[j].e1) { printf("BAD B terms\n"); ++bad; break; }
-            want(brp, BK[Bv[j].e0 + cnt].ks / RB, k, "B kappa", c);
-            if (BK[Bv[j].e0 + cnt].sgn != Y.cs[e]) { printf("BAD B sign\n"); ++bad; }
-            ++cnt;
-          }
-      if (cnt != Bv[j].e1 - Bv[j].e0) { printf("BAD B term count\n"); ++bad; }
-    }
-    for (int j = 0; j < h[PH_NC]; ++j) {
-      const int bus = S.perm_lam[Cv[j].wpos];
-      seenC[bus]++;
-      want(lamp, Cv[j].ls / RB, bus, "C lam", c);
-      want(dp, Cv[j].ds / RB, bus, "C d", c);
-      if (Cv[j].e1 - Cv[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD C degree\n"); ++bad; }
-      for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
-        const int l = n.bus_inc[n.bus_ptr[bus] + e - Cv[j].e0] >> 1;
-        if (IC[e].br != l) { printf("BAD C order\n"); ++bad; }
-        want(fc, IC[e].f / CRB, l, "C f", c);
-      }
-    }
-    for (int j = 0; j < h[PH_NA]; ++j) {
-      const int k = S.perm_br[Dv[j].wpos];
-      seenD[k]++;
-      want(brp, Dv[j].ks / RB, k, "D kappa", c);
-      if (Dv[j].e1 - Dv[j].e0 != Y.cp[k + 1] - Y.cp[k]) { printf("BAD D length\n"); ++bad; continue; }
-      for (int e = Dv[j].e0; e < Dv[j].e1; ++e) {
-        const int q = Y.cp[k] + e - Dv[j].e0, l = Y.cb[q];
-        want(fc, De[e].fs / CRB, l, "D f", c);
-        const double sx = (Y.cs[q] > 0 ? 1.0 : -1.0) / n.b[l];
-        if (De[e].t[2] != n.F[l] * sx || De[e].t[0] != -n.F[l] * sx) { printf("BAD D coefficient\n"); ++bad; }
-      }
-    }
-    issue(c + P + 1);
-  }
-  for (int l = 0; l < n.nl; ++l) if (seenB[l] != 1) { printf("BAD cover br %d\n", l); ++bad; break; }
-  for (int i = 0; i < n.nb; ++i) if (seenC[i] != 1) { printf("BAD cover bus %d\n", i); ++bad; break; }
-  for (int k = 0; k < Y.nc; ++k) if (seenD[k] != 1) { printf("BAD cover cycle %d\n", k); ++bad; break; }
-  printf("chunks %d slots br %d lam %d d %d th %d f %d smem %d copies %d sticky %d bad %d\n", S.nch, S.n_br_slots,
-         S.n_lam_slots, S.n_d_slots, S.n_th_slots, S.n_f_slots, S.total, S.n_copies, S.n_sticky_copies, bad);
-  return bad ? 1 : 0;
-}
-
 // Split-tile replay (build_schedule_split, forms F2 / KVL): every part runs its
 // steps with its own pools; worst-case (instant) copy landing; a code read at
 // step c must see a code written at a step <= c - 1 of the same part, and a
@@ -122,7 +26,7 @@ static int check_kvl(const NetInternal &n, const Schedule &S, const CycleBasis &
 // last read.  Owned items must cover every bus / branch (/ cycle) exactly
 // once over the parts; halo items may repeat.
 static int check_split(const NetInternal &n, const Schedule &S, const CycleBasis *Y, int P, int GAP) {
-  const bool kvl = n.form == 2;
+  const bool kvl = n.form == 2, f1 = n.form == 1;
   const int RB = S.row_bytes, BR = S.br_row_bytes, CRB = S.code_row_bytes;
   const int nrows_br = kvl ? Y->nc : n.nl;
   std::vector<int> seenA(n.nb, 0), seenB(n.nl, 0), seenC(n.nb, 0), seenD(kvl ? Y->nc : 0, 0);
@@ -183,9 +87,11 @@ static int check_split(const NetInternal &n, const Schedule &S, const CycleBasis
       const int *h = reinterpret_cast<const int *>(pg);
       const RecC *Cv = reinterpret_cast<const RecC *>(pg + h[PH_OFF_C]);
       const RecIC2 *IC = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
+      const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
       if (!kvl) {
         const RecA *A = reinterpret_cast<const RecA *>(pg + h[PH_OFF_A]);
         const RecIA2 *IA = reinterpret_cast<const RecIA2 *>(pg + h[PH_OFF_IA]);
+        const RecIA1 *IA1 = reinterpret_cast<const RecIA1 *>(pg + h[PH_OFF_IA]);
         const RecB *Bv = reinterpret_cast<const RecB *>(pg + h[PH_OFF_B]);
         for (int j = 0; j < h[PH_NA]; ++j) {
           const int bus = A[j].bus;
@@ -196,6 +102,14 @@ static int check_split(const NetInternal &n, const Schedule &S, const CycleBasis
           if (A[j].e1 - A[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) BADF("A degree", c, bus);
           for (int e = A[j].e0; e < A[j].e1; ++e) {
             const int k = n.bus_ptr[bus] + e - A[j].e0, l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
+            if (f1) {
+              if ((IA1[e].br < 0 ? l : IA1[e].br) != l) BADF("A order", c, bus);
+              if (IA1[e].sb != (to ? -n.b[l] : n.b[l])) BADF("A sign", c, bus);
+              want(brp, IA1[e].row, BR, l, "A mu", c);
+              want(lamp, IA1[e].ls, RB, n.bs[l], "A lam_s", c);
+              want(lamp, IA1[e].lt, RB, n.bt[l], "A lam_t", c);
+              continue;
+            }
             if (IA[e].br != l) BADF("A order", c, bus);
             if (IA[e].sb != (to ? n.b[l] : -n.b[l])) BADF("A sign", c, bus);
             want(brp, IA[e].row, BR, l, "A nu", c);
@@ -208,8 +122,10 @@ static int check_split(const NetInternal &n, const Schedule &S, const CycleBasis
           if (lite) { ++halo; if (!(own(lo) && hi >= b1)) BADF("lite B not a halo branch", c, l); }
           else { seenB[l]++; if (!own(hi)) BADF("B of a foreign branch", c, l); }
           want(brp, Bv[j].row, BR, l, "B nu", c);
-          want(lamp, Bv[j].ls, RB, n.bs[l], "B lam_s", c);
-          want(lamp, Bv[j].lt, RB, n.bt[l], "B lam_t", c);
+          if (!f1) {
+            want(lamp, Bv[j].ls, RB, n.bs[l], "B lam_s", c);
+            want(lamp, Bv[j].lt, RB, n.bt[l], "B lam_t", c);
+          }
           if (Bv[j].b != n.b[l] || Bv[j].F != n.F[l]) BADF("B data", c, l);
         }
         // theta* reads (own B) see codes of earlier steps; then this step's A writes land
@@ -219,16 +135,25 @@ static int check_split(const NetInternal &n, const Schedule &S, const CycleBasis
             code_r(th, thw, thr, Bv[j].ts, n.bs[l], c, "B th_s");
             code_r(th, thw, thr, Bv[j].tt, n.bt[l], c, "B th_t");
           }
-        for (int j = 0; j < h[PH_NA]; ++j) code_w(th, thw, thr, A[j].th, A[j].bus, c, "A th write");
+        // (C's reads: F1 theta* codes of both endpoints, F2 f* codes -- before this step's writes land)
         for (int j = 0; j < h[PH_NC]; ++j) {
           const int bus = S.perm_lam[Cv[j].wpos];
-          for (int e = Cv[j].e0; e < Cv[j].e1; ++e) code_r(fc, fw, fr, IC[e].f, IC[e].br, c, "C f");
-          (void)bus;
+          for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
+            const int l = n.bus_inc[n.bus_ptr[bus] + e - Cv[j].e0] >> 1;
+            if (f1) {
+              code_r(th, thw, thr, IC1[e].ts, n.bs[l], c, "C th_s");
+              code_r(th, thw, thr, IC1[e].tt, n.bt[l], c, "C th_t");
+            } else {
+              code_r(fc, fw, fr, IC[e].f, IC[e].br, c, "C f");
+            }
+          }
         }
-        for (int j = 0; j < h[PH_NB]; ++j) {
-          const int l = Bv[j].wpos < 0 ? -1 - Bv[j].wpos : S.perm_br[Bv[j].wpos];
-          code_w(fc, fw, fr, Bv[j].fs, l, c, "B f write");
-        }
+        for (int j = 0; j < h[PH_NA]; ++j) code_w(th, thw, thr, A[j].th, A[j].bus, c, "A th write");
+        if (!f1)
+          for (int j = 0; j < h[PH_NB]; ++j) {
+            const int l = Bv[j].wpos < 0 ? -1 - Bv[j].wpos : S.perm_br[Bv[j].wpos];
+            code_w(fc, fw, fr, Bv[j].fs, l, c, "B f write");
+          }
       } else {
         const RecBK *Bv = reinterpret_cast<const RecBK *>(pg + h[PH_OFF_B]);
         const RecBKe *BK = reinterpret_cast<const RecBKe *>(pg + h[PH_PAD]);
@@ -277,6 +202,10 @@ static int check_split(const NetInternal &n, const Schedule &S, const CycleBasis
         if (Cv[j].e1 - Cv[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) BADF("C degree", c, bus);
         for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
           const int k = n.bus_ptr[bus] + e - Cv[j].e0, l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
+          if (f1) {
+            if ((IC1[e].br < 0 ? l : IC1[e].br) != l || IC1[e].sb != (to ? n.b[l] : -n.b[l])) BADF("C order / sign", c, bus);
+            continue;
+          }
           const double F = (!kvl || n.b[l] > 0.0) ? n.F[l] : 0.0;
           if (IC[e].br != l || IC[e].sF != (to ? F : -F)) BADF("C order / sign", c, bus);
         }
@@ -322,134 +251,9 @@ int main(int argc, char **argv) {
     for (int &l : Yi.def) l = in.br_inv[l];
     for (int &l : Yi.cb) l = in.br_inv[l];
   }
-  // argv[5], argv[6]: instances per lane and parts -> the split-tile compiler
-  if (argc > 6) {
-    const int V = atoi(argv[5]), C = atoi(argv[6]);
-    std::string e2 = build_schedule_split(n, CH, P, W, V, 8, C, {}, &S, form == 2 ? &Yi : nullptr);
-    if (!e2.empty()) { printf("ERR %s\n", e2.c_str()); return 1; }
-    return check_split(n, S, form == 2 ? &Yi : nullptr, P, S.pool_gap);
-  }
-  std::string err = build_schedule(n, CH, P, W, 8, &S, form == 2 ? &Yi : nullptr);
-
-  if (!err.empty()) { printf("ERR %s\n", err.c_str()); return 1; }
-  const bool f1 = n.form == 1;
-  if (form == 2) return check_kvl(n, S, Yi, P);
-  std::vector<int> brp(S.n_br_slots, -1), lamp(S.n_lam_slots, -1), dp(S.n_d_slots, -1), th(S.n_th_slots, -1),
-      fc(S.n_f_slots, -1);
-  std::vector<int> seenA(n.nb, 0), seenB(n.nl, 0), seenC(n.nb, 0);
-  int bad = 0;
-  auto issue = [&](int c) {
-    if (c >= S.nsteps) return;
-    for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
-      const int4_t x = S.ld[e];
-      std::vector<int> &pool = x.a == LD_LAM ? lamp : x.a == LD_D ? dp : brp;
-      const std::vector<int> &perm = x.a == LD_LAM ? S.perm_lam : x.a == LD_D ? S.perm_d : S.perm_br;
-      for (int r = 0; r < x.c; ++r) {
-        if (x.d + r >= (int)pool.size()) { printf("BAD slot range\n"); ++bad; continue; }
-        pool[x.d + r] = perm[x.b + r];
-      }
-    }
-  };
-  auto want = [&](std::vector<int> &pool, int slot, int ent, const char *what, int c) {
-    if (slot < 0 || slot >= (int)pool.size() || pool[slot] != ent) {
-      if (bad < 10) printf("BAD %s chunk %d slot %d want %d have %d\n", what, c, slot, ent,
-                           (slot >= 0 && slot < (int)pool.size()) ? pool[slot] : -9);
-      ++bad;
-    }
-  };
-  // expect_tx of every chunk = program block + the rows the producer copies
-  for (int c = 0; c < S.nsteps; ++c) {
-    long bytes = S.prog_bytes[c];
-    for (int e = S.ld_ptr[c]; e < S.ld_ptr[c + 1]; ++e) {
-      const int4_t x = S.ld[e];
-      if (x.a != LD_LAM && x.a != LD_D && x.a != LD_BR) { printf("BAD kind %d\n", x.a); ++bad; }
-      bytes += (long)x.c * ((x.a == LD_BR) ? S.br_row_bytes : S.row_bytes);
-    }
-    if (bytes != S.tx_bytes[c] || S.prog_bytes[c] % 16 || S.prog_bytes[c] > S.max_prog_bytes) {
-      printf("BAD tx chunk %d: %ld vs %d\n", c, bytes, S.tx_bytes[c]);
-      ++bad;
-    }
-  }
-  const int RB = S.row_bytes, BR = S.br_row_bytes;
-  for (int c = 0; c <= P; ++c) issue(c);
-  for (int c = 0; c < S.nsteps; ++c) {
-    const uint8_t *pg = S.prog.data() + S.prog_off[c];
-    const int *h = reinterpret_cast<const int *>(pg);
-    const RecA *A = reinterpret_cast<const RecA *>(pg + h[PH_OFF_A]);
-    const RecIA2 *IA2 = reinterpret_cast<const RecIA2 *>(pg + h[PH_OFF_IA]);
-    const RecIA1 *IA1 = reinterpret_cast<const RecIA1 *>(pg + h[PH_OFF_IA]);
-    const RecB *Bv = reinterpret_cast<const RecB *>(pg + h[PH_OFF_B]);
-    const RecC *Cv = reinterpret_cast<const RecC *>(pg + h[PH_OFF_C]);
-    const RecIC2 *IC2 = reinterpret_cast<const RecIC2 *>(pg + h[PH_OFF_IC]);
-    const RecIC1 *IC1 = reinterpret_cast<const RecIC1 *>(pg + h[PH_OFF_IC]);
-    // the step's code writes land first (worst case for the concurrent readers)
-    for (int j = 0; j < h[PH_NA]; ++j) th[A[j].th / S.code_row_bytes] = A[j].bus;
-    if (!f1) for (int j = 0; j < h[PH_NB]; ++j) fc[Bv[j].fs / S.code_row_bytes] = S.perm_br[Bv[j].wpos];
-    // A(c)
-    for (int j = 0; j < h[PH_NA]; ++j) {
-      int bus = A[j].bus;
-      seenA[bus]++;
-      if (bus / S.CH != c) { printf("BAD A step\n"); ++bad; }
-      if (A[j].e1 - A[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD A degree\n"); ++bad; }
-      for (int e = A[j].e0; e < A[j].e1; ++e) {
-        const int k = n.bus_ptr[bus] + e - A[j].e0;
-        const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
-        const int br = f1 ? (IA1[e].br < 0 ? l : IA1[e].br) : IA2[e].br;
-        const double sb = f1 ? IA1[e].sb : IA2[e].sb;
-        if (br != l) { printf("BAD A order\n"); ++bad; }
-        if (sb != ((to ^ (int)f1) ? n.b[l] : -n.b[l])) { printf("BAD A sign\n"); ++bad; }
-        const int row = f1 ? IA1[e].row : IA2[e].row;
-        if (row % BR) { printf("BAD A row align\n"); ++bad; }
-        want(brp, row / BR, l, "A br", c);
-        if (f1) { want(lamp, IA1[e].ls / RB, n.bs[l], "A lam_s", c); want(lamp, IA1[e].lt / RB, n.bt[l], "A lam_t", c); }
-      }
-    }
-    // B(c-1)
-    for (int j = 0; j < h[PH_NB]; ++j) {
-      int l = S.perm_br[Bv[j].wpos];  // items are reordered for warp balance
-      seenB[l]++;
-      if (std::max(n.bs[l], n.bt[l]) / S.CH != c - 1) { printf("BAD B step\n"); ++bad; }
-      want(brp, Bv[j].row / BR, l, "B br", c);
-      want(th, Bv[j].ts / S.code_row_bytes, n.bs[l], "B th_s", c);
-      want(th, Bv[j].tt / S.code_row_bytes, n.bt[l], "B th_t", c);
-      if (!f1) {
-        want(lamp, Bv[j].ls / RB, n.bs[l], "B lam_s", c);
-        want(lamp, Bv[j].lt / RB, n.bt[l], "B lam_t", c);
-      }
-    }
-    // C(c-2)
-    for (int j = 0; j < h[PH_NC]; ++j) {
-      int bus = S.perm_lam[Cv[j].wpos];
-      seenC[bus]++;
-      want(lamp, Cv[j].ls / RB, bus, "C lam", c);
-      want(dp, Cv[j].ds / RB, bus, "C d", c);
-      if (Cv[j].e1 - Cv[j].e0 != n.bus_ptr[bus + 1] - n.bus_ptr[bus]) { printf("BAD C degree\n"); ++bad; }
-      for (int e = Cv[j].e0; e < Cv[j].e1; ++e) {
-        const int k = n.bus_ptr[bus] + e - Cv[j].e0;
-        const int l = n.bus_inc[k] >> 1, to = n.bus_inc[k] & 1;
-        if ((f1 ? (IC1[e].br < 0 ? l : IC1[e].br) : IC2[e].br) != l) { printf("BAD C order\n"); ++bad; }
-        if (!f1) {
-          want(fc, IC2[e].f / S.code_row_bytes, l, "C f", c);
-          if (IC2[e].sF != (to ? n.F[l] : -n.F[l])) { printf("BAD C sign\n"); ++bad; }
-        } else {
-          want(th, IC1[e].ts / S.code_row_bytes, n.bs[l], "C th_s", c);
-          want(th, IC1[e].tt / S.code_row_bytes, n.bt[l], "C th_t", c);
-          if (IC1[e].sb != (to ? n.b[l] : -n.b[l])) { printf("BAD C sign\n"); ++bad; }
-        }
-      }
-    }
-    issue(c + P + 1);
-  }
-  if (getenv("DUMP_ROWS")) {
-    for (int st = 0; st < S.nsteps; ++st)
-      for (int e = S.ld_ptr[st]; e < S.ld_ptr[st + 1]; ++e) {
-        const int4_t x = S.ld[e];
-        fprintf(stderr, "L %d %d %d %d\n", x.a, x.b, x.c, st);
-      }
-  }
-  for (int i = 0; i < n.nb; ++i) if (seenA[i] != 1 || seenC[i] != 1) { printf("BAD cover bus %d\n", i); ++bad; break; }
-  for (int l = 0; l < n.nl; ++l) if (seenB[l] != 1) { printf("BAD cover br %d\n", l); ++bad; break; }
-  printf("chunks %d slots br %d lam %d d %d th %d f %d smem %d copies %d sticky %d bad %d\n", S.nch, S.n_br_slots,
-         S.n_lam_slots, S.n_d_slots, S.n_th_slots, S.n_f_slots, S.total, S.n_copies, S.n_sticky_copies, bad);
-  return bad ? 1 : 0;
+  // argv[5], argv[6]: instances per lane and parts (default 2, 1: the unsplit sweep)
+  const int V = argc > 6 ? atoi(argv[5]) : 2, C = argc > 6 ? atoi(argv[6]) : 1;
+  std::string e2 = build_schedule_split(n, CH, P, W, V, 8, C, {}, &S, form == 2 ? &Yi : nullptr);
+  if (!e2.empty()) { printf("ERR %s\n", e2.c_str()); return 1; }
+  return check_split(n, S, form == 2 ? &Yi : nullptr, P, S.pool_gap);
 }

@@ -681,12 +681,14 @@ def test_optimizer_batched_config4_kvl_sampled(name):
 # lane; every (V, C) gives the oracle's multipliers bitwise
 
 
-@pytest.mark.parametrize("form", [FORM_F2, oracle.FORM_KVL])
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1, oracle.FORM_KVL])
 @pytest.mark.parametrize("V,C", [(2, 1), (4, 1), (2, 3), (4, 2), (4, 7), (4, 16)])
 def test_split_tiles_bitwise(form, V, C):
     """2000-bus network, 150 config-4-style instances (per-bus load factors,
     0-3 non-tree outages, ragged last tile) at every tiling: owned items, halo
     recomputation and the once-per-sweep meeting of the parts."""
+    if form == FORM_F1 and V == 4:
+        pytest.skip("F1 runs 2 instances per lane")
     net = inst.make_network(1)
     sw = non_tree_switchable(net)
     B = 150
@@ -703,7 +705,7 @@ def test_split_tiles_bitwise(form, V, C):
     assert_parity(net, gpu, orc, bitwise_multipliers=True)
 
 
-@pytest.mark.parametrize("form", [FORM_F2, oracle.FORM_KVL])
+@pytest.mark.parametrize("form", [FORM_F2, FORM_F1, oracle.FORM_KVL])
 @pytest.mark.parametrize("B", [1024, 2048, 4096])
 def test_strong_scaling_shards_sampled(form, B):
     """The per-GPU shards of the literal config-4 split (8192 over 8 / 4 / 2
@@ -741,11 +743,13 @@ def test_split_tiles_optimizer_and_evaluate(V, C):
     orc = oracle.solve(net, batch.load, outages=batch.outages, K=K, alpha=a, switchable=sw, opt=opt, history=True,
                        threads=8)
     assert_parity(net, gpu, orc, bitwise_multipliers=True)
-    # evaluate at the oracle's final multipliers
+    # evaluate at the oracle's final multipliers, on a handle with Adam set (the
+    # evaluate kernel runs on the optimiser variant's schedule / warp count)
     dev = torch.device("cuda:0")
     h = dual.DcopfDual(net, path=dual.PATH_BATCHED, switchable=sw, tile_parts=C, lane_instances=V)
     h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev),
                          torch.from_numpy(batch.outages).to(dev))
+    h.set_optimizer(opt["variant"], 0.0, opt["beta1"], opt["beta2"], opt["eps"])
     h.set_multipliers(torch.from_numpy(np.ascontiguousarray(orc.lam.T)).to(dev),
                       torch.from_numpy(np.ascontiguousarray(orc.br.T)).to(dev))
     val = torch.empty(B, dtype=torch.float64, device=dev)
