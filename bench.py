@@ -598,12 +598,16 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "alg_bytes_per_inst_iter": info.alg_bytes_per_inst_iter, "peak_source": peak_src}
-        if dense and B <= 4:  # skinny batch: two matrix-vector passes, H_g read twice per step (HBM-bound)
-            per_step = 16.0 * net.n_branch * net.n_gen + 8.0 * B * (7 * net.n_branch + 2 * net.n_gen)
+        if dense and B <= 4:  # skinny batch: matrix-vector passes over H_g (HBM-bound)
+            single = B == 1 and info.smem_bytes > 0  # the single-read step: H_g read once per step
+            per_step = (8.0 if single else 16.0) * net.n_branch * net.n_gen \
+                + 8.0 * B * (7 * net.n_branch + 2 * net.n_gen)
             ach = per_step * K / (ms / 1e3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                     "traffic": None, "alg_bytes_per_step": per_step, "peak_source": peak_src,
-                    "kernel": "the whole step (2 matrix-vector kernels reading H_g, epilogues, fused finisher)"}
+                    "kernel": ("the whole step (single-read line pass over H_g with the mu step and the H_g^T nu "
+                               "accumulation, generator pass, fused finisher)" if single else
+                               "the whole step (2 matrix-vector kernels reading H_g, epilogues, fused finisher)")}
         elif dense:  # two GEMMs per step, 2 n_l n_g flops each per instance (the final evaluation not counted)
             flops = 4.0 * net.n_branch * net.n_gen * B * K
             ach_t = flops / (ms / 1e3) / 1e12

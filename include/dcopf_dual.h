@@ -303,7 +303,9 @@ typedef struct {
   int64_t alg_bytes_per_inst_iter;/* algorithmic HBM bytes per instance-iteration:
                                      F2 8(3 n_bus + 2 n_branch), F1 8(3 n_bus + 4 n_branch) */
   int32_t bandwidth;              /* bus bandwidth of the internal (RCM) order */
-  int32_t smem_bytes;             /* dynamic shared memory of the iteration kernel */
+  int32_t smem_bytes;             /* dynamic shared memory of the iteration kernel (dense path,
+                                     B <= 4: > 0 only when iterate() takes the B = 1 single-read
+                                     step: plain / GDM / GDM-classic steps) */
   int32_t threads_per_block;
   int32_t grid;                   /* CTAs per iteration launch */
   int32_t launches_per_iter;      /* kernel launches per ascent step (0: one launch per call) */
@@ -339,6 +341,8 @@ void dcopf_dual_destroy(dcopf_dual_t h);           /* NULL is a no-op */
  * parity-tested; DESIGN.md §6 records what they measured):
  *   DCOPF_PTDF_SKINNY=0|1   dense path: force the GEMM or the matrix-vector kernels
  *   DCOPF_PTDF_SPLITK=0     dense path: disable the split-K GEMM1 for medium batches
+ *   DCOPF_PTDF_FUSED=0      dense path, B = 1: the two-pass matrix-vector kernels instead of the
+ *                           single-read step
  *   DCOPF_PTDF_GROUP=n, DCOPF_PTDF_SPLIT=1|2   dense path: column-group size / stream split
  *   DCOPF_CLUSTER_DEBUG=n   cluster path: skip phases (synchronisation floor, timing only;
  *                           results are NOT the dual iteration when set)

@@ -857,6 +857,380 @@ __global__ void k_compact_nu(const double *nu, long ld, int nl, int NB, double *
 }
 
 // ---------------------------------------------------------------------------
+// One instance (B = 1): the single-read step.  The two products of a step,
+// y = H_g p*_k (line rows) and Q_{k+1} = H_g^T nu_{k+1} (generator columns),
+// both read H_g; the skinny kernels above read it twice per step from HBM
+// (H_g and H_g^T, 2 x 254 MB at config 3).  Here one pass over the rows of
+// H_g does both.  Each CTA streams a contiguous block of rows, R rows (a
+// group) at a time, into shared-memory stages with TMA bulk copies (issued by
+// the last warp).  The 16 warps own column pairs j = tid + 512 m of every row:
+// per group they load their columns of the R rows into registers, form the
+// row dots with p*_k (registers) and pass the warp sums through shared memory;
+// after one CTA barrier (which also frees the group's stage: S - 1 groups stay
+// in flight) every warp adds the 16 warp sums in the same fixed order, takes
+// the projected step of the R rows' mu (lane r: row r; bit-identical in every
+// warp, warp 0 stores it) and adds H_g[l,:] nu_{k+1,l} into its column
+// accumulators from the registers.  The CTAs' column partials are summed in
+// CTA order by k_fused_gen, which applies the generator minimiser for k+1.
+//   k_fused_line<0>: Q_0 = H_g^T nu (start of a call; no line work)
+//   k_fused_line<1>: line step k (+ Q_{k+1} partials); its last CTA runs the
+//                    finisher of step k (dual value g_k, the lambda step)
+//   k_fused_line<2>: line terms of the final value at y_K (no step, no Q)
+// The step sits on each group's path, so the variants whose per-row step is a
+// long dependent chain (AdaGrad, Adam: divisions, square roots) keep the
+// two-pass kernels (measured on config 3: Adam 121 us/it single-read against
+// 99 us two-pass; the plain step 62 against 96).
+constexpr int FT = 512, FW = FT / 32;  // threads (the last warp also issues the TMA copies)
+constexpr int FMAX = 4;                // double2 columns per thread: n_g <= 2 * FT * FMAX
+__host__ __device__ constexpr int fused_rows(int M) { return 6 / M; }  // rows per group: 6 double2 held per thread
+constexpr int FSMAX = 8;               // stages
+// shared memory: the stages (S - 1 groups, >= 120 KB, in flight per SM), the
+// warp dots, and the CTA's rows' data (nu, r, F, mu+-, optimiser state: 9 x rpc)
+constexpr long kFusedSmemBytes = 220 * 1024;
+inline size_t fused_smem(long ldh, int R, int S, int rpc) {
+  return (size_t)S * R * ldh * 8 + FSMAX * 8 + 2 * 6 * FW * 8 + FW * 8 + 9 * (size_t)rpc * 8;
+}
+
+struct FusedArgs {
+  const double *Hg;
+  long ldh;           // = ngk (row stride of H_g, doubles; rows 128-byte aligned)
+  int S;              // shared-memory stages (groups)
+  int rpc;            // >= rows per CTA
+  int ng;             // generators (columns of H_g in use)
+  const double *pcv;  // p*_k [ngk] (generator order; entries >= n_g unused)
+  double *nuc;        // compact nu copy (kept current for the skinny evaluate())
+  double *part_q;     // [CTA][ngk] column partials of Q_{k+1}
+  double *part_line;  // [CTA] line value terms
+  double *part_obj, *part_p;  // [k_fused_gen block]
+  double *acc;        // [2]: sum_g (a p^2 + q p), sum_g p at the current point
+  unsigned *ticket;   // [2]: k_fused_line, k_fused_gen (zero between launches)
+};
+
+__device__ __forceinline__ unsigned f_smem(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void f_bar_wait(uint64_t *bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(f_smem(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// M: double2 columns per thread (column pair j = tid + FT m, m < M)
+template <int MODE, int M>
+__global__ void __launch_bounds__(FT, 1) k_fused_line(const FusedArgs a, const GemmArgs g, const FinArgs f) {
+  constexpr int R = fused_rows(M);
+  extern __shared__ __align__(128) unsigned char fsm[];
+  const int S = a.S, rpc = a.rpc;
+  const long ldh = a.ldh;
+  double *stage = reinterpret_cast<double *>(fsm);  // [S][R][ldh]
+  uint64_t *full = reinterpret_cast<uint64_t *>(stage + (size_t)S * R * ldh);  // [FSMAX]
+  double *part = reinterpret_cast<double *>(full + FSMAX);  // [2][R][FW] warp dots, by group parity
+  double *svw = part + 2 * 6 * FW;                          // [FW]
+  double *rowv = svw + FW;  // [9][rpc]: nu, r, F, mu+, mu-, s1+, s2+, s1-, s2- of the CTA's rows
+  __shared__ bool last;
+  __shared__ double red[FT];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int r0 = (int)((long)g.nl * c / G), r1 = (int)((long)g.nl * (c + 1) / G);
+  const int nrow = r1 - r0, ngr = (nrow + R - 1) / R;
+  const int h2 = (int)(ldh / 2);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(f_smem(&full[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const bool optst = MODE == 1 && g.opt != 0, st2 = g.s2p != nullptr;
+  for (int t = tid; t < nrow; t += FT) {  // the rows' data, once (off the per-group path)
+    const int row = r0 + t;
+    const size_t o = (size_t)row * g.ld;
+    rowv[t] = g.nu[o];
+    if (MODE != 0) {
+      rowv[rpc + t] = g.r[o];
+      rowv[2 * rpc + t] = g.F[row];
+      rowv[3 * rpc + t] = g.mup[o];
+      rowv[4 * rpc + t] = g.mum[o];
+      if (optst) {
+        rowv[5 * rpc + t] = g.s1p[o];
+        rowv[7 * rpc + t] = g.s1m[o];
+        if (st2) {
+          rowv[6 * rpc + t] = g.s2p[o];
+          rowv[8 * rpc + t] = g.s2m[o];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // the last warp issues the TMA copies: one bulk copy per row, lane r copies row r
+  const bool producer = warp == FW - 1;
+  const unsigned rowb = (unsigned)(ldh * 8);
+  auto issue = [&](int gi) {
+    const int st = gi % S, t0 = gi * R, nr = min(R, nrow - t0);
+    const unsigned bar = f_smem(&full[st]);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nr * rowb)
+                   : "memory");
+    __syncwarp();
+    if (lane < nr)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              f_smem(stage + ((size_t)st * R + lane) * ldh)),
+          "l"(a.Hg + (size_t)(r0 + t0 + lane) * ldh), "r"(rowb), "r"(bar)
+          : "memory");
+  };
+  if (producer)
+    for (int gi = 0; gi < min(S, ngr); ++gi) issue(gi);
+  double2 pv[M], qv[M];
+  const bool tail = tid + FT * (M - 1) >= h2;  // this thread's last column pair is past the row
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int j = tid + FT * m;
+    double2 p = make_double2(0.0, 0.0);
+    if (MODE != 0 && j < h2) {
+      if (2 * j < a.ng) p.x = a.pcv[2 * j];
+      if (2 * j + 1 < a.ng) p.y = a.pcv[2 * j + 1];
+    }
+    pv[m] = p;
+    qv[m] = make_double2(0.0, 0.0);
+  }
+  const bool step = MODE == 1 && g.status[0] == 0;
+  const double al = MODE == 1 ? g.alpha[g.k] : 0.0;
+  double sv = 0.0;  // warp 0: its lanes' rows' value terms
+  int s = 0;
+  unsigned ph = 0;
+  for (int i = 0; i < ngr; ++i) {
+    const int t0 = i * R, nr = min(R, nrow - t0);
+    f_bar_wait(&full[s], ph);
+    const double2 *H = reinterpret_cast<const double2 *>(stage + (size_t)s * R * ldh) + tid;
+    double2 h[R][M];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        h[r][m] = (r < nr && (m < M - 1 || !tail)) ? H[(size_t)r * h2 + FT * m] : make_double2(0.0, 0.0);
+    double *pp = part + (i & 1) * 6 * FW + warp;
+    if (MODE != 0) {  // row dots: each thread's columns, then the warp's xor tree
+      double d[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        d[r] = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          d[r] = fma(h[r][m].x, pv[m].x, d[r]);
+          d[r] = fma(h[r][m].y, pv[m].y, d[r]);
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int r = 0; r < R; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], off);
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < R; ++r) pp[r * FW] = d[r];
+    }
+    __syncthreads();  // the group's warp dots are in; every warp holds the group: its stage is free
+    if (producer && i + S < ngr) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S);
+    }
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
+    // lane r: row t0 + r's step -- the same arithmetic on the same values in
+    // every warp, so every warp holds the same nu_{k+1}; warp 0 stores it
+    const bool live = lane < nr;
+    const int t = t0 + (live ? lane : 0), crow = r0 + t;
+    double nn = rowv[t];
+    if (MODE != 0 && live) {
+      const double rr = rowv[rpc + t], F = rowv[2 * rpc + t], mp = rowv[3 * rpc + t], mm = rowv[4 * rpc + t];
+      const double *pr = part + (i & 1) * 6 * FW + lane * FW;
+      // (H_g p*)_l: the 16 warp dots in a fixed order (four interleaved chains)
+      double y0 = pr[0], y1 = pr[1], y2 = pr[2], y3 = pr[3];
+#pragma unroll
+      for (int w = 4; w < FW; w += 4) {
+        y0 += pr[w];
+        y1 += pr[w + 1];
+        y2 += pr[w + 2];
+        y3 += pr[w + 3];
+      }
+      const double y = (y0 + y1) + (y2 + y3);
+      if (warp == 0) sv += mm * (rr - F) - mp * (rr + F);
+      if (step) {
+        const double gp = (y - rr) - F, gm = (rr - y) - F;
+        double vp, vm, a1 = 0.0, a2 = 0.0, b1 = 0.0, b2 = 0.0;
+        if (g.opt == 0) {
+          vp = mp + al * gp;
+          vm = mm + al * gm;
+        } else {
+          a1 = rowv[5 * rpc + t];
+          b1 = rowv[7 * rpc + t];
+          if (st2) {
+            a2 = rowv[6 * rpc + t];
+            b2 = rowv[8 * rpc + t];
+          }
+          vp = opt_step(g, mp, gp, al, a1, a2);
+          vm = opt_step(g, mm, gm, al, b1, b2);
+        }
+        const double np = vp > 0.0 ? vp : 0.0, nm = vm > 0.0 ? vm : 0.0;  // mu <- max(mu, 0)
+        nn = np - nm;
+        if (warp == 0) {
+          const size_t o = (size_t)crow * g.ld;
+          if (g.opt != 0) {
+            g.s1p[o] = a1;
+            g.s1m[o] = b1;
+            if (st2) {
+              g.s2p[o] = a2;
+              g.s2m[o] = b2;
+            }
+          }
+          g.mup[o] = np;
+          g.mum[o] = nm;
+          g.nu[o] = nn;
+          a.nuc[crow] = nn;
+        }
+      }
+    }
+    if (MODE != 2) {  // Q += H_g[l, :]^T nu_{k+1,l} over the group's rows
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double v = __shfl_sync(0xffffffffu, nn, r);
+        if (r < nr)
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            qv[m].x = fma(h[r][m].x, v, qv[m].x);
+            qv[m].y = fma(h[r][m].y, v, qv[m].y);
+          }
+      }
+    }
+  }
+  if (MODE != 2) {
+    double2 *q = reinterpret_cast<double2 *>(a.part_q + (size_t)c * ldh) + tid;
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+      if (m < M - 1 || !tail) q[FT * m] = qv[m];
+  }
+  if (MODE == 0) return;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, off);
+  if (lane == 0) svw[warp] = sv;
+  __syncthreads();
+  if (tid == 0) {
+    double t = svw[0];
+    for (int w = 1; w < FW; ++w) t += svw[w];
+    a.part_line[c] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(&a.ticket[0], 1u) == (unsigned)G - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the last CTA: the CTAs' line terms summed by a fixed tree (loads in parallel)
+  red[tid] = tid < G ? __ldcg(a.part_line + tid) : 0.0;
+  for (int b = tid + FT; b < G; b += FT) red[tid] += __ldcg(a.part_line + b);
+  __syncthreads();
+  for (int w = FT / 2; w > 0; w >>= 1) {
+    if (tid < w) red[tid] += red[tid + w];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    finish_one<false>(f, 0, __ldcg(a.acc), __ldcg(a.acc + 1), red[0]);
+    a.ticket[0] = 0u;
+  }
+}
+
+// Q_{k+1} = sum over CTAs (in order) of the column partials, then p*_{k+1} and
+// the generator value terms; 32 columns per block, the CTA range split over
+// 8 warps (combined in warp order); the last block sums the block terms
+constexpr int FGW = 16;
+__global__ void __launch_bounds__(FGW * 32) k_fused_gen(const FusedArgs a, const GemmArgs g, int G) {
+  __shared__ double red[FGW][32];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * 32 + lane;
+  double q = 0.0;
+  if (col < g.ng) {  // CTAs [b0, b1) in order; four loads in flight ahead of the adds
+    const double *pq = a.part_q + col;
+    int b = G * warp / FGW;
+    const int b1 = G * (warp + 1) / FGW;
+    for (; b + 4 <= b1; b += 4) {
+      const double v0 = __ldcg(pq + (size_t)b * a.ldh), v1 = __ldcg(pq + (size_t)(b + 1) * a.ldh);
+      const double v2 = __ldcg(pq + (size_t)(b + 2) * a.ldh), v3 = __ldcg(pq + (size_t)(b + 3) * a.ldh);
+      q += v0;
+      q += v1;
+      q += v2;
+      q += v3;
+    }
+    for (; b < b1; ++b) q += __ldcg(pq + (size_t)b * a.ldh);
+  }
+  red[warp][lane] = q;
+  __syncthreads();
+  if (warp == 0) {
+    double Q = red[0][lane];
+    for (int w = 1; w < FGW; ++w) Q += red[w][lane];
+    double so = 0.0, sp = 0.0;
+    if (col < g.ng) {
+      const double aq = g.ga ? g.ga[col] : 0.0;
+      const double qq = (g.gc[col] + g.lam[0]) + Q;
+      const double p = minimiser(qq, g.glo[col], g.ghi[col], aq);
+      const_cast<double *>(a.pcv)[col] = p;
+      so = aq * p * p + qq * p;
+      sp = p;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      so += __shfl_xor_sync(0xffffffffu, so, off);
+      sp += __shfl_xor_sync(0xffffffffu, sp, off);
+    }
+    if (lane == 0) {
+      a.part_obj[blockIdx.x] = so;
+      a.part_p[blockIdx.x] = sp;
+      __threadfence();
+      last = atomicAdd(&a.ticket[1], 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  // the last block: the blocks' generator terms summed by a fixed tree (loads in parallel)
+  __threadfence();
+  const int t = threadIdx.x, nb = gridDim.x;
+  double to = 0.0, tp = 0.0;
+  for (int b = t; b < nb; b += FGW * 32) {
+    to += __ldcg(a.part_obj + b);
+    tp += __ldcg(a.part_p + b);
+  }
+  double *ro = &red[0][0], *rp = ro + FGW * 16;
+  __syncthreads();
+  if (t < FGW * 16) {
+    ro[t] = to;
+    rp[t] = tp;
+  }
+  __syncthreads();
+  if (t >= FGW * 16) {  // fold the upper half in (fixed pairing t - FGW * 16 <-> t)
+    ro[t - FGW * 16] += to;
+    rp[t - FGW * 16] += tp;
+  }
+  __syncthreads();
+  for (int w = FGW * 8; w > 0; w >>= 1) {
+    if (t < w) {
+      ro[t] += ro[t + w];
+      rp[t] += rp[t + w];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    a.acc[0] = ro[0];
+    a.acc[1] = rp[0];
+    a.ticket[1] = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // construction kernels (tree flows, cycle sums, H_a assembly, generator columns)
 struct TreeDev {
   const int *tin, *tout;   // DFS entry / exit times per bus
@@ -975,7 +1349,12 @@ struct PtdfState {
   // skinny batches (B <= 4): matrix-vector kernels; nbv = instance columns computed (0: GEMM mode)
   int nbv = 0;
   double *nuc = nullptr, *pcv = nullptr, *sp_obj = nullptr, *sp_p = nullptr, *sp_line = nullptr;
-  unsigned *ticket = nullptr;  // last-block ticket of the skinny line kernel (zero between launches)
+  unsigned *ticket = nullptr;  // [2] last-block tickets of the skinny / single-read kernels (zero between launches)
+  // B = 1: the single-read step (k_fused_line / k_fused_gen); fG CTAs, fS stages, fR rows per
+  // group, frpc >= rows per CTA
+  bool fused = false;
+  int nsm = 148, fG = 0, fS = 0, fR = 0, fgb = 0, frpc = 0;
+  double *fq = nullptr, *fline = nullptr, *fobj = nullptr, *fp = nullptr, *facc = nullptr;
   // medium batches: split-K scratch of GEMM1 ([S][n_g pad][B_pad]), CTA slots of the GPU
   double *qsplit = nullptr;
   size_t qsplit_n = 0;
@@ -1437,6 +1816,7 @@ int ptdf_create(const PtdfNetIn &net, int device, PtdfState **out, std::string *
     int nsm = 148;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess)
       st->n_slots = CTAS_PER_SM * nsm;
+    st->nsm = nsm;
   }
   // ---- device: S = C X T, W = L^{-T} (L^{-1} S), H_a = T - C^T W ----
   int *d_tin = nullptr, *d_tout = nullptr, *d_child = nullptr, *d_cp = nullptr, *d_cb = nullptr, *d_bp = nullptr,
@@ -1541,7 +1921,7 @@ void ptdf_destroy(PtdfState *st) {
   cudaSetDevice(st->device);
   free_batch(st);
   double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch, st->nuc, st->pcv,
-                  st->sp_obj, st->sp_p, st->sp_line, st->qsplit};
+                  st->sp_obj, st->sp_p, st->sp_line, st->qsplit, st->fq, st->fline, st->fobj, st->fp, st->facc};
   for (double *p : dp) cudaFree(p);
   for (int c = 0; c < 2; ++c) {
     if (st->sub[c]) cudaStreamDestroy(st->sub[c]);
@@ -1592,10 +1972,33 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
     if (!rc0) rc0 = dalloc(&st->sp_p, (size_t)skinny_blocks_g(st->ng) * 16, err);
     if (!rc0) rc0 = dalloc(&st->sp_line, (size_t)skinny_blocks_l(st->nl) * 16, err);
     if (!rc0 && !st->ticket) {
-      PCK(cudaMalloc(&st->ticket, sizeof(unsigned)));
-      PCK(cudaMemset(st->ticket, 0, sizeof(unsigned)));
+      PCK(cudaMalloc(&st->ticket, 2 * sizeof(unsigned)));
+      PCK(cudaMemset(st->ticket, 0, 2 * sizeof(unsigned)));
     }
     if (rc0) return rc0;
+    // B = 1: the single-read step when a group of rows fits the shared-memory
+    // stages (DCOPF_PTDF_FUSED=0 keeps the two-pass kernels; measurement)
+    const char *fe = getenv("DCOPF_PTDF_FUSED");
+    const long rowb = st->ngk * 8;
+    st->fused = false;
+    if (st->nbv == 1 && st->nl > 0 && st->ng > 0 && st->ngk <= 2L * FT * FMAX && !(fe && atoi(fe) == 0)) {
+      const int M = (int)((st->ngk / 2 + FT - 1) / FT);
+      st->fR = fused_rows(M);
+      st->fG = std::min(st->nsm, st->nl);
+      st->frpc = (st->nl + st->fG - 1) / st->fG + 1;
+      const long fixed = (long)fused_smem(0, 0, 0, st->frpc);
+      st->fS = (int)std::max<long>(0, std::min<long>(FSMAX, (kFusedSmemBytes - fixed) / (st->fR * rowb)));
+      st->fgb = (st->ng + 31) / 32;
+      if (st->fS >= 3) {  // >= 2 groups in flight ahead of the one being read
+        st->fused = true;
+        rc0 = dalloc(&st->fq, (size_t)st->fG * st->ngk, err);
+        if (!rc0) rc0 = dalloc(&st->fline, st->fG, err);
+        if (!rc0) rc0 = dalloc(&st->fobj, st->fgb, err);
+        if (!rc0) rc0 = dalloc(&st->fp, st->fgb, err);
+        if (!rc0) rc0 = dalloc(&st->facc, 2, err);
+        if (rc0) return rc0;
+      }
+    }
   }
   // loads: [n_bus][B] -> Dm [nbk][Bp] (zero padded), r = H_a Dm, D = 1^T d
   const size_t dm = (size_t)st->nbk * Bp;
@@ -1623,6 +2026,71 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
   return reset_opt(st, err);
 }
 
+template <int M>
+int fused_loop(PtdfState *st, int64_t K, const FusedArgs &a, GemmArgs g, const GemmArgs &gg, FinArgs f,
+               size_t smem, cudaStream_t s, std::string *err);
+
+// B = 1: Q_0 pass + generator pass, then per step the single-read line pass
+// (its last CTA runs the finisher) and the generator pass, then the final
+// evaluation's line terms
+int fused_iterate(PtdfState *st, int64_t K, GemmArgs g, FinArgs f, cudaStream_t s, std::string *err) {
+  FusedArgs a;
+  a.Hg = st->Hg;
+  a.ldh = st->ngk;
+  a.S = st->fS;
+  a.rpc = st->frpc;
+  a.ng = st->ng;
+  a.pcv = st->pcv;
+  a.nuc = st->nuc;
+  a.part_q = st->fq;
+  a.part_line = st->fline;
+  a.part_obj = st->fobj;
+  a.part_p = st->fp;
+  a.acc = st->facc;
+  a.ticket = st->ticket;
+  GemmArgs gg = gen_args(st);
+  const size_t smem = fused_smem(a.ldh, st->fR, a.S, a.rpc);
+  const int M = (int)((a.ldh / 2 + FT - 1) / FT);
+  switch (M) {
+    case 1: return fused_loop<1>(st, K, a, g, gg, f, smem, s, err);
+    case 2: return fused_loop<2>(st, K, a, g, gg, f, smem, s, err);
+    case 3: return fused_loop<3>(st, K, a, g, gg, f, smem, s, err);
+    default: return fused_loop<4>(st, K, a, g, gg, f, smem, s, err);
+  }
+}
+
+template <int M>
+int fused_loop(PtdfState *st, int64_t K, const FusedArgs &a, GemmArgs g, const GemmArgs &gg, FinArgs f,
+               size_t smem, cudaStream_t s, std::string *err) {
+  PCK(cudaFuncSetAttribute(k_fused_line<0, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PCK(cudaFuncSetAttribute(k_fused_line<1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PCK(cudaFuncSetAttribute(k_fused_line<2, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int G = st->fG, T = FT;
+  k_fused_line<0, M><<<G, T, smem, s>>>(a, g, f);
+  k_fused_gen<<<st->fgb, FGW * 32, 0, s>>>(a, gg, G);
+  PCK(cudaGetLastError());
+  for (int64_t k = 0; k <= K; ++k) {
+    const bool step = k < K;
+    if (step && st->opt.variant == DCOPF_OPT_ADAM) {  // beta^t by repeated products (reading A-26)
+      st->b1t = st->b1t * st->opt.beta1;
+      st->b2t = st->b2t * st->opt.beta2;
+    }
+    g.k = f.k = (int)k;
+    g.b1t = f.b1t = st->b1t;
+    g.b2t = f.b2t = st->b2t;
+    f.first = k == 0;
+    if (step) {
+      k_fused_line<1, M><<<G, T, smem, s>>>(a, g, f);
+      k_fused_gen<<<st->fgb, FGW * 32, 0, s>>>(a, gg, G);
+    } else {
+      k_fused_line<2, M><<<G, T, smem, s>>>(a, g, f);
+    }
+    PCK(cudaGetLastError());
+  }
+  st->k_base += K;
+  return DCOPF_OK;
+}
+
 int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist, cudaStream_t s, std::string *err) {
   GemmArgs g1 = gen_args(st), g2 = line_args(st);
   g2.alpha = alpha_dev;
@@ -1633,6 +2101,10 @@ int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist
   f.k_base = st->k_base;
   f.target = st->has_target ? st->target : nullptr;
   f.hit = st->hit;
+  // B = 1: the single-read step, except for the variants with a long per-row
+  // step chain (AdaGrad, Adam), which keep the two-pass kernels (see k_fused_line)
+  if (st->fused && st->opt.variant != DCOPF_OPT_ADAGRAD && st->opt.variant != DCOPF_OPT_ADAM)
+    return fused_iterate(st, K, g2, f, s, err);
   if (st->nbv) {  // skinny batch: matrix-vector passes on the caller's stream
     fin_tiles(st, &f);
     for (int64_t k = 0; k <= K; ++k) {
@@ -1860,6 +2332,12 @@ void ptdf_info(const PtdfState *st, dcopf_info *info) {
     info->grid = skinny_blocks_l(st->nl);
     info->launches_per_iter = 2;
     info->tile_width = st->nbv;
+    if (st->fused && st->opt.variant != DCOPF_OPT_ADAGRAD && st->opt.variant != DCOPF_OPT_ADAM) {
+      // B = 1, the single-read step (with this step variant): its line kernel's stages and grid
+      info->smem_bytes = (int)fused_smem(st->ngk, st->fR, st->fS, st->frpc);
+      info->threads_per_block = FT;
+      info->grid = st->fG;
+    }
   }
   info->cluster_size = 1;
 }

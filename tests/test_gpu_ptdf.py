@@ -97,11 +97,13 @@ def test_ptdf_matrix(which):
 # the iteration
 
 
-@pytest.mark.parametrize("skinny", ["1", "0"])
-def test_config0_full_K(skinny, monkeypatch):
-    """B = 1: the matrix-vector kernels (skinny mode, default for B <= 4) and,
-    forced, the GEMM kernels on a 128-column tile."""
+@pytest.mark.parametrize("skinny,fused", [("1", "1"), ("1", "0"), ("0", "1")])
+def test_config0_full_K(skinny, fused, monkeypatch):
+    """B = 1: the single-read step (default), the two-pass matrix-vector
+    kernels (skinny mode without it) and, forced, the GEMM kernels on a
+    128-column tile."""
     monkeypatch.setenv("DCOPF_PTDF_SKINNY", skinny)
+    monkeypatch.setenv("DCOPF_PTDF_FUSED", fused)
     net = inst.make_network(0)
     K = inst.ITERS[0]
     a = inst.alpha_schedule(K)
@@ -110,6 +112,60 @@ def test_config0_full_K(skinny, monkeypatch):
     assert_parity(net, gpu, orc)
     info = gpu["info"]
     assert info.path == dual.PATH_DENSE and info.form == dual.FORM_PTDF
+
+
+@pytest.mark.parametrize("which", ["config3_gdm", "config3_plain", "config2_quadratic", "config1_warm"])
+def test_single_read_step(which):
+    """B = 1 on the single-read step (plain and momentum steps; AdaGrad / Adam
+    keep the two-pass kernels): config 3's H_g (2 500 generator columns: two
+    20 KB rows per group, 148 CTAs of ~86 lines) over several calls; the
+    quadratic config-2 network; a warm start from random multipliers (Q_0 from
+    the set nu) followed by the two-pass evaluate()."""
+    import torch
+    if which.startswith("config3"):
+        net = inst.make_network(3)
+        gdm = which == "config3_gdm"
+        K = 60
+        a = inst.alpha_schedule(K, 1e-3 if gdm else 2e-3)
+        loads = net.base_load[None]
+        gpu = _gpu(net, loads, K, a, opt=GDM if gdm else None, split=25)
+        orc = _orc(net, loads, K, a, opt=GDM if gdm else None)
+        assert gpu["info"].smem_bytes > 0  # the single-read kernels ran
+        assert_parity(net, gpu, orc)
+        return
+    if which == "config2_quadratic":
+        net = inst.make_network(2, quadratic=True)
+        K, a = 300, inst.alpha_schedule(300)
+        loads = _scaled_loads(net, 1, 6)
+        gpu = _gpu(net, loads, K, a, split=110)
+        orc = _orc(net, loads, K, a)
+        assert_parity(net, gpu, orc)
+        return
+    net = inst.make_network(1)
+    Ha = P.ptdf(net)
+    rng = np.random.default_rng(9)
+    loads = _scaled_loads(net, 1, 3)
+    lam = rng.normal(0, 20, 1)
+    mu = np.abs(rng.normal(0, 5, (1, 2 * net.n_branch))) * (rng.random((1, 2 * net.n_branch)) < 0.3)
+    h = dual.DcopfDual(net, form=dual.FORM_PTDF)
+    h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(loads.T)).to(torch.device("cuda:0")))
+    h.set_multipliers(np.ascontiguousarray(lam[None, :]), np.ascontiguousarray(mu.T))
+    K = 80
+    a = inst.alpha_schedule(K, 1e-3)
+    h.set_optimizer(P.OPT_GDM, GDM["rho"])
+    h.iterate(30, a[:30])
+    h.iterate(K - 30, a[30:])
+    bound, best, status, l2, b2 = h.results_numpy()
+    val = np.empty(1)
+    h.evaluate(val)  # the two-pass evaluate() after the single-read steps (nu_c kept current)
+    h.close()
+    r = P.solve(net, loads, K, a, Ha=Ha, lam0=lam, mu0=mu, opt=GDM)
+    S = cost_scale(net)
+    assert np.all(np.abs(bound - r.bound) <= BOUND_RTOL * np.maximum(np.abs(r.bound), S))
+    assert np.all(np.abs(val - bound) <= BOUND_RTOL * np.maximum(np.abs(bound), S))
+    y_g = np.concatenate([l2.T, b2.T], axis=1)
+    y_o = np.concatenate([r.lam[:, None], r.mu], axis=1)
+    assert np.max(np.abs(y_g - y_o) / np.maximum(1.0, np.abs(y_o).max(axis=1, keepdims=True))) <= MULT_TOL
 
 
 def _no_flow_lines(net, Ha, loads):

@@ -1,19 +1,16 @@
 # B = 1 dense path: the single-read step against the two-pass kernels
-# (parity subset, config-3 bench lines, launch list, one ncu --set full capture)
+# (agreement at small K, parity subset, config-3 bench lines, launch list, one ncu --set full capture)
 set -x
 O=gpurun_out/fused
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build=$?
-timeout 1200 python -m pytest tests/test_gpu_ptdf.py -q -x -k "config0_full_K or single_read or skinny or first_hit or evaluate or ragged" > $O/pytest.log 2>&1; echo tests=$?
+timeout 600 python tools/dbg_fused.py > $O/dbg.log 2>&1; echo dbg=$?
+timeout 1200 python -m pytest tests/test_gpu_ptdf.py -q -x > $O/pytest.log 2>&1; echo tests=$?
 B() { name=$1; shift; timeout 900 python bench.py "$@" > $O/bench_$name.json 2> $O/bench_$name.err; echo $name=$?; }
 B c3_plain --workload config3 --form PTDF --steps 1000 --warmup 20 --no-cpu-baseline --no-gap
 DCOPF_PTDF_FUSED=0 B c3_plain_2pass --workload config3 --form PTDF --steps 1000 --warmup 20 --no-cpu-baseline --no-gap
 B c3_adam --workload config3 --form PTDF --opt adam --alpha 5 --decay inv:200 --steps 2000 --warmup 100 --no-cpu-baseline
 DCOPF_PTDF_FUSED=0 B c3_adam_2pass --workload config3 --form PTDF --opt adam --alpha 5 --decay inv:200 --steps 2000 --warmup 100 --no-cpu-baseline
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_c3_ptdf.csv python bench.py --workload config3 --form PTDF --steps 20 --warmup 3 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_launch.log 2>&1; echo launches=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused_line -s 6 -c 1 -o $O/ncu_fused_line python bench.py --workload config3 --form PTDF --steps 5 --warmup 3 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_full.log 2>&1; echo ncu=$?
-
-timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x > $O/pytest_sweep.log 2>&1; echo sweep_tests=$?
-B f2_k20 --steps 20 --warmup 5 --no-cpu-baseline --no-gap --no-e2e
-B f2_k100 --no-cpu-baseline --no-gap --no-e2e
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 6 -c 2 -o $O/ncu_fused python bench.py --workload config3 --form PTDF --steps 5 --warmup 3 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_full.log 2>&1; echo ncu=$?
 echo done
