@@ -99,6 +99,28 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// x / d for a positive finite d, sqrt(x) for x >= 0, skipping the operation
+// where x == 0 (the result is x itself; CUDA's zero-operand case is an
+// out-of-line slow path taken by the whole warp).  Bitwise the same results.
+// (the compiler evaluates both sides of a select and would fold a plain
+// (x == 0 ? 1 : x) back into x, so the zero lanes' operand 1 is selected in
+// asm: they divide 1 by d -- never the slow path -- and keep x)
+__device__ __forceinline__ double nz_or_one(double x) {
+  double r;
+  asm("{\n\t.reg .pred z;\n\tsetp.eq.f64 z, %1, 0d0000000000000000;\n\tselp.f64 %0, 0d3FF0000000000000, %1, z;\n\t}"
+      : "=d"(r)
+      : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double div_pos(double x, double d) {
+  const double q = nz_or_one(x) / d;
+  return x == 0.0 ? x : q;
+}
+__device__ __forceinline__ double sqrt_nz(double x) {
+  const double r = sqrt(nz_or_one(x));
+  return x == 0.0 ? x : r;
+}
+
 __device__ __forceinline__ double opt_step(const GemmArgs &g, double y, double gr, double al, double &s1,
                                            double &s2) {
   switch (g.opt) {
@@ -116,15 +138,15 @@ __device__ __forceinline__ double opt_step(const GemmArgs &g, double y, double g
     case 3: {  // AdaGrad (reading A-26)
       const double G = s1 + gr * gr;
       s1 = G;
-      return y + (al * gr) / (sqrt(G) + g.eps);
+      return y + div_pos(al * gr, sqrt_nz(G) + g.eps);
     }
     case 4: {  // Adam (reading A-26)
       const double m = g.beta1 * s1 + (1.0 - g.beta1) * gr;
       const double v = g.beta2 * s2 + (1.0 - g.beta2) * (gr * gr);
       s1 = m;
       s2 = v;
-      const double mh = m / (1.0 - g.b1t), vh = v / (1.0 - g.b2t);
-      return y + (al * mh) / (sqrt(vh) + g.eps);
+      const double mh = div_pos(m, 1.0 - g.b1t), vh = div_pos(v, 1.0 - g.b2t);
+      return y + div_pos(al * mh, sqrt_nz(vh) + g.eps);
     }
     default:
       return y + al * gr;

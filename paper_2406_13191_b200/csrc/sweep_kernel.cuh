@@ -206,6 +206,9 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void l2_prefetch(const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -479,6 +482,16 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             tma_load_1d(sbase + a.off_dp + x.w * RB, d_src + (size_t)x.y * RB, x.z * RB, full_sa + 8 * st);
           else
             tma_load_1d(sbase + a.off_brp + x.w * BR, br_src + (size_t)x.y * BR, x.z * BR, full_sa + 8 * st);
+          if (OPT && k < K && x.x != LD_D) {
+            // the optimiser state rows of these multiplier rows (same storage
+            // positions) into L2, P steps before their update reads them
+            const bool lam = x.x == LD_LAM;
+            const size_t rb = lam ? RB : BR, rows = lam ? a.n_bus : a.n_brows;
+            const size_t off = (tile * rows + (size_t)x.y) * rb;
+            l2_prefetch(reinterpret_cast<const uint8_t *>(lam ? a.s1_lam : a.s1_br) + off, (unsigned)(x.z * rb));
+            if (a.opt == 4)
+              l2_prefetch(reinterpret_cast<const uint8_t *>(lam ? a.s2_lam : a.s2_br) + off, (unsigned)(x.z * rb));
+          }
         }
       }
     }
