@@ -900,8 +900,8 @@ __global__ void k_compact_nu(const double *nu, long ld, int nl, int NB, double *
 //   k_fused_line<2>: line terms of the final value at y_K (no step, no Q)
 // The step sits on each group's path, so the variants whose per-row step is a
 // long dependent chain (AdaGrad, Adam: divisions, square roots) keep the
-// two-pass kernels (measured on config 3: Adam 121 us/it single-read against
-// 99 us two-pass; the plain step 62 against 96).
+// two-pass kernels (measured on config 3: Adam 105 us/it single-read against
+// 99 us two-pass; the plain step 60.5 against 96).
 constexpr int FT = 512, FW = FT / 32;  // threads (the last warp also issues the TMA copies)
 constexpr int FMAX = 4;                // double2 columns per thread: n_g <= 2 * FT * FMAX
 __host__ __device__ constexpr int fused_rows(int M) { return 6 / M; }  // rows per group: 6 double2 held per thread

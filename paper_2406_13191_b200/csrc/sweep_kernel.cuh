@@ -482,6 +482,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             tma_load_1d(sbase + a.off_dp + x.w * RB, d_src + (size_t)x.y * RB, x.z * RB, full_sa + 8 * st);
           else
             tma_load_1d(sbase + a.off_brp + x.w * BR, br_src + (size_t)x.y * BR, x.z * BR, full_sa + 8 * st);
+#ifndef DCOPF_NO_OPT_L2PF
           if (OPT && k < K && x.x != LD_D) {
             // the optimiser state rows of these multiplier rows (same storage
             // positions) into L2, P steps before their update reads them
@@ -492,6 +493,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
             if (a.opt == 4)
               l2_prefetch(reinterpret_cast<const uint8_t *>(lam ? a.s2_lam : a.s2_br) + off, (unsigned)(x.z * rb));
           }
+#endif
         }
       }
     }
