@@ -57,8 +57,8 @@ struct ClusterArgs {
 };
 
 __device__ __forceinline__ double opt_step(const ClusterArgs &a, double y, double g, double al, double *s1,
-                                           double *s2, double b1t, double b2t) {
-  return opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y, g, al, *s1, *s2, b1t, b2t);
+                                           double *s2, const AdamC &ac) {
+  return opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y, g, al, *s1, *s2, ac);
 }
 
 __device__ __forceinline__ unsigned cl_rank() {
@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
       b1t = b1t * a.beta1;
       b2t = b2t * a.beta2;
     }
+    const AdamC ac = adam_consts(b1t, b2t);
     double val = 0.0;
     // ---------------- A: w_i, theta*_i (not in the angle-free KVL form) ----------------
     if (FORM != kFormKVL) {
@@ -337,16 +338,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
         fc_s[j] = f;
         const double g = f - phi;  // Kirchhoff residual
         val += q * f;
-        if (step) br_s[j] = ost ? opt_step(a, nu, g, alpha, &s1b[j], &s2b[j], b1t, b2t) : nu + alpha * g;
+        if (step) br_s[j] = ost ? opt_step(a, nu, g, alpha, &s1b[j], &s2b[j], ac) : nu + alpha * g;
         if (MODE == kModeEval) a.grad_br[b * (size_t)a.n_br + H.br0 + j] = g;
       } else {
         const double mp = br_s[2 * j], mm = br_s[2 * j + 1];
         const double gp = phi - r.F, gm = -phi - r.F;
         val += -(r.F * (mp + mm));
         if (step) {
-          const double vp = ost ? opt_step(a, mp, gp, alpha, &s1b[2 * j], &s2b[2 * j], b1t, b2t) : mp + alpha * gp;
+          const double vp = ost ? opt_step(a, mp, gp, alpha, &s1b[2 * j], &s2b[2 * j], ac) : mp + alpha * gp;
           const double vm =
-              ost ? opt_step(a, mm, gm, alpha, &s1b[2 * j + 1], &s2b[2 * j + 1], b1t, b2t) : mm + alpha * gm;
+              ost ? opt_step(a, mm, gm, alpha, &s1b[2 * j + 1], &s2b[2 * j + 1], ac) : mm + alpha * gm;
           br_s[2 * j] = (vp > 0.0) ? vp : 0.0;  // mu <- max(mu, 0)
           br_s[2 * j + 1] = (vm > 0.0) ? vm : 0.0;
         }
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
         }
       }
       val += -(li * di);
-      if (step) lam_s[i] = ost ? opt_step(a, li, gl, alpha, &s1l[i], &s2l[i], b1t, b2t) : li + alpha * gl;
+      if (step) lam_s[i] = ost ? opt_step(a, li, gl, alpha, &s1l[i], &s2l[i], ac) : li + alpha * gl;
       if (MODE == kModeEval) a.grad_lam[b * (size_t)a.n_bus + H.bus0 + i] = gl;
     }
     if (FORM == kFormKVL) {
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
           acc = acc + cl_ld(x.f) * x.sx;
         }
         const double kv = br_s[c];
-        if (step) br_s[c] = ost ? opt_step(a, kv, acc, alpha, &s1b[c], &s2b[c], b1t, b2t) : kv + alpha * acc;
+        if (step) br_s[c] = ost ? opt_step(a, kv, acc, alpha, &s1b[c], &s2b[c], ac) : kv + alpha * acc;
         if (MODE == kModeEval) a.grad_br[b * (size_t)a.n_bm + H.cy0 + c] = acc;
       }
     }

@@ -556,6 +556,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       ob1t = ob1t * a.beta1;
       ob2t = ob2t * a.beta2;
     }
+    const AdamC oac = adam_consts(ob1t, ob2t);
     // optimiser-variant update of one row of the lane's instances (the state
     // row sits at the same offset of the state arrays); oload issues the
     // state loads at the start of an item so their latency overlaps the item's
@@ -581,7 +582,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
                      const bool (&do_)[V]) {
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        if (do_[j]) y[j] = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y[j], g[j], alpha, o.s1[j], o.s2[j], ob1t, ob2t);
+        if (do_[j]) y[j] = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y[j], g[j], alpha, o.s1[j], o.s2[j], oac);
       stv<V>((lam_side ? os1l : os1b) + off, o.s1, hb);
       if (ost2) stv<V>((lam_side ? os2l : os2b) + off, o.s2, hb);
     };
