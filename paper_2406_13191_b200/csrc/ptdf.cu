@@ -923,9 +923,9 @@ struct FusedArgs {
   double *nuc;        // compact nu copy (kept current for the skinny evaluate())
   double *part_q;     // [CTA][ngk] column partials of Q_{k+1}
   double *part_line;  // [CTA] line value terms
-  double *part_obj, *part_p;  // [k_fused_gen block]
-  double *acc;        // [2]: sum_g (a p^2 + q p), sum_g p at the current point
-  unsigned *ticket;   // [2]: k_fused_line, k_fused_gen (zero between launches)
+  double *part_obj, *part_p;  // [k_fused_gen block]: sum_g (a p^2 + q p), sum_g p at the current point
+  int ngb;            // k_fused_gen blocks
+  unsigned *ticket;   // k_fused_line's last-CTA ticket (zero between launches)
 };
 
 __device__ __forceinline__ unsigned f_smem(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -1152,16 +1152,33 @@ __global__ void __launch_bounds__(FT, 1) k_fused_line(const FusedArgs a, const G
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // the last CTA: the CTAs' line terms summed by a fixed tree (loads in parallel)
+  // the last CTA: the CTAs' line terms and the generator pass's block terms,
+  // each summed by a fixed tree (loads in parallel)
+  double *ro = stage, *rp = stage + FT / 4;  // (the stages are free now: >= 288 doubles)
   red[tid] = tid < G ? __ldcg(a.part_line + tid) : 0.0;
   for (int b = tid + FT; b < G; b += FT) red[tid] += __ldcg(a.part_line + b);
+  if (tid < FT / 4) {
+    double to = 0.0, tp = 0.0;
+    for (int b = tid; b < a.ngb; b += FT / 4) {
+      to += __ldcg(a.part_obj + b);
+      tp += __ldcg(a.part_p + b);
+    }
+    ro[tid] = to;
+    rp[tid] = tp;
+  }
   __syncthreads();
   for (int w = FT / 2; w > 0; w >>= 1) {
-    if (tid < w) red[tid] += red[tid + w];
+    if (tid < w) {
+      red[tid] += red[tid + w];
+      if (w < FT / 4) {
+        ro[tid] += ro[tid + w];
+        rp[tid] += rp[tid + w];
+      }
+    }
     __syncthreads();
   }
   if (tid == 0) {
-    finish_one<false>(f, 0, __ldcg(a.acc), __ldcg(a.acc + 1), red[0]);
+    finish_one<false>(f, 0, ro[0], rp[0], red[0]);
     a.ticket[0] = 0u;
   }
 }
@@ -1172,7 +1189,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_line(const FusedArgs a, const G
 constexpr int FGW = 16;
 __global__ void __launch_bounds__(FGW * 32) k_fused_gen(const FusedArgs a, const GemmArgs g, int G) {
   __shared__ double red[FGW][32];
-  __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = blockIdx.x * 32 + lane;
   double q = 0.0;
@@ -1209,46 +1225,10 @@ __global__ void __launch_bounds__(FGW * 32) k_fused_gen(const FusedArgs a, const
       so += __shfl_xor_sync(0xffffffffu, so, off);
       sp += __shfl_xor_sync(0xffffffffu, sp, off);
     }
-    if (lane == 0) {
+    if (lane == 0) {  // the block's generator terms (summed by the next line kernel's finisher)
       a.part_obj[blockIdx.x] = so;
       a.part_p[blockIdx.x] = sp;
-      __threadfence();
-      last = atomicAdd(&a.ticket[1], 1u) == gridDim.x - 1;
     }
-  }
-  __syncthreads();
-  if (!last) return;
-  // the last block: the blocks' generator terms summed by a fixed tree (loads in parallel)
-  __threadfence();
-  const int t = threadIdx.x, nb = gridDim.x;
-  double to = 0.0, tp = 0.0;
-  for (int b = t; b < nb; b += FGW * 32) {
-    to += __ldcg(a.part_obj + b);
-    tp += __ldcg(a.part_p + b);
-  }
-  double *ro = &red[0][0], *rp = ro + FGW * 16;
-  __syncthreads();
-  if (t < FGW * 16) {
-    ro[t] = to;
-    rp[t] = tp;
-  }
-  __syncthreads();
-  if (t >= FGW * 16) {  // fold the upper half in (fixed pairing t - FGW * 16 <-> t)
-    ro[t - FGW * 16] += to;
-    rp[t - FGW * 16] += tp;
-  }
-  __syncthreads();
-  for (int w = FGW * 8; w > 0; w >>= 1) {
-    if (t < w) {
-      ro[t] += ro[t + w];
-      rp[t] += rp[t + w];
-    }
-    __syncthreads();
-  }
-  if (t == 0) {
-    a.acc[0] = ro[0];
-    a.acc[1] = rp[0];
-    a.ticket[1] = 0u;
   }
 }
 
@@ -1376,7 +1356,7 @@ struct PtdfState {
   // group, frpc >= rows per CTA
   bool fused = false;
   int nsm = 148, fG = 0, fS = 0, fR = 0, fgb = 0, frpc = 0;
-  double *fq = nullptr, *fline = nullptr, *fobj = nullptr, *fp = nullptr, *facc = nullptr;
+  double *fq = nullptr, *fline = nullptr, *fobj = nullptr, *fp = nullptr;
   // medium batches: split-K scratch of GEMM1 ([S][n_g pad][B_pad]), CTA slots of the GPU
   double *qsplit = nullptr;
   size_t qsplit_n = 0;
@@ -1943,7 +1923,7 @@ void ptdf_destroy(PtdfState *st) {
   cudaSetDevice(st->device);
   free_batch(st);
   double *dp[] = {st->Ha, st->HgT, st->Hg, st->F, st->gc, st->glo, st->ghi, st->ga, st->scratch, st->nuc, st->pcv,
-                  st->sp_obj, st->sp_p, st->sp_line, st->qsplit, st->fq, st->fline, st->fobj, st->fp, st->facc};
+                  st->sp_obj, st->sp_p, st->sp_line, st->qsplit, st->fq, st->fline, st->fobj, st->fp};
   for (double *p : dp) cudaFree(p);
   for (int c = 0; c < 2; ++c) {
     if (st->sub[c]) cudaStreamDestroy(st->sub[c]);
@@ -2017,7 +1997,6 @@ int ptdf_set_batch(PtdfState *st, int64_t B, const double *load, cudaStream_t s,
         if (!rc0) rc0 = dalloc(&st->fline, st->fG, err);
         if (!rc0) rc0 = dalloc(&st->fobj, st->fgb, err);
         if (!rc0) rc0 = dalloc(&st->fp, st->fgb, err);
-        if (!rc0) rc0 = dalloc(&st->facc, 2, err);
         if (rc0) return rc0;
       }
     }
@@ -2068,7 +2047,7 @@ int fused_iterate(PtdfState *st, int64_t K, GemmArgs g, FinArgs f, cudaStream_t 
   a.part_line = st->fline;
   a.part_obj = st->fobj;
   a.part_p = st->fp;
-  a.acc = st->facc;
+  a.ngb = st->fgb;
   a.ticket = st->ticket;
   GemmArgs gg = gen_args(st);
   const size_t smem = fused_smem(a.ldh, st->fR, a.S, a.rpc);
