@@ -1,7 +1,7 @@
 # round-2 evidence on a B200: smoke, the GPU suite, every bench line, the
 # launch list of the default bench and ncu --set full captures of the sweep
 set -x
-O=gpurun_out/final
+O=${O:-gpurun_out/final}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build=$?
 timeout 900 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo smoke=$?
@@ -23,10 +23,13 @@ B config4b_PTDF --workload config4b --form PTDF --no-cpu-baseline --steps 20 --w
 B config3_F2 --workload config3 --steps 2000 --warmup 100 --no-cpu-baseline
 B config3_KVL_adam --workload config3 --form KVL --opt adam --alpha 0.1 --steps 2000 --warmup 100 --no-cpu-baseline
 B config3_PTDF_adam --workload config3 --form PTDF --opt adam --alpha 5 --decay inv:200 --steps 2000 --warmup 100 --no-cpu-baseline
+B config3_PTDF --workload config3 --form PTDF --steps 1000 --warmup 20 --no-cpu-baseline --no-gap
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_config4_F2.csv python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_launch.log 2>&1; echo launches=$?
 N() { tag=$1; shift; timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -c 1 -o $O/ncu_$tag python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-gap "$@" > $O/ncu_$tag.log 2>&1; echo ncu_$tag=$?; }
 N config4_F2
 N config4_KVL --form KVL
 N shard1024_F2 --batch 1024
 N config4b_KVL_adam --workload config4b --form KVL --opt adam
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_config3_PTDF.csv python bench.py --workload config3 --form PTDF --steps 20 --warmup 3 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_launch_ptdf.log 2>&1; echo launches_ptdf=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused -c 2 -o $O/ncu_k_fused_config3 python bench.py --workload config3 --form PTDF --steps 5 --warmup 3 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_fused.log 2>&1; echo ncu_fused=$?
 echo done
