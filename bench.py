@@ -551,15 +551,18 @@ def main():
         status_h = torch.empty(B, dtype=torch.int32).pin_memory()
         h2d = load_host.numel() * 8 + (0 if outs_host is None else outs_host.numel() * 4)
         d2h = B * (8 + 8 + 4)
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        h.set_instance_batch(load_host, outs_host, stream=stream)
-        h.iterate(K, alpha, stream=stream)
-        h.get_bound(bound_h, best_h, status_h, stream=stream)
-        torch.cuda.synchronize()
-        barrier()
-        e2e_s = time.perf_counter() - t0
+        samples = []
+        for _ in range(3):  # the median of three calls (one call is exposed to host-side noise)
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            h.set_instance_batch(load_host, outs_host, stream=stream)
+            h.iterate(K, alpha, stream=stream)
+            h.get_bound(bound_h, best_h, status_h, stream=stream)
+            torch.cuda.synchronize()
+            barrier()
+            samples.append(time.perf_counter() - t0)
+        e2e_s = sorted(samples)[1]
         te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
             tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
@@ -568,7 +571,8 @@ def main():
         e2e = {"value": B_total * K / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": h2d / max(K, 1),
                "d2h_bytes_per_step": d2h / max(K, 1), "h2d_bytes_per_call": int(h2d),
                "d2h_bytes_per_call": int(d2h), "steps_per_call": K,
-               "timed": "set_instance_batch(host pinned) + iterate(K) + get_bound(host), wall clock, max over ranks"}
+               "timed": "set_instance_batch(host pinned) + iterate(K) + get_bound(host), wall clock, max over ranks, "
+                        "median of 3 calls", "call_seconds": samples}
 
     dense = form == dual.FORM_PTDF
     if rank == 0 and dense and B > 4:

@@ -1192,19 +1192,17 @@ __global__ void __launch_bounds__(FGW * 32) k_fused_gen(const FusedArgs a, const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = blockIdx.x * 32 + lane;
   double q = 0.0;
-  if (col < g.ng) {  // CTAs [b0, b1) in order; four loads in flight ahead of the adds
+  if (col < g.ng) {  // CTAs [b0, b1) in order, all loads in flight ahead of the adds
     const double *pq = a.part_q + col;
-    int b = G * warp / FGW;
-    const int b1 = G * (warp + 1) / FGW;
-    for (; b + 4 <= b1; b += 4) {
-      const double v0 = __ldcg(pq + (size_t)b * a.ldh), v1 = __ldcg(pq + (size_t)(b + 1) * a.ldh);
-      const double v2 = __ldcg(pq + (size_t)(b + 2) * a.ldh), v3 = __ldcg(pq + (size_t)(b + 3) * a.ldh);
-      q += v0;
-      q += v1;
-      q += v2;
-      q += v3;
-    }
-    for (; b < b1; ++b) q += __ldcg(pq + (size_t)b * a.ldh);
+    const int b0 = G * warp / FGW, nb = G * (warp + 1) / FGW - b0;
+    constexpr int U = 12;  // >= ceil(CTAs / FGW) for up to 192 CTAs
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = u < nb ? __ldcg(pq + (size_t)(b0 + u) * a.ldh) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (u < nb) q += v[u];
+    for (int b = b0 + U; b < b0 + nb; ++b) q += __ldcg(pq + (size_t)b * a.ldh);  // (> 192 CTAs)
   }
   red[warp][lane] = q;
   __syncthreads();
