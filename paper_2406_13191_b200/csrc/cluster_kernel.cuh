@@ -107,7 +107,9 @@ __device__ __forceinline__ double2 cl_ld2(unsigned addr) {
 #endif
 constexpr int kClusterThreads = DCOPF_CLUSTER_THREADS;
 
-template <int FORM, int MODE>
+// OPT: the optimiser-variant instantiation (the plain step's kernel carries
+// none of the variants' code: its registers stay with the plain path)
+template <int FORM, int MODE, bool OPT = false>
 __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int BRW = (FORM == kFormF2) ? 1 : 2;
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
   }
   for (int j = tid; j < nbm; j += nthr) br_s[j] = br_g[j];
   // optimiser state (same layout as the multipliers)
-  const bool ost = (MODE == kModeStep) && a.opt != DCOPF_OPT_PLAIN;
+  const bool ost = OPT && (MODE == kModeStep) && a.opt != DCOPF_OPT_PLAIN;
   const bool ost2 = ost && a.opt == DCOPF_OPT_ADAM;
   double *s1l = reinterpret_cast<double *>(smem + H.off_s1l), *s2l = reinterpret_cast<double *>(smem + H.off_s2l);
   double *s1b = reinterpret_cast<double *>(smem + H.off_s1b), *s2b = reinterpret_cast<double *>(smem + H.off_s2b);
@@ -279,7 +281,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster(const ClusterArg
       b1t = b1t * a.beta1;
       b2t = b2t * a.beta2;
     }
-    const AdamC ac = adam_consts(b1t, b2t);
+    AdamC ac = {1.0, 1.0, 1.0, 1.0};
+    if (ost2) ac = adam_consts(b1t, b2t);
     double val = 0.0;
     // ---------------- A: w_i, theta*_i (not in the angle-free KVL form) ----------------
     if (FORM != kFormKVL) {

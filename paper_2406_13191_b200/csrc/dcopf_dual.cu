@@ -525,9 +525,12 @@ int configure_cluster(dcopf_dual_t h) {
     auto fn = (h->form == DCOPF_FORM_FLOW_BOX)   ? k_cluster<kFormF2, kModeStep>
               : (h->form == DCOPF_FORM_CYCLE) ? k_cluster<kFormKVL, kModeStep>
                                               : k_cluster<kFormF1, kModeStep>;
-    const void *fns[6] = {(const void *)k_cluster<kFormF2, kModeStep>,  (const void *)k_cluster<kFormF2, kModeEval>,
+    const void *fns[9] = {(const void *)k_cluster<kFormF2, kModeStep>,  (const void *)k_cluster<kFormF2, kModeEval>,
                           (const void *)k_cluster<kFormF1, kModeStep>,  (const void *)k_cluster<kFormF1, kModeEval>,
-                          (const void *)k_cluster<kFormKVL, kModeStep>, (const void *)k_cluster<kFormKVL, kModeEval>};
+                          (const void *)k_cluster<kFormKVL, kModeStep>, (const void *)k_cluster<kFormKVL, kModeEval>,
+                          (const void *)k_cluster<kFormF2, kModeStep, true>,
+                          (const void *)k_cluster<kFormF1, kModeStep, true>,
+                          (const void *)k_cluster<kFormKVL, kModeStep, true>};
     for (const void *f : fns) {
       CK(h, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
       if (C > 8) CK(h, cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -620,9 +623,10 @@ int launch_cluster(dcopf_dual_t h, const ClusterArgs &a, cudaStream_t s) {
   cfg.numAttrs = 1;
   // (the dynamic shared-memory limit is per function and shared by every
   // handle: set it for this handle's plan right before its launch)
-  auto fn = (h->form == DCOPF_FORM_FLOW_BOX) ? k_cluster<kFormF2, MODE>
-            : (h->form == DCOPF_FORM_CYCLE)  ? k_cluster<kFormKVL, MODE>
-                                             : k_cluster<kFormF1, MODE>;
+  const bool opt = MODE == kModeStep && h->opt.variant != DCOPF_OPT_PLAIN;
+  auto fn = (h->form == DCOPF_FORM_FLOW_BOX) ? (opt ? k_cluster<kFormF2, MODE, true> : k_cluster<kFormF2, MODE>)
+            : (h->form == DCOPF_FORM_CYCLE)  ? (opt ? k_cluster<kFormKVL, MODE, true> : k_cluster<kFormKVL, MODE>)
+                                             : (opt ? k_cluster<kFormF1, MODE, true> : k_cluster<kFormF1, MODE>);
   CK(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cplan.smem));
   CK(h, cudaLaunchKernelEx(&cfg, fn, a));
   CK(h, cudaGetLastError());

@@ -556,7 +556,8 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       ob1t = ob1t * a.beta1;
       ob2t = ob2t * a.beta2;
     }
-    const AdamC oac = adam_consts(ob1t, ob2t);
+    AdamC oac = {1.0, 1.0, 1.0, 1.0};
+    if (OPT && a.opt == 4) oac = adam_consts(ob1t, ob2t);
     // optimiser-variant update of one row of the lane's instances (the state
     // row sits at the same offset of the state arrays); oload issues the
     // state loads at the start of an item so their latency overlaps the item's
