@@ -1006,6 +1006,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_line(const FusedArgs a, const G
   };
   if (producer)
     for (int gi = 0; gi < min(S, ngr); ++gi) issue(gi);
+  // programmatic dependent launch: everything above (barriers, the rows' data
+  // written by the previous line kernel, the first H_g copies) overlaps the
+  // tail of the preceding generator pass; p*_k is read after it completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   double2 pv[M], qv[M];
   const bool tail = tid + FT * (M - 1) >= h2;  // this thread's last column pair is past the row
 #pragma unroll
@@ -1189,6 +1193,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_line(const FusedArgs a, const G
 constexpr int FGW = 16;
 __global__ void __launch_bounds__(FGW * 32) k_fused_gen(const FusedArgs a, const GemmArgs g, int G) {
   __shared__ double red[FGW][32];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the line kernel's partials are complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next line kernel may start its prologue
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = blockIdx.x * 32 + lane;
   double q = 0.0;
@@ -2065,9 +2071,24 @@ int fused_loop(PtdfState *st, int64_t K, const FusedArgs &a, GemmArgs g, const G
   PCK(cudaFuncSetAttribute(k_fused_line<1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   PCK(cudaFuncSetAttribute(k_fused_line<2, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int G = st->fG, T = FT;
-  k_fused_line<0, M><<<G, T, smem, s>>>(a, g, f);
-  k_fused_gen<<<st->fgb, FGW * 32, 0, s>>>(a, gg, G);
-  PCK(cudaGetLastError());
+  // both kernels launched with programmatic stream serialization (each waits
+  // for its predecessor with griddepcontrol.wait where it reads its results)
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cl = {}, cg = {};
+  cl.gridDim = dim3(G);
+  cl.blockDim = dim3(T);
+  cl.dynamicSmemBytes = smem;
+  cl.stream = s;
+  cl.attrs = at;
+  cl.numAttrs = 1;
+  cg = cl;
+  cg.gridDim = dim3(st->fgb);
+  cg.blockDim = dim3(FGW * 32);
+  cg.dynamicSmemBytes = 0;
+  PCK(cudaLaunchKernelEx(&cl, k_fused_line<0, M>, a, g, f));
+  PCK(cudaLaunchKernelEx(&cg, k_fused_gen, a, gg, G));
   for (int64_t k = 0; k <= K; ++k) {
     const bool step = k < K;
     if (step && st->opt.variant == DCOPF_OPT_ADAM) {  // beta^t by repeated products (reading A-26)
@@ -2079,12 +2100,11 @@ int fused_loop(PtdfState *st, int64_t K, const FusedArgs &a, GemmArgs g, const G
     g.b2t = f.b2t = st->b2t;
     f.first = k == 0;
     if (step) {
-      k_fused_line<1, M><<<G, T, smem, s>>>(a, g, f);
-      k_fused_gen<<<st->fgb, FGW * 32, 0, s>>>(a, gg, G);
+      PCK(cudaLaunchKernelEx(&cl, k_fused_line<1, M>, a, g, f));
+      PCK(cudaLaunchKernelEx(&cg, k_fused_gen, a, gg, G));
     } else {
-      k_fused_line<2, M><<<G, T, smem, s>>>(a, g, f);
+      PCK(cudaLaunchKernelEx(&cl, k_fused_line<2, M>, a, g, f));
     }
-    PCK(cudaGetLastError());
   }
   st->k_base += K;
   return DCOPF_OK;
