@@ -58,7 +58,13 @@ struct ClusterArgs {
 
 __device__ __forceinline__ double opt_step(const ClusterArgs &a, double y, double g, double al, double *s1,
                                            double *s2, const AdamC &ac) {
-  return opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y, g, al, *s1, *s2, ac);
+  double yv[1] = {y}, s1v[1] = {*s1}, s2v[1] = {*s2};
+  const double gv[1] = {g};
+  const bool on[1] = {true};
+  opt_update_v<1>(a.opt, a.rho, a.beta1, a.beta2, a.eps, yv, gv, al, s1v, s2v, ac, on);
+  *s1 = s1v[0];
+  *s2 = s2v[0];
+  return yv[0];
 }
 
 __device__ __forceinline__ unsigned cl_rank() {

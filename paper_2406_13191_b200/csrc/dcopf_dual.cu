@@ -86,6 +86,7 @@ struct dcopf_dual_s {
   // sched_V instances per lane, sched_C parts per tile)
   Schedule sch;
   int sched_W = 0, sched_V = 0, sched_C = 0, sched_nw = 0;
+  bool sched_opt = false;  // compiled with the optimiser kernels' shared-memory block
   int tile_V = 2, tile_C = 1;  // loaded batch: instances per lane, parts (CTAs) per tile
   uint8_t *d_prog = nullptr;
   int *d_part_step0 = nullptr;
@@ -327,7 +328,9 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
 // split-tile compiler (split_schedule.cpp; C = 1 is the unsplit sweep).
 int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
   const int nw = sweep_warps(V, h->opt.variant != DCOPF_OPT_PLAIN);
-  if (h->sched_W == W && h->sched_V == V && h->sched_C == C && h->sched_nw == nw) return DCOPF_OK;
+  const bool optv = h->opt.variant != DCOPF_OPT_PLAIN;
+  if (h->sched_W == W && h->sched_V == V && h->sched_C == C && h->sched_nw == nw && h->sched_opt == optv)
+    return DCOPF_OK;
   // the same tiling for another warp count (an optimiser variant switched on
   // or off with a batch loaded): keep the chunk and ring life, so the storage
   // order of the loaded state -- which depends only on them -- stays valid
@@ -351,6 +354,10 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
       sc = Schedule();
       sc.ring_life = life;
       sc.pool_gap = 3;  // soft step sync: consumer warps drift by up to two steps
+      // optimiser kernels: the tile's state-row byte offsets (16 B) and each
+      // consumer warp's step constants (64 B) live in shared memory, not in
+      // registers across the step loop (sweep_kernel.cuh)
+      sc.opt_bytes = optv ? 16 + 64 * nw : 0;
       const CycleBasis *cy = h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr;
       const std::string err = build_schedule_split(h->ni, ch, P, W, V, nw, C, {}, &sc, cy);
       if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
@@ -417,6 +424,7 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
   h->sched_V = V;
   h->sched_C = C;
   h->sched_nw = nw;
+  h->sched_opt = optv;
   return DCOPF_OK;
 }
 
@@ -730,7 +738,8 @@ int launch_sweep(dcopf_dual_t h, const SweepArgs &a, cudaStream_t s) {
   constexpr int N2 = kSweepWarps2, N4 = kSweepWarps4;
   const bool opt = !EVAL && h->opt.variant != DCOPF_OPT_PLAIN;  // optimiser variants
   const bool v4 = h->tile_V == 4;
-  if (h->sched_nw != sweep_warps(h->tile_V, h->opt.variant != DCOPF_OPT_PLAIN))
+  if (h->sched_nw != sweep_warps(h->tile_V, h->opt.variant != DCOPF_OPT_PLAIN) ||
+      h->sched_opt != (h->opt.variant != DCOPF_OPT_PLAIN))
     return fail(h, DCOPF_ESTATE, "batched schedule compiled for another warp count");
   if (h->form == DCOPF_FORM_FLOW_BOX) {
     if (v4) return opt ? launch_sweep_t<kFormF2, false, true, 4, N4>(h, a, s) : launch_sweep_t<kFormF2, EVAL, false, 4, N4>(h, a, s);

@@ -224,7 +224,7 @@ void layout_smem(Schedule &S, int nl, int nw) {
   // full[S], empty[S], A-done[4], B-done[4] mbarriers, then the part's step
   // range (2 int, padded to 16 bytes)
   S.off_bar = off;
-  off = al(off + 16 * S.S + 64 + 16);
+  off = al(off + 16 * S.S + 64 + 16 + S.opt_bytes);
   const int TS = 32 * S.V;  // per-tile instance slots (a lane's instances are below 32 V)
   S.off_frz = off;  // frozen flags [TS] int, then running best and previous g [TS] double
   off = al(off + 4 * TS + 2 * 8 * TS);

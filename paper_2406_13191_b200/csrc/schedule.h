@@ -104,6 +104,8 @@ struct Schedule {
   std::vector<int> part_bus0;               // [C+1] internal bus range owned by each part
   int halo_a = 0, halo_b = 0;               // halo items over all parts (recomputed codes)
   int ring_life = 6;                        // rows live <= this many steps go to the rings
+  int opt_bytes = 0;                        // optimiser kernels: per-CTA state-row offsets + per-warp
+                                            // step constants, after the barriers (set before compiling)
   int pool_gap = 1;                         // theta* / f* pool slots are reused only pool_gap steps after
                                             // their last read (2: consumer warps may drift by one step)
   int ring_lam = 0, ring_d = 0, ring_br = 0, n_copies = 0, n_sticky_copies = 0;

@@ -284,6 +284,18 @@ __device__ __forceinline__ unsigned lds_u32(unsigned sa) {
 __device__ __forceinline__ void sts_u16(unsigned sa, unsigned v) {
   *reinterpret_cast<unsigned short *>(__cvta_shared_to_generic((size_t)sa)) = (unsigned short)v;
 }
+__device__ __forceinline__ void sts_u64(unsigned sa, unsigned long long v) {
+  *reinterpret_cast<unsigned long long *>(__cvta_shared_to_generic((size_t)sa)) = v;
+}
+__device__ __forceinline__ unsigned long long lds_u64(unsigned sa) {
+  return *reinterpret_cast<const unsigned long long *>(__cvta_shared_to_generic((size_t)sa));
+}
+__device__ __forceinline__ void sts_f64(unsigned sa, double v) {
+  *reinterpret_cast<double *>(__cvta_shared_to_generic((size_t)sa)) = v;
+}
+__device__ __forceinline__ double lds_f64(unsigned sa) {
+  return *reinterpret_cast<const double *>(__cvta_shared_to_generic((size_t)sa));
+}
 __device__ __forceinline__ void sts_u32(unsigned sa, unsigned v) {
   *reinterpret_cast<unsigned *>(__cvta_shared_to_generic((size_t)sa)) = v;
 }
@@ -412,9 +424,18 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   // instance (within the tile) of this lane's j-th value
   auto inst = [&](int j) { return (j < 2) ? 2 * lane + j : hW + 2 * lane + (j - 2); };
 
+  // optimiser kernels (schedule opt_bytes): after the step range, the tile's
+  // byte offsets of its lambda-side / branch-side state rows, then per consumer
+  // warp [1 - beta1^t, 1 - beta2^t, their reciprocals, beta1^t, beta2^t] -- kept
+  // here rather than in registers across the step loop, where they spilled
+  const unsigned opt_sa = bdone_sa + 48;
   if (threadIdx.x == 0) {
     s_rng[0] = a.part_step0[DCOPF_PART];
     s_rng[1] = a.part_step0[DCOPF_PART + 1];
+    if (OPT) {
+      sts_u64(opt_sa, (unsigned long long)(DCOPF_TILE * (size_t)a.n_bus * a.row_bytes));
+      sts_u64(opt_sa + 8, (unsigned long long)(DCOPF_TILE * (size_t)a.n_brows * a.br_row_bytes));
+    }
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], SOFT ? CT : 1);  // soft: one arrival per consumer thread
@@ -507,14 +528,18 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   const unsigned brp = sbase + a.off_brp + lofs;
   const unsigned lamp = sbase + a.off_lamp + lofs;
   const unsigned dp = sbase + a.off_dp + lofs;
-  // optimiser state rows of this tile (OPT kernels)
-  const size_t tile0 = OPT ? DCOPF_TILE : 0;
-  uint8_t *os1l = OPT ? reinterpret_cast<uint8_t *>(a.s1_lam) + tile0 * (size_t)a.n_bus * RB + lofs : nullptr;
-  uint8_t *os2l = OPT ? reinterpret_cast<uint8_t *>(a.s2_lam) + tile0 * (size_t)a.n_bus * RB + lofs : nullptr;
-  uint8_t *os1b = OPT ? reinterpret_cast<uint8_t *>(a.s1_br) + tile0 * (size_t)a.n_brows * BR + lofs : nullptr;
-  uint8_t *os2b = OPT ? reinterpret_cast<uint8_t *>(a.s2_br) + tile0 * (size_t)a.n_brows * BR + lofs : nullptr;
+  // optimiser state rows of this tile (OPT kernels): base + the tile offset
+  // from shared memory + the lane's 16 bytes, formed at each use
+  auto obase = [&](bool lam_side, bool second) -> uint8_t * {
+    const double *b = lam_side ? (second ? a.s2_lam : a.s1_lam) : (second ? a.s2_br : a.s1_br);
+    return reinterpret_cast<uint8_t *>(const_cast<double *>(b)) + lds_u64(opt_sa + (lam_side ? 0 : 8)) + lofs;
+  };
   const bool ost2 = OPT && a.opt == 4;  // Adam: two state arrays
-  double ob1t = a.b1t, ob2t = a.b2t;
+  const unsigned oc_sa = opt_sa + 16 + 64 * warp;  // this warp's step constants
+  if (OPT && lane == 0) {
+    sts_f64(oc_sa + 32, a.b1t);
+    sts_f64(oc_sa + 40, a.b2t);
+  }
   const unsigned thp = sbase + a.off_th + V * lane;  // theta*_i code rows
   const unsigned fcp = sbase + a.off_fc + V * lane;  // f*_l code rows (F2)
   // Consumer warps are not stepped in lock-step.  In step g a warp waits on
@@ -552,12 +577,17 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #pragma unroll
     for (int j = 0; j < V; ++j) stp[j] = !EVAL && !last && !frz[inst(j)];
     const double alpha = (EVAL || last) ? 0.0 : a.alpha[k];
-    if (OPT && !EVAL && !last) {  // Adam's beta^t, t = steps since the state was reset
-      ob1t = ob1t * a.beta1;
-      ob2t = ob2t * a.beta2;
+    if (OPT && a.opt == 4 && !last && lane == 0) {  // Adam's beta^t, t = steps since the state was reset
+      const double b1t = lds_f64(oc_sa + 32) * a.beta1, b2t = lds_f64(oc_sa + 40) * a.beta2;
+      const AdamC c = adam_consts(b1t, b2t);
+      sts_f64(oc_sa, c.d1);
+      sts_f64(oc_sa + 8, c.d2);
+      sts_f64(oc_sa + 16, c.r1);
+      sts_f64(oc_sa + 24, c.r2);
+      sts_f64(oc_sa + 32, b1t);
+      sts_f64(oc_sa + 40, b2t);
     }
-    AdamC oac = {1.0, 1.0, 1.0, 1.0};
-    if (OPT && a.opt == 4) oac = adam_consts(ob1t, ob2t);
+    if (OPT) __syncwarp();
     // optimiser-variant update of one row of the lane's instances (the state
     // row sits at the same offset of the state arrays); oload issues the
     // state loads at the start of an item so their latency overlaps the item's
@@ -567,11 +597,11 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
 #pragma unroll
       for (int j = 0; j < V; ++j) o.s1[j] = o.s2[j] = 0.0;
       if (on) {
-        const DV<V> x = ldv<V>((lam_side ? os1l : os1b), (int)off, hb);
+        const DV<V> x = ldv<V>(obase(lam_side, false), (int)off, hb);
 #pragma unroll
         for (int j = 0; j < V; ++j) o.s1[j] = x.v[j];
         if (ost2) {
-          const DV<V> y = ldv<V>((lam_side ? os2l : os2b), (int)off, hb);
+          const DV<V> y = ldv<V>(obase(lam_side, true), (int)off, hb);
 #pragma unroll
           for (int j = 0; j < V; ++j) o.s2[j] = y.v[j];
         }
@@ -581,11 +611,14 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     // y[j] <- update (only where do_[j]); state stored back
     auto ostep = [&](OState<V> &o, double (&y)[V], const double (&g)[V], size_t off, bool lam_side,
                      const bool (&do_)[V]) {
-#pragma unroll
-      for (int j = 0; j < V; ++j)
-        if (do_[j]) y[j] = opt_update(a.opt, a.rho, a.beta1, a.beta2, a.eps, y[j], g[j], alpha, o.s1[j], o.s2[j], oac);
-      stv<V>((lam_side ? os1l : os1b) + off, o.s1, hb);
-      if (ost2) stv<V>((lam_side ? os2l : os2b) + off, o.s2, hb);
+      AdamC oac = {1.0, 1.0, 1.0, 1.0};
+      if (ost2) {
+        const double2 c01 = lds_f64x2(oc_sa), c23 = lds_f64x2(oc_sa + 16);
+        oac = AdamC{c01.x, c01.y, c23.x, c23.y};
+      }
+      opt_update_v<V>(a.opt, a.rho, a.beta1, a.beta2, a.eps, y, g, alpha, o.s1, o.s2, oac, do_);
+      stv<V>(obase(lam_side, false) + off, o.s1, hb);
+      if (ost2) stv<V>(obase(lam_side, true) + off, o.s2, hb);
     };
     double v[V];
 #pragma unroll
