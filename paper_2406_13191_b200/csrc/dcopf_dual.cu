@@ -342,7 +342,10 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
 #ifndef DCOPF_PREFETCH_F2
 #define DCOPF_PREFETCH_F2 2
 #endif
-  const int P = (h->form == DCOPF_FORM_CYCLE) ? 1 : (h->form == DCOPF_FORM_FLOW_BOX ? DCOPF_PREFETCH_F2 : 2);
+#ifndef DCOPF_PREFETCH_KVL
+#define DCOPF_PREFETCH_KVL 1
+#endif
+  const int P = (h->form == DCOPF_FORM_CYCLE) ? DCOPF_PREFETCH_KVL : (h->form == DCOPF_FORM_FLOW_BOX ? DCOPF_PREFETCH_F2 : 2);
   const int chs[] = {48, 40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1},
             lifes[] = {6, 4, 2};
   Schedule sc;

@@ -52,12 +52,18 @@
 // Per-entity arithmetic and operation order match dual_kernels.cuh and the
 // oracle (reading A-19); only the dual value is summed in another fixed order.
 #pragma once
+#include <cstddef>
 #include <type_traits>
 
 #include "dual_kernels.cuh"
 #include "schedule.h"
 
 namespace dcopf {
+
+// (byte offsets of the records' wpos field: the optimiser kernels read the next
+// item's wpos alone to prefetch its state rows)
+static_assert(offsetof(RecC, wpos) == 0 && offsetof(RecB, wpos) == 24 && offsetof(RecD, wpos) == 4,
+              "record layout");
 
 struct SweepArgs {
   double *lam0, *lam1, *br0, *br1;  // ping-pong state (tile-major)
@@ -208,6 +214,9 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
 }
 __device__ __forceinline__ void l2_prefetch(const void *src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -620,6 +629,32 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       stv<V>(obase(lam_side, false) + off, o.s1, hb);
       if (ost2) stv<V>(obase(lam_side, true) + off, o.s2, hb);
     };
+    // the NEXT item's optimiser state rows into L1 (OPT kernels, F2 / F1): its
+    // oload at the item's start then hits L1 instead of waiting the L2 latency
+    // (the producer already brought the rows into L2); rec_sa: the record's
+    // wpos.  Measured (config 4b, Adam, K = 100, profiles/r2/fastdiv): F2 +1.8%;
+    // KVL -7% (its 48-bus steps' prefetches overrun the L1 left beside the
+    // 220 KB of shared memory), so KVL does without
+    auto opf = [&](unsigned rec_sa, bool lam_side, int rb, bool two) {
+#ifndef DCOPF_NO_OPT_L1PF
+      if (OPT && FORM != kFormKVL && !EVAL && write && act) {
+        const int wpos = (int)lds_u32(rec_sa);
+        if (wpos >= 0) {
+          const size_t off = (size_t)wpos * rb;
+          uint8_t *p1 = obase(lam_side, false) + off;
+          prefetch_l1(p1);
+          if (V == 4) prefetch_l1(p1 + hb);
+          if (two) prefetch_l1(p1 + RB);
+          if (ost2) {
+            uint8_t *p2 = obase(lam_side, true) + off;
+            prefetch_l1(p2);
+            if (V == 4) prefetch_l1(p2 + hb);
+            if (two) prefetch_l1(p2 + RB);
+          }
+        }
+      }
+#endif
+    };
     double v[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) v[j] = 0.0;
@@ -656,6 +691,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         const unsigned Cv = prog + h2.w, G = prog + h3.x;
         ITEM_LOOP(ph, tr, h0.w) {
           const RecC r = lds_rec<RecC>(Cv + j * (unsigned)sizeof(RecC));
+          if (OPT && j + 1 < je) opf(Cv + (j + 1) * (unsigned)sizeof(RecC), true, RB, false);
           OState<V> ost = oload((size_t)r.wpos * RB, true, OPT && !EVAL && write && act);
           const DV<V> li = ldsv<V>(lamp, r.ls, hb), di = ldsv<V>(dp, r.ds, hb);
           double gl[V];
@@ -800,6 +836,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         const unsigned Dv = prog + h2.x, De = prog + h2.y;
         ITEM_LOOP(2, wr.z, h0.x) {
           const RecD r = lds_rec<RecD>(Dv + j * (unsigned)sizeof(RecD));
+          if (OPT && j + 1 < je) opf(Dv + (j + 1) * (unsigned)sizeof(RecD) + 4, false, BR, false);
           OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
           const DV<V> kv = ldsv<V>(brp, r.ks, hb);
           double acc[V];
@@ -1040,6 +1077,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
         };
         ITEM_LOOP(1, wr.y, h0.z) {
           const RecB r = lds_rec<RecB>(Bv + j * (unsigned)sizeof(RecB));
+          if (OPT && j + 1 < je) opf(Bv + (j + 1) * (unsigned)sizeof(RecB) + 24, false, BR, FORM == kFormF1);
           if (r.obr >= 0 && flagged(r.obr)) bitem(r, std::integral_constant<bool, true>{});  // (obr < 0: never out)
           else bitem(r, std::integral_constant<bool, false>{});
         }

@@ -1,6 +1,7 @@
 # A/B of library builds (paper_2406_13191_b200/lib/variants/NAME.so vs the current build) on bench lines,
 # alternating builds, K = 100:  bash tools/gpu_r2_ab_lib.sh NAME [NAME...]
 O=gpurun_out/ab_lib
+rm -rf $O
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build=$?
 V=paper_2406_13191_b200/lib/variants
@@ -12,6 +13,7 @@ for rep in 1 2; do
     B "$L" --workload config4b --form KVL --opt adam > $O/${v}_kvl_adam_$rep.json 2>/dev/null
     B "$L" --workload config4b --form F2 --opt adam > $O/${v}_f2_adam_$rep.json 2>/dev/null
     B "$L" > $O/${v}_f2_$rep.json 2>/dev/null
+    B "$L" --form KVL > $O/${v}_kvl_$rep.json 2>/dev/null
   done
 done
 for f in $O/*_[12].json; do python -c "
