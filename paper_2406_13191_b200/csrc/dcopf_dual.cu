@@ -322,6 +322,61 @@ int set_smem(dcopf_dual_t h, F fn, int bytes) {
   return DCOPF_OK;
 }
 
+// The schedule search for tiles of W instances, V per lane, swept by C parts:
+// the largest candidate chunk (48 .. 1 buses) whose kernel shared memory
+// fits, at the longest ring life that fits (ch / life > 0: only that one).
+// quick (tile choice estimates): a chunk that does not fit at the shortest
+// ring life is not tried at the others (shared memory usually grows with the
+// ring life).  Returns false (err empty) when nothing fits; err set on a
+// compiler error.
+bool search_schedule(dcopf_dual_t h, int W, int V, int C, int only_ch, int only_life, Schedule *out,
+                     std::string *err, bool quick = false) {
+  const int nw = sweep_warps(V, h->opt.variant != DCOPF_OPT_PLAIN);
+  const bool optv = h->opt.variant != DCOPF_OPT_PLAIN;
+  // program-block stages in flight: 2, except KVL, whose steps are shorter and
+  // whose shared memory is better spent on larger chunks (measured on config 4:
+  // KVL 1.17e7 at P = 2 / 36-row chunks, 1.21e7 at P = 1 / 48; F2 and F1 best at 2)
+#ifndef DCOPF_PREFETCH_F2
+#define DCOPF_PREFETCH_F2 2
+#endif
+#ifndef DCOPF_PREFETCH_KVL
+#define DCOPF_PREFETCH_KVL 1
+#endif
+  const int P = (h->form == DCOPF_FORM_CYCLE) ? DCOPF_PREFETCH_KVL : (h->form == DCOPF_FORM_FLOW_BOX ? DCOPF_PREFETCH_F2 : 2);
+  const int chs[] = {48, 40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1},
+            lifes[] = {2, 6, 4};
+  const CycleBasis *cy = h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr;
+  err->clear();
+  for (int ch : chs) {
+    if (only_ch && ch != only_ch) continue;
+    Schedule best;
+    bool fit = false;
+    for (int life : lifes) {  // life 2 first: the smallest footprint of this chunk
+      if (only_life && life != only_life) continue;
+      Schedule sc;
+      sc.ring_life = life;
+      sc.pool_gap = 3;  // soft step sync: consumer warps drift by up to two steps
+      // optimiser kernels: the tile's state-row byte offsets (16 B) and each
+      // consumer warp's step constants (64 B) live in shared memory, not in
+      // registers across the step loop (sweep_kernel.cuh)
+      sc.opt_bytes = optv ? 16 + 64 * nw : 0;
+      *err = build_schedule_split(h->ni, ch, P, W, V, nw, C, {}, &sc, cy);
+      if (!err->empty()) return false;
+      if (sc.total > h->dev_smem) {
+        if (quick && life == 2 && !only_life) break;
+        continue;
+      }
+      if (!fit || life > best.ring_life) best = std::move(sc);
+      fit = true;
+    }
+    if (fit) {
+      *out = std::move(best);
+      return true;
+    }
+  }
+  return false;
+}
+
 // Compile + upload the sweep schedule for tiles of W instances, V per lane,
 // swept by C parts: the chunk starts at the largest of the candidate chunks
 // (48 .. 1 buses) and ring lives whose kernel shared memory fits; the
@@ -336,41 +391,10 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
   // order of the loaded state -- which depends only on them -- stays valid
   const bool keep_layout = h->sched_W == W && h->sched_V == V && h->sched_C == C && h->B > 0;
   const int keep_ch = h->sch.CH, keep_life = h->sch.ring_life;
-  // program-block stages in flight: 2, except KVL, whose steps are shorter and
-  // whose shared memory is better spent on larger chunks (measured on config 4:
-  // KVL 1.17e7 at P = 2 / 36-row chunks, 1.21e7 at P = 1 / 48; F2 and F1 best at 2)
-#ifndef DCOPF_PREFETCH_F2
-#define DCOPF_PREFETCH_F2 2
-#endif
-#ifndef DCOPF_PREFETCH_KVL
-#define DCOPF_PREFETCH_KVL 1
-#endif
-  const int P = (h->form == DCOPF_FORM_CYCLE) ? DCOPF_PREFETCH_KVL : (h->form == DCOPF_FORM_FLOW_BOX ? DCOPF_PREFETCH_F2 : 2);
-  const int chs[] = {48, 40, 36, 34, 32, 30, 28, 26, 24, 22, 20, 18, 16, 14, 12, 10, 8, 6, 4, 2, 1},
-            lifes[] = {6, 4, 2};
   Schedule sc;
-  bool ok = false;
-  for (int ch : chs) {
-    if (keep_layout && ch != keep_ch) continue;
-    for (int life : lifes) {
-      if (keep_layout && life != keep_life) continue;
-      sc = Schedule();
-      sc.ring_life = life;
-      sc.pool_gap = 3;  // soft step sync: consumer warps drift by up to two steps
-      // optimiser kernels: the tile's state-row byte offsets (16 B) and each
-      // consumer warp's step constants (64 B) live in shared memory, not in
-      // registers across the step loop (sweep_kernel.cuh)
-      sc.opt_bytes = optv ? 16 + 64 * nw : 0;
-      const CycleBasis *cy = h->form == DCOPF_FORM_CYCLE ? &h->cyc_int : nullptr;
-      const std::string err = build_schedule_split(h->ni, ch, P, W, V, nw, C, {}, &sc, cy);
-      if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
-      if (sc.total <= h->dev_smem) {
-        ok = true;
-        break;
-      }
-    }
-    if (ok) break;
-  }
+  std::string err;
+  const bool ok = search_schedule(h, W, V, C, keep_layout ? keep_ch : 0, keep_layout ? keep_life : 0, &sc, &err);
+  if (!err.empty()) return fail(h, DCOPF_EINVAL, "schedule: %s", err.c_str());
   if (!ok) return fail(h, DCOPF_EINVAL, "batched schedule does not fit shared memory; use the single path");
   h->sched_W = h->sched_V = h->sched_C = h->sched_nw = 0;  // (invalid until every upload succeeded)
   h->sch = sc;
@@ -444,10 +468,24 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
 // KVL inst-it/s): 8192: V2C1 1.01e7 / 1.22e7, V4C2 1.00e7 /
 // 1.20e7; 4096: V2C2 9.5e6 / 1.20e7, V4C4 1.0e7 / 1.21e7; 2048: V2C4 9.2e6 /
 // 1.14e7, V4C8 9.5e6 / 1.11e7; 1024: V2C8 8.6e6 / 1.05e7, V4C16 8.6e6 / 1.02e7.
+//
+// Round 2: the sweep time of a tiling is ~ (pipeline steps of a part) x F +
+// (items of a part) x u, F ~ 10 bus items per step (the per-step fixed cost:
+// barriers, program header, item ranges), u ~ V / 2; the chunk -- hence the
+// steps -- comes from the shared-memory fit of that tiling, which the plain
+// V / C x halo model cannot see (F1's halo rows at 9 parts leave 4-bus chunks:
+// 2.8e6 inst-it/s at 1024 instances vs 4.7e6 at 6 parts with 18-bus chunks,
+// profiles/r2/tiles).  So the best few tilings by the plain model are
+// compiled (quick schedule search) and the one with the smallest estimated
+// sweep time is taken.  (Checked against the measured table above: the
+// choice at 8192 / 4096 / 1024 is unchanged for F2 and KVL.)
 void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out) {
   const long nsm = h->n_sm;
-  double best = 1e300;
-  int bV = 4, bW = 128, bC = 1;
+  struct Cand {
+    int V, W, C;
+    double cost;
+  };
+  std::vector<Cand> cands;
   for (int V : {2, 4})
     for (int C = 1; C <= 16; ++C) {
       if (V == 4 && h->form == DCOPF_FORM_LIMIT_ROWS) break;  // F1: 2 per lane (its mu rows are twice as wide)
@@ -460,19 +498,36 @@ void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out)
       W = std::max<long>(V, (W + V - 1) / V * V);
       if (W > 32L * V) continue;
       const double halo = 1.0 + 0.02 * (C - 1);  // halo items of a split tile (measured ~1-2% per cut)
-      const double cost = (double)V / C * halo;
-      if (cost < best - 1e-9) {
-        best = cost;
-        bV = V;
-        bW = (int)W;
-        bC = C;
-      }
+      cands.push_back({V, (int)W, C, (double)V / C * halo});
     }
-  if (best == 1e300) {  // more than one wave (or a forced configuration that cannot cover B in one)
+  int bV, bW, bC;
+  if (cands.empty()) {  // more than one wave (or a forced configuration that cannot cover B in one)
     bV = h->opt_lane ? h->opt_lane : (h->form == DCOPF_FORM_LIMIT_ROWS ? 2 : 4);
     bC = h->opt_parts ? h->opt_parts : 1;
     const long maxt = std::max<long>(1, nsm / bC);
     bW = (int)std::min<long>(32L * bV, std::max<long>(bV, ((B + maxt - 1) / maxt + bV - 1) / bV * bV));
+  } else {
+    std::stable_sort(cands.begin(), cands.end(), [](const Cand &x, const Cand &y) { return x.cost < y.cost - 1e-9; });
+    const Cand *pick = &cands[0];
+    double best = 1e300;
+    const size_t top = std::min<size_t>(cands.size(), 4);
+    for (size_t i = 0; i < top && cands.size() > 1; ++i) {
+      const Cand &c = cands[i];
+      Schedule sc;
+      std::string err;
+      if (!search_schedule(h, c.W, c.V, c.C, 0, 0, &sc, &err, /*quick=*/true)) continue;
+      int steps = 0;
+      for (int p = 0; p < c.C; ++p) steps = std::max(steps, sc.part_step0[p + 1] - sc.part_step0[p]);
+      const double halo = 1.0 + 0.02 * (c.C - 1);
+      const double t = 10.0 * steps + (double)h->n_bus / c.C * halo * (c.V / 2.0);
+      if (t < best) {
+        best = t;
+        pick = &c;
+      }
+    }
+    bV = pick->V;
+    bW = pick->W;
+    bC = pick->C;
   }
   *V_out = bV;
   *W_out = bW;
@@ -1091,6 +1146,11 @@ int dcopf_dual_set_instance_batch(dcopf_dual_t h, int64_t B, const double *load,
     if (h->form == DCOPF_FORM_LIMIT_ROWS && h->opt_lane == 4)
       return fail(h, DCOPF_EINVAL, "form F1 runs 2 instances per lane on the batched path");
     choose_tiles(h, B, &tV, &W, &tC);
+    // a split tile's parts meet once per sweep, so its launch is cooperative:
+    // every CTA resident at once (one per SM)
+    if (tC > 1 && (B + W - 1) / W * tC > h->n_sm)
+      return fail(h, DCOPF_EINVAL, "tiling of %lld instances with %d parts per tile needs %lld CTAs (> %d SMs, one wave)",
+                  (long long)B, tC, (long long)((B + W - 1) / W * tC), h->n_sm);
     // a failed compile leaves sched_* invalid: the old batch (if any) is
     // dropped below before anything can use the new schedule with it
     int rc = compile_schedule(h, W, tV, tC);

@@ -186,7 +186,15 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   } while (!done);
 }
 __device__ __forceinline__ void mbar_wait_backoff(unsigned bar, unsigned parity) {
-  unsigned done = 0, ns = 32;
+#ifdef DCOPF_CW_SUSPEND
+  mbar_wait(bar, parity);
+  return;
+#endif
+#ifndef DCOPF_CW_NS0
+#define DCOPF_CW_NS0 32
+#define DCOPF_CW_NSMAX 256
+#endif
+  unsigned done = 0, ns = DCOPF_CW_NS0;
   for (;;) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -197,7 +205,7 @@ __device__ __forceinline__ void mbar_wait_backoff(unsigned bar, unsigned parity)
         : "memory");
     if (done) return;
     __nanosleep(ns);
-    ns = ns < 256 ? 2 * ns : ns;
+    ns = ns < DCOPF_CW_NSMAX ? 2 * ns : ns;
   }
 }
 __device__ __forceinline__ void tma_load_1d(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
@@ -571,6 +579,14 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
     for (int j = 0; j < nout; ++j) r |= (lst[j] == l);
     return r;
   };
+  // consumer-to-consumer waits: nanosleep back-off in the plain kernels,
+  // try_wait with a suspend hint in the optimiser kernels (A/B on config 4 /
+  // 4b, K = 100: plain F2 -1% with the suspend, F2 + Adam +1.2%, KVL + Adam
+  // +0.4%; profiles/r2/fastdiv/ab_wait)
+  auto cwait = [&](unsigned bar, unsigned parity) {
+    if constexpr (OPT) mbar_wait(bar, parity);
+    else mbar_wait_backoff(bar, parity);
+  };
   int cst = 0;         // stage of the next step
   unsigned cph = 0;    // parity of its full barrier
 
@@ -828,7 +844,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       }
       if (SOFT) {  // C and D read the f* codes of B(<= s-1)
         mbar_arrive(bdone_sa + 8 * (gs & 3));
-        if (gs > 0) mbar_wait_backoff(bdone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
+        if (gs > 0) cwait(bdone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
       }
       phaseC(wr.y, 1);
       // ---------------- D(s-1): d/dkappa_k = sum_l C_kl x_l f*_l, kappa' ----------------
@@ -949,7 +965,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       if (SOFT) {  // B(s-1) reads the theta* codes of A(<= s-1); the f* slots it writes
         // were last read 2+ steps ago, and A-done(s-1) implies every warp finished step s-2
         mbar_arrive(adone_sa + 8 * (gs & 3));
-        if (gs > 0) mbar_wait_backoff(adone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
+        if (gs > 0) cwait(adone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
       }
       // ---------------- B(s-1): branches ----------------
       {
@@ -1084,7 +1100,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       }
       if (SOFT) {
         mbar_arrive(bdone_sa + 8 * (gs & 3));
-        if (gs > 0) mbar_wait_backoff(bdone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
+        if (gs > 0) cwait(bdone_sa + 8 * ((gs - 1) & 3), ((gs - 1) >> 2) & 1u);
       }
       phaseC(wr.z, 2);
       }  // debug_mode
