@@ -709,8 +709,9 @@ def test_split_tiles_bitwise(form, V, C):
 @pytest.mark.parametrize("B", [1024, 2048, 4096])
 def test_strong_scaling_shards_sampled(form, B):
     """The per-GPU shards of the literal config-4 split (8192 over 8 / 4 / 2
-    GPUs) in the library's own tiling (4 instances per lane, 16 / 8 / 4 parts),
-    full K = 5000, sampled instances vs the oracle."""
+    GPUs) in the library's own tiling (split tiles, the parts chosen by the
+    chunk-aware model: e.g. F2 9 / 4 / 2 parts), full K = 5000, sampled
+    instances vs the oracle."""
     net = inst.make_network(4)
     sw = non_tree_switchable(net)
     K = inst.ITERS[4]
@@ -762,3 +763,19 @@ def test_split_tiles_optimizer_and_evaluate(V, C):
     np.testing.assert_array_equal(gl.cpu().numpy().T, ogl)
     np.testing.assert_array_equal(gb.cpu().numpy().T, ogb)
     h.close()
+
+
+def test_forced_split_tiling_beyond_one_wave_rejected():
+    """A split tile is a cooperative launch (its parts meet every sweep): a
+    forced tiling needing more CTAs than SMs is rejected at set_instance_batch
+    with EINVAL, leaving no batch loaded."""
+    import torch
+    net = inst.make_network(4)
+    sw = non_tree_switchable(net)
+    B = 1024
+    batch = inst.config4_batch(net, range(B))
+    dev = torch.device("cuda:0")
+    h = dual.DcopfDual(net, path=dual.PATH_BATCHED, switchable=sw, tile_parts=12, lane_instances=2)
+    with pytest.raises(dual.DcopfError, match="EINVAL"):
+        h.set_instance_batch(torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev),
+                             torch.from_numpy(batch.outages).to(dev))

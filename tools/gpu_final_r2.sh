@@ -19,6 +19,10 @@ for b in 4096 2048 1024; do
 done
 B config4b_KVL_adam --workload config4b --form KVL --opt adam --no-cpu-baseline
 B config4b_F2_adam --workload config4b --form F2 --opt adam --no-cpu-baseline
+B config4b_KVL_adagrad --workload config4b --form KVL --opt adagrad --no-cpu-baseline --no-gap
+B config4_F2_K100 --steps 100 --warmup 5 --no-cpu-baseline --no-gap --no-e2e
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -Ipaper_2406_13191_b200/csrc tools/fp64_fastpath_check.cu -o /tmp/fp64_fastpath_check > $O/check_build.log 2>&1
+timeout 300 /tmp/fp64_fastpath_check 64 > $O/fp64_fastpath_check.json 2>&1; echo fastpath=$?
 B config4b_PTDF --workload config4b --form PTDF --no-cpu-baseline --steps 20 --warmup 3
 B config3_F2 --workload config3 --steps 2000 --warmup 100 --no-cpu-baseline
 B config3_KVL_adam --workload config3 --form KVL --opt adam --alpha 0.1 --steps 2000 --warmup 100 --no-cpu-baseline
@@ -30,6 +34,8 @@ N config4_F2
 N config4_KVL --form KVL
 N shard1024_F2 --batch 1024
 N config4b_KVL_adam --workload config4b --form KVL --opt adam
+N config4b_F2_adam --workload config4b --form F2 --opt adam
+N shard1024_F1 --batch 1024 --form F1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_config3_PTDF.csv python bench.py --workload config3 --form PTDF --steps 20 --warmup 3 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_launch_ptdf.log 2>&1; echo launches_ptdf=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused -c 2 -o $O/ncu_k_fused_config3 python bench.py --workload config3 --form PTDF --steps 5 --warmup 3 --no-cpu-baseline --no-gap --no-e2e > $O/ncu_fused.log 2>&1; echo ncu_fused=$?
 echo done
