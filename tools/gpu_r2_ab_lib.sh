@@ -16,5 +16,6 @@ for rep in 1 2; do
     B "$L" --form KVL > $O/${v}_kvl_$rep.json 2>/dev/null
   done
 done
+timeout 2400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_compact.py -x -q -k "split or strong_scaling or compaction or config4 or batch or optimizer or kvl or f1" > $O/tests.log 2>&1; echo tests=$?; tail -1 $O/tests.log
 for f in $O/*_[12].json; do python -c "
 import json; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['value']), round(d['roofline']['frac'],3))"; done
