@@ -87,6 +87,11 @@ struct dcopf_dual_s {
   Schedule sch;
   int sched_W = 0, sched_V = 0, sched_C = 0, sched_nw = 0;
   bool sched_opt = false;  // compiled with the optimiser kernels' shared-memory block
+  // the last tiling choice (choose_tiles compiles candidate schedules: ~0.1 s
+  // per candidate on the host): reused while the batch size and the variant
+  // (warp count, shared-memory block) are unchanged
+  int64_t tc_B = -1;
+  int tc_opt = -1, tc_V = 0, tc_W = 0, tc_C = 0;
   int tile_V = 2, tile_C = 1;  // loaded batch: instances per lane, parts (CTAs) per tile
   uint8_t *d_prog = nullptr;
   int *d_part_step0 = nullptr;
@@ -480,6 +485,13 @@ int compile_schedule(dcopf_dual_t h, int W, int V, int C) {
 // sweep time is taken.  (Checked against the measured table above: the
 // choice at 8192 / 4096 / 1024 is unchanged for F2 and KVL.)
 void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out) {
+  const int optk = h->opt.variant != DCOPF_OPT_PLAIN;
+  if (h->tc_B == B && h->tc_opt == optk) {
+    *V_out = h->tc_V;
+    *W_out = h->tc_W;
+    *C_out = h->tc_C;
+    return;
+  }
   const long nsm = h->n_sm;
   struct Cand {
     int V, W, C;
@@ -532,6 +544,11 @@ void choose_tiles(dcopf_dual_t h, int64_t B, int *V_out, int *W_out, int *C_out)
   *V_out = bV;
   *W_out = bW;
   *C_out = bC;
+  h->tc_B = B;
+  h->tc_opt = optk;
+  h->tc_V = bV;
+  h->tc_W = bW;
+  h->tc_C = bC;
 }
 
 // state-layout permutations of the current path (storage position <-> original id)
