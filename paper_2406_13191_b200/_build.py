@@ -12,7 +12,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libdcopf_dual.so")
 SOURCES = [os.path.join(CSRC, "dcopf_dual.cu"), os.path.join(CSRC, "schedule.cpp"),
            os.path.join(CSRC, "split_schedule.cpp"), os.path.join(CSRC, "cluster.cpp"), os.path.join(CSRC, "ptdf.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dual_kernels.cuh", "sweep_kernel.cuh", "schedule.h", "schedule_detail.h", "cluster.h",
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("dual_kernels.cuh", "fp64_fast.cuh", "sweep_kernel.cuh", "schedule.h", "schedule_detail.h", "cluster.h",
                                               "cluster_kernel.cuh", "ptdf.h")] + [
     os.path.join(ROOT, "include", "dcopf_dual.h")]
 

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "cluster.h"
+#include "fp64_fast.cuh"
 
 namespace dcopf {
 namespace {
@@ -151,6 +152,52 @@ __device__ __forceinline__ double opt_step(const GemmArgs &g, double y, double g
     default:
       return y + al * gr;
   }
+}
+
+// The adaptive variants (AdaGrad, Adam) on a row's two multipliers (mu+,
+// mu-) at once, in opt_step's operation order, every division and square root
+// on the branch-free fast paths (fp64_fast.cuh) so the two Newton chains
+// overlap, then ONE warp vote: every value passed -- opt_step's bits;
+// otherwise opt_step itself.  Other variants: opt_step.
+__device__ __forceinline__ void opt_step2(const GemmArgs &g, double yp, double gp, double ym, double gm, double al,
+                                          double &s1p, double &s2p, double &s1m, double &s2m, double &vp,
+                                          double &vm) {
+  if (g.opt == 3 || g.opt == 4) {
+    bool ok = true;
+    double y[2] = {yp, ym}, gr[2] = {gp, gm}, s1[2] = {s1p, s1m}, s2[2] = {s2p, s2m}, out[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double num, arg;
+      if (g.opt == 4) {
+        const double m = g.beta1 * s1[j] + (1.0 - g.beta1) * gr[j];
+        const double v = g.beta2 * s2[j] + (1.0 - g.beta2) * (gr[j] * gr[j]);
+        s1[j] = m;
+        s2[j] = v;
+        const double mq = ddiv_fast(nz_or_one(m), 1.0 - g.b1t, ok), vq = ddiv_fast(nz_or_one(v), 1.0 - g.b2t, ok);
+        num = al * (m == 0.0 ? m : mq);
+        arg = v == 0.0 ? v : vq;
+      } else {
+        const double G = s1[j] + gr[j] * gr[j];
+        s1[j] = G;
+        num = al * gr[j];
+        arg = G;
+      }
+      const double sr = dsqrt_fast(nz_or_one(arg), ok);
+      const double q = ddiv_fast(nz_or_one(num), (arg == 0.0 ? arg : sr) + g.eps, ok);
+      out[j] = y[j] + (num == 0.0 ? num : q);
+    }
+    if (__all_sync(__activemask(), ok)) {
+      vp = out[0];
+      vm = out[1];
+      s1p = s1[0];
+      s1m = s1[1];
+      s2p = s2[0];
+      s2m = s2[1];
+      return;
+    }
+  }
+  vp = opt_step(g, yp, gp, al, s1p, s2p);
+  vm = opt_step(g, ym, gm, al, s1m, s2m);
 }
 
 // p* = argmin over [lo, hi] of a p^2 + q p: clip(-q / 2a) (reading A-6), else
@@ -360,8 +407,7 @@ __global__ void __launch_bounds__(NTHR, CTAS_PER_SM) k_dgemm(const GemmArgs g) {
             vm = mm + al * gm;
           } else {
             double a1 = g.s1p[o], a2 = g.s2p ? g.s2p[o] : 0.0, b1 = g.s1m[o], b2 = g.s2m ? g.s2m[o] : 0.0;
-            vp = opt_step(g, mp, gp, al, a1, a2);
-            vm = opt_step(g, mm, gm, al, b1, b2);
+            opt_step2(g, mp, gp, mm, gm, al, a1, a2, b1, b2, vp, vm);
             g.s1p[o] = a1;
             g.s1m[o] = b1;
             if (g.s2p) {
@@ -825,8 +871,7 @@ __global__ void __launch_bounds__(VT, skinny_minb(NB)) k_line_row(const GemmArgs
           vm = mm + al * gm;
         } else {
           double a1 = g.s1p[o], a2 = g.s2p ? g.s2p[o] : 0.0, b1 = g.s1m[o], b2 = g.s2m ? g.s2m[o] : 0.0;
-          vp = opt_step(g, mp, gp, al, a1, a2);
-          vm = opt_step(g, mm, gm, al, b1, b2);
+          opt_step2(g, mp, gp, mm, gm, al, a1, a2, b1, b2, vp, vm);
           g.s1p[o] = a1;
           g.s1m[o] = b1;
           if (g.s2p) {
@@ -1099,8 +1144,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_line(const FusedArgs a, const G
             a2 = rowv[6 * rpc + t];
             b2 = rowv[8 * rpc + t];
           }
-          vp = opt_step(g, mp, gp, al, a1, a2);
-          vm = opt_step(g, mm, gm, al, b1, b2);
+          opt_step2(g, mp, gp, mm, gm, al, a1, a2, b1, b2, vp, vm);
         }
         const double np = vp > 0.0 ? vp : 0.0, nm = vm > 0.0 ? vm : 0.0;  // mu <- max(mu, 0)
         nn = np - nm;
@@ -2110,6 +2154,15 @@ int fused_loop(PtdfState *st, int64_t K, const FusedArgs &a, GemmArgs g, const G
   return DCOPF_OK;
 }
 
+// the single-read step serves this batch and step variant
+#ifndef DCOPF_PTDF_FUSED_ADAPTIVE
+#define DCOPF_PTDF_FUSED_ADAPTIVE 1
+#endif
+static bool fused_for(const PtdfState *st) {
+  return st->fused && (DCOPF_PTDF_FUSED_ADAPTIVE ||
+                       (st->opt.variant != DCOPF_OPT_ADAGRAD && st->opt.variant != DCOPF_OPT_ADAM));
+}
+
 int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist, cudaStream_t s, std::string *err) {
   GemmArgs g1 = gen_args(st), g2 = line_args(st);
   g2.alpha = alpha_dev;
@@ -2120,10 +2173,10 @@ int ptdf_iterate(PtdfState *st, int64_t K, const double *alpha_dev, double *hist
   f.k_base = st->k_base;
   f.target = st->has_target ? st->target : nullptr;
   f.hit = st->hit;
-  // B = 1: the single-read step, except for the variants with a long per-row
-  // step chain (AdaGrad, Adam), which keep the two-pass kernels (see k_fused_line)
-  if (st->fused && st->opt.variant != DCOPF_OPT_ADAGRAD && st->opt.variant != DCOPF_OPT_ADAM)
-    return fused_iterate(st, K, g2, f, s, err);
+  // B = 1: the single-read step (every variant since the adaptive steps run
+  // on the branch-free division / square root, opt_step2; before that their
+  // per-row chain kept AdaGrad / Adam on the two-pass kernels)
+  if (fused_for(st)) return fused_iterate(st, K, g2, f, s, err);
   if (st->nbv) {  // skinny batch: matrix-vector passes on the caller's stream
     fin_tiles(st, &f);
     for (int64_t k = 0; k <= K; ++k) {
@@ -2351,7 +2404,7 @@ void ptdf_info(const PtdfState *st, dcopf_info *info) {
     info->grid = skinny_blocks_l(st->nl);
     info->launches_per_iter = 2;
     info->tile_width = st->nbv;
-    if (st->fused && st->opt.variant != DCOPF_OPT_ADAGRAD && st->opt.variant != DCOPF_OPT_ADAM) {
+    if (fused_for(st)) {
       // B = 1, the single-read step (with this step variant): its line kernel's stages and grid
       info->smem_bytes = (int)fused_smem(st->ngk, st->fR, st->fS, st->frpc);
       info->threads_per_block = FT;

@@ -114,22 +114,25 @@ def test_config0_full_K(skinny, fused, monkeypatch):
     assert info.path == dual.PATH_DENSE and info.form == dual.FORM_PTDF
 
 
-@pytest.mark.parametrize("which", ["config3_gdm", "config3_plain", "config2_quadratic", "config1_warm"])
+@pytest.mark.parametrize("which", ["config3_gdm", "config3_plain", "config3_adam", "config3_adagrad",
+                                   "config2_quadratic", "config1_warm"])
 def test_single_read_step(which):
-    """B = 1 on the single-read step (plain and momentum steps; AdaGrad / Adam
-    keep the two-pass kernels): config 3's H_g (2 500 generator columns: two
-    20 KB rows per group, 148 CTAs of ~86 lines) over several calls; the
-    quadratic config-2 network; a warm start from random multipliers (Q_0 from
-    the set nu) followed by the two-pass evaluate()."""
+    """B = 1 on the single-read step (every step variant: AdaGrad / Adam on the
+    branch-free fp64 division / square root since round 2): config 3's H_g
+    (2 500 generator columns: two 20 KB rows per group, 148 CTAs of ~86
+    lines) over several calls; the quadratic config-2 network; a warm start
+    from random multipliers (Q_0 from the set nu) followed by the two-pass
+    evaluate()."""
     import torch
     if which.startswith("config3"):
         net = inst.make_network(3)
-        gdm = which == "config3_gdm"
+        opt, alpha = {"config3_gdm": (GDM, 1e-3), "config3_plain": (None, 2e-3), "config3_adam": (ADAM, 0.5),
+                      "config3_adagrad": (dict(variant=P.OPT_ADAGRAD, eps=1e-8), 0.5)}[which]
         K = 60
-        a = inst.alpha_schedule(K, 1e-3 if gdm else 2e-3)
+        a = inst.alpha_schedule(K, alpha)
         loads = net.base_load[None]
-        gpu = _gpu(net, loads, K, a, opt=GDM if gdm else None, split=25)
-        orc = _orc(net, loads, K, a, opt=GDM if gdm else None)
+        gpu = _gpu(net, loads, K, a, opt=opt, split=25)
+        orc = _orc(net, loads, K, a, opt=opt)
         assert gpu["info"].smem_bytes > 0  # the single-read kernels ran
         assert_parity(net, gpu, orc)
         return
