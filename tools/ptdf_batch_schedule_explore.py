@@ -1,0 +1,67 @@
+"""Step schedules for the batched true time to gap (config 4b, dense PTDF +
+Adam): runs the 512 instances that have exact LP optima
+(tests/golden/optima_config4b.json) under each schedule and reports the
+iteration at which the LAST of them reaches a true 1e-3 gap (the kernels'
+first-hit record).  Selection only -- the bench line then runs the chosen
+schedule on the whole 8192-instance batch.  python tools/ptdf_batch_schedule_explore.py"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2406_13191_b200 import dual, instances as inst  # noqa: E402
+
+ref = json.load(open(os.path.join(ROOT, "tests", "golden", "optima_config4b.json")))
+ids = np.asarray(ref["instance_ids"], dtype=np.int64)
+popt = np.asarray(ref["primal_opt"], dtype=np.float64)
+net = inst.make_network(4)
+batch = inst.config4_batch(net, ids.tolist(), variant="4b", total=inst.CONFIG4_BATCH)
+dev = torch.device("cuda:0")
+load_dev = torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev)
+target = popt - 1e-3 * np.abs(popt)
+K_max, chunk = 6000, 500
+out = []
+# round 1 (profiles/r2/ptdf_sched/round1.jsonl): 5/inv:200 3008 (the bench's), 8/inv:100 2713,
+# 12/inv:100 2858, 2/step:0.5:1000 3007, others 3173-4846 or not all reached by 6000
+# round 2 (round2.jsonl): step decay wins -- every instance closes right after a halving once alpha
+# is down to ~0.2-0.4: 3/step:0.5:500 2004, 3/step:0.5:700 2133, 2/step:0.5:600 2403; inv:T at best 2562
+# round 3 (round3.jsonl): 3/step:0.5:300 1519, 4/step:0.5:400 1610, 3/step:0.5:400 1617; starting
+# at alpha <= 2 with fast halving never gets there (too little progress before alpha is small)
+# round 4 (round4.jsonl): 8/step:0.5:200 1012, 5/step:0.5:200 1201, 6/step:0.5:250 1254
+# round 5 (round5.jsonl): 48/step:0.5:100 716, 16/step:0.5:120 730, 32/step:0.5:120 844, 10/step:0.5:150 903
+# round 6 (round6.jsonl): 24/step:0.5:70 498, 16/step:0.5:60 560, 16/step:0.5:80 566, 16/step:0.5:100 622
+# round 7 (round7.jsonl): 32/step:0.5:50 403, 40/step:0.5:50 403, 24/step:0.5:50 412, 32/step:0.5:60 438
+SCHEDULES = [(32.0, "step:0.5:40"), (48.0, "step:0.5:40"), (64.0, "step:0.5:40"), (32.0, "step:0.5:45"),
+             (48.0, "step:0.5:45"), (64.0, "step:0.5:50"), (24.0, "step:0.5:40"), (96.0, "step:0.5:40"),
+             (64.0, "step:0.5:30"), (128.0, "step:0.5:30")]
+# selection half (instance ids = 0 mod 32) and hold-out half (16 mod 32) of the covered instances
+sel = (ids % 32) == 0
+for a0, decay in SCHEDULES:
+    h = dual.DcopfDual(net, form=dual.FORM_PTDF, path=dual.PATH_DENSE)
+    h.set_optimizer(dual.OPT_ADAM, 0.0, 0.9, 0.999, 1e-8)
+    h.set_instance_batch(load_dev)
+    h.set_target(target)
+    alpha = inst.alpha_schedule(K_max, a0, decay)
+    k0 = 0
+    while k0 < K_max:
+        h.iterate(chunk, alpha[k0:k0 + chunk])
+        k0 += chunk
+        hit = h.get_first_hit()
+        if np.all(hit >= 0):
+            break
+    best = np.empty(len(ids))
+    h.get_bound(best=best)
+    gaps = (popt - best) / np.abs(popt)
+    r = {"alpha0": a0, "decay": decay, "reached": int(np.sum(hit >= 0)),
+         "max_hit_selection_half": int(hit[sel].max()) if np.all(hit[sel] >= 0) else None,
+         "max_hit_holdout_half": int(hit[~sel].max()) if np.all(hit[~sel] >= 0) else None,
+         "max_hit": int(hit.max()) if np.all(hit >= 0) else None,
+         "p90_hit": float(np.percentile(hit[hit >= 0], 90)) if np.any(hit >= 0) else None,
+         "gap_median_at_stop": float(np.median(gaps)), "gap_max_at_stop": float(np.max(gaps)), "run": k0}
+    print(json.dumps(r), flush=True)
+    out.append(r)
+    h.close()
