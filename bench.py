@@ -330,6 +330,63 @@ def time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, 
 TRUE_GAP_ALPHA, TRUE_GAP_DECAY = 48.0, "step:0.5:40"
 
 
+def single_true_gap(args, h, batch, load_dev, stream, rel=1e-3, chunk=250):
+    """Time to a TRUE 1e-3 gap on one instance (configs 1-3): the exact
+    optimum of Eq. 1 for the workload (HiGHS; Kelley cutting planes for QP,
+    tests/golden/targets.json, tools/make_targets.py) as the target, the
+    bench's own form / step / schedule from y_0, in chunks of `chunk` steps
+    until the running best reaches it (the first hit recorded on device), at
+    most the workload's K.  Reports the device time at the hit iteration (the
+    chunks before it plus its chunk prorated) and the time of the chunks run."""
+    import torch
+    try:
+        refs = json.load(open(os.path.join(ROOT, "tests", "golden", "targets.json")))
+    except (OSError, ValueError):
+        return {"unavailable": "no targets.json"}
+    wl = args.workload + "/"
+    popt = next((r["primal_opt"] for k, r in refs.items() if k.startswith(wl) and r.get("primal_opt") is not None),
+                None)
+    if popt is None or batch.B != 1:
+        return {"unavailable": f"no exact optimum for {args.workload}"}
+    popt = float(np.atleast_1d(popt)[0])
+    K_max = int(inst.ITERS[WORKLOADS[args.workload][0]])
+    ospec, alpha0 = opt_spec(args)
+    alpha = inst.alpha_schedule(K_max, alpha0, args.decay)
+    h.set_instance_batch(load_dev, None, stream=stream)  # from y_0 (resets the multipliers and the state)
+    if args.opt != "plain":
+        h.set_optimizer(ospec["variant"], ospec.get("rho", 0.0), ospec.get("beta1", 0.0), ospec.get("beta2", 0.0),
+                        ospec.get("eps", 0.0))
+    h.set_target(np.array([popt - rel * abs(popt)]), stream=stream)
+    chunks, k0, hit = [], 0, -1
+    while k0 < K_max:
+        n = min(chunk, K_max - k0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h.iterate(n, alpha[k0:k0 + n], stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        chunks.append((k0, n, e0.elapsed_time(e1)))
+        k0 += n
+        hit = int(h.get_first_hit()[0])
+        if hit >= 0:
+            break
+    best = np.empty(1)
+    h.get_bound(best=best)
+    at_hit = None
+    if hit >= 0:
+        at_hit = sum(ms for (c0, n, ms) in chunks if c0 + n <= hit)
+        for (c0, n, ms) in chunks:
+            if c0 <= hit < c0 + n:
+                at_hit += ms * (hit - c0 + 1) / n
+        at_hit /= 1e3
+    return {"rel_gap": rel, "reference": "exact optimum of Eq. 1 (HiGHS; tests/golden/targets.json)",
+            "primal_opt": popt, "schedule": {"alpha": alpha0, "decay": args.decay}, "hit_iteration": hit if hit >= 0
+            else None, "seconds": at_hit, "seconds_run": sum(ms for (_, _, ms) in chunks) / 1e3,
+            "iterations_run": k0, "true_gap_at_stop": (popt - float(best[0])) / abs(popt),
+            "timing": f"device events over iterate() chunks of {chunk} steps; seconds = the chunks before the hit "
+                      "+ the hit's chunk prorated"}
+
+
 def batched_true_gap(dev, stream, rel=1e-3, chunk=50, K_max=5000):
     """Time to a TRUE 1e-3 gap on the batched workload (BASELINE.json metric
     "time to 1e-3 gap"; Tables 1-3 report t(s) to Gap%): the whole
@@ -559,6 +616,11 @@ def main():
     if not args.no_gap:
         ttg = time_to_gap(args, h, net, batch, lo, hi, load_dev, outs_dev, stream, world, dev)
 
+    # ---- one instance's time to a TRUE 1e-3 gap (exact optimum) --------------
+    ttg_single = None
+    if not args.no_gap and B_total == 1 and world == 1:
+        ttg_single = single_true_gap(args, h, batch, load_dev, stream)
+
     # ---- the batched workload's time to a TRUE 1e-3 gap (best route) ----------
     ttg_batched = None
     if (not args.no_gap and world == 1 and args.workload == "config4" and args.form == "F2"
@@ -683,8 +745,9 @@ def main():
                        "l2": ("inputs larger than L2: state %.2f GB per GPU" %
                               ((info.B_padded * (2 * net.n_bus + 2 * net.n_branch * (1 if form == 0 else 2)
                                                  + net.n_bus) * 8) / 1e9))
-                       if B_total > 1 and not dense else ("H_g %.2f GB read twice per step" %
-                                                            (2 * 8 * net.n_branch * net.n_gen / 1e9)
+                       if B_total > 1 and not dense else ("H_g %.2f GB read %s per step" %
+                                                            (8 * net.n_branch * net.n_gen / 1e9,
+                                                             "once" if (B == 1 and info.smem_bytes > 0) else "twice")
                                                             if dense else "state on chip (single instance)"),
                        "timed_launches": (f"{(2 if B <= 4 else 3) * (K + 1)} launches: {2 if B <= 4 else 3} per step "
                                           f"({K} steps) + the final evaluation"
@@ -693,6 +756,7 @@ def main():
             "cpu_baseline": cpu,
             "time_to_gap": ttg,
             "time_to_true_gap_batched": ttg_batched,
+            "time_to_true_gap_single": ttg_single,
             "e2e": e2e,
             "gpu_launches": ((2 if B <= 4 else 3) * (K + 1)) if dense else 1,
             "clocks": clk,
