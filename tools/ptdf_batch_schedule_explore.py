@@ -23,7 +23,8 @@ batch = inst.config4_batch(net, ids.tolist(), variant="4b", total=inst.CONFIG4_B
 dev = torch.device("cuda:0")
 load_dev = torch.from_numpy(np.ascontiguousarray(batch.load.T)).to(dev)
 target = popt - 1e-3 * np.abs(popt)
-K_max, chunk = 6000, 500
+FORM = os.environ.get("EXPLORE_FORM", "PTDF")  # PTDF (the route) or KVL / F2 (the sparse batched forms)
+K_max, chunk = (6000, 500) if FORM == "PTDF" else (20000, 1000)
 out = []
 # round 1 (profiles/r2/ptdf_sched/round1.jsonl): 5/inv:200 3008 (the bench's), 8/inv:100 2713,
 # 12/inv:100 2858, 2/step:0.5:1000 3007, others 3173-4846 or not all reached by 6000
@@ -40,8 +41,18 @@ SCHEDULES = [(32.0, "step:0.5:40"), (48.0, "step:0.5:40"), (64.0, "step:0.5:40")
              (64.0, "step:0.5:30"), (128.0, "step:0.5:30")]
 # selection half (instance ids = 0 mod 32) and hold-out half (16 mod 32) of the covered instances
 sel = (ids % 32) == 0
+if FORM != "PTDF":
+    SCHEDULES = [(0.1, None), (0.3, "step:0.5:1000"), (1.0, "step:0.5:1000"), (3.0, "step:0.5:1000"),
+                 (1.0, "step:0.5:500"), (3.0, "step:0.5:500"), (10.0, "step:0.5:500"), (3.0, "step:0.5:2000"),
+                 (1.0, "step:0.5:3000"), (0.3, "step:0.5:4000"), (10.0, "step:0.5:200"), (30.0, "step:0.5:200")]
 for a0, decay in SCHEDULES:
-    h = dual.DcopfDual(net, form=dual.FORM_PTDF, path=dual.PATH_DENSE)
+    if FORM == "PTDF":
+        h = dual.DcopfDual(net, form=dual.FORM_PTDF, path=dual.PATH_DENSE)
+    else:
+        sw = np.zeros(net.n_branch, np.uint8)
+        sw[net.n_tree:] = 1
+        h = dual.DcopfDual(net, form=dual.FORM_KVL if FORM == "KVL" else dual.FORM_F2, path=dual.PATH_BATCHED,
+                           switchable=sw)
     h.set_optimizer(dual.OPT_ADAM, 0.0, 0.9, 0.999, 1e-8)
     h.set_instance_batch(load_dev)
     h.set_target(target)
