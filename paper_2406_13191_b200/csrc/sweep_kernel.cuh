@@ -593,6 +593,16 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
   for (long k = 0; k <= K; ++k) {
     const bool last = (k == K);
     const bool write = EVAL || !last;
+    // the launch's final sweep only evaluates g(y_K) (Algorithm 1's value of
+    // the last iteration): the work that only forms the gradient
+    // -- the f* / theta* sums of phase C, phi of phase B, the whole of phase D
+    // (KVL) -- is skipped there (not in EVAL launches, which return it).  Only
+    // where it measured faster (A/B against the kernel without it, config 4 /
+    // 4b, profiles/r2/tried/final_sweep_gskip*): the plain KVL kernel (+2.2% at
+    // the driver's K = 20) and the F2 optimiser kernel (+1.6%); in the plain
+    // F2 / F1 kernels the extra branches cost the other sweeps more than the
+    // final one saves (F2 -3.5%), KVL + Adam -0.5%, F1 + Adam unchanged
+    const bool gskip = ((FORM == kFormKVL && !OPT) || (FORM == kFormF2 && OPT)) && !EVAL && last;
     const int par = (a.cur + (int)(k & 1)) & 1;
     uint8_t *lam_o = reinterpret_cast<uint8_t *>(EVAL ? a.g_lam : (par ? a.lam0 : a.lam1)) +
                      DCOPF_TILE * (size_t)a.n_bus * RB + lofs;
@@ -737,7 +747,9 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
               }
             }
           }
-          if (FORM != kFormF1) {
+          if (gskip) {
+            // (value only: the incidence sums feed the gradient alone)
+          } else if (FORM != kFormF1) {
             const unsigned IC = prog + h3.y + r.e0 * (unsigned)sizeof(RecIC2);
             const int n = r.e1 - r.e0;
             auto acc = [&](const RecIC2 &x) {
@@ -848,7 +860,7 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
       }
       phaseC(wr.y, 1);
       // ---------------- D(s-1): d/dkappa_k = sum_l C_kl x_l f*_l, kappa' ----------------
-      {
+      if (!gskip) {  // (gradient and step only)
         const unsigned Dv = prog + h2.x, De = prog + h2.y;
         ITEM_LOOP(2, wr.z, h0.x) {
           const RecD r = lds_rec<RecD>(Dv + j * (unsigned)sizeof(RecD));
@@ -1003,10 +1015,15 @@ __global__ void __maxnreg__(SweepRegs<NW>::value) k_sweep(const SweepArgs a) {
           }
           OState<V> ost = oload((size_t)r.wpos * BR, false, OPT && !EVAL && write && act);
           OState<V> ost_m = oload((size_t)r.wpos * BR + RB, false, FORM == kFormF1 && OPT && !EVAL && write && act);
-          const DV<V> ths = ld_code<V>(thp, r.ts, r.ths), tht = ld_code<V>(thp, r.tt, r.tht);
-          double phi[V];
+          double phi[V];  // (the gradient's flow term; not needed by the final sweep's value)
+          if (gskip) {
 #pragma unroll
-          for (int q = 0; q < V; ++q) phi[q] = b[q] * (ths.v[q] - tht.v[q]);
+            for (int q = 0; q < V; ++q) phi[q] = 0.0;
+          } else {
+            const DV<V> ths = ld_code<V>(thp, r.ts, r.ths), tht = ld_code<V>(thp, r.tt, r.tht);
+#pragma unroll
+            for (int q = 0; q < V; ++q) phi[q] = b[q] * (ths.v[q] - tht.v[q]);
+          }
           uint8_t *dst = br_o + (size_t)r.wpos * BR;
           if (FORM == kFormF2) {
             const DV<V> nu = ldsv<V>(brp, r.row, hb), ls = ldsv<V>(lamp, r.ls, hb), lt = ldsv<V>(lamp, r.lt, hb);
