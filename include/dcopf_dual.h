@@ -241,8 +241,11 @@ int dcopf_dual_evaluate(dcopf_dual_t h, double *value, double *grad_lambda, doub
  * in HBM beside the multipliers, read and written at the update: 1 or 2 more
  * rows per multiplier and iteration); not on DCOPF_PATH_SINGLE (iterate()
  * fails with ESTATE).  Errors: EINVAL (unknown variant, rho/b1/b2 outside
- * [0, 1), eps < 0, or the cluster partition plus the optimiser state does not
- * fit shared memory). */
+ * [0, 1), eps < 0 (AdaGrad / Adam: eps <= 0), the cluster partition plus the
+ * optimiser state does not fit shared memory, or -- a batch loaded on the
+ * batched path -- the loaded schedule's chunk does not fit with the optimiser
+ * kernels' 1.2 KB shared-memory block; set the variant before
+ * set_instance_batch() then).  On an error the handle is unchanged. */
 enum { DCOPF_OPT_PLAIN = 0, DCOPF_OPT_GDM = 1, DCOPF_OPT_GDM_CLASSIC = 2, DCOPF_OPT_ADAGRAD = 3, DCOPF_OPT_ADAM = 4 };
 typedef struct {
   int32_t variant;   /* DCOPF_OPT_* */
